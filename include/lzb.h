@@ -1,0 +1,152 @@
+/*
+ * lzb.h — C-ABI of the B200-native delayed-assembly hot path (liblzb.so).
+ *
+ * Plain pointers and sizes only. Host-buffer entry points copy in/out inside
+ * the call; *_dev entry points take device pointers and a cudaStream_t passed
+ * as void* and are asynchronous on that stream.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/proj/include/lazymg/*.hpp). The reference exposes C++
+ * only; these are the symbols its call sites bind through the host shim
+ * (INTEGRATION.md). Errors: every function returns an lzb_status; the
+ * message is in lzb_last_error() (thread-local). A missing GPU is
+ * LZB_ERR_CUDA — there is no CPU fallback.
+ */
+#ifndef LZB_H
+#define LZB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "lzb_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ----------------------------------------------------------------- runtime */
+const char* lzb_last_error(void);
+int lzb_version(void);
+/* Number of kernels this library has launched since load (evidence counter). */
+uint64_t lzb_launch_count(void);
+
+typedef struct lzb_ctx lzb_ctx;
+/* Device + two streams: solve (high priority) and assembly (low priority). */
+int lzb_ctx_create(int device, lzb_ctx** out);
+void lzb_ctx_destroy(lzb_ctx* ctx);
+int lzb_ctx_synchronize(lzb_ctx* ctx);
+/* Raw stream handles (cudaStream_t) for callers that mix their own work in. */
+void* lzb_ctx_solve_stream(lzb_ctx* ctx);
+void* lzb_ctx_assembly_stream(lzb_ctx* ctx);
+
+/* ------------------------------------------------------------------ fields */
+/* BASELINE config 1 checkerboard; host-side helper. */
+void lzb_field_checkerboard(lzb_field* f, uint64_t seed, int blocks);
+double lzb_field_eval_host(const lzb_field* f, double x, double y);
+
+/* ----------------------------------------------------------------- element */
+/* integrate_element(CellBox{x0,y0,h}, eps, n)          element.hpp:36-49
+ * batched over cells; out = ncells x 16 doubles (row-major Mat4).
+ * integration: LZB_INTEGRATE_EXACT (bit-identical) or LZB_INTEGRATE_FAST. */
+int lzb_integrate_elements(lzb_ctx* ctx, const lzb_field* eps, int64_t ncells,
+                           const double* x0, const double* y0, const double* h,
+                           const int32_t* n, double* out, int integration);
+int lzb_integrate_elements_dev(lzb_ctx* ctx, const lzb_field* eps, int64_t ncells,
+                               const double* x0, const double* y0, const double* h,
+                               const int32_t* n, double* out, int integration, void* stream);
+/* All cells of one regular level at one n: out[(cy*N+cx)*16 + k], N = 3^level,
+ * boxes as cell_box() (element.hpp:29-32) with h = pow(1/3, level) (mesh.hpp:87). */
+int lzb_integrate_level_dev(lzb_ctx* ctx, const lzb_field* eps, int level, int n,
+                            double* out, int integration, void* stream);
+/* reference_subcell_stiffness(a,b,c,d)                   element.hpp:19 */
+int lzb_subcell_stiffness(lzb_ctx* ctx, double a, double b, double c, double d, double* out16);
+
+/* ------------------------------------------------------------------- codec */
+/* codec::encode_value, batched: count values at one p3 -> count*p3 bytes. codec.hpp:23-26
+ * Non-finite input -> LZB_ERR_PROTOCOL (codec.cpp:10). */
+int lzb_codec_encode(lzb_ctx* ctx, int64_t count, const double* x, int p3, uint8_t* out);
+/* codec::decode_value, batched.                                              codec.hpp:28 */
+int lzb_codec_decode(lzb_ctx* ctx, int64_t count, const uint8_t* in, int p3, double* out);
+/* codec::choose_precision over nrec records of `entries` values.          codec.hpp:35-37 */
+int lzb_codec_choose_precision(lzb_ctx* ctx, int64_t nrec, int32_t entries, const double* values,
+                               double delta_max, int32_t* out_p3);
+int lzb_codec_choose_precision_dev(lzb_ctx* ctx, int64_t nrec, int32_t entries,
+                                   const double* values, double delta_max, int32_t* out_p3,
+                                   void* stream);
+/* pack_header / unpack_header                                         stream.hpp:30-33 */
+uint8_t lzb_pack_header(int32_t p1, int p2, int p3);
+int lzb_unpack_header(uint8_t h, int* p1_class, int* p2, int* p3);
+
+/* ---------------------------------------------------------------- transfer */
+/* galerkin_coarse_element(children, P): npatch x (9x16 children, child lx*3+ly)
+ * P = npatch x 64 or NULL for geometric_prolongation().       transfer.hpp:31-32 */
+int lzb_galerkin(lzb_ctx* ctx, int64_t npatch, const double* children, const double* P,
+                 double* out);
+/* boxmg_prolongation(children) -> npatch x 64, fallback rows.   transfer.hpp:28 */
+int lzb_boxmg(lzb_ctx* ctx, int64_t npatch, const double* children, double* P,
+              int32_t* fallback_rows);
+void lzb_geometric_prolongation(double* out64);
+
+/* -------------------------------------------------------------------- grid */
+/* One regular 2D spacetree with its operator stream, assembler and additive
+ * multigrid solver resident in HBM: Mesh + CellStream + Assembler +
+ * AdditiveSolver (mesh.hpp:64, stream.hpp:72, assembly.hpp:38, solver.hpp:72). */
+typedef struct lzb_grid lzb_grid;
+int lzb_grid_create(lzb_ctx* ctx, const lzb_grid_desc* desc, lzb_grid** out);
+void lzb_grid_destroy(lzb_grid* g);
+/* init_noise(mesh, problem)                                        problem.hpp:50 */
+int lzb_grid_init_noise(lzb_grid* g, uint64_t seed);
+/* Assembler::eager_setup                                          assembly.hpp:47 */
+int lzb_grid_eager_setup(lzb_grid* g);
+/* Fixed-p assembly (BASELINE config 1): every leaf integrated at n, published, p1 = top. */
+int lzb_grid_assemble_fixed(lzb_grid* g, int n);
+/* AdditiveSolver::step / run_cycles                             solver.hpp:78-79 */
+int lzb_grid_step(lzb_grid* g, lzb_cycle_report* out);
+int lzb_grid_run(lzb_grid* g, lzb_cycle_report* out, int cap, int* count);
+/* Individual passes (solver.hpp:91-98): 0 assembly, 1 residual (value = norm),
+ * 2 update, 3 prolong, 4 finish_cycle_sync, 5 stream begin_cycle, 6 pool begin_cycle. */
+int lzb_grid_pass(lzb_grid* g, int which, double* value);
+int lzb_grid_cycle(lzb_grid* g);
+/* Dense per-level vertex field: (N+1)^2 doubles, index iy*(N+1)+ix. */
+int lzb_grid_vertices(lzb_grid* g, int level, int field, double* buf, int write);
+/* Dense per-level cells, index cy*N+cx: element_or_baseline (16 doubles), markers. */
+int lzb_grid_cells(lzb_grid* g, int level, double* ops, int32_t* p1, int32_t* n, int32_t* p3,
+                   uint32_t* epoch);
+/* Transfer block of a refined cell (transfer_or_geometric, stream.hpp:106). */
+int lzb_grid_transfer(lzb_grid* g, int level, int cx, int cy, double* out64);
+/* CellStream::publish_element + marker store (stream.hpp:88, assembly protocol). */
+int lzb_grid_publish_element(lzb_grid* g, int level, int cx, int cy, const double* m16,
+                             int n, int32_t p1);
+/* Assembler::adaptive_step(cell)                                   assembly.hpp:40 */
+int lzb_grid_adaptive_step(lzb_grid* g, int level, int cx, int cy);
+/* CellStream::compression_stats                                    stream.hpp:118 */
+int lzb_grid_stats(lzb_grid* g, lzb_compression_stats* out);
+/* CellStream::save/load byte image ("LZMG" v1, stream.cpp:303-394).
+ * lzb_grid_stream_image with out == NULL returns the size in *size. */
+int lzb_grid_stream_image(lzb_grid* g, uint8_t* out, int64_t cap, int64_t* size);
+int lzb_grid_stream_load(lzb_grid* g, const uint8_t* in, int64_t size);
+int lzb_grid_save(lzb_grid* g, const char* path);
+int lzb_grid_load(lzb_grid* g, const char* path);
+/* Pending background tasks (TaskPool::pending_count, scheduler.hpp:45). */
+int64_t lzb_grid_pending(lzb_grid* g);
+/* Device pointers for callers composing their own kernels (read-only use). */
+int lzb_grid_device_view(lzb_grid* g, int level, int field, void** ptr);
+
+/* -------------------------------------------------------------- experiment */
+/* run_experiment(parse_config_file(path))               experiment.hpp:75,89
+ * Writes the telemetry CSV when the config names one; returns the exit code
+ * in *exit_code (0 converged, 2 diverged, 3 timeout, experiment.cpp:213-220). */
+int lzb_run_experiment_file(const char* cfg_path, int* exit_code, int* ncycles);
+int lzb_run_experiment_text(const char* cfg_text, int* exit_code, int* ncycles);
+/* Reports of the last run_experiment on this thread. */
+int lzb_last_reports(lzb_cycle_report* out, int cap, int* count);
+/* ExperimentConfig::to_keys rendered as "key = value\n" lines. experiment.hpp:68 */
+int lzb_config_keys(const char* cfg_text, char* out, int64_t cap);
+/* emit_table / compare_runs                                   experiment.hpp:99-104 */
+int lzb_emit_table(const char* csv_paths_newline_separated, char* out, int64_t cap);
+int lzb_compare_runs(const char* csv_a, const char* csv_b, char* out, int64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LZB_H */

@@ -1,1 +1,473 @@
-"""B200-native delayed-assembly hot path."""
+"""B200-native delayed-assembly hot path of arXiv 2005.03606.
+
+Python view of the C-ABI in ``include/lzb.h`` (``lib/liblzb.so``: hand-written
+sm_100a kernels + host C++). Names mirror the reference's C++ interface
+(``/root/reference/proj/include/lazymg``): ``integrate_element``,
+``codec.encode_value/decode_value/choose_precision``, ``galerkin_coarse_element``,
+``boxmg_prolongation``, and ``Grid`` = Mesh + CellStream + Assembler +
+AdditiveSolver on a regular 2D spacetree, plus ``run_experiment`` /
+``emit_table`` / ``compare_runs`` for the config / telemetry interface.
+
+There is no CPU fallback: every call runs on the GPU, and a missing library
+or device raises ``LzbError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+from . import _types as T
+from ._types import (CompressionStats, CycleReport, Field, GridDesc, Rhs, field_checkerboard,  # noqa: F401
+                     field_constant, field_quadrant, field_sinusoid, field_theta, report_dict)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "liblzb.so")
+
+
+class LzbError(RuntimeError):
+    """Status-coded failure of a C-ABI call (codes in include/lzb_types.h)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[lzb status {code}] {msg}")
+        self.code = code
+
+
+class ProtocolError(LzbError):  # lazymg::protocol_error
+    pass
+
+
+class CorruptStreamError(LzbError):  # lazymg::corrupt_stream_error
+    pass
+
+
+class ResourceError(LzbError):  # lazymg::resource_error
+    pass
+
+
+_EXC = {T.ERR_PROTOCOL: ProtocolError, T.ERR_CORRUPT: CorruptStreamError, T.ERR_RESOURCE: ResourceError}
+
+_lib = None
+
+
+def build():
+    """Compile liblzb.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+    subprocess.run(["make", "-s", "-C", os.path.join(HERE, "csrc")], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise LzbError(T.ERR_CUDA, f"{LIB_PATH} missing: run paper_2005_03606_b200.build()")
+        L = C.CDLL(LIB_PATH)
+        vp, i64, i32, dbl = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+        L.lzb_last_error.restype = C.c_char_p
+        L.lzb_launch_count.restype = C.c_uint64
+        L.lzb_ctx_create.argtypes = [C.c_int, C.POINTER(vp)]
+        L.lzb_ctx_destroy.argtypes = [vp]
+        L.lzb_ctx_synchronize.argtypes = [vp]
+        L.lzb_ctx_solve_stream.restype = vp
+        L.lzb_ctx_solve_stream.argtypes = [vp]
+        L.lzb_ctx_assembly_stream.restype = vp
+        L.lzb_ctx_assembly_stream.argtypes = [vp]
+        L.lzb_field_checkerboard.argtypes = [C.POINTER(Field), C.c_uint64, C.c_int]
+        L.lzb_field_eval_host.restype = dbl
+        L.lzb_field_eval_host.argtypes = [C.POINTER(Field), dbl, dbl]
+        L.lzb_integrate_elements.argtypes = [vp, C.POINTER(Field), i64, vp, vp, vp, vp, vp, C.c_int]
+        L.lzb_integrate_elements_dev.argtypes = [vp, C.POINTER(Field), i64, vp, vp, vp, vp, vp, C.c_int, vp]
+        L.lzb_integrate_level_dev.argtypes = [vp, C.POINTER(Field), C.c_int, C.c_int, vp, C.c_int, vp]
+        L.lzb_subcell_stiffness.argtypes = [vp, dbl, dbl, dbl, dbl, vp]
+        L.lzb_codec_encode.argtypes = [vp, i64, vp, C.c_int, vp]
+        L.lzb_codec_decode.argtypes = [vp, i64, vp, C.c_int, vp]
+        L.lzb_codec_choose_precision.argtypes = [vp, i64, i32, vp, dbl, vp]
+        L.lzb_codec_choose_precision_dev.argtypes = [vp, i64, i32, vp, dbl, vp, vp]
+        L.lzb_pack_header.restype = C.c_uint8
+        L.lzb_pack_header.argtypes = [i32, C.c_int, C.c_int]
+        L.lzb_unpack_header.argtypes = [C.c_uint8] + [C.POINTER(C.c_int)] * 3
+        L.lzb_galerkin.argtypes = [vp, i64, vp, vp, vp]
+        L.lzb_boxmg.argtypes = [vp, i64, vp, vp, vp]
+        L.lzb_geometric_prolongation.argtypes = [vp]
+        L.lzb_grid_create.argtypes = [vp, C.POINTER(GridDesc), C.POINTER(vp)]
+        L.lzb_grid_destroy.argtypes = [vp]
+        L.lzb_grid_init_noise.argtypes = [vp, C.c_uint64]
+        L.lzb_grid_eager_setup.argtypes = [vp]
+        L.lzb_grid_assemble_fixed.argtypes = [vp, C.c_int]
+        L.lzb_grid_step.argtypes = [vp, C.POINTER(CycleReport)]
+        L.lzb_grid_run.argtypes = [vp, vp, C.c_int, C.POINTER(C.c_int)]
+        L.lzb_grid_pass.argtypes = [vp, C.c_int, C.POINTER(dbl)]
+        L.lzb_grid_cycle.argtypes = [vp]
+        L.lzb_grid_vertices.argtypes = [vp, C.c_int, C.c_int, vp, C.c_int]
+        L.lzb_grid_cells.argtypes = [vp, C.c_int, vp, vp, vp, vp, vp]
+        L.lzb_grid_transfer.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp]
+        L.lzb_grid_publish_element.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, i32]
+        L.lzb_grid_adaptive_step.argtypes = [vp, C.c_int, C.c_int, C.c_int]
+        L.lzb_grid_stats.argtypes = [vp, C.POINTER(CompressionStats)]
+        L.lzb_grid_stream_image.argtypes = [vp, vp, i64, C.POINTER(i64)]
+        L.lzb_grid_stream_load.argtypes = [vp, vp, i64]
+        L.lzb_grid_save.argtypes = [vp, C.c_char_p]
+        L.lzb_grid_load.argtypes = [vp, C.c_char_p]
+        L.lzb_grid_pending.restype = i64
+        L.lzb_grid_pending.argtypes = [vp]
+        L.lzb_grid_device_view.argtypes = [vp, C.c_int, C.c_int, C.POINTER(vp)]
+        L.lzb_run_experiment_file.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.lzb_run_experiment_text.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.lzb_last_reports.argtypes = [vp, C.c_int, C.POINTER(C.c_int)]
+        L.lzb_config_keys.argtypes = [C.c_char_p, C.c_char_p, i64]
+        L.lzb_emit_table.argtypes = [C.c_char_p, C.c_char_p, i64]
+        L.lzb_compare_runs.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, i64]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib().lzb_last_error().decode()
+        raise _EXC.get(rc, LzbError)(rc, msg)
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def launch_count() -> int:
+    return lib().lzb_launch_count()
+
+
+class Context:
+    """Device + solve (high-priority) and assembly (low-priority) streams."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _check(lib().lzb_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().lzb_ctx_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def synchronize(self):
+        _check(lib().lzb_ctx_synchronize(self.h))
+
+    @property
+    def solve_stream(self):
+        return lib().lzb_ctx_solve_stream(self.h)
+
+
+_default_ctx = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(int(os.environ.get("LZB_DEVICE", "0")))
+    return _default_ctx
+
+
+def checkerboard(seed=1, blocks=8) -> Field:
+    """BASELINE config 1 eps (8x8 blocks of 10^U(-2,2)); table computed in C."""
+    f = Field()
+    lib().lzb_field_checkerboard(C.byref(f), seed, blocks)
+    return f
+
+
+# ------------------------------------------------------------------ element
+def integrate_elements(field: Field, x0, y0, h, n, integration="exact", ctx: Context | None = None):
+    """Batched integrate_element(CellBox{x0,y0,h}, eps, n) (element.hpp:36-49)."""
+    ctx = ctx or default_context()
+    x0 = np.ascontiguousarray(x0, dtype=np.float64).reshape(-1)
+    y0 = np.ascontiguousarray(np.broadcast_to(y0, x0.shape), dtype=np.float64)
+    h = np.ascontiguousarray(np.broadcast_to(h, x0.shape), dtype=np.float64)
+    n = np.ascontiguousarray(np.broadcast_to(n, x0.shape), dtype=np.int32)
+    out = np.zeros((x0.size, 16))
+    mode = T.INTEGRATE_FAST if integration == "fast" else T.INTEGRATE_EXACT
+    _check(lib().lzb_integrate_elements(ctx.h, C.byref(field), x0.size, _ptr(x0), _ptr(y0), _ptr(h), _ptr(n),
+                                        _ptr(out), mode))
+    return out
+
+
+def integrate_element(box, field: Field, n: int, integration="exact", ctx=None):
+    x0, y0, h = box
+    return integrate_elements(field, [x0], [y0], [h], [n], integration, ctx)[0]
+
+
+def reference_subcell_stiffness(a, b, c, d, ctx=None):
+    ctx = ctx or default_context()
+    out = np.zeros(16)
+    _check(lib().lzb_subcell_stiffness(ctx.h, a, b, c, d, _ptr(out)))
+    return out
+
+
+# ------------------------------------------------------------------ codec
+class codec:
+    """codec::encode_value / decode_value / roundtrip / choose_precision (codec.hpp:23-37)."""
+
+    @staticmethod
+    def encode(values, p3, ctx=None) -> np.ndarray:
+        ctx = ctx or default_context()
+        x = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+        out = np.zeros(x.size * p3, dtype=np.uint8)
+        _check(lib().lzb_codec_encode(ctx.h, x.size, _ptr(x), p3, _ptr(out)))
+        return out
+
+    @staticmethod
+    def decode(data, p3, ctx=None) -> np.ndarray:
+        ctx = ctx or default_context()
+        b = np.ascontiguousarray(data, dtype=np.uint8).reshape(-1)
+        out = np.zeros(b.size // p3)
+        _check(lib().lzb_codec_decode(ctx.h, out.size, _ptr(b), p3, _ptr(out)))
+        return out
+
+    @staticmethod
+    def encode_value(x, p3, ctx=None) -> bytes:
+        return codec.encode([x], p3, ctx).tobytes() if p3 else b""
+
+    @staticmethod
+    def decode_value(data, p3, ctx=None) -> float:
+        return float(codec.decode(np.frombuffer(bytes(data), np.uint8), p3, ctx)[0])
+
+    @staticmethod
+    def roundtrip(values, p3, ctx=None):
+        if p3 == 0:
+            return np.zeros(np.size(values))
+        return codec.decode(codec.encode(values, p3, ctx), p3, ctx)
+
+    @staticmethod
+    def choose_precision_records(values, entries, delta_max, ctx=None) -> np.ndarray:
+        ctx = ctx or default_context()
+        v = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+        nrec = v.size // entries
+        out = np.zeros(nrec, dtype=np.int32)
+        _check(lib().lzb_codec_choose_precision(ctx.h, nrec, entries, _ptr(v), delta_max, _ptr(out)))
+        return out
+
+    @staticmethod
+    def choose_precision(values, delta_max, ctx=None) -> int:
+        v = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+        return int(codec.choose_precision_records(v, v.size, delta_max, ctx)[0])
+
+
+def pack_header(p1, p2, p3) -> int:
+    return lib().lzb_pack_header(p1, 1 if p2 else 0, p3)
+
+
+def unpack_header(h):
+    cls, p2, p3 = C.c_int(), C.c_int(), C.c_int()
+    _check(lib().lzb_unpack_header(h, C.byref(cls), C.byref(p2), C.byref(p3)))
+    return cls.value, bool(p2.value), p3.value
+
+
+# ------------------------------------------------------------------ transfer
+def geometric_prolongation() -> np.ndarray:
+    out = np.zeros(64)
+    lib().lzb_geometric_prolongation(_ptr(out))
+    return out
+
+
+def galerkin_coarse_element(children, P=None, ctx=None) -> np.ndarray:
+    """Batched R A_patch P (transfer.hpp:31): children (..., 9, 16), P (..., 64) or None."""
+    ctx = ctx or default_context()
+    ch = np.ascontiguousarray(children, dtype=np.float64).reshape(-1, 144)
+    Pp = None if P is None else np.ascontiguousarray(P, dtype=np.float64).reshape(-1, 64)
+    out = np.zeros((ch.shape[0], 16))
+    _check(lib().lzb_galerkin(ctx.h, ch.shape[0], _ptr(ch), None if Pp is None else _ptr(Pp), _ptr(out)))
+    return out
+
+
+def boxmg_prolongation(children, ctx=None):
+    ctx = ctx or default_context()
+    ch = np.ascontiguousarray(children, dtype=np.float64).reshape(-1, 144)
+    P = np.zeros((ch.shape[0], 64))
+    fb = np.zeros(ch.shape[0], np.int32)
+    _check(lib().lzb_boxmg(ctx.h, ch.shape[0], _ptr(ch), _ptr(P), _ptr(fb)))
+    return P, fb
+
+
+# ------------------------------------------------------------------ grid
+def make_desc(depth=2, field: Field | None = None, rhs: float = 0.0, rhs_kind="constant",
+              rhs_scale=2 * np.pi ** 2, delta_max=1e-8, solver="adafac-pi", omega=0.7, target=1e-10,
+              divergence=1e2, max_cycles=500, assembly="adaptive", termination_c=0.01, schedule="increment",
+              n_max=0, integration="exact", transfer="geometric", gating=True, throttle=0, seed=0,
+              concurrent=False) -> GridDesc:
+    d = GridDesc()
+    d.dim = 2
+    d.depth = depth
+    d.field = field if field is not None else field_constant(1.0)
+    d.rhs = Rhs(kind=T.RHS_SINPROD, value=rhs_scale) if rhs_kind == "sinprod" else Rhs(kind=T.RHS_CONSTANT,
+                                                                                      value=rhs)
+    d.delta_max = delta_max
+    d.variant = {"additive": T.ADDITIVE, "adafac-jac": T.ADAFAC_JAC, "adafac-pi": T.ADAFAC_PI}[solver]
+    d.max_cycles = max_cycles
+    d.omega, d.target, d.divergence = omega, target, divergence
+    d.mode = {"eager": T.EAGER, "lazy": T.LAZY, "adaptive": T.ADAPTIVE, "anarchic": T.ANARCHIC}[assembly]
+    d.schedule = T.SCHEDULE_DOUBLE if schedule == "double" else T.SCHEDULE_INCREMENT
+    d.termination_c = termination_c
+    d.n_max = n_max
+    d.integration = T.INTEGRATE_FAST if integration == "fast" else T.INTEGRATE_EXACT
+    d.transfer = T.BOXMG if transfer == "boxmg" else T.GEOMETRIC
+    d.policy = T.ALWAYS
+    d.gating = 1 if gating else 0
+    d.concurrent = 1 if concurrent else 0
+    d.throttle = throttle
+    d.noise_seed = seed
+    return d
+
+
+class Grid:
+    """Mesh + CellStream + Assembler + AdditiveSolver of one regular 2D
+    spacetree, resident on the GPU (solver.hpp:72-126 semantics)."""
+
+    def __init__(self, desc: GridDesc, noise_seed: int | None = None, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.desc = desc
+        self.depth = desc.depth
+        h = C.c_void_p()
+        _check(lib().lzb_grid_create(self.ctx.h, C.byref(desc), C.byref(h)))
+        self.h = h
+        if noise_seed is not None:
+            self.init_noise(noise_seed)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().lzb_grid_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def init_noise(self, seed):
+        _check(lib().lzb_grid_init_noise(self.h, seed))
+
+    def eager_setup(self):
+        _check(lib().lzb_grid_eager_setup(self.h))
+
+    def assemble_fixed(self, n):
+        _check(lib().lzb_grid_assemble_fixed(self.h, n))
+
+    def step(self) -> dict:
+        r = CycleReport()
+        _check(lib().lzb_grid_step(self.h, C.byref(r)))
+        return report_dict(r)
+
+    def run(self, cap=100000):
+        arr = (CycleReport * cap)()
+        n = C.c_int()
+        _check(lib().lzb_grid_run(self.h, arr, cap, C.byref(n)))
+        return [report_dict(arr[i]) for i in range(min(cap, n.value))]
+
+    def pass_(self, which):
+        v = C.c_double()
+        _check(lib().lzb_grid_pass(self.h, which, C.byref(v)))
+        return v.value
+
+    assembly_pass = lambda self: self.pass_(0)  # noqa: E731
+    residual_pass = lambda self: self.pass_(1)  # noqa: E731
+
+    def cycle(self):
+        return lib().lzb_grid_cycle(self.h)
+
+    def vertices(self, level, field):
+        N = 3 ** level
+        out = np.zeros((N + 1) * (N + 1))
+        _check(lib().lzb_grid_vertices(self.h, level, field, _ptr(out), 0))
+        return out.reshape(N + 1, N + 1)
+
+    def set_vertices(self, level, field, values):
+        v = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+        _check(lib().lzb_grid_vertices(self.h, level, field, _ptr(v), 1))
+
+    def cells(self, level):
+        N = 3 ** level
+        ops = np.zeros((N * N, 16))
+        p1 = np.zeros(N * N, np.int32)
+        n = np.zeros(N * N, np.int32)
+        p3 = np.zeros(N * N, np.int32)
+        ep = np.zeros(N * N, np.uint32)
+        _check(lib().lzb_grid_cells(self.h, level, _ptr(ops), _ptr(p1), _ptr(n), _ptr(p3), _ptr(ep)))
+        return dict(ops=ops, p1=p1, n=n, p3=p3, epoch=ep)
+
+    def transfer(self, level, cx, cy):
+        out = np.zeros(64)
+        _check(lib().lzb_grid_transfer(self.h, level, cx, cy, _ptr(out)))
+        return out
+
+    def publish_element(self, level, cx, cy, m, n, p1):
+        m = np.ascontiguousarray(m, dtype=np.float64)
+        _check(lib().lzb_grid_publish_element(self.h, level, cx, cy, _ptr(m), n, p1))
+
+    def adaptive_step(self, level, cx, cy):
+        _check(lib().lzb_grid_adaptive_step(self.h, level, cx, cy))
+
+    def stats(self) -> CompressionStats:
+        s = CompressionStats()
+        _check(lib().lzb_grid_stats(self.h, C.byref(s)))
+        return s
+
+    def stream_image(self) -> bytes:
+        size = C.c_int64()
+        _check(lib().lzb_grid_stream_image(self.h, None, 0, C.byref(size)))
+        buf = np.zeros(size.value, np.uint8)
+        _check(lib().lzb_grid_stream_image(self.h, _ptr(buf), buf.size, C.byref(size)))
+        return buf[: size.value].tobytes()
+
+    def load_image(self, data: bytes):
+        b = np.frombuffer(data, np.uint8).copy()
+        _check(lib().lzb_grid_stream_load(self.h, _ptr(b), b.size))
+
+    def save(self, path):
+        _check(lib().lzb_grid_save(self.h, str(path).encode()))
+
+    def load(self, path):
+        _check(lib().lzb_grid_load(self.h, str(path).encode()))
+
+    def pending(self) -> int:
+        return lib().lzb_grid_pending(self.h)
+
+    def device_view(self, level, field) -> int:
+        p = C.c_void_p()
+        _check(lib().lzb_grid_device_view(self.h, level, field, C.byref(p)))
+        return p.value
+
+
+# ------------------------------------------------------------------ experiment
+def run_experiment(cfg_text: str):
+    """run_experiment(parse_config_file) (experiment.hpp:75,89); returns (exit_code, reports)."""
+    ec, nc = C.c_int(), C.c_int()
+    _check(lib().lzb_run_experiment_text(cfg_text.encode(), C.byref(ec), C.byref(nc)))
+    arr = (CycleReport * max(nc.value, 1))()
+    cnt = C.c_int()
+    lib().lzb_last_reports(arr, max(nc.value, 1), C.byref(cnt))
+    return ec.value, [report_dict(arr[i]) for i in range(nc.value)]
+
+
+def run_experiment_file(path: str):
+    ec, nc = C.c_int(), C.c_int()
+    _check(lib().lzb_run_experiment_file(str(path).encode(), C.byref(ec), C.byref(nc)))
+    return ec.value, nc.value
+
+
+def config_keys(cfg_text: str) -> dict:
+    buf = C.create_string_buffer(1 << 16)
+    _check(lib().lzb_config_keys(cfg_text.encode(), buf, len(buf)))
+    out = {}
+    for line in buf.value.decode().splitlines():
+        k, v = line.split(" = ", 1)
+        out[k] = v
+    return out
+
+
+def emit_table(paths) -> str:
+    buf = C.create_string_buffer(1 << 20)
+    _check(lib().lzb_emit_table("\n".join(str(p) for p in paths).encode(), buf, len(buf)))
+    return buf.value.decode()
+
+
+def compare_runs(a, b) -> str:
+    buf = C.create_string_buffer(1 << 16)
+    _check(lib().lzb_compare_runs(str(a).encode(), str(b).encode(), buf, len(buf)))
+    return buf.value.decode()

@@ -1,0 +1,291 @@
+// device.cuh — sm_100a device primitives of the delayed-assembly path.
+//
+// Translation units that include this header for the EXACT path are compiled
+// with -fmad=false: every expression below keeps the reference's operand
+// order, so with FMA contraction off the device produces the same IEEE-754
+// results as the reference on x86-64 (which has no FMA at -O3 without -march).
+#pragma once
+
+#include <cstdint>
+
+#include "lzb_types.h"
+
+namespace lzb {
+
+constexpr double kPi = 3.14159265358979323846;  // == std::numbers::pi (problem.cpp:11)
+// quadrant centre, problem.cpp:18: 0.5 + 1/(2*2187)
+constexpr double kQuadCentre = 0.5 + 1.0 / (2.0 * 2187.0);
+
+__host__ __device__ inline int cdx(int c) { return c & 1; }   // types.hpp:14
+__host__ __device__ inline int cdy(int c) { return c >> 1; }  // types.hpp:15
+
+// ------------------------------------------------------------------ eps parts
+// eps(x, y) = combine(xpart(x), ypart(y)) reproduces the reference expression
+// tree exactly (problem.cpp:9-31 for kinds 0-2; BASELINE kinds 3-4):
+//   theta:    1.0 + ((0.15 * px) * py),  px = exp(-t x) cos(pi t x)
+//   sinusoid: 1.0 + ((amp * sx) * sy),   sx = sin(freq pi x)
+//   quadrant: (x >= c) == (y >= c) ? 1 : eps_low
+//   checker:  T[min(B-1, int(B x))][min(B-1, int(B y))]
+__device__ inline double field_xpart(const lzb_field& f, double x) {
+    switch (f.kind) {
+        case LZB_FIELD_THETA: {
+            const double amplitude = 0.3 / 2.0;
+            double px = exp(-f.theta * x) * cos(kPi * f.theta * x);
+            return amplitude * px;
+        }
+        case LZB_FIELD_QUADRANT: return x >= kQuadCentre ? 1.0 : 0.0;
+        case LZB_FIELD_CHECKER: {
+            int b = static_cast<int>(f.blocks * x);
+            return static_cast<double>(b < f.blocks - 1 ? b : f.blocks - 1);
+        }
+        case LZB_FIELD_SINUSOID: return f.amp * sin(f.freq * kPi * x);
+        default: return 0.0;
+    }
+}
+__device__ inline double field_ypart(const lzb_field& f, double y) {
+    switch (f.kind) {
+        case LZB_FIELD_THETA: return exp(-f.theta * y) * cos(kPi * f.theta * y);
+        case LZB_FIELD_QUADRANT: return y >= kQuadCentre ? 1.0 : 0.0;
+        case LZB_FIELD_CHECKER: {
+            int b = static_cast<int>(f.blocks * y);
+            return static_cast<double>(b < f.blocks - 1 ? b : f.blocks - 1);
+        }
+        case LZB_FIELD_SINUSOID: return sin(f.freq * kPi * y);
+        default: return 0.0;
+    }
+}
+__device__ inline double field_combine(const lzb_field& f, double xp, double yp) {
+    switch (f.kind) {
+        case LZB_FIELD_THETA:
+        case LZB_FIELD_SINUSOID: return 1.0 + xp * yp;
+        case LZB_FIELD_QUADRANT: return xp == yp ? 1.0 : f.eps_low;
+        case LZB_FIELD_CHECKER:
+            return f.table[static_cast<int>(xp) * f.blocks + static_cast<int>(yp)];
+        default: return f.value;
+    }
+}
+__device__ inline double field_eval(const lzb_field& f, double x, double y) {
+    return field_combine(f, field_xpart(f, x), field_ypart(f, y));
+}
+
+// ------------------------------------------------------- sub-cell stiffness
+// seg_int, element.cpp:8-15 (same operand order).
+__host__ __device__ inline double seg_int(int si, int sj, double a, double b) {
+    double a0 = si ? 0.0 : 1.0, a1 = si ? 1.0 : -1.0;
+    double b0 = sj ? 0.0 : 1.0, b1 = sj ? 1.0 : -1.0;
+    double Fb = a0 * b0 * b + (a0 * b1 + a1 * b0) * b * b / 2.0 + a1 * b1 * b * b * b / 3.0;
+    double Fa = a0 * b0 * a + (a0 * b1 + a1 * b0) * a * a / 2.0 + a1 * b1 * a * a * a / 3.0;
+    return Fb - Fa;
+}
+
+// Per-axis part of reference_subcell_stiffness on [t0, t1] (element.cpp:19-32):
+// len = t1 - t0 and S_k = seg_int over the three corner-pair classes
+// k = s_i + s_j (seg_int(0,1) == seg_int(1,0) bit for bit).
+struct AxisSeg {
+    double len, s0, s1, s2;
+};
+__host__ __device__ inline AxisSeg axis_seg(int i, double inv) {
+    double a = i * inv, b = (i + 1) * inv;
+    return {b - a, seg_int(0, 0, a, b), seg_int(0, 1, a, b), seg_int(1, 1, a, b)};
+}
+
+// The 16 entries of K_sub(i,j) take 9 distinct values (symmetry and the
+// (0,3)/(1,2) coincidence). K = sign_x * len_x*S_y[cy_r+cy_c] + sign_y * len_y*S_x[cx_r+cx_c]
+// with sign_x = + iff cx_r == cx_c; each product/sum rounds exactly as in
+// element.cpp:26-27 because the +-1 factors are exact.
+struct K9 {
+    double k00, k11, k22, k33, k01, k23, k02, k13, k03;
+};
+__host__ __device__ inline K9 ksub(const AxisSeg& X, const AxisSeg& Y) {
+    double A0 = X.len * Y.s0, A1 = X.len * Y.s1, A2 = X.len * Y.s2;
+    double B0 = Y.len * X.s0, B1 = Y.len * X.s1, B2 = Y.len * X.s2;
+    K9 k;
+    k.k00 = A0 + B0;
+    k.k11 = A0 + B2;
+    k.k22 = A2 + B0;
+    k.k33 = A2 + B2;
+    k.k01 = -A0 + B1;
+    k.k23 = -A2 + B1;
+    k.k02 = A1 + -B0;
+    k.k13 = A1 + -B2;
+    k.k03 = -A1 + -B1;
+    return k;
+}
+__host__ __device__ inline void k9_expand(const double* a9, double* m) {
+    // a9 order: k00,k11,k22,k33,k01,k23,k02,k13,k03
+    m[0] = a9[0]; m[5] = a9[1]; m[10] = a9[2]; m[15] = a9[3];
+    m[1] = m[4] = a9[4];
+    m[11] = m[14] = a9[5];
+    m[2] = m[8] = a9[6];
+    m[7] = m[13] = a9[7];
+    m[3] = m[12] = m[6] = m[9] = a9[8];
+}
+
+// ------------------------------------------------------------------ codec
+// codec.cpp:8-85, value-for-value.
+__host__ __device__ inline int mantissa_bits(int p3) { return 8 * (p3 - 1) - 1; }
+
+__device__ inline bool dev_isfinite(double x) {
+    return (__double_as_longlong(x) & 0x7ff0000000000000ll) != 0x7ff0000000000000ll;
+}
+
+// Returns false for non-finite x (protocol_error, codec.cpp:10).
+__device__ inline bool encode_value(double x, int p3, uint8_t* out) {
+    if (p3 == 0) return true;
+    if (!dev_isfinite(x)) return false;
+    if (p3 == 8) {
+        unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+        for (int k = 0; k < 8; ++k) out[k] = static_cast<uint8_t>(b >> (8 * k));
+        return true;
+    }
+    const int m = mantissa_bits(p3);
+    unsigned long long frac_bits = 0;
+    int sign = 0, e_hat = -128;
+    if (x != 0.0) {
+        sign = __double_as_longlong(x) < 0 ? 1 : 0;
+        int e;
+        double f = frexp(fabs(x), &e);
+        e -= 1;
+        double frac = 2.0 * f - 1.0;
+        e_hat = e < -128 ? -128 : (e > 127 ? 127 : e);
+        frac_bits = static_cast<unsigned long long>(ldexp(frac, m));
+    }
+    unsigned long long packed = (static_cast<unsigned long long>(sign) << m) | frac_bits;
+    const int total_bits = m + 1;
+    for (int b = 0; b < p3 - 1; ++b)
+        out[b] = static_cast<uint8_t>(packed >> (total_bits - 8 * (b + 1)));
+    out[p3 - 1] = static_cast<uint8_t>(static_cast<int8_t>(e_hat));
+    return true;
+}
+
+__device__ inline double decode_value(const uint8_t* in, int p3) {
+    if (p3 == 8) {
+        unsigned long long b = 0;
+        for (int k = 7; k >= 0; --k) b = (b << 8) | in[k];
+        return __longlong_as_double(static_cast<long long>(b));
+    }
+    const int m = mantissa_bits(p3);
+    unsigned long long packed = 0;
+    for (int b = 0; b < p3 - 1; ++b) packed = (packed << 8) | in[b];
+    int sign = static_cast<int>((packed >> m) & 1ull);
+    unsigned long long frac_bits = packed & ((1ull << m) - 1);
+    int e_hat = static_cast<int8_t>(in[p3 - 1]);
+    if (sign == 0 && frac_bits == 0 && e_hat == -128) return 0.0;
+    double mant = 1.0 + ldexp(static_cast<double>(frac_bits), -m);
+    double v = ldexp(mant, e_hat);
+    return sign ? -v : v;
+}
+
+// codec::roundtrip (codec.hpp:28-33) without the byte detour: the same
+// encode/decode arithmetic on registers. Returns false for non-finite.
+__device__ inline bool roundtrip(double x, int p3, double& out) {
+    if (p3 == 0) {
+        out = 0.0;
+        return true;
+    }
+    if (!dev_isfinite(x)) return false;
+    if (p3 == 8) {
+        out = x;
+        return true;
+    }
+    const int m = mantissa_bits(p3);
+    if (x == 0.0) {
+        out = 0.0;  // sign 0, frac 0, exponent -128 -> decodes to +0 (codec.cpp:28,58)
+        return true;
+    }
+    int e;
+    double f = frexp(fabs(x), &e);
+    e -= 1;
+    double frac = 2.0 * f - 1.0;
+    int e_hat = e < -128 ? -128 : (e > 127 ? 127 : e);
+    unsigned long long frac_bits = static_cast<unsigned long long>(ldexp(frac, m));
+    bool neg = __double_as_longlong(x) < 0;
+    if (!neg && frac_bits == 0 && e_hat == -128) {
+        out = 0.0;
+        return true;
+    }
+    double mant = 1.0 + ldexp(static_cast<double>(frac_bits), -m);
+    double v = ldexp(mant, e_hat);
+    out = neg ? -v : v;
+    return true;
+}
+
+// codec::choose_precision (codec.cpp:65-85). Returns -1 for non-finite input.
+__device__ inline int choose_precision(const double* v, int count, double delta) {
+    bool all_small = true;
+    for (int i = 0; i < count; ++i)
+        if (fabs(v[i]) > delta) {
+            all_small = false;
+            break;
+        }
+    if (all_small) return 0;
+    for (int p3 = 2; p3 < 8; ++p3) {
+        bool ok = true;
+        for (int i = 0; i < count; ++i) {
+            double rt;
+            if (!roundtrip(v[i], p3, rt)) return -1;
+            if (fabs(rt - v[i]) > delta) {
+                ok = false;
+                break;
+            }
+        }
+        if (ok) return p3;
+    }
+    return 8;
+}
+
+__host__ __device__ inline uint8_t pack_header(int32_t p1, int p2, int p3) {  // stream.cpp:44-47
+    int cls = p1 == LZB_P1_BOTTOM ? 0 : (p1 == LZB_P1_TOP ? 2 : 1);
+    return static_cast<uint8_t>((cls << 6) | (p2 ? 0x20 : 0) | (p3 & 0x0f));
+}
+
+// ------------------------------------------------------------- spacetree
+// Regular k=3 spacetree, level l has N = 3^l cells per axis. Creation rank of
+// cell (cx,cy) in level_cells order (mesh.cpp:83-93: parents in order,
+// children x-major) is rx[cx] + ry[cy]; same-level pre-order slots order the
+// same way, which is what owns_lattice_vertex compares (solver.cpp:39-57).
+struct LevelView {
+    int N;
+    int depth_of_grid;
+    double h;       // pow(1/3, l)    mesh.hpp:87
+    double pow3l;   // pow(3.0, l)    mesh.hpp:158 (Vertex::x divisor)
+    const int32_t* rx;
+    const int32_t* ry;
+    double* v[LZB_V_NFIELDS];
+    double* op;     // 16 doubles per cell (decoded stored operator, AoS)
+    double* P;      // 64 doubles per refined cell, or nullptr (geometric)
+    int32_t* p1;
+    uint8_t* p2;
+    int8_t* p3;
+    int32_t* n;
+    uint32_t* epoch;
+    uint8_t* has_P;
+};
+
+__device__ inline int32_t crank(const LevelView& L, int cx, int cy) { return L.rx[cx] + L.ry[cy]; }
+
+// Owner patch (level l-1 cell) of fine vertex (fx,fy): the minimum-rank
+// refined patch whose 4x4 lattice contains it (solver.cpp:39-57).
+__device__ inline void owner_patch(const LevelView& C, int fx, int fy, int& px, int& py) {
+    int x1 = fx / 3, y1 = fy / 3;
+    int x0 = (fx % 3 == 0 && x1 > 0) ? x1 - 1 : x1;
+    int y0 = (fy % 3 == 0 && y1 > 0) ? y1 - 1 : y1;
+    if (x1 > C.N - 1) x1 = C.N - 1;
+    if (y1 > C.N - 1) y1 = C.N - 1;
+    px = x0;
+    py = y0;
+    int32_t best = crank(C, x0, y0);
+    int32_t r;
+    if (x1 != x0 && (r = crank(C, x1, y0)) < best) { best = r; px = x1; py = y0; }
+    if (y1 != y0 && (r = crank(C, x0, y1)) < best) { best = r; px = x0; py = y1; }
+    if (x1 != x0 && y1 != y0 && (r = crank(C, x1, y1)) < best) { best = r; px = x1; py = y1; }
+}
+
+// Geometric transfer weights (transfer.cpp:11-21), as a function.
+__host__ __device__ inline double geo_weight(int L, int c) {
+    int lx = L % 4, ly = L / 4;
+    double fx = lx / 3.0, fy = ly / 3.0;
+    return (cdx(c) ? fx : 1.0 - fx) * (cdy(c) ? fy : 1.0 - fy);
+}
+
+}  // namespace lzb

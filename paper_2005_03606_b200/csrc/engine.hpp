@@ -1,0 +1,110 @@
+// engine.hpp — host-side runtime of liblzb.so: context, errors, launch
+// accounting, the regular-grid engine class.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lzb.h"
+
+namespace lzb {
+
+// One exception type per lzb_status; the C-ABI maps them to codes and the C++
+// host shim rethrows the reference's own exception types.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+extern std::atomic<uint64_t> g_launches;
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw Error(LZB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define LZB_CUDA(x) ::lzb::cuda_check((x), #x)
+// Every kernel launch goes through this: counts launches and surfaces
+// launch-configuration errors immediately.
+#define LZB_LAUNCH(kernel, grid, block, smem, stream, ...)                         \
+    do {                                                                           \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                \
+        ::lzb::g_launches.fetch_add(1, std::memory_order_relaxed);                 \
+        ::lzb::cuda_check(cudaGetLastError(), #kernel);                            \
+    } while (0)
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return LZB_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_last_error("host allocation failed");
+        return LZB_ERR_RESOURCE;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return LZB_ERR_IO;
+    }
+}
+
+inline unsigned blocks_for(int64_t n, int threads) {
+    int64_t b = (n + threads - 1) / threads;
+    return static_cast<unsigned>(b < 1 ? 1 : b);
+}
+
+// Device buffer with RAII.
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) {
+            cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+            if (e != cudaSuccess)
+                throw Error(e == cudaErrorMemoryAllocation ? LZB_ERR_RESOURCE : LZB_ERR_CUDA,
+                            std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        }
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+}  // namespace lzb
+
+struct lzb_ctx {
+    int device = 0;
+    cudaStream_t solve = nullptr;
+    cudaStream_t assembly = nullptr;
+    lzb::DevBuf<int> err;  // device error flag (non-finite encode etc.)
+};
+
+namespace lzb {
+lzb_ctx* make_ctx(int device);
+void destroy_ctx(lzb_ctx* c);
+// Throws LZB_ERR_PROTOCOL if a device kernel raised the error flag since the last check.
+void check_device_flag(lzb_ctx* c, cudaStream_t s);
+}  // namespace lzb

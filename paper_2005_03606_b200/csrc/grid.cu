@@ -1,0 +1,1616 @@
+// grid.cu — the regular-grid engine: Mesh + CellStream + Assembler +
+// AdditiveSolver of the reference, resident in HBM, driven by sm_100a kernels.
+//
+// Layout in HBM (per level l, N = 3^l):
+//   vertex fields u, fl, r, rhat, uhat, diag, aux, usnap: (N+1)^2 doubles each,
+//     index iy*(N+1)+ix (SoA: one coalesced stream per field);
+//   cell operators: 16 doubles per cell (AoS, 128 B = one cache line pair),
+//     index cy*N+cx; markers p1 (int32), p2 (u8), p3 (i8), n, epoch;
+//   transfer blocks: 64 doubles per refined cell, only for transfer = boxmg
+//     (geometric blocks are implicit: decoded P == geometric, stream.cpp:134-151).
+//
+// Every floating-point accumulation that the reference performs in a fixed
+// order (cell-wise scatter over level_cells, patch-wise restriction over owned
+// lattice vertices) is re-expressed as a per-vertex gather that visits the
+// contributing cells in the reference's creation-rank order, so the solver
+// state is bit-identical to the reference (tests/test_gpu_parity.py).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <functional>
+
+#include "engine.hpp"
+#include "kernels.cuh"
+
+namespace lzb {
+
+void build_axis_tables(const lzb_field& f, int N, double h, int n, double* tx, double* ty,
+                       cudaStream_t s);
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kNormBlocks = 296;  // 2 x 148 SMs
+constexpr int kNHist = 4097;      // p1 histogram bins (n < 4096)
+
+// Result block copied to the host once per cycle.
+struct Result {
+    double norm;
+    unsigned long long s[16];
+};
+enum StatSlot {
+    S_HIST = 0,         // 0..8 p3 histogram over leaves
+    S_FINE_BYTES = 9,
+    S_NSUM = 10,
+    S_MAXN = 11,
+    S_TOTAL_BYTES = 12,
+    S_ZERO_NORM = 13,   // cumulative
+    S_MAXDELTA = 14,    // cumulative, bits of a non-negative double
+    S_MAXSAMPLES = 15,  // cumulative
+};
+
+__device__ inline int64_t gtid() { return blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; }
+
+__device__ inline double baseline_entry(int k, double e) { return 0.0 + c_kunit[k] * e; }
+
+__device__ inline double centre_eps(const lzb_field& f, const LevelView& L, int cx, int cy) {
+    // integrate_element(box, eps, 1): sample at x0 + ((0+0.5)*1.0)*h (element.hpp:44)
+    double x0 = cx * L.h, y0 = cy * L.h;
+    return field_eval(f, x0 + (0 + 0.5) * 1.0 * L.h, y0 + (0 + 0.5) * 1.0 * L.h);
+}
+
+__device__ inline const double* transfer_of(const LevelView& C, int c) {
+    return (C.has_P[c] && C.P) ? C.P + 64 * static_cast<int64_t>(c) : c_geo;
+}
+
+__device__ inline void element_or_baseline(const lzb_field& f, const LevelView& L, int cx, int cy,
+                                           double* K) {
+    int c = cy * L.N + cx;
+    if (L.p1[c] != LZB_P1_BOTTOM) {
+        const double2* src = reinterpret_cast<const double2*>(L.op + 16 * static_cast<int64_t>(c));
+        for (int k = 0; k < 8; ++k) {
+            double2 t = src[k];
+            K[2 * k] = t.x;
+            K[2 * k + 1] = t.y;
+        }
+    } else {
+        double e = centre_eps(f, L, cx, cy);
+        for (int k = 0; k < 16; ++k) K[k] = baseline_entry(k, e);
+    }
+}
+
+__device__ inline void atomic_max_double_bits(unsigned long long* a, double v) {
+    atomicMax(a, static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+// CellStream::publish_element (stream.cpp:100-132); caller stores p1.
+__device__ inline bool publish_leaf(const LevelView& F, int c, const double* m, int n, double e_c,
+                                    double delta_max, uint32_t cycle, unsigned long long* stats) {
+    double base[16], sur[16];
+    for (int k = 0; k < 16; ++k) {
+        base[k] = baseline_entry(k, e_c);
+        sur[k] = m[k] - base[k];
+    }
+    int p3 = choose_precision(sur, 16, delta_max);
+    if (p3 < 0) return false;
+    double delta = 0.0;
+    double* op = F.op + 16 * static_cast<int64_t>(c);
+    for (int k = 0; k < 16; ++k) {
+        double rt;
+        roundtrip(sur[k], p3, rt);
+        double err = fabs(rt - sur[k]);
+        delta = delta < err ? err : delta;
+        op[k] = base[k] + rt;
+    }
+    atomic_max_double_bits(&stats[S_MAXDELTA], delta);
+    atomicMax(&stats[S_MAXSAMPLES], static_cast<unsigned long long>(n));
+    F.n[c] = n;
+    F.epoch[c] = cycle;
+    F.p3[c] = static_cast<int8_t>(p3);
+    return true;
+}
+
+// -------------------------------------------------------------- assembly
+__global__ void k_compact(LevelView F, int selector, int32_t* list, int32_t* snap, int* count,
+                          unsigned* hist, const long long* keys, long long key_limit) {
+    int64_t c = gtid();
+    int64_t nc = static_cast<int64_t>(F.N) * F.N;
+    bool take = false;
+    int32_t p1 = 0;
+    if (c < nc) {
+        p1 = F.p1[c];
+        if (selector == 0) take = p1 != LZB_P1_TOP;                        // unconverged
+        else if (selector == 1) take = F.p2[c] != 0 && (!keys || keys[c] <= key_limit);  // tasks
+        else take = p1 == LZB_P1_BOTTOM;                                   // bottom
+        if (p1 == LZB_P1_TOP) take = take && selector == 1;  // a task on a top cell still completes
+    }
+    unsigned mask = __ballot_sync(0xffffffffu, take);
+    if (!mask) return;
+    int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(count, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (take) {
+        int pos = base + __popc(mask & ((1u << lane) - 1));
+        list[pos] = static_cast<int32_t>(c);
+        snap[pos] = p1;
+        int bin = p1 == LZB_P1_TOP ? kNHist - 1 : (p1 < kNHist - 1 ? p1 : kNHist - 1);
+        atomicAdd(&hist[bin], 1u);
+    }
+}
+
+// p1 = bottom -> integrate with n = 1, publish, p1 = 1 (assembly.cpp:26-34).
+__global__ void k_bottom(LevelView F, lzb_field f, const int32_t* list, const int32_t* snap,
+                         int count, double delta_max, uint32_t cycle, int clear_p2,
+                         unsigned long long* stats, int* err) {
+    int64_t t = gtid();
+    if (t >= count || snap[t] != LZB_P1_BOTTOM) return;
+    int c = list[t], cx = c % F.N, cy = c / F.N;
+    double e = centre_eps(f, F, cx, cy), m[16];
+    for (int k = 0; k < 16; ++k) m[k] = baseline_entry(k, e);
+    if (!publish_leaf(F, c, m, 1, e, delta_max, cycle, stats)) atomicExch(err, 1);
+    F.p1[c] = 1;
+    if (clear_p2) F.p2[c] = 0;
+}
+
+// p1 = n -> (n+1)^2 (or (2n)^2) integration, max-norm comparison, keep or
+// publish (assembly.cpp:36-59). Fused K1 + K3: integrate, surplus,
+// choose_precision, roundtrip, store.
+template <int KIND, bool FAST>
+__global__ void __launch_bounds__(128) k_step(LevelView F, lzb_field f, const int32_t* list,
+                                              const int32_t* snap, int count, int n, int nn,
+                                              int n_cap_top, const double* __restrict__ tx,
+                                              const double* __restrict__ ty, double term_c,
+                                              double delta_max, uint32_t cycle, int clear_p2,
+                                              unsigned long long* stats, int* err) {
+    __shared__ double s_table[64];
+    if (KIND == LZB_FIELD_CHECKER)
+        for (int i = threadIdx.x; i < 64; i += blockDim.x) s_table[i] = f.table[i];
+    __syncthreads();
+    int64_t t = gtid();
+    if (t >= count || snap[t] != n) return;
+    int c = list[t], cx = c % F.N, cy = c / F.N;
+    if (n_cap_top) {  // sampling cap reached: the marker becomes top, nothing integrated
+        F.p1[c] = LZB_P1_TOP;
+        if (clear_p2) F.p2[c] = 0;
+        return;
+    }
+    double fresh[16];
+    const double* txc = tx + static_cast<int64_t>(cx) * nn * kTab;
+    const double* tyc = ty + static_cast<int64_t>(cy) * nn * kTab;
+    if (FAST)
+        integrate_fast_tab<KIND>(txc, tyc, nn, f.value, f.eps_low, f.blocks, s_table, fresh);
+    else
+        integrate_exact_tab<KIND>(txc, tyc, nn, f.value, f.eps_low, f.blocks, s_table, fresh);
+    const double* old = F.op + 16 * static_cast<int64_t>(c);
+    double denom = 0.0, dmax = 0.0;
+    for (int k = 0; k < 16; ++k) {
+        double a = fabs(old[k]);
+        denom = denom < a ? a : denom;
+        double d = fabs(fresh[k] - old[k]);
+        dmax = dmax < d ? d : dmax;
+    }
+    double ratio = 0.0;
+    if (denom == 0.0) atomicAdd(&stats[S_ZERO_NORM], 1ull);
+    else ratio = dmax / denom;
+    if (ratio < term_c) {
+        F.p1[c] = LZB_P1_TOP;  // keep the old matrix (assembly.cpp:47-53)
+    } else {
+        double e_c = centre_eps(f, F, cx, cy);
+        if (!publish_leaf(F, c, fresh, nn, e_c, delta_max, cycle, stats)) atomicExch(err, 1);
+        F.p1[c] = nn;
+    }
+    if (clear_p2) F.p2[c] = 0;
+}
+
+// Anarchic request_stencil for non-bottom leaves: spawn if not top and not in
+// flight (assembly.cpp:95-106); key = FIFO position (spawn cycle, pre-order).
+__global__ void k_spawn(LevelView F, uint32_t cycle, long long leaf_count, long long* keys) {
+    int64_t c = gtid();
+    if (c >= static_cast<int64_t>(F.N) * F.N) return;
+    if (F.p1[c] == LZB_P1_TOP || F.p2[c]) return;
+    F.p2[c] = 1;
+    if (keys) keys[c] = static_cast<long long>(cycle) * leaf_count + crank(F, c % F.N, c / F.N);
+}
+
+// Fixed-p assembly: every leaf integrated at n, published, p1 = top.
+template <int KIND, bool FAST>
+__global__ void __launch_bounds__(128) k_fixed(LevelView F, lzb_field f, int n,
+                                               const double* __restrict__ tx,
+                                               const double* __restrict__ ty, double delta_max,
+                                               uint32_t cycle, unsigned long long* stats,
+                                               int* err) {
+    __shared__ double s_table[64];
+    if (KIND == LZB_FIELD_CHECKER)
+        for (int i = threadIdx.x; i < 64; i += blockDim.x) s_table[i] = f.table[i];
+    __syncthreads();
+    int64_t c = gtid();
+    if (c >= static_cast<int64_t>(F.N) * F.N) return;
+    int cx = static_cast<int>(c % F.N), cy = static_cast<int>(c / F.N);
+    double m[16];
+    const double* txc = tx + static_cast<int64_t>(cx) * n * kTab;
+    const double* tyc = ty + static_cast<int64_t>(cy) * n * kTab;
+    if (FAST)
+        integrate_fast_tab<KIND>(txc, tyc, n, f.value, f.eps_low, f.blocks, s_table, m);
+    else
+        integrate_exact_tab<KIND>(txc, tyc, n, f.value, f.eps_low, f.blocks, s_table, m);
+    double e_c = centre_eps(f, F, cx, cy);
+    if (!publish_leaf(F, static_cast<int>(c), m, n, e_c, delta_max, cycle, stats)) atomicExch(err, 1);
+    F.p1[c] = LZB_P1_TOP;
+}
+
+// recompute_coarse + publish_coarse (solver.cpp:59-77, stream.cpp:134-184).
+__global__ void __launch_bounds__(64) k_coarse(LevelView C, LevelView F, lzb_field f, int boxmg,
+                                               double delta_max, uint32_t cycle,
+                                               unsigned long long* stats, int* err) {
+    int64_t c = gtid();
+    if (c >= static_cast<int64_t>(C.N) * C.N) return;
+    int cx = static_cast<int>(c % C.N), cy = static_cast<int>(c / C.N);
+    double ch[144];
+    for (int lx = 0; lx < 3; ++lx)
+        for (int ly = 0; ly < 3; ++ly) {
+            int64_t fc = static_cast<int64_t>(3 * cy + ly) * F.N + 3 * cx + lx;
+            if (F.p1[fc] == LZB_P1_BOTTOM) return;  // delayed semantics (solver.cpp:65)
+            const double* src = F.op + 16 * fc;
+            for (int k = 0; k < 16; ++k) ch[(lx * 3 + ly) * 16 + k] = src[k];
+        }
+    double A[256], P[64], m[16];
+    patch_operator_dev(ch, A);
+    if (boxmg) boxmg_from_A(A, P);
+    else
+        for (int k = 0; k < 64; ++k) P[k] = c_geo[k];
+    galerkin_from_A(A, P, m);
+    // publish_coarse: one p3 across A-hat and P-hat
+    double e_c = centre_eps(f, C, cx, cy);
+    double joint[80];
+    for (int k = 0; k < 16; ++k) joint[k] = m[k] - baseline_entry(k, e_c);
+    for (int k = 0; k < 64; ++k) joint[16 + k] = P[k] - c_geo[k];
+    int p3 = choose_precision(joint, 80, delta_max);
+    if (p3 < 0) {
+        atomicExch(err, 1);
+        return;
+    }
+    double delta = 0.0;
+    for (int k = 0; k < 80; ++k) {
+        double rt;
+        roundtrip(joint[k], p3, rt);
+        double e = fabs(rt - joint[k]);
+        delta = delta < e ? e : delta;
+        if (k < 16) m[k] = baseline_entry(k, e_c) + rt;
+        else P[k - 16] = c_geo[k - 16] + rt;
+    }
+    double* op = C.op + 16 * c;
+    if (C.p1[c] == LZB_P1_TOP && C.has_P[c]) {
+        bool same = true;
+        for (int k = 0; k < 16; ++k) same = same && (m[k] == op[k]);
+        const double* cur = C.P ? C.P + 64 * c : c_geo;
+        for (int k = 0; k < 64; ++k) same = same && (P[k] == cur[k]);
+        if (same) return;  // epoch stamps track real information flow (stream.cpp:153-158)
+    }
+    atomic_max_double_bits(&stats[S_MAXDELTA], delta);
+    for (int k = 0; k < 16; ++k) op[k] = m[k];
+    if (C.P)
+        for (int k = 0; k < 64; ++k) C.P[64 * c + k] = P[k];
+    C.has_P[c] = 1;
+    C.n[c] = 1;
+    C.epoch[c] = cycle;
+    C.p3[c] = static_cast<int8_t>(p3);
+    C.p1[c] = LZB_P1_TOP;
+}
+
+// ------------------------------------------------------------------ cycle
+__device__ inline void vcoords(int64_t vi, int N, int& ix, int& iy) {
+    ix = static_cast<int>(vi % (N + 1));
+    iy = static_cast<int>(vi / (N + 1));
+}
+__device__ inline bool boundary(int N, int ix, int iy) {
+    return ix == 0 || iy == 0 || ix == N || iy == N;
+}
+
+// Cells adjacent to vertex (ix,iy) sorted by creation rank; row = the
+// vertex's corner index in that cell.
+struct Adj {
+    int n;
+    int cx[4], cy[4], row[4];
+};
+__device__ inline Adj adjacent_cells(const LevelView& L, int ix, int iy) {
+    Adj a;
+    a.n = 0;
+    int32_t rk[4];
+    for (int dy = 0; dy < 2; ++dy)
+        for (int dx = 0; dx < 2; ++dx) {
+            int cx = ix - dx, cy = iy - dy;
+            if (cx < 0 || cy < 0 || cx >= L.N || cy >= L.N) continue;
+            int32_t r = crank(L, cx, cy);
+            int p = a.n++;
+            while (p > 0 && rk[p - 1] > r) {
+                rk[p] = rk[p - 1];
+                a.cx[p] = a.cx[p - 1];
+                a.cy[p] = a.cy[p - 1];
+                a.row[p] = a.row[p - 1];
+                --p;
+            }
+            rk[p] = r;
+            a.cx[p] = cx;
+            a.cy[p] = cy;
+            a.row[p] = dx + 2 * dy;
+        }
+    return a;
+}
+
+// init_level_rhs on the leaf level (solver.cpp:99-118): fl = sum over
+// adjacent leaves of w * f(v) (identical terms, so order-free).
+__global__ void k_init_rhs(LevelView F, lzb_rhs rhs, double w) {
+    int64_t vi = gtid();
+    if (vi >= static_cast<int64_t>(F.N + 1) * (F.N + 1)) return;
+    int ix, iy;
+    vcoords(vi, F.N, ix, iy);
+    int adj = 0;
+    for (int dy = 0; dy < 2; ++dy)
+        for (int dx = 0; dx < 2; ++dx) {
+            int cx = ix - dx, cy = iy - dy;
+            adj += (cx >= 0 && cy >= 0 && cx < F.N && cy < F.N);
+        }
+    double x = ix / F.pow3l, y = iy / F.pow3l;
+    double fv = rhs.kind == LZB_RHS_SINPROD ? rhs.value * sin(kPi * x) * sin(kPi * y) : rhs.value;
+    double term = w * fv, fl = 0.0;
+    for (int k = 0; k < adj; ++k) fl += term;
+    F.v[LZB_V_FL][vi] = fl;
+}
+
+// compute_uhat (solver.cpp:120-143).
+__global__ void k_uhat(LevelView F, LevelView C, int has_coarse) {
+    int64_t vi = gtid();
+    if (vi >= static_cast<int64_t>(F.N + 1) * (F.N + 1)) return;
+    double u = F.v[LZB_V_U][vi];
+    if (!has_coarse) {
+        F.v[LZB_V_UHAT][vi] = u;
+        return;
+    }
+    int fx, fy, px, py;
+    vcoords(vi, F.N, fx, fy);
+    owner_patch(C, fx, fy, px, py);
+    const double* P = transfer_of(C, py * C.N + px);
+    int L = (fy - 3 * py) * 4 + (fx - 3 * px);
+    double interp = 0.0;
+    for (int k = 0; k < 4; ++k)
+        interp += P[L * 4 + k] * C.v[LZB_V_U][(py + cdy(k)) * (C.N + 1) + px + cdx(k)];
+    F.v[LZB_V_UHAT][vi] = u - interp;
+}
+
+// residual_pass cell mat-vec, as a gather (solver.cpp:149-175).
+__global__ void k_residual(LevelView F, lzb_field f) {
+    int64_t vi = gtid();
+    if (vi >= static_cast<int64_t>(F.N + 1) * (F.N + 1)) return;
+    int ix, iy;
+    vcoords(vi, F.N, ix, iy);
+    const int NV = F.N + 1;
+    double fl = F.v[LZB_V_FL][vi];
+    double r = fl, rh = fl, dg = 0.0;
+    Adj a = adjacent_cells(F, ix, iy);
+    for (int q = 0; q < a.n; ++q) {
+        double K[16];
+        element_or_baseline(f, F, a.cx[q], a.cy[q], K);
+        int row = a.row[q];
+        double au = 0.0, auh = 0.0;
+        for (int col = 0; col < 4; ++col) {
+            int64_t cv = static_cast<int64_t>(a.cy[q] + cdy(col)) * NV + a.cx[q] + cdx(col);
+            au += K[row * 4 + col] * F.v[LZB_V_U][cv];
+            auh += K[row * 4 + col] * F.v[LZB_V_UHAT][cv];
+        }
+        r -= au;
+        rh -= auh;
+        dg += K[row * 4 + row];
+    }
+    if (boundary(F.N, ix, iy)) {
+        r = 0.0;
+        rh = 0.0;
+    }
+    F.v[LZB_V_R][vi] = r;
+    F.v[LZB_V_RHAT][vi] = rh;
+    F.v[LZB_V_DIAG][vi] = dg;
+}
+
+// Restriction fl_{l-1} += P^T rhat_l over owned lattice vertices
+// (solver.cpp:177-200), gathered per coarse vertex in (cell rank, L) order.
+// mode 0: rhs restriction of rhat into fl; mode 1: adaFAC-Jac smoothed
+// residual into aux (solver.cpp:250-268).
+__global__ void k_restrict(LevelView F, LevelView C, int mode, double omega) {
+    int64_t vi = gtid();
+    if (vi >= static_cast<int64_t>(C.N + 1) * (C.N + 1)) return;
+    int IX, IY;
+    vcoords(vi, C.N, IX, IY);
+    const int NV = F.N + 1;
+    Adj a = adjacent_cells(C, IX, IY);
+    double acc_v = 0.0;
+    for (int q = 0; q < a.n; ++q) {
+        int cx = a.cx[q], cy = a.cy[q], k = a.row[q];
+        const double* P = transfer_of(C, cy * C.N + cx);
+        double acc = 0.0;
+        for (int L = 0; L < 16; ++L) {
+            int lx = L & 3, ly = L >> 2;
+            int fx = 3 * cx + lx, fy = 3 * cy + ly;
+            if (lx == 0 || lx == 3 || ly == 0 || ly == 3) {
+                int px, py;
+                owner_patch(C, fx, fy, px, py);
+                if (px != cx || py != cy) continue;
+            }
+            int64_t fi = static_cast<int64_t>(fy) * NV + fx;
+            if (mode == 0) {
+                double rh = F.v[LZB_V_RHAT][fi];
+                if (rh == 0.0) continue;
+                acc_v += P[L * 4 + k] * rh;
+            } else {
+                if (boundary(F.N, fx, fy)) continue;
+                double dg = F.v[LZB_V_DIAG][fi];
+                double sres = F.v[LZB_V_R][fi] - (dg != 0.0 ? omega / dg * F.v[LZB_V_AUX][fi] : 0.0);
+                acc += P[L * 4 + k] * sres;
+            }
+        }
+        if (mode == 1) acc_v += acc;
+    }
+    if (mode == 0) C.v[LZB_V_FL][vi] = acc_v;
+    else C.v[LZB_V_AUX][vi] = acc_v;
+}
+
+__global__ void k_norm_partial(LevelView F, double* partial) {
+    __shared__ double sh[kThreads];
+    double s = 0.0;
+    const int64_t nv = static_cast<int64_t>(F.N + 1) * (F.N + 1);
+    for (int64_t vi = gtid(); vi < nv; vi += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int ix, iy;
+        vcoords(vi, F.N, ix, iy);
+        if (boundary(F.N, ix, iy)) continue;
+        double r = F.v[LZB_V_R][vi];
+        s += r * r;
+    }
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void k_norm_final(const double* partial, int n, Result* res) {
+    __shared__ double sh[kThreads];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += partial[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) res->norm = sqrt(sh[0]);
+}
+
+// compression_stats over leaves + record bytes of refined cells (stream.cpp:268-301).
+__global__ void k_stats(LevelView L, int leaf, unsigned long long* s) {
+    __shared__ unsigned long long sh[16];
+    if (threadIdx.x < 16) sh[threadIdx.x] = 0;
+    __syncthreads();
+    int64_t c = gtid();
+    if (c < static_cast<int64_t>(L.N) * L.N) {
+        int32_t p1 = L.p1[c];
+        int p3 = p1 != LZB_P1_BOTTOM ? L.p3[c] : 0;
+        unsigned long long bytes = p1 == LZB_P1_BOTTOM ? 1ull : 1ull + p3 * (leaf ? 16ull : 144ull);
+        atomicAdd(&sh[S_TOTAL_BYTES], bytes);
+        if (leaf) {
+            atomicAdd(&sh[S_HIST + p3], 1ull);
+            atomicAdd(&sh[S_FINE_BYTES], bytes);
+            unsigned long long n = p1 != LZB_P1_BOTTOM ? static_cast<unsigned long long>(L.n[c]) : 0ull;
+            atomicAdd(&sh[S_NSUM], n);
+            atomicMax(&sh[S_MAXN], n);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 13 && sh[threadIdx.x]) {
+        if (threadIdx.x == S_MAXN) atomicMax(&s[S_MAXN], sh[S_MAXN]);
+        else atomicAdd(&s[threadIdx.x], sh[threadIdx.x]);
+    }
+}
+
+__global__ void k_count_p2(LevelView L, unsigned long long* out) {
+    int64_t c = gtid();
+    bool on = c < static_cast<int64_t>(L.N) * L.N && L.p2[c];
+    unsigned m = __ballot_sync(0xffffffffu, on);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(out, static_cast<unsigned long long>(__popc(m)));
+}
+
+// update_pass pieces (solver.cpp:212-313)
+__global__ void k_snap(LevelView L) {
+    int64_t vi = gtid();
+    if (vi >= static_cast<int64_t>(L.N + 1) * (L.N + 1)) return;
+    L.v[LZB_V_USNAP][vi] = L.v[LZB_V_U][vi];
+    L.v[LZB_V_AUX][vi] = 0.0;
+}
+__global__ void k_aux_inject(LevelView F, LevelView C) {  // adaFAC-PI: R~ = injection
+    int64_t vi = gtid();
+    if (vi >= static_cast<int64_t>(C.N + 1) * (C.N + 1)) return;
+    int ix, iy;
+    vcoords(vi, C.N, ix, iy);
+    C.v[LZB_V_AUX][vi] = F.v[LZB_V_R][static_cast<int64_t>(3 * iy) * (F.N + 1) + 3 * ix];
+}
+__global__ void k_aux_Ar(LevelView F, lzb_field f) {  // adaFAC-Jac: aux = A r on level l
+    int64_t vi = gtid();
+    if (vi >= static_cast<int64_t>(F.N + 1) * (F.N + 1)) return;
+    int ix, iy;
+    vcoords(vi, F.N, ix, iy);
+    const int NV = F.N + 1;
+    Adj a = adjacent_cells(F, ix, iy);
+    double aux = 0.0;
+    for (int q = 0; q < a.n; ++q) {
+        double K[16];
+        element_or_baseline(f, F, a.cx[q], a.cy[q], K);
+        double ar = 0.0;
+        for (int col = 0; col < 4; ++col)
+            ar += K[a.row[q] * 4 + col] *
+                  F.v[LZB_V_R][static_cast<int64_t>(a.cy[q] + cdy(col)) * NV + a.cx[q] + cdx(col)];
+        aux += ar;
+    }
+    F.v[LZB_V_AUX][vi] = aux;
+}
+// u_l -= P (omega/diag_c aux_c) on interior fine vertices (solver.cpp:271-297)
+__global__ void k_aux_sub(LevelView F, LevelView C, double omega) {
+    int64_t vi = gtid();
+    if (vi >= static_cast<int64_t>(F.N + 1) * (F.N + 1)) return;
+    int fx, fy, px, py;
+    vcoords(vi, F.N, fx, fy);
+    if (boundary(F.N, fx, fy)) return;
+    owner_patch(C, fx, fy, px, py);
+    const double* P = transfer_of(C, py * C.N + px);
+    int L = (fy - 3 * py) * 4 + (fx - 3 * px);
+    double p = 0.0;
+    for (int k = 0; k < 4; ++k) {
+        int cx = px + cdx(k), cy = py + cdy(k);
+        int64_t ci = static_cast<int64_t>(cy) * (C.N + 1) + cx;
+        double dg = C.v[LZB_V_DIAG][ci];
+        double caux = (!boundary(C.N, cx, cy) && dg != 0.0) ? omega / dg * C.v[LZB_V_AUX][ci] : 0.0;
+        p += P[L * 4 + k] * caux;
+    }
+    F.v[LZB_V_U][vi] -= p;
+}
+__global__ void k_jacobi(LevelView F, double damping) {
+    int64_t vi = gtid();
+    if (vi >= static_cast<int64_t>(F.N + 1) * (F.N + 1)) return;
+    int ix, iy;
+    vcoords(vi, F.N, ix, iy);
+    if (boundary(F.N, ix, iy)) return;
+    double dg = F.v[LZB_V_DIAG][vi];
+    if (dg != 0.0) F.v[LZB_V_U][vi] += damping / dg * F.v[LZB_V_R][vi];
+}
+// prolong_corrections (solver.cpp:315-342)
+__global__ void k_prolong(LevelView F, LevelView C) {
+    int64_t vi = gtid();
+    if (vi >= static_cast<int64_t>(F.N + 1) * (F.N + 1)) return;
+    int fx, fy, px, py;
+    vcoords(vi, F.N, fx, fy);
+    if (boundary(F.N, fx, fy)) return;
+    owner_patch(C, fx, fy, px, py);
+    double delta[4];
+    bool any = false;
+    for (int k = 0; k < 4; ++k) {
+        int64_t ci = static_cast<int64_t>(py + cdy(k)) * (C.N + 1) + px + cdx(k);
+        delta[k] = C.v[LZB_V_U][ci] - C.v[LZB_V_USNAP][ci];
+        any |= delta[k] != 0.0;
+    }
+    if (!any) return;
+    const double* P = transfer_of(C, py * C.N + px);
+    int L = (fy - 3 * py) * 4 + (fx - 3 * px);
+    double p = 0.0;
+    for (int k = 0; k < 4; ++k) p += P[L * 4 + k] * delta[k];
+    F.v[LZB_V_U][vi] += p;
+}
+// inject_solution (mesh.cpp:226-234)
+__global__ void k_inject(LevelView F, LevelView C) {
+    int64_t vi = gtid();
+    if (vi >= static_cast<int64_t>(C.N + 1) * (C.N + 1)) return;
+    int ix, iy;
+    vcoords(vi, C.N, ix, iy);
+    C.v[LZB_V_U][vi] = F.v[LZB_V_U][static_cast<int64_t>(3 * iy) * (F.N + 1) + 3 * ix];
+}
+// init_noise (problem.cpp:50-68), before the injection.
+__global__ void k_noise(LevelView L, int level, uint64_t seed, double gval) {
+    int64_t vi = gtid();
+    if (vi >= static_cast<int64_t>(L.N + 1) * (L.N + 1)) return;
+    int ix, iy;
+    vcoords(vi, L.N, ix, iy);
+    if (boundary(L.N, ix, iy)) {
+        L.v[LZB_V_U][vi] = gval;
+        return;
+    }
+    auto mix = [](uint64_t z) {
+        z += 0x9e3779b97f4a7c15ull;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    };
+    uint64_t k = mix(seed ^ mix((static_cast<uint64_t>(level) << 48) ^
+                                (static_cast<uint64_t>(static_cast<uint32_t>(ix)) << 24) ^
+                                static_cast<uint64_t>(static_cast<uint32_t>(iy))));
+    L.v[LZB_V_U][vi] = (4.0 / 3.0) * static_cast<double>(k >> 11) * 0x1.0p-53;
+}
+
+// ------------------------------------------------------- stream image (save)
+// Pre-order slot of a cell on a regular tree of depth D: slot(child ci of a
+// level-(k-1) cell with slot s) = s + 1 + ci * S_k, S_k = sum_{j<=D-k} 9^j
+// (mesh.cpp:152-167).
+__device__ inline int64_t preorder_slot(int l, int cx, int cy, const int64_t* subtree) {
+    int64_t slot = 0;
+    int64_t p = 1;
+    for (int k = 1; k < l; ++k) p *= 3;
+    for (int k = 1; k <= l; ++k) {
+        int dx = static_cast<int>((cx / p) % 3), dy = static_cast<int>((cy / p) % 3);
+        slot += 1 + (dx * 3 + dy) * subtree[k];
+        p /= 3;
+    }
+    return slot;
+}
+
+
+struct SlotTable {
+    int64_t subtree[16];
+};
+
+__global__ void k_record_sizes(LevelView L, int level, int leaf, SlotTable st, int64_t* sizes) {
+    int64_t c = gtid();
+    if (c >= static_cast<int64_t>(L.N) * L.N) return;
+    int cx = static_cast<int>(c % L.N), cy = static_cast<int>(c / L.N);
+    int32_t p1 = L.p1[c];
+    int p3 = p1 != LZB_P1_BOTTOM ? L.p3[c] : 0;
+    int64_t bytes = (p1 == LZB_P1_BOTTOM || p3 == 0) ? 1 : 1 + p3 * (leaf ? 16 : 144);
+    sizes[preorder_slot(level, cx, cy, st.subtree)] = bytes;
+}
+
+// CellStream::save record (stream.cpp:315-337): header byte, then the
+// surplus against the n = 1 baseline (and P-hat, R-hat copy) at p3 bytes.
+__global__ void k_pack(LevelView L, lzb_field f, int level, int leaf, SlotTable st,
+                       const int64_t* __restrict__ offsets, uint8_t* __restrict__ out, int* err) {
+    int64_t c = gtid();
+    if (c >= static_cast<int64_t>(L.N) * L.N) return;
+    int cx = static_cast<int>(c % L.N), cy = static_cast<int>(c / L.N);
+    int64_t off = 12 + offsets[preorder_slot(level, cx, cy, st.subtree)];
+    int32_t p1 = L.p1[c];
+    int p3 = p1 != LZB_P1_BOTTOM ? L.p3[c] : 0;
+    out[off] = pack_header(p1, L.p2[c], p3);
+    if (p1 == LZB_P1_BOTTOM || p3 == 0) return;
+    uint8_t* cur = out + off + 1;
+    double e = centre_eps(f, L, cx, cy);
+    const double* op = L.op + 16 * c;
+    bool ok = true;
+    for (int k = 0; k < 16; ++k, cur += p3) ok &= encode_value(op[k] - baseline_entry(k, e), p3, cur);
+    if (!leaf) {
+        const double* P = transfer_of(L, static_cast<int>(c));
+        for (int rep = 0; rep < 2; ++rep)
+            for (int k = 0; k < 64; ++k, cur += p3) ok &= encode_value(P[k] - c_geo[k], p3, cur);
+    }
+    if (!ok) atomicExch(err, 1);
+}
+
+// CellStream::load record (stream.cpp:355-392); offsets from the host parse.
+__global__ void k_unpack(LevelView L, lzb_field f, int level, int leaf, SlotTable st,
+                         const int64_t* __restrict__ offsets, const uint8_t* __restrict__ in,
+                         double delta_max, uint32_t cycle, unsigned long long* stats, int* err) {
+    int64_t c = gtid();
+    if (c >= static_cast<int64_t>(L.N) * L.N) return;
+    int cx = static_cast<int>(c % L.N), cy = static_cast<int>(c / L.N);
+    const uint8_t* rec = in + offsets[preorder_slot(level, cx, cy, st.subtree)];
+    uint8_t h = rec[0];
+    int cls = (h >> 6) & 3, p2 = (h & 0x20) != 0, p3 = h & 0x0f;
+    L.p2[c] = static_cast<uint8_t>(p2);
+    if (cls == 0) {
+        L.p1[c] = LZB_P1_BOTTOM;
+        return;
+    }
+    double e = centre_eps(f, L, cx, cy);
+    double m[16], P[64];
+    for (int k = 0; k < 16; ++k) m[k] = baseline_entry(k, e);
+    for (int k = 0; k < 64; ++k) P[k] = c_geo[k];
+    if (p3 != 0) {
+        const uint8_t* cur = rec + 1;
+        for (int k = 0; k < 16; ++k, cur += p3) m[k] += decode_value(cur, p3);
+        if (!leaf)
+            for (int k = 0; k < 64; ++k, cur += p3) P[k] += decode_value(cur, p3);
+    }
+    if (leaf) {
+        if (!publish_leaf(L, static_cast<int>(c), m, 1, e, delta_max, cycle, stats)) atomicExch(err, 1);
+    } else {
+        // publish_coarse (stream.cpp:134-184)
+        double joint[80];
+        for (int k = 0; k < 16; ++k) joint[k] = m[k] - baseline_entry(k, e);
+        for (int k = 0; k < 64; ++k) joint[16 + k] = P[k] - c_geo[k];
+        int q3 = choose_precision(joint, 80, delta_max);
+        if (q3 < 0) {
+            atomicExch(err, 1);
+            return;
+        }
+        double delta = 0.0;
+        for (int k = 0; k < 80; ++k) {
+            double rt;
+            roundtrip(joint[k], q3, rt);
+            double d = fabs(rt - joint[k]);
+            delta = delta < d ? d : delta;
+            if (k < 16) m[k] = baseline_entry(k, e) + rt;
+            else P[k - 16] = c_geo[k - 16] + rt;
+        }
+        double* op = L.op + 16 * c;
+        bool same = L.p1[c] == LZB_P1_TOP && L.has_P[c];
+        if (same) {
+            const double* cur = L.P ? L.P + 64 * c : c_geo;
+            for (int k = 0; k < 16; ++k) same = same && m[k] == op[k];
+            for (int k = 0; k < 64; ++k) same = same && P[k] == cur[k];
+        }
+        if (!same) {
+            atomic_max_double_bits(&stats[S_MAXDELTA], delta);
+            for (int k = 0; k < 16; ++k) op[k] = m[k];
+            if (L.P)
+                for (int k = 0; k < 64; ++k) L.P[64 * c + k] = P[k];
+            L.has_P[c] = 1;
+            L.n[c] = 1;
+            L.epoch[c] = cycle;
+            L.p3[c] = static_cast<int8_t>(q3);
+        }
+    }
+    L.p1[c] = cls == 2 ? LZB_P1_TOP : 1;
+    L.p3[c] = static_cast<int8_t>(p3);
+}
+
+// Single-cell protocol ops for the per-cell compatibility API.
+__global__ void k_publish_one(LevelView F, lzb_field f, int c, const double* m, int n, int32_t p1,
+                              double delta_max, uint32_t cycle, unsigned long long* stats, int* err) {
+    if (gtid() != 0) return;
+    double e = centre_eps(f, F, c % F.N, c / F.N);
+    if (!publish_leaf(F, c, m, n, e, delta_max, cycle, stats)) atomicExch(err, 1);
+    F.p1[c] = p1;
+}
+
+__global__ void k_step_one(LevelView F, lzb_field f, int c, int schedule, int n_max, double term_c,
+                           double delta_max, uint32_t cycle, int fast, unsigned long long* stats,
+                           int* err) {
+    if (gtid() != 0) return;
+    int cx = c % F.N, cy = c / F.N;
+    int32_t p1 = F.p1[c];
+    if (p1 == LZB_P1_TOP) return;
+    double e = centre_eps(f, F, cx, cy);
+    if (p1 == LZB_P1_BOTTOM) {
+        double m[16];
+        for (int k = 0; k < 16; ++k) m[k] = baseline_entry(k, e);
+        if (!publish_leaf(F, c, m, 1, e, delta_max, cycle, stats)) atomicExch(err, 1);
+        F.p1[c] = 1;
+        return;
+    }
+    int n = p1;
+    if (n_max > 0 && n >= n_max) {
+        F.p1[c] = LZB_P1_TOP;
+        return;
+    }
+    int nn = schedule == LZB_SCHEDULE_DOUBLE ? 2 * n : n + 1;
+    if (n_max > 0 && nn > n_max) nn = n_max;
+    double fresh[16];
+    integrate_cell(f, cx * F.h, cy * F.h, F.h, nn, fast, fresh);
+    const double* old = F.op + 16 * static_cast<int64_t>(c);
+    double denom = 0.0, dmax = 0.0;
+    for (int k = 0; k < 16; ++k) {
+        double a = fabs(old[k]);
+        denom = denom < a ? a : denom;
+        double d = fabs(fresh[k] - old[k]);
+        dmax = dmax < d ? d : dmax;
+    }
+    double ratio = 0.0;
+    if (denom == 0.0) atomicAdd(&stats[S_ZERO_NORM], 1ull);
+    else ratio = dmax / denom;
+    if (ratio < term_c) {
+        F.p1[c] = LZB_P1_TOP;
+        return;
+    }
+    if (!publish_leaf(F, c, fresh, nn, e, delta_max, cycle, stats)) atomicExch(err, 1);
+    F.p1[c] = nn;
+}
+
+__global__ void k_clear_p2(LevelView F, const int32_t* list, int count) {
+    int64_t t = gtid();
+    if (t < count) F.p2[list[t]] = 0;
+}
+
+__global__ void k_reset_stats(Result* r) {
+    if (threadIdx.x < 13) r->s[threadIdx.x] = 0;
+    if (threadIdx.x == 0) r->norm = 0.0;
+}
+
+template <int KIND>
+void launch_step(bool fast, unsigned grid, cudaStream_t s, const LevelView& F, const lzb_field& f,
+                 const int32_t* list, const int32_t* snap, int count, int n, int nn, int cap,
+                 const double* tx, const double* ty, double term_c, double dmax, uint32_t cycle,
+                 unsigned long long* stats, int* err) {
+    if (fast)
+        LZB_LAUNCH((k_step<KIND, true>), grid, 128, 0, s, F, f, list, snap, count, n, nn, cap, tx, ty,
+                   term_c, dmax, cycle, 0, stats, err);
+    else
+        LZB_LAUNCH((k_step<KIND, false>), grid, 128, 0, s, F, f, list, snap, count, n, nn, cap, tx,
+                   ty, term_c, dmax, cycle, 0, stats, err);
+}
+
+template <int KIND>
+void launch_fixed(bool fast, unsigned grid, cudaStream_t s, const LevelView& F, const lzb_field& f,
+                  int n, const double* tx, const double* ty, double dmax, uint32_t cycle,
+                  unsigned long long* stats, int* err) {
+    if (fast)
+        LZB_LAUNCH((k_fixed<KIND, true>), grid, 128, 0, s, F, f, n, tx, ty, dmax, cycle, stats, err);
+    else
+        LZB_LAUNCH((k_fixed<KIND, false>), grid, 128, 0, s, F, f, n, tx, ty, dmax, cycle, stats, err);
+}
+
+}  // namespace
+
+// ==================================================================== host
+struct Level {
+    int N = 1;
+    int64_t nc = 1, nv = 4;
+    double h = 1.0, pow3l = 1.0;
+    DevBuf<int32_t> rx, ry;
+    DevBuf<double> v[LZB_V_NFIELDS];
+    DevBuf<double> op, P;
+    DevBuf<int32_t> p1, n;
+    DevBuf<uint8_t> p2, has_P;
+    DevBuf<int8_t> p3;
+    DevBuf<uint32_t> epoch;
+    LevelView view(int depth) const {
+        LevelView L{};
+        L.N = N;
+        L.depth_of_grid = depth;
+        L.h = h;
+        L.pow3l = pow3l;
+        L.rx = rx.p;
+        L.ry = ry.p;
+        for (int f = 0; f < LZB_V_NFIELDS; ++f) L.v[f] = v[f].p;
+        L.op = op.p;
+        L.P = P.p;
+        L.p1 = p1.p;
+        L.p2 = p2.p;
+        L.p3 = p3.p;
+        L.n = n.p;
+        L.epoch = epoch.p;
+        L.has_P = has_P.p;
+        return L;
+    }
+};
+
+class Grid {
+public:
+    Grid(lzb_ctx* ctx, const lzb_grid_desc& d) : ctx_(ctx), d_(d), D_(d.depth) {
+        if (d.dim != 2) throw Error(LZB_ERR_INVALID, "only dim = 2 is implemented in this round");
+        if (d.depth < 1) throw Error(LZB_ERR_INVALID, "mesh depth must be >= 1");
+        if (d.depth > 9) throw Error(LZB_ERR_RESOURCE, "initial mesh depth exceeds the cell limit");
+        if (d.field.kind == LZB_FIELD_CHECKER && (d.field.blocks < 1 || d.field.blocks > 8))
+            throw Error(LZB_ERR_INVALID, "checkerboard blocks must be in 1..8");
+        LZB_CUDA(cudaSetDevice(ctx->device));
+        s_ = ctx->solve;
+        L_.resize(D_ + 1);
+        std::vector<int32_t> prx{0}, pry{0};
+        for (int l = 0; l <= D_; ++l) {
+            Level& L = L_[l];
+            L.N = 1;
+            for (int i = 0; i < l; ++i) L.N *= 3;
+            L.nc = static_cast<int64_t>(L.N) * L.N;
+            L.nv = static_cast<int64_t>(L.N + 1) * (L.N + 1);
+            L.h = std::pow(1.0 / 3, l);
+            L.pow3l = std::pow(3.0, l);
+            std::vector<int32_t> rx(L.N), ry(L.N);
+            for (int c = 0; c < L.N; ++c) {
+                rx[c] = l == 0 ? 0 : 9 * prx[c / 3] + 3 * (c % 3);
+                ry[c] = l == 0 ? 0 : 9 * pry[c / 3] + (c % 3);
+            }
+            L.rx.alloc(L.N);
+            L.ry.alloc(L.N);
+            LZB_CUDA(cudaMemcpy(L.rx.p, rx.data(), L.N * sizeof(int32_t), cudaMemcpyHostToDevice));
+            LZB_CUDA(cudaMemcpy(L.ry.p, ry.data(), L.N * sizeof(int32_t), cudaMemcpyHostToDevice));
+            prx.swap(rx);
+            pry.swap(ry);
+            for (int f = 0; f < LZB_V_NFIELDS; ++f) {
+                L.v[f].alloc(L.nv);
+                LZB_CUDA(cudaMemsetAsync(L.v[f].p, 0, L.v[f].bytes(), s_));
+            }
+            L.op.alloc(16 * L.nc);
+            L.p1.alloc(L.nc);
+            L.n.alloc(L.nc);
+            L.p2.alloc(L.nc);
+            L.p3.alloc(L.nc);
+            L.epoch.alloc(L.nc);
+            L.has_P.alloc(L.nc);
+            LZB_CUDA(cudaMemsetAsync(L.op.p, 0, L.op.bytes(), s_));
+            LZB_CUDA(cudaMemsetAsync(L.p1.p, 0, L.p1.bytes(), s_));
+            LZB_CUDA(cudaMemsetAsync(L.n.p, 0, L.n.bytes(), s_));
+            LZB_CUDA(cudaMemsetAsync(L.p2.p, 0, L.p2.bytes(), s_));
+            LZB_CUDA(cudaMemsetAsync(L.p3.p, 0, L.p3.bytes(), s_));
+            LZB_CUDA(cudaMemsetAsync(L.epoch.p, 0, L.epoch.bytes(), s_));
+            LZB_CUDA(cudaMemsetAsync(L.has_P.p, 0, L.has_P.bytes(), s_));
+            if (l < D_ && d.transfer == LZB_BOXMG) {
+                L.P.alloc(64 * L.nc);
+                LZB_CUDA(cudaMemsetAsync(L.P.p, 0, L.P.bytes(), s_));
+            }
+        }
+        leaves_ = L_[D_].nc;
+        list_.alloc(leaves_);
+        snap_.alloc(leaves_);
+        counter_.alloc(1);
+        hist_.alloc(kNHist);
+        partial_.alloc(kNormBlocks);
+        res_.alloc(1);
+        LZB_CUDA(cudaMemsetAsync(res_.p, 0, sizeof(Result), s_));
+        if (d.throttle) keys_.alloc(leaves_);
+        LZB_CUDA(cudaMallocHost(&hres_, sizeof(Result)));
+        LZB_CUDA(cudaMallocHost(&hhist_, kNHist * sizeof(unsigned) + sizeof(int)));
+        // subtree sizes for pre-order slots
+        for (int k = 0; k <= D_; ++k) {
+            int64_t s = 0, p = 1;
+            for (int j = 0; j <= D_ - k; ++j, p *= 9) s += p;
+            slots_.subtree[k] = s;
+        }
+        for (int l = 0; l <= D_; ++l) total_cells_ += L_[l].nc;
+        for (int l = 0; l <= D_; ++l) total_vertices_ += L_[l].nv;
+        LZB_CUDA(cudaStreamSynchronize(s_));
+    }
+
+    ~Grid() {
+        cudaStreamSynchronize(s_);
+        if (hres_) cudaFreeHost(hres_);
+        if (hhist_) cudaFreeHost(hhist_);
+    }
+
+    LevelView V(int l) const { return L_[l].view(D_); }
+    const lzb_grid_desc& desc() const { return d_; }
+    int depth() const { return D_; }
+    uint32_t cycle() const { return cycle_; }
+
+    void init_noise(uint64_t seed) {
+        for (int l = 0; l <= D_; ++l)
+            LZB_LAUNCH(k_noise, blocks_for(L_[l].nv, kThreads), kThreads, 0, s_, V(l), l, seed,
+                       d_.boundary_value);
+        inject();
+        sync_check();
+    }
+
+    // ------------------------------------------------------ assembly protocol
+    int next_n(int n) const {
+        int nn = d_.schedule == LZB_SCHEDULE_DOUBLE ? 2 * n : n + 1;
+        if (d_.n_max > 0 && nn > d_.n_max) nn = d_.n_max;
+        return nn;
+    }
+
+    void ensure_tables(int nn) {
+        size_t need = static_cast<size_t>(L_[D_].N) * nn * kTab;
+        if (tx_.n < need) {
+            LZB_CUDA(cudaStreamSynchronize(s_));
+            tx_.alloc(need);
+            ty_.alloc(need);
+        }
+        build_axis_tables(d_.field, L_[D_].N, L_[D_].h, nn, tx_.p, ty_.p, s_);
+    }
+
+    // One batched round of adaptive steps over the selected leaves; returns
+    // the number of selected leaves. selector: 0 unconverged, 1 tasks, 2 bottom.
+    int64_t round(int selector, bool complete_tasks, long long key_limit = -1) {
+        LevelView F = V(D_);
+        LZB_CUDA(cudaMemsetAsync(counter_.p, 0, sizeof(int), s_));
+        LZB_CUDA(cudaMemsetAsync(hist_.p, 0, kNHist * sizeof(unsigned), s_));
+        LZB_LAUNCH(k_compact, blocks_for(leaves_, kThreads), kThreads, 0, s_, F, selector, list_.p,
+                   snap_.p, counter_.p, hist_.p, key_limit >= 0 ? keys_.p : nullptr, key_limit);
+        LZB_CUDA(cudaMemcpyAsync(hhist_, hist_.p, kNHist * sizeof(unsigned), cudaMemcpyDeviceToHost, s_));
+        LZB_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(hhist_) + kNHist * sizeof(unsigned),
+                                 counter_.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
+        sync_check();
+        int count = *reinterpret_cast<int*>(reinterpret_cast<char*>(hhist_) + kNHist * sizeof(unsigned));
+        if (count == 0) return 0;
+        if (hhist_[kNHist - 1] && selector != 1)
+            throw Error(LZB_ERR_RESOURCE, "sub-sample count beyond 4095 per axis");
+        unsigned grid = blocks_for(count, 128);
+        unsigned long long* stats = res_.p->s;
+        if (hhist_[0])
+            LZB_LAUNCH(k_bottom, blocks_for(count, kThreads), kThreads, 0, s_, F, d_.field, list_.p,
+                       snap_.p, count, d_.delta_max, cycle_, 0, stats, ctx_->err.p);
+        for (int n = 1; n < kNHist - 1; ++n) {
+            if (!hhist_[n]) continue;
+            bool cap = d_.n_max > 0 && n >= d_.n_max;
+            int nn = next_n(n);
+            if (!cap) ensure_tables(nn);
+            bool fast = d_.integration == LZB_INTEGRATE_FAST;
+            const double *tx = tx_.p, *ty = ty_.p;
+            switch (d_.field.kind) {
+                case LZB_FIELD_THETA: launch_step<LZB_FIELD_THETA>(fast, grid, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, tx, ty, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+                case LZB_FIELD_QUADRANT: launch_step<LZB_FIELD_QUADRANT>(fast, grid, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, tx, ty, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+                case LZB_FIELD_CHECKER: launch_step<LZB_FIELD_CHECKER>(fast, grid, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, tx, ty, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+                case LZB_FIELD_SINUSOID: launch_step<LZB_FIELD_SINUSOID>(fast, grid, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, tx, ty, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+                default: launch_step<LZB_FIELD_CONSTANT>(fast, grid, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, tx, ty, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+            }
+        }
+        if (complete_tasks)
+            LZB_LAUNCH(k_clear_p2, blocks_for(count, kThreads), kThreads, 0, s_, F, list_.p, count);
+        return count;
+    }
+
+    void eager_setup() {  // assembly.cpp:111-118, batched by rounds
+        while (round(0, false) > 0) {
+        }
+    }
+
+    void assemble_fixed(int n) {
+        if (n < 1) throw Error(LZB_ERR_INVALID, "n must be >= 1");
+        ensure_tables(n);
+        LevelView F = V(D_);
+        unsigned grid = blocks_for(leaves_, 128);
+        bool fast = d_.integration == LZB_INTEGRATE_FAST;
+        unsigned long long* stats = res_.p->s;
+        switch (d_.field.kind) {
+            case LZB_FIELD_THETA: launch_fixed<LZB_FIELD_THETA>(fast, grid, s_, F, d_.field, n, tx_.p, ty_.p, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+            case LZB_FIELD_QUADRANT: launch_fixed<LZB_FIELD_QUADRANT>(fast, grid, s_, F, d_.field, n, tx_.p, ty_.p, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+            case LZB_FIELD_CHECKER: launch_fixed<LZB_FIELD_CHECKER>(fast, grid, s_, F, d_.field, n, tx_.p, ty_.p, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+            case LZB_FIELD_SINUSOID: launch_fixed<LZB_FIELD_SINUSOID>(fast, grid, s_, F, d_.field, n, tx_.p, ty_.p, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+            default: launch_fixed<LZB_FIELD_CONSTANT>(fast, grid, s_, F, d_.field, n, tx_.p, ty_.p, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+        }
+    }
+
+    void coarse_pass() {  // pre-order semantics: coarse levels first, each reads l+1
+        for (int l = 0; l < D_; ++l)
+            LZB_LAUNCH(k_coarse, blocks_for(L_[l].nc, 64), 64, 0, s_, V(l), V(l + 1), d_.field,
+                       d_.transfer == LZB_BOXMG ? 1 : 0, d_.delta_max, cycle_, res_.p->s, ctx_->err.p);
+    }
+
+    void pool_begin_cycle() {  // TaskPool::begin_cycle, workers = 1 (scheduler.cpp:88-111)
+        if (d_.mode != LZB_ANARCHIC || pending_ == 0) return;
+        long long limit = -1;
+        if (d_.throttle && static_cast<uint64_t>(pending_) > d_.throttle) {
+            // FIFO: only the `throttle` oldest spawns run this cycle
+            std::vector<long long> k(leaves_);
+            std::vector<uint8_t> p2(leaves_);
+            LZB_CUDA(cudaMemcpyAsync(k.data(), keys_.p, leaves_ * sizeof(long long), cudaMemcpyDeviceToHost, s_));
+            LZB_CUDA(cudaMemcpyAsync(p2.data(), L_[D_].p2.p, leaves_, cudaMemcpyDeviceToHost, s_));
+            sync_check();
+            std::vector<long long> pend;
+            for (int64_t c = 0; c < leaves_; ++c)
+                if (p2[c]) pend.push_back(k[c]);
+            std::nth_element(pend.begin(), pend.begin() + (d_.throttle - 1), pend.end());
+            limit = pend[d_.throttle - 1];
+        }
+        round(1, true, limit);
+    }
+
+    void assembly_pass() {  // solver.cpp:79-97
+        coarse_pass();
+        switch (d_.mode) {
+            case LZB_EAGER:
+            case LZB_LAZY:
+                while (round(0, false) > 0) {
+                }
+                break;
+            case LZB_ADAPTIVE: round(0, false); break;
+            case LZB_ANARCHIC:
+                round(2, false);  // the initial stencil computation is not deferred
+                LZB_LAUNCH(k_spawn, blocks_for(leaves_, kThreads), kThreads, 0, s_, V(D_), cycle_,
+                           static_cast<long long>(leaves_), keys_.p);
+                break;
+        }
+    }
+
+    void residual_launches() {  // solver.cpp:145-210
+        LevelView F = V(D_);
+        bool rhs_on = d_.rhs.kind == LZB_RHS_SINPROD || d_.rhs.value != 0.0;
+        if (rhs_on)
+            LZB_LAUNCH(k_init_rhs, blocks_for(L_[D_].nv, kThreads), kThreads, 0, s_, F, d_.rhs,
+                       L_[D_].h * L_[D_].h / 4.0);
+        else
+            LZB_CUDA(cudaMemsetAsync(L_[D_].v[LZB_V_FL].p, 0, L_[D_].v[LZB_V_FL].bytes(), s_));
+        for (int l = D_; l >= 0; --l) {
+            unsigned g = blocks_for(L_[l].nv, kThreads);
+            LZB_LAUNCH(k_uhat, g, kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
+            LZB_LAUNCH(k_residual, g, kThreads, 0, s_, V(l), d_.field);
+            if (l > 0)
+                LZB_LAUNCH(k_restrict, blocks_for(L_[l - 1].nv, kThreads), kThreads, 0, s_, V(l),
+                           V(l - 1), 0, 0.0);
+        }
+        LZB_LAUNCH(k_norm_partial, kNormBlocks, kThreads, 0, s_, F, partial_.p);
+        LZB_LAUNCH(k_norm_final, 1, kThreads, 0, s_, partial_.p, kNormBlocks, res_.p);
+    }
+
+    void stats_launches() {
+        LZB_LAUNCH(k_reset_stats, 1, 32, 0, s_, res_.p);
+        for (int l = 0; l <= D_; ++l)
+            LZB_LAUNCH(k_stats, blocks_for(L_[l].nc, kThreads), kThreads, 0, s_, V(l), l == D_ ? 1 : 0,
+                       res_.p->s);
+    }
+
+    void update_launches() {  // solver.cpp:212-313
+        const double omega = d_.omega;
+        for (int l = 0; l <= D_; ++l)
+            LZB_LAUNCH(k_snap, blocks_for(L_[l].nv, kThreads), kThreads, 0, s_, V(l));
+        for (int l = D_; l >= 0; --l) {
+            bool aux = d_.variant != LZB_ADDITIVE && l > 0;
+            unsigned g = blocks_for(L_[l].nv, kThreads);
+            if (aux) {
+                unsigned gc = blocks_for(L_[l - 1].nv, kThreads);
+                if (d_.variant == LZB_ADAFAC_PI) {
+                    LZB_LAUNCH(k_aux_inject, gc, kThreads, 0, s_, V(l), V(l - 1));
+                } else {
+                    LZB_LAUNCH(k_aux_Ar, g, kThreads, 0, s_, V(l), d_.field);
+                    LZB_LAUNCH(k_restrict, gc, kThreads, 0, s_, V(l), V(l - 1), 1, omega);
+                }
+                LZB_LAUNCH(k_aux_sub, g, kThreads, 0, s_, V(l), V(l - 1), omega);
+            }
+            double damping = d_.variant == LZB_ADDITIVE ? std::pow(omega, D_ - l + 1) : omega;
+            LZB_LAUNCH(k_jacobi, g, kThreads, 0, s_, V(l), damping);
+        }
+    }
+
+    void prolong_launches() {
+        for (int l = 1; l <= D_; ++l)
+            LZB_LAUNCH(k_prolong, blocks_for(L_[l].nv, kThreads), kThreads, 0, s_, V(l), V(l - 1));
+    }
+
+    void inject() {
+        for (int l = D_; l >= 1; --l)
+            LZB_LAUNCH(k_inject, blocks_for(L_[l - 1].nv, kThreads), kThreads, 0, s_, V(l), V(l - 1));
+    }
+
+    void fetch_result() {
+        LZB_CUDA(cudaMemcpyAsync(hres_, res_.p, sizeof(Result), cudaMemcpyDeviceToHost, s_));
+        sync_check();
+    }
+
+    void sync_check() {
+        LZB_CUDA(cudaStreamSynchronize(s_));
+        int flag = 0;
+        LZB_CUDA(cudaMemcpy(&flag, ctx_->err.p, sizeof(int), cudaMemcpyDeviceToHost));
+        if (flag) {
+            LZB_CUDA(cudaMemset(ctx_->err.p, 0, sizeof(int)));
+            throw Error(LZB_ERR_PROTOCOL, "cannot encode non-finite operator entry");
+        }
+    }
+
+    int64_t count_pending() {
+        LZB_CUDA(cudaMemsetAsync(counter_.p, 0, sizeof(int), s_));
+        // reuse hist_ slot 0 as a 64-bit counter area
+        LZB_CUDA(cudaMemsetAsync(hist_.p, 0, 2 * sizeof(unsigned), s_));
+        LZB_LAUNCH(k_count_p2, blocks_for(leaves_, kThreads), kThreads, 0, s_, V(D_),
+                   reinterpret_cast<unsigned long long*>(hist_.p));
+        unsigned long long v = 0;
+        LZB_CUDA(cudaMemcpyAsync(&v, hist_.p, sizeof v, cudaMemcpyDeviceToHost, s_));
+        sync_check();
+        return static_cast<int64_t>(v);
+    }
+
+    void fill_stats(const Result& r, lzb_compression_stats& st) const {
+        std::memset(&st, 0, sizeof st);
+        st.fine_cells = static_cast<uint64_t>(leaves_);
+        st.fine_stored_bytes = r.s[S_FINE_BYTES];
+        st.fine_uncompressed_bytes = 128ull * leaves_;
+        double ratio_sum = 0.0;
+        for (int p = 0; p <= 8; ++p) {
+            st.p3_histogram[p] = r.s[S_HIST + p];
+            ratio_sum += static_cast<double>(r.s[S_HIST + p]) * (128.0 / (p == 0 ? 1.0 : 1.0 + 16.0 * p));
+        }
+        st.max_n = static_cast<int32_t>(r.s[S_MAXN]);
+        if (st.fine_cells) {
+            st.fine_factor_totals = static_cast<double>(st.fine_uncompressed_bytes) /
+                                    static_cast<double>(st.fine_stored_bytes);
+            st.fine_factor_mean = ratio_sum / static_cast<double>(st.fine_cells);
+            long double nsum = static_cast<long double>(r.s[S_NSUM]);
+            st.avg_n = static_cast<double>(nsum / st.fine_cells);
+        }
+        st.total_stored_bytes = r.s[S_TOTAL_BYTES];
+        uint64_t unc = 0;
+        for (int l = 0; l <= D_; ++l) unc += 8ull * (l == D_ ? 16 : 144) * L_[l].nc;
+        st.total_uncompressed_bytes = unc;
+        if (st.total_stored_bytes)
+            st.total_factor = static_cast<double>(unc) / static_cast<double>(st.total_stored_bytes);
+        double md;
+        std::memcpy(&md, &r.s[S_MAXDELTA], sizeof md);
+        st.max_delta = md;
+        st.max_sample_count = static_cast<int32_t>(r.s[S_MAXSAMPLES]);
+    }
+
+    lzb_compression_stats stats() {
+        stats_launches();
+        fetch_result();
+        lzb_compression_stats st;
+        fill_stats(*hres_, st);
+        return st;
+    }
+
+    int check_termination() const {  // solver.cpp:8-16
+        if (history_.empty()) return LZB_CONTINUE;
+        double normalized = history_.back() / history_.front();
+        if (normalized <= d_.target) return LZB_CONVERGED;
+        if (normalized >= d_.divergence) return LZB_DIVERGED;
+        if (static_cast<int>(cycle_) >= d_.max_cycles) return LZB_TIMEOUT;
+        return LZB_CONTINUE;
+    }
+
+    lzb_cycle_report step() {  // solver.cpp:349-400
+        auto t0 = std::chrono::steady_clock::now();
+        lzb_cycle_report rep;
+        std::memset(&rep, 0, sizeof rep);
+        ++cycle_;
+        pool_begin_cycle();
+        rep.cycle = static_cast<int32_t>(cycle_);
+        assembly_pass();
+        residual_launches();
+        stats_launches();
+        fetch_result();
+        Result r = *hres_;
+        rep.residual = r.norm;
+        if (first_residual_ < 0.0) first_residual_ = rep.residual > 0.0 ? rep.residual : 1.0;
+        rep.normalized = rep.residual / first_residual_;
+        history_.push_back(rep.residual);
+        rep.status = check_termination();
+        if (rep.status == LZB_CONTINUE || rep.status == LZB_TIMEOUT) {
+            update_launches();
+            prolong_launches();
+            inject();
+            uint64_t Nf = static_cast<uint64_t>(L_[D_].N);
+            rep.dof_updates = (Nf - 1) * (Nf - 1);
+            for (int l = 0; l < D_; ++l) {
+                uint64_t N = static_cast<uint64_t>(L_[l].N);
+                rep.coarse_updates += N > 1 ? (N - 1) * (N - 1) : 0;
+            }
+        }
+        dof_total_ += rep.dof_updates;
+        rep.dof_updates_total = dof_total_;
+        pending_ = d_.mode == LZB_ANARCHIC ? count_pending() : 0;
+        rep.pending_tasks = static_cast<uint64_t>(pending_);
+        lzb_compression_stats st;
+        fill_stats(r, st);
+        rep.max_n = st.max_n;
+        rep.avg_n = st.avg_n;
+        rep.max_samples = st.max_sample_count;
+        rep.factor_totals = st.fine_factor_totals;
+        rep.factor_mean = st.fine_factor_mean;
+        rep.levels = D_ + 1;
+        rep.cells = static_cast<uint64_t>(total_cells_);
+        for (int l = 0; l <= D_ && l < 32; ++l) rep.enabled_mask |= 1u << l;
+        uint64_t Nf = static_cast<uint64_t>(L_[D_].N);
+        rep.dofs_fine_interior = (Nf - 1) * (Nf - 1);
+        rep.grid_points_total = static_cast<uint64_t>(total_vertices_);
+        LZB_CUDA(cudaStreamSynchronize(s_));
+        rep.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return rep;
+    }
+
+    std::vector<lzb_cycle_report> run() {  // solver.cpp:421-444 (no AMR on regular grids)
+        std::vector<lzb_cycle_report> out;
+        if (d_.mode == LZB_EAGER) eager_setup();
+        for (;;) {
+            out.push_back(step());
+            if (out.back().status != LZB_CONTINUE) break;
+        }
+        return out;
+    }
+
+    double pass(int which) {
+        switch (which) {
+            case 0: assembly_pass(); sync_check(); return 0.0;
+            case 1: residual_launches(); fetch_result(); return hres_->norm;
+            case 2: update_launches(); sync_check(); return 0.0;
+            case 3: prolong_launches(); sync_check(); return 0.0;
+            case 4: inject(); sync_check(); return 0.0;
+            case 5: return 0.0;
+            case 6: pool_begin_cycle(); sync_check(); pending_ = count_pending(); return 0.0;
+            default: throw Error(LZB_ERR_INVALID, "unknown pass");
+        }
+    }
+
+    void vertices(int level, int field, double* buf, bool write) {
+        check_level(level);
+        if (field < 0 || field >= LZB_V_NFIELDS) throw Error(LZB_ERR_INVALID, "bad vertex field");
+        auto& b = L_[level].v[field];
+        if (write) LZB_CUDA(cudaMemcpyAsync(b.p, buf, b.bytes(), cudaMemcpyHostToDevice, s_));
+        else LZB_CUDA(cudaMemcpyAsync(buf, b.p, b.bytes(), cudaMemcpyDeviceToHost, s_));
+        sync_check();
+    }
+
+    void cells(int level, double* ops, int32_t* p1, int32_t* n, int32_t* p3, uint32_t* epoch) {
+        check_level(level);
+        const Level& L = L_[level];
+        std::vector<int32_t> hp1(L.nc), hn(L.nc);
+        std::vector<int8_t> hp3(L.nc);
+        std::vector<uint32_t> hep(L.nc);
+        std::vector<double> hop(16 * L.nc);
+        LZB_CUDA(cudaMemcpyAsync(hp1.data(), L.p1.p, L.p1.bytes(), cudaMemcpyDeviceToHost, s_));
+        LZB_CUDA(cudaMemcpyAsync(hn.data(), L.n.p, L.n.bytes(), cudaMemcpyDeviceToHost, s_));
+        LZB_CUDA(cudaMemcpyAsync(hp3.data(), L.p3.p, L.p3.bytes(), cudaMemcpyDeviceToHost, s_));
+        LZB_CUDA(cudaMemcpyAsync(hep.data(), L.epoch.p, L.epoch.bytes(), cudaMemcpyDeviceToHost, s_));
+        LZB_CUDA(cudaMemcpyAsync(hop.data(), L.op.p, L.op.bytes(), cudaMemcpyDeviceToHost, s_));
+        sync_check();
+        double kunit[16];
+        host_kunit(kunit);
+        for (int64_t c = 0; c < L.nc; ++c) {
+            bool valid = hp1[c] != LZB_P1_BOTTOM;
+            if (p1) p1[c] = hp1[c];
+            if (n) n[c] = valid ? hn[c] : 0;
+            if (p3) p3[c] = hp3[c];
+            if (epoch) epoch[c] = valid ? hep[c] : 0;
+            if (ops) {
+                if (valid) {
+                    std::memcpy(ops + 16 * c, hop.data() + 16 * c, 128);
+                } else {  // baseline, evaluated on the host only for this debug view
+                    int cx = static_cast<int>(c % L.N), cy = static_cast<int>(c / L.N);
+                    double x0 = cx * L.h, y0 = cy * L.h;
+                    double e = lzb_field_eval_host(&d_.field, x0 + (0 + 0.5) * 1.0 * L.h,
+                                                   y0 + (0 + 0.5) * 1.0 * L.h);
+                    for (int k = 0; k < 16; ++k) ops[16 * c + k] = 0.0 + kunit[k] * e;
+                }
+            }
+        }
+    }
+
+    void transfer(int level, int cx, int cy, double* out) {
+        check_level(level);
+        if (level >= D_) throw Error(LZB_ERR_INVALID, "leaf cells have no transfer block");
+        int64_t c = static_cast<int64_t>(cy) * L_[level].N + cx;
+        uint8_t has = 0;
+        LZB_CUDA(cudaMemcpy(&has, L_[level].has_P.p + c, 1, cudaMemcpyDeviceToHost));
+        if (has && L_[level].P.p)
+            LZB_CUDA(cudaMemcpy(out, L_[level].P.p + 64 * c, 512, cudaMemcpyDeviceToHost));
+        else
+            host_geo(out);
+    }
+
+    void publish_element(int level, int cx, int cy, const double* m, int n, int32_t p1) {
+        check_cell(level, cx, cy);
+        if (level != D_) throw Error(LZB_ERR_INVALID, "publish_element is for leaf cells");
+        DevBuf<double> dm(16);
+        LZB_CUDA(cudaMemcpyAsync(dm.p, m, 128, cudaMemcpyHostToDevice, s_));
+        LZB_LAUNCH(k_publish_one, 1, 32, 0, s_, V(D_), d_.field, cy * L_[D_].N + cx, dm.p, n, p1,
+                   d_.delta_max, cycle_, res_.p->s, ctx_->err.p);
+        sync_check();
+    }
+
+    void adaptive_step(int level, int cx, int cy) {
+        check_cell(level, cx, cy);
+        if (level != D_) throw Error(LZB_ERR_INVALID, "adaptive steps are for leaf cells");
+        LZB_LAUNCH(k_step_one, 1, 32, 0, s_, V(D_), d_.field, cy * L_[D_].N + cx, d_.schedule,
+                   d_.n_max, d_.termination_c, d_.delta_max, cycle_,
+                   d_.integration == LZB_INTEGRATE_FAST ? 1 : 0, res_.p->s, ctx_->err.p);
+        sync_check();
+    }
+
+    // ------------------------------------------------------------ stream I/O
+    int64_t image_size() {
+        DevBuf<int64_t> sizes(total_cells_);
+        record_sizes(sizes.p);
+        std::vector<int64_t> h(total_cells_);
+        LZB_CUDA(cudaMemcpyAsync(h.data(), sizes.p, sizes.bytes(), cudaMemcpyDeviceToHost, s_));
+        sync_check();
+        int64_t s = 12;
+        for (int64_t v : h) s += v;
+        return s;
+    }
+
+    void record_sizes(int64_t* sizes) {
+        for (int l = 0; l <= D_; ++l)
+            LZB_LAUNCH(k_record_sizes, blocks_for(L_[l].nc, kThreads), kThreads, 0, s_, V(l), l,
+                       l == D_ ? 1 : 0, slots_, sizes);
+    }
+
+    std::vector<uint8_t> image() {  // CellStream::save byte image, packed on the device
+        DevBuf<int64_t> sizes(total_cells_);
+        record_sizes(sizes.p);
+        std::vector<int64_t> h(total_cells_);
+        LZB_CUDA(cudaMemcpyAsync(h.data(), sizes.p, sizes.bytes(), cudaMemcpyDeviceToHost, s_));
+        sync_check();
+        int64_t acc = 0;
+        for (auto& v : h) {
+            int64_t t = v;
+            v = acc;
+            acc += t;
+        }
+        LZB_CUDA(cudaMemcpyAsync(sizes.p, h.data(), sizes.bytes(), cudaMemcpyHostToDevice, s_));
+        std::vector<uint8_t> out(12 + acc);
+        uint32_t hdr[3] = {0x4c5a4d47u, 1u, static_cast<uint32_t>(total_cells_)};
+        std::memcpy(out.data(), hdr, 12);
+        DevBuf<uint8_t> dout(out.size());
+        for (int l = 0; l <= D_; ++l)
+            LZB_LAUNCH(k_pack, blocks_for(L_[l].nc, kThreads), kThreads, 0, s_, V(l), d_.field, l,
+                       l == D_ ? 1 : 0, slots_, sizes.p, dout.p, ctx_->err.p);
+        LZB_CUDA(cudaMemcpyAsync(out.data() + 12, dout.p + 12, acc, cudaMemcpyDeviceToHost, s_));
+        sync_check();
+        return out;
+    }
+
+    void load(const uint8_t* in, int64_t size) {  // CellStream::load (stream.cpp:340-394)
+        if (size < 4) throw Error(LZB_ERR_CORRUPT, "truncated stream file");
+        uint32_t hdr[3] = {0, 0, 0};
+        std::memcpy(&hdr[0], in, 4);
+        if (hdr[0] != 0x4c5a4d47u) throw Error(LZB_ERR_CORRUPT, "bad stream magic");
+        if (size < 8) throw Error(LZB_ERR_CORRUPT, "truncated stream file");
+        std::memcpy(&hdr[1], in + 4, 4);
+        if (hdr[1] != 1u) throw Error(LZB_ERR_CORRUPT, "unsupported stream version");
+        if (size < 12) throw Error(LZB_ERR_CORRUPT, "truncated stream file");
+        std::memcpy(&hdr[2], in + 8, 4);
+        if (hdr[2] != static_cast<uint32_t>(total_cells_))
+            throw Error(LZB_ERR_CORRUPT, "stream cell count does not match the mesh");
+        // sequential header walk in pre-order: the record sizes chain the offsets
+        std::vector<int64_t> offsets(total_cells_);
+        int64_t pos = 12, slot = 0;
+        std::vector<int> stack;  // levels of the pre-order walk
+        std::function<void(int)> walk = [&](int l) {
+            if (pos >= size) throw Error(LZB_ERR_CORRUPT, "truncated stream file");
+            uint8_t h = in[pos];
+            int cls = (h >> 6) & 3, p3 = h & 0x0f;
+            if (cls == 3 || p3 == 1 || p3 > 8) throw Error(LZB_ERR_CORRUPT, "invalid record header byte");
+            offsets[slot++] = pos;
+            int64_t len = 1;
+            if (cls != 0 && p3 != 0) len += static_cast<int64_t>(p3) * (l == D_ ? 16 : 144);
+            if (pos + len > size) throw Error(LZB_ERR_CORRUPT, "truncated record payload");
+            pos += len;
+            if (l < D_)
+                for (int k = 0; k < 9; ++k) walk(l + 1);
+        };
+        walk(0);
+        // p3 == 0 payload-less class-1/2 records of refined cells: only 1 byte (handled by len)
+        DevBuf<int64_t> doff(total_cells_);
+        DevBuf<uint8_t> din(size);
+        LZB_CUDA(cudaMemcpyAsync(doff.p, offsets.data(), doff.bytes(), cudaMemcpyHostToDevice, s_));
+        LZB_CUDA(cudaMemcpyAsync(din.p, in, size, cudaMemcpyHostToDevice, s_));
+        for (int l = 0; l <= D_; ++l)
+            LZB_LAUNCH(k_unpack, blocks_for(L_[l].nc, 64), 64, 0, s_, V(l), d_.field, l,
+                       l == D_ ? 1 : 0, slots_, doff.p, din.p, d_.delta_max, cycle_, res_.p->s,
+                       ctx_->err.p);
+        sync_check();
+        pending_ = count_pending();
+    }
+
+    int64_t pending() const { return pending_; }
+    double* device_field(int level, int field) {
+        check_level(level);
+        if (field < 0 || field >= LZB_V_NFIELDS) throw Error(LZB_ERR_INVALID, "bad vertex field");
+        return L_[level].v[field].p;
+    }
+
+private:
+    void check_level(int level) const {
+        if (level < 0 || level > D_) throw Error(LZB_ERR_INVALID, "level out of range");
+    }
+    void check_cell(int level, int cx, int cy) const {
+        check_level(level);
+        if (cx < 0 || cy < 0 || cx >= L_[level].N || cy >= L_[level].N)
+            throw Error(LZB_ERR_INVALID, "cell out of range");
+    }
+
+    lzb_ctx* ctx_;
+    lzb_grid_desc d_;
+    int D_;
+    cudaStream_t s_;
+    std::vector<Level> L_;
+    int64_t leaves_ = 0, total_cells_ = 0, total_vertices_ = 0;
+    DevBuf<int32_t> list_, snap_;
+    DevBuf<int> counter_;
+    DevBuf<unsigned> hist_;
+    DevBuf<double> partial_;
+    DevBuf<Result> res_;
+    DevBuf<long long> keys_;
+    DevBuf<double> tx_, ty_;
+    Result* hres_ = nullptr;
+    unsigned* hhist_ = nullptr;
+    SlotTable slots_{};
+    uint32_t cycle_ = 0;
+    double first_residual_ = -1.0;
+    std::vector<double> history_;
+    uint64_t dof_total_ = 0;
+    int64_t pending_ = 0;
+};
+
+}  // namespace lzb
+
+struct lzb_grid {
+    lzb::Grid* g;
+};
+
+using namespace lzb;
+
+extern "C" {
+
+int lzb_grid_create(lzb_ctx* ctx, const lzb_grid_desc* desc, lzb_grid** out) {
+    return guarded([&] {
+        auto* g = new lzb_grid{nullptr};
+        try {
+            g->g = new Grid(ctx, *desc);
+        } catch (...) {
+            delete g;
+            throw;
+        }
+        *out = g;
+    });
+}
+void lzb_grid_destroy(lzb_grid* g) {
+    if (!g) return;
+    delete g->g;
+    delete g;
+}
+int lzb_grid_init_noise(lzb_grid* g, uint64_t seed) { return guarded([&] { g->g->init_noise(seed); }); }
+int lzb_grid_eager_setup(lzb_grid* g) {
+    return guarded([&] {
+        g->g->eager_setup();
+        g->g->sync_check();
+    });
+}
+int lzb_grid_assemble_fixed(lzb_grid* g, int n) {
+    return guarded([&] {
+        g->g->assemble_fixed(n);
+        g->g->sync_check();
+    });
+}
+int lzb_grid_step(lzb_grid* g, lzb_cycle_report* out) { return guarded([&] { *out = g->g->step(); }); }
+int lzb_grid_run(lzb_grid* g, lzb_cycle_report* out, int cap, int* count) {
+    return guarded([&] {
+        auto reps = g->g->run();
+        for (size_t i = 0; i < reps.size() && static_cast<int>(i) < cap; ++i) out[i] = reps[i];
+        *count = static_cast<int>(reps.size());
+    });
+}
+int lzb_grid_pass(lzb_grid* g, int which, double* value) {
+    return guarded([&] {
+        double v = g->g->pass(which);
+        if (value) *value = v;
+    });
+}
+int lzb_grid_cycle(lzb_grid* g) { return static_cast<int>(g->g->cycle()); }
+int lzb_grid_vertices(lzb_grid* g, int level, int field, double* buf, int write) {
+    return guarded([&] { g->g->vertices(level, field, buf, write != 0); });
+}
+int lzb_grid_cells(lzb_grid* g, int level, double* ops, int32_t* p1, int32_t* n, int32_t* p3,
+                   uint32_t* epoch) {
+    return guarded([&] { g->g->cells(level, ops, p1, n, p3, epoch); });
+}
+int lzb_grid_transfer(lzb_grid* g, int level, int cx, int cy, double* out64) {
+    return guarded([&] { g->g->transfer(level, cx, cy, out64); });
+}
+int lzb_grid_publish_element(lzb_grid* g, int level, int cx, int cy, const double* m16, int n,
+                             int32_t p1) {
+    return guarded([&] { g->g->publish_element(level, cx, cy, m16, n, p1); });
+}
+int lzb_grid_adaptive_step(lzb_grid* g, int level, int cx, int cy) {
+    return guarded([&] { g->g->adaptive_step(level, cx, cy); });
+}
+int lzb_grid_stats(lzb_grid* g, lzb_compression_stats* out) {
+    return guarded([&] { *out = g->g->stats(); });
+}
+int lzb_grid_stream_image(lzb_grid* g, uint8_t* out, int64_t cap, int64_t* size) {
+    return guarded([&] {
+        if (!out) {
+            *size = g->g->image_size();
+            return;
+        }
+        auto img = g->g->image();
+        *size = static_cast<int64_t>(img.size());
+        if (static_cast<int64_t>(img.size()) > cap) throw Error(LZB_ERR_INVALID, "buffer too small");
+        std::memcpy(out, img.data(), img.size());
+    });
+}
+int lzb_grid_stream_load(lzb_grid* g, const uint8_t* in, int64_t size) {
+    return guarded([&] { g->g->load(in, size); });
+}
+int lzb_grid_save(lzb_grid* g, const char* path) {
+    return guarded([&] {
+        auto img = g->g->image();
+        std::ofstream f(path, std::ios::binary);
+        if (!f) throw Error(LZB_ERR_IO, std::string("cannot open stream file for writing: ") + path);
+        f.write(reinterpret_cast<const char*>(img.data()), static_cast<std::streamsize>(img.size()));
+    });
+}
+int lzb_grid_load(lzb_grid* g, const char* path) {
+    return guarded([&] {
+        std::ifstream f(path, std::ios::binary);
+        if (!f) throw Error(LZB_ERR_IO, std::string("cannot open stream file: ") + path);
+        std::vector<uint8_t> buf((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+        g->g->load(buf.data(), static_cast<int64_t>(buf.size()));
+    });
+}
+int64_t lzb_grid_pending(lzb_grid* g) { return g->g->pending(); }
+int lzb_grid_device_view(lzb_grid* g, int level, int field, void** ptr) {
+    return guarded([&] { *ptr = g->g->device_field(level, field); });
+}
+
+}  // extern "C"

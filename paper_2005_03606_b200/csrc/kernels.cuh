@@ -1,0 +1,53 @@
+// kernels.cuh — declarations shared between the .cu translation units.
+#pragma once
+
+#include "device.cuh"
+#include "integrate.cuh"
+
+namespace lzb {
+
+// Constant tables uploaded once per device (make_ctx): K_unit = the reference
+// reference_subcell_stiffness(0,1,0,1) and the geometric transfer block.
+// (liblzb.so has a single device translation unit, lzb_unity.cu.)
+__constant__ double c_kunit[16];
+__constant__ double c_geo[64];
+
+void upload_constants();
+void host_kunit(double* out16);
+void host_geo(double* out64);
+
+// Galerkin RAP in the reference loop order (transfer.cpp:81-93,182-200).
+__device__ inline void patch_operator_dev(const double* ch, double* A) {
+    for (int i = 0; i < 256; ++i) A[i] = 0.0;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            const double* K = ch + 16 * (i * 3 + j);
+            int ids[4];
+            for (int c = 0; c < 4; ++c) ids[c] = (j + cdy(c)) * 4 + (i + cdx(c));
+            for (int a = 0; a < 4; ++a)
+                for (int b = 0; b < 4; ++b) A[ids[a] * 16 + ids[b]] += K[a * 4 + b];
+        }
+}
+
+__device__ inline void galerkin_from_A(const double* A, const double* P, double* out) {
+    double T[64];
+    for (int i = 0; i < 64; ++i) T[i] = 0.0;
+    for (int r = 0; r < 16; ++r)
+        for (int k = 0; k < 16; ++k) {
+            double a = A[r * 16 + k];
+            if (a == 0.0) continue;
+            for (int c = 0; c < 4; ++c) T[r * 4 + c] += a * P[k * 4 + c];
+        }
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) {
+            double v = 0.0;
+            for (int k = 0; k < 16; ++k) v += P[k * 4 + r] * T[k * 4 + c];
+            out[r * 4 + c] = v;
+        }
+}
+
+// BoxMG operator-dependent prolongation (transfer.cpp:95-180). Returns
+// fallback rows.
+__device__ int boxmg_from_A(const double* A, double* P);
+
+}  // namespace lzb
