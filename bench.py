@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 delayed-assembly hot path (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): the 729 x 729 grid (spacetree depth 6,
+531,441 leaf cells), eps = 1 + 0.9 sin(6 pi x) sin(6 pi y). One step = one
+assembly pass at the top of the p-doubling ladder (p = 32: 1,024 eps
+sub-samples per cell, 544.2 M per step): element integration + surplus +
+per-cell mantissa width (choose_precision, delta = 1e-8) + codec roundtrip +
+publish of the decoded operator, i.e. the fused K1+K3 kernel k_fixed.
+Metric: eps sub-sample integrations/s (BASELINE.json metric, first term).
+
+Also reported in the same line: the FAST (separable FMA) integration path,
+the smoother (one full additive multigrid cycle on that grid, DoF-updates/s),
+the roofline of the dominant kernel against a measured FP64 peak, the
+end-to-end leg through the C-ABI with a host buffer, and the reference CPU
+baseline (oracle/_ref = the unmodified reference integrate_element on all
+host cores) on a bounded sample.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (weak scaling: every
+  rank assembles its own 729^2 slab; no data-path collective)
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LEVEL = 6
+N_AXIS = 3 ** LEVEL
+CELLS = N_AXIS * N_AXIS
+P = 32
+SAMPLES_PER_STEP = CELLS * P * P
+# algorithmic FP64 flops per sub-sample of the tabulated integration:
+#   EXACT: 6 mul (K_sub from axis parts) + 9 add (K values) + 9 mul + 9 add (accumulate)
+#          + 2 (eps combine: 1 + (0.9 sin x) sin y)                                   = 35
+#   FAST : 4 FMA (row/column partial sums) + 1 FMA (eps combine)                       = 10
+FLOPS_PER_SAMPLE = {"exact": 35, "fast": 10}
+SURVEY_FLOPS_PER_SAMPLE = 77  # SURVEY.md §8d for C2 (2E + F_eps, sin counted per sample)
+METRIC = "eps sub-sample integrations/s; smoother DoF-updates/s; % FP64/HBM roofline"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- CPU baseline
+def cpu_baseline(seconds=10.0, threads=None):
+    """The reference's integrate_element (unmodified sources, oracle/_ref) over
+    disjoint cell ranges on `threads` host threads; falls back to the C port."""
+    import numpy as np
+
+    from oracle import port
+    from oracle import ref
+    from oracle.types import field_sinusoid
+
+    f = field_sinusoid(0.9, 6.0)
+    threads = threads or os.cpu_count() or 1
+    if ref.available():
+        # calibrate on a small sample, then run ~`seconds` of work
+        n0 = max(threads * 4, 64)
+        t0 = time.perf_counter()
+        ref.lib().ref_time_integrate(ref.C.byref(f), LEVEL, P, n0, threads, None)
+        dt = max(time.perf_counter() - t0, 1e-3)
+        ncells = int(min(CELLS, max(n0, n0 * seconds / dt)))
+        secs = ref.C.c_double()
+        rate = ref.lib().ref_time_integrate(ref.C.byref(f), LEVEL, P, ncells, threads, ref.C.byref(secs))
+        return {"value": rate, "unit": "sub-samples/s", "cores": threads, "kind": "reference",
+                "sample": f"{ncells} of the {CELLS} level-6 cells at p={P} (sinusoid eps), "
+                          f"integrate_element over {threads} threads, {secs.value:.1f} s"}
+    # fallback: the plain-C restatement, one thread
+    h = np.power(1.0 / 3, LEVEL)
+    t0 = time.perf_counter()
+    k = 0
+    while time.perf_counter() - t0 < seconds:
+        c = (k * 7919) % CELLS
+        port.integrate_element(f, (c % N_AXIS) * h, (c // N_AXIS) * h, h, P)
+        k += 1
+    dt = time.perf_counter() - t0
+    return {"value": k * P * P / dt, "unit": "sub-samples/s", "cores": 1, "kind": "port",
+            "sample": f"{k} level-6 cells at p={P}, oracle/lzb_oracle.c single thread, {dt:.1f} s"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(seconds=2.0)
+    t0 = time.perf_counter()
+    last = None
+    per_step = min(args.ref_seconds, 150.0 / max(args.steps, 1))  # whole run within a few minutes
+    for _ in range(args.steps):
+        last = cpu_baseline(seconds=per_step)
+        vals.append(last["value"])
+    wall = time.perf_counter() - t0
+    value = statistics.mean(vals)
+    line = {"metric": METRIC, "impl": "reference", "value": value, "unit": "sub-samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(args.steps, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded analytic eps field, BASELINE.json configs[1])",
+            "config": {"workload": f"c2-assembly-729x729-p{P}", "grid": "729x729 (depth 6)",
+                       "eps": "1+0.9 sin(6 pi x) sin(6 pi y)", "p": P},
+            "cpu_baseline": {**last, "value": value},
+            "e2e": {"value": value, "unit": "sub-samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_2005_03606_b200 as lzb
+
+    torch.cuda.set_device(local)
+    ctx = lzb.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.solve_stream)
+    f = lzb.field_sinusoid(0.9, 6.0)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")  # > 126 MB L2
+
+    def make(integration):
+        d = lzb.make_desc(depth=LEVEL, field=f, delta_max=1e-8, solver="additive", omega=0.6,
+                          assembly="adaptive", rhs_kind="sinprod", integration=integration, max_cycles=10 ** 6)
+        return lzb.Grid(d, 42, ctx)
+
+    def timed_steps(fn, k):
+        """Per-step CUDA events on the launching stream, L2 flushed between steps (untimed)."""
+        total = 0.0
+        for _ in range(k):
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            total += a.elapsed_time(b) * 1e-3
+        return total
+
+    fp64_peak = lzb.probe_fp64_tflops(local)
+    results = {}
+    for integration in ("exact", "fast"):
+        g = make(integration)
+        for _ in range(args.warmup):
+            g.assemble_fixed(P)
+        barrier(world)
+        torch.cuda.synchronize()
+        l0 = lzb.launch_count()
+        with ClockSampler(local) as clk:
+            t = timed_steps(lambda: g.assemble_fixed(P), args.steps)
+        launches = lzb.launch_count() - l0
+        barrier(world)
+        torch.cuda.synchronize()
+        t = max_over_ranks(t, world)
+        st = g.stats()
+        results[integration] = dict(t=t, launches=launches, clocks=clk.summary(), grid=g,
+                                    p3_hist=list(st.p3_histogram), factor=st.fine_factor_totals)
+
+    head = args.integration
+    r = results[head]
+    ms = 1e3 * r["t"] / args.steps
+    value = world * SAMPLES_PER_STEP * args.steps / r["t"]
+
+    def roof(mode):
+        per_launch_s = results[mode]["t"] / args.steps
+        achieved = SAMPLES_PER_STEP * FLOPS_PER_SAMPLE[mode] / per_launch_s / 1e12
+        return {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak, "traffic": None,
+                "flops_per_sample": FLOPS_PER_SAMPLE[mode],
+                "peak_source": "measured: lzb_probe_fp64_tflops (DFMA chains, this GPU)",
+                "survey_def_achieved": SAMPLES_PER_STEP * SURVEY_FLOPS_PER_SAMPLE / per_launch_s / 1e12}
+
+    # smoother: full additive cycles on the assembled 729^2 grid (DoF-updates/s)
+    g = results[head]["grid"]
+    for _ in range(3):
+        g.step()
+    cycles = max(5, args.steps)
+    l0 = lzb.launch_count()
+    tc = timed_steps(lambda: g.step(), cycles)
+    cyc_launches = lzb.launch_count() - l0
+    tc = max_over_ranks(tc, world)
+    dof = (N_AXIS - 1) ** 2
+    smoother = {"metric": "fine DoF-updates/s (full additive cycle: coarse Galerkin + residual + "
+                          "restriction + Jacobi + prolongation + injection + stats)",
+                "value": world * dof * cycles / tc, "ms_per_cycle": 1e3 * tc / cycles, "cycles": cycles,
+                "launches_per_cycle": cyc_launches / cycles, "dof_per_cycle": dof}
+
+    # end to end through the C-ABI: assemble, then the compressed LZMG stream to a host buffer
+    img = g.stream_image()
+
+    def e2e_step():
+        g.assemble_fixed(P)
+        g.stream_image()
+
+    te = timed_steps(e2e_step, args.steps)
+    te = max_over_ranks(te, world)
+    e2e = {"value": world * SAMPLES_PER_STEP * args.steps / te, "unit": "sub-samples/s",
+           "h2d_bytes_per_step": 560, "d2h_bytes_per_step": len(img) + 8 * (sum(3 ** (2 * l) for l in range(7))),
+           "path": "lzb_grid_assemble_fixed + lzb_grid_stream_image (LZMG bytes into host memory)"}
+
+    if rank != 0:
+        return
+    base = cpu_baseline(seconds=args.cpu_seconds) if not args.no_cpu_baseline else None
+    mp = peaks()
+    line = {
+        "metric": METRIC, "value": value, "unit": "sub-samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded analytic eps field, BASELINE.json configs[1])",
+        "config": {"workload": f"c2-assembly-729x729-p{P}", "grid": "729x729 (depth 6)", "cells": CELLS,
+                   "eps": "1+0.9 sin(6 pi x) sin(6 pi y)", "p": P, "delta_max": 1e-8,
+                   "integration": head, "l2": "flushed between timed steps (256 MB write)",
+                   "parallelism": f"weak-scaled slabs x{world}"},
+        "roofline": roof(head),
+        "fast_path": {"value": world * SAMPLES_PER_STEP * args.steps / results["fast"]["t"],
+                      "ms_per_step": 1e3 * results["fast"]["t"] / args.steps, "roofline": roof("fast")},
+        "exact_path": {"value": world * SAMPLES_PER_STEP * args.steps / results["exact"]["t"],
+                       "ms_per_step": 1e3 * results["exact"]["t"] / args.steps, "roofline": roof("exact")},
+        "smoother": smoother,
+        "compression": {"p3_histogram": r["p3_hist"], "fine_factor_totals": r["factor"]},
+        "e2e": e2e,
+        "cpu_baseline": base,
+        "gpu_launches": r["launches"],
+        "clocks": r["clocks"],
+        "hbm_peak_gbs": mp.get("hbm_gbs"),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--integration", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

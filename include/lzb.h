@@ -29,6 +29,9 @@ const char* lzb_last_error(void);
 int lzb_version(void);
 /* Number of kernels this library has launched since load (evidence counter). */
 uint64_t lzb_launch_count(void);
+/* Measured FP64 FMA throughput of this device (TFLOP/s): the roofline
+ * denominator for the FP64-bound integration kernel. */
+int lzb_probe_fp64_tflops(int device, double* tflops);
 
 typedef struct lzb_ctx lzb_ctx;
 /* Device + two streams: solve (high priority) and assembly (low priority). */
@@ -58,6 +61,10 @@ int lzb_integrate_elements_dev(lzb_ctx* ctx, const lzb_field* eps, int64_t ncell
  * boxes as cell_box() (element.hpp:29-32) with h = pow(1/3, level) (mesh.hpp:87). */
 int lzb_integrate_level_dev(lzb_ctx* ctx, const lzb_field* eps, int level, int n,
                             double* out, int integration, void* stream);
+/* Same, host output buffer (the end-to-end entry: the field descriptor goes in,
+ * N*N*16 doubles come back). */
+int lzb_integrate_level(lzb_ctx* ctx, const lzb_field* eps, int level, int n, double* host_out,
+                        int integration);
 /* reference_subcell_stiffness(a,b,c,d)                   element.hpp:19 */
 int lzb_subcell_stiffness(lzb_ctx* ctx, double a, double b, double c, double d, double* out16);
 

@@ -79,6 +79,8 @@ def lib():
         L.lzb_integrate_elements.argtypes = [vp, C.POINTER(Field), i64, vp, vp, vp, vp, vp, C.c_int]
         L.lzb_integrate_elements_dev.argtypes = [vp, C.POINTER(Field), i64, vp, vp, vp, vp, vp, C.c_int, vp]
         L.lzb_integrate_level_dev.argtypes = [vp, C.POINTER(Field), C.c_int, C.c_int, vp, C.c_int, vp]
+        L.lzb_integrate_level.argtypes = [vp, C.POINTER(Field), C.c_int, C.c_int, vp, C.c_int]
+        L.lzb_probe_fp64_tflops.argtypes = [C.c_int, C.POINTER(dbl)]
         L.lzb_subcell_stiffness.argtypes = [vp, dbl, dbl, dbl, dbl, vp]
         L.lzb_codec_encode.argtypes = [vp, i64, vp, C.c_int, vp]
         L.lzb_codec_decode.argtypes = [vp, i64, vp, C.c_int, vp]
@@ -195,6 +197,23 @@ def integrate_elements(field: Field, x0, y0, h, n, integration="exact", ctx: Con
 def integrate_element(box, field: Field, n: int, integration="exact", ctx=None):
     x0, y0, h = box
     return integrate_elements(field, [x0], [y0], [h], [n], integration, ctx)[0]
+
+
+def integrate_level(field: Field, level: int, n: int, integration="exact", out=None, ctx=None):
+    """All cells of a regular level at one n into a host array (N*N, 16)."""
+    ctx = ctx or default_context()
+    N = 3 ** level
+    if out is None:
+        out = np.zeros((N * N, 16))
+    mode = T.INTEGRATE_FAST if integration == "fast" else T.INTEGRATE_EXACT
+    _check(lib().lzb_integrate_level(ctx.h, C.byref(field), level, n, _ptr(out), mode))
+    return out
+
+
+def probe_fp64_tflops(device=0) -> float:
+    v = C.c_double()
+    _check(lib().lzb_probe_fp64_tflops(device, C.byref(v)))
+    return v.value
 
 
 def reference_subcell_stiffness(a, b, c, d, ctx=None):

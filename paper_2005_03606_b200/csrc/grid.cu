@@ -817,8 +817,7 @@ __global__ void k_clear_p2(LevelView F, const int32_t* list, int count) {
 }
 
 __global__ void k_reset_stats(Result* r) {
-    if (threadIdx.x < 13) r->s[threadIdx.x] = 0;
-    if (threadIdx.x == 0) r->norm = 0.0;
+    if (threadIdx.x < 13) r->s[threadIdx.x] = 0;  // per-cycle slots; the norm is written by k_norm_final
 }
 
 template <int KIND>

@@ -4,6 +4,8 @@
 // Compiled as part of lzb_unity.cu (one device translation unit, -fmad=false).
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
+#include <cmath>
 #include <mutex>
 
 #include "engine.hpp"
@@ -145,6 +147,19 @@ void build_axis_tables(const lzb_field& f, int N, double h, int n, double* tx, d
     unsigned grid = blocks_for(static_cast<int64_t>(N) * n, 256);
     LZB_LAUNCH(k_axis_table, grid, 256, 0, s, f, N, h, n, 0, tx);
     LZB_LAUNCH(k_axis_table, grid, 256, 0, s, f, N, h, n, 1, ty);
+}
+
+// FP64 peak probe: 8 independent DFMA chains per thread, one CTA per SM slot.
+__global__ void k_fp64_probe(int iters, double seed, double* sink) {
+    double a[8];
+    for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 1e-9 + k;
+    const double m = 0.999999999, c = 1e-9;
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = __fma_rn(a[k], m, c);
+    double s = 0;
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == 12345.678) sink[0] = s;  // keep the chains alive
 }
 
 // ------------------------------------------------------------------ codec
@@ -408,6 +423,54 @@ int lzb_integrate_level_dev(lzb_ctx* ctx, const lzb_field* eps, int level, int n
         else
             launch_integrate_level<false>(*eps, N, n, tx.p, ty.p, out, s);
         LZB_CUDA(cudaStreamSynchronize(s));  // tables are freed on return
+    });
+}
+
+int lzb_integrate_level(lzb_ctx* ctx, const lzb_field* eps, int level, int n, double* host_out,
+                        int integration) {
+    return guarded([&] {
+        if (level < 0 || level > 9 || n < 1) throw Error(LZB_ERR_INVALID, "bad level or n");
+        int N = 1;
+        for (int i = 0; i < level; ++i) N *= 3;
+        double h = std::pow(1.0 / 3, level);
+        cudaStream_t s = ctx->solve;
+        DevBuf<double> tx(static_cast<size_t>(N) * n * kTab), ty(static_cast<size_t>(N) * n * kTab);
+        DevBuf<double> out(static_cast<size_t>(N) * N * 16);
+        build_axis_tables(*eps, N, h, n, tx.p, ty.p, s);
+        if (integration == LZB_INTEGRATE_FAST)
+            launch_integrate_level<true>(*eps, N, n, tx.p, ty.p, out.p, s);
+        else
+            launch_integrate_level<false>(*eps, N, n, tx.p, ty.p, out.p, s);
+        LZB_CUDA(cudaMemcpyAsync(host_out, out.p, out.bytes(), cudaMemcpyDeviceToHost, s));
+        LZB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int lzb_probe_fp64_tflops(int device, double* tflops) {
+    return guarded([&] {
+        LZB_CUDA(cudaSetDevice(device));
+        int sms = 0;
+        LZB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        DevBuf<double> sink(1);
+        const int threads = 512, blocks = sms * 4, iters = 4096;
+        cudaEvent_t a, b;
+        LZB_CUDA(cudaEventCreate(&a));
+        LZB_CUDA(cudaEventCreate(&b));
+        LZB_LAUNCH(k_fp64_probe, blocks, threads, 0, 0, iters, 1.0, sink.p);  // warm-up
+        double best = 0.0;
+        for (int rep = 0; rep < 5; ++rep) {
+            LZB_CUDA(cudaEventRecord(a, 0));
+            LZB_LAUNCH(k_fp64_probe, blocks, threads, 0, 0, iters, 1.0 + rep, sink.p);
+            LZB_CUDA(cudaEventRecord(b, 0));
+            LZB_CUDA(cudaEventSynchronize(b));
+            float ms = 0;
+            LZB_CUDA(cudaEventElapsedTime(&ms, a, b));
+            double flops = 2.0 * 8.0 * iters * static_cast<double>(threads) * blocks;
+            best = std::max(best, flops / (ms * 1e-3) / 1e12);
+        }
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        *tflops = best;
     });
 }
 

@@ -105,18 +105,22 @@ def test_cycle_transcendental_fields_within_tolerance(setup):
     assert_state(g, o, d.depth, exact=False)
 
 
-def test_fixed_p_checkerboard_sinprod_delta0():
-    """BASELINE config 1 shape (depth 4 here): fixed p, exact storage, additive, omega 0.6."""
+@pytest.mark.parametrize("rhs_kind", ["constant", "sinprod"])
+def test_fixed_p_checkerboard_delta0(rhs_kind):
+    """BASELINE config 1 shape (depth 4 here): fixed p, exact storage, additive, omega 0.6.
+    The sinprod rhs goes through CUDA sin (ulp-level differences): tolerance, not bits."""
     text = "setup = checkerboard\ndepth = 4\nsolver = additive\nassembly = adaptive\nmax-cycles = 6\nomega = 0.6\n" \
-           "compression-threshold = 0\nseed = 42\n"
-    g, o, d = grid_pair(text, rhs=lzb.Rhs(kind=lzb.T.RHS_SINPROD, value=2 * np.pi ** 2))
+           "compression-threshold = 0\nrhs = 1\nseed = 42\n"
+    kw = {"rhs": lzb.Rhs(kind=lzb.T.RHS_SINPROD, value=2 * np.pi ** 2)} if rhs_kind == "sinprod" else {}
+    g, o, d = grid_pair(text, **kw)
     for p in (1, 2, 4):
         g.assemble_fixed(p)
         o.assemble_fixed(p)
         assert np.array_equal(g.cells(4)["ops"], o.cells(4)["ops"])
     rg, ro = [g.step() for _ in range(6)], [o.step() for _ in range(6)]
-    assert_reports(rg, ro)
-    assert_state(g, o, 4)
+    exact = rhs_kind == "constant"
+    assert_reports(rg, ro, rel=1e-13 if exact else 1e-10)
+    assert_state(g, o, 4, exact=exact)
 
 
 def test_double_schedule_and_cap():
@@ -201,7 +205,8 @@ def test_large_grid_properties():
     g.assemble_fixed(4)
     ops = g.cells(6)["ops"].reshape(-1, 4, 4)
     assert np.max(np.abs(ops - ops.transpose(0, 2, 1))) <= 1e-12 * np.max(np.abs(ops))  # symmetry
-    assert np.max(np.abs(ops.sum(axis=2))) <= 1e-12 * np.max(np.abs(ops))              # zero row sums
+    # zero row sums up to the absorbed codec error (|rt - surplus| <= delta_max per entry)
+    assert np.max(np.abs(ops.sum(axis=2))) <= 4 * d.delta_max + 1e-12 * np.max(np.abs(ops))
     # a sample of cells against the oracle element (codec-absorbed with delta 1e-8)
     rng = np.random.default_rng(0)
     idx = rng.integers(0, 729 * 729, 64)
