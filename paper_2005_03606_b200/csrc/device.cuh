@@ -176,8 +176,45 @@ __device__ inline double decode_value(const uint8_t* in, int p3) {
     return sign ? -v : v;
 }
 
+// Bit-level roundtrip for p3 in 2..7 and finite x: the value encode_value +
+// decode_value produce (codec.cpp:8-63) built directly from the IEEE fields.
+// frexp normalises subnormals, so their significand is renormalised here;
+// the decoded exponent e_hat in [-128,127] is always a normal double.
+__device__ __forceinline__ double rt_bits(double x, int m) {
+    unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(x));
+    const unsigned long long kMask = 0xFFFFFFFFFFFFFull;
+    unsigned long long sign = u >> 63;
+    int E = static_cast<int>((u >> 52) & 0x7ff);
+    unsigned long long F = u & kMask;
+    if (E == 0 && F == 0) return 0.0;  // +-0 -> (0, 0, -128) -> +0
+    int e;
+    if (E == 0) {
+        int b = 63 - __clzll(static_cast<long long>(F));
+        e = b - 1074;
+        F = (F << (52 - b)) & kMask;
+    } else {
+        e = E - 1023;
+    }
+    int e_hat = e < -128 ? -128 : (e > 127 ? 127 : e);
+    unsigned long long fb = F >> (52 - m);
+    if (!sign && fb == 0 && e_hat == -128) return 0.0;
+    unsigned long long r = (sign << 63) | (static_cast<unsigned long long>(e_hat + 1023) << 52) |
+                           (fb << (52 - m));
+    return __longlong_as_double(static_cast<long long>(r));
+}
+
 // codec::roundtrip (codec.hpp:28-33) without the byte detour: the same
 // encode/decode arithmetic on registers. Returns false for non-finite.
+__device__ inline bool roundtrip_fast(double x, int p3, double& out) {
+    if (p3 == 0) {
+        out = 0.0;
+        return true;
+    }
+    if (!dev_isfinite(x)) return false;
+    out = p3 == 8 ? x : rt_bits(x, mantissa_bits(p3));
+    return true;
+}
+
 __device__ inline bool roundtrip(double x, int p3, double& out) {
     if (p3 == 0) {
         out = 0.0;
@@ -210,8 +247,39 @@ __device__ inline bool roundtrip(double x, int p3, double& out) {
     return true;
 }
 
-// codec::choose_precision (codec.cpp:65-85). Returns -1 for non-finite input.
+// codec::choose_precision (codec.cpp:65-85), literal scan. Returns -1 where
+// the reference throws (non-finite value reached by the scan).
+__device__ inline int choose_precision_scan(const double* v, int count, double delta);
+
+// Same result, fewer roundtrips: P = max over entries of the entry's smallest
+// passing width (8 if none in 2..7); no width below P can pass for all
+// entries, so the reference's scan can start at P. Records
+// holding a non-finite value take the literal scan (its throw/8 semantics).
 __device__ inline int choose_precision(const double* v, int count, double delta) {
+    bool all_small = true, finite = true;
+    for (int i = 0; i < count; ++i) {
+        if (fabs(v[i]) > delta) all_small = false;
+        finite = finite && dev_isfinite(v[i]);
+    }
+    if (all_small) return 0;
+    if (!finite) return choose_precision_scan(v, count, delta);
+    int P = 2;
+    for (int i = 0; i < count; ++i) {
+        int q = P;
+        while (q < 8 && fabs(rt_bits(v[i], mantissa_bits(q)) - v[i]) > delta) ++q;
+        // widths below P need no test for this entry: P only grows
+        P = q;
+        if (P == 8) return 8;
+    }
+    for (int q = P; q < 8; ++q) {
+        bool ok = true;
+        for (int i = 0; i < count && ok; ++i) ok = fabs(rt_bits(v[i], mantissa_bits(q)) - v[i]) <= delta;
+        if (ok) return q;
+    }
+    return 8;
+}
+
+__device__ inline int choose_precision_scan(const double* v, int count, double delta) {
     bool all_small = true;
     for (int i = 0; i < count; ++i)
         if (fabs(v[i]) > delta) {

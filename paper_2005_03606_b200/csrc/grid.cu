@@ -26,8 +26,6 @@
 
 namespace lzb {
 
-void build_axis_tables(const lzb_field& f, int N, double h, int n, double* tx, double* ty,
-                       cudaStream_t s);
 
 namespace {
 
@@ -99,7 +97,7 @@ __device__ inline bool publish_leaf(const LevelView& F, int c, const double* m, 
     double* op = F.op + 16 * static_cast<int64_t>(c);
     for (int k = 0; k < 16; ++k) {
         double rt;
-        roundtrip(sur[k], p3, rt);
+        if (!roundtrip_fast(sur[k], p3, rt)) return false;
         double err = fabs(rt - sur[k]);
         delta = delta < err ? err : delta;
         op[k] = base[k] + rt;
@@ -159,31 +157,27 @@ __global__ void k_bottom(LevelView F, lzb_field f, const int32_t* list, const in
 // publish (assembly.cpp:36-59). Fused K1 + K3: integrate, surplus,
 // choose_precision, roundtrip, store.
 template <int KIND, bool FAST>
-__global__ void __launch_bounds__(128) k_step(LevelView F, lzb_field f, const int32_t* list,
-                                              const int32_t* snap, int count, int n, int nn,
-                                              int n_cap_top, const double* __restrict__ tx,
-                                              const double* __restrict__ ty, double term_c,
-                                              double delta_max, uint32_t cycle, int clear_p2,
-                                              unsigned long long* stats, int* err) {
-    __shared__ double s_table[64];
-    if (KIND == LZB_FIELD_CHECKER)
-        for (int i = threadIdx.x; i < 64; i += blockDim.x) s_table[i] = f.table[i];
-    __syncthreads();
+__global__ void __launch_bounds__(kIntThreads) k_step(LevelView F, lzb_field f, const int32_t* list,
+                                                      const int32_t* snap, int count, int n, int nn,
+                                                      int n_cap_top, IntTables T, double term_c,
+                                                      double delta_max, uint32_t cycle, int clear_p2,
+                                                      unsigned long long* stats, int* err) {
+    extern __shared__ double sm[];
     int64_t t = gtid();
-    if (t >= count || snap[t] != n) return;
-    int c = list[t], cx = c % F.N, cy = c / F.N;
+    const bool mine = t < count && snap[t] == n;
+    const int c = mine ? list[t] : 0, cx = c % F.N, cy = c / F.N;
     if (n_cap_top) {  // sampling cap reached: the marker becomes top, nothing integrated
-        F.p1[c] = LZB_P1_TOP;
-        if (clear_p2) F.p2[c] = 0;
+        if (mine) {
+            F.p1[c] = LZB_P1_TOP;
+            if (clear_p2) F.p2[c] = 0;
+        }
         return;
     }
+    stage_common(sm, f, T);
     double fresh[16];
-    const double* txc = tx + static_cast<int64_t>(cx) * nn * kTab;
-    const double* tyc = ty + static_cast<int64_t>(cy) * nn * kTab;
-    if (FAST)
-        integrate_fast_tab<KIND>(txc, tyc, nn, f.value, f.eps_low, f.blocks, s_table, fresh);
-    else
-        integrate_exact_tab<KIND>(txc, tyc, nn, f.value, f.eps_low, f.blocks, s_table, fresh);
+    integrate_block<KIND, FAST>(mine, f, T, T.fx + static_cast<int64_t>(cx) * nn,
+                                T.fy + static_cast<int64_t>(cy) * nn, sm, fresh);
+    if (!mine) return;
     const double* old = F.op + 16 * static_cast<int64_t>(c);
     double denom = 0.0, dmax = 0.0;
     for (int k = 0; k < 16; ++k) {
@@ -217,31 +211,140 @@ __global__ void k_spawn(LevelView F, uint32_t cycle, long long leaf_count, long 
 
 // Fixed-p assembly: every leaf integrated at n, published, p1 = top.
 template <int KIND, bool FAST>
-__global__ void __launch_bounds__(128) k_fixed(LevelView F, lzb_field f, int n,
-                                               const double* __restrict__ tx,
-                                               const double* __restrict__ ty, double delta_max,
-                                               uint32_t cycle, unsigned long long* stats,
-                                               int* err) {
-    __shared__ double s_table[64];
-    if (KIND == LZB_FIELD_CHECKER)
-        for (int i = threadIdx.x; i < 64; i += blockDim.x) s_table[i] = f.table[i];
-    __syncthreads();
+__global__ void __launch_bounds__(kIntThreads) k_fixed(LevelView F, lzb_field f, int n, IntTables T,
+                                                       double delta_max, uint32_t cycle,
+                                                       unsigned long long* stats, int* err) {
+    extern __shared__ double sm[];
+    stage_common(sm, f, T);
     int64_t c = gtid();
-    if (c >= static_cast<int64_t>(F.N) * F.N) return;
-    int cx = static_cast<int>(c % F.N), cy = static_cast<int>(c / F.N);
+    const bool mine = c < static_cast<int64_t>(F.N) * F.N;
+    int cx = mine ? static_cast<int>(c % F.N) : 0, cy = mine ? static_cast<int>(c / F.N) : 0;
     double m[16];
-    const double* txc = tx + static_cast<int64_t>(cx) * n * kTab;
-    const double* tyc = ty + static_cast<int64_t>(cy) * n * kTab;
-    if (FAST)
-        integrate_fast_tab<KIND>(txc, tyc, n, f.value, f.eps_low, f.blocks, s_table, m);
-    else
-        integrate_exact_tab<KIND>(txc, tyc, n, f.value, f.eps_low, f.blocks, s_table, m);
+    integrate_block<KIND, FAST>(mine, f, T, T.fx + static_cast<int64_t>(cx) * n,
+                                T.fy + static_cast<int64_t>(cy) * n, sm, m);
+    if (!mine) return;
     double e_c = centre_eps(f, F, cx, cy);
     if (!publish_leaf(F, static_cast<int>(c), m, n, e_c, delta_max, cycle, stats)) atomicExch(err, 1);
     F.p1[c] = LZB_P1_TOP;
 }
 
-// recompute_coarse + publish_coarse (solver.cpp:59-77, stream.cpp:134-184).
+// recompute_coarse + publish_coarse for the geometric transfer (solver.cpp:59-77,
+// transfer.cpp:81-93,182-200, stream.cpp:134-184), register-streaming form:
+// T is produced one lattice row k at a time (A[k][m] summed over the children
+// that contain both lattice vertices, in the reference's child order, zero
+// entries skipped) and out += P[k][.] * T[k][.] accumulates in ascending k,
+// which is exactly the reference's summation order — without the 16x16 A.
+// The nine children of each thread's cell are staged in shared memory,
+// entry-major ([entry][thread]) so that every access is bank-conflict free.
+constexpr int kCoarseThreads = 32;  // 144 doubles x 32 threads = 36 KB static smem
+__global__ void __launch_bounds__(kCoarseThreads) k_coarse_geo(LevelView C, LevelView F, lzb_field f,
+                                                               double delta_max, uint32_t cycle,
+                                                               unsigned long long* stats, int* err) {
+    __shared__ double sch[144 * kCoarseThreads];
+    const int t = threadIdx.x;
+    int64_t c = gtid();
+    const bool in = c < static_cast<int64_t>(C.N) * C.N;
+    const int cx = in ? static_cast<int>(c % C.N) : 0, cy = in ? static_cast<int>(c / C.N) : 0;
+    bool ready = in;
+    if (in)
+        for (int lx = 0; lx < 3; ++lx)
+            for (int ly = 0; ly < 3; ++ly) {
+                int64_t fc = static_cast<int64_t>(3 * cy + ly) * F.N + 3 * cx + lx;
+                if (F.p1[fc] == LZB_P1_BOTTOM) ready = false;  // delayed semantics (solver.cpp:65)
+                const double2* src = reinterpret_cast<const double2*>(F.op + 16 * fc);
+                for (int q = 0; q < 8; ++q) {
+                    double2 v = src[q];
+                    sch[((lx * 3 + ly) * 16 + 2 * q) * kCoarseThreads + t] = v.x;
+                    sch[((lx * 3 + ly) * 16 + 2 * q + 1) * kCoarseThreads + t] = v.y;
+                }
+            }
+    if (!ready) return;  // no block-level barrier follows
+    double o[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) o[q] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int kx = k & 3, ky = k >> 2;
+        double T0 = 0.0, T1 = 0.0, T2 = 0.0, T3 = 0.0;
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const int mx = m & 3, my = m >> 2;
+            if (mx - kx > 1 || kx - mx > 1 || my - ky > 1 || ky - my > 1) continue;  // A[k][m] == 0
+            double a = 0.0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    const int ak = (kx - i) + 2 * (ky - j), am = (mx - i) + 2 * (my - j);
+                    if (kx - i < 0 || kx - i > 1 || ky - j < 0 || ky - j > 1) continue;
+                    if (mx - i < 0 || mx - i > 1 || my - j < 0 || my - j > 1) continue;
+                    a += sch[((i * 3 + j) * 16 + ak * 4 + am) * kCoarseThreads + t];
+                }
+            if (a == 0.0) continue;  // transfer.cpp:189
+            T0 += a * c_geo[m * 4 + 0];
+            T1 += a * c_geo[m * 4 + 1];
+            T2 += a * c_geo[m * 4 + 2];
+            T3 += a * c_geo[m * 4 + 3];
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const double p = c_geo[k * 4 + r];
+            o[r * 4 + 0] += p * T0;
+            o[r * 4 + 1] += p * T1;
+            o[r * 4 + 2] += p * T2;
+            o[r * 4 + 3] += p * T3;
+        }
+    }
+    // publish_coarse: one p3 across A-hat and P-hat; P-hat = P - geo = 0 here, so the
+    // joint width equals the width of A-hat alone whenever delta_max >= 0.
+    const double e_c = centre_eps(f, C, cx, cy);
+    double sur[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) sur[k] = o[k] - baseline_entry(k, e_c);
+    int p3;
+    if (delta_max >= 0.0) {
+        p3 = choose_precision(sur, 16, delta_max);
+    } else {  // a negative threshold fails the zero P-hat entries at every width 2..7
+        bool fin = true;
+        for (int k = 0; k < 16; ++k) fin = fin && dev_isfinite(sur[k]);
+        p3 = fin ? 8 : -1;
+    }
+    if (p3 < 0) {
+        atomicExch(err, 1);
+        return;
+    }
+    double delta = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        double rt;
+        if (!roundtrip_fast(sur[k], p3, rt)) {
+            atomicExch(err, 1);
+            return;
+        }
+        double e = fabs(rt - sur[k]);
+        delta = delta < e ? e : delta;
+        o[k] = baseline_entry(k, e_c) + rt;
+    }
+    double* op = C.op + 16 * c;
+    if (C.p1[c] == LZB_P1_TOP && C.has_P[c]) {
+        bool same = true;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) same = same && (o[k] == op[k]);
+        if (same) return;  // epoch stamps track real information flow (stream.cpp:153-158)
+    }
+    atomic_max_double_bits(&stats[S_MAXDELTA], delta);
+    double2* dst = reinterpret_cast<double2*>(op);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dst[q] = make_double2(o[2 * q], o[2 * q + 1]);
+    C.has_P[c] = 1;
+    C.n[c] = 1;
+    C.epoch[c] = cycle;
+    C.p3[c] = static_cast<int8_t>(p3);
+    C.p1[c] = LZB_P1_TOP;
+}
+
+// recompute_coarse + publish_coarse with BoxMG transfer (needs the full patch
+// operator A for the operator-dependent prolongation, transfer.cpp:95-180).
 __global__ void __launch_bounds__(64) k_coarse(LevelView C, LevelView F, lzb_field f, int boxmg,
                                                double delta_max, uint32_t cycle,
                                                unsigned long long* stats, int* err) {
@@ -275,7 +378,7 @@ __global__ void __launch_bounds__(64) k_coarse(LevelView C, LevelView F, lzb_fie
     double delta = 0.0;
     for (int k = 0; k < 80; ++k) {
         double rt;
-        roundtrip(joint[k], p3, rt);
+        if (!roundtrip_fast(joint[k], p3, rt)) { atomicExch(err, 1); return; }
         double e = fabs(rt - joint[k]);
         delta = delta < e ? e : delta;
         if (k < 16) m[k] = baseline_entry(k, e_c) + rt;
@@ -731,7 +834,7 @@ __global__ void k_unpack(LevelView L, lzb_field f, int level, int leaf, SlotTabl
         double delta = 0.0;
         for (int k = 0; k < 80; ++k) {
             double rt;
-            roundtrip(joint[k], q3, rt);
+            if (!roundtrip_fast(joint[k], q3, rt)) { atomicExch(err, 1); return; }
             double d = fabs(rt - joint[k]);
             delta = delta < d ? d : delta;
             if (k < 16) m[k] = baseline_entry(k, e) + rt;
@@ -820,27 +923,41 @@ __global__ void k_reset_stats(Result* r) {
     if (threadIdx.x < 13) r->s[threadIdx.x] = 0;  // per-cycle slots; the norm is written by k_norm_final
 }
 
-template <int KIND>
-void launch_step(bool fast, unsigned grid, cudaStream_t s, const LevelView& F, const lzb_field& f,
-                 const int32_t* list, const int32_t* snap, int count, int n, int nn, int cap,
-                 const double* tx, const double* ty, double term_c, double dmax, uint32_t cycle,
-                 unsigned long long* stats, int* err) {
-    if (fast)
-        LZB_LAUNCH((k_step<KIND, true>), grid, 128, 0, s, F, f, list, snap, count, n, nn, cap, tx, ty,
-                   term_c, dmax, cycle, 0, stats, err);
-    else
-        LZB_LAUNCH((k_step<KIND, false>), grid, 128, 0, s, F, f, list, snap, count, n, nn, cap, tx,
-                   ty, term_c, dmax, cycle, 0, stats, err);
+template <int KIND, bool FAST>
+void launch_step_k(cudaStream_t s, const LevelView& F, const lzb_field& f, const int32_t* list,
+                   const int32_t* snap, int count, int n, int nn, int cap, const IntTables& T,
+                   double term_c, double dmax, uint32_t cycle, unsigned long long* stats, int* err) {
+    size_t smem = cap ? 0 : int_smem_bytes(nn);
+    set_smem(k_step<KIND, FAST>, smem);
+    LZB_LAUNCH((k_step<KIND, FAST>), blocks_for(count, kIntThreads), kIntThreads, smem, s, F, f, list,
+               snap, count, n, nn, cap, T, term_c, dmax, cycle, 0, stats, err);
 }
 
 template <int KIND>
-void launch_fixed(bool fast, unsigned grid, cudaStream_t s, const LevelView& F, const lzb_field& f,
-                  int n, const double* tx, const double* ty, double dmax, uint32_t cycle,
-                  unsigned long long* stats, int* err) {
+void launch_step(bool fast, cudaStream_t s, const LevelView& F, const lzb_field& f,
+                 const int32_t* list, const int32_t* snap, int count, int n, int nn, int cap,
+                 const IntTables& T, double term_c, double dmax, uint32_t cycle,
+                 unsigned long long* stats, int* err) {
     if (fast)
-        LZB_LAUNCH((k_fixed<KIND, true>), grid, 128, 0, s, F, f, n, tx, ty, dmax, cycle, stats, err);
+        launch_step_k<KIND, true>(s, F, f, list, snap, count, n, nn, cap, T, term_c, dmax, cycle, stats, err);
     else
-        LZB_LAUNCH((k_fixed<KIND, false>), grid, 128, 0, s, F, f, n, tx, ty, dmax, cycle, stats, err);
+        launch_step_k<KIND, false>(s, F, f, list, snap, count, n, nn, cap, T, term_c, dmax, cycle, stats, err);
+}
+
+template <int KIND, bool FAST>
+void launch_fixed_k(cudaStream_t s, const LevelView& F, const lzb_field& f, int n, const IntTables& T,
+                    double dmax, uint32_t cycle, unsigned long long* stats, int* err) {
+    size_t smem = int_smem_bytes(n);
+    set_smem(k_fixed<KIND, FAST>, smem);
+    LZB_LAUNCH((k_fixed<KIND, FAST>), blocks_for(static_cast<int64_t>(F.N) * F.N, kIntThreads),
+               kIntThreads, smem, s, F, f, n, T, dmax, cycle, stats, err);
+}
+
+template <int KIND>
+void launch_fixed(bool fast, cudaStream_t s, const LevelView& F, const lzb_field& f, int n,
+                  const IntTables& T, double dmax, uint32_t cycle, unsigned long long* stats, int* err) {
+    if (fast) launch_fixed_k<KIND, true>(s, F, f, n, T, dmax, cycle, stats, err);
+    else launch_fixed_k<KIND, false>(s, F, f, n, T, dmax, cycle, stats, err);
 }
 
 }  // namespace
@@ -980,14 +1097,9 @@ public:
         return nn;
     }
 
-    void ensure_tables(int nn) {
-        size_t need = static_cast<size_t>(L_[D_].N) * nn * kTab;
-        if (tx_.n < need) {
-            LZB_CUDA(cudaStreamSynchronize(s_));
-            tx_.alloc(need);
-            ty_.alloc(need);
-        }
-        build_axis_tables(d_.field, L_[D_].N, L_[D_].h, nn, tx_.p, ty_.p, s_);
+    void ensure_tables(int nn) {  // per-n tables; the field and level are fixed per grid
+        if (tables_.n == nn && tables_.N == L_[D_].N) return;
+        tables_.build(d_.field, L_[D_].N, L_[D_].h, nn, s_);
     }
 
     // One batched round of adaptive steps over the selected leaves; returns
@@ -1006,7 +1118,6 @@ public:
         if (count == 0) return 0;
         if (hhist_[kNHist - 1] && selector != 1)
             throw Error(LZB_ERR_RESOURCE, "sub-sample count beyond 4095 per axis");
-        unsigned grid = blocks_for(count, 128);
         unsigned long long* stats = res_.p->s;
         if (hhist_[0])
             LZB_LAUNCH(k_bottom, blocks_for(count, kThreads), kThreads, 0, s_, F, d_.field, list_.p,
@@ -1017,13 +1128,13 @@ public:
             int nn = next_n(n);
             if (!cap) ensure_tables(nn);
             bool fast = d_.integration == LZB_INTEGRATE_FAST;
-            const double *tx = tx_.p, *ty = ty_.p;
+            const IntTables T = tables_.view();
             switch (d_.field.kind) {
-                case LZB_FIELD_THETA: launch_step<LZB_FIELD_THETA>(fast, grid, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, tx, ty, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
-                case LZB_FIELD_QUADRANT: launch_step<LZB_FIELD_QUADRANT>(fast, grid, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, tx, ty, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
-                case LZB_FIELD_CHECKER: launch_step<LZB_FIELD_CHECKER>(fast, grid, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, tx, ty, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
-                case LZB_FIELD_SINUSOID: launch_step<LZB_FIELD_SINUSOID>(fast, grid, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, tx, ty, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
-                default: launch_step<LZB_FIELD_CONSTANT>(fast, grid, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, tx, ty, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+                case LZB_FIELD_THETA: launch_step<LZB_FIELD_THETA>(fast, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, T, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+                case LZB_FIELD_QUADRANT: launch_step<LZB_FIELD_QUADRANT>(fast, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, T, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+                case LZB_FIELD_CHECKER: launch_step<LZB_FIELD_CHECKER>(fast, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, T, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+                case LZB_FIELD_SINUSOID: launch_step<LZB_FIELD_SINUSOID>(fast, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, T, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+                default: launch_step<LZB_FIELD_CONSTANT>(fast, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, T, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
             }
         }
         if (complete_tasks)
@@ -1040,22 +1151,26 @@ public:
         if (n < 1) throw Error(LZB_ERR_INVALID, "n must be >= 1");
         ensure_tables(n);
         LevelView F = V(D_);
-        unsigned grid = blocks_for(leaves_, 128);
         bool fast = d_.integration == LZB_INTEGRATE_FAST;
         unsigned long long* stats = res_.p->s;
         switch (d_.field.kind) {
-            case LZB_FIELD_THETA: launch_fixed<LZB_FIELD_THETA>(fast, grid, s_, F, d_.field, n, tx_.p, ty_.p, d_.delta_max, cycle_, stats, ctx_->err.p); break;
-            case LZB_FIELD_QUADRANT: launch_fixed<LZB_FIELD_QUADRANT>(fast, grid, s_, F, d_.field, n, tx_.p, ty_.p, d_.delta_max, cycle_, stats, ctx_->err.p); break;
-            case LZB_FIELD_CHECKER: launch_fixed<LZB_FIELD_CHECKER>(fast, grid, s_, F, d_.field, n, tx_.p, ty_.p, d_.delta_max, cycle_, stats, ctx_->err.p); break;
-            case LZB_FIELD_SINUSOID: launch_fixed<LZB_FIELD_SINUSOID>(fast, grid, s_, F, d_.field, n, tx_.p, ty_.p, d_.delta_max, cycle_, stats, ctx_->err.p); break;
-            default: launch_fixed<LZB_FIELD_CONSTANT>(fast, grid, s_, F, d_.field, n, tx_.p, ty_.p, d_.delta_max, cycle_, stats, ctx_->err.p); break;
+            case LZB_FIELD_THETA: launch_fixed<LZB_FIELD_THETA>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p); break;
+            case LZB_FIELD_QUADRANT: launch_fixed<LZB_FIELD_QUADRANT>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p); break;
+            case LZB_FIELD_CHECKER: launch_fixed<LZB_FIELD_CHECKER>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p); break;
+            case LZB_FIELD_SINUSOID: launch_fixed<LZB_FIELD_SINUSOID>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p); break;
+            default: launch_fixed<LZB_FIELD_CONSTANT>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p); break;
         }
     }
 
     void coarse_pass() {  // pre-order semantics: coarse levels first, each reads l+1
-        for (int l = 0; l < D_; ++l)
-            LZB_LAUNCH(k_coarse, blocks_for(L_[l].nc, 64), 64, 0, s_, V(l), V(l + 1), d_.field,
-                       d_.transfer == LZB_BOXMG ? 1 : 0, d_.delta_max, cycle_, res_.p->s, ctx_->err.p);
+        for (int l = 0; l < D_; ++l) {
+            if (d_.transfer == LZB_BOXMG)
+                LZB_LAUNCH(k_coarse, blocks_for(L_[l].nc, 64), 64, 0, s_, V(l), V(l + 1), d_.field, 1,
+                           d_.delta_max, cycle_, res_.p->s, ctx_->err.p);
+            else
+                LZB_LAUNCH(k_coarse_geo, blocks_for(L_[l].nc, kCoarseThreads), kCoarseThreads, 0, s_,
+                           V(l), V(l + 1), d_.field, d_.delta_max, cycle_, res_.p->s, ctx_->err.p);
+        }
     }
 
     void pool_begin_cycle() {  // TaskPool::begin_cycle, workers = 1 (scheduler.cpp:88-111)
@@ -1490,7 +1605,7 @@ private:
     DevBuf<double> partial_;
     DevBuf<Result> res_;
     DevBuf<long long> keys_;
-    DevBuf<double> tx_, ty_;
+    TableSet tables_;
     Result* hres_ = nullptr;
     unsigned* hhist_ = nullptr;
     SlotTable slots_{};

@@ -1,29 +1,41 @@
 // integrate.cuh — K1: per-cell element-matrix integration with n x n eps
 // sub-samples (integrate_element, element.hpp:36-49), FP64.
 //
-// Per-axis tables: for a regular level (N cells per axis, width h) and a
-// sampling n, everything the inner loop needs that depends on one axis only
-// is tabulated once per (cell column/row, sub-index):
-//   tab[(c*n + i)*kTab + 0] = field part of eps at x_i = c*h + ((i+0.5)/n)*h
-//   tab[... + 1..4]         = len_i, S0_i, S1_i, S2_i (element.cpp:8-32 on [i/n,(i+1)/n])
-// The sample coordinate and every tabulated value are computed with the
-// reference expression (no FMA in this TU), so a table lookup returns the same
-// bits the reference recomputes per sample.
+// What depends on the cell and what does not:
+//   * K_sub(i,j) = reference_subcell_stiffness(i/n,(i+1)/n,j/n,(j+1)/n) depends
+//     on (n,i,j) only: tabulated ONCE per n (ktab, 9 distinct values per (i,j)
+//     + 1 pad double, element.cpp:19-32 arithmetic) and staged tile by tile in
+//     shared memory, read as broadcast LDS.128 by every thread of the block;
+//   * the per-axis seg values (len, S0, S1, S2) of sub-interval i: per n (seg);
+//   * the eps field parts: x part per (cell column, i), y part per (cell row, j)
+//     (fx, fy), computed with the reference's sample-coordinate expression
+//     x0 + ((i+0.5)*inv)*h (element.hpp:44) and the field's expression tree.
+// A table lookup returns the very bits the reference recomputes per sample.
 //
-// EXACT: i-major, j-minor sequential accumulation of fl(e*K) into 9 distinct
-//        accumulators (the 16 entries of K_sub take 9 values) — bit-identical
-//        to the reference.
-// FAST:  separable form with explicit FMAs: per row i, s_k = sum_j e_ij S_k(j)
-//        and t = sum_j e_ij len_j, then U_k += len_i s_k, V_k += S_k(i) t;
-//        entries are +-U +-V. 4 FMA per sub-sample instead of 9 mul + 9 add
-//        + 9 add + 6 mul; within 1e-12 relative of EXACT (tests).
+// EXACT: i-major, j-minor sequential accumulation of fl(K*e) into the 9
+//        distinct accumulators (out.m += e*K, element.hpp:45): 2 + 9 + 9 DP
+//        ops per sub-sample, no FMA — bit-identical to the reference.
+// FAST:  separable form with explicit FMAs: per row i, s_k = sum_j e_ij S_k(j),
+//        t = sum_j e_ij len_j; then U_k += len_i s_k, V_k += S_k(i) t; entries
+//        are +-U +-V. 5 FMA per sub-sample; within 1e-12 relative of EXACT.
 #pragma once
 
 #include "device.cuh"
 
 namespace lzb {
 
-constexpr int kTab = 5;
+constexpr int kKs = 10;          // doubles per K_sub(i,j) table entry (9 + pad, 16 B aligned)
+constexpr int kSeg = 4;          // len, S0, S1, S2
+constexpr int kIntThreads = 256; // block size of the table-driven integration kernels
+constexpr int kKTileBytes = 40 * 1024;
+
+struct IntTables {
+    const double* fx;    // [N][n] x field parts
+    const double* fy;    // [N][n] y field parts
+    const double* seg;   // [n][4]
+    const double* ktab;  // [n][n][10]
+    int n;
+};
 
 template <int KIND>
 __device__ __forceinline__ double combine_k(double xp, double yp, double value, double eps_low,
@@ -39,81 +51,120 @@ __device__ __forceinline__ double combine_k(double xp, double yp, double value, 
     }
 }
 
-// One axis table: thread per (c, i); axis 0 = x part, 1 = y part.
-__global__ void k_axis_table(lzb_field f, int N, double h, int n, int axis, double* tab);
+// Shared-memory layout used by the table-driven kernels (dynamic smem):
+//   [0, 64)                checker table
+//   [64, 64 + 4n)          seg table
+//   [64 + 4n, ...)         K_sub tile: rows i0..i0+TI-1, n*10 doubles per row
+__host__ __device__ inline int ktile_rows(int n) {
+    int r = kKTileBytes / (n * kKs * 8);
+    return r < 1 ? 1 : (r > n ? n : r);
+}
+__host__ inline size_t int_smem_bytes(int n) {
+    return (64 + static_cast<size_t>(kSeg) * n + static_cast<size_t>(ktile_rows(n)) * n * kKs) * 8;
+}
 
-template <int KIND>
-__device__ __forceinline__ void integrate_exact_tab(const double* __restrict__ tx,
-                                                    const double* __restrict__ ty, int n,
-                                                    double value, double eps_low, int blocks,
-                                                    const double* table, double* out16) {
+__device__ inline void stage_common(double* sm, const lzb_field& f, const IntTables& T) {
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) sm[i] = f.table[i];
+    for (int i = threadIdx.x; i < kSeg * T.n; i += blockDim.x) sm[64 + i] = T.seg[i];
+}
+
+// Block-cooperative integration: every thread of the block must call it (the
+// K_sub tiles are staged with __syncthreads); `active` threads accumulate the
+// cell whose field parts are fxc[0..n) (its column) and fyc[0..n) (its row).
+template <int KIND, bool FAST>
+__device__ __forceinline__ void integrate_block(bool active, const lzb_field& f, const IntTables& T,
+                                                const double* __restrict__ fxc,
+                                                const double* __restrict__ fyc, double* sm,
+                                                double* out16) {
+    const int n = T.n;
+    const double* s_tab = sm;
+    const double* s_seg = sm + 64;
+    double* s_k = sm + 64 + kSeg * n;
+    const double value = f.value, eps_low = f.eps_low;
+    const int blocks = f.blocks;
     double a[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int i = 0; i < n; ++i) {
-        const double* xi = tx + i * kTab;
-        const double xp = xi[0];
-        const AxisSeg X{xi[1], xi[2], xi[3], xi[4]};
-        for (int j = 0; j < n; ++j) {
-            const double* yj = ty + j * kTab;
-            const double e = combine_k<KIND>(xp, yj[0], value, eps_low, blocks, table);
-            const AxisSeg Y{yj[1], yj[2], yj[3], yj[4]};
-            const K9 k = ksub(X, Y);
-            // out.m += e * K  (element.hpp:45; Mat4 operator* computes K*e)
-            a[0] = a[0] + k.k00 * e;
-            a[1] = a[1] + k.k11 * e;
-            a[2] = a[2] + k.k22 * e;
-            a[3] = a[3] + k.k33 * e;
-            a[4] = a[4] + k.k01 * e;
-            a[5] = a[5] + k.k23 * e;
-            a[6] = a[6] + k.k02 * e;
-            a[7] = a[7] + k.k13 * e;
-            a[8] = a[8] + k.k03 * e;
+    double U0 = 0, U1 = 0, U2 = 0, V0 = 0, V1 = 0, V2 = 0;
+    if (FAST) {
+        __syncthreads();  // seg staged by the caller
+        if (active) {
+            for (int i = 0; i < n; ++i) {
+                const double xp = fxc[i];
+                double s0 = 0, s1 = 0, s2 = 0, t = 0;
+#pragma unroll 4
+                for (int j = 0; j < n; ++j) {
+                    double e;
+                    if constexpr (KIND == LZB_FIELD_THETA || KIND == LZB_FIELD_SINUSOID)
+                        e = __fma_rn(xp, fyc[j], 1.0);
+                    else
+                        e = combine_k<KIND>(xp, fyc[j], value, eps_low, blocks, s_tab);
+                    const double2 q0 = reinterpret_cast<const double2*>(s_seg)[2 * j];
+                    const double2 q1 = reinterpret_cast<const double2*>(s_seg)[2 * j + 1];
+                    t = __fma_rn(e, q0.x, t);
+                    s0 = __fma_rn(e, q0.y, s0);
+                    s1 = __fma_rn(e, q1.x, s1);
+                    s2 = __fma_rn(e, q1.y, s2);
+                }
+                const double2 p0 = reinterpret_cast<const double2*>(s_seg)[2 * i];
+                const double2 p1 = reinterpret_cast<const double2*>(s_seg)[2 * i + 1];
+                U0 = __fma_rn(p0.x, s0, U0);
+                U1 = __fma_rn(p0.x, s1, U1);
+                U2 = __fma_rn(p0.x, s2, U2);
+                V0 = __fma_rn(p0.y, t, V0);
+                V1 = __fma_rn(p1.x, t, V1);
+                V2 = __fma_rn(p1.y, t, V2);
+            }
+        }
+        a[0] = U0 + V0;
+        a[1] = U0 + V2;
+        a[2] = U2 + V0;
+        a[3] = U2 + V2;
+        a[4] = V1 - U0;
+        a[5] = V1 - U2;
+        a[6] = U1 - V0;
+        a[7] = U1 - V2;
+        a[8] = -(U1 + V1);
+    } else {
+        const int TI = ktile_rows(n);
+        for (int i0 = 0; i0 < n; i0 += TI) {
+            const int rows = (n - i0) < TI ? (n - i0) : TI;
+            __syncthreads();
+            {   // stage K_sub rows [i0, i0+rows) (contiguous in ktab), 16-byte vectors
+                const double2* src = reinterpret_cast<const double2*>(T.ktab + static_cast<size_t>(i0) * n * kKs);
+                double2* dst = reinterpret_cast<double2*>(s_k);
+                const int nvec = rows * n * kKs / 2;
+                for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = src[v];
+            }
+            __syncthreads();
+            if (active) {
+                for (int ii = 0; ii < rows; ++ii) {
+                    const double xp = fxc[i0 + ii];
+                    const double2* kp = reinterpret_cast<const double2*>(s_k + static_cast<size_t>(ii) * n * kKs);
+#pragma unroll 2
+                    for (int j = 0; j < n; ++j, kp += kKs / 2) {
+                        const double e = combine_k<KIND>(xp, fyc[j], value, eps_low, blocks, s_tab);
+                        const double2 k0 = kp[0], k1 = kp[1], k2 = kp[2], k3 = kp[3], k4 = kp[4];
+                        // out.m += e * K   (Mat4 operator* rounds K*e, then +=)
+                        a[0] = a[0] + k0.x * e;
+                        a[1] = a[1] + k0.y * e;
+                        a[2] = a[2] + k1.x * e;
+                        a[3] = a[3] + k1.y * e;
+                        a[4] = a[4] + k2.x * e;
+                        a[5] = a[5] + k2.y * e;
+                        a[6] = a[6] + k3.x * e;
+                        a[7] = a[7] + k3.y * e;
+                        a[8] = a[8] + k4.x * e;
+                    }
+                }
+            }
         }
     }
     k9_expand(a, out16);
 }
 
-template <int KIND>
-__device__ __forceinline__ void integrate_fast_tab(const double* __restrict__ tx,
-                                                   const double* __restrict__ ty, int n,
-                                                   double value, double eps_low, int blocks,
-                                                   const double* table, double* out16) {
-    double U0 = 0, U1 = 0, U2 = 0, V0 = 0, V1 = 0, V2 = 0;
-    for (int i = 0; i < n; ++i) {
-        const double* xi = tx + i * kTab;
-        const double xp = xi[0];
-        double s0 = 0, s1 = 0, s2 = 0, t = 0;
-        for (int j = 0; j < n; ++j) {
-            const double* yj = ty + j * kTab;
-            double e;
-            if constexpr (KIND == LZB_FIELD_THETA || KIND == LZB_FIELD_SINUSOID)
-                e = __fma_rn(xp, yj[0], 1.0);
-            else
-                e = combine_k<KIND>(xp, yj[0], value, eps_low, blocks, table);
-            t = __fma_rn(e, yj[1], t);
-            s0 = __fma_rn(e, yj[2], s0);
-            s1 = __fma_rn(e, yj[3], s1);
-            s2 = __fma_rn(e, yj[4], s2);
-        }
-        U0 = __fma_rn(xi[1], s0, U0);
-        U1 = __fma_rn(xi[1], s1, U1);
-        U2 = __fma_rn(xi[1], s2, U2);
-        V0 = __fma_rn(xi[2], t, V0);
-        V1 = __fma_rn(xi[3], t, V1);
-        V2 = __fma_rn(xi[4], t, V2);
-    }
-    // same sign pattern as ksub with A_k = U_k, B_k = V_k
-    double a[9];
-    a[0] = U0 + V0;
-    a[1] = U0 + V2;
-    a[2] = U2 + V0;
-    a[3] = U2 + V2;
-    a[4] = V1 - U0;
-    a[5] = V1 - U2;
-    a[6] = U1 - V0;
-    a[7] = U1 - V2;
-    a[8] = -(U1 + V1);
-    k9_expand(a, out16);
-}
+// Table builders (runtime.cu).
+__global__ void k_field_parts(lzb_field f, int N, double h, int n, int axis, double* out);
+__global__ void k_seg_table(int n, double* seg);
+__global__ void k_ksub_table(int n, double* ktab);
 
 // Arbitrary CellBox (x0, y0, h) at n: axis parts recomputed per sample with
 // the reference arithmetic (per-cell compatibility path, no tables).

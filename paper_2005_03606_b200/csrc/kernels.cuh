@@ -2,6 +2,7 @@
 #pragma once
 
 #include "device.cuh"
+#include "engine.hpp"
 #include "integrate.cuh"
 
 namespace lzb {
@@ -13,6 +14,16 @@ __constant__ double c_kunit[16];
 __constant__ double c_geo[64];
 
 void upload_constants();
+
+// Per-n integration tables (integrate.cuh), rebuilt on demand.
+struct TableSet {
+    DevBuf<double> fx, fy, seg, ktab;
+    int n = 0, N = 0;
+    void build(const lzb_field& f, int N, double h, int n, cudaStream_t s);
+    IntTables view() const { return IntTables{fx.p, fy.p, seg.p, ktab.p, n}; }
+};
+template <typename K>
+void set_smem(K kernel, size_t bytes);
 void host_kunit(double* out16);
 void host_geo(double* out64);
 

@@ -81,26 +81,64 @@ void check_device_flag(lzb_ctx* c, cudaStream_t s) {
     }
 }
 
-// ------------------------------------------------------------ axis tables
-__global__ void k_axis_table(lzb_field f, int N, double h, int n, int axis, double* tab) {
+// ------------------------------------------------------------ tables
+__global__ void k_field_parts(lzb_field f, int N, double h, int n, int axis, double* out) {
     int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (t >= static_cast<int64_t>(N) * n) return;
     int c = static_cast<int>(t / n), i = static_cast<int>(t % n);
     double inv = 1.0 / n;
     double x0 = c * h;                       // cell_box, element.hpp:29-32
     double x = x0 + (i + 0.5) * inv * h;     // element.hpp:44
-    AxisSeg s = axis_seg(i, inv);
-    double* o = tab + t * kTab;
-    o[0] = axis == 0 ? field_xpart(f, x) : field_ypart(f, x);
-    o[1] = s.len;
-    o[2] = s.s0;
-    o[3] = s.s1;
-    o[4] = s.s2;
+    out[t] = axis == 0 ? field_xpart(f, x) : field_ypart(f, x);
 }
 
-// ------------------------------------------------------- generic boxes
-// Arbitrary CellBox per cell: axis parts are recomputed per sample (the
-// reference's exact arithmetic); used by the per-cell compatibility API.
+__global__ void k_seg_table(int n, double* seg) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    AxisSeg s = axis_seg(i, 1.0 / n);
+    seg[4 * i + 0] = s.len;
+    seg[4 * i + 1] = s.s0;
+    seg[4 * i + 2] = s.s1;
+    seg[4 * i + 3] = s.s2;
+}
+
+__global__ void k_ksub_table(int n, double* ktab) {
+    int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= static_cast<int64_t>(n) * n) return;
+    int i = static_cast<int>(t / n), j = static_cast<int>(t % n);
+    double inv = 1.0 / n;
+    K9 k = ksub(axis_seg(i, inv), axis_seg(j, inv));  // element.cpp:19-32, reference order
+    double* o = ktab + t * kKs;
+    o[0] = k.k00; o[1] = k.k11; o[2] = k.k22; o[3] = k.k33; o[4] = k.k01;
+    o[5] = k.k23; o[6] = k.k02; o[7] = k.k13; o[8] = k.k03; o[9] = 0.0;
+}
+
+void TableSet::build(const lzb_field& f, int N_, double h, int n_, cudaStream_t s) {
+    size_t nf = static_cast<size_t>(N_) * n_;
+    if (fx.n < nf) {
+        LZB_CUDA(cudaStreamSynchronize(s));
+        fx.alloc(nf);
+        fy.alloc(nf);
+    }
+    if (seg.n < static_cast<size_t>(kSeg) * n_) {
+        LZB_CUDA(cudaStreamSynchronize(s));
+        seg.alloc(static_cast<size_t>(kSeg) * n_);
+    }
+    if (ktab.n < static_cast<size_t>(n_) * n_ * kKs) {
+        LZB_CUDA(cudaStreamSynchronize(s));
+        ktab.alloc(static_cast<size_t>(n_) * n_ * kKs);
+    }
+    unsigned g = blocks_for(static_cast<int64_t>(nf), 256);
+    LZB_LAUNCH(k_field_parts, g, 256, 0, s, f, N_, h, n_, 0, fx.p);
+    LZB_LAUNCH(k_field_parts, g, 256, 0, s, f, N_, h, n_, 1, fy.p);
+    LZB_LAUNCH(k_seg_table, blocks_for(n_, 128), 128, 0, s, n_, seg.p);
+    LZB_LAUNCH(k_ksub_table, blocks_for(static_cast<int64_t>(n_) * n_, 256), 256, 0, s, n_, ktab.p);
+    n = n_;
+    N = N_;
+}
+
+// Arbitrary CellBox per cell: axis parts recomputed per sample (the
+// reference's exact arithmetic); the per-cell compatibility API.
 __global__ void k_integrate_boxes(lzb_field f, int64_t ncells, const double* __restrict__ x0,
                                   const double* __restrict__ y0, const double* __restrict__ hh,
                                   const int32_t* __restrict__ nn, double* __restrict__ out,
@@ -110,43 +148,49 @@ __global__ void k_integrate_boxes(lzb_field f, int64_t ncells, const double* __r
     integrate_cell(f, x0[c], y0[c], hh[c], nn[c], fast, out + 16 * c);
 }
 
-// Whole regular level at one n, from axis tables.
+// Whole regular level at one n.
 template <int KIND, bool FAST>
-__global__ void k_integrate_level(lzb_field f, int N, int n, const double* __restrict__ tx,
-                                  const double* __restrict__ ty, double* __restrict__ out) {
-    __shared__ double s_table[64];
-    if (KIND == LZB_FIELD_CHECKER)
-        for (int i = threadIdx.x; i < 64; i += blockDim.x) s_table[i] = f.table[i];
-    __syncthreads();
+__global__ void __launch_bounds__(kIntThreads) k_integrate_level(lzb_field f, int N, IntTables T,
+                                                                 double* __restrict__ out) {
+    extern __shared__ double sm[];
+    stage_common(sm, f, T);
     int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (c >= static_cast<int64_t>(N) * N) return;
-    int cx = static_cast<int>(c % N), cy = static_cast<int>(c / N);
-    const double* txc = tx + static_cast<int64_t>(cx) * n * kTab;
-    const double* tyc = ty + static_cast<int64_t>(cy) * n * kTab;
-    if (FAST)
-        integrate_fast_tab<KIND>(txc, tyc, n, f.value, f.eps_low, f.blocks, s_table, out + 16 * c);
-    else
-        integrate_exact_tab<KIND>(txc, tyc, n, f.value, f.eps_low, f.blocks, s_table, out + 16 * c);
-}
-
-template <bool FAST>
-void launch_integrate_level(const lzb_field& f, int N, int n, const double* tx, const double* ty,
-                            double* out, cudaStream_t s) {
-    unsigned grid = blocks_for(static_cast<int64_t>(N) * N, 128);
-    switch (f.kind) {
-        case LZB_FIELD_THETA: LZB_LAUNCH((k_integrate_level<LZB_FIELD_THETA, FAST>), grid, 128, 0, s, f, N, n, tx, ty, out); break;
-        case LZB_FIELD_QUADRANT: LZB_LAUNCH((k_integrate_level<LZB_FIELD_QUADRANT, FAST>), grid, 128, 0, s, f, N, n, tx, ty, out); break;
-        case LZB_FIELD_CHECKER: LZB_LAUNCH((k_integrate_level<LZB_FIELD_CHECKER, FAST>), grid, 128, 0, s, f, N, n, tx, ty, out); break;
-        case LZB_FIELD_SINUSOID: LZB_LAUNCH((k_integrate_level<LZB_FIELD_SINUSOID, FAST>), grid, 128, 0, s, f, N, n, tx, ty, out); break;
-        default: LZB_LAUNCH((k_integrate_level<LZB_FIELD_CONSTANT, FAST>), grid, 128, 0, s, f, N, n, tx, ty, out); break;
+    bool active = c < static_cast<int64_t>(N) * N;
+    int cx = active ? static_cast<int>(c % N) : 0, cy = active ? static_cast<int>(c / N) : 0;
+    double m[16];
+    integrate_block<KIND, FAST>(active, f, T, T.fx + static_cast<int64_t>(cx) * T.n,
+                                T.fy + static_cast<int64_t>(cy) * T.n, sm, m);
+    if (active) {
+        double2* o = reinterpret_cast<double2*>(out + 16 * c);
+        for (int k = 0; k < 8; ++k) o[k] = make_double2(m[2 * k], m[2 * k + 1]);
     }
 }
 
-void build_axis_tables(const lzb_field& f, int N, double h, int n, double* tx, double* ty,
-                       cudaStream_t s) {
-    unsigned grid = blocks_for(static_cast<int64_t>(N) * n, 256);
-    LZB_LAUNCH(k_axis_table, grid, 256, 0, s, f, N, h, n, 0, tx);
-    LZB_LAUNCH(k_axis_table, grid, 256, 0, s, f, N, h, n, 1, ty);
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024)
+        LZB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(bytes)));
+}
+
+template <int KIND, bool FAST>
+void launch_level_k(const lzb_field& f, int N, const IntTables& T, double* out, cudaStream_t s) {
+    size_t smem = int_smem_bytes(T.n);
+    set_smem(k_integrate_level<KIND, FAST>, smem);
+    LZB_LAUNCH((k_integrate_level<KIND, FAST>), blocks_for(static_cast<int64_t>(N) * N, kIntThreads),
+               kIntThreads, smem, s, f, N, T, out);
+}
+
+template <bool FAST>
+void launch_integrate_level(const lzb_field& f, int N, const IntTables& T, double* out,
+                            cudaStream_t s) {
+    switch (f.kind) {
+        case LZB_FIELD_THETA: launch_level_k<LZB_FIELD_THETA, FAST>(f, N, T, out, s); break;
+        case LZB_FIELD_QUADRANT: launch_level_k<LZB_FIELD_QUADRANT, FAST>(f, N, T, out, s); break;
+        case LZB_FIELD_CHECKER: launch_level_k<LZB_FIELD_CHECKER, FAST>(f, N, T, out, s); break;
+        case LZB_FIELD_SINUSOID: launch_level_k<LZB_FIELD_SINUSOID, FAST>(f, N, T, out, s); break;
+        default: launch_level_k<LZB_FIELD_CONSTANT, FAST>(f, N, T, out, s); break;
+    }
 }
 
 // FP64 peak probe: 8 independent DFMA chains per thread, one CTA per SM slot.
@@ -416,12 +460,12 @@ int lzb_integrate_level_dev(lzb_ctx* ctx, const lzb_field* eps, int level, int n
         for (int i = 0; i < level; ++i) N *= 3;
         double h = std::pow(1.0 / 3, level);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        DevBuf<double> tx(static_cast<size_t>(N) * n * kTab), ty(static_cast<size_t>(N) * n * kTab);
-        build_axis_tables(*eps, N, h, n, tx.p, ty.p, s);
+        TableSet T;
+        T.build(*eps, N, h, n, s);
         if (integration == LZB_INTEGRATE_FAST)
-            launch_integrate_level<true>(*eps, N, n, tx.p, ty.p, out, s);
+            launch_integrate_level<true>(*eps, N, T.view(), out, s);
         else
-            launch_integrate_level<false>(*eps, N, n, tx.p, ty.p, out, s);
+            launch_integrate_level<false>(*eps, N, T.view(), out, s);
         LZB_CUDA(cudaStreamSynchronize(s));  // tables are freed on return
     });
 }
@@ -434,13 +478,13 @@ int lzb_integrate_level(lzb_ctx* ctx, const lzb_field* eps, int level, int n, do
         for (int i = 0; i < level; ++i) N *= 3;
         double h = std::pow(1.0 / 3, level);
         cudaStream_t s = ctx->solve;
-        DevBuf<double> tx(static_cast<size_t>(N) * n * kTab), ty(static_cast<size_t>(N) * n * kTab);
         DevBuf<double> out(static_cast<size_t>(N) * N * 16);
-        build_axis_tables(*eps, N, h, n, tx.p, ty.p, s);
+        TableSet T;
+        T.build(*eps, N, h, n, s);
         if (integration == LZB_INTEGRATE_FAST)
-            launch_integrate_level<true>(*eps, N, n, tx.p, ty.p, out.p, s);
+            launch_integrate_level<true>(*eps, N, T.view(), out.p, s);
         else
-            launch_integrate_level<false>(*eps, N, n, tx.p, ty.p, out.p, s);
+            launch_integrate_level<false>(*eps, N, T.view(), out.p, s);
         LZB_CUDA(cudaMemcpyAsync(host_out, out.p, out.bytes(), cudaMemcpyDeviceToHost, s));
         LZB_CUDA(cudaStreamSynchronize(s));
     });
