@@ -274,16 +274,18 @@ def run_ours(args, world, rank, local):
 
     # end to end through the C-ABI: assemble, then the compressed LZMG stream to a host buffer
     img = g.stream_image()
+    host = torch.empty(len(img) + (1 << 20), dtype=torch.uint8, pin_memory=True).numpy()
 
     def e2e_step():
         g.assemble_fixed(P)
-        g.stream_image()
+        g.stream_image(host)
 
     te = timed_steps(e2e_step, args.steps)
     te = max_over_ranks(te, world)
     e2e = {"value": world * SAMPLES_PER_STEP * args.steps / te, "unit": "sub-samples/s",
-           "h2d_bytes_per_step": 560, "d2h_bytes_per_step": len(img) + 8 * (sum(3 ** (2 * l) for l in range(7))),
-           "path": "lzb_grid_assemble_fixed + lzb_grid_stream_image (LZMG bytes into host memory)"}
+           "h2d_bytes_per_step": 560, "d2h_bytes_per_step": len(img) + 16,
+           "ms_per_step": 1e3 * te / args.steps,
+           "path": "lzb_grid_assemble_fixed + lzb_grid_stream_image into pinned host memory (LZMG bytes)"}
 
     if rank != 0:
         return

@@ -427,8 +427,13 @@ class Grid:
         _check(lib().lzb_grid_stats(self.h, C.byref(s)))
         return s
 
-    def stream_image(self) -> bytes:
+    def stream_image(self, out: np.ndarray | None = None):
+        """CellStream::save byte image. With `out` (a uint8 host array, ideally
+        pinned) the image is copied straight into it and its size returned."""
         size = C.c_int64()
+        if out is not None:
+            _check(lib().lzb_grid_stream_image(self.h, _ptr(out), out.size, C.byref(size)))
+            return size.value
         _check(lib().lzb_grid_stream_image(self.h, None, 0, C.byref(size)))
         buf = np.zeros(size.value, np.uint8)
         _check(lib().lzb_grid_stream_image(self.h, _ptr(buf), buf.size, C.byref(size)))

@@ -21,6 +21,8 @@
 #include <fstream>
 #include <functional>
 
+#include <cub/device/device_scan.cuh>
+
 #include "engine.hpp"
 #include "kernels.cuh"
 
@@ -111,27 +113,90 @@ __device__ inline bool publish_leaf(const LevelView& F, int c, const double* m, 
 }
 
 // -------------------------------------------------------------- assembly
-__global__ void k_compact(LevelView F, int selector, int32_t* list, int32_t* snap, int* count,
-                          unsigned* hist, const long long* keys, long long key_limit) {
+// Order-preserving compaction of the selected leaves (ascending cell index,
+// so a block of list entries covers few cell rows): count per block, scan,
+// scatter. selector: 0 unconverged, 1 tasks (p2 set, FIFO key <= limit), 2 bottom.
+__device__ inline bool selected(const LevelView& F, int64_t c, int selector, const long long* keys,
+                                long long key_limit, int32_t& p1) {
+    p1 = F.p1[c];
+    if (selector == 0) return p1 != LZB_P1_TOP;
+    if (selector == 1) return F.p2[c] != 0 && (!keys || keys[c] <= key_limit);  // a task on a top cell still completes
+    return p1 == LZB_P1_BOTTOM;
+}
+
+constexpr int kCompactThreads = 256;
+
+__global__ void k_compact_count(LevelView F, int selector, const long long* keys, long long key_limit,
+                                int* block_counts) {
+    __shared__ int warp_n[kCompactThreads / 32];
     int64_t c = gtid();
-    int64_t nc = static_cast<int64_t>(F.N) * F.N;
-    bool take = false;
-    int32_t p1 = 0;
-    if (c < nc) {
-        p1 = F.p1[c];
-        if (selector == 0) take = p1 != LZB_P1_TOP;                        // unconverged
-        else if (selector == 1) take = F.p2[c] != 0 && (!keys || keys[c] <= key_limit);  // tasks
-        else take = p1 == LZB_P1_BOTTOM;                                   // bottom
-        if (p1 == LZB_P1_TOP) take = take && selector == 1;  // a task on a top cell still completes
-    }
+    int32_t p1;
+    bool take = c < static_cast<int64_t>(F.N) * F.N && selected(F, c, selector, keys, key_limit, p1);
     unsigned mask = __ballot_sync(0xffffffffu, take);
-    if (!mask) return;
-    int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
-    int base = 0;
-    if (lane == leader) base = atomicAdd(count, __popc(mask));
-    base = __shfl_sync(0xffffffffu, base, leader);
+    if ((threadIdx.x & 31) == 0) warp_n[threadIdx.x >> 5] = __popc(mask);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int w = 0; w < kCompactThreads / 32; ++w) s += warp_n[w];
+        block_counts[blockIdx.x] = s;
+    }
+}
+
+// Exclusive scan of the block counts in one CTA; total into *count.
+__global__ void k_compact_scan(int* block_counts, int nblocks, int* count) {
+    __shared__ int carry;
+    __shared__ int warp_sum[32];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < nblocks; base += blockDim.x) {
+        int i = base + threadIdx.x;
+        int v = i < nblocks ? block_counts[i] : 0;
+        int x = v;  // inclusive warp scan
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, x, o);
+            if ((threadIdx.x & 31) >= o) x += y;
+        }
+        if ((threadIdx.x & 31) == 31) warp_sum[threadIdx.x >> 5] = x;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            int w = threadIdx.x < (blockDim.x >> 5) ? warp_sum[threadIdx.x] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, w, o);
+                if (threadIdx.x >= o) w += y;
+            }
+            warp_sum[threadIdx.x] = w;  // inclusive over warps
+        }
+        __syncthreads();
+        int before = (threadIdx.x >> 5) ? warp_sum[(threadIdx.x >> 5) - 1] : 0;
+        if (i < nblocks) block_counts[i] = carry + before + x - v;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += before + x;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *count = carry;
+}
+
+__global__ void k_compact_scatter(LevelView F, int selector, const long long* keys, long long key_limit,
+                                  const int* block_offsets, int32_t* list, int32_t* snap, unsigned* hist) {
+    __shared__ int warp_off[kCompactThreads / 32];
+    int64_t c = gtid();
+    int32_t p1 = 0;
+    bool take = c < static_cast<int64_t>(F.N) * F.N && selected(F, c, selector, keys, key_limit, p1);
+    unsigned mask = __ballot_sync(0xffffffffu, take);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) warp_off[w] = __popc(mask);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = block_offsets[blockIdx.x];
+        for (int k = 0; k < kCompactThreads / 32; ++k) {
+            int t = warp_off[k];
+            warp_off[k] = s;
+            s += t;
+        }
+    }
+    __syncthreads();
     if (take) {
-        int pos = base + __popc(mask & ((1u << lane) - 1));
+        int pos = warp_off[w] + __popc(mask & ((1u << lane) - 1));
         list[pos] = static_cast<int32_t>(c);
         snap[pos] = p1;
         int bin = p1 == LZB_P1_TOP ? kNHist - 1 : (p1 < kNHist - 1 ? p1 : kNHist - 1);
@@ -157,11 +222,11 @@ __global__ void k_bottom(LevelView F, lzb_field f, const int32_t* list, const in
 // publish (assembly.cpp:36-59). Fused K1 + K3: integrate, surplus,
 // choose_precision, roundtrip, store.
 template <int KIND, bool FAST>
-__global__ void __launch_bounds__(kIntThreads) k_step(LevelView F, lzb_field f, const int32_t* list,
-                                                      const int32_t* snap, int count, int n, int nn,
-                                                      int n_cap_top, IntTables T, double term_c,
-                                                      double delta_max, uint32_t cycle, int clear_p2,
-                                                      unsigned long long* stats, int* err) {
+__global__ void __launch_bounds__(kIntThreads, 3) k_step(LevelView F, lzb_field f, const int32_t* list,
+                                                         const int32_t* snap, int count, int n, int nn,
+                                                         int n_cap_top, IntTables T, double term_c,
+                                                         double delta_max, uint32_t cycle, int clear_p2,
+                                                         unsigned long long* stats, int* err) {
     extern __shared__ double sm[];
     int64_t t = gtid();
     const bool mine = t < count && snap[t] == n;
@@ -174,9 +239,15 @@ __global__ void __launch_bounds__(kIntThreads) k_step(LevelView F, lzb_field f, 
         return;
     }
     stage_common(sm, f, T);
+    // the list is in ascending cell order: the block's rows span first..last entry
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x;
+    const int64_t t1 = (t0 + blockDim.x < count ? t0 + blockDim.x : count) - 1;
+    const int row_lo = list[t0] / F.N, rows = list[t1] / F.N - row_lo + 1;
+    const double* s_fy = stage_rows(sm, T, row_lo, rows);
+    const double* fyc = s_fy ? s_fy + static_cast<int64_t>(cy - row_lo) * nn
+                             : T.fy + static_cast<int64_t>(cy) * nn;
     double fresh[16];
-    integrate_block<KIND, FAST>(mine, f, T, T.fx + static_cast<int64_t>(cx) * nn,
-                                T.fy + static_cast<int64_t>(cy) * nn, sm, fresh);
+    integrate_block<KIND, FAST>(mine, f, T, T.fx + static_cast<int64_t>(cx) * nn, fyc, sm, fresh);
     if (!mine) return;
     const double* old = F.op + 16 * static_cast<int64_t>(c);
     double denom = 0.0, dmax = 0.0;
@@ -211,17 +282,23 @@ __global__ void k_spawn(LevelView F, uint32_t cycle, long long leaf_count, long 
 
 // Fixed-p assembly: every leaf integrated at n, published, p1 = top.
 template <int KIND, bool FAST>
-__global__ void __launch_bounds__(kIntThreads) k_fixed(LevelView F, lzb_field f, int n, IntTables T,
-                                                       double delta_max, uint32_t cycle,
-                                                       unsigned long long* stats, int* err) {
+__global__ void __launch_bounds__(kIntThreads, 3) k_fixed(LevelView F, lzb_field f, int n, IntTables T,
+                                                          double delta_max, uint32_t cycle,
+                                                          unsigned long long* stats, int* err) {
     extern __shared__ double sm[];
     stage_common(sm, f, T);
     int64_t c = gtid();
-    const bool mine = c < static_cast<int64_t>(F.N) * F.N;
+    const int64_t ncell = static_cast<int64_t>(F.N) * F.N;
+    const bool mine = c < ncell;
     int cx = mine ? static_cast<int>(c % F.N) : 0, cy = mine ? static_cast<int>(c / F.N) : 0;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * blockDim.x;
+    const int64_t c1 = (c0 + blockDim.x < ncell ? c0 + blockDim.x : ncell) - 1;
+    const int row_lo = static_cast<int>(c0 / F.N), rows = static_cast<int>(c1 / F.N) - row_lo + 1;
+    const double* s_fy = stage_rows(sm, T, row_lo, rows);
+    const double* fyc = s_fy ? s_fy + static_cast<int64_t>(cy - row_lo) * n
+                             : T.fy + static_cast<int64_t>(cy) * n;
     double m[16];
-    integrate_block<KIND, FAST>(mine, f, T, T.fx + static_cast<int64_t>(cx) * n,
-                                T.fy + static_cast<int64_t>(cy) * n, sm, m);
+    integrate_block<KIND, FAST>(mine, f, T, T.fx + static_cast<int64_t>(cx) * n, fyc, sm, m);
     if (!mine) return;
     double e_c = centre_eps(f, F, cx, cy);
     if (!publish_leaf(F, static_cast<int>(c), m, n, e_c, delta_max, cycle, stats)) atomicExch(err, 1);
@@ -1053,6 +1130,7 @@ public:
         list_.alloc(leaves_);
         snap_.alloc(leaves_);
         counter_.alloc(1);
+        blockcnt_.alloc(blocks_for(leaves_, kCompactThreads));
         hist_.alloc(kNHist);
         partial_.alloc(kNormBlocks);
         res_.alloc(1);
@@ -1108,8 +1186,12 @@ public:
         LevelView F = V(D_);
         LZB_CUDA(cudaMemsetAsync(counter_.p, 0, sizeof(int), s_));
         LZB_CUDA(cudaMemsetAsync(hist_.p, 0, kNHist * sizeof(unsigned), s_));
-        LZB_LAUNCH(k_compact, blocks_for(leaves_, kThreads), kThreads, 0, s_, F, selector, list_.p,
-                   snap_.p, counter_.p, hist_.p, key_limit >= 0 ? keys_.p : nullptr, key_limit);
+        const long long* keys = key_limit >= 0 ? keys_.p : nullptr;
+        const unsigned nb = blocks_for(leaves_, kCompactThreads);
+        LZB_LAUNCH(k_compact_count, nb, kCompactThreads, 0, s_, F, selector, keys, key_limit, blockcnt_.p);
+        LZB_LAUNCH(k_compact_scan, 1, 1024, 0, s_, blockcnt_.p, static_cast<int>(nb), counter_.p);
+        LZB_LAUNCH(k_compact_scatter, nb, kCompactThreads, 0, s_, F, selector, keys, key_limit, blockcnt_.p,
+                   list_.p, snap_.p, hist_.p);
         LZB_CUDA(cudaMemcpyAsync(hhist_, hist_.p, kNHist * sizeof(unsigned), cudaMemcpyDeviceToHost, s_));
         LZB_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(hhist_) + kNHist * sizeof(unsigned),
                                  counter_.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
@@ -1491,45 +1573,55 @@ public:
     }
 
     // ------------------------------------------------------------ stream I/O
-    int64_t image_size() {
-        DevBuf<int64_t> sizes(total_cells_);
-        record_sizes(sizes.p);
-        std::vector<int64_t> h(total_cells_);
-        LZB_CUDA(cudaMemcpyAsync(h.data(), sizes.p, sizes.bytes(), cudaMemcpyDeviceToHost, s_));
-        sync_check();
-        int64_t s = 12;
-        for (int64_t v : h) s += v;
-        return s;
-    }
-
     void record_sizes(int64_t* sizes) {
         for (int l = 0; l <= D_; ++l)
             LZB_LAUNCH(k_record_sizes, blocks_for(L_[l].nc, kThreads), kThreads, 0, s_, V(l), l,
                        l == D_ ? 1 : 0, slots_, sizes);
     }
 
-    std::vector<uint8_t> image() {  // CellStream::save byte image, packed on the device
-        DevBuf<int64_t> sizes(total_cells_);
-        record_sizes(sizes.p);
-        std::vector<int64_t> h(total_cells_);
-        LZB_CUDA(cudaMemcpyAsync(h.data(), sizes.p, sizes.bytes(), cudaMemcpyDeviceToHost, s_));
-        sync_check();
-        int64_t acc = 0;
-        for (auto& v : h) {
-            int64_t t = v;
-            v = acc;
-            acc += t;
+    // Record sizes -> device exclusive scan (cub) -> total. Returns the image size.
+    int64_t scan_records() {
+        if (rec_sizes_.n < static_cast<size_t>(total_cells_)) {
+            rec_sizes_.alloc(total_cells_);
+            rec_offs_.alloc(total_cells_ + 1);
+            size_t tb = 0;
+            LZB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, rec_sizes_.p, rec_offs_.p,
+                                                  static_cast<int>(total_cells_ + 1), s_));
+            scan_tmp_.alloc(tb);
         }
-        LZB_CUDA(cudaMemcpyAsync(sizes.p, h.data(), sizes.bytes(), cudaMemcpyHostToDevice, s_));
-        std::vector<uint8_t> out(12 + acc);
+        record_sizes(rec_sizes_.p);
+        size_t tb = scan_tmp_.n;
+        // exclusive offsets; the image size is the last offset plus the last record
+        LZB_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp_.p, tb, rec_sizes_.p, rec_offs_.p,
+                                              static_cast<int>(total_cells_), s_));
+        int64_t last[2];
+        LZB_CUDA(cudaMemcpyAsync(&last[0], rec_offs_.p + total_cells_ - 1, 8, cudaMemcpyDeviceToHost, s_));
+        LZB_CUDA(cudaMemcpyAsync(&last[1], rec_sizes_.p + total_cells_ - 1, 8, cudaMemcpyDeviceToHost, s_));
+        sync_check();
+        return 12 + last[0] + last[1];
+    }
+
+    int64_t image_size() { return scan_records(); }
+
+    // CellStream::save byte image: packed on the device (k_pack) from the
+    // decoded operators, copied once into the caller's buffer.
+    int64_t image_into(uint8_t* out, int64_t cap) {
+        int64_t size = scan_records();
+        if (size > cap) throw Error(LZB_ERR_INVALID, "stream image buffer too small");
+        if (img_.n < static_cast<size_t>(size)) img_.alloc(static_cast<size_t>(size) + (size >> 3));
         uint32_t hdr[3] = {0x4c5a4d47u, 1u, static_cast<uint32_t>(total_cells_)};
-        std::memcpy(out.data(), hdr, 12);
-        DevBuf<uint8_t> dout(out.size());
+        std::memcpy(out, hdr, 12);
         for (int l = 0; l <= D_; ++l)
             LZB_LAUNCH(k_pack, blocks_for(L_[l].nc, kThreads), kThreads, 0, s_, V(l), d_.field, l,
-                       l == D_ ? 1 : 0, slots_, sizes.p, dout.p, ctx_->err.p);
-        LZB_CUDA(cudaMemcpyAsync(out.data() + 12, dout.p + 12, acc, cudaMemcpyDeviceToHost, s_));
+                       l == D_ ? 1 : 0, slots_, rec_offs_.p, img_.p, ctx_->err.p);
+        LZB_CUDA(cudaMemcpyAsync(out + 12, img_.p + 12, size - 12, cudaMemcpyDeviceToHost, s_));
         sync_check();
+        return size;
+    }
+
+    std::vector<uint8_t> image() {
+        std::vector<uint8_t> out(static_cast<size_t>(scan_records()));
+        image_into(out.data(), static_cast<int64_t>(out.size()));
         return out;
     }
 
@@ -1600,12 +1692,15 @@ private:
     std::vector<Level> L_;
     int64_t leaves_ = 0, total_cells_ = 0, total_vertices_ = 0;
     DevBuf<int32_t> list_, snap_;
-    DevBuf<int> counter_;
+    DevBuf<int> counter_, blockcnt_;
     DevBuf<unsigned> hist_;
     DevBuf<double> partial_;
     DevBuf<Result> res_;
     DevBuf<long long> keys_;
     TableSet tables_;
+    DevBuf<int64_t> rec_sizes_, rec_offs_;
+    DevBuf<unsigned char> scan_tmp_;
+    DevBuf<uint8_t> img_;
     Result* hres_ = nullptr;
     unsigned* hhist_ = nullptr;
     SlotTable slots_{};
@@ -1697,10 +1792,7 @@ int lzb_grid_stream_image(lzb_grid* g, uint8_t* out, int64_t cap, int64_t* size)
             *size = g->g->image_size();
             return;
         }
-        auto img = g->g->image();
-        *size = static_cast<int64_t>(img.size());
-        if (static_cast<int64_t>(img.size()) > cap) throw Error(LZB_ERR_INVALID, "buffer too small");
-        std::memcpy(out, img.data(), img.size());
+        *size = g->g->image_into(out, cap);
     });
 }
 int lzb_grid_stream_load(lzb_grid* g, const uint8_t* in, int64_t size) {

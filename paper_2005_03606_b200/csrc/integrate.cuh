@@ -59,13 +59,30 @@ __host__ __device__ inline int ktile_rows(int n) {
     int r = kKTileBytes / (n * kKs * 8);
     return r < 1 ? 1 : (r > n ? n : r);
 }
+//   [.., + kFyRows*n)      y field parts of the (<= kFyRows) cell rows the block touches
+constexpr int kFyRows = 8;
 __host__ inline size_t int_smem_bytes(int n) {
-    return (64 + static_cast<size_t>(kSeg) * n + static_cast<size_t>(ktile_rows(n)) * n * kKs) * 8;
+    return (64 + static_cast<size_t>(kSeg) * n + static_cast<size_t>(ktile_rows(n)) * n * kKs +
+            static_cast<size_t>(kFyRows) * n) * 8;
+}
+__device__ inline double* fy_region(double* sm, int n) {
+    return sm + 64 + kSeg * n + static_cast<size_t>(ktile_rows(n)) * n * kKs;
 }
 
 __device__ inline void stage_common(double* sm, const lzb_field& f, const IntTables& T) {
     for (int i = threadIdx.x; i < 64; i += blockDim.x) sm[i] = f.table[i];
     for (int i = threadIdx.x; i < kSeg * T.n; i += blockDim.x) sm[64 + i] = T.seg[i];
+}
+
+// Stage the y field parts of cell rows [row_lo, row_lo+rows) when they fit;
+// returns the base the caller indexes by (cy - row_lo) * n, or nullptr (read
+// the global table instead). Visible after integrate_block's first barrier.
+__device__ inline const double* stage_rows(double* sm, const IntTables& T, int row_lo, int rows) {
+    if (rows > kFyRows) return nullptr;
+    double* dst = fy_region(sm, T.n);
+    const double* src = T.fy + static_cast<size_t>(row_lo) * T.n;
+    for (int i = threadIdx.x; i < rows * T.n; i += blockDim.x) dst[i] = src[i];
+    return dst;
 }
 
 // Block-cooperative integration: every thread of the block must call it (the

@@ -150,16 +150,22 @@ __global__ void k_integrate_boxes(lzb_field f, int64_t ncells, const double* __r
 
 // Whole regular level at one n.
 template <int KIND, bool FAST>
-__global__ void __launch_bounds__(kIntThreads) k_integrate_level(lzb_field f, int N, IntTables T,
-                                                                 double* __restrict__ out) {
+__global__ void __launch_bounds__(kIntThreads, 3) k_integrate_level(lzb_field f, int N, IntTables T,
+                                                                    double* __restrict__ out) {
     extern __shared__ double sm[];
     stage_common(sm, f, T);
     int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    bool active = c < static_cast<int64_t>(N) * N;
+    const int64_t ncell = static_cast<int64_t>(N) * N;
+    bool active = c < ncell;
     int cx = active ? static_cast<int>(c % N) : 0, cy = active ? static_cast<int>(c / N) : 0;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * blockDim.x;
+    const int64_t c1 = (c0 + blockDim.x < ncell ? c0 + blockDim.x : ncell) - 1;
+    const int row_lo = static_cast<int>(c0 / N), rows = static_cast<int>(c1 / N) - row_lo + 1;
+    const double* s_fy = stage_rows(sm, T, row_lo, rows);
+    const double* fyc = s_fy ? s_fy + static_cast<int64_t>(cy - row_lo) * T.n
+                             : T.fy + static_cast<int64_t>(cy) * T.n;
     double m[16];
-    integrate_block<KIND, FAST>(active, f, T, T.fx + static_cast<int64_t>(cx) * T.n,
-                                T.fy + static_cast<int64_t>(cy) * T.n, sm, m);
+    integrate_block<KIND, FAST>(active, f, T, T.fx + static_cast<int64_t>(cx) * T.n, fyc, sm, m);
     if (active) {
         double2* o = reinterpret_cast<double2*>(out + 16 * c);
         for (int k = 0; k < 8; ++k) o[k] = make_double2(m[2 * k], m[2 * k + 1]);
