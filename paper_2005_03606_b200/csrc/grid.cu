@@ -222,52 +222,70 @@ __global__ void k_bottom(LevelView F, lzb_field f, const int32_t* list, const in
 // publish (assembly.cpp:36-59). Fused K1 + K3: integrate, surplus,
 // choose_precision, roundtrip, store.
 template <int KIND, bool FAST>
-__global__ void __launch_bounds__(kIntThreads, 3) k_step(LevelView F, lzb_field f, const int32_t* list,
+__global__ void __launch_bounds__(kIntThreads, 2) k_step(LevelView F, lzb_field f, const int32_t* list,
                                                          const int32_t* snap, int count, int n, int nn,
                                                          int n_cap_top, IntTables T, double term_c,
                                                          double delta_max, uint32_t cycle, int clear_p2,
                                                          unsigned long long* stats, int* err) {
     extern __shared__ double sm[];
-    int64_t t = gtid();
-    const bool mine = t < count && snap[t] == n;
-    const int c = mine ? list[t] : 0, cx = c % F.N, cy = c / F.N;
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x * kCPT;
+    bool mine[kCPT];
+    int cc[kCPT];
+#pragma unroll
+    for (int q = 0; q < kCPT; ++q) {
+        const int64_t t = t0 + threadIdx.x + q * blockDim.x;
+        mine[q] = t < count && snap[t] == n;
+        cc[q] = mine[q] ? list[t] : list[t0];
+    }
     if (n_cap_top) {  // sampling cap reached: the marker becomes top, nothing integrated
-        if (mine) {
-            F.p1[c] = LZB_P1_TOP;
-            if (clear_p2) F.p2[c] = 0;
-        }
+#pragma unroll
+        for (int q = 0; q < kCPT; ++q)
+            if (mine[q]) {
+                F.p1[cc[q]] = LZB_P1_TOP;
+                if (clear_p2) F.p2[cc[q]] = 0;
+            }
         return;
     }
     stage_common(sm, f, T);
     // the list is in ascending cell order: the block's rows span first..last entry
-    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x;
-    const int64_t t1 = (t0 + blockDim.x < count ? t0 + blockDim.x : count) - 1;
+    const int64_t t1 = (t0 + static_cast<int64_t>(blockDim.x) * kCPT < count
+                            ? t0 + static_cast<int64_t>(blockDim.x) * kCPT : count) - 1;
     const int row_lo = list[t0] / F.N, rows = list[t1] / F.N - row_lo + 1;
     const double* s_fy = stage_rows(sm, T, row_lo, rows);
-    const double* fyc = s_fy ? s_fy + static_cast<int64_t>(cy - row_lo) * nn
-                             : T.fy + static_cast<int64_t>(cy) * nn;
-    double fresh[16];
-    integrate_block<KIND, FAST>(mine, f, T, T.fx + static_cast<int64_t>(cx) * nn, fyc, sm, fresh);
-    if (!mine) return;
-    const double* old = F.op + 16 * static_cast<int64_t>(c);
-    double denom = 0.0, dmax = 0.0;
-    for (int k = 0; k < 16; ++k) {
-        double a = fabs(old[k]);
-        denom = denom < a ? a : denom;
-        double d = fabs(fresh[k] - old[k]);
-        dmax = dmax < d ? d : dmax;
+    const double* fxc[kCPT];
+    const double* fyc[kCPT];
+#pragma unroll
+    for (int q = 0; q < kCPT; ++q) {
+        const int cx = cc[q] % F.N, cy = cc[q] / F.N;
+        fxc[q] = T.fx + static_cast<int64_t>(cx) * nn;
+        fyc[q] = s_fy ? s_fy + static_cast<int64_t>(cy - row_lo) * nn : T.fy + static_cast<int64_t>(cy) * nn;
     }
-    double ratio = 0.0;
-    if (denom == 0.0) atomicAdd(&stats[S_ZERO_NORM], 1ull);
-    else ratio = dmax / denom;
-    if (ratio < term_c) {
-        F.p1[c] = LZB_P1_TOP;  // keep the old matrix (assembly.cpp:47-53)
-    } else {
-        double e_c = centre_eps(f, F, cx, cy);
-        if (!publish_leaf(F, c, fresh, nn, e_c, delta_max, cycle, stats)) atomicExch(err, 1);
-        F.p1[c] = nn;
+    double fresh[kCPT][16];
+    integrate_block<KIND, FAST, kCPT>(mine, f, T, fxc, fyc, sm, fresh);
+#pragma unroll
+    for (int q = 0; q < kCPT; ++q) {
+        if (!mine[q]) continue;
+        const int c = cc[q], cx = c % F.N, cy = c / F.N;
+        const double* old = F.op + 16 * static_cast<int64_t>(c);
+        double denom = 0.0, dmax = 0.0;
+        for (int k = 0; k < 16; ++k) {
+            double a = fabs(old[k]);
+            denom = denom < a ? a : denom;
+            double d = fabs(fresh[q][k] - old[k]);
+            dmax = dmax < d ? d : dmax;
+        }
+        double ratio = 0.0;
+        if (denom == 0.0) atomicAdd(&stats[S_ZERO_NORM], 1ull);
+        else ratio = dmax / denom;
+        if (ratio < term_c) {
+            F.p1[c] = LZB_P1_TOP;  // keep the old matrix (assembly.cpp:47-53)
+        } else {
+            double e_c = centre_eps(f, F, cx, cy);
+            if (!publish_leaf(F, c, fresh[q], nn, e_c, delta_max, cycle, stats)) atomicExch(err, 1);
+            F.p1[c] = nn;
+        }
+        if (clear_p2) F.p2[c] = 0;
     }
-    if (clear_p2) F.p2[c] = 0;
 }
 
 // Anarchic request_stencil for non-bottom leaves: spawn if not top and not in
@@ -282,27 +300,41 @@ __global__ void k_spawn(LevelView F, uint32_t cycle, long long leaf_count, long 
 
 // Fixed-p assembly: every leaf integrated at n, published, p1 = top.
 template <int KIND, bool FAST>
-__global__ void __launch_bounds__(kIntThreads, 3) k_fixed(LevelView F, lzb_field f, int n, IntTables T,
+__global__ void __launch_bounds__(kIntThreads, 2) k_fixed(LevelView F, lzb_field f, int n, IntTables T,
                                                           double delta_max, uint32_t cycle,
                                                           unsigned long long* stats, int* err) {
     extern __shared__ double sm[];
     stage_common(sm, f, T);
-    int64_t c = gtid();
     const int64_t ncell = static_cast<int64_t>(F.N) * F.N;
-    const bool mine = c < ncell;
-    int cx = mine ? static_cast<int>(c % F.N) : 0, cy = mine ? static_cast<int>(c / F.N) : 0;
-    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * blockDim.x;
-    const int64_t c1 = (c0 + blockDim.x < ncell ? c0 + blockDim.x : ncell) - 1;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * blockDim.x * kCPT;
+    const int64_t c1 = (c0 + static_cast<int64_t>(blockDim.x) * kCPT < ncell
+                            ? c0 + static_cast<int64_t>(blockDim.x) * kCPT : ncell) - 1;
     const int row_lo = static_cast<int>(c0 / F.N), rows = static_cast<int>(c1 / F.N) - row_lo + 1;
     const double* s_fy = stage_rows(sm, T, row_lo, rows);
-    const double* fyc = s_fy ? s_fy + static_cast<int64_t>(cy - row_lo) * n
-                             : T.fy + static_cast<int64_t>(cy) * n;
-    double m[16];
-    integrate_block<KIND, FAST>(mine, f, T, T.fx + static_cast<int64_t>(cx) * n, fyc, sm, m);
-    if (!mine) return;
-    double e_c = centre_eps(f, F, cx, cy);
-    if (!publish_leaf(F, static_cast<int>(c), m, n, e_c, delta_max, cycle, stats)) atomicExch(err, 1);
-    F.p1[c] = LZB_P1_TOP;
+    bool mine[kCPT];
+    int64_t cc[kCPT];
+    const double* fxc[kCPT];
+    const double* fyc[kCPT];
+#pragma unroll
+    for (int q = 0; q < kCPT; ++q) {
+        const int64_t c = c0 + threadIdx.x + q * blockDim.x;
+        mine[q] = c < ncell;
+        cc[q] = mine[q] ? c : c0;
+        const int cx = static_cast<int>(cc[q] % F.N), cy = static_cast<int>(cc[q] / F.N);
+        fxc[q] = T.fx + static_cast<int64_t>(cx) * n;
+        fyc[q] = s_fy ? s_fy + static_cast<int64_t>(cy - row_lo) * n : T.fy + static_cast<int64_t>(cy) * n;
+    }
+    double m[kCPT][16];
+    integrate_block<KIND, FAST, kCPT>(mine, f, T, fxc, fyc, sm, m);
+#pragma unroll
+    for (int q = 0; q < kCPT; ++q) {
+        if (!mine[q]) continue;
+        const int cx = static_cast<int>(cc[q] % F.N), cy = static_cast<int>(cc[q] / F.N);
+        double e_c = centre_eps(f, F, cx, cy);
+        if (!publish_leaf(F, static_cast<int>(cc[q]), m[q], n, e_c, delta_max, cycle, stats))
+            atomicExch(err, 1);
+        F.p1[cc[q]] = LZB_P1_TOP;
+    }
 }
 
 // recompute_coarse + publish_coarse for the geometric transfer (solver.cpp:59-77,
@@ -1006,7 +1038,7 @@ void launch_step_k(cudaStream_t s, const LevelView& F, const lzb_field& f, const
                    double term_c, double dmax, uint32_t cycle, unsigned long long* stats, int* err) {
     size_t smem = cap ? 0 : int_smem_bytes(nn);
     set_smem(k_step<KIND, FAST>, smem);
-    LZB_LAUNCH((k_step<KIND, FAST>), blocks_for(count, kIntThreads), kIntThreads, smem, s, F, f, list,
+    LZB_LAUNCH((k_step<KIND, FAST>), blocks_for(count, kIntThreads * kCPT), kIntThreads, smem, s, F, f, list,
                snap, count, n, nn, cap, T, term_c, dmax, cycle, 0, stats, err);
 }
 
@@ -1026,7 +1058,7 @@ void launch_fixed_k(cudaStream_t s, const LevelView& F, const lzb_field& f, int 
                     double dmax, uint32_t cycle, unsigned long long* stats, int* err) {
     size_t smem = int_smem_bytes(n);
     set_smem(k_fixed<KIND, FAST>, smem);
-    LZB_LAUNCH((k_fixed<KIND, FAST>), blocks_for(static_cast<int64_t>(F.N) * F.N, kIntThreads),
+    LZB_LAUNCH((k_fixed<KIND, FAST>), blocks_for(static_cast<int64_t>(F.N) * F.N, kIntThreads * kCPT),
                kIntThreads, smem, s, F, f, n, T, dmax, cycle, stats, err);
 }
 

@@ -27,6 +27,7 @@ namespace lzb {
 constexpr int kKs = 10;          // doubles per K_sub(i,j) table entry (9 + pad, 16 B aligned)
 constexpr int kSeg = 4;          // len, S0, S1, S2
 constexpr int kIntThreads = 256; // block size of the table-driven integration kernels
+constexpr int kCPT = 2;          // cells per thread (share K_sub loads, 2x independent chains)
 constexpr int kKTileBytes = 40 * 1024;
 
 struct IntTables {
@@ -60,7 +61,7 @@ __host__ __device__ inline int ktile_rows(int n) {
     return r < 1 ? 1 : (r > n ? n : r);
 }
 //   [.., + kFyRows*n)      y field parts of the (<= kFyRows) cell rows the block touches
-constexpr int kFyRows = 8;
+constexpr int kFyRows = 8;  // rows a block of kIntThreads*kCPT cells may span before falling back to global
 __host__ inline size_t int_smem_bytes(int n) {
     return (64 + static_cast<size_t>(kSeg) * n + static_cast<size_t>(ktile_rows(n)) * n * kKs +
             static_cast<size_t>(kFyRows) * n) * 8;
@@ -85,61 +86,87 @@ __device__ inline const double* stage_rows(double* sm, const IntTables& T, int r
     return dst;
 }
 
-// Block-cooperative integration: every thread of the block must call it (the
-// K_sub tiles are staged with __syncthreads); `active` threads accumulate the
-// cell whose field parts are fxc[0..n) (its column) and fyc[0..n) (its row).
-template <int KIND, bool FAST>
-__device__ __forceinline__ void integrate_block(bool active, const lzb_field& f, const IntTables& T,
-                                                const double* __restrict__ fxc,
-                                                const double* __restrict__ fyc, double* sm,
-                                                double* out16) {
+// Block-cooperative integration of CPT cells per thread: every thread of the
+// block must call it (the K_sub tiles are staged with __syncthreads). Cell q
+// of the thread is active if act[q]; its field parts are fxc[q][0..n) (its
+// column) and fyc[q][0..n) (its row); inactive cells must still point at
+// readable tables (their results are discarded). The CPT cells share every
+// K_sub / seg load and give the DP pipe CPT x 9 independent chains.
+template <int KIND, bool FAST, int CPT>
+__device__ __forceinline__ void integrate_block(const bool* act, const lzb_field& f, const IntTables& T,
+                                                const double* const* fxc, const double* const* fyc,
+                                                double* sm, double (*out16)[16]) {
     const int n = T.n;
     const double* s_tab = sm;
     const double* s_seg = sm + 64;
     double* s_k = sm + 64 + kSeg * n;
     const double value = f.value, eps_low = f.eps_low;
     const int blocks = f.blocks;
-    double a[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    double U0 = 0, U1 = 0, U2 = 0, V0 = 0, V1 = 0, V2 = 0;
+    bool any = false;
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) any = any || act[q];
+    double a[CPT][9];
+#pragma unroll
+    for (int q = 0; q < CPT; ++q)
+#pragma unroll
+        for (int r = 0; r < 9; ++r) a[q][r] = 0.0;
     if (FAST) {
-        __syncthreads();  // seg staged by the caller
-        if (active) {
+        double U[CPT][3], V[CPT][3];
+#pragma unroll
+        for (int q = 0; q < CPT; ++q)
+#pragma unroll
+            for (int r = 0; r < 3; ++r) U[q][r] = V[q][r] = 0.0;
+        __syncthreads();  // seg / rows staged by the caller
+        if (any) {
             for (int i = 0; i < n; ++i) {
-                const double xp = fxc[i];
-                double s0 = 0, s1 = 0, s2 = 0, t = 0;
-#pragma unroll 4
+                double xp[CPT], s0[CPT], s1[CPT], s2[CPT], t[CPT];
+#pragma unroll
+                for (int q = 0; q < CPT; ++q) {
+                    xp[q] = fxc[q][i];
+                    s0[q] = s1[q] = s2[q] = t[q] = 0.0;
+                }
+#pragma unroll 2
                 for (int j = 0; j < n; ++j) {
-                    double e;
-                    if constexpr (KIND == LZB_FIELD_THETA || KIND == LZB_FIELD_SINUSOID)
-                        e = __fma_rn(xp, fyc[j], 1.0);
-                    else
-                        e = combine_k<KIND>(xp, fyc[j], value, eps_low, blocks, s_tab);
                     const double2 q0 = reinterpret_cast<const double2*>(s_seg)[2 * j];
                     const double2 q1 = reinterpret_cast<const double2*>(s_seg)[2 * j + 1];
-                    t = __fma_rn(e, q0.x, t);
-                    s0 = __fma_rn(e, q0.y, s0);
-                    s1 = __fma_rn(e, q1.x, s1);
-                    s2 = __fma_rn(e, q1.y, s2);
+#pragma unroll
+                    for (int q = 0; q < CPT; ++q) {
+                        double e;
+                        if constexpr (KIND == LZB_FIELD_THETA || KIND == LZB_FIELD_SINUSOID)
+                            e = __fma_rn(xp[q], fyc[q][j], 1.0);
+                        else
+                            e = combine_k<KIND>(xp[q], fyc[q][j], value, eps_low, blocks, s_tab);
+                        t[q] = __fma_rn(e, q0.x, t[q]);
+                        s0[q] = __fma_rn(e, q0.y, s0[q]);
+                        s1[q] = __fma_rn(e, q1.x, s1[q]);
+                        s2[q] = __fma_rn(e, q1.y, s2[q]);
+                    }
                 }
                 const double2 p0 = reinterpret_cast<const double2*>(s_seg)[2 * i];
                 const double2 p1 = reinterpret_cast<const double2*>(s_seg)[2 * i + 1];
-                U0 = __fma_rn(p0.x, s0, U0);
-                U1 = __fma_rn(p0.x, s1, U1);
-                U2 = __fma_rn(p0.x, s2, U2);
-                V0 = __fma_rn(p0.y, t, V0);
-                V1 = __fma_rn(p1.x, t, V1);
-                V2 = __fma_rn(p1.y, t, V2);
+#pragma unroll
+                for (int q = 0; q < CPT; ++q) {
+                    U[q][0] = __fma_rn(p0.x, s0[q], U[q][0]);
+                    U[q][1] = __fma_rn(p0.x, s1[q], U[q][1]);
+                    U[q][2] = __fma_rn(p0.x, s2[q], U[q][2]);
+                    V[q][0] = __fma_rn(p0.y, t[q], V[q][0]);
+                    V[q][1] = __fma_rn(p1.x, t[q], V[q][1]);
+                    V[q][2] = __fma_rn(p1.y, t[q], V[q][2]);
+                }
             }
         }
-        a[0] = U0 + V0;
-        a[1] = U0 + V2;
-        a[2] = U2 + V0;
-        a[3] = U2 + V2;
-        a[4] = V1 - U0;
-        a[5] = V1 - U2;
-        a[6] = U1 - V0;
-        a[7] = U1 - V2;
-        a[8] = -(U1 + V1);
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+            a[q][0] = U[q][0] + V[q][0];
+            a[q][1] = U[q][0] + V[q][2];
+            a[q][2] = U[q][2] + V[q][0];
+            a[q][3] = U[q][2] + V[q][2];
+            a[q][4] = V[q][1] - U[q][0];
+            a[q][5] = V[q][1] - U[q][2];
+            a[q][6] = U[q][1] - V[q][0];
+            a[q][7] = U[q][1] - V[q][2];
+            a[q][8] = -(U[q][1] + V[q][1]);
+        }
     } else {
         const int TI = ktile_rows(n);
         for (int i0 = 0; i0 < n; i0 += TI) {
@@ -152,30 +179,36 @@ __device__ __forceinline__ void integrate_block(bool active, const lzb_field& f,
                 for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = src[v];
             }
             __syncthreads();
-            if (active) {
+            if (any) {
                 for (int ii = 0; ii < rows; ++ii) {
-                    const double xp = fxc[i0 + ii];
+                    double xp[CPT];
+#pragma unroll
+                    for (int q = 0; q < CPT; ++q) xp[q] = fxc[q][i0 + ii];
                     const double2* kp = reinterpret_cast<const double2*>(s_k + static_cast<size_t>(ii) * n * kKs);
 #pragma unroll 2
                     for (int j = 0; j < n; ++j, kp += kKs / 2) {
-                        const double e = combine_k<KIND>(xp, fyc[j], value, eps_low, blocks, s_tab);
                         const double2 k0 = kp[0], k1 = kp[1], k2 = kp[2], k3 = kp[3], k4 = kp[4];
-                        // out.m += e * K   (Mat4 operator* rounds K*e, then +=)
-                        a[0] = a[0] + k0.x * e;
-                        a[1] = a[1] + k0.y * e;
-                        a[2] = a[2] + k1.x * e;
-                        a[3] = a[3] + k1.y * e;
-                        a[4] = a[4] + k2.x * e;
-                        a[5] = a[5] + k2.y * e;
-                        a[6] = a[6] + k3.x * e;
-                        a[7] = a[7] + k3.y * e;
-                        a[8] = a[8] + k4.x * e;
+#pragma unroll
+                        for (int q = 0; q < CPT; ++q) {
+                            const double e = combine_k<KIND>(xp[q], fyc[q][j], value, eps_low, blocks, s_tab);
+                            // out.m += e * K   (Mat4 operator* rounds K*e, then +=)
+                            a[q][0] = a[q][0] + k0.x * e;
+                            a[q][1] = a[q][1] + k0.y * e;
+                            a[q][2] = a[q][2] + k1.x * e;
+                            a[q][3] = a[q][3] + k1.y * e;
+                            a[q][4] = a[q][4] + k2.x * e;
+                            a[q][5] = a[q][5] + k2.y * e;
+                            a[q][6] = a[q][6] + k3.x * e;
+                            a[q][7] = a[q][7] + k3.y * e;
+                            a[q][8] = a[q][8] + k4.x * e;
+                        }
                     }
                 }
             }
         }
     }
-    k9_expand(a, out16);
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) k9_expand(a[q], out16[q]);
 }
 
 // Table builders (runtime.cu).

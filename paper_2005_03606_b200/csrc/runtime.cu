@@ -150,25 +150,36 @@ __global__ void k_integrate_boxes(lzb_field f, int64_t ncells, const double* __r
 
 // Whole regular level at one n.
 template <int KIND, bool FAST>
-__global__ void __launch_bounds__(kIntThreads, 3) k_integrate_level(lzb_field f, int N, IntTables T,
+__global__ void __launch_bounds__(kIntThreads, 2) k_integrate_level(lzb_field f, int N, IntTables T,
                                                                     double* __restrict__ out) {
     extern __shared__ double sm[];
     stage_common(sm, f, T);
-    int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     const int64_t ncell = static_cast<int64_t>(N) * N;
-    bool active = c < ncell;
-    int cx = active ? static_cast<int>(c % N) : 0, cy = active ? static_cast<int>(c / N) : 0;
-    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * blockDim.x;
-    const int64_t c1 = (c0 + blockDim.x < ncell ? c0 + blockDim.x : ncell) - 1;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * blockDim.x * kCPT;
+    const int64_t c1 = (c0 + static_cast<int64_t>(blockDim.x) * kCPT < ncell
+                            ? c0 + static_cast<int64_t>(blockDim.x) * kCPT : ncell) - 1;
     const int row_lo = static_cast<int>(c0 / N), rows = static_cast<int>(c1 / N) - row_lo + 1;
     const double* s_fy = stage_rows(sm, T, row_lo, rows);
-    const double* fyc = s_fy ? s_fy + static_cast<int64_t>(cy - row_lo) * T.n
-                             : T.fy + static_cast<int64_t>(cy) * T.n;
-    double m[16];
-    integrate_block<KIND, FAST>(active, f, T, T.fx + static_cast<int64_t>(cx) * T.n, fyc, sm, m);
-    if (active) {
-        double2* o = reinterpret_cast<double2*>(out + 16 * c);
-        for (int k = 0; k < 8; ++k) o[k] = make_double2(m[2 * k], m[2 * k + 1]);
+    bool act[kCPT];
+    int64_t cc[kCPT];
+    const double* fxc[kCPT];
+    const double* fyc[kCPT];
+#pragma unroll
+    for (int q = 0; q < kCPT; ++q) {
+        const int64_t c = c0 + threadIdx.x + q * blockDim.x;
+        act[q] = c < ncell;
+        cc[q] = act[q] ? c : c0;
+        const int cx = static_cast<int>(cc[q] % N), cy = static_cast<int>(cc[q] / N);
+        fxc[q] = T.fx + static_cast<int64_t>(cx) * T.n;
+        fyc[q] = s_fy ? s_fy + static_cast<int64_t>(cy - row_lo) * T.n : T.fy + static_cast<int64_t>(cy) * T.n;
+    }
+    double m[kCPT][16];
+    integrate_block<KIND, FAST, kCPT>(act, f, T, fxc, fyc, sm, m);
+#pragma unroll
+    for (int q = 0; q < kCPT; ++q) {
+        if (!act[q]) continue;
+        double2* o = reinterpret_cast<double2*>(out + 16 * cc[q]);
+        for (int k = 0; k < 8; ++k) o[k] = make_double2(m[q][2 * k], m[q][2 * k + 1]);
     }
 }
 
@@ -183,7 +194,7 @@ template <int KIND, bool FAST>
 void launch_level_k(const lzb_field& f, int N, const IntTables& T, double* out, cudaStream_t s) {
     size_t smem = int_smem_bytes(T.n);
     set_smem(k_integrate_level<KIND, FAST>, smem);
-    LZB_LAUNCH((k_integrate_level<KIND, FAST>), blocks_for(static_cast<int64_t>(N) * N, kIntThreads),
+    LZB_LAUNCH((k_integrate_level<KIND, FAST>), blocks_for(static_cast<int64_t>(N) * N, kIntThreads * kCPT),
                kIntThreads, smem, s, f, N, T, out);
 }
 
