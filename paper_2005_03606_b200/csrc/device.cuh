@@ -250,6 +250,47 @@ __device__ inline bool roundtrip(double x, int p3, double& out) {
 // codec::choose_precision (codec.cpp:65-85), literal scan. Returns -1 where
 // the reference throws (non-finite value reached by the scan).
 __device__ inline int choose_precision_scan(const double* v, int count, double delta);
+__device__ inline int choose_precision(const double* v, int count, double delta);
+
+// "Regular" value: finite, normal, unbiased exponent in [-128,127] (no clamp).
+// For regular values the truncation error |rt_m(v) - v| is non-increasing in
+// m (the dropped bits of a wider width are a subset), so the set of passing
+// widths is upward closed.
+__device__ __forceinline__ bool codec_regular(double v) {
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(v));
+    const int E = static_cast<int>((u >> 52) & 0x7ff);
+    // +-0 roundtrips to 0 at every width: its error (0) is constant in the width
+    return (E >= 1023 - 128 && E <= 1023 + 127) || (u << 1) == 0;
+}
+// Smallest width in 2..7 that keeps a regular v within delta, else 8.
+__device__ __forceinline__ int min_width(double v, double delta) {
+#pragma unroll
+    for (int q = 2; q < 8; ++q)
+        if (fabs(rt_bits(v, mantissa_bits(q)) - v) <= delta) return q;
+    return 8;
+}
+
+// choose_precision for a 4x4 element matrix given its 9 distinct values
+// (k9 order; the 16 entries repeat them, duplicates never change the result).
+// All-regular records take max(min_width) — exact by upward closure; any
+// irregular / zero / non-finite entry takes the general routine on all 16.
+__device__ inline int choose_precision_k9(const double* s9, const double* s16, double delta) {
+    bool all_small = true, regular = true;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        all_small = all_small && !(fabs(s9[i]) > delta);
+        regular = regular && codec_regular(s9[i]);
+    }
+    if (all_small) return 0;
+    if (!regular) return choose_precision(s16, 16, delta);
+    int P = 2;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        const int q = min_width(s9[i], delta);
+        P = q > P ? q : P;
+    }
+    return P;
+}
 
 // Same result, fewer roundtrips: P = max over entries of the entry's smallest
 // passing width (8 if none in 2..7); no width below P can pass for all

@@ -112,6 +112,47 @@ __device__ inline bool publish_leaf(const LevelView& F, int c, const double* m, 
     return true;
 }
 
+// publish_element for a matrix produced by the integration kernels, whose 16
+// entries are the 9 k9 values by construction (k9_expand), as are the
+// baseline's (0 + K_unit*e): surplus, width choice and roundtrip run on the 9
+// distinct values; the stored 16 are their bitwise copies.
+__constant__ int c_k9pos[9] = {0, 5, 10, 15, 1, 11, 2, 7, 3};
+
+__device__ inline bool publish_leaf_k9(const LevelView& F, int c, const double* m16, int n, double e_c,
+                                       double delta_max, uint32_t cycle, unsigned long long* stats) {
+    double base9[9], sur9[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        const int k = c_k9pos[i];
+        base9[i] = baseline_entry(k, e_c);
+        sur9[i] = m16[k] - base9[i];
+    }
+    double sur16[16];
+    k9_expand(sur9, sur16);
+    const int p3 = choose_precision_k9(sur9, sur16, delta_max);
+    if (p3 < 0) return false;
+    double delta = 0.0, dec9[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        double rt;
+        if (!roundtrip_fast(sur9[i], p3, rt)) return false;
+        const double err = fabs(rt - sur9[i]);
+        delta = delta < err ? err : delta;
+        dec9[i] = base9[i] + rt;
+    }
+    double dec[16];
+    k9_expand(dec9, dec);
+    double2* op = reinterpret_cast<double2*>(F.op + 16 * static_cast<int64_t>(c));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) op[q] = make_double2(dec[2 * q], dec[2 * q + 1]);
+    atomic_max_double_bits(&stats[S_MAXDELTA], delta);
+    atomicMax(&stats[S_MAXSAMPLES], static_cast<unsigned long long>(n));
+    F.n[c] = n;
+    F.epoch[c] = cycle;
+    F.p3[c] = static_cast<int8_t>(p3);
+    return true;
+}
+
 // -------------------------------------------------------------- assembly
 // Order-preserving compaction of the selected leaves (ascending cell index,
 // so a block of list entries covers few cell rows): count per block, scan,
@@ -213,7 +254,7 @@ __global__ void k_bottom(LevelView F, lzb_field f, const int32_t* list, const in
     int c = list[t], cx = c % F.N, cy = c / F.N;
     double e = centre_eps(f, F, cx, cy), m[16];
     for (int k = 0; k < 16; ++k) m[k] = baseline_entry(k, e);
-    if (!publish_leaf(F, c, m, 1, e, delta_max, cycle, stats)) atomicExch(err, 1);
+    if (!publish_leaf_k9(F, c, m, 1, e, delta_max, cycle, stats)) atomicExch(err, 1);
     F.p1[c] = 1;
     if (clear_p2) F.p2[c] = 0;
 }
@@ -281,7 +322,7 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_step(LevelView F, lzb_field 
             F.p1[c] = LZB_P1_TOP;  // keep the old matrix (assembly.cpp:47-53)
         } else {
             double e_c = centre_eps(f, F, cx, cy);
-            if (!publish_leaf(F, c, fresh[q], nn, e_c, delta_max, cycle, stats)) atomicExch(err, 1);
+            if (!publish_leaf_k9(F, c, fresh[q], nn, e_c, delta_max, cycle, stats)) atomicExch(err, 1);
             F.p1[c] = nn;
         }
         if (clear_p2) F.p2[c] = 0;
@@ -331,7 +372,7 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_fixed(LevelView F, lzb_field
         if (!mine[q]) continue;
         const int cx = static_cast<int>(cc[q] % F.N), cy = static_cast<int>(cc[q] / F.N);
         double e_c = centre_eps(f, F, cx, cy);
-        if (!publish_leaf(F, static_cast<int>(cc[q]), m[q], n, e_c, delta_max, cycle, stats))
+        if (!publish_leaf_k9(F, static_cast<int>(cc[q]), m[q], n, e_c, delta_max, cycle, stats))
             atomicExch(err, 1);
         F.p1[cc[q]] = LZB_P1_TOP;
     }
@@ -991,7 +1032,7 @@ __global__ void k_step_one(LevelView F, lzb_field f, int c, int schedule, int n_
     if (p1 == LZB_P1_BOTTOM) {
         double m[16];
         for (int k = 0; k < 16; ++k) m[k] = baseline_entry(k, e);
-        if (!publish_leaf(F, c, m, 1, e, delta_max, cycle, stats)) atomicExch(err, 1);
+        if (!publish_leaf_k9(F, c, m, 1, e, delta_max, cycle, stats)) atomicExch(err, 1);
         F.p1[c] = 1;
         return;
     }
