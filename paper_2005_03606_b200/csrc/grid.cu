@@ -81,8 +81,14 @@ __device__ inline void element_or_baseline(const lzb_field& f, const LevelView& 
     }
 }
 
-__device__ inline void atomic_max_double_bits(unsigned long long* a, double v) {
-    atomicMax(a, static_cast<unsigned long long>(__double_as_longlong(v)));
+// Running maxima shared by every publishing thread: read first, and only
+// contend for the atomic when the value would raise the maximum (after the
+// first few cells almost none do), instead of one serialised atomic per cell.
+__device__ inline void atomic_max_u64(unsigned long long* a, unsigned long long v) {
+    if (v > *reinterpret_cast<volatile unsigned long long*>(a)) atomicMax(a, v);
+}
+__device__ inline void atomic_max_double_bits(unsigned long long* a, double v) {  // v >= 0
+    atomic_max_u64(a, static_cast<unsigned long long>(__double_as_longlong(v)));
 }
 
 // CellStream::publish_element (stream.cpp:100-132); caller stores p1.
@@ -105,7 +111,7 @@ __device__ inline bool publish_leaf(const LevelView& F, int c, const double* m, 
         op[k] = base[k] + rt;
     }
     atomic_max_double_bits(&stats[S_MAXDELTA], delta);
-    atomicMax(&stats[S_MAXSAMPLES], static_cast<unsigned long long>(n));
+    atomic_max_u64(&stats[S_MAXSAMPLES], static_cast<unsigned long long>(n));
     F.n[c] = n;
     F.epoch[c] = cycle;
     F.p3[c] = static_cast<int8_t>(p3);
@@ -146,7 +152,7 @@ __device__ inline bool publish_leaf_k9(const LevelView& F, int c, const double* 
 #pragma unroll
     for (int q = 0; q < 8; ++q) op[q] = make_double2(dec[2 * q], dec[2 * q + 1]);
     atomic_max_double_bits(&stats[S_MAXDELTA], delta);
-    atomicMax(&stats[S_MAXSAMPLES], static_cast<unsigned long long>(n));
+    atomic_max_u64(&stats[S_MAXSAMPLES], static_cast<unsigned long long>(n));
     F.n[c] = n;
     F.epoch[c] = cycle;
     F.p3[c] = static_cast<int8_t>(p3);
@@ -747,22 +753,37 @@ __global__ void k_stats(LevelView L, int leaf, unsigned long long* s) {
     if (threadIdx.x < 16) sh[threadIdx.x] = 0;
     __syncthreads();
     int64_t c = gtid();
-    if (c < static_cast<int64_t>(L.N) * L.N) {
+    const bool in = c < static_cast<int64_t>(L.N) * L.N;
+    int p3 = 0;
+    unsigned bytes = 0, n = 0;
+    if (in) {
         int32_t p1 = L.p1[c];
-        int p3 = p1 != LZB_P1_BOTTOM ? L.p3[c] : 0;
-        unsigned long long bytes = p1 == LZB_P1_BOTTOM ? 1ull : 1ull + p3 * (leaf ? 16ull : 144ull);
-        atomicAdd(&sh[S_TOTAL_BYTES], bytes);
-        if (leaf) {
-            atomicAdd(&sh[S_HIST + p3], 1ull);
-            atomicAdd(&sh[S_FINE_BYTES], bytes);
-            unsigned long long n = p1 != LZB_P1_BOTTOM ? static_cast<unsigned long long>(L.n[c]) : 0ull;
-            atomicAdd(&sh[S_NSUM], n);
-            atomicMax(&sh[S_MAXN], n);
+        p3 = p1 != LZB_P1_BOTTOM ? L.p3[c] : 0;
+        bytes = p1 == LZB_P1_BOTTOM ? 1u : 1u + p3 * (leaf ? 16u : 144u);
+        n = p1 != LZB_P1_BOTTOM ? static_cast<unsigned>(L.n[c]) : 0u;
+    }
+    // warp reductions, then one shared atomic per warp and one global per block
+    const unsigned full = 0xffffffffu;
+    const unsigned wbytes = __reduce_add_sync(full, bytes);
+    const unsigned wn = __reduce_add_sync(full, n);
+    const unsigned wmax = __reduce_max_sync(full, n);
+    const bool lead = (threadIdx.x & 31) == 0;
+    if (lead) atomicAdd(&sh[S_TOTAL_BYTES], static_cast<unsigned long long>(wbytes));
+    if (leaf) {
+#pragma unroll
+        for (int b = 0; b <= 8; ++b) {
+            const unsigned cnt = __popc(__ballot_sync(full, in && p3 == b));
+            if (lead && cnt) atomicAdd(&sh[S_HIST + b], static_cast<unsigned long long>(cnt));
+        }
+        if (lead) {
+            atomicAdd(&sh[S_FINE_BYTES], static_cast<unsigned long long>(wbytes));
+            atomicAdd(&sh[S_NSUM], static_cast<unsigned long long>(wn));
+            atomicMax(&sh[S_MAXN], static_cast<unsigned long long>(wmax));
         }
     }
     __syncthreads();
     if (threadIdx.x < 13 && sh[threadIdx.x]) {
-        if (threadIdx.x == S_MAXN) atomicMax(&s[S_MAXN], sh[S_MAXN]);
+        if (threadIdx.x == S_MAXN) atomic_max_u64(&s[S_MAXN], sh[S_MAXN]);
         else atomicAdd(&s[threadIdx.x], sh[threadIdx.x]);
     }
 }
