@@ -111,7 +111,8 @@ int lzb_grid_assemble_fixed(lzb_grid* g, int n);
 int lzb_grid_step(lzb_grid* g, lzb_cycle_report* out);
 int lzb_grid_run(lzb_grid* g, lzb_cycle_report* out, int cap, int* count);
 /* Individual passes (solver.hpp:91-98): 0 assembly, 1 residual (value = norm),
- * 2 update, 3 prolong, 4 finish_cycle_sync, 5 stream begin_cycle, 6 pool begin_cycle. */
+ * 2 update, 3 prolong, 4 finish_cycle_sync, 5 stream begin_cycle, 6 pool begin_cycle,
+ * 7 drain every pending assembly task (TaskPool::drain_all, scheduler.hpp:59). */
 int lzb_grid_pass(lzb_grid* g, int which, double* value);
 int lzb_grid_cycle(lzb_grid* g);
 /* Dense per-level vertex field: (N+1)^2 doubles, index iy*(N+1)+ix. */

@@ -387,6 +387,11 @@ class Grid:
     assembly_pass = lambda self: self.pass_(0)  # noqa: E731
     residual_pass = lambda self: self.pass_(1)  # noqa: E731
 
+    def drain(self) -> int:
+        """TaskPool::drain_all: finish every pending assembly task (commits an
+        in-flight concurrent batch first); returns the tasks left (0)."""
+        return int(self.pass_(7))
+
     def cycle(self):
         return lib().lzb_grid_cycle(self.h)
 

@@ -236,7 +236,9 @@ struct ExperimentConfig {
         if (integration == "exact") d.integration = LZB_INTEGRATE_EXACT;
         else if (integration == "fast") d.integration = LZB_INTEGRATE_FAST;
         else throw Fail(LZB_ERR_IO, "unknown integration: " + integration);
-        d.concurrent = workers > 1 ? 1 : 0;
+        // workers > 1: background integration (scheduler.cpp:5-12) = the concurrent
+        // assembly stream; only anarchic mode ever spawns tasks
+        d.concurrent = (workers > 1 && assembly == "anarchic") ? 1 : 0;
         d.throttle = throttle;
         d.noise_seed = seed;
         d.boundary_value = 0.0;

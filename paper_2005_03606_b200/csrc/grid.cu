@@ -269,13 +269,19 @@ __global__ void k_bottom(LevelView F, lzb_field f, const int32_t* list, const in
 // publish (assembly.cpp:36-59). Fused K1 + K3: integrate, surplus,
 // choose_precision, roundtrip, store.
 template <int KIND, bool FAST>
-__global__ void __launch_bounds__(kIntThreads, 2) k_step(LevelView F, lzb_field f, const int32_t* list,
-                                                         const int32_t* snap, int count, int n, int nn,
+// F = live state (old matrix, markers); D = destination of the outcome (== F in
+// the deterministic modes; the staging copy for concurrent assembly batches,
+// swapped in by k_commit). count is read on the device (no host round trip).
+__global__ void __launch_bounds__(kIntThreads, 2) k_step(LevelView F, LevelView D, lzb_field f,
+                                                         const int32_t* list, const int32_t* snap,
+                                                         const int* count_ptr, int n, int nn,
                                                          int n_cap_top, IntTables T, double term_c,
                                                          double delta_max, uint32_t cycle, int clear_p2,
                                                          unsigned long long* stats, int* err) {
     extern __shared__ double sm[];
+    const int count = *count_ptr;
     const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x * kCPT;
+    if (t0 >= count) return;  // uniform per block: no barrier is skipped by part of a block
     bool mine[kCPT];
     int cc[kCPT];
 #pragma unroll
@@ -288,7 +294,7 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_step(LevelView F, lzb_field 
 #pragma unroll
         for (int q = 0; q < kCPT; ++q)
             if (mine[q]) {
-                F.p1[cc[q]] = LZB_P1_TOP;
+                D.p1[cc[q]] = LZB_P1_TOP;
                 if (clear_p2) F.p2[cc[q]] = 0;
             }
         return;
@@ -325,11 +331,11 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_step(LevelView F, lzb_field 
         if (denom == 0.0) atomicAdd(&stats[S_ZERO_NORM], 1ull);
         else ratio = dmax / denom;
         if (ratio < term_c) {
-            F.p1[c] = LZB_P1_TOP;  // keep the old matrix (assembly.cpp:47-53)
+            D.p1[c] = LZB_P1_TOP;  // keep the old matrix (assembly.cpp:47-53)
         } else {
             double e_c = centre_eps(f, F, cx, cy);
-            if (!publish_leaf_k9(F, c, fresh[q], nn, e_c, delta_max, cycle, stats)) atomicExch(err, 1);
-            F.p1[c] = nn;
+            if (!publish_leaf_k9(D, c, fresh[q], nn, e_c, delta_max, cycle, stats)) atomicExch(err, 1);
+            D.p1[c] = nn;
         }
         if (clear_p2) F.p2[c] = 0;
     }
@@ -1090,29 +1096,106 @@ __global__ void k_clear_p2(LevelView F, const int32_t* list, int count) {
     if (t < count) F.p2[list[t]] = 0;
 }
 
+// Concurrent assembly, fallback for batch entries off the lockstep n: the
+// adaptive step with on-the-fly axis parts (same arithmetic), outcome to D.
+__global__ void k_step_generic(LevelView F, LevelView D, lzb_field f, const int32_t* list,
+                               const int32_t* snap, const int* count_ptr, int n_main, int schedule,
+                               int n_max, int fast, double term_c, double delta_max, uint32_t cycle,
+                               unsigned long long* stats, int* err) {
+    int64_t t = gtid();
+    if (t >= *count_ptr) return;
+    const int32_t p1 = snap[t];
+    if (p1 == n_main || p1 == LZB_P1_BOTTOM) return;  // main kernel / inline bottom round
+    const int c = list[t], cx = c % F.N, cy = c / F.N;
+    if (p1 == LZB_P1_TOP || (n_max > 0 && p1 >= n_max)) {
+        D.p1[c] = LZB_P1_TOP;
+        return;
+    }
+    int nn = schedule == LZB_SCHEDULE_DOUBLE ? 2 * p1 : p1 + 1;
+    if (n_max > 0 && nn > n_max) nn = n_max;
+    double fresh[16];
+    integrate_cell(f, cx * F.h, cy * F.h, F.h, nn, fast, fresh);
+    const double* old = F.op + 16 * static_cast<int64_t>(c);
+    double denom = 0.0, dmax = 0.0;
+    for (int k = 0; k < 16; ++k) {
+        double a = fabs(old[k]);
+        denom = denom < a ? a : denom;
+        double d = fabs(fresh[k] - old[k]);
+        dmax = dmax < d ? d : dmax;
+    }
+    double ratio = 0.0;
+    if (denom == 0.0) atomicAdd(&stats[S_ZERO_NORM], 1ull);
+    else ratio = dmax / denom;
+    if (ratio < term_c) {
+        D.p1[c] = LZB_P1_TOP;
+        return;
+    }
+    if (!publish_leaf_k9(D, c, fresh, nn, centre_eps(f, F, cx, cy), delta_max, cycle, stats))
+        atomicExch(err, 1);
+    D.p1[c] = nn;
+}
+
+// Swap-in of a completed concurrent batch, on the solve stream: the outcome of
+// every task in the batch becomes the live operator / marker, and the task
+// completes (p2 cleared, assembly.cpp:66-68).
+__global__ void k_commit(LevelView F, LevelView S, const int32_t* list, const int* count_ptr) {
+    int64_t t = gtid();
+    if (t >= *count_ptr) return;
+    const int c = list[t];
+    const int32_t p1 = S.p1[c];
+    if (p1 != LZB_P1_TOP) {
+        const double2* src = reinterpret_cast<const double2*>(S.op + 16 * static_cast<int64_t>(c));
+        double2* dst = reinterpret_cast<double2*>(F.op + 16 * static_cast<int64_t>(c));
+        for (int q = 0; q < 8; ++q) dst[q] = src[q];
+        F.n[c] = S.n[c];
+        F.p3[c] = S.p3[c];
+        F.epoch[c] = S.epoch[c];
+    }
+    F.p1[c] = p1;
+    F.p2[c] = 0;
+}
+
 __global__ void k_reset_stats(Result* r) {
     if (threadIdx.x < 13) r->s[threadIdx.x] = 0;  // per-cycle slots; the norm is written by k_norm_final
 }
 
 template <int KIND, bool FAST>
-void launch_step_k(cudaStream_t s, const LevelView& F, const lzb_field& f, const int32_t* list,
-                   const int32_t* snap, int count, int n, int nn, int cap, const IntTables& T,
-                   double term_c, double dmax, uint32_t cycle, unsigned long long* stats, int* err) {
+void launch_step_k(cudaStream_t s, const LevelView& F, const LevelView& D, const lzb_field& f,
+                   const int32_t* list, const int32_t* snap, const int* count_ptr, int64_t max_count,
+                   int n, int nn, int cap, const IntTables& T, double term_c, double dmax, uint32_t cycle,
+                   unsigned long long* stats, int* err) {
     size_t smem = cap ? 0 : int_smem_bytes(nn);
     set_smem(k_step<KIND, FAST>, smem);
-    LZB_LAUNCH((k_step<KIND, FAST>), blocks_for(count, kIntThreads * kCPT), kIntThreads, smem, s, F, f, list,
-               snap, count, n, nn, cap, T, term_c, dmax, cycle, 0, stats, err);
+    LZB_LAUNCH((k_step<KIND, FAST>), blocks_for(max_count, kIntThreads * kCPT), kIntThreads, smem, s, F, D,
+               f, list, snap, count_ptr, n, nn, cap, T, term_c, dmax, cycle, 0, stats, err);
 }
 
 template <int KIND>
-void launch_step(bool fast, cudaStream_t s, const LevelView& F, const lzb_field& f,
-                 const int32_t* list, const int32_t* snap, int count, int n, int nn, int cap,
-                 const IntTables& T, double term_c, double dmax, uint32_t cycle,
+void launch_step(bool fast, cudaStream_t s, const LevelView& F, const LevelView& D, const lzb_field& f,
+                 const int32_t* list, const int32_t* snap, const int* count_ptr, int64_t max_count,
+                 int n, int nn, int cap, const IntTables& T, double term_c, double dmax, uint32_t cycle,
                  unsigned long long* stats, int* err) {
     if (fast)
-        launch_step_k<KIND, true>(s, F, f, list, snap, count, n, nn, cap, T, term_c, dmax, cycle, stats, err);
+        launch_step_k<KIND, true>(s, F, D, f, list, snap, count_ptr, max_count, n, nn, cap, T, term_c, dmax,
+                                  cycle, stats, err);
     else
-        launch_step_k<KIND, false>(s, F, f, list, snap, count, n, nn, cap, T, term_c, dmax, cycle, stats, err);
+        launch_step_k<KIND, false>(s, F, D, f, list, snap, count_ptr, max_count, n, nn, cap, T, term_c, dmax,
+                                   cycle, stats, err);
+}
+
+// Dispatch on the field kind (one instantiation per kind).
+inline void dispatch_step(bool fast, cudaStream_t s, const LevelView& F, const LevelView& D,
+                          const lzb_field& f, const int32_t* list, const int32_t* snap,
+                          const int* count_ptr, int64_t max_count, int n, int nn, int cap,
+                          const IntTables& T, double term_c, double dmax, uint32_t cycle,
+                          unsigned long long* stats, int* err) {
+    switch (f.kind) {
+        case LZB_FIELD_THETA: launch_step<LZB_FIELD_THETA>(fast, s, F, D, f, list, snap, count_ptr, max_count, n, nn, cap, T, term_c, dmax, cycle, stats, err); break;
+        case LZB_FIELD_QUADRANT: launch_step<LZB_FIELD_QUADRANT>(fast, s, F, D, f, list, snap, count_ptr, max_count, n, nn, cap, T, term_c, dmax, cycle, stats, err); break;
+        case LZB_FIELD_CHECKER: launch_step<LZB_FIELD_CHECKER>(fast, s, F, D, f, list, snap, count_ptr, max_count, n, nn, cap, T, term_c, dmax, cycle, stats, err); break;
+        case LZB_FIELD_SINUSOID: launch_step<LZB_FIELD_SINUSOID>(fast, s, F, D, f, list, snap, count_ptr, max_count, n, nn, cap, T, term_c, dmax, cycle, stats, err); break;
+        default: launch_step<LZB_FIELD_CONSTANT>(fast, s, F, D, f, list, snap, count_ptr, max_count, n, nn, cap, T, term_c, dmax, cycle, stats, err); break;
+    }
 }
 
 template <int KIND, bool FAST>
@@ -1230,6 +1313,25 @@ public:
         res_.alloc(1);
         LZB_CUDA(cudaMemsetAsync(res_.p, 0, sizeof(Result), s_));
         if (d.throttle) keys_.alloc(leaves_);
+        if (d.concurrent) {
+            if (d.mode != LZB_ANARCHIC)
+                throw Error(LZB_ERR_INVALID, "concurrent assembly needs assembly = anarchic");
+            if (d.throttle)
+                throw Error(LZB_ERR_INVALID, "concurrent assembly runs every pending task (throttle = 0)");
+            a_ = ctx->assembly;
+            alist_.alloc(leaves_);
+            asnap_.alloc(leaves_);
+            acounter_.alloc(1);
+            ablockcnt_.alloc(blocks_for(leaves_, kCompactThreads));
+            ahist_.alloc(kNHist);
+            sop_.alloc(16 * leaves_);
+            sp1_.alloc(leaves_);
+            sn_.alloc(leaves_);
+            sp3_.alloc(leaves_);
+            sepoch_.alloc(leaves_);
+            LZB_CUDA(cudaEventCreateWithFlags(&ev_batch_, cudaEventDisableTiming));
+            LZB_CUDA(cudaEventCreateWithFlags(&ev_spawn_, cudaEventDisableTiming));
+        }
         LZB_CUDA(cudaMallocHost(&hres_, sizeof(Result)));
         LZB_CUDA(cudaMallocHost(&hhist_, kNHist * sizeof(unsigned) + sizeof(int)));
         // subtree sizes for pre-order slots
@@ -1245,6 +1347,9 @@ public:
 
     ~Grid() {
         cudaStreamSynchronize(s_);
+        if (a_) cudaStreamSynchronize(a_);
+        if (ev_batch_) cudaEventDestroy(ev_batch_);
+        if (ev_spawn_) cudaEventDestroy(ev_spawn_);
         if (hres_) cudaFreeHost(hres_);
         if (hhist_) cudaFreeHost(hhist_);
     }
@@ -1276,16 +1381,87 @@ public:
 
     // One batched round of adaptive steps over the selected leaves; returns
     // the number of selected leaves. selector: 0 unconverged, 1 tasks, 2 bottom.
-    int64_t round(int selector, bool complete_tasks, long long key_limit = -1) {
+    // Order-preserving compaction of the selected leaves into (list, snap),
+    // count and p1 histogram left on the device.
+    void compact(cudaStream_t st, int selector, long long key_limit, int32_t* list, int32_t* snap,
+                 int* counter, int* blockcnt, unsigned* hist) {
         LevelView F = V(D_);
-        LZB_CUDA(cudaMemsetAsync(counter_.p, 0, sizeof(int), s_));
-        LZB_CUDA(cudaMemsetAsync(hist_.p, 0, kNHist * sizeof(unsigned), s_));
+        LZB_CUDA(cudaMemsetAsync(hist, 0, kNHist * sizeof(unsigned), st));
         const long long* keys = key_limit >= 0 ? keys_.p : nullptr;
         const unsigned nb = blocks_for(leaves_, kCompactThreads);
-        LZB_LAUNCH(k_compact_count, nb, kCompactThreads, 0, s_, F, selector, keys, key_limit, blockcnt_.p);
-        LZB_LAUNCH(k_compact_scan, 1, 1024, 0, s_, blockcnt_.p, static_cast<int>(nb), counter_.p);
-        LZB_LAUNCH(k_compact_scatter, nb, kCompactThreads, 0, s_, F, selector, keys, key_limit, blockcnt_.p,
-                   list_.p, snap_.p, hist_.p);
+        LZB_LAUNCH(k_compact_count, nb, kCompactThreads, 0, st, F, selector, keys, key_limit, blockcnt);
+        LZB_LAUNCH(k_compact_scan, 1, 1024, 0, st, blockcnt, static_cast<int>(nb), counter);
+        LZB_LAUNCH(k_compact_scatter, nb, kCompactThreads, 0, st, F, selector, keys, key_limit, blockcnt, list,
+                   snap, hist);
+    }
+
+    // ------------------------------------------- concurrent (anarchic) assembly
+    // A batch = one adaptive step for every task pending when it starts, on the
+    // low-priority assembly stream, outcomes into the staging copy S; it is
+    // swapped in (k_commit) by the first cycle that finds its event complete.
+    LevelView staging() const {
+        LevelView S = V(D_);
+        S.op = sop_.p;
+        S.p1 = sp1_.p;
+        S.n = sn_.p;
+        S.p3 = sp3_.p;
+        S.epoch = sepoch_.p;
+        return S;
+    }
+
+    void launch_batch() {
+        LZB_CUDA(cudaEventRecord(ev_spawn_, s_));
+        LZB_CUDA(cudaStreamWaitEvent(a_, ev_spawn_, 0));
+        compact(a_, 1, -1, alist_.p, asnap_.p, acounter_.p, ablockcnt_.p, ahist_.p);
+        // tasks advance in lockstep (all cells start at n = 1, every pending task
+        // runs in every batch): the main kernel takes n = batch_n_, the generic
+        // kernel any entry that is off the lockstep
+        const int n = batch_n_;
+        const bool cap = d_.n_max > 0 && n >= d_.n_max;
+        const int nn = next_n(n);
+        if (!cap && !(atables_.n == nn && atables_.N == L_[D_].N))
+            atables_.build(d_.field, L_[D_].N, L_[D_].h, nn, a_);
+        const bool fast = d_.integration == LZB_INTEGRATE_FAST;
+        unsigned long long* stats = res_.p->s;
+        dispatch_step(fast, a_, V(D_), staging(), d_.field, alist_.p, asnap_.p, acounter_.p, leaves_, n, nn,
+                      cap, atables_.view(), d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p);
+        LZB_LAUNCH(k_step_generic, blocks_for(leaves_, kThreads), kThreads, 0, a_, V(D_), staging(), d_.field,
+                   alist_.p, asnap_.p, acounter_.p, n, d_.schedule, d_.n_max, fast ? 1 : 0, d_.termination_c,
+                   d_.delta_max, cycle_, stats, ctx_->err.p);
+        LZB_CUDA(cudaEventRecord(ev_batch_, a_));
+        batch_inflight_ = true;
+        batch_n_ = cap ? n : nn;
+        ++batches_launched_;
+    }
+
+    // Swap in the in-flight batch if it has finished (wait = block until it has).
+    bool try_commit(bool wait) {
+        if (!batch_inflight_) return false;
+        if (!wait) {
+            cudaError_t q = cudaEventQuery(ev_batch_);
+            if (q == cudaErrorNotReady) return false;
+            LZB_CUDA(q);
+        }
+        LZB_CUDA(cudaStreamWaitEvent(s_, ev_batch_, 0));
+        LZB_LAUNCH(k_commit, blocks_for(leaves_, kThreads), kThreads, 0, s_, V(D_), staging(), alist_.p,
+                   acounter_.p);
+        batch_inflight_ = false;
+        ++batches_committed_;
+        return true;
+    }
+
+    // TaskPool::drain_all (scheduler.cpp:125-141): finish every pending task.
+    void drain() {
+        if (d_.concurrent) try_commit(true);
+        if (d_.mode == LZB_ANARCHIC) {
+            while (count_pending() > 0) round(1, true);
+        }
+        pending_ = count_pending();
+    }
+
+    int64_t round(int selector, bool complete_tasks, long long key_limit = -1) {
+        LevelView F = V(D_);
+        compact(s_, selector, key_limit, list_.p, snap_.p, counter_.p, blockcnt_.p, hist_.p);
         LZB_CUDA(cudaMemcpyAsync(hhist_, hist_.p, kNHist * sizeof(unsigned), cudaMemcpyDeviceToHost, s_));
         LZB_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(hhist_) + kNHist * sizeof(unsigned),
                                  counter_.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
@@ -1305,13 +1481,8 @@ public:
             if (!cap) ensure_tables(nn);
             bool fast = d_.integration == LZB_INTEGRATE_FAST;
             const IntTables T = tables_.view();
-            switch (d_.field.kind) {
-                case LZB_FIELD_THETA: launch_step<LZB_FIELD_THETA>(fast, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, T, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
-                case LZB_FIELD_QUADRANT: launch_step<LZB_FIELD_QUADRANT>(fast, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, T, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
-                case LZB_FIELD_CHECKER: launch_step<LZB_FIELD_CHECKER>(fast, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, T, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
-                case LZB_FIELD_SINUSOID: launch_step<LZB_FIELD_SINUSOID>(fast, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, T, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
-                default: launch_step<LZB_FIELD_CONSTANT>(fast, s_, F, d_.field, list_.p, snap_.p, count, n, nn, cap, T, d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p); break;
-            }
+            dispatch_step(fast, s_, F, F, d_.field, list_.p, snap_.p, counter_.p, count, n, nn, cap, T,
+                          d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p);
         }
         if (complete_tasks)
             LZB_LAUNCH(k_clear_p2, blocks_for(count, kThreads), kThreads, 0, s_, F, list_.p, count);
@@ -1523,9 +1694,11 @@ public:
         lzb_cycle_report rep;
         std::memset(&rep, 0, sizeof rep);
         ++cycle_;
-        pool_begin_cycle();
+        if (d_.concurrent) try_commit(false);  // swap in a finished batch before the walk
+        else pool_begin_cycle();
         rep.cycle = static_cast<int32_t>(cycle_);
         assembly_pass();
+        if (d_.concurrent && !batch_inflight_ && (cycle_ == 1 || pending_ > 0)) launch_batch();
         residual_launches();
         stats_launches();
         fetch_result();
@@ -1587,6 +1760,7 @@ public:
             case 4: inject(); sync_check(); return 0.0;
             case 5: return 0.0;
             case 6: pool_begin_cycle(); sync_check(); pending_ = count_pending(); return 0.0;
+            case 7: drain(); sync_check(); return static_cast<double>(pending_);
             default: throw Error(LZB_ERR_INVALID, "unknown pass");
         }
     }
@@ -1792,6 +1966,25 @@ private:
     DevBuf<Result> res_;
     DevBuf<long long> keys_;
     TableSet tables_;
+    // concurrent assembly
+    cudaStream_t a_ = nullptr;
+    TableSet atables_;
+    DevBuf<int32_t> alist_, asnap_, sp1_, sn_;
+    DevBuf<int> acounter_, ablockcnt_;
+    DevBuf<unsigned> ahist_;
+    DevBuf<double> sop_;
+    DevBuf<int8_t> sp3_;
+    DevBuf<uint32_t> sepoch_;
+    cudaEvent_t ev_batch_ = nullptr, ev_spawn_ = nullptr;
+    bool batch_inflight_ = false;
+    int batch_n_ = 1;
+    int64_t batches_launched_ = 0, batches_committed_ = 0;
+
+public:
+    int64_t batches_launched() const { return batches_launched_; }
+    int64_t batches_committed() const { return batches_committed_; }
+
+private:
     DevBuf<int64_t> rec_sizes_, rec_offs_;
     DevBuf<unsigned char> scan_tmp_;
     DevBuf<uint8_t> img_;

@@ -221,3 +221,37 @@ def test_large_grid_properties():
     for lvl in range(1, 7):
         c, f = g.vertices(lvl - 1, lzb.T.V_U), g.vertices(lvl, lzb.T.V_U)
         assert np.array_equal(c, f[::3, ::3])
+
+
+@pytest.mark.parametrize("setup", ["setup = quadrant\neps-low = 1e-3", "setup = checkerboard\nfield-seed = 3"])
+def test_concurrent_anarchic_converges_to_eager_solution(setup):
+    """Assembly batches on the low-priority stream, swapped in via events: the
+    final operators are bit-identical to eager assembly (each cell's protocol
+    is timing-independent) and the solve reaches the same discrete solution."""
+    base = f"{setup}\ndepth = 4\nsolver = additive\nomega = 0.6\nrhs = 1\nseed = 11\nmax-cycles = 400\n"
+    k = port.parse_keys(base + "assembly = anarchic\n")
+    d = port.desc_from_keys(k)
+    d.concurrent = 1
+    g = lzb.Grid(d, 11)
+    reps = g.run()
+    assert reps[-1]["status"] == lzb.T.CONVERGED
+    assert g.drain() == 0
+    # eager reference: every leaf integrated to top before the solve
+    ke = port.parse_keys(base + "assembly = eager\n")
+    o = port.Grid(port.desc_from_keys(ke), 11)
+    o.run()
+    ca, cb = g.cells(4), o.cells(4)
+    assert np.all(ca["p1"] == lzb.T.P1_TOP)
+    assert np.array_equal(ca["ops"], cb["ops"]) and np.array_equal(ca["n"], cb["n"])
+    # continue the concurrent grid on the final operators to the same tolerance
+    d2 = port.desc_from_keys(port.parse_keys(base + "assembly = anarchic\n"))
+    more = [g.step() for _ in range(200)]
+    ue, ua = o.vertices(4, lzb.T.V_U), g.vertices(4, lzb.T.V_U)
+    assert np.max(np.abs(ua - ue)) <= 1e-7 * np.max(np.abs(ue))
+    del d2, more
+
+
+def test_concurrent_rejects_non_anarchic():
+    d = lzb.make_desc(depth=2, assembly="adaptive", concurrent=True)
+    with pytest.raises(lzb.LzbError):
+        lzb.Grid(d)
