@@ -6,7 +6,7 @@
  * as void* and are asynchronous on that stream.
  *
  * Each entry point names the reference interface it replaces
- * (/root/reference/proj/include/lazymg/*.hpp). The reference exposes C++
+ * (the headers under /root/reference/proj/include/lazymg). The reference exposes C++
  * only; these are the symbols its call sites bind through the host shim
  * (INTEGRATION.md). Errors: every function returns an lzb_status; the
  * message is in lzb_last_error() (thread-local). A missing GPU is

@@ -203,6 +203,34 @@ __device__ __forceinline__ double rt_bits(double x, int m) {
     return __longlong_as_double(static_cast<long long>(r));
 }
 
+// Byte `pos` (0..p3-1) of encode_value(x, p3) (codec.cpp:8-45) for finite x,
+// computed from the IEEE fields (same values as the frexp/ldexp form).
+__device__ __forceinline__ uint8_t encode_byte(double x, int p3, int pos) {
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(x));
+    if (p3 == 8) return static_cast<uint8_t>(u >> (8 * pos));  // memcpy, little endian
+    const int m = mantissa_bits(p3);
+    unsigned long long sign = 0, fb = 0;
+    int e_hat = -128;
+    if ((u << 1) != 0) {
+        sign = u >> 63;
+        const int E = static_cast<int>((u >> 52) & 0x7ff);
+        unsigned long long F = u & 0xFFFFFFFFFFFFFull;
+        int e;
+        if (E == 0) {
+            const int b = 63 - __clzll(static_cast<long long>(F));
+            e = b - 1074;
+            F = (F << (52 - b)) & 0xFFFFFFFFFFFFFull;
+        } else {
+            e = E - 1023;
+        }
+        e_hat = e < -128 ? -128 : (e > 127 ? 127 : e);
+        fb = F >> (52 - m);
+    }
+    if (pos == p3 - 1) return static_cast<uint8_t>(static_cast<int8_t>(e_hat));
+    const unsigned long long packed = (sign << m) | fb;
+    return static_cast<uint8_t>(packed >> (8 * (p3 - 2 - pos)));
+}
+
 // codec::roundtrip (codec.hpp:28-33) without the byte detour: the same
 // encode/decode arithmetic on registers. Returns false for non-finite.
 __device__ inline bool roundtrip_fast(double x, int p3, double& out) {

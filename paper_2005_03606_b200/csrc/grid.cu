@@ -396,31 +396,22 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_fixed(LevelView F, lzb_field
 // that contain both lattice vertices, in the reference's child order, zero
 // entries skipped) and out += P[k][.] * T[k][.] accumulates in ascending k,
 // which is exactly the reference's summation order — without the 16x16 A.
-// The nine children of each thread's cell are staged in shared memory,
-// entry-major ([entry][thread]) so that every access is bank-conflict free.
-constexpr int kCoarseThreads = 32;  // 144 doubles x 32 threads = 36 KB static smem
+// Each child entry feeds exactly one A entry, so the 144 child values are read
+// once each, straight from the (L1/L2-resident) fine operator array.
+constexpr int kCoarseThreads = 128;
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_geo(LevelView C, LevelView F, lzb_field f,
                                                                double delta_max, uint32_t cycle,
                                                                unsigned long long* stats, int* err) {
-    __shared__ double sch[144 * kCoarseThreads];
-    const int t = threadIdx.x;
     int64_t c = gtid();
-    const bool in = c < static_cast<int64_t>(C.N) * C.N;
-    const int cx = in ? static_cast<int>(c % C.N) : 0, cy = in ? static_cast<int>(c / C.N) : 0;
-    bool ready = in;
-    if (in)
-        for (int lx = 0; lx < 3; ++lx)
-            for (int ly = 0; ly < 3; ++ly) {
-                int64_t fc = static_cast<int64_t>(3 * cy + ly) * F.N + 3 * cx + lx;
-                if (F.p1[fc] == LZB_P1_BOTTOM) ready = false;  // delayed semantics (solver.cpp:65)
-                const double2* src = reinterpret_cast<const double2*>(F.op + 16 * fc);
-                for (int q = 0; q < 8; ++q) {
-                    double2 v = src[q];
-                    sch[((lx * 3 + ly) * 16 + 2 * q) * kCoarseThreads + t] = v.x;
-                    sch[((lx * 3 + ly) * 16 + 2 * q + 1) * kCoarseThreads + t] = v.y;
-                }
-            }
-    if (!ready) return;  // no block-level barrier follows
+    if (c >= static_cast<int64_t>(C.N) * C.N) return;
+    const int cx = static_cast<int>(c % C.N), cy = static_cast<int>(c / C.N);
+    const double* ch[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            int64_t fc = static_cast<int64_t>(3 * cy + j) * F.N + 3 * cx + i;
+            if (F.p1[fc] == LZB_P1_BOTTOM) return;  // delayed semantics (solver.cpp:65)
+            ch[i * 3 + j] = F.op + 16 * fc;
+        }
     double o[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) o[q] = 0.0;
@@ -440,7 +431,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_geo(LevelView C, Leve
                     const int ak = (kx - i) + 2 * (ky - j), am = (mx - i) + 2 * (my - j);
                     if (kx - i < 0 || kx - i > 1 || ky - j < 0 || ky - j > 1) continue;
                     if (mx - i < 0 || mx - i > 1 || my - j < 0 || my - j > 1) continue;
-                    a += sch[((i * 3 + j) * 16 + ak * 4 + am) * kCoarseThreads + t];
+                    a += __ldg(ch[i * 3 + j] + ak * 4 + am);
                 }
             if (a == 0.0) continue;  // transfer.cpp:189
             T0 += a * c_geo[m * 4 + 0];
@@ -656,18 +647,27 @@ __global__ void k_residual(LevelView F, lzb_field f) {
     double r = fl, rh = fl, dg = 0.0;
     Adj a = adjacent_cells(F, ix, iy);
     for (int q = 0; q < a.n; ++q) {
-        double K[16];
-        element_or_baseline(f, F, a.cx[q], a.cy[q], K);
-        int row = a.row[q];
+        // only this vertex's row of the cell matrix is needed: 32 B, two 16-B loads
+        const int row = a.row[q];
+        const int c = a.cy[q] * F.N + a.cx[q];
+        double Kr[4];
+        if (F.p1[c] != LZB_P1_BOTTOM) {
+            const double2* src = reinterpret_cast<const double2*>(F.op + 16 * static_cast<int64_t>(c) + 4 * row);
+            const double2 k01 = src[0], k23 = src[1];
+            Kr[0] = k01.x; Kr[1] = k01.y; Kr[2] = k23.x; Kr[3] = k23.y;
+        } else {
+            const double e = centre_eps(f, F, a.cx[q], a.cy[q]);
+            for (int col = 0; col < 4; ++col) Kr[col] = baseline_entry(row * 4 + col, e);
+        }
         double au = 0.0, auh = 0.0;
         for (int col = 0; col < 4; ++col) {
             int64_t cv = static_cast<int64_t>(a.cy[q] + cdy(col)) * NV + a.cx[q] + cdx(col);
-            au += K[row * 4 + col] * F.v[LZB_V_U][cv];
-            auh += K[row * 4 + col] * F.v[LZB_V_UHAT][cv];
+            au += Kr[col] * F.v[LZB_V_U][cv];
+            auh += Kr[col] * F.v[LZB_V_UHAT][cv];
         }
         r -= au;
         rh -= auh;
-        dg += K[row * 4 + row];
+        dg += Kr[row];
     }
     if (boundary(F.N, ix, iy)) {
         r = 0.0;
@@ -971,6 +971,95 @@ __global__ void k_pack(LevelView L, lzb_field f, int level, int leaf, SlotTable 
     if (!ok) atomicExch(err, 1);
 }
 
+// -------------------------------------------- slot-ordered stream packing
+// The LZMG image lists records in pre-order (stream.cpp:311-337). Working in
+// slot order, consecutive lanes own consecutive records, so a warp writes one
+// contiguous span; each record is emitted by the whole warp, 32 consecutive
+// bytes per store instruction (coalesced), every lane encoding its own byte.
+constexpr int kMaxLevels = 10;
+struct AllLevels {
+    LevelView L[kMaxLevels];
+    SlotTable st;
+    int D;
+};
+
+// slot -> (level, cx, cy): undo slot = sum_k (1 + ci_k * S_k), ci = lx*3 + ly.
+__device__ inline void decode_slot(int64_t s, const AllLevels& A, int& level, int& cx, int& cy) {
+    level = 0;
+    cx = cy = 0;
+    while (s != 0) {
+        s -= 1;
+        const int64_t sub = A.st.subtree[level + 1];
+        const int ci = static_cast<int>(s / sub);
+        s -= ci * sub;
+        cx = 3 * cx + ci / 3;
+        cy = 3 * cy + ci % 3;
+        ++level;
+    }
+}
+
+__global__ void k_record_sizes_slots(AllLevels A, int64_t total, int64_t* sizes) {
+    int64_t s = gtid();
+    if (s >= total) return;
+    int l, cx, cy;
+    decode_slot(s, A, l, cx, cy);
+    const LevelView& L = A.L[l];
+    const int64_t c = static_cast<int64_t>(cy) * L.N + cx;
+    const int32_t p1 = L.p1[c];
+    const int p3 = p1 != LZB_P1_BOTTOM ? L.p3[c] : 0;
+    sizes[s] = (p1 == LZB_P1_BOTTOM || p3 == 0) ? 1 : 1 + p3 * (l == A.D ? 16 : 144);
+}
+
+__global__ void k_pack_slots(AllLevels A, lzb_field f, int64_t total, const int64_t* __restrict__ offsets,
+                             uint8_t* __restrict__ out, int* err) {
+    const int lane = threadIdx.x & 31;
+    const int64_t s = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
+    int l = 0, cx = 0, cy = 0, p3 = 0, size = 0;
+    int64_t c = 0, off = 0;
+    uint8_t hdr = 0;
+    double e = 0.0;
+    if (s < total) {
+        decode_slot(s, A, l, cx, cy);
+        const LevelView& L = A.L[l];
+        c = static_cast<int64_t>(cy) * L.N + cx;
+        const int32_t p1 = L.p1[c];
+        p3 = p1 != LZB_P1_BOTTOM ? L.p3[c] : 0;
+        hdr = pack_header(p1, L.p2[c], p3);
+        size = (p1 == LZB_P1_BOTTOM || p3 == 0) ? 1 : 1 + p3 * (l == A.D ? 16 : 144);
+        off = 12 + offsets[s];
+        if (size > 1) e = centre_eps(f, L, cx, cy);
+    }
+    bool ok = true;
+    for (int r = 0; r < 32; ++r) {
+        const int rsize = __shfl_sync(0xffffffffu, size, r);
+        if (rsize == 0) continue;
+        const int64_t roff = __shfl_sync(0xffffffffu, off, r);
+        const uint8_t rhdr = static_cast<uint8_t>(__shfl_sync(0xffffffffu, static_cast<int>(hdr), r));
+        if (lane == 0) out[roff] = rhdr;
+        if (rsize == 1) continue;
+        const int rl = __shfl_sync(0xffffffffu, l, r);
+        const int rp3 = __shfl_sync(0xffffffffu, p3, r);
+        const int64_t rc = __shfl_sync(0xffffffffu, c, r);
+        const double re = __shfl_sync(0xffffffffu, e, r);
+        const LevelView& L = A.L[rl];
+        const double* op = L.op + 16 * rc;
+        const double* P = transfer_of(L, static_cast<int>(rc));
+        for (int b = 1 + lane; b < rsize; b += 32) {
+            const int i = (b - 1) / rp3, pos = (b - 1) - i * rp3;
+            double v;
+            if (i < 16) {
+                v = op[i] - baseline_entry(i, re);  // surplus of the stored matrix (stream.cpp:322-324)
+            } else {
+                const int k = (i - 16) & 63;        // P-hat, then the R-hat copy (stream.cpp:326-335)
+                v = P[k] - c_geo[k];
+            }
+            ok = ok && dev_isfinite(v);
+            out[roff + b] = encode_byte(v, rp3, pos);
+        }
+    }
+    if (!ok) atomicExch(err, 1);
+}
+
 // CellStream::load record (stream.cpp:355-392); offsets from the host parse.
 __global__ void k_unpack(LevelView L, lzb_field f, int level, int leaf, SlotTable st,
                          const int64_t* __restrict__ offsets, const uint8_t* __restrict__ in,
@@ -1254,7 +1343,7 @@ public:
     Grid(lzb_ctx* ctx, const lzb_grid_desc& d) : ctx_(ctx), d_(d), D_(d.depth) {
         if (d.dim != 2) throw Error(LZB_ERR_INVALID, "only dim = 2 is implemented in this round");
         if (d.depth < 1) throw Error(LZB_ERR_INVALID, "mesh depth must be >= 1");
-        if (d.depth > 9) throw Error(LZB_ERR_RESOURCE, "initial mesh depth exceeds the cell limit");
+        if (d.depth > kMaxLevels - 1) throw Error(LZB_ERR_RESOURCE, "initial mesh depth exceeds the cell limit");
         if (d.field.kind == LZB_FIELD_CHECKER && (d.field.blocks < 1 || d.field.blocks > 8))
             throw Error(LZB_ERR_INVALID, "checkerboard blocks must be in 1..8");
         LZB_CUDA(cudaSetDevice(ctx->device));
@@ -1841,10 +1930,17 @@ public:
     }
 
     // ------------------------------------------------------------ stream I/O
+    AllLevels all_levels() const {
+        AllLevels A{};
+        for (int l = 0; l <= D_; ++l) A.L[l] = V(l);
+        A.st = slots_;
+        A.D = D_;
+        return A;
+    }
+
     void record_sizes(int64_t* sizes) {
-        for (int l = 0; l <= D_; ++l)
-            LZB_LAUNCH(k_record_sizes, blocks_for(L_[l].nc, kThreads), kThreads, 0, s_, V(l), l,
-                       l == D_ ? 1 : 0, slots_, sizes);
+        LZB_LAUNCH(k_record_sizes_slots, blocks_for(total_cells_, kThreads), kThreads, 0, s_, all_levels(),
+                   total_cells_, sizes);
     }
 
     // Record sizes -> device exclusive scan (cub) -> total. Returns the image size.
@@ -1879,9 +1975,8 @@ public:
         if (img_.n < static_cast<size_t>(size)) img_.alloc(static_cast<size_t>(size) + (size >> 3));
         uint32_t hdr[3] = {0x4c5a4d47u, 1u, static_cast<uint32_t>(total_cells_)};
         std::memcpy(out, hdr, 12);
-        for (int l = 0; l <= D_; ++l)
-            LZB_LAUNCH(k_pack, blocks_for(L_[l].nc, kThreads), kThreads, 0, s_, V(l), d_.field, l,
-                       l == D_ ? 1 : 0, slots_, rec_offs_.p, img_.p, ctx_->err.p);
+        LZB_LAUNCH(k_pack_slots, blocks_for(total_cells_, kThreads), kThreads, 0, s_, all_levels(), d_.field,
+                   total_cells_, rec_offs_.p, img_.p, ctx_->err.p);
         LZB_CUDA(cudaMemcpyAsync(out + 12, img_.p + 12, size - 12, cudaMemcpyDeviceToHost, s_));
         sync_check();
         return size;

@@ -1,0 +1,64 @@
+"""Summarise an ncu launch list + a `--set full` report into profiles/<tag>_*.
+
+usage: python tools/summarize_profiles.py <tag> <launches.csv> <full.ncu-rep>
+"""
+import collections
+import csv
+import io
+import os
+import subprocess
+import sys
+
+tag, launches, rep = sys.argv[1], sys.argv[2], sys.argv[3]
+out_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
+rows = list(csv.reader(open(launches)))
+hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+h, data = rows[hi], rows[hi + 1:]
+ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+tot = collections.defaultdict(lambda: [0, 0.0])
+seq = []
+for r in data:
+    if len(r) <= vi:
+        continue
+    name = r[ki].split("(")[0].replace("lzb::<unnamed>::", "").replace("(anonymous namespace)::", "")
+    v = float(r[vi].replace(",", ""))
+    v = v * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(r[ui], 1.0)
+    tot[name][0] += 1
+    tot[name][1] += v
+    seq.append((name, v))
+grand = sum(t for _, t in tot.values())
+lines = [f"# {tag}: ncu launch list (gpu__time_duration, --clock-control none; cold-cache, serialised)", "",
+         f"source: `{os.path.basename(launches)}` ({len(seq)} launches, {grand:.1f} us total)", "",
+         "| kernel | launches | total us | share | avg us |", "|---|---|---|---|---|"]
+for name, (n, t) in sorted(tot.items(), key=lambda x: -x[1][1]):
+    lines.append(f"| `{name}` | {n} | {t:.1f} | {100 * t / grand:.1f}% | {t / n:.1f} |")
+open(os.path.join(out_dir, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
+with open(os.path.join(out_dir, f"{tag}_launches.csv"), "w") as f:
+    f.write("kernel,duration_us\n")
+    for name, v in seq:
+        f.write(f"{name},{v:.3f}\n")
+
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rr = list(csv.reader(io.StringIO(raw)))
+hdr, units, vals = rr[0], rr[1], rr[2:]
+want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__t_bytes.sum"]
+col = {w: hdr.index(w) for w in want if w in hdr}
+kn = hdr.index("Kernel Name")
+lines = [f"# {tag}: ncu --set full (selected metrics per captured launch)", "",
+         f"source: `{os.path.basename(rep)}`", "",
+         "| kernel | " + " | ".join(w.split(".")[0] + ("" if "pct" not in w else " %") for w in col) + " |",
+         "|---|" + "---|" * len(col)]
+for v in vals:
+    name = v[kn].split("(")[0].replace("lzb::<unnamed>::", "").replace("(anonymous namespace)::", "")
+    cells = []
+    for w, i in col.items():
+        u = units[i]
+        cells.append(f"{v[i]} {u}".strip())
+    lines.append(f"| `{name}` | " + " | ".join(cells) + " |")
+open(os.path.join(out_dir, f"{tag}_ncu_full.md"), "w").write("\n".join(lines) + "\n")
+print("\n".join(lines))
