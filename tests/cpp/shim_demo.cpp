@@ -38,7 +38,7 @@ int main(int argc, char** argv) {
                              -e, -2 * e, 4 * e, -e, -2 * e, -e, -e, 4 * e};
     for (int i = 0; i < 16; ++i) CHECK(std::fabs(em.m[i] - want[i]) <= 1e-14);
     // codec known answers (test_codec.cpp:21-35)
-    uint8_t b[2];
+    uint8_t b[8];
     lm::codec::encode_value(*ctx, 1.0, 2, b);
     CHECK(b[0] == 0x00 && b[1] == 0x00);
     lm::codec::encode_value(*ctx, -0.75, 2, b);
