@@ -397,25 +397,31 @@ struct LevelView {
     int32_t* n;
     uint32_t* epoch;
     uint8_t* has_P;
+    // change tracking for the coarse recompute: chg = 1 + cycle of the last
+    // publish of this cell (0 = never); seen = 1 + cycle of the last
+    // recompute attempt of a refined cell (0 = never)
+    uint32_t* chg;
+    uint32_t* seen;
 };
 
 __device__ inline int32_t crank(const LevelView& L, int cx, int cy) { return L.rx[cx] + L.ry[cy]; }
 
 // Owner patch (level l-1 cell) of fine vertex (fx,fy): the minimum-rank
 // refined patch whose 4x4 lattice contains it (solver.cpp:39-57).
+// Creation rank (and pre-order slot) is strictly increasing in cx for fixed cy
+// and in cy for fixed cx (rx, ry are increasing), so among the candidate
+// patches the lower-left one always has the smallest slot: the owner is the
+// patch with the smallest candidate x and y.
 __device__ inline void owner_patch(const LevelView& C, int fx, int fy, int& px, int& py) {
-    int x1 = fx / 3, y1 = fy / 3;
-    int x0 = (fx % 3 == 0 && x1 > 0) ? x1 - 1 : x1;
-    int y0 = (fy % 3 == 0 && y1 > 0) ? y1 - 1 : y1;
-    if (x1 > C.N - 1) x1 = C.N - 1;
-    if (y1 > C.N - 1) y1 = C.N - 1;
-    px = x0;
-    py = y0;
-    int32_t best = crank(C, x0, y0);
-    int32_t r;
-    if (x1 != x0 && (r = crank(C, x1, y0)) < best) { best = r; px = x1; py = y0; }
-    if (y1 != y0 && (r = crank(C, x0, y1)) < best) { best = r; px = x0; py = y1; }
-    if (x1 != x0 && y1 != y0 && (r = crank(C, x1, y1)) < best) { best = r; px = x1; py = y1; }
+    const int x1 = fx / 3, y1 = fy / 3;
+    px = (fx - 3 * x1 == 0 && x1 > 0) ? x1 - 1 : x1;
+    py = (fy - 3 * y1 == 0 && y1 > 0) ? y1 - 1 : y1;
+    if (px > C.N - 1) px = C.N - 1;
+    if (py > C.N - 1) py = C.N - 1;
+}
+// owns_lattice_vertex(c, lx, ly) in closed form (same argument).
+__device__ inline bool owns_lattice(int cx, int cy, int lx, int ly) {
+    return (lx != 0 || cx == 0) && (ly != 0 || cy == 0);
 }
 
 // Geometric transfer weights (transfer.cpp:11-21), as a function.

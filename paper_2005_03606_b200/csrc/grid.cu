@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <functional>
@@ -114,6 +115,7 @@ __device__ inline bool publish_leaf(const LevelView& F, int c, const double* m, 
     atomic_max_u64(&stats[S_MAXSAMPLES], static_cast<unsigned long long>(n));
     F.n[c] = n;
     F.epoch[c] = cycle;
+    F.chg[c] = cycle + 1;
     F.p3[c] = static_cast<int8_t>(p3);
     return true;
 }
@@ -155,6 +157,7 @@ __device__ inline bool publish_leaf_k9(const LevelView& F, int c, const double* 
     atomic_max_u64(&stats[S_MAXSAMPLES], static_cast<unsigned long long>(n));
     F.n[c] = n;
     F.epoch[c] = cycle;
+    F.chg[c] = cycle + 1;
     F.p3[c] = static_cast<int8_t>(p3);
     return true;
 }
@@ -400,11 +403,30 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_fixed(LevelView F, lzb_field
 // once each, straight from the (L1/L2-resident) fine operator array.
 constexpr int kCoarseThreads = 128;
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_geo(LevelView C, LevelView F, lzb_field f,
-                                                               double delta_max, uint32_t cycle,
+                                                               double delta_max, const uint32_t* cycle_ptr,
                                                                unsigned long long* stats, int* err) {
+    const uint32_t cycle = *cycle_ptr;  // device-resident: the cycle is replayed as a CUDA graph
     int64_t c = gtid();
     if (c >= static_cast<int64_t>(C.N) * C.N) return;
     const int cx = static_cast<int>(c % C.N), cy = static_cast<int>(c / C.N);
+
+    // policy `always` recomputes every refined cell each cycle (solver.cpp:83-85);
+    // recomputing a patch none of whose children changed since the last attempt
+    // reproduces the stored result bit for bit and publish_coarse would be a
+    // no-op (stream.cpp:153-158), so those patches are skipped
+    {
+        const uint32_t seen = C.seen[c];
+        if (seen != 0) {
+            uint32_t mx = 0;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) {
+                    const uint32_t v = F.chg[static_cast<int64_t>(3 * cy + j) * F.N + 3 * cx + i];
+                    mx = v > mx ? v : mx;
+                }
+            if (mx < seen) return;
+        }
+        C.seen[c] = cycle + 1;
+    }
     const double* ch[9];
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) {
@@ -492,6 +514,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_geo(LevelView C, Leve
     C.has_P[c] = 1;
     C.n[c] = 1;
     C.epoch[c] = cycle;
+    C.chg[c] = cycle + 1;
     C.p3[c] = static_cast<int8_t>(p3);
     C.p1[c] = LZB_P1_TOP;
 }
@@ -499,11 +522,30 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_geo(LevelView C, Leve
 // recompute_coarse + publish_coarse with BoxMG transfer (needs the full patch
 // operator A for the operator-dependent prolongation, transfer.cpp:95-180).
 __global__ void __launch_bounds__(64) k_coarse(LevelView C, LevelView F, lzb_field f, int boxmg,
-                                               double delta_max, uint32_t cycle,
+                                               double delta_max, const uint32_t* cycle_ptr,
                                                unsigned long long* stats, int* err) {
+    const uint32_t cycle = *cycle_ptr;
     int64_t c = gtid();
     if (c >= static_cast<int64_t>(C.N) * C.N) return;
     int cx = static_cast<int>(c % C.N), cy = static_cast<int>(c / C.N);
+
+    // policy `always` recomputes every refined cell each cycle (solver.cpp:83-85);
+    // recomputing a patch none of whose children changed since the last attempt
+    // reproduces the stored result bit for bit and publish_coarse would be a
+    // no-op (stream.cpp:153-158), so those patches are skipped
+    {
+        const uint32_t seen = C.seen[c];
+        if (seen != 0) {
+            uint32_t mx = 0;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) {
+                    const uint32_t v = F.chg[static_cast<int64_t>(3 * cy + j) * F.N + 3 * cx + i];
+                    mx = v > mx ? v : mx;
+                }
+            if (mx < seen) return;
+        }
+        C.seen[c] = cycle + 1;
+    }
     double ch[144];
     for (int lx = 0; lx < 3; ++lx)
         for (int ly = 0; ly < 3; ++ly) {
@@ -552,14 +594,20 @@ __global__ void __launch_bounds__(64) k_coarse(LevelView C, LevelView F, lzb_fie
     C.has_P[c] = 1;
     C.n[c] = 1;
     C.epoch[c] = cycle;
+    C.chg[c] = cycle + 1;
     C.p3[c] = static_cast<int8_t>(p3);
     C.p1[c] = LZB_P1_TOP;
 }
 
 // ------------------------------------------------------------------ cycle
-__device__ inline void vcoords(int64_t vi, int N, int& ix, int& iy) {
-    ix = static_cast<int>(vi % (N + 1));
-    iy = static_cast<int>(vi / (N + 1));
+// Vertex kernels run on a 2D grid: x = column block, y = vertex row (no
+// integer division for coordinates).
+__device__ inline bool vertex_xy(const LevelView& L, int& ix, int& iy, int64_t& vi) {
+    ix = blockIdx.x * blockDim.x + threadIdx.x;
+    iy = blockIdx.y;
+    if (ix > L.N) return false;
+    vi = static_cast<int64_t>(iy) * (L.N + 1) + ix;
+    return true;
 }
 __device__ inline bool boundary(int N, int ix, int iy) {
     return ix == 0 || iy == 0 || ix == N || iy == N;
@@ -571,38 +619,38 @@ struct Adj {
     int n;
     int cx[4], cy[4], row[4];
 };
+// Creation rank is strictly increasing in cx (fixed cy) and in cy (fixed cx),
+// so the lower-left cell comes first and the upper-right last; only the
+// lower-right / upper-left pair needs a rank comparison.
 __device__ inline Adj adjacent_cells(const LevelView& L, int ix, int iy) {
     Adj a;
     a.n = 0;
-    int32_t rk[4];
-    for (int dy = 0; dy < 2; ++dy)
-        for (int dx = 0; dx < 2; ++dx) {
-            int cx = ix - dx, cy = iy - dy;
-            if (cx < 0 || cy < 0 || cx >= L.N || cy >= L.N) continue;
-            int32_t r = crank(L, cx, cy);
-            int p = a.n++;
-            while (p > 0 && rk[p - 1] > r) {
-                rk[p] = rk[p - 1];
-                a.cx[p] = a.cx[p - 1];
-                a.cy[p] = a.cy[p - 1];
-                a.row[p] = a.row[p - 1];
-                --p;
-            }
-            rk[p] = r;
-            a.cx[p] = cx;
-            a.cy[p] = cy;
-            a.row[p] = dx + 2 * dy;
-        }
+    auto add = [&](int cx, int cy, int row) {
+        if (cx < 0 || cy < 0 || cx >= L.N || cy >= L.N) return;
+        a.cx[a.n] = cx;
+        a.cy[a.n] = cy;
+        a.row[a.n] = row;
+        ++a.n;
+    };
+    add(ix - 1, iy - 1, 3);  // the vertex is that cell's NE corner
+    const bool both = ix >= 1 && ix < L.N && iy >= 1 && iy < L.N;
+    if (!both || crank(L, ix, iy - 1) < crank(L, ix - 1, iy)) {
+        add(ix, iy - 1, 2);
+        add(ix - 1, iy, 1);
+    } else {
+        add(ix - 1, iy, 1);
+        add(ix, iy - 1, 2);
+    }
+    add(ix, iy, 0);
     return a;
 }
 
 // init_level_rhs on the leaf level (solver.cpp:99-118): fl = sum over
 // adjacent leaves of w * f(v) (identical terms, so order-free).
 __global__ void k_init_rhs(LevelView F, lzb_rhs rhs, double w) {
-    int64_t vi = gtid();
-    if (vi >= static_cast<int64_t>(F.N + 1) * (F.N + 1)) return;
     int ix, iy;
-    vcoords(vi, F.N, ix, iy);
+    int64_t vi;
+    if (!vertex_xy(F, ix, iy, vi)) return;
     int adj = 0;
     for (int dy = 0; dy < 2; ++dy)
         for (int dx = 0; dx < 2; ++dx) {
@@ -618,15 +666,14 @@ __global__ void k_init_rhs(LevelView F, lzb_rhs rhs, double w) {
 
 // compute_uhat (solver.cpp:120-143).
 __global__ void k_uhat(LevelView F, LevelView C, int has_coarse) {
-    int64_t vi = gtid();
-    if (vi >= static_cast<int64_t>(F.N + 1) * (F.N + 1)) return;
+    int fx, fy, px, py;
+    int64_t vi;
+    if (!vertex_xy(F, fx, fy, vi)) return;
     double u = F.v[LZB_V_U][vi];
     if (!has_coarse) {
         F.v[LZB_V_UHAT][vi] = u;
         return;
     }
-    int fx, fy, px, py;
-    vcoords(vi, F.N, fx, fy);
     owner_patch(C, fx, fy, px, py);
     const double* P = transfer_of(C, py * C.N + px);
     int L = (fy - 3 * py) * 4 + (fx - 3 * px);
@@ -638,10 +685,9 @@ __global__ void k_uhat(LevelView F, LevelView C, int has_coarse) {
 
 // residual_pass cell mat-vec, as a gather (solver.cpp:149-175).
 __global__ void k_residual(LevelView F, lzb_field f) {
-    int64_t vi = gtid();
-    if (vi >= static_cast<int64_t>(F.N + 1) * (F.N + 1)) return;
     int ix, iy;
-    vcoords(vi, F.N, ix, iy);
+    int64_t vi;
+    if (!vertex_xy(F, ix, iy, vi)) return;
     const int NV = F.N + 1;
     double fl = F.v[LZB_V_FL][vi];
     double r = fl, rh = fl, dg = 0.0;
@@ -683,10 +729,9 @@ __global__ void k_residual(LevelView F, lzb_field f) {
 // mode 0: rhs restriction of rhat into fl; mode 1: adaFAC-Jac smoothed
 // residual into aux (solver.cpp:250-268).
 __global__ void k_restrict(LevelView F, LevelView C, int mode, double omega) {
-    int64_t vi = gtid();
-    if (vi >= static_cast<int64_t>(C.N + 1) * (C.N + 1)) return;
     int IX, IY;
-    vcoords(vi, C.N, IX, IY);
+    int64_t vi;
+    if (!vertex_xy(C, IX, IY, vi)) return;
     const int NV = F.N + 1;
     Adj a = adjacent_cells(C, IX, IY);
     double acc_v = 0.0;
@@ -697,11 +742,7 @@ __global__ void k_restrict(LevelView F, LevelView C, int mode, double omega) {
         for (int L = 0; L < 16; ++L) {
             int lx = L & 3, ly = L >> 2;
             int fx = 3 * cx + lx, fy = 3 * cy + ly;
-            if (lx == 0 || lx == 3 || ly == 0 || ly == 3) {
-                int px, py;
-                owner_patch(C, fx, fy, px, py);
-                if (px != cx || py != cy) continue;
-            }
+            if (!owns_lattice(cx, cy, lx, ly)) continue;
             int64_t fi = static_cast<int64_t>(fy) * NV + fx;
             if (mode == 0) {
                 double rh = F.v[LZB_V_RHAT][fi];
@@ -724,13 +765,13 @@ __global__ void k_norm_partial(LevelView F, double* partial) {
     __shared__ double sh[kThreads];
     double s = 0.0;
     const int64_t nv = static_cast<int64_t>(F.N + 1) * (F.N + 1);
-    for (int64_t vi = gtid(); vi < nv; vi += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        int ix, iy;
-        vcoords(vi, F.N, ix, iy);
-        if (boundary(F.N, ix, iy)) continue;
-        double r = F.v[LZB_V_R][vi];
-        s += r * r;
-    }
+    (void)nv;
+    // rows blockIdx.x, +gridDim.x, ...; interior columns only (no division)
+    for (int iy = 1 + blockIdx.x; iy < F.N; iy += gridDim.x)
+        for (int ix = 1 + threadIdx.x; ix < F.N; ix += blockDim.x) {
+            double r = F.v[LZB_V_R][static_cast<int64_t>(iy) * (F.N + 1) + ix];
+            s += r * r;
+        }
     sh[threadIdx.x] = s;
     __syncthreads();
     for (int w = blockDim.x / 2; w > 0; w >>= 1) {
@@ -809,17 +850,15 @@ __global__ void k_snap(LevelView L) {
     L.v[LZB_V_AUX][vi] = 0.0;
 }
 __global__ void k_aux_inject(LevelView F, LevelView C) {  // adaFAC-PI: R~ = injection
-    int64_t vi = gtid();
-    if (vi >= static_cast<int64_t>(C.N + 1) * (C.N + 1)) return;
     int ix, iy;
-    vcoords(vi, C.N, ix, iy);
+    int64_t vi;
+    if (!vertex_xy(C, ix, iy, vi)) return;
     C.v[LZB_V_AUX][vi] = F.v[LZB_V_R][static_cast<int64_t>(3 * iy) * (F.N + 1) + 3 * ix];
 }
 __global__ void k_aux_Ar(LevelView F, lzb_field f) {  // adaFAC-Jac: aux = A r on level l
-    int64_t vi = gtid();
-    if (vi >= static_cast<int64_t>(F.N + 1) * (F.N + 1)) return;
     int ix, iy;
-    vcoords(vi, F.N, ix, iy);
+    int64_t vi;
+    if (!vertex_xy(F, ix, iy, vi)) return;
     const int NV = F.N + 1;
     Adj a = adjacent_cells(F, ix, iy);
     double aux = 0.0;
@@ -836,10 +875,9 @@ __global__ void k_aux_Ar(LevelView F, lzb_field f) {  // adaFAC-Jac: aux = A r o
 }
 // u_l -= P (omega/diag_c aux_c) on interior fine vertices (solver.cpp:271-297)
 __global__ void k_aux_sub(LevelView F, LevelView C, double omega) {
-    int64_t vi = gtid();
-    if (vi >= static_cast<int64_t>(F.N + 1) * (F.N + 1)) return;
     int fx, fy, px, py;
-    vcoords(vi, F.N, fx, fy);
+    int64_t vi;
+    if (!vertex_xy(F, fx, fy, vi)) return;
     if (boundary(F.N, fx, fy)) return;
     owner_patch(C, fx, fy, px, py);
     const double* P = transfer_of(C, py * C.N + px);
@@ -855,20 +893,18 @@ __global__ void k_aux_sub(LevelView F, LevelView C, double omega) {
     F.v[LZB_V_U][vi] -= p;
 }
 __global__ void k_jacobi(LevelView F, double damping) {
-    int64_t vi = gtid();
-    if (vi >= static_cast<int64_t>(F.N + 1) * (F.N + 1)) return;
     int ix, iy;
-    vcoords(vi, F.N, ix, iy);
+    int64_t vi;
+    if (!vertex_xy(F, ix, iy, vi)) return;
     if (boundary(F.N, ix, iy)) return;
     double dg = F.v[LZB_V_DIAG][vi];
     if (dg != 0.0) F.v[LZB_V_U][vi] += damping / dg * F.v[LZB_V_R][vi];
 }
 // prolong_corrections (solver.cpp:315-342)
 __global__ void k_prolong(LevelView F, LevelView C) {
-    int64_t vi = gtid();
-    if (vi >= static_cast<int64_t>(F.N + 1) * (F.N + 1)) return;
     int fx, fy, px, py;
-    vcoords(vi, F.N, fx, fy);
+    int64_t vi;
+    if (!vertex_xy(F, fx, fy, vi)) return;
     if (boundary(F.N, fx, fy)) return;
     owner_patch(C, fx, fy, px, py);
     double delta[4];
@@ -887,18 +923,16 @@ __global__ void k_prolong(LevelView F, LevelView C) {
 }
 // inject_solution (mesh.cpp:226-234)
 __global__ void k_inject(LevelView F, LevelView C) {
-    int64_t vi = gtid();
-    if (vi >= static_cast<int64_t>(C.N + 1) * (C.N + 1)) return;
     int ix, iy;
-    vcoords(vi, C.N, ix, iy);
+    int64_t vi;
+    if (!vertex_xy(C, ix, iy, vi)) return;
     C.v[LZB_V_U][vi] = F.v[LZB_V_U][static_cast<int64_t>(3 * iy) * (F.N + 1) + 3 * ix];
 }
 // init_noise (problem.cpp:50-68), before the injection.
 __global__ void k_noise(LevelView L, int level, uint64_t seed, double gval) {
-    int64_t vi = gtid();
-    if (vi >= static_cast<int64_t>(L.N + 1) * (L.N + 1)) return;
     int ix, iy;
-    vcoords(vi, L.N, ix, iy);
+    int64_t vi;
+    if (!vertex_xy(L, ix, iy, vi)) return;
     if (boundary(L.N, ix, iy)) {
         L.v[LZB_V_U][vi] = gval;
         return;
@@ -1073,6 +1107,7 @@ __global__ void k_unpack(LevelView L, lzb_field f, int level, int leaf, SlotTabl
     L.p2[c] = static_cast<uint8_t>(p2);
     if (cls == 0) {
         L.p1[c] = LZB_P1_BOTTOM;
+        L.chg[c] = cycle + 1;  // the payload disappears: parents must see it
         return;
     }
     double e = centre_eps(f, L, cx, cy);
@@ -1121,6 +1156,7 @@ __global__ void k_unpack(LevelView L, lzb_field f, int level, int leaf, SlotTabl
             L.has_P[c] = 1;
             L.n[c] = 1;
             L.epoch[c] = cycle;
+            L.chg[c] = cycle + 1;
             L.p3[c] = static_cast<int8_t>(q3);
         }
     }
@@ -1227,7 +1263,8 @@ __global__ void k_step_generic(LevelView F, LevelView D, lzb_field f, const int3
 // Swap-in of a completed concurrent batch, on the solve stream: the outcome of
 // every task in the batch becomes the live operator / marker, and the task
 // completes (p2 cleared, assembly.cpp:66-68).
-__global__ void k_commit(LevelView F, LevelView S, const int32_t* list, const int* count_ptr) {
+__global__ void k_commit(LevelView F, LevelView S, const int32_t* list, const int* count_ptr,
+                         uint32_t cycle) {
     int64_t t = gtid();
     if (t >= *count_ptr) return;
     const int c = list[t];
@@ -1239,6 +1276,7 @@ __global__ void k_commit(LevelView F, LevelView S, const int32_t* list, const in
         F.n[c] = S.n[c];
         F.p3[c] = S.p3[c];
         F.epoch[c] = S.epoch[c];
+        F.chg[c] = cycle + 1;  // swapped in at this cycle's start: the walk sees it
     }
     F.p1[c] = p1;
     F.p2[c] = 0;
@@ -1316,7 +1354,7 @@ struct Level {
     DevBuf<int32_t> p1, n;
     DevBuf<uint8_t> p2, has_P;
     DevBuf<int8_t> p3;
-    DevBuf<uint32_t> epoch;
+    DevBuf<uint32_t> epoch, chg, seen;
     LevelView view(int depth) const {
         LevelView L{};
         L.N = N;
@@ -1333,6 +1371,8 @@ struct Level {
         L.p3 = p3.p;
         L.n = n.p;
         L.epoch = epoch.p;
+        L.chg = chg.p;
+        L.seen = seen.p;
         L.has_P = has_P.p;
         return L;
     }
@@ -1379,6 +1419,10 @@ public:
             L.p2.alloc(L.nc);
             L.p3.alloc(L.nc);
             L.epoch.alloc(L.nc);
+            L.chg.alloc(L.nc);
+            L.seen.alloc(L.nc);
+            LZB_CUDA(cudaMemsetAsync(L.chg.p, 0, L.chg.bytes(), s_));
+            LZB_CUDA(cudaMemsetAsync(L.seen.p, 0, L.seen.bytes(), s_));
             L.has_P.alloc(L.nc);
             LZB_CUDA(cudaMemsetAsync(L.op.p, 0, L.op.bytes(), s_));
             LZB_CUDA(cudaMemsetAsync(L.p1.p, 0, L.p1.bytes(), s_));
@@ -1418,11 +1462,18 @@ public:
             sn_.alloc(leaves_);
             sp3_.alloc(leaves_);
             sepoch_.alloc(leaves_);
+            schg_.alloc(leaves_);
             LZB_CUDA(cudaEventCreateWithFlags(&ev_batch_, cudaEventDisableTiming));
             LZB_CUDA(cudaEventCreateWithFlags(&ev_spawn_, cudaEventDisableTiming));
         }
         LZB_CUDA(cudaMallocHost(&hres_, sizeof(Result)));
         LZB_CUDA(cudaMallocHost(&hhist_, kNHist * sizeof(unsigned) + sizeof(int)));
+        LZB_CUDA(cudaMallocHost(&hcycle_, sizeof(uint32_t)));
+        LZB_CUDA(cudaMallocHost(&herr_, sizeof(int)));
+        *hcycle_ = 0;
+        *herr_ = 0;
+        dcycle_.alloc(1);
+        use_graphs_ = std::getenv("LZB_NO_GRAPHS") == nullptr;
         // subtree sizes for pre-order slots
         for (int k = 0; k <= D_; ++k) {
             int64_t s = 0, p = 1;
@@ -1441,16 +1492,22 @@ public:
         if (ev_spawn_) cudaEventDestroy(ev_spawn_);
         if (hres_) cudaFreeHost(hres_);
         if (hhist_) cudaFreeHost(hhist_);
+        if (hcycle_) cudaFreeHost(hcycle_);
+        if (herr_) cudaFreeHost(herr_);
+        for (cudaGraphExec_t* e : {&g_coarse_, &g_front_, &g_back_})
+            if (*e) cudaGraphExecDestroy(*e);
     }
 
     LevelView V(int l) const { return L_[l].view(D_); }
+    // 2D launch geometry of the vertex kernels: x = column blocks, y = rows
+    dim3 vgrid(int l) const { return dim3(blocks_for(L_[l].N + 1, kThreads), L_[l].N + 1); }
     const lzb_grid_desc& desc() const { return d_; }
     int depth() const { return D_; }
     uint32_t cycle() const { return cycle_; }
 
     void init_noise(uint64_t seed) {
         for (int l = 0; l <= D_; ++l)
-            LZB_LAUNCH(k_noise, blocks_for(L_[l].nv, kThreads), kThreads, 0, s_, V(l), l, seed,
+            LZB_LAUNCH(k_noise, vgrid(l), kThreads, 0, s_, V(l), l, seed,
                        d_.boundary_value);
         inject();
         sync_check();
@@ -1495,6 +1552,7 @@ public:
         S.n = sn_.p;
         S.p3 = sp3_.p;
         S.epoch = sepoch_.p;
+        S.chg = schg_.p;  // publish into staging must not signal the live parents
         return S;
     }
 
@@ -1533,7 +1591,8 @@ public:
         }
         LZB_CUDA(cudaStreamWaitEvent(s_, ev_batch_, 0));
         LZB_LAUNCH(k_commit, blocks_for(leaves_, kThreads), kThreads, 0, s_, V(D_), staging(), alist_.p,
-                   acounter_.p);
+                   acounter_.p, cycle_);
+        all_top_ = false;
         batch_inflight_ = false;
         ++batches_committed_;
         return true;
@@ -1585,6 +1644,7 @@ public:
 
     void assemble_fixed(int n) {
         if (n < 1) throw Error(LZB_ERR_INVALID, "n must be >= 1");
+        all_top_ = true;  // every leaf ends at p1 = top
         ensure_tables(n);
         LevelView F = V(D_);
         bool fast = d_.integration == LZB_INTEGRATE_FAST;
@@ -1599,14 +1659,59 @@ public:
     }
 
     void coarse_pass() {  // pre-order semantics: coarse levels first, each reads l+1
+        // the epoch comes from pinned host memory at execution time (graph-replayable)
+        LZB_CUDA(cudaMemcpyAsync(dcycle_.p, hcycle_, sizeof(uint32_t), cudaMemcpyHostToDevice, s_));
         for (int l = 0; l < D_; ++l) {
             if (d_.transfer == LZB_BOXMG)
                 LZB_LAUNCH(k_coarse, blocks_for(L_[l].nc, 64), 64, 0, s_, V(l), V(l + 1), d_.field, 1,
-                           d_.delta_max, cycle_, res_.p->s, ctx_->err.p);
+                           d_.delta_max, dcycle_.p, res_.p->s, ctx_->err.p);
             else
                 LZB_LAUNCH(k_coarse_geo, blocks_for(L_[l].nc, kCoarseThreads), kCoarseThreads, 0, s_,
-                           V(l), V(l + 1), d_.field, d_.delta_max, cycle_, res_.p->s, ctx_->err.p);
+                           V(l), V(l + 1), d_.field, d_.delta_max, dcycle_.p, res_.p->s, ctx_->err.p);
         }
+    }
+
+    // ------------------------------------------------------------ CUDA graphs
+    // The fixed part of a cycle is replayed as two graphs: (coarse recompute +
+    // residual pass + stats + result copy) and (update + prolongation +
+    // injection). All kernel arguments are stable per grid; the epoch and the
+    // result travel through pinned host memory read/written at replay time.
+    void run_graph(cudaGraphExec_t& exec, void (Grid::*body)()) {
+        if (!use_graphs_) {
+            (this->*body)();
+            return;
+        }
+        const int slot = &exec == &g_coarse_ ? 0 : (&exec == &g_front_ ? 1 : 2);
+        if (!exec) {
+            cudaGraph_t g = nullptr;
+            const uint64_t l0 = g_launches.load();
+            LZB_CUDA(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal));
+            try {
+                (this->*body)();
+            } catch (...) {
+                cudaStreamEndCapture(s_, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            LZB_CUDA(cudaStreamEndCapture(s_, &g));
+            graph_kernels_[slot] = g_launches.load() - l0;  // kernels per replay
+            g_launches.fetch_sub(graph_kernels_[slot]);      // counted when they run
+            LZB_CUDA(cudaGraphInstantiate(&exec, g, 0));
+            LZB_CUDA(cudaGraphDestroy(g));
+        }
+        LZB_CUDA(cudaGraphLaunch(exec, s_));
+        g_launches.fetch_add(graph_kernels_[slot], std::memory_order_relaxed);
+    }
+    void front_body() {  // residual pass + stats + result / error flag D2H
+        residual_launches();
+        stats_launches();
+        LZB_CUDA(cudaMemcpyAsync(hres_, res_.p, sizeof(Result), cudaMemcpyDeviceToHost, s_));
+        LZB_CUDA(cudaMemcpyAsync(herr_, ctx_->err.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
+    }
+    void back_body() {  // update + prolongation + injection
+        update_launches();
+        prolong_launches();
+        inject();
     }
 
     void pool_begin_cycle() {  // TaskPool::begin_cycle, workers = 1 (scheduler.cpp:88-111)
@@ -1629,14 +1734,26 @@ public:
     }
 
     void assembly_pass() {  // solver.cpp:79-97
+        *hcycle_ = cycle_;
         coarse_pass();
+        leaves_pass();
+    }
+
+    // request_stencil over every leaf, mode by mode (assembly.cpp:76-109). Once a
+    // round has found every leaf converged (p1 = top) nothing can change until a
+    // publish / load / adaptive_step, so the compaction is skipped.
+    void leaves_pass() {
+        if (all_top_) return;
         switch (d_.mode) {
             case LZB_EAGER:
             case LZB_LAZY:
                 while (round(0, false) > 0) {
                 }
+                all_top_ = true;
                 break;
-            case LZB_ADAPTIVE: round(0, false); break;
+            case LZB_ADAPTIVE:
+                if (round(0, false) == 0) all_top_ = true;
+                break;
             case LZB_ANARCHIC:
                 round(2, false);  // the initial stencil computation is not deferred
                 LZB_LAUNCH(k_spawn, blocks_for(leaves_, kThreads), kThreads, 0, s_, V(D_), cycle_,
@@ -1649,16 +1766,16 @@ public:
         LevelView F = V(D_);
         bool rhs_on = d_.rhs.kind == LZB_RHS_SINPROD || d_.rhs.value != 0.0;
         if (rhs_on)
-            LZB_LAUNCH(k_init_rhs, blocks_for(L_[D_].nv, kThreads), kThreads, 0, s_, F, d_.rhs,
+            LZB_LAUNCH(k_init_rhs, vgrid(D_), kThreads, 0, s_, F, d_.rhs,
                        L_[D_].h * L_[D_].h / 4.0);
         else
             LZB_CUDA(cudaMemsetAsync(L_[D_].v[LZB_V_FL].p, 0, L_[D_].v[LZB_V_FL].bytes(), s_));
         for (int l = D_; l >= 0; --l) {
-            unsigned g = blocks_for(L_[l].nv, kThreads);
+            const dim3 g = vgrid(l);
             LZB_LAUNCH(k_uhat, g, kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
             LZB_LAUNCH(k_residual, g, kThreads, 0, s_, V(l), d_.field);
             if (l > 0)
-                LZB_LAUNCH(k_restrict, blocks_for(L_[l - 1].nv, kThreads), kThreads, 0, s_, V(l),
+                LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l),
                            V(l - 1), 0, 0.0);
         }
         LZB_LAUNCH(k_norm_partial, kNormBlocks, kThreads, 0, s_, F, partial_.p);
@@ -1678,9 +1795,9 @@ public:
             LZB_LAUNCH(k_snap, blocks_for(L_[l].nv, kThreads), kThreads, 0, s_, V(l));
         for (int l = D_; l >= 0; --l) {
             bool aux = d_.variant != LZB_ADDITIVE && l > 0;
-            unsigned g = blocks_for(L_[l].nv, kThreads);
+            const dim3 g = vgrid(l);
             if (aux) {
-                unsigned gc = blocks_for(L_[l - 1].nv, kThreads);
+                const dim3 gc = vgrid(l - 1);
                 if (d_.variant == LZB_ADAFAC_PI) {
                     LZB_LAUNCH(k_aux_inject, gc, kThreads, 0, s_, V(l), V(l - 1));
                 } else {
@@ -1696,12 +1813,12 @@ public:
 
     void prolong_launches() {
         for (int l = 1; l <= D_; ++l)
-            LZB_LAUNCH(k_prolong, blocks_for(L_[l].nv, kThreads), kThreads, 0, s_, V(l), V(l - 1));
+            LZB_LAUNCH(k_prolong, vgrid(l), kThreads, 0, s_, V(l), V(l - 1));
     }
 
     void inject() {
         for (int l = D_; l >= 1; --l)
-            LZB_LAUNCH(k_inject, blocks_for(L_[l - 1].nv, kThreads), kThreads, 0, s_, V(l), V(l - 1));
+            LZB_LAUNCH(k_inject, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1));
     }
 
     void fetch_result() {
@@ -1783,14 +1900,20 @@ public:
         lzb_cycle_report rep;
         std::memset(&rep, 0, sizeof rep);
         ++cycle_;
+        *hcycle_ = cycle_;
         if (d_.concurrent) try_commit(false);  // swap in a finished batch before the walk
         else pool_begin_cycle();
         rep.cycle = static_cast<int32_t>(cycle_);
-        assembly_pass();
+        run_graph(g_coarse_, &Grid::coarse_pass);
+        leaves_pass();
         if (d_.concurrent && !batch_inflight_ && (cycle_ == 1 || pending_ > 0)) launch_batch();
-        residual_launches();
-        stats_launches();
-        fetch_result();
+        run_graph(g_front_, &Grid::front_body);  // residual + stats + result/error copy-out
+        LZB_CUDA(cudaStreamSynchronize(s_));
+        if (*herr_) {
+            LZB_CUDA(cudaMemset(ctx_->err.p, 0, sizeof(int)));
+            *herr_ = 0;
+            throw Error(LZB_ERR_PROTOCOL, "cannot encode non-finite operator entry");
+        }
         Result r = *hres_;
         rep.residual = r.norm;
         if (first_residual_ < 0.0) first_residual_ = rep.residual > 0.0 ? rep.residual : 1.0;
@@ -1798,9 +1921,7 @@ public:
         history_.push_back(rep.residual);
         rep.status = check_termination();
         if (rep.status == LZB_CONTINUE || rep.status == LZB_TIMEOUT) {
-            update_launches();
-            prolong_launches();
-            inject();
+            run_graph(g_back_, &Grid::back_body);  // update + prolongation + injection
             uint64_t Nf = static_cast<uint64_t>(L_[D_].N);
             rep.dof_updates = (Nf - 1) * (Nf - 1);
             for (int l = 0; l < D_; ++l) {
@@ -1912,6 +2033,7 @@ public:
 
     void publish_element(int level, int cx, int cy, const double* m, int n, int32_t p1) {
         check_cell(level, cx, cy);
+        all_top_ = false;
         if (level != D_) throw Error(LZB_ERR_INVALID, "publish_element is for leaf cells");
         DevBuf<double> dm(16);
         LZB_CUDA(cudaMemcpyAsync(dm.p, m, 128, cudaMemcpyHostToDevice, s_));
@@ -1922,6 +2044,7 @@ public:
 
     void adaptive_step(int level, int cx, int cy) {
         check_cell(level, cx, cy);
+        all_top_ = false;
         if (level != D_) throw Error(LZB_ERR_INVALID, "adaptive steps are for leaf cells");
         LZB_LAUNCH(k_step_one, 1, 32, 0, s_, V(D_), d_.field, cy * L_[D_].N + cx, d_.schedule,
                    d_.n_max, d_.termination_c, d_.delta_max, cycle_,
@@ -1989,6 +2112,7 @@ public:
     }
 
     void load(const uint8_t* in, int64_t size) {  // CellStream::load (stream.cpp:340-394)
+        all_top_ = false;
         if (size < 4) throw Error(LZB_ERR_CORRUPT, "truncated stream file");
         uint32_t hdr[3] = {0, 0, 0};
         std::memcpy(&hdr[0], in, 4);
@@ -2069,7 +2193,7 @@ private:
     DevBuf<unsigned> ahist_;
     DevBuf<double> sop_;
     DevBuf<int8_t> sp3_;
-    DevBuf<uint32_t> sepoch_;
+    DevBuf<uint32_t> sepoch_, schg_;
     cudaEvent_t ev_batch_ = nullptr, ev_spawn_ = nullptr;
     bool batch_inflight_ = false;
     int batch_n_ = 1;
@@ -2087,6 +2211,13 @@ private:
     unsigned* hhist_ = nullptr;
     SlotTable slots_{};
     uint32_t cycle_ = 0;
+    uint32_t* hcycle_ = nullptr;  // pinned: read by the coarse-pass graph at replay
+    int* herr_ = nullptr;         // pinned: device error flag copied out by the front graph
+    DevBuf<uint32_t> dcycle_;
+    bool use_graphs_ = true;
+    bool all_top_ = false;        // every leaf converged (no request_stencil work left)
+    cudaGraphExec_t g_coarse_ = nullptr, g_front_ = nullptr, g_back_ = nullptr;
+    uint64_t graph_kernels_[3] = {0, 0, 0};
     double first_residual_ = -1.0;
     std::vector<double> history_;
     uint64_t dof_total_ = 0;
