@@ -149,7 +149,8 @@ class Context:
 
     def close(self):
         if getattr(self, "h", None):
-            lib().lzb_ctx_destroy(self.h)
+            if _lib is not None:  # interpreter teardown may have released the module
+                _lib.lzb_ctx_destroy(self.h)
             self.h = None
 
     __del__ = close
@@ -354,7 +355,8 @@ class Grid:
 
     def close(self):
         if getattr(self, "h", None):
-            lib().lzb_grid_destroy(self.h)
+            if _lib is not None:
+                _lib.lzb_grid_destroy(self.h)
             self.h = None
 
     __del__ = close

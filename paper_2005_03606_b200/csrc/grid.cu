@@ -39,7 +39,7 @@ constexpr int kNHist = 4097;      // p1 histogram bins (n < 4096)
 // Result block copied to the host once per cycle.
 struct Result {
     double norm;
-    unsigned long long s[16];
+    unsigned long long s[20];
 };
 enum StatSlot {
     S_HIST = 0,         // 0..8 p3 histogram over leaves
@@ -50,6 +50,7 @@ enum StatSlot {
     S_ZERO_NORM = 13,   // cumulative
     S_MAXDELTA = 14,    // cumulative, bits of a non-negative double
     S_MAXSAMPLES = 15,  // cumulative
+    S_PENDING = 16,     // leaves with a task in flight (p2), per cycle
 };
 
 __device__ inline int64_t gtid() { return blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; }
@@ -796,11 +797,12 @@ __global__ void k_norm_final(const double* partial, int n, Result* res) {
 
 // compression_stats over leaves + record bytes of refined cells (stream.cpp:268-301).
 __global__ void k_stats(LevelView L, int leaf, unsigned long long* s) {
-    __shared__ unsigned long long sh[16];
-    if (threadIdx.x < 16) sh[threadIdx.x] = 0;
+    __shared__ unsigned long long sh[20];
+    if (threadIdx.x < 20) sh[threadIdx.x] = 0;
     __syncthreads();
     int64_t c = gtid();
     const bool in = c < static_cast<int64_t>(L.N) * L.N;
+    const bool task = in && leaf && L.p2[c];
     int p3 = 0;
     unsigned bytes = 0, n = 0;
     if (in) {
@@ -827,9 +829,13 @@ __global__ void k_stats(LevelView L, int leaf, unsigned long long* s) {
             atomicAdd(&sh[S_NSUM], static_cast<unsigned long long>(wn));
             atomicMax(&sh[S_MAXN], static_cast<unsigned long long>(wmax));
         }
+        {
+            const unsigned np = __popc(__ballot_sync(full, task));
+            if (lead && np) atomicAdd(&sh[S_PENDING], static_cast<unsigned long long>(np));
+        }
     }
     __syncthreads();
-    if (threadIdx.x < 13 && sh[threadIdx.x]) {
+    if ((threadIdx.x < 13 || threadIdx.x == S_PENDING) && sh[threadIdx.x]) {
         if (threadIdx.x == S_MAXN) atomic_max_u64(&s[S_MAXN], sh[S_MAXN]);
         else atomicAdd(&s[threadIdx.x], sh[threadIdx.x]);
     }
@@ -1283,7 +1289,8 @@ __global__ void k_commit(LevelView F, LevelView S, const int32_t* list, const in
 }
 
 __global__ void k_reset_stats(Result* r) {
-    if (threadIdx.x < 13) r->s[threadIdx.x] = 0;  // per-cycle slots; the norm is written by k_norm_final
+    // per-cycle slots; the norm is written by k_norm_final
+    if (threadIdx.x < 13 || threadIdx.x == S_PENDING) r->s[threadIdx.x] = 0;
 }
 
 template <int KIND, bool FAST>
@@ -1931,7 +1938,10 @@ public:
         }
         dof_total_ += rep.dof_updates;
         rep.dof_updates_total = dof_total_;
-        pending_ = d_.mode == LZB_ANARCHIC ? count_pending() : 0;
+        pending_ = d_.mode == LZB_ANARCHIC ? static_cast<int64_t>(r.s[S_PENDING]) : 0;
+        // anarchic: no task pending and nothing bottom means every leaf is top
+        // (request_stencil spawns a task for every other leaf)
+        if (d_.mode == LZB_ANARCHIC && pending_ == 0 && !batch_inflight_) all_top_ = true;
         rep.pending_tasks = static_cast<uint64_t>(pending_);
         lzb_compression_stats st;
         fill_stats(r, st);
