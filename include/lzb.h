@@ -107,6 +107,16 @@ int lzb_grid_init_noise(lzb_grid* g, uint64_t seed);
 int lzb_grid_eager_setup(lzb_grid* g);
 /* Fixed-p assembly (BASELINE config 1): every leaf integrated at n, published, p1 = top. */
 int lzb_grid_assemble_fixed(lzb_grid* g, int n);
+/* Same for the leaf cell rows [row0, row1) only: one slab of a multi-GPU
+ * decomposition (cells are independent). */
+int lzb_grid_assemble_rows(lzb_grid* g, int n, int row0, int row1);
+/* Device pointers of one level's cell arrays (op: 16 doubles per cell, p1 i32,
+ * n i32, p3 i8, epoch u32, chg u32; index cy*N+cx), for in-place collectives. */
+int lzb_grid_cell_arrays(lzb_grid* g, int level, void** op, void** p1, void** n, void** p3,
+                         void** epoch, void** chg);
+/* The cell state was written through lzb_grid_cell_arrays: re-derive the
+ * engine's host-side bookkeeping before the next cycle. */
+int lzb_grid_invalidate(lzb_grid* g);
 /* AdditiveSolver::step / run_cycles                             solver.hpp:78-79 */
 int lzb_grid_step(lzb_grid* g, lzb_cycle_report* out);
 int lzb_grid_run(lzb_grid* g, lzb_cycle_report* out, int cap, int* count);

@@ -359,11 +359,12 @@ __global__ void k_spawn(LevelView F, uint32_t cycle, long long leaf_count, long 
 template <int KIND, bool FAST>
 __global__ void __launch_bounds__(kIntThreads, 2) k_fixed(LevelView F, lzb_field f, int n, IntTables T,
                                                           double delta_max, uint32_t cycle,
-                                                          unsigned long long* stats, int* err) {
+                                                          unsigned long long* stats, int* err,
+                                                          int64_t cbeg, int64_t cend) {
     extern __shared__ double sm[];
     stage_common(sm, f, T);
-    const int64_t ncell = static_cast<int64_t>(F.N) * F.N;
-    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * blockDim.x * kCPT;
+    const int64_t ncell = cend;  // cells [cbeg, cend): a slab of whole rows
+    const int64_t c0 = cbeg + static_cast<int64_t>(blockIdx.x) * blockDim.x * kCPT;
     const int64_t c1 = (c0 + static_cast<int64_t>(blockDim.x) * kCPT < ncell
                             ? c0 + static_cast<int64_t>(blockDim.x) * kCPT : ncell) - 1;
     const int row_lo = static_cast<int>(c0 / F.N), rows = static_cast<int>(c1 / F.N) - row_lo + 1;
@@ -1334,18 +1335,20 @@ inline void dispatch_step(bool fast, cudaStream_t s, const LevelView& F, const L
 
 template <int KIND, bool FAST>
 void launch_fixed_k(cudaStream_t s, const LevelView& F, const lzb_field& f, int n, const IntTables& T,
-                    double dmax, uint32_t cycle, unsigned long long* stats, int* err) {
+                    double dmax, uint32_t cycle, unsigned long long* stats, int* err, int64_t cbeg,
+                    int64_t cend) {
     size_t smem = int_smem_bytes(n);
     set_smem(k_fixed<KIND, FAST>, smem);
-    LZB_LAUNCH((k_fixed<KIND, FAST>), blocks_for(static_cast<int64_t>(F.N) * F.N, kIntThreads * kCPT),
-               kIntThreads, smem, s, F, f, n, T, dmax, cycle, stats, err);
+    LZB_LAUNCH((k_fixed<KIND, FAST>), blocks_for(cend - cbeg, kIntThreads * kCPT), kIntThreads, smem, s, F,
+               f, n, T, dmax, cycle, stats, err, cbeg, cend);
 }
 
 template <int KIND>
 void launch_fixed(bool fast, cudaStream_t s, const LevelView& F, const lzb_field& f, int n,
-                  const IntTables& T, double dmax, uint32_t cycle, unsigned long long* stats, int* err) {
-    if (fast) launch_fixed_k<KIND, true>(s, F, f, n, T, dmax, cycle, stats, err);
-    else launch_fixed_k<KIND, false>(s, F, f, n, T, dmax, cycle, stats, err);
+                  const IntTables& T, double dmax, uint32_t cycle, unsigned long long* stats, int* err,
+                  int64_t cbeg, int64_t cend) {
+    if (fast) launch_fixed_k<KIND, true>(s, F, f, n, T, dmax, cycle, stats, err, cbeg, cend);
+    else launch_fixed_k<KIND, false>(s, F, f, n, T, dmax, cycle, stats, err, cbeg, cend);
 }
 
 }  // namespace
@@ -1649,19 +1652,26 @@ public:
         }
     }
 
-    void assemble_fixed(int n) {
+    void assemble_fixed(int n) { assemble_fixed_rows(n, 0, L_[D_].N); }
+
+    // Fixed-p assembly of the leaf cell rows [row0, row1) (a slab of a
+    // multi-GPU decomposition: cells are independent, no exchange needed).
+    void assemble_fixed_rows(int n, int row0, int row1) {
         if (n < 1) throw Error(LZB_ERR_INVALID, "n must be >= 1");
-        all_top_ = true;  // every leaf ends at p1 = top
+        if (row0 < 0 || row1 > L_[D_].N || row0 >= row1) throw Error(LZB_ERR_INVALID, "bad row range");
+        const int64_t cbeg = static_cast<int64_t>(row0) * L_[D_].N, cend = static_cast<int64_t>(row1) * L_[D_].N;
+        // the whole level ends at p1 = top only when every row is assembled here
+        all_top_ = row0 == 0 && row1 == L_[D_].N;
         ensure_tables(n);
         LevelView F = V(D_);
         bool fast = d_.integration == LZB_INTEGRATE_FAST;
         unsigned long long* stats = res_.p->s;
         switch (d_.field.kind) {
-            case LZB_FIELD_THETA: launch_fixed<LZB_FIELD_THETA>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p); break;
-            case LZB_FIELD_QUADRANT: launch_fixed<LZB_FIELD_QUADRANT>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p); break;
-            case LZB_FIELD_CHECKER: launch_fixed<LZB_FIELD_CHECKER>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p); break;
-            case LZB_FIELD_SINUSOID: launch_fixed<LZB_FIELD_SINUSOID>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p); break;
-            default: launch_fixed<LZB_FIELD_CONSTANT>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p); break;
+            case LZB_FIELD_THETA: launch_fixed<LZB_FIELD_THETA>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p, cbeg, cend); break;
+            case LZB_FIELD_QUADRANT: launch_fixed<LZB_FIELD_QUADRANT>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p, cbeg, cend); break;
+            case LZB_FIELD_CHECKER: launch_fixed<LZB_FIELD_CHECKER>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p, cbeg, cend); break;
+            case LZB_FIELD_SINUSOID: launch_fixed<LZB_FIELD_SINUSOID>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p, cbeg, cend); break;
+            default: launch_fixed<LZB_FIELD_CONSTANT>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p, cbeg, cend); break;
         }
     }
 
@@ -2166,6 +2176,24 @@ public:
     }
 
     int64_t pending() const { return pending_; }
+
+    // The leaf state was modified outside the engine (e.g. rows received from
+    // other ranks): re-derive the converged flag on the next leaf pass.
+    void invalidate() {
+        LZB_CUDA(cudaStreamSynchronize(s_));
+        all_top_ = false;
+    }
+
+    void cell_arrays(int level, void** op, void** p1, void** n, void** p3, void** epoch, void** chg) {
+        check_level(level);
+        const Level& L = L_[level];
+        if (op) *op = L.op.p;
+        if (p1) *p1 = L.p1.p;
+        if (n) *n = L.n.p;
+        if (p3) *p3 = L.p3.p;
+        if (epoch) *epoch = L.epoch.p;
+        if (chg) *chg = L.chg.p;
+    }
     double* device_field(int level, int field) {
         check_level(level);
         if (field < 0 || field >= LZB_V_NFIELDS) throw Error(LZB_ERR_INVALID, "bad vertex field");
@@ -2267,6 +2295,19 @@ int lzb_grid_eager_setup(lzb_grid* g) {
         g->g->eager_setup();
         g->g->sync_check();
     });
+}
+int lzb_grid_assemble_rows(lzb_grid* g, int n, int row0, int row1) {
+    return guarded([&] {
+        g->g->assemble_fixed_rows(n, row0, row1);
+        g->g->sync_check();
+    });
+}
+int lzb_grid_invalidate(lzb_grid* g) {
+    return guarded([&] { g->g->invalidate(); });
+}
+int lzb_grid_cell_arrays(lzb_grid* g, int level, void** op, void** p1, void** n, void** p3, void** epoch,
+                         void** chg) {
+    return guarded([&] { g->g->cell_arrays(level, op, p1, n, p3, epoch, chg); });
 }
 int lzb_grid_assemble_fixed(lzb_grid* g, int n) {
     return guarded([&] {
