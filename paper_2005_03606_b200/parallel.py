@@ -85,7 +85,8 @@ def leaf_tensors(grid):
     op, p1, n, p3, ep, chg = (p.value for p in ptrs)
     return {"op": device_tensor(op, 16 * nc, "<f8"), "p1": device_tensor(p1, nc, "<i4"),
             "n": device_tensor(n, nc, "<i4"), "p3": device_tensor(p3, nc, "|i1"),
-            "epoch": device_tensor(ep, nc, "<u4"), "chg": device_tensor(chg, nc, "<u4")}
+            # u32 arrays travel as i32 (same bits; torch's NCCL group has no uint32)
+            "epoch": device_tensor(ep, nc, "<i4"), "chg": device_tensor(chg, nc, "<i4")}
 
 
 def distributed_assemble(grid, n: int, group=None):
