@@ -120,6 +120,8 @@ def dist_setup():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 or "TORCHELASTIC_RUN_ID" in os.environ:
+        # NCCL's own log lines ("NCCL version ...") go to stderr: stdout carries one JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
