@@ -395,6 +395,61 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_fixed(LevelView F, lzb_field
     }
 }
 
+// Persistent fixed-p assembly: one contiguous cell range per resident block,
+// the whole K_sub table and the range's eps rows staged once, then every
+// thread strides through its cells kCPT at a time with no barrier.
+template <int KIND, bool FAST>
+__global__ void __launch_bounds__(kIntThreads, 2) k_fixed_res(LevelView F, lzb_field f, int n, IntTables T,
+                                                              double delta_max, uint32_t cycle,
+                                                              unsigned long long* stats, int* err,
+                                                              int64_t cbeg, int64_t cend) {
+    extern __shared__ double sm[];
+    stage_common(sm, f, T);
+    if (!FAST) {
+        const double2* src = reinterpret_cast<const double2*>(T.ktab);
+        double2* dst = reinterpret_cast<double2*>(sm + 64 + kSeg * n);
+        for (int v = threadIdx.x; v < n * n * kKs / 2; v += blockDim.x) dst[v] = src[v];
+    }
+    const int64_t total = cend - cbeg;
+    const int64_t b0 = cbeg + blockIdx.x * total / gridDim.x;
+    const int64_t b1 = cbeg + (blockIdx.x + 1) * total / gridDim.x;
+    const int row_lo = static_cast<int>(b0 / F.N);
+    const int rows = b1 > b0 ? static_cast<int>((b1 - 1) / F.N) - row_lo + 1 : 0;
+    double* s_fy = nullptr;
+    if (rows > 0 && rows <= kFyRows) {
+        s_fy = res_fy_region(sm, n);
+        const double* src = T.fy + static_cast<size_t>(row_lo) * n;
+        for (int i = threadIdx.x; i < rows * n; i += blockDim.x) s_fy[i] = src[i];
+    }
+    __syncthreads();
+    for (int64_t base = b0 + threadIdx.x; base < b1; base += static_cast<int64_t>(kCPT) * blockDim.x) {
+        bool mine[kCPT];
+        int64_t cc[kCPT];
+        const double* fxc[kCPT];
+        const double* fyc[kCPT];
+#pragma unroll
+        for (int q = 0; q < kCPT; ++q) {
+            const int64_t c = base + static_cast<int64_t>(q) * blockDim.x;
+            mine[q] = c < b1;
+            cc[q] = mine[q] ? c : base;
+            const int cx = static_cast<int>(cc[q] % F.N), cy = static_cast<int>(cc[q] / F.N);
+            fxc[q] = T.fx + static_cast<int64_t>(cx) * n;
+            fyc[q] = s_fy ? s_fy + static_cast<int64_t>(cy - row_lo) * n : T.fy + static_cast<int64_t>(cy) * n;
+        }
+        double m[kCPT][16];
+        integrate_block<KIND, FAST, kCPT, true>(mine, f, T, fxc, fyc, sm, m);
+#pragma unroll
+        for (int q = 0; q < kCPT; ++q) {
+            if (!mine[q]) continue;
+            const int cx = static_cast<int>(cc[q] % F.N), cy = static_cast<int>(cc[q] / F.N);
+            if (!publish_leaf_k9(F, static_cast<int>(cc[q]), m[q], n, centre_eps(f, F, cx, cy), delta_max, cycle,
+                                 stats))
+                atomicExch(err, 1);
+            F.p1[cc[q]] = LZB_P1_TOP;
+        }
+    }
+}
+
 // recompute_coarse + publish_coarse for the geometric transfer (solver.cpp:59-77,
 // transfer.cpp:81-93,182-200, stream.cpp:134-184), register-streaming form:
 // T is produced one lattice row k at a time (A[k][m] summed over the children
@@ -1337,6 +1392,25 @@ template <int KIND, bool FAST>
 void launch_fixed_k(cudaStream_t s, const LevelView& F, const lzb_field& f, int n, const IntTables& T,
                     double dmax, uint32_t cycle, unsigned long long* stats, int* err, int64_t cbeg,
                     int64_t cend) {
+    const size_t rsmem = res_smem_bytes(n);
+    if (rsmem <= kResidentSmemMax) {  // persistent: K_sub table resident, one range per block
+        static int grid = 0;          // per instantiation: resident blocks x SMs
+        set_smem(k_fixed_res<KIND, FAST>, rsmem);
+        if (!grid) {
+            int dev = 0, sms = 0, per = 0;
+            LZB_CUDA(cudaGetDevice(&dev));
+            LZB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            LZB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fixed_res<KIND, FAST>, kIntThreads,
+                                                                   rsmem));
+            grid = (per > 0 ? per : 1) * sms;
+        }
+        // never more blocks than cell pairs
+        const int64_t want = (cend - cbeg + kCPT - 1) / kCPT;
+        const unsigned g = static_cast<unsigned>(want < grid ? (want > 0 ? want : 1) : grid);
+        LZB_LAUNCH((k_fixed_res<KIND, FAST>), g, kIntThreads, rsmem, s, F, f, n, T, dmax, cycle, stats, err,
+                   cbeg, cend);
+        return;
+    }
     size_t smem = int_smem_bytes(n);
     set_smem(k_fixed<KIND, FAST>, smem);
     LZB_LAUNCH((k_fixed<KIND, FAST>), blocks_for(cend - cbeg, kIntThreads * kCPT), kIntThreads, smem, s, F,

@@ -92,7 +92,7 @@ __device__ inline const double* stage_rows(double* sm, const IntTables& T, int r
 // column) and fyc[q][0..n) (its row); inactive cells must still point at
 // readable tables (their results are discarded). The CPT cells share every
 // K_sub / seg load and give the DP pipe CPT x 9 independent chains.
-template <int KIND, bool FAST, int CPT>
+template <int KIND, bool FAST, int CPT, bool RESIDENT = false>
 __device__ __forceinline__ void integrate_block(const bool* act, const lzb_field& f, const IntTables& T,
                                                 const double* const* fxc, const double* const* fyc,
                                                 double* sm, double (*out16)[16]) {
@@ -116,7 +116,7 @@ __device__ __forceinline__ void integrate_block(const bool* act, const lzb_field
         for (int q = 0; q < CPT; ++q)
 #pragma unroll
             for (int r = 0; r < 3; ++r) U[q][r] = V[q][r] = 0.0;
-        __syncthreads();  // seg / rows staged by the caller
+        if (!RESIDENT) __syncthreads();  // seg / rows staged by the caller
         if (any) {
             for (int i = 0; i < n; ++i) {
                 double xp[CPT], s0[CPT], s1[CPT], s2[CPT], t[CPT];
@@ -168,17 +168,20 @@ __device__ __forceinline__ void integrate_block(const bool* act, const lzb_field
             a[q][8] = -(U[q][1] + V[q][1]);
         }
     } else {
-        const int TI = ktile_rows(n);
+        // RESIDENT: the caller staged the whole K_sub table once (persistent kernels)
+        const int TI = RESIDENT ? n : ktile_rows(n);
         for (int i0 = 0; i0 < n; i0 += TI) {
             const int rows = (n - i0) < TI ? (n - i0) : TI;
-            __syncthreads();
-            {   // stage K_sub rows [i0, i0+rows) (contiguous in ktab), 16-byte vectors
-                const double2* src = reinterpret_cast<const double2*>(T.ktab + static_cast<size_t>(i0) * n * kKs);
-                double2* dst = reinterpret_cast<double2*>(s_k);
-                const int nvec = rows * n * kKs / 2;
-                for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = src[v];
+            if (!RESIDENT) {
+                __syncthreads();
+                {   // stage K_sub rows [i0, i0+rows) (contiguous in ktab), 16-byte vectors
+                    const double2* src = reinterpret_cast<const double2*>(T.ktab + static_cast<size_t>(i0) * n * kKs);
+                    double2* dst = reinterpret_cast<double2*>(s_k);
+                    const int nvec = rows * n * kKs / 2;
+                    for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = src[v];
+                }
+                __syncthreads();
             }
-            __syncthreads();
             if (any) {
                 for (int ii = 0; ii < rows; ++ii) {
                     double xp[CPT];
@@ -209,6 +212,16 @@ __device__ __forceinline__ void integrate_block(const bool* act, const lzb_field
     }
 #pragma unroll
     for (int q = 0; q < CPT; ++q) k9_expand(a[q], out16[q]);
+}
+
+// Persistent ("resident") layout: [64 table][4n seg][n*n*10 K_sub][kFyRows*n fy].
+constexpr size_t kResidentSmemMax = 100 * 1024;  // 2 blocks per SM
+__host__ __device__ inline size_t res_smem_bytes(int n) {
+    return (64 + static_cast<size_t>(kSeg) * n + static_cast<size_t>(n) * n * kKs +
+            static_cast<size_t>(kFyRows) * n) * 8;
+}
+__device__ inline double* res_fy_region(double* sm, int n) {
+    return sm + 64 + kSeg * n + static_cast<size_t>(n) * n * kKs;
 }
 
 // Table builders (runtime.cu).
