@@ -302,7 +302,14 @@ __device__ __forceinline__ int min_width(double v, double delta) {
 // (k9 order; the 16 entries repeat them, duplicates never change the result).
 // All-regular records take max(min_width) — exact by upward closure; any
 // irregular / zero / non-finite entry takes the general routine on all 16.
-__device__ inline int choose_precision_k9(const double* s9, const double* s16, double delta) {
+struct K9Vals {
+    double v[9];
+};
+// Irregular records (rare): expand to the 16 entries and take the general
+// routine; out of line so the caller's values stay in registers.
+__device__ __noinline__ int choose_precision_k9_general(K9Vals s, double delta);
+
+__device__ inline int choose_precision_k9(const double* s9, double delta) {
     bool all_small = true, regular = true;
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
@@ -310,7 +317,12 @@ __device__ inline int choose_precision_k9(const double* s9, const double* s16, d
         regular = regular && codec_regular(s9[i]);
     }
     if (all_small) return 0;
-    if (!regular) return choose_precision(s16, 16, delta);
+    if (!regular) {
+        K9Vals k;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) k.v[i] = s9[i];
+        return choose_precision_k9_general(k, delta);
+    }
     int P = 2;
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
@@ -429,6 +441,12 @@ __host__ __device__ inline double geo_weight(int L, int c) {
     int lx = L % 4, ly = L / 4;
     double fx = lx / 3.0, fy = ly / 3.0;
     return (cdx(c) ? fx : 1.0 - fx) * (cdy(c) ? fy : 1.0 - fy);
+}
+
+__device__ __noinline__ int choose_precision_k9_general(K9Vals s, double delta) {
+    double v16[16];
+    k9_expand(s.v, v16);
+    return choose_precision(v16, 16, delta);
 }
 
 }  // namespace lzb

@@ -125,20 +125,19 @@ __device__ inline bool publish_leaf(const LevelView& F, int c, const double* m, 
 // entries are the 9 k9 values by construction (k9_expand), as are the
 // baseline's (0 + K_unit*e): surplus, width choice and roundtrip run on the 9
 // distinct values; the stored 16 are their bitwise copies.
-__constant__ int c_k9pos[9] = {0, 5, 10, 15, 1, 11, 2, 7, 3};
+// (positions of the 9 distinct values in the 16 entries: compile-time, so m16 stays in registers)
 
 __device__ inline bool publish_leaf_k9(const LevelView& F, int c, const double* m16, int n, double e_c,
                                        double delta_max, uint32_t cycle, unsigned long long* stats) {
     double base9[9], sur9[9];
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
-        const int k = c_k9pos[i];
+        constexpr int kpos[9] = {0, 5, 10, 15, 1, 11, 2, 7, 3};
+        const int k = kpos[i];
         base9[i] = baseline_entry(k, e_c);
         sur9[i] = m16[k] - base9[i];
     }
-    double sur16[16];
-    k9_expand(sur9, sur16);
-    const int p3 = choose_precision_k9(sur9, sur16, delta_max);
+    const int p3 = choose_precision_k9(sur9, delta_max);
     if (p3 < 0) return false;
     double delta = 0.0, dec9[9];
 #pragma unroll
@@ -337,7 +336,7 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_step(LevelView F, LevelView 
         if (ratio < term_c) {
             D.p1[c] = LZB_P1_TOP;  // keep the old matrix (assembly.cpp:47-53)
         } else {
-            double e_c = centre_eps(f, F, cx, cy);
+            const double e_c = combine_k<KIND>(T.cxp[cx], T.cyp[cy], f.value, f.eps_low, f.blocks, sm);
             if (!publish_leaf_k9(D, c, fresh[q], nn, e_c, delta_max, cycle, stats)) atomicExch(err, 1);
             D.p1[c] = nn;
         }
@@ -388,7 +387,7 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_fixed(LevelView F, lzb_field
     for (int q = 0; q < kCPT; ++q) {
         if (!mine[q]) continue;
         const int cx = static_cast<int>(cc[q] % F.N), cy = static_cast<int>(cc[q] / F.N);
-        double e_c = centre_eps(f, F, cx, cy);
+        const double e_c = combine_k<KIND>(T.cxp[cx], T.cyp[cy], f.value, f.eps_low, f.blocks, sm);
         if (!publish_leaf_k9(F, static_cast<int>(cc[q]), m[q], n, e_c, delta_max, cycle, stats))
             atomicExch(err, 1);
         F.p1[cc[q]] = LZB_P1_TOP;
@@ -442,8 +441,8 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_fixed_res(LevelView F, lzb_f
         for (int q = 0; q < kCPT; ++q) {
             if (!mine[q]) continue;
             const int cx = static_cast<int>(cc[q] % F.N), cy = static_cast<int>(cc[q] / F.N);
-            if (!publish_leaf_k9(F, static_cast<int>(cc[q]), m[q], n, centre_eps(f, F, cx, cy), delta_max, cycle,
-                                 stats))
+            const double e_c = combine_k<KIND>(T.cxp[cx], T.cyp[cy], f.value, f.eps_low, f.blocks, sm);
+            if (!publish_leaf_k9(F, static_cast<int>(cc[q]), m[q], n, e_c, delta_max, cycle, stats))
                 atomicExch(err, 1);
             F.p1[cc[q]] = LZB_P1_TOP;
         }

@@ -35,6 +35,8 @@ struct IntTables {
     const double* fy;    // [N][n] y field parts
     const double* seg;   // [n][4]
     const double* ktab;  // [n][n][10]
+    const double* cxp;   // [N] x field part at the cell centre (the n = 1 sample)
+    const double* cyp;   // [N] y field part at the cell centre
     int n;
 };
 

@@ -17,10 +17,10 @@ void upload_constants();
 
 // Per-n integration tables (integrate.cuh), rebuilt on demand.
 struct TableSet {
-    DevBuf<double> fx, fy, seg, ktab;
+    DevBuf<double> fx, fy, seg, ktab, cxp, cyp;
     int n = 0, N = 0;
     void build(const lzb_field& f, int N, double h, int n, cudaStream_t s);
-    IntTables view() const { return IntTables{fx.p, fy.p, seg.p, ktab.p, n}; }
+    IntTables view() const { return IntTables{fx.p, fy.p, seg.p, ktab.p, cxp.p, cyp.p, n}; }
 };
 template <typename K>
 void set_smem(K kernel, size_t bytes);

@@ -128,6 +128,14 @@ void TableSet::build(const lzb_field& f, int N_, double h, int n_, cudaStream_t 
         LZB_CUDA(cudaStreamSynchronize(s));
         ktab.alloc(static_cast<size_t>(n_) * n_ * kKs);
     }
+    if (cxp.n < static_cast<size_t>(N_)) {
+        LZB_CUDA(cudaStreamSynchronize(s));
+        cxp.alloc(N_);
+        cyp.alloc(N_);
+    }
+    // cell-centre parts: the n = 1 sample, x0 + ((0+0.5)*1.0)*h (element.hpp:44)
+    LZB_LAUNCH(k_field_parts, blocks_for(N_, 256), 256, 0, s, f, N_, h, 1, 0, cxp.p);
+    LZB_LAUNCH(k_field_parts, blocks_for(N_, 256), 256, 0, s, f, N_, h, 1, 1, cyp.p);
     unsigned g = blocks_for(static_cast<int64_t>(nf), 256);
     LZB_LAUNCH(k_field_parts, g, 256, 0, s, f, N_, h, n_, 0, fx.p);
     LZB_LAUNCH(k_field_parts, g, 256, 0, s, f, N_, h, n_, 1, fy.p);
