@@ -149,6 +149,10 @@ int lzb_grid_load(lzb_grid* g, const char* path);
 int64_t lzb_grid_pending(lzb_grid* g);
 /* Device pointers for callers composing their own kernels (read-only use). */
 int lzb_grid_device_view(lzb_grid* g, int level, int field, void** ptr);
+/* Device time (CUDA events on the solve stream) of one hot kernel of the
+ * leaf level, averaged over `reps` back-to-back launches: LZB_TK_* ids.
+ * No reference counterpart: the measurement hook behind bench.py's roofline. */
+int lzb_grid_time_kernel(lzb_grid* g, int what, int reps, double* avg_ms);
 
 /* -------------------------------------------------------------- experiment */
 /* run_experiment(parse_config_file(path))               experiment.hpp:75,89

@@ -160,6 +160,12 @@ enum lzb_vertex_field {
     LZB_V_DIAG = 5, LZB_V_AUX = 6, LZB_V_USNAP = 7, LZB_V_NFIELDS = 8
 };
 
+/* kernels timed by lzb_grid_time_kernel (leaf level) */
+enum {
+    LZB_TK_UHAT = 0, LZB_TK_RESIDUAL = 1, LZB_TK_RESTRICT = 2, LZB_TK_JACOBI = 3,
+    LZB_TK_PROLONG = 4, LZB_TK_PACK = 5, LZB_TK_FRONT = 6, LZB_TK_BACK = 7
+};
+
 #ifdef __cplusplus
 }
 #endif

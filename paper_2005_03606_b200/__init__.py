@@ -21,7 +21,8 @@ import numpy as np
 
 from . import _types as T
 from ._types import (CompressionStats, CycleReport, Field, GridDesc, Rhs, field_checkerboard,  # noqa: F401
-                     field_constant, field_quadrant, field_sinusoid, field_theta, report_dict)
+                     field_constant, field_quadrant, field_sinusoid, field_theta, report_dict,
+                     TK_UHAT, TK_RESIDUAL, TK_RESTRICT, TK_JACOBI, TK_PROLONG, TK_PACK, TK_FRONT, TK_BACK)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "liblzb.so")
@@ -114,6 +115,7 @@ def lib():
         L.lzb_grid_pending.restype = i64
         L.lzb_grid_pending.argtypes = [vp]
         L.lzb_grid_device_view.argtypes = [vp, C.c_int, C.c_int, C.POINTER(vp)]
+        L.lzb_grid_time_kernel.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.lzb_run_experiment_file.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.lzb_run_experiment_text.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.lzb_last_reports.argtypes = [vp, C.c_int, C.POINTER(C.c_int)]
@@ -446,6 +448,11 @@ class Grid:
         _check(lib().lzb_grid_stream_image(self.h, _ptr(buf), buf.size, C.byref(size)))
         return buf[: size.value].tobytes()
 
+    def stream_image_size(self) -> int:
+        size = C.c_int64()
+        _check(lib().lzb_grid_stream_image(self.h, None, 0, C.byref(size)))
+        return size.value
+
     def load_image(self, data: bytes):
         b = np.frombuffer(data, np.uint8).copy()
         _check(lib().lzb_grid_stream_load(self.h, _ptr(b), b.size))
@@ -463,6 +470,12 @@ class Grid:
         p = C.c_void_p()
         _check(lib().lzb_grid_device_view(self.h, level, field, C.byref(p)))
         return p.value
+
+    def time_kernel(self, what, reps=20) -> float:
+        """Average device ms of one leaf-level kernel (TK_* id), CUDA events on the solve stream."""
+        ms = C.c_double()
+        _check(lib().lzb_grid_time_kernel(self.h, what, reps, C.byref(ms)))
+        return ms.value
 
 
 # ------------------------------------------------------------------ experiment

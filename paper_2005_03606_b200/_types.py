@@ -18,6 +18,8 @@ SCHEDULE_INCREMENT, SCHEDULE_DOUBLE = range(2)
 INTEGRATE_EXACT, INTEGRATE_FAST = range(2)
 P1_BOTTOM, P1_TOP = 0, -1
 V_U, V_FL, V_R, V_RHAT, V_UHAT, V_DIAG, V_AUX, V_USNAP = range(8)
+# lzb_grid_time_kernel ids (lzb_types.h)
+TK_UHAT, TK_RESIDUAL, TK_RESTRICT, TK_JACOBI, TK_PROLONG, TK_PACK, TK_FRONT, TK_BACK = range(8)
 
 STATUS_NAMES = {CONTINUE: "continue", CONVERGED: "converged", DIVERGED: "diverged", TIMEOUT: "timeout"}
 

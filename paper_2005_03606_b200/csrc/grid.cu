@@ -740,38 +740,79 @@ __global__ void k_uhat(LevelView F, LevelView C, int has_coarse) {
 }
 
 // residual_pass cell mat-vec, as a gather (solver.cpp:149-175).
-__global__ void k_residual(LevelView F, lzb_field f) {
+//
+// The four adjacent cells sit at fixed positions q = b*2 + a, cell
+// (ix-1+a, iy-1+b), the vertex being its corner row (1-a) + 2(1-b). Every
+// load (four 32-B operator rows, p1, the 3x3 u / uhat neighbourhood) is
+// issued up front, independent of the creation-rank order, which only picks
+// the accumulation order of positions 1 and 2 afterwards.
+__global__ void __launch_bounds__(kThreads) k_residual(LevelView F, lzb_field f) {
     int ix, iy;
     int64_t vi;
     if (!vertex_xy(F, ix, iy, vi)) return;
-    const int NV = F.N + 1;
-    double fl = F.v[LZB_V_FL][vi];
-    double r = fl, rh = fl, dg = 0.0;
-    Adj a = adjacent_cells(F, ix, iy);
-    for (int q = 0; q < a.n; ++q) {
-        // only this vertex's row of the cell matrix is needed: 32 B, two 16-B loads
-        const int row = a.row[q];
-        const int c = a.cy[q] * F.N + a.cx[q];
-        double Kr[4];
-        if (F.p1[c] != LZB_P1_BOTTOM) {
-            const double2* src = reinterpret_cast<const double2*>(F.op + 16 * static_cast<int64_t>(c) + 4 * row);
-            const double2 k01 = src[0], k23 = src[1];
-            Kr[0] = k01.x; Kr[1] = k01.y; Kr[2] = k23.x; Kr[3] = k23.y;
-        } else {
-            const double e = centre_eps(f, F, a.cx[q], a.cy[q]);
+    const int N = F.N, NV = N + 1;
+    bool has[4];
+    has[0] = ix >= 1 && iy >= 1;
+    has[1] = ix < N && iy >= 1;
+    has[2] = ix >= 1 && iy < N;
+    has[3] = ix < N && iy < N;
+    double2 k01[4], k23[4];
+    int32_t p1[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int a = q & 1, b = q >> 1, row = (1 - a) + 2 * (1 - b);
+        const int cx = has[q] ? ix - 1 + a : 0, cy = has[q] ? iy - 1 + b : 0;
+        const int64_t c = static_cast<int64_t>(cy) * N + cx;
+        const double2* src = reinterpret_cast<const double2*>(F.op + 16 * c + 4 * row);
+        k01[q] = __ldcs(src);
+        k23[q] = __ldcs(src + 1);
+        p1[q] = F.p1[c];
+    }
+    double uu[3][3], uh[3][3];
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+            const int x = min(max(ix - 1 + dx, 0), N), y = min(max(iy - 1 + dy, 0), N);
+            const int64_t cv = static_cast<int64_t>(y) * NV + x;
+            uu[dy][dx] = F.v[LZB_V_U][cv];
+            uh[dy][dx] = F.v[LZB_V_UHAT][cv];
+        }
+    const double fl = F.v[LZB_V_FL][vi];
+    // creation-rank order: position 0 first, 3 last; 1 before 2 unless the rank says otherwise
+    const bool both = has[0] && has[3];
+    const bool swap12 = both && !(crank(F, ix, iy - 1) < crank(F, ix - 1, iy));
+    double au[4], auh[4], kd[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int a = q & 1, b = q >> 1, row = (1 - a) + 2 * (1 - b);
+        double Kr[4] = {k01[q].x, k01[q].y, k23[q].x, k23[q].y};
+        if (has[q] && p1[q] == LZB_P1_BOTTOM) {
+            const double e = centre_eps(f, F, ix - 1 + a, iy - 1 + b);
             for (int col = 0; col < 4; ++col) Kr[col] = baseline_entry(row * 4 + col, e);
         }
-        double au = 0.0, auh = 0.0;
+        double s = 0.0, sh = 0.0;
+#pragma unroll
         for (int col = 0; col < 4; ++col) {
-            int64_t cv = static_cast<int64_t>(a.cy[q] + cdy(col)) * NV + a.cx[q] + cdx(col);
-            au += Kr[col] * F.v[LZB_V_U][cv];
-            auh += Kr[col] * F.v[LZB_V_UHAT][cv];
+            const int dy = b + cdy(col), dx = a + cdx(col);
+            s += Kr[col] * uu[dy][dx];
+            sh += Kr[col] * uh[dy][dx];
         }
-        r -= au;
-        rh -= auh;
-        dg += Kr[row];
+        au[q] = s;
+        auh[q] = sh;
+        kd[q] = Kr[row];
     }
-    if (boundary(F.N, ix, iy)) {
+    // accumulate in creation-rank order (positions 1 and 2 possibly swapped)
+    const double a1 = swap12 ? au[2] : au[1], a2 = swap12 ? au[1] : au[2];
+    const double h1 = swap12 ? auh[2] : auh[1], h2 = swap12 ? auh[1] : auh[2];
+    const double d1 = swap12 ? kd[2] : kd[1], d2 = swap12 ? kd[1] : kd[2];
+    const bool e1 = swap12 ? has[2] : has[1], e2 = swap12 ? has[1] : has[2];
+    double r = fl, rh = fl, dg = 0.0;
+    if (has[0]) { r -= au[0]; rh -= auh[0]; dg += kd[0]; }
+    if (e1) { r -= a1; rh -= h1; dg += d1; }
+    if (e2) { r -= a2; rh -= h2; dg += d2; }
+    if (has[3]) { r -= au[3]; rh -= auh[3]; dg += kd[3]; }
+    if (boundary(N, ix, iy)) {
         r = 0.0;
         rh = 0.0;
     }
@@ -2198,6 +2239,55 @@ public:
         return size;
     }
 
+    // Device time of one hot kernel of the cycle / stream path on the solve
+    // stream: `reps` back-to-back launches bracketed by CUDA events, average
+    // ms per launch. The kernels run on the grid's live state (idempotent
+    // except the Jacobi / prolongation updates of u, which only drift it).
+    double time_kernel(int what, int reps) {
+        if (reps < 1) throw Error(LZB_ERR_INVALID, "reps must be >= 1");
+        const int l = D_;
+        if (what == LZB_TK_PACK) {
+            const int64_t size = scan_records();
+            if (img_.n < static_cast<size_t>(size)) img_.alloc(static_cast<size_t>(size) + (size >> 3));
+        }
+        if ((what == LZB_TK_RESTRICT || what == LZB_TK_PROLONG) && D_ < 1)
+            throw Error(LZB_ERR_INVALID, "needs depth >= 1");
+        auto launch = [&] {
+            switch (what) {
+                case LZB_TK_UHAT:
+                    LZB_LAUNCH(k_uhat, vgrid(l), kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
+                    break;
+                case LZB_TK_RESIDUAL: LZB_LAUNCH(k_residual, vgrid(l), kThreads, 0, s_, V(l), d_.field); break;
+                case LZB_TK_RESTRICT:
+                    LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1), 0, 0.0);
+                    break;
+                case LZB_TK_JACOBI: LZB_LAUNCH(k_jacobi, vgrid(l), kThreads, 0, s_, V(l), 0.0); break;
+                case LZB_TK_PROLONG: LZB_LAUNCH(k_prolong, vgrid(l), kThreads, 0, s_, V(l), V(l - 1)); break;
+                case LZB_TK_PACK:
+                    LZB_LAUNCH(k_pack_slots, blocks_for(total_cells_, kThreads), kThreads, 0, s_, all_levels(),
+                               d_.field, total_cells_, rec_offs_.p, img_.p, ctx_->err.p);
+                    break;
+                case LZB_TK_FRONT: run_graph(g_front_, &Grid::front_body); break;
+                case LZB_TK_BACK: run_graph(g_back_, &Grid::back_body); break;
+                default: throw Error(LZB_ERR_INVALID, "unknown kernel id");
+            }
+        };
+        launch();  // warm (and graph instantiation)
+        cudaEvent_t a, b;
+        LZB_CUDA(cudaEventCreate(&a));
+        LZB_CUDA(cudaEventCreate(&b));
+        LZB_CUDA(cudaEventRecord(a, s_));
+        for (int i = 0; i < reps; ++i) launch();
+        LZB_CUDA(cudaEventRecord(b, s_));
+        LZB_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        LZB_CUDA(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        sync_check();
+        return static_cast<double>(ms) / reps;
+    }
+
     std::vector<uint8_t> image() {
         std::vector<uint8_t> out(static_cast<size_t>(scan_records()));
         image_into(out.data(), static_cast<int64_t>(out.size()));
@@ -2431,6 +2521,9 @@ int lzb_grid_stream_image(lzb_grid* g, uint8_t* out, int64_t cap, int64_t* size)
         }
         *size = g->g->image_into(out, cap);
     });
+}
+int lzb_grid_time_kernel(lzb_grid* g, int what, int reps, double* avg_ms) {
+    return guarded([&] { *avg_ms = g->g->time_kernel(what, reps); });
 }
 int lzb_grid_stream_load(lzb_grid* g, const uint8_t* in, int64_t size) {
     return guarded([&] { g->g->load(in, size); });
