@@ -231,6 +231,103 @@ __device__ __forceinline__ uint8_t encode_byte(double x, int p3, int pos) {
     return static_cast<uint8_t>(packed >> (8 * (p3 - 2 - pos)));
 }
 
+// All p3 bytes of encode_value(x, p3) for finite x, byte `pos` at bits
+// 8*pos (little-endian word): the big-endian sign|fraction bytes, then the
+// exponent byte (codec.cpp:8-45); p3 = 8 is the raw IEEE image.
+__device__ __forceinline__ unsigned long long encode_word(double x, int p3) {
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(x));
+    if (p3 == 8) return u;
+    const int m = mantissa_bits(p3);
+    unsigned long long sign = 0, fb = 0;
+    int e_hat = -128;
+    if ((u << 1) != 0) {
+        sign = u >> 63;
+        const int E = static_cast<int>((u >> 52) & 0x7ff);
+        unsigned long long F = u & 0xFFFFFFFFFFFFFull;
+        int e;
+        if (E == 0) {
+            const int b = 63 - __clzll(static_cast<long long>(F));
+            e = b - 1074;
+            F = (F << (52 - b)) & 0xFFFFFFFFFFFFFull;
+        } else {
+            e = E - 1023;
+        }
+        e_hat = e < -128 ? -128 : (e > 127 ? 127 : e);
+        fb = F >> (52 - m);
+    }
+    const unsigned long long packed = (sign << m) | fb;  // 8*(p3-1) significant bits
+    const unsigned lo = static_cast<unsigned>(packed), hi = static_cast<unsigned>(packed >> 32);
+    const unsigned long long sw = (static_cast<unsigned long long>(__byte_perm(lo, 0, 0x0123)) << 32) |
+                                  __byte_perm(hi, 0, 0x0123);
+    return (sw >> (8 * (9 - p3))) |
+           (static_cast<unsigned long long>(static_cast<uint8_t>(static_cast<int8_t>(e_hat))) << (8 * (p3 - 1)));
+}
+
+// encode_word with selects instead of branches (lanes with different p3
+// stay converged); identical bytes.
+__device__ __forceinline__ unsigned long long encode_word_sel(double x, int p3) {
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(x));
+    const int m = min(mantissa_bits(p3), 47);  // p3 = 8 takes the raw image below
+    const int E = static_cast<int>((u >> 52) & 0x7ff);
+    unsigned long long F = u & 0xFFFFFFFFFFFFFull;
+    int e = E - 1023;
+    if (E == 0 && F != 0) {  // subnormal: renormalise like frexp
+        const int b = 63 - __clzll(static_cast<long long>(F));
+        e = b - 1074;
+        F = (F << (52 - b)) & 0xFFFFFFFFFFFFFull;
+    }
+    const bool zero = (u << 1) == 0;
+    const int e_hat = zero ? -128 : min(max(e, -128), 127);
+    const unsigned long long sign = zero ? 0ull : (u >> 63);
+    const unsigned long long fb = zero ? 0ull : (F >> (52 - m));
+    const unsigned long long packed = (sign << m) | fb;
+    const unsigned lo = static_cast<unsigned>(packed), hi = static_cast<unsigned>(packed >> 32);
+    const unsigned long long sw = (static_cast<unsigned long long>(__byte_perm(lo, 0, 0x0123)) << 32) |
+                                  __byte_perm(hi, 0, 0x0123);
+    const unsigned long long w =
+        (sw >> (8 * (9 - min(p3, 7)))) |
+        (static_cast<unsigned long long>(static_cast<uint8_t>(static_cast<int8_t>(e_hat))) << (8 * (min(p3, 7) - 1)));
+    return p3 == 8 ? u : w;
+}
+
+// Byte strings appended to shared memory as aligned 32-bit words. The window
+// is zeroed first; the first and the last word of a run may be shared with a
+// neighbour's bytes and are merged with atomicOr, the others stored plainly.
+struct WordSink {
+    uint32_t* w;
+    unsigned long long acc;
+    int nb;  // pending bits in acc, < 32
+    bool first;
+    __device__ explicit WordSink(uint8_t* p) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+        w = reinterpret_cast<uint32_t*>(a & ~uintptr_t{3});
+        nb = 8 * static_cast<int>(a & 3);
+        acc = 0;
+        first = true;
+    }
+    __device__ __forceinline__ void put32(unsigned long long chunk, int bits) {  // chunk < 2^bits, bits <= 32
+        acc |= chunk << nb;
+        nb += bits;
+        if (nb >= 32) {
+            const uint32_t word = static_cast<uint32_t>(acc);
+            if (first) atomicOr(w, word);
+            else *w = word;
+            first = false;
+            ++w;
+            acc >>= 32;
+            nb -= 32;
+        }
+    }
+    __device__ __forceinline__ void put(unsigned long long x, int p3) {  // the low p3 bytes of x
+        const int b = 8 * p3;
+        put32(x & 0xffffffffull, min(b, 32));
+        put32(x >> 32, max(b - 32, 0));
+    }
+    __device__ __forceinline__ void flush() {
+        if (nb > 0) atomicOr(w, static_cast<uint32_t>(acc));
+    }
+};
+
 // codec::roundtrip (codec.hpp:28-33) without the byte detour: the same
 // encode/decode arithmetic on registers. Returns false for non-finite.
 __device__ inline bool roundtrip_fast(double x, int p3, double& out) {

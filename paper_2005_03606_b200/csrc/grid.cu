@@ -1053,65 +1053,24 @@ __global__ void k_noise(LevelView L, int level, uint64_t seed, double gval) {
 
 // ------------------------------------------------------- stream image (save)
 // Pre-order slot of a cell on a regular tree of depth D: slot(child ci of a
-// level-(k-1) cell with slot s) = s + 1 + ci * S_k, S_k = sum_{j<=D-k} 9^j
-// (mesh.cpp:152-167).
-__device__ inline int64_t preorder_slot(int l, int cx, int cy, const int64_t* subtree) {
-    int64_t slot = 0;
-    int64_t p = 1;
-    for (int k = 1; k < l; ++k) p *= 3;
-    for (int k = 1; k <= l; ++k) {
-        int dx = static_cast<int>((cx / p) % 3), dy = static_cast<int>((cy / p) % 3);
-        slot += 1 + (dx * 3 + dy) * subtree[k];
-        p /= 3;
-    }
-    return slot;
-}
-
-
+// level-(k-1) cell with slot s) = s + 1 + ci * S_k, S_k = sum_{j<=D-k} 9^j,
+// ci = lx*3 + ly (mesh.cpp:152-167).
 struct SlotTable {
     int64_t subtree[16];
+    // slot(l, cx, cy) = l + sx[l][cx] + sy[l][cy]: the base-3 digit sums
+    // sum_k 3*dx_k*S_k and sum_k dy_k*S_k of the pre-order slot
+    const int64_t* sx[16];
+    const int64_t* sy[16];
 };
 
-__global__ void k_record_sizes(LevelView L, int level, int leaf, SlotTable st, int64_t* sizes) {
-    int64_t c = gtid();
-    if (c >= static_cast<int64_t>(L.N) * L.N) return;
-    int cx = static_cast<int>(c % L.N), cy = static_cast<int>(c / L.N);
-    int32_t p1 = L.p1[c];
-    int p3 = p1 != LZB_P1_BOTTOM ? L.p3[c] : 0;
-    int64_t bytes = (p1 == LZB_P1_BOTTOM || p3 == 0) ? 1 : 1 + p3 * (leaf ? 16 : 144);
-    sizes[preorder_slot(level, cx, cy, st.subtree)] = bytes;
-}
-
-// CellStream::save record (stream.cpp:315-337): header byte, then the
-// surplus against the n = 1 baseline (and P-hat, R-hat copy) at p3 bytes.
-__global__ void k_pack(LevelView L, lzb_field f, int level, int leaf, SlotTable st,
-                       const int64_t* __restrict__ offsets, uint8_t* __restrict__ out, int* err) {
-    int64_t c = gtid();
-    if (c >= static_cast<int64_t>(L.N) * L.N) return;
-    int cx = static_cast<int>(c % L.N), cy = static_cast<int>(c / L.N);
-    int64_t off = 12 + offsets[preorder_slot(level, cx, cy, st.subtree)];
-    int32_t p1 = L.p1[c];
-    int p3 = p1 != LZB_P1_BOTTOM ? L.p3[c] : 0;
-    out[off] = pack_header(p1, L.p2[c], p3);
-    if (p1 == LZB_P1_BOTTOM || p3 == 0) return;
-    uint8_t* cur = out + off + 1;
-    double e = centre_eps(f, L, cx, cy);
-    const double* op = L.op + 16 * c;
-    bool ok = true;
-    for (int k = 0; k < 16; ++k, cur += p3) ok &= encode_value(op[k] - baseline_entry(k, e), p3, cur);
-    if (!leaf) {
-        const double* P = transfer_of(L, static_cast<int>(c));
-        for (int rep = 0; rep < 2; ++rep)
-            for (int k = 0; k < 64; ++k, cur += p3) ok &= encode_value(P[k] - c_geo[k], p3, cur);
-    }
-    if (!ok) atomicExch(err, 1);
+__device__ __forceinline__ int64_t slot_at(const SlotTable& st, int l, int cx, int cy) {
+    return l + st.sx[l][cx] + st.sy[l][cy];
 }
 
 // -------------------------------------------- slot-ordered stream packing
-// The LZMG image lists records in pre-order (stream.cpp:311-337). Working in
-// slot order, consecutive lanes own consecutive records, so a warp writes one
-// contiguous span; each record is emitted by the whole warp, 32 consecutive
-// bytes per store instruction (coalesced), every lane encoding its own byte.
+// The LZMG image lists records in pre-order (stream.cpp:311-337): record
+// sizes -> device exclusive scan -> offsets, then k_pack_patches / k_pack_upper fill
+// the image.
 constexpr int kMaxLevels = 10;
 struct AllLevels {
     LevelView L[kMaxLevels];
@@ -1119,81 +1078,243 @@ struct AllLevels {
     int D;
 };
 
-// slot -> (level, cx, cy): undo slot = sum_k (1 + ci_k * S_k), ci = lx*3 + ly.
-__device__ inline void decode_slot(int64_t s, const AllLevels& A, int& level, int& cx, int& cy) {
-    level = 0;
-    cx = cy = 0;
-    while (s != 0) {
-        s -= 1;
-        const int64_t sub = A.st.subtree[level + 1];
-        const int ci = static_cast<int>(s / sub);
-        s -= ci * sub;
-        cx = 3 * cx + ci / 3;
-        cy = 3 * cy + ci % 3;
-        ++level;
+__device__ __forceinline__ int record_size(int p1, int p3, bool leaf) {  // stream.cpp:227-237
+    return (p1 == LZB_P1_BOTTOM || p3 == 0) ? 1 : 1 + p3 * (leaf ? 16 : 144);
+}
+
+// The p3 bytes of an encode_word at d (p3 uniform per record: unrolled).
+__device__ __forceinline__ void put_bytes(uint8_t* d, unsigned long long w, int p3) {
+    switch (p3) {
+        case 8: d[7] = static_cast<uint8_t>(w >> 56); [[fallthrough]];
+        case 7: d[6] = static_cast<uint8_t>(w >> 48); [[fallthrough]];
+        case 6: d[5] = static_cast<uint8_t>(w >> 40); [[fallthrough]];
+        case 5: d[4] = static_cast<uint8_t>(w >> 32); [[fallthrough]];
+        case 4: d[3] = static_cast<uint8_t>(w >> 24); [[fallthrough]];
+        case 3: d[2] = static_cast<uint8_t>(w >> 16); [[fallthrough]];
+        case 2: d[1] = static_cast<uint8_t>(w >> 8); d[0] = static_cast<uint8_t>(w); break;
+        default: break;
     }
 }
 
-__global__ void k_record_sizes_slots(AllLevels A, int64_t total, int64_t* sizes) {
-    int64_t s = gtid();
-    if (s >= total) return;
-    int l, cx, cy;
-    decode_slot(s, A, l, cx, cy);
-    const LevelView& L = A.L[l];
-    const int64_t c = static_cast<int64_t>(cy) * L.N + cx;
-    const int32_t p1 = L.p1[c];
-    const int p3 = p1 != LZB_P1_BOTTOM ? L.p3[c] : 0;
-    sizes[s] = (p1 == LZB_P1_BOTTOM || p3 == 0) ? 1 : 1 + p3 * (l == A.D ? 16 : 144);
-}
+// CellStream::save records of level-(D-1) patches with their 9 leaves. In
+// pre-order a patch and its leaves are 10 consecutive records (slot sP, then
+// sP+1+ci, ci = lx*3+ly), and sibling patches (px, 3q+j), j = 0..2, follow
+// one another: one warp packs such a triple, 30 records, one contiguous byte
+// range of the image. Lane = record: a leaf lane encodes its own 16 values
+// (one encode_word each) into the warp's shared-memory window; the refined
+// records (144 values: Â, P̂ and the R̂ copy) are then encoded by the whole
+// warp, lane = value; the window leaves in 16-B aligned vector stores. No
+// block barriers.
+constexpr int kPackWarps = 4;
+constexpr int kPatchBytes = 1153 + 9 * 129;  // refined record + 9 leaf records at p3 = 8
+constexpr int kPackWindow = (3 * kPatchBytes + 16 + 15) & ~15;
 
-__global__ void k_pack_slots(AllLevels A, lzb_field f, int64_t total, const int64_t* __restrict__ offsets,
-                             uint8_t* __restrict__ out, int* err) {
-    const int lane = threadIdx.x & 31;
-    const int64_t s = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
-    int l = 0, cx = 0, cy = 0, p3 = 0, size = 0;
-    int64_t c = 0, off = 0;
-    uint8_t hdr = 0;
+struct PackArgs {
+    const double *cxF, *cyF, *cxC, *cyC;  // centre field parts, leaf and patch level
+};
+
+__global__ void __launch_bounds__(kPackWarps * 32) k_pack_patches(AllLevels A, lzb_field f, PackArgs T, int per,
+                                                                  const int64_t* __restrict__ offsets,
+                                                                  uint8_t* __restrict__ out, int* err) {
+    __shared__ __align__(16) uint8_t wbuf[kPackWarps][kPackWindow];
+    __shared__ double s_geo[64], s_kunit[16];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x < 64) s_geo[threadIdx.x] = c_geo[threadIdx.x];
+    if (threadIdx.x < 16) s_kunit[threadIdx.x] = c_kunit[threadIdx.x];
+    __syncthreads();
+    const int D = A.D;
+    const LevelView C = A.L[D - 1];
+    const LevelView F = A.L[D];
+    // 2D grid: x = patch columns (kPackWarps per block), y = groups of `per` sibling patches
+    const int px = blockIdx.x * kPackWarps + warp, py0 = blockIdx.y * per;
+    if (px >= C.N) return;
+    const unsigned full = 0xffffffffu;
+    const int64_t s0 = slot_at(A.st, D - 1, px, py0);
+    const int nrec = 10 * per;
+    // lane r < nrec: record r of the range = patch r/10, then leaf (r%10)-1
+    const int pj = lane / 10, k = lane % 10;
+    const bool have = lane < nrec, leaf = have && k > 0;
+    int p3 = 0, size = 0, cell = 0;
+    int64_t off = 0;
     double e = 0.0;
-    if (s < total) {
-        decode_slot(s, A, l, cx, cy);
-        const LevelView& L = A.L[l];
-        c = static_cast<int64_t>(cy) * L.N + cx;
-        const int32_t p1 = L.p1[c];
-        p3 = p1 != LZB_P1_BOTTOM ? L.p3[c] : 0;
-        hdr = pack_header(p1, L.p2[c], p3);
-        size = (p1 == LZB_P1_BOTTOM || p3 == 0) ? 1 : 1 + p3 * (l == A.D ? 16 : 144);
-        off = 12 + offsets[s];
-        if (size > 1) e = centre_eps(f, L, cx, cy);
+    uint8_t hdr = 0;
+    if (have) {
+        int cx = px, cy = py0 + pj, N = C.N;
+        const int32_t* p1a = C.p1;
+        const int8_t* p3a = C.p3;
+        const uint8_t* p2a = C.p2;
+        if (leaf) {
+            cx = 3 * px + (k - 1) / 3;
+            cy = 3 * (py0 + pj) + (k - 1) % 3;
+            N = F.N;
+            p1a = F.p1;
+            p3a = F.p3;
+            p2a = F.p2;
+        }
+        cell = cy * N + cx;
+        // independent loads first
+        const int32_t p1 = p1a[cell];
+        const int p3raw = p3a[cell];
+        const uint8_t p2 = p2a[cell];
+        off = offsets[s0 + lane];
+        const double ex = leaf ? T.cxF[cx] : T.cxC[cx], ey = leaf ? T.cyF[cy] : T.cyC[cy];
+        p3 = p1 != LZB_P1_BOTTOM ? p3raw : 0;
+        hdr = pack_header(p1, p2, p3);
+        size = record_size(p1, p3, leaf);
+        // centre eps = field at the n = 1 sample (tabulated parts; element.hpp:44)
+        if (size > 1) e = field_combine(f, ex, ey);
     }
+    const int64_t off0 = __shfl_sync(full, off, 0);
+    const int rel = static_cast<int>(off - off0);
+    const int64_t g0 = 12 + off0;
+    const int shift = static_cast<int>(g0 & 15);
+    const int bytes = __shfl_sync(full, rel + size, nrec - 1);
+    uint8_t* buf = wbuf[warp];
+    // zero the window (payload words are OR-merged at record boundaries)
+    {
+        uint4* z = reinterpret_cast<uint4*>(buf);
+        const int nz = (shift + bytes + 15) >> 4;
+        for (int q = lane; q < nz; q += 32) z[q] = make_uint4(0, 0, 0, 0);
+    }
+    __syncwarp();
+    if (have) buf[shift + rel] = hdr;
+    __syncwarp();
     bool ok = true;
-    for (int r = 0; r < 32; ++r) {
-        const int rsize = __shfl_sync(0xffffffffu, size, r);
-        if (rsize == 0) continue;
-        const int64_t roff = __shfl_sync(0xffffffffu, off, r);
-        const uint8_t rhdr = static_cast<uint8_t>(__shfl_sync(0xffffffffu, static_cast<int>(hdr), r));
-        if (lane == 0) out[roff] = rhdr;
-        if (rsize == 1) continue;
-        const int rl = __shfl_sync(0xffffffffu, l, r);
-        const int rp3 = __shfl_sync(0xffffffffu, p3, r);
-        const int64_t rc = __shfl_sync(0xffffffffu, c, r);
-        const double re = __shfl_sync(0xffffffffu, e, r);
-        const LevelView& L = A.L[rl];
-        const double* op = L.op + 16 * rc;
-        const double* P = transfer_of(L, static_cast<int>(rc));
-        for (int b = 1 + lane; b < rsize; b += 32) {
-            const int i = (b - 1) / rp3, pos = (b - 1) - i * rp3;
-            double v;
-            if (i < 16) {
-                v = op[i] - baseline_entry(i, re);  // surplus of the stored matrix (stream.cpp:322-324)
-            } else {
-                const int k = (i - 16) & 63;        // P-hat, then the R-hat copy (stream.cpp:326-335)
-                v = P[k] - c_geo[k];
+    // leaves: one lane per record, 16 values, aligned word stores
+    if (leaf && size > 1) {
+        const double2* src = reinterpret_cast<const double2*>(F.op + 16 * static_cast<int64_t>(cell));
+        double2 v[8];  // the whole operator in flight before any use
+#pragma unroll
+        for (int h = 0; h < 8; ++h) v[h] = __ldcs(src + h);
+        WordSink sink(buf + shift + rel + 1);
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+            const double x0 = v[h].x - (0.0 + c_kunit[2 * h] * e);
+            const double x1 = v[h].y - (0.0 + c_kunit[2 * h + 1] * e);
+            ok = ok && dev_isfinite(x0) && dev_isfinite(x1);
+            sink.put(encode_word_sel(x0, p3), p3);
+            sink.put(encode_word_sel(x1, p3), p3);
+        }
+        sink.flush();
+    }
+    __syncwarp();
+    // refined records with a payload: the whole warp, lane = value
+    unsigned todo = __ballot_sync(full, have && !leaf && size > 1);
+    while (todo) {
+        const int r = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int rp3 = __shfl_sync(full, p3, r), rrel = __shfl_sync(full, rel, r);
+        const int rcell = __shfl_sync(full, cell, r);
+        const double re = __shfl_sync(full, e, r);
+        const double* P = (C.P && C.has_P[rcell]) ? C.P + 64 * static_cast<int64_t>(rcell) : nullptr;
+        uint8_t* dst = buf + shift + rrel + 1;
+        if (!P) {
+            // geometric transfer: Â, then P̂ = R̂ = geo - geo = +0 -> (0, 0, -128),
+            // whose only non-zero byte is the exponent (raw +0 at p3 = 8)
+            if (lane < 16) {
+                const double x = C.op[16 * static_cast<int64_t>(rcell) + lane] - (0.0 + s_kunit[lane] * re);
+                ok = ok && dev_isfinite(x);
+                put_bytes(dst + lane * rp3, encode_word(x, rp3), rp3);
             }
-            ok = ok && dev_isfinite(v);
-            out[roff + b] = encode_byte(v, rp3, pos);
+            if (rp3 < 8)
+                for (int q = lane; q < 128; q += 32) dst[(16 + q) * rp3 + rp3 - 1] = 0x80;
+            continue;
+        }
+        for (int i = lane; i < 144; i += 32) {
+            double x;
+            if (i < 16) {
+                x = C.op[16 * static_cast<int64_t>(rcell) + i] - (0.0 + s_kunit[i] * re);
+            } else {
+                const int kk = (i - 16) & 63;  // P-hat, then the R-hat copy (stream.cpp:326-335)
+                x = P ? P[kk] - s_geo[kk] : s_geo[kk] - s_geo[kk];
+            }
+            ok = ok && dev_isfinite(x);
+            put_bytes(dst + i * rp3, encode_word(x, rp3), rp3);
         }
     }
+    __syncwarp();
+    // write-out of [g0, g0 + bytes)
+    const int64_t a0 = (g0 + 15) & ~int64_t{15}, end = g0 + bytes;
+    const int64_t a1 = max(a0, end & ~int64_t{15});
+    const int head = static_cast<int>(min(a0, end) - g0);
+    if (lane < head) out[g0 + lane] = buf[shift + lane];
+    const int nvec = static_cast<int>((a1 - a0) >> 4);
+    const uint4* src = reinterpret_cast<const uint4*>(buf + (a0 - g0) + shift);
+    uint4* dst = reinterpret_cast<uint4*>(out + a0);
+    for (int q = lane; q < nvec; q += 32) __stcs(dst + q, src[q]);
+    if (a0 < end && lane < end - a1) out[a1 + lane] = buf[shift + (a1 - g0) + lane];
+    if (!__all_sync(full, ok) && lane == 0) atomicExch(err, 1);
+}
+
+// Records of levels 0..D-2 (1/80 of the image): one thread per record,
+// bytes straight to global memory.
+__global__ void k_pack_upper(AllLevels A, lzb_field f, int64_t ncells, const int64_t* __restrict__ offsets,
+                             uint8_t* __restrict__ out, int* err) {
+    int64_t t = gtid();
+    if (t >= ncells) return;
+    int l = 0;
+    int64_t n = 1;
+    while (t >= n) {
+        t -= n;
+        ++l;
+        n *= 9;
+    }
+    const LevelView& L = A.L[l];
+    const int cx = static_cast<int>(t % L.N), cy = static_cast<int>(t / L.N);
+    const int c = cy * L.N + cx;
+    const int32_t p1 = L.p1[c];
+    const int p3 = p1 != LZB_P1_BOTTOM ? L.p3[c] : 0;
+    const int size = record_size(p1, p3, false);
+    uint8_t* rec = out + 12 + offsets[slot_at(A.st, l, cx, cy)];
+    rec[0] = pack_header(p1, L.p2[c], p3);
+    if (size == 1) return;
+    const double e = centre_eps(f, L, cx, cy);
+    const double* P = transfer_of(L, c);
+    bool ok = true;
+    for (int i = 0; i < 144; ++i) {
+        const double x = i < 16 ? L.op[16 * static_cast<int64_t>(c) + i] - baseline_entry(i, e)
+                                : P[(i - 16) & 63] - c_geo[(i - 16) & 63];
+        ok = ok && dev_isfinite(x);
+        put_bytes(rec + 1 + i * p3, encode_word(x, p3), p3);
+    }
     if (!ok) atomicExch(err, 1);
+}
+
+// Record sizes in slot order (stream.cpp:227-237): one thread per
+// level-(D-1) patch writes its record and its 9 leaves' (10 consecutive
+// slots); one thread per cell of the levels above.
+__global__ void k_record_sizes_patches(AllLevels A, int64_t* __restrict__ sizes) {
+    const int D = A.D;
+    const LevelView& C = A.L[D - 1];
+    const LevelView& F = A.L[D];
+    const int px = blockIdx.x * blockDim.x + threadIdx.x, py = blockIdx.y;
+    if (px >= C.N) return;
+    const int64_t sP = slot_at(A.st, D - 1, px, py);
+    int c = py * C.N + px;
+    int32_t p1 = C.p1[c];
+    sizes[sP] = record_size(p1, p1 != LZB_P1_BOTTOM ? C.p3[c] : 0, false);
+#pragma unroll
+    for (int ci = 0; ci < 9; ++ci) {
+        c = (3 * py + ci % 3) * F.N + 3 * px + ci / 3;
+        p1 = F.p1[c];
+        sizes[sP + 1 + ci] = record_size(p1, p1 != LZB_P1_BOTTOM ? F.p3[c] : 0, true);
+    }
+}
+__global__ void k_record_sizes_upper(AllLevels A, int64_t ncells, int64_t* __restrict__ sizes) {
+    int64_t t = gtid();
+    if (t >= ncells) return;
+    int l = 0;
+    int64_t n = 1;
+    while (t >= n) {
+        t -= n;
+        ++l;
+        n *= 9;
+    }
+    const LevelView& L = A.L[l];
+    const int cx = static_cast<int>(t % L.N), cy = static_cast<int>(t / L.N);
+    const int c = cy * L.N + cx;
+    const int32_t p1 = L.p1[c];
+    sizes[slot_at(A.st, l, cx, cy)] = record_size(p1, p1 != LZB_P1_BOTTOM ? L.p3[c] : 0, false);
 }
 
 // CellStream::load record (stream.cpp:355-392); offsets from the host parse.
@@ -1203,7 +1324,7 @@ __global__ void k_unpack(LevelView L, lzb_field f, int level, int leaf, SlotTabl
     int64_t c = gtid();
     if (c >= static_cast<int64_t>(L.N) * L.N) return;
     int cx = static_cast<int>(c % L.N), cy = static_cast<int>(c / L.N);
-    const uint8_t* rec = in + offsets[preorder_slot(level, cx, cy, st.subtree)];
+    const uint8_t* rec = in + offsets[slot_at(st, level, cx, cy)];
     uint8_t h = rec[0];
     int cls = (h >> 6) & 3, p2 = (h & 0x20) != 0, p3 = h & 0x0f;
     L.p2[c] = static_cast<uint8_t>(p2);
@@ -1560,6 +1681,16 @@ public:
                 LZB_CUDA(cudaMemsetAsync(L.P.p, 0, L.P.bytes(), s_));
             }
         }
+        // centre field parts (the n = 1 sample) of the patch and leaf levels
+        for (int k = 0; k < 2; ++k) {
+            const Level& L = L_[D_ - 1 + k];
+            centre_[k].x.alloc(L.N);
+            centre_[k].y.alloc(L.N);
+            LZB_LAUNCH(k_field_parts, blocks_for(L.N, kThreads), kThreads, 0, s_, d.field, L.N, L.h, 1, 0,
+                       centre_[k].x.p);
+            LZB_LAUNCH(k_field_parts, blocks_for(L.N, kThreads), kThreads, 0, s_, d.field, L.N, L.h, 1, 1,
+                       centre_[k].y.p);
+        }
         leaves_ = L_[D_].nc;
         list_.alloc(leaves_);
         snap_.alloc(leaves_);
@@ -1603,6 +1734,26 @@ public:
             int64_t s = 0, p = 1;
             for (int j = 0; j <= D_ - k; ++j, p *= 9) s += p;
             slots_.subtree[k] = s;
+        }
+        for (int l = 0; l <= D_; ++l) {
+            const int N = L_[l].N;
+            std::vector<int64_t> sx(N), sy(N);
+            for (int c = 0; c < N; ++c) {
+                int64_t ax = 0, ay = 0, p = N / 3;
+                for (int k = 1; k <= l; ++k, p /= 3) {
+                    const int64_t d = (c / p) % 3;
+                    ax += 3 * d * slots_.subtree[k];
+                    ay += d * slots_.subtree[k];
+                }
+                sx[c] = ax;
+                sy[c] = ay;
+            }
+            slot_x_[l].alloc(N);
+            slot_y_[l].alloc(N);
+            LZB_CUDA(cudaMemcpy(slot_x_[l].p, sx.data(), N * sizeof(int64_t), cudaMemcpyHostToDevice));
+            LZB_CUDA(cudaMemcpy(slot_y_[l].p, sy.data(), N * sizeof(int64_t), cudaMemcpyHostToDevice));
+            slots_.sx[l] = slot_x_[l].p;
+            slots_.sy[l] = slot_y_[l].p;
         }
         for (int l = 0; l <= D_; ++l) total_cells_ += L_[l].nc;
         for (int l = 0; l <= D_; ++l) total_vertices_ += L_[l].nv;
@@ -2196,8 +2347,12 @@ public:
     }
 
     void record_sizes(int64_t* sizes) {
-        LZB_LAUNCH(k_record_sizes_slots, blocks_for(total_cells_, kThreads), kThreads, 0, s_, all_levels(),
-                   total_cells_, sizes);
+        const dim3 grid(blocks_for(L_[D_ - 1].N, 64), L_[D_ - 1].N);
+        LZB_LAUNCH(k_record_sizes_patches, grid, 64, 0, s_, all_levels(), sizes);
+        const int64_t upper = total_cells_ - L_[D_].nc - L_[D_ - 1].nc;
+        if (upper > 0)
+            LZB_LAUNCH(k_record_sizes_upper, blocks_for(upper, kThreads), kThreads, 0, s_, all_levels(), upper,
+                       sizes);
     }
 
     // Record sizes -> device exclusive scan (cub) -> total. Returns the image size.
@@ -2224,7 +2379,21 @@ public:
 
     int64_t image_size() { return scan_records(); }
 
-    // CellStream::save byte image: packed on the device (k_pack) from the
+    // Stream records into img (offsets from scan_records): the level-(D-1)
+    // patches with their leaves, then the levels above.
+    void pack_launches(uint8_t* img) {
+        const PackArgs T{centre_[1].x.p, centre_[1].y.p, centre_[0].x.p, centre_[0].y.p};
+        const int per = L_[D_ - 1].N >= 3 ? 3 : 1;  // sibling patches per warp
+        const dim3 grid(blocks_for(L_[D_ - 1].N, kPackWarps), L_[D_ - 1].N / per);
+        LZB_LAUNCH(k_pack_patches, grid, kPackWarps * 32, 0, s_, all_levels(), d_.field, T, per, rec_offs_.p, img,
+                   ctx_->err.p);
+        const int64_t upper = total_cells_ - L_[D_].nc - L_[D_ - 1].nc;
+        if (upper > 0)
+            LZB_LAUNCH(k_pack_upper, blocks_for(upper, kThreads), kThreads, 0, s_, all_levels(), d_.field, upper,
+                       rec_offs_.p, img, ctx_->err.p);
+    }
+
+    // CellStream::save byte image: packed on the device (k_pack_patches) from the
     // decoded operators, copied once into the caller's buffer.
     int64_t image_into(uint8_t* out, int64_t cap) {
         int64_t size = scan_records();
@@ -2232,8 +2401,7 @@ public:
         if (img_.n < static_cast<size_t>(size)) img_.alloc(static_cast<size_t>(size) + (size >> 3));
         uint32_t hdr[3] = {0x4c5a4d47u, 1u, static_cast<uint32_t>(total_cells_)};
         std::memcpy(out, hdr, 12);
-        LZB_LAUNCH(k_pack_slots, blocks_for(total_cells_, kThreads), kThreads, 0, s_, all_levels(), d_.field,
-                   total_cells_, rec_offs_.p, img_.p, ctx_->err.p);
+        pack_launches(img_.p);
         LZB_CUDA(cudaMemcpyAsync(out + 12, img_.p + 12, size - 12, cudaMemcpyDeviceToHost, s_));
         sync_check();
         return size;
@@ -2264,8 +2432,7 @@ public:
                 case LZB_TK_JACOBI: LZB_LAUNCH(k_jacobi, vgrid(l), kThreads, 0, s_, V(l), 0.0); break;
                 case LZB_TK_PROLONG: LZB_LAUNCH(k_prolong, vgrid(l), kThreads, 0, s_, V(l), V(l - 1)); break;
                 case LZB_TK_PACK:
-                    LZB_LAUNCH(k_pack_slots, blocks_for(total_cells_, kThreads), kThreads, 0, s_, all_levels(),
-                               d_.field, total_cells_, rec_offs_.p, img_.p, ctx_->err.p);
+                    pack_launches(img_.p);
                     break;
                 case LZB_TK_FRONT: run_graph(g_front_, &Grid::front_body); break;
                 case LZB_TK_BACK: run_graph(g_back_, &Grid::back_body); break;
@@ -2411,6 +2578,10 @@ private:
     Result* hres_ = nullptr;
     unsigned* hhist_ = nullptr;
     SlotTable slots_{};
+    DevBuf<int64_t> slot_x_[kMaxLevels], slot_y_[kMaxLevels];
+    struct CentreParts {
+        DevBuf<double> x, y;
+    } centre_[2];  // levels D-1 and D
     uint32_t cycle_ = 0;
     uint32_t* hcycle_ = nullptr;  // pinned: read by the coarse-pass graph at replay
     int* herr_ = nullptr;         // pinned: device error flag copied out by the front graph

@@ -2,7 +2,7 @@
 large 2D grid (run it under `ncu -k regex:...`; the printed times are
 meaningless under the profiler).
 
-usage: python tools/profile_smoother.py [depth] [kernel ids, e.g. 1,5]
+usage: python tools/profile_smoother.py [depth] [kernel ids, e.g. 1,5] [cycles before]
 """
 import os
 import sys
@@ -18,6 +18,8 @@ d = lzb.make_desc(depth=depth, field=f, solver="adafac-pi", omega=0.6, rhs_kind=
                   delta_max=1e-8, integration="fast")
 g = lzb.Grid(d, 1)
 g.assemble_fixed(4)
+for _ in range(int(sys.argv[3]) if len(sys.argv) > 3 else 0):
+    g.step()
 for tk in ids:
     print(tk, g.time_kernel(tk, 1))
 g.close()

@@ -45,7 +45,7 @@ def run(depth, peak):
     img = g.stream_image_size()
     ab = algorithmic_bytes(depth, img, {"cells_total": total_cells, "payload_cells": payload})
     names = {lzb.TK_UHAT: "k_uhat", lzb.TK_RESIDUAL: "k_residual", lzb.TK_RESTRICT: "k_restrict",
-             lzb.TK_JACOBI: "k_jacobi", lzb.TK_PROLONG: "k_prolong", lzb.TK_PACK: "k_pack_slots"}
+             lzb.TK_JACOBI: "k_jacobi", lzb.TK_PROLONG: "k_prolong", lzb.TK_PACK: "k_pack_groups"}
     out = {"depth": depth, "N": 3 ** depth, "image_bytes": img, "kernels": {}}
     for tk, name in names.items():
         ms = g.time_kernel(tk, 10)
