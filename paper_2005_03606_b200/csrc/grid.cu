@@ -33,7 +33,6 @@ namespace lzb {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kNormBlocks = 296;  // 2 x 148 SMs
 constexpr int kNHist = 4097;      // p1 histogram bins (n < 4096)
 
 // Result block copied to the host once per cycle.
@@ -64,7 +63,7 @@ __device__ inline double centre_eps(const lzb_field& f, const LevelView& L, int 
 }
 
 __device__ inline const double* transfer_of(const LevelView& C, int c) {
-    return (C.has_P[c] && C.P) ? C.P + 64 * static_cast<int64_t>(c) : c_geo;
+    return (C.P && C.has_P[c]) ? C.P + 64 * static_cast<int64_t>(c) : c_geo;
 }
 
 __device__ inline void element_or_baseline(const lzb_field& f, const LevelView& L, int cx, int cy,
@@ -858,18 +857,31 @@ __global__ void k_restrict(LevelView F, LevelView C, int mode, double omega) {
     else C.v[LZB_V_AUX][vi] = acc_v;
 }
 
-__global__ void k_norm_partial(LevelView F, double* partial) {
+// Residual norm partials (solver.cpp:202-209): fine interior vertices. Block
+// b sums rows 1+b, 1+b+G, ... four rows per step (independent loads in
+// flight), then a fixed-order tree; k_norm_final adds the kNormBlocks partials.
+constexpr int kNormBlocks = 148 * 4;
+__global__ void __launch_bounds__(kThreads) k_norm_partial(LevelView F, double* partial) {
     __shared__ double sh[kThreads];
-    double s = 0.0;
-    const int64_t nv = static_cast<int64_t>(F.N + 1) * (F.N + 1);
-    (void)nv;
-    // rows blockIdx.x, +gridDim.x, ...; interior columns only (no division)
-    for (int iy = 1 + blockIdx.x; iy < F.N; iy += gridDim.x)
-        for (int ix = 1 + threadIdx.x; ix < F.N; ix += blockDim.x) {
-            double r = F.v[LZB_V_R][static_cast<int64_t>(iy) * (F.N + 1) + ix];
-            s += r * r;
+    const int N = F.N;
+    const double* r = F.v[LZB_V_R];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    const int G = gridDim.x;
+    for (int iy = 1 + blockIdx.x; iy < N; iy += 4 * G) {
+        const int64_t b0 = static_cast<int64_t>(iy) * (N + 1);
+        const bool h1 = iy + G < N, h2 = iy + 2 * G < N, h3 = iy + 3 * G < N;
+        for (int ix = 1 + threadIdx.x; ix < N; ix += blockDim.x) {
+            const double a0 = r[b0 + ix];
+            const double a1 = h1 ? r[b0 + static_cast<int64_t>(G) * (N + 1) + ix] : 0.0;
+            const double a2 = h2 ? r[b0 + static_cast<int64_t>(2 * G) * (N + 1) + ix] : 0.0;
+            const double a3 = h3 ? r[b0 + static_cast<int64_t>(3 * G) * (N + 1) + ix] : 0.0;
+            s0 += a0 * a0;
+            s1 += a1 * a1;
+            s2 += a2 * a2;
+            s3 += a3 * a3;
         }
-    sh[threadIdx.x] = s;
+    }
+    sh[threadIdx.x] = (s0 + s1) + (s2 + s3);
     __syncthreads();
     for (int w = blockDim.x / 2; w > 0; w >>= 1) {
         if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
@@ -878,8 +890,9 @@ __global__ void k_norm_partial(LevelView F, double* partial) {
     if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
 }
 
-__global__ void k_norm_final(const double* partial, int n, Result* res) {
-    __shared__ double sh[kThreads];
+constexpr int kNormFinalThreads = 1024;
+__global__ void __launch_bounds__(kNormFinalThreads) k_norm_final(const double* partial, int n, Result* res) {
+    __shared__ double sh[kNormFinalThreads];
     double s = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) s += partial[i];
     sh[threadIdx.x] = s;
@@ -892,42 +905,50 @@ __global__ void k_norm_final(const double* partial, int n, Result* res) {
 }
 
 // compression_stats over leaves + record bytes of refined cells (stream.cpp:268-301).
-__global__ void k_stats(LevelView L, int leaf, unsigned long long* s) {
+// Grid-stride: per-thread counters over the cells, then warp reductions and
+// one atomic per counter per block.
+constexpr int kStatsBlocks = 148 * 4;
+__global__ void __launch_bounds__(kThreads) k_stats(LevelView L, int leaf, unsigned long long* s) {
     __shared__ unsigned long long sh[20];
     if (threadIdx.x < 20) sh[threadIdx.x] = 0;
     __syncthreads();
-    int64_t c = gtid();
-    const bool in = c < static_cast<int64_t>(L.N) * L.N;
-    const bool task = in && leaf && L.p2[c];
-    int p3 = 0;
-    unsigned bytes = 0, n = 0;
-    if (in) {
-        int32_t p1 = L.p1[c];
-        p3 = p1 != LZB_P1_BOTTOM ? L.p3[c] : 0;
-        bytes = p1 == LZB_P1_BOTTOM ? 1u : 1u + p3 * (leaf ? 16u : 144u);
-        n = p1 != LZB_P1_BOTTOM ? static_cast<unsigned>(L.n[c]) : 0u;
+    const int64_t nc = static_cast<int64_t>(L.N) * L.N;
+    unsigned long long bytes = 0, nsum = 0;
+    unsigned nmax = 0, pend = 0, h[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t c = gtid(); c < nc; c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t p1 = L.p1[c];
+        const int p3raw = L.p3[c];
+        const int p3 = p1 != LZB_P1_BOTTOM ? p3raw : 0;
+        bytes += p1 == LZB_P1_BOTTOM ? 1u : 1u + p3 * (leaf ? 16u : 144u);
+        if (leaf) {
+            const unsigned n = p1 != LZB_P1_BOTTOM ? static_cast<unsigned>(L.n[c]) : 0u;
+            nsum += n;
+            nmax = max(nmax, n);
+            pend += L.p2[c] ? 1u : 0u;
+#pragma unroll
+            for (int b = 0; b <= 8; ++b) h[b] += p3 == b ? 1u : 0u;
+        }
     }
-    // warp reductions, then one shared atomic per warp and one global per block
     const unsigned full = 0xffffffffu;
-    const unsigned wbytes = __reduce_add_sync(full, bytes);
-    const unsigned wn = __reduce_add_sync(full, n);
-    const unsigned wmax = __reduce_max_sync(full, n);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        bytes += __shfl_down_sync(full, bytes, o);
+        nsum += __shfl_down_sync(full, nsum, o);
+    }
     const bool lead = (threadIdx.x & 31) == 0;
-    if (lead) atomicAdd(&sh[S_TOTAL_BYTES], static_cast<unsigned long long>(wbytes));
+    if (lead && bytes) atomicAdd(&sh[S_TOTAL_BYTES], bytes);
     if (leaf) {
 #pragma unroll
         for (int b = 0; b <= 8; ++b) {
-            const unsigned cnt = __popc(__ballot_sync(full, in && p3 == b));
+            const unsigned cnt = __reduce_add_sync(full, h[b]);
             if (lead && cnt) atomicAdd(&sh[S_HIST + b], static_cast<unsigned long long>(cnt));
         }
+        const unsigned wmax = __reduce_max_sync(full, nmax), wp = __reduce_add_sync(full, pend);
         if (lead) {
-            atomicAdd(&sh[S_FINE_BYTES], static_cast<unsigned long long>(wbytes));
-            atomicAdd(&sh[S_NSUM], static_cast<unsigned long long>(wn));
-            atomicMax(&sh[S_MAXN], static_cast<unsigned long long>(wmax));
-        }
-        {
-            const unsigned np = __popc(__ballot_sync(full, task));
-            if (lead && np) atomicAdd(&sh[S_PENDING], static_cast<unsigned long long>(np));
+            if (bytes) atomicAdd(&sh[S_FINE_BYTES], bytes);
+            if (nsum) atomicAdd(&sh[S_NSUM], nsum);
+            if (wmax) atomicMax(&sh[S_MAXN], static_cast<unsigned long long>(wmax));
+            if (wp) atomicAdd(&sh[S_PENDING], static_cast<unsigned long long>(wp));
         }
     }
     __syncthreads();
@@ -1022,6 +1043,60 @@ __global__ void k_prolong(LevelView F, LevelView C) {
     double p = 0.0;
     for (int k = 0; k < 4; ++k) p += P[L * 4 + k] * delta[k];
     F.v[LZB_V_U][vi] += p;
+}
+// The leaf level's three updates of one cycle in one pass over u (u is
+// touched by nothing else in between): the adaFAC-PI aux correction
+// (k_aux_sub, when caux_c is given), the damped Jacobi step (k_jacobi) and the
+// prolongated coarse correction (k_prolong), in that order per vertex, so the
+// result is bit-identical to the three kernels. Runs after the coarse levels
+// are final (prolongation cascade down to level D-1).
+// The coarse factor of k_aux_sub, omega/diag_c * aux_c (0 on the boundary
+// and where diag_c = 0), once per coarse vertex instead of four times per
+// fine vertex; same expression, same bits.
+__global__ void k_scale_aux(LevelView C, double omega, double* __restrict__ out) {
+    int cx, cy;
+    int64_t ci;
+    if (!vertex_xy(C, cx, cy, ci)) return;
+    const double cdg = C.v[LZB_V_DIAG][ci];
+    out[ci] = (!boundary(C.N, cx, cy) && cdg != 0.0) ? omega / cdg * C.v[LZB_V_AUX][ci] : 0.0;
+}
+
+__global__ void k_update_fine(LevelView F, LevelView C, const double* __restrict__ caux_c, double damping) {
+    int fx, fy, px, py;
+    int64_t vi;
+    if (!vertex_xy(F, fx, fy, vi)) return;
+    if (boundary(F.N, fx, fy)) return;
+    owner_patch(C, fx, fy, px, py);
+    const double* P = transfer_of(C, py * C.N + px);
+    const int L = (fy - 3 * py) * 4 + (fx - 3 * px);
+    const double dg = F.v[LZB_V_DIAG][vi], r = F.v[LZB_V_R][vi];
+    double u = F.v[LZB_V_U][vi];
+    double cu[4], cs[4], caux[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t ci = static_cast<int64_t>(py + cdy(k)) * (C.N + 1) + px + cdx(k);
+        cu[k] = C.v[LZB_V_U][ci];
+        cs[k] = C.v[LZB_V_USNAP][ci];
+        caux[k] = caux_c ? caux_c[ci] : 0.0;
+    }
+    if (caux_c) {  // k_aux_sub
+        double p = 0.0;
+        for (int k = 0; k < 4; ++k) p += P[L * 4 + k] * caux[k];
+        u -= p;
+    }
+    if (dg != 0.0) u += damping / dg * r;  // k_jacobi
+    double delta[4];  // k_prolong
+    bool any = false;
+    for (int k = 0; k < 4; ++k) {
+        delta[k] = cu[k] - cs[k];
+        any |= delta[k] != 0.0;
+    }
+    if (any) {
+        double p = 0.0;
+        for (int k = 0; k < 4; ++k) p += P[L * 4 + k] * delta[k];
+        u += p;
+    }
+    F.v[LZB_V_U][vi] = u;
 }
 // inject_solution (mesh.cpp:226-234)
 __global__ void k_inject(LevelView F, LevelView C) {
@@ -1698,6 +1773,7 @@ public:
         blockcnt_.alloc(blocks_for(leaves_, kCompactThreads));
         hist_.alloc(kNHist);
         partial_.alloc(kNormBlocks);
+        if (d.variant == LZB_ADAFAC_PI) caux_.alloc(L_[D_ - 1].nv);
         res_.alloc(1);
         LZB_CUDA(cudaMemsetAsync(res_.p, 0, sizeof(Result), s_));
         if (d.throttle) keys_.alloc(leaves_);
@@ -1991,8 +2067,12 @@ public:
         LZB_CUDA(cudaMemcpyAsync(herr_, ctx_->err.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
     }
     void back_body() {  // update + prolongation + injection
-        update_launches();
-        prolong_launches();
+        update_launches(true);
+        prolong_launches(D_ - 1);
+        const bool pi = d_.variant == LZB_ADAFAC_PI;
+        if (pi) LZB_LAUNCH(k_scale_aux, vgrid(D_ - 1), kThreads, 0, s_, V(D_ - 1), d_.omega, caux_.p);
+        LZB_LAUNCH(k_update_fine, vgrid(D_), kThreads, 0, s_, V(D_), V(D_ - 1), pi ? caux_.p : nullptr,
+                   damping(D_));
         inject();
     }
 
@@ -2044,14 +2124,21 @@ public:
         }
     }
 
-    void residual_launches() {  // solver.cpp:145-210
-        LevelView F = V(D_);
-        bool rhs_on = d_.rhs.kind == LZB_RHS_SINPROD || d_.rhs.value != 0.0;
+    // init_level_rhs on the leaf level (solver.cpp:99-118). The lumped load is
+    // a fixed vector (the restriction only writes coarser levels), so it is
+    // computed once, outside the replayed cycle graphs; writing the leaf fl
+    // through lzb_grid_vertices invalidates it.
+    void ensure_rhs() {
+        if (rhs_ready_) return;
+        const bool rhs_on = d_.rhs.kind == LZB_RHS_SINPROD || d_.rhs.value != 0.0;
         if (rhs_on)
-            LZB_LAUNCH(k_init_rhs, vgrid(D_), kThreads, 0, s_, F, d_.rhs,
-                       L_[D_].h * L_[D_].h / 4.0);
+            LZB_LAUNCH(k_init_rhs, vgrid(D_), kThreads, 0, s_, V(D_), d_.rhs, L_[D_].h * L_[D_].h / 4.0);
         else
             LZB_CUDA(cudaMemsetAsync(L_[D_].v[LZB_V_FL].p, 0, L_[D_].v[LZB_V_FL].bytes(), s_));
+        rhs_ready_ = true;
+    }
+
+    void residual_launches() {  // solver.cpp:145-210
         for (int l = D_; l >= 0; --l) {
             const dim3 g = vgrid(l);
             LZB_LAUNCH(k_uhat, g, kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
@@ -2060,20 +2147,28 @@ public:
                 LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l),
                            V(l - 1), 0, 0.0);
         }
-        LZB_LAUNCH(k_norm_partial, kNormBlocks, kThreads, 0, s_, F, partial_.p);
-        LZB_LAUNCH(k_norm_final, 1, kThreads, 0, s_, partial_.p, kNormBlocks, res_.p);
+        LZB_LAUNCH(k_norm_partial, kNormBlocks, kThreads, 0, s_, V(D_), partial_.p);
+        LZB_LAUNCH(k_norm_final, 1, kNormFinalThreads, 0, s_, partial_.p, kNormBlocks, res_.p);
     }
 
     void stats_launches() {
         LZB_LAUNCH(k_reset_stats, 1, 32, 0, s_, res_.p);
         for (int l = 0; l <= D_; ++l)
-            LZB_LAUNCH(k_stats, blocks_for(L_[l].nc, kThreads), kThreads, 0, s_, V(l), l == D_ ? 1 : 0,
-                       res_.p->s);
+            LZB_LAUNCH(k_stats, static_cast<unsigned>(std::min<int64_t>(blocks_for(L_[l].nc, kThreads), kStatsBlocks)),
+                       kThreads, 0, s_, V(l), l == D_ ? 1 : 0, res_.p->s);
     }
 
-    void update_launches() {  // solver.cpp:212-313
+    double damping(int l) const {
+        return d_.variant == LZB_ADDITIVE ? std::pow(d_.omega, D_ - l + 1) : d_.omega;
+    }
+
+    // fuse_fine: the leaf level's Jacobi step (and, for adaFAC-PI, its aux
+    // correction) is left to k_update_fine at the end of the back graph.
+    void update_launches(bool fuse_fine = false) {  // solver.cpp:212-313
         const double omega = d_.omega;
-        for (int l = 0; l <= D_; ++l)
+        // usnap / aux of the leaf level are never read (prolongation reads the
+        // coarse snapshots; adaFAC-Jac rewrites the leaf aux before use)
+        for (int l = 0; l < D_; ++l)
             LZB_LAUNCH(k_snap, blocks_for(L_[l].nv, kThreads), kThreads, 0, s_, V(l));
         for (int l = D_; l >= 0; --l) {
             bool aux = d_.variant != LZB_ADDITIVE && l > 0;
@@ -2086,15 +2181,16 @@ public:
                     LZB_LAUNCH(k_aux_Ar, g, kThreads, 0, s_, V(l), d_.field);
                     LZB_LAUNCH(k_restrict, gc, kThreads, 0, s_, V(l), V(l - 1), 1, omega);
                 }
-                LZB_LAUNCH(k_aux_sub, g, kThreads, 0, s_, V(l), V(l - 1), omega);
+                if (!(fuse_fine && l == D_ && d_.variant == LZB_ADAFAC_PI))
+                    LZB_LAUNCH(k_aux_sub, g, kThreads, 0, s_, V(l), V(l - 1), omega);
             }
-            double damping = d_.variant == LZB_ADDITIVE ? std::pow(omega, D_ - l + 1) : omega;
-            LZB_LAUNCH(k_jacobi, g, kThreads, 0, s_, V(l), damping);
+            if (!(fuse_fine && l == D_)) LZB_LAUNCH(k_jacobi, g, kThreads, 0, s_, V(l), damping(l));
         }
     }
 
-    void prolong_launches() {
-        for (int l = 1; l <= D_; ++l)
+    void prolong_launches(int lmax = -1) {
+        if (lmax < 0) lmax = D_;
+        for (int l = 1; l <= lmax; ++l)
             LZB_LAUNCH(k_prolong, vgrid(l), kThreads, 0, s_, V(l), V(l - 1));
     }
 
@@ -2189,6 +2285,7 @@ public:
         run_graph(g_coarse_, &Grid::coarse_pass);
         leaves_pass();
         if (d_.concurrent && !batch_inflight_ && (cycle_ == 1 || pending_ > 0)) launch_batch();
+        ensure_rhs();
         run_graph(g_front_, &Grid::front_body);  // residual + stats + result/error copy-out
         LZB_CUDA(cudaStreamSynchronize(s_));
         if (*herr_) {
@@ -2249,7 +2346,7 @@ public:
     double pass(int which) {
         switch (which) {
             case 0: assembly_pass(); sync_check(); return 0.0;
-            case 1: residual_launches(); fetch_result(); return hres_->norm;
+            case 1: ensure_rhs(); residual_launches(); fetch_result(); return hres_->norm;
             case 2: update_launches(); sync_check(); return 0.0;
             case 3: prolong_launches(); sync_check(); return 0.0;
             case 4: inject(); sync_check(); return 0.0;
@@ -2264,6 +2361,7 @@ public:
         check_level(level);
         if (field < 0 || field >= LZB_V_NFIELDS) throw Error(LZB_ERR_INVALID, "bad vertex field");
         auto& b = L_[level].v[field];
+        if (write && level == D_ && field == LZB_V_FL) rhs_ready_ = false;
         if (write) LZB_CUDA(cudaMemcpyAsync(b.p, buf, b.bytes(), cudaMemcpyHostToDevice, s_));
         else LZB_CUDA(cudaMemcpyAsync(buf, b.p, b.bytes(), cudaMemcpyDeviceToHost, s_));
         sync_check();
@@ -2414,6 +2512,7 @@ public:
     double time_kernel(int what, int reps) {
         if (reps < 1) throw Error(LZB_ERR_INVALID, "reps must be >= 1");
         const int l = D_;
+        ensure_rhs();
         if (what == LZB_TK_PACK) {
             const int64_t size = scan_records();
             if (img_.n < static_cast<size_t>(size)) img_.alloc(static_cast<size_t>(size) + (size >> 3));
@@ -2425,7 +2524,9 @@ public:
                 case LZB_TK_UHAT:
                     LZB_LAUNCH(k_uhat, vgrid(l), kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
                     break;
-                case LZB_TK_RESIDUAL: LZB_LAUNCH(k_residual, vgrid(l), kThreads, 0, s_, V(l), d_.field); break;
+                case LZB_TK_RESIDUAL:
+                    LZB_LAUNCH(k_residual, vgrid(l), kThreads, 0, s_, V(l), d_.field);
+                    break;
                 case LZB_TK_RESTRICT:
                     LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1), 0, 0.0);
                     break;
@@ -2587,6 +2688,8 @@ private:
     int* herr_ = nullptr;         // pinned: device error flag copied out by the front graph
     DevBuf<uint32_t> dcycle_;
     bool use_graphs_ = true;
+    DevBuf<double> caux_;         // scaled aux of level D-1 (k_update_fine)
+    bool rhs_ready_ = false;      // leaf-level lumped load in place
     bool all_top_ = false;        // every leaf converged (no request_stencil work left)
     cudaGraphExec_t g_coarse_ = nullptr, g_front_ = nullptr, g_back_ = nullptr;
     uint64_t graph_kernels_[3] = {0, 0, 0};
