@@ -11,7 +11,8 @@ Metric: eps sub-sample integrations/s (BASELINE.json metric, first term).
 
 Also reported in the same line: the FAST (separable FMA) integration path,
 the smoother (one full additive multigrid cycle on that grid, DoF-updates/s),
-the roofline of the dominant kernel against a measured FP64 peak, the
+the roofline of the dominant kernel against a measured FP64 peak, the HBM
+roofline of the cycle kernels and the LZMG stream pack on a 6561^2 grid, the
 end-to-end leg through the C-ABI with a host buffer, and the reference CPU
 baseline (oracle/_ref = the unmodified reference integrate_element on all
 host cores) on a bounded sample.
@@ -37,6 +38,7 @@ N_AXIS = 3 ** LEVEL
 CELLS = N_AXIS * N_AXIS
 P = 32
 SAMPLES_PER_STEP = CELLS * P * P
+HBM_LEVEL = 8  # smoother / stream-pack roofline grid (6561^2, beyond L2)
 # algorithmic FP64 flops per sub-sample of the tabulated integration:
 #   EXACT: 6 mul (K_sub from axis parts) + 9 add (K values) + 9 mul + 9 add (accumulate)
 #          + 2 (eps combine: 1 + (0.9 sin x) sin y)                                   = 35
@@ -306,6 +308,32 @@ def run_ours(args, world, rank, local):
                 "value": world * dof * cycles / tc, "ms_per_cycle": 1e3 * tc / cycles, "cycles": cycles,
                 "launches_per_cycle": cyc_launches / cycles, "dof_per_cycle": dof}
 
+    # HBM-bound regime: the 729^2 working set (~150 MB) is largely L2-resident
+    # (SURVEY.md §8d), so the smoother and stream-pack rooflines are measured on
+    # the 6561^2 grid (depth 8, 43 M leaves, ~12 GB resident): leaf-level cycle
+    # kernels and the LZMG pack, CUDA events per kernel on the solve stream
+    from paper_2005_03606_b200 import measure
+    hbm_peak = float(peaks().get("hbm_gbs") or 7700.0)
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks().get("hbm_gbs") else "B200_PROFILING fallback"
+    gh = lzb.Grid(lzb.make_desc(depth=HBM_LEVEL, field=f, delta_max=1e-8, solver="adafac-pi", omega=0.6,
+                                rhs_kind="sinprod", integration="fast", max_cycles=10 ** 6), 42, ctx)
+    gh.assemble_fixed(4)
+    for _ in range(2):
+        gh.step()
+    hbm_tab = measure.hbm_kernel_table(gh, HBM_LEVEL, hbm_peak, reps=max(5, args.steps))
+    gh.close()
+    del gh
+    torch.cuda.empty_cache()
+
+    def hbm_roof(kernel):
+        k = hbm_tab[kernel]
+        return {"bound": "hbm", "achieved": k["GB/s"], "peak": hbm_peak, "unit": "GB/s", "frac": k["frac"],
+                "traffic": None, "kernel": kernel, "ms": k["ms"], "algorithmic_bytes": k["bytes"],
+                "grid": f"{3 ** HBM_LEVEL}^2 (depth {HBM_LEVEL}), p = 4 assembly", "peak_source": hbm_src}
+
+    smoother["roofline"] = hbm_roof("k_residual")
+    smoother["hbm_kernels"] = {k: v for k, v in hbm_tab.items() if k != "image_bytes"}
+
     # strong-scaling slab decomposition (§8e): each rank assembles 1/world of the rows,
     # then one all-gather of the leaf state (NCCL) makes the operator replicated
     strong = None
@@ -394,7 +422,8 @@ def run_ours(args, world, rank, local):
         "smoother": smoother,
         "time_to_solution": tts,
         "strong_slabs": strong,
-        "compression": {"p3_histogram": r["p3_hist"], "fine_factor_totals": r["factor"]},
+        "compression": {"p3_histogram": r["p3_hist"], "fine_factor_totals": r["factor"],
+                        "roofline": hbm_roof("k_pack_patches"), "image_bytes_depth8": hbm_tab["image_bytes"]},
         "e2e": e2e,
         "cpu_baseline": base,
         "gpu_launches": r["launches"],
