@@ -1321,11 +1321,12 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_pack_patches(AllLevels A, l
     if (!__all_sync(full, ok) && lane == 0) atomicExch(err, 1);
 }
 
-// Records of levels 0..D-2 (1/80 of the image): one thread per record,
-// bytes straight to global memory.
+// Records of levels 0..D-2 (1/80 of the image): one warp per record, lane =
+// value, bytes straight to global memory.
 __global__ void k_pack_upper(AllLevels A, lzb_field f, int64_t ncells, const int64_t* __restrict__ offsets,
                              uint8_t* __restrict__ out, int* err) {
-    int64_t t = gtid();
+    const int lane = threadIdx.x & 31;
+    int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (t >= ncells) return;
     int l = 0;
     int64_t n = 1;
@@ -1341,18 +1342,24 @@ __global__ void k_pack_upper(AllLevels A, lzb_field f, int64_t ncells, const int
     const int p3 = p1 != LZB_P1_BOTTOM ? L.p3[c] : 0;
     const int size = record_size(p1, p3, false);
     uint8_t* rec = out + 12 + offsets[slot_at(A.st, l, cx, cy)];
-    rec[0] = pack_header(p1, L.p2[c], p3);
+    if (lane == 0) rec[0] = pack_header(p1, L.p2[c], p3);
     if (size == 1) return;
     const double e = centre_eps(f, L, cx, cy);
-    const double* P = transfer_of(L, c);
+    const double* P = (L.P && L.has_P[c]) ? L.P + 64 * static_cast<int64_t>(c) : nullptr;
+    uint8_t* dst = rec + 1;
+    const unsigned long long zero = encode_word(0.0, p3);  // geometric P-hat / R-hat: geo - geo = +0
     bool ok = true;
-    for (int i = 0; i < 144; ++i) {
+    for (int i = lane; i < 144; i += 32) {
+        if (i >= 16 && !P) {
+            put_bytes(dst + i * p3, zero, p3);
+            continue;
+        }
         const double x = i < 16 ? L.op[16 * static_cast<int64_t>(c) + i] - baseline_entry(i, e)
                                 : P[(i - 16) & 63] - c_geo[(i - 16) & 63];
         ok = ok && dev_isfinite(x);
-        put_bytes(rec + 1 + i * p3, encode_word(x, p3), p3);
+        put_bytes(dst + i * p3, encode_word(x, p3), p3);
     }
-    if (!ok) atomicExch(err, 1);
+    if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicExch(err, 1);
 }
 
 // Record sizes in slot order (stream.cpp:227-237): one thread per
@@ -2487,8 +2494,8 @@ public:
                    ctx_->err.p);
         const int64_t upper = total_cells_ - L_[D_].nc - L_[D_ - 1].nc;
         if (upper > 0)
-            LZB_LAUNCH(k_pack_upper, blocks_for(upper, kThreads), kThreads, 0, s_, all_levels(), d_.field, upper,
-                       rec_offs_.p, img, ctx_->err.p);
+            LZB_LAUNCH(k_pack_upper, blocks_for(upper, kThreads / 32), kThreads, 0, s_, all_levels(), d_.field,
+                       upper, rec_offs_.p, img, ctx_->err.p);
     }
 
     // CellStream::save byte image: packed on the device (k_pack_patches) from the
