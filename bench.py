@@ -48,6 +48,17 @@ SURVEY_FLOPS_PER_SAMPLE = 77  # SURVEY.md §8d for C2 (2E + F_eps, sin counted p
 METRIC = "eps sub-sample integrations/s; smoother DoF-updates/s; % FP64/HBM roofline"
 
 
+def traffic_of(kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
+    --set full capture (profiles/traffic.json, tools/summarize_profiles.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f).get(kernel)
+        return None if t is None else t["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -288,7 +299,7 @@ def run_ours(args, world, rank, local):
         per_launch_s = results[mode]["t"] / args.steps
         achieved = SAMPLES_PER_STEP * FLOPS_PER_SAMPLE[mode] / per_launch_s / 1e12
         return {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak, "traffic": None,
+                "frac": achieved / fp64_peak, "traffic": traffic_of("k_fixed_res"), "kernel": "k_fixed_res",
                 "flops_per_sample": FLOPS_PER_SAMPLE[mode],
                 "peak_source": "measured: lzb_probe_fp64_tflops (DFMA chains, this GPU)",
                 "survey_def_achieved": SAMPLES_PER_STEP * SURVEY_FLOPS_PER_SAMPLE / per_launch_s / 1e12}
@@ -328,7 +339,7 @@ def run_ours(args, world, rank, local):
     def hbm_roof(kernel):
         k = hbm_tab[kernel]
         return {"bound": "hbm", "achieved": k["GB/s"], "peak": hbm_peak, "unit": "GB/s", "frac": k["frac"],
-                "traffic": None, "kernel": kernel, "ms": k["ms"], "algorithmic_bytes": k["bytes"],
+                "traffic": traffic_of(kernel), "kernel": kernel, "ms": k["ms"], "algorithmic_bytes": k["bytes"],
                 "grid": f"{3 ** HBM_LEVEL}^2 (depth {HBM_LEVEL}), p = 4 assembly", "peak_source": hbm_src}
 
     smoother["roofline"] = hbm_roof("k_residual")

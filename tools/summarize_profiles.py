@@ -1,8 +1,11 @@
 """Summarise an ncu launch list + a `--set full` report into profiles/<tag>_*.
 
-usage: python tools/summarize_profiles.py <tag> <launches.csv> <full.ncu-rep>
+usage: python tools/summarize_profiles.py <tag> <launches.csv | -> <full.ncu-rep>
+Also merges the per-launch DRAM traffic of every captured kernel into
+profiles/traffic.json (read by bench.py for roofline.traffic).
 """
 import collections
+import json
 import csv
 import io
 import os
@@ -11,7 +14,7 @@ import sys
 
 tag, launches, rep = sys.argv[1], sys.argv[2], sys.argv[3]
 out_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
-rows = list(csv.reader(open(launches)))
+rows = list(csv.reader(open(launches))) if launches != "-" else [["Kernel Name", "Metric Value", "Metric Unit"]]
 hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 h, data = rows[hi], rows[hi + 1:]
 ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
@@ -32,11 +35,12 @@ lines = [f"# {tag}: ncu launch list (gpu__time_duration, --clock-control none; c
          "| kernel | launches | total us | share | avg us |", "|---|---|---|---|---|"]
 for name, (n, t) in sorted(tot.items(), key=lambda x: -x[1][1]):
     lines.append(f"| `{name}` | {n} | {t:.1f} | {100 * t / grand:.1f}% | {t / n:.1f} |")
-open(os.path.join(out_dir, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
-with open(os.path.join(out_dir, f"{tag}_launches.csv"), "w") as f:
-    f.write("kernel,duration_us\n")
-    for name, v in seq:
-        f.write(f"{name},{v:.3f}\n")
+if launches != "-":
+    open(os.path.join(out_dir, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
+    with open(os.path.join(out_dir, f"{tag}_launches.csv"), "w") as f:
+        f.write("kernel,duration_us\n")
+        for name, v in seq:
+            f.write(f"{name},{v:.3f}\n")
 
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rr = list(csv.reader(io.StringIO(raw)))
@@ -62,3 +66,14 @@ for v in vals:
     lines.append(f"| `{name}` | " + " | ".join(cells) + " |")
 open(os.path.join(out_dir, f"{tag}_ncu_full.md"), "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
+
+# per-launch DRAM traffic (bytes) of each captured kernel, last capture wins
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+tpath = os.path.join(out_dir, "traffic.json")
+traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
+ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+for v in vals:
+    name = v[kn].split("(")[0].split("::")[-1].replace("void ", "").split("<")[0].strip()
+    b = float(v[ir].replace(",", "")) * scale.get(units[ir], 1) + float(v[iw].replace(",", "")) * scale.get(units[iw], 1)
+    traffic[name] = {"dram_bytes_per_launch": b, "report": os.path.basename(rep), "tag": tag}
+json.dump(traffic, open(tpath, "w"), indent=1, sort_keys=True)
