@@ -149,6 +149,20 @@ int lzb_grid_load(lzb_grid* g, const char* path);
 int64_t lzb_grid_pending(lzb_grid* g);
 /* Device pointers for callers composing their own kernels (read-only use). */
 int lzb_grid_device_view(lzb_grid* g, int level, int field, void** ptr);
+/* Slab-distributed cycle (no reference counterpart: the
+ * reference is shared-memory only). One rank per GPU holds the whole grid;
+ * the leaf level's vertex rows [v0, v1) (multiples of 3, v1 may be N+1) are
+ * this rank's slab, the coarse levels run replicated. A cycle is
+ * lzb_grid_dist_phase 0..5 with the host exchanges in between
+ * (paper_2005_03606_b200/parallel.py: r̂ halo after 0, all-gather of level
+ * D-1 fl after 1, all-reduce of lzb_grid_dist_result after 2 then
+ * lzb_grid_dist_report, all-gather of aux / u of level D-1 after 3 / 4, u
+ * halo after 5). flags bit 0 on phase 0: count the coarse levels' stats
+ * (one rank). Every vertex value is bit-identical to the one-GPU cycle. */
+int lzb_grid_set_slab(lzb_grid* g, int v0, int v1);
+int lzb_grid_dist_phase(lzb_grid* g, int phase, int flags);
+int lzb_grid_dist_result(lzb_grid* g, double* norm2, uint64_t* slots20);
+int lzb_grid_dist_report(lzb_grid* g, double norm2, const uint64_t* slots20, lzb_cycle_report* rep);
 /* Device time (CUDA events on the solve stream) of one hot kernel of the
  * leaf level, averaged over `reps` back-to-back launches: LZB_TK_* ids.
  * No reference counterpart: the measurement hook behind bench.py's roofline. */

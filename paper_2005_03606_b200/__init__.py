@@ -13,9 +13,11 @@ or device raises ``LzbError``.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
 import subprocess
+import weakref
 
 import numpy as np
 
@@ -116,6 +118,10 @@ def lib():
         L.lzb_grid_pending.argtypes = [vp]
         L.lzb_grid_device_view.argtypes = [vp, C.c_int, C.c_int, C.POINTER(vp)]
         L.lzb_grid_time_kernel.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_double)]
+        L.lzb_grid_set_slab.argtypes = [vp, C.c_int, C.c_int]
+        L.lzb_grid_dist_phase.argtypes = [vp, C.c_int, C.c_int]
+        L.lzb_grid_dist_result.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+        L.lzb_grid_dist_report.argtypes = [vp, C.c_double, C.POINTER(C.c_uint64), C.POINTER(CycleReport)]
         L.lzb_run_experiment_file.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.lzb_run_experiment_text.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.lzb_last_reports.argtypes = [vp, C.c_int, C.POINTER(C.c_int)]
@@ -341,6 +347,17 @@ def make_desc(depth=2, field: Field | None = None, rhs: float = 0.0, rhs_kind="c
     return d
 
 
+# grids still alive at interpreter exit are destroyed before the CUDA runtime
+# tears down (objects kept alive by tracebacks would otherwise be freed late)
+_live_grids: "weakref.WeakSet" = weakref.WeakSet()
+
+
+@atexit.register
+def _close_live_grids():
+    for g in list(_live_grids):
+        g.close()
+
+
 class Grid:
     """Mesh + CellStream + Assembler + AdditiveSolver of one regular 2D
     spacetree, resident on the GPU (solver.hpp:72-126 semantics)."""
@@ -352,6 +369,7 @@ class Grid:
         h = C.c_void_p()
         _check(lib().lzb_grid_create(self.ctx.h, C.byref(desc), C.byref(h)))
         self.h = h
+        _live_grids.add(self)
         if noise_seed is not None:
             self.init_noise(noise_seed)
 
@@ -382,6 +400,25 @@ class Grid:
         n = C.c_int()
         _check(lib().lzb_grid_run(self.h, arr, cap, C.byref(n)))
         return [report_dict(arr[i]) for i in range(min(cap, n.value))]
+
+    # slab-distributed cycle (parallel.py drives the phases and the exchanges)
+    def set_slab(self, v0, v1):
+        _check(lib().lzb_grid_set_slab(self.h, v0, v1))
+
+    def dist_phase(self, phase, flags=0):
+        _check(lib().lzb_grid_dist_phase(self.h, phase, flags))
+
+    def dist_result(self):
+        n2 = C.c_double()
+        slots = (C.c_uint64 * 20)()
+        _check(lib().lzb_grid_dist_result(self.h, C.byref(n2), slots))
+        return n2.value, list(slots)
+
+    def dist_report(self, norm2, slots) -> dict:
+        arr = (C.c_uint64 * 20)(*[int(x) for x in slots])
+        r = CycleReport()
+        _check(lib().lzb_grid_dist_report(self.h, float(norm2), arr, C.byref(r)))
+        return report_dict(r)
 
     def pass_(self, which):
         v = C.c_double()

@@ -511,6 +511,9 @@ struct LevelView {
     // recompute attempt of a refined cell (0 = never)
     uint32_t* chg;
     uint32_t* seen;
+    // first vertex row of a row-range launch of the 2D vertex kernels
+    // (blockIdx.y + row0); 0 for whole-level launches
+    int row0;
 };
 
 __device__ inline int32_t crank(const LevelView& L, int cx, int cy) { return L.rx[cx] + L.ry[cy]; }

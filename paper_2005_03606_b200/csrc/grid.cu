@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(64) k_coarse(LevelView C, LevelView F, lzb_fie
 // integer division for coordinates).
 __device__ inline bool vertex_xy(const LevelView& L, int& ix, int& iy, int64_t& vi) {
     ix = blockIdx.x * blockDim.x + threadIdx.x;
-    iy = blockIdx.y;
+    iy = blockIdx.y + L.row0;
     if (ix > L.N) return false;
     vi = static_cast<int64_t>(iy) * (L.N + 1) + ix;
     return true;
@@ -861,15 +861,17 @@ __global__ void k_restrict(LevelView F, LevelView C, int mode, double omega) {
 // b sums rows 1+b, 1+b+G, ... four rows per step (independent loads in
 // flight), then a fixed-order tree; k_norm_final adds the kNormBlocks partials.
 constexpr int kNormBlocks = 148 * 4;
-__global__ void __launch_bounds__(kThreads) k_norm_partial(LevelView F, double* partial) {
+__global__ void __launch_bounds__(kThreads) k_norm_partial(LevelView F, int y0, int y1, double* partial) {
     __shared__ double sh[kThreads];
     const int N = F.N;
     const double* r = F.v[LZB_V_R];
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     const int G = gridDim.x;
-    for (int iy = 1 + blockIdx.x; iy < N; iy += 4 * G) {
+    // interior rows [max(y0,1), min(y1,N))
+    const int ylo = max(y0, 1), yhi = min(y1, N);
+    for (int iy = ylo + blockIdx.x; iy < yhi; iy += 4 * G) {
         const int64_t b0 = static_cast<int64_t>(iy) * (N + 1);
-        const bool h1 = iy + G < N, h2 = iy + 2 * G < N, h3 = iy + 3 * G < N;
+        const bool h1 = iy + G < yhi, h2 = iy + 2 * G < yhi, h3 = iy + 3 * G < yhi;
         for (int ix = 1 + threadIdx.x; ix < N; ix += blockDim.x) {
             const double a0 = r[b0 + ix];
             const double a1 = h1 ? r[b0 + static_cast<int64_t>(G) * (N + 1) + ix] : 0.0;
@@ -891,7 +893,8 @@ __global__ void __launch_bounds__(kThreads) k_norm_partial(LevelView F, double* 
 }
 
 constexpr int kNormFinalThreads = 1024;
-__global__ void __launch_bounds__(kNormFinalThreads) k_norm_final(const double* partial, int n, Result* res) {
+__global__ void __launch_bounds__(kNormFinalThreads) k_norm_final(const double* partial, int n, Result* res,
+                                                                   int squared = 0) {
     __shared__ double sh[kNormFinalThreads];
     double s = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) s += partial[i];
@@ -901,21 +904,22 @@ __global__ void __launch_bounds__(kNormFinalThreads) k_norm_final(const double* 
         if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
         __syncthreads();
     }
-    if (threadIdx.x == 0) res->norm = sqrt(sh[0]);
+    if (threadIdx.x == 0) res->norm = squared ? sh[0] : sqrt(sh[0]);
 }
 
 // compression_stats over leaves + record bytes of refined cells (stream.cpp:268-301).
 // Grid-stride: per-thread counters over the cells, then warp reductions and
 // one atomic per counter per block.
 constexpr int kStatsBlocks = 148 * 4;
-__global__ void __launch_bounds__(kThreads) k_stats(LevelView L, int leaf, unsigned long long* s) {
+__global__ void __launch_bounds__(kThreads) k_stats(LevelView L, int leaf, unsigned long long* s,
+                                                    int64_t cbeg = 0, int64_t cend = -1) {
     __shared__ unsigned long long sh[20];
     if (threadIdx.x < 20) sh[threadIdx.x] = 0;
     __syncthreads();
-    const int64_t nc = static_cast<int64_t>(L.N) * L.N;
+    const int64_t nc = cend < 0 ? static_cast<int64_t>(L.N) * L.N : cend;
     unsigned long long bytes = 0, nsum = 0;
     unsigned nmax = 0, pend = 0, h[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int64_t c = gtid(); c < nc; c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    for (int64_t c = cbeg + gtid(); c < nc; c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int32_t p1 = L.p1[c];
         const int p3raw = L.p3[c];
         const int p3 = p1 != LZB_P1_BOTTOM ? p3raw : 0;
@@ -1780,7 +1784,7 @@ public:
         blockcnt_.alloc(blocks_for(leaves_, kCompactThreads));
         hist_.alloc(kNHist);
         partial_.alloc(kNormBlocks);
-        if (d.variant == LZB_ADAFAC_PI) caux_.alloc(L_[D_ - 1].nv);
+        if (d.variant == LZB_ADAFAC_PI && D_ >= 1) caux_.alloc(L_[D_ - 1].nv);
         res_.alloc(1);
         LZB_CUDA(cudaMemsetAsync(res_.p, 0, sizeof(Result), s_));
         if (d.throttle) keys_.alloc(leaves_);
@@ -2154,7 +2158,7 @@ public:
                 LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l),
                            V(l - 1), 0, 0.0);
         }
-        LZB_LAUNCH(k_norm_partial, kNormBlocks, kThreads, 0, s_, V(D_), partial_.p);
+        LZB_LAUNCH(k_norm_partial, kNormBlocks, kThreads, 0, s_, V(D_), 0, L_[D_].N + 1, partial_.p);
         LZB_LAUNCH(k_norm_final, 1, kNormFinalThreads, 0, s_, partial_.p, kNormBlocks, res_.p);
     }
 
@@ -2301,13 +2305,23 @@ public:
             throw Error(LZB_ERR_PROTOCOL, "cannot encode non-finite operator entry");
         }
         Result r = *hres_;
+        if (front_report(rep, r)) run_graph(g_back_, &Grid::back_body);  // update + prolongation + injection
+        finish_report(rep, r);
+        LZB_CUDA(cudaStreamSynchronize(s_));
+        rep.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return rep;
+    }
+
+    // step() bookkeeping after the residual pass (solver.cpp:359-370): history,
+    // normalisation, termination; true when the update passes run.
+    bool front_report(lzb_cycle_report& rep, const Result& r) {
         rep.residual = r.norm;
         if (first_residual_ < 0.0) first_residual_ = rep.residual > 0.0 ? rep.residual : 1.0;
         rep.normalized = rep.residual / first_residual_;
         history_.push_back(rep.residual);
         rep.status = check_termination();
-        if (rep.status == LZB_CONTINUE || rep.status == LZB_TIMEOUT) {
-            run_graph(g_back_, &Grid::back_body);  // update + prolongation + injection
+        const bool update = rep.status == LZB_CONTINUE || rep.status == LZB_TIMEOUT;
+        if (update) {
             uint64_t Nf = static_cast<uint64_t>(L_[D_].N);
             rep.dof_updates = (Nf - 1) * (Nf - 1);
             for (int l = 0; l < D_; ++l) {
@@ -2315,6 +2329,11 @@ public:
                 rep.coarse_updates += N > 1 ? (N - 1) * (N - 1) : 0;
             }
         }
+        return update;
+    }
+
+    // step() telemetry after the cycle (solver.cpp:371-400).
+    void finish_report(lzb_cycle_report& rep, const Result& r) {
         dof_total_ += rep.dof_updates;
         rep.dof_updates_total = dof_total_;
         pending_ = d_.mode == LZB_ANARCHIC ? static_cast<int64_t>(r.s[S_PENDING]) : 0;
@@ -2335,8 +2354,136 @@ public:
         uint64_t Nf = static_cast<uint64_t>(L_[D_].N);
         rep.dofs_fine_interior = (Nf - 1) * (Nf - 1);
         rep.grid_points_total = static_cast<uint64_t>(total_vertices_);
-        LZB_CUDA(cudaStreamSynchronize(s_));
-        rep.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+
+    // ------------------------------------------------ slab-distributed cycle
+    // SURVEY.md §8e. The leaf level is cut into slabs of vertex rows [v0, v1)
+    // (multiples of 3, so every level-(D-1) vertex row 3*IY belongs to one
+    // slab); the coarse levels are small (1/8 of the leaf work together) and
+    // run replicated. One cycle = phases 0..5 with exchanges in between, done
+    // by the host layer (paper_2005_03606_b200/parallel.py, NCCL):
+    //   0  cycle start, coarse recompute, leaf û (slab +-1 row), residual,
+    //      norm^2 partial, leaf stats of the slab     -> r̂ halo (3 rows)
+    //   1  restriction into level D-1, owned rows       -> all-gather fl_{D-1}
+    //   2  residual pass of levels D-1..0, result to host -> all-reduce, report
+    //   3  snapshots, adaFAC-PI injection into aux_{D-1} -> all-gather aux_{D-1}
+    //   4  coarse updates, prolongation to D-1, fused leaf update of the slab,
+    //      injection into u_{D-1}                      -> all-gather u_{D-1}
+    //   5  injections D-1..1                           -> u halo (1 row)
+    // Every vertex value is computed by the same kernel in the same order as
+    // on one GPU, so u, r, fl are bit-identical; only the norm sum is regrouped.
+    void set_slab(int v0, int v1) {
+        const int NV = L_[D_].N + 1;
+        if (D_ < 1) throw Error(LZB_ERR_INVALID, "slabs need depth >= 1");
+        if (v0 < 0 || v1 > NV || v0 >= v1) throw Error(LZB_ERR_INVALID, "bad slab rows");
+        if (v0 % 3 != 0 || (v1 % 3 != 0 && v1 != NV)) throw Error(LZB_ERR_INVALID, "slab rows must be multiples of 3");
+        if (d_.variant == LZB_ADAFAC_JAC)
+            throw Error(LZB_ERR_INVALID, "the distributed cycle supports additive and adafac-pi");
+        if (d_.concurrent) throw Error(LZB_ERR_INVALID, "the distributed cycle runs the deterministic modes");
+        slab_v0_ = v0;
+        slab_v1_ = v1;
+    }
+    LevelView Vrow(int l, int r0) const {
+        LevelView v = V(l);
+        v.row0 = r0;
+        return v;
+    }
+    dim3 vgrid_rows(int l, int r0, int r1) const { return dim3(blocks_for(L_[l].N + 1, kThreads), r1 - r0); }
+
+    void dist_phase(int phase, int flags) {
+        const int N = L_[D_].N, v0 = slab_v0_, v1 = slab_v1_ < 0 ? N + 1 : slab_v1_;
+        const int c0 = v0 / 3, c1 = (v1 + 2) / 3;
+        switch (phase) {
+            case 0: {
+                dist_t0_ = std::chrono::steady_clock::now();
+                ++cycle_;
+                *hcycle_ = cycle_;
+                pool_begin_cycle();
+                run_graph(g_coarse_, &Grid::coarse_pass);
+                leaves_pass();
+                ensure_rhs();
+                const int u0 = std::max(v0 - 1, 0), u1 = std::min(v1 + 1, N + 1);
+                LZB_LAUNCH(k_uhat, vgrid_rows(D_, u0, u1), kThreads, 0, s_, Vrow(D_, u0), V(D_ - 1), 1);
+                LZB_LAUNCH(k_residual, vgrid_rows(D_, v0, v1), kThreads, 0, s_, Vrow(D_, v0), d_.field);
+                LZB_LAUNCH(k_reset_stats, 1, 32, 0, s_, res_.p);
+                const int cr1 = std::min(v1, N);
+                if (cr1 > v0)
+                    LZB_LAUNCH(k_stats, static_cast<unsigned>(kStatsBlocks), kThreads, 0, s_, V(D_), 1, res_.p->s,
+                               static_cast<int64_t>(v0) * N, static_cast<int64_t>(cr1) * N);
+                if (flags & 1)  // the replicated coarse levels are counted by one rank
+                    for (int l = 0; l < D_; ++l)
+                        LZB_LAUNCH(k_stats, static_cast<unsigned>(std::min<int64_t>(blocks_for(L_[l].nc, kThreads),
+                                                                                    kStatsBlocks)),
+                                   kThreads, 0, s_, V(l), 0, res_.p->s);
+                LZB_LAUNCH(k_norm_partial, kNormBlocks, kThreads, 0, s_, V(D_), v0, v1, partial_.p);
+                LZB_LAUNCH(k_norm_final, 1, kNormFinalThreads, 0, s_, partial_.p, kNormBlocks, res_.p, 1);
+                break;
+            }
+            case 1:
+                LZB_LAUNCH(k_restrict, vgrid_rows(D_ - 1, c0, c1), kThreads, 0, s_, V(D_), Vrow(D_ - 1, c0), 0, 0.0);
+                break;
+            case 2:
+                for (int l = D_ - 1; l >= 0; --l) {
+                    const dim3 g = vgrid(l);
+                    LZB_LAUNCH(k_uhat, g, kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
+                    LZB_LAUNCH(k_residual, g, kThreads, 0, s_, V(l), d_.field);
+                    if (l > 0) LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1), 0, 0.0);
+                }
+                LZB_CUDA(cudaMemcpyAsync(hres_, res_.p, sizeof(Result), cudaMemcpyDeviceToHost, s_));
+                sync_check();
+                break;
+            case 3:
+                for (int l = 0; l < D_; ++l)
+                    LZB_LAUNCH(k_snap, blocks_for(L_[l].nv, kThreads), kThreads, 0, s_, V(l));
+                if (d_.variant == LZB_ADAFAC_PI)
+                    LZB_LAUNCH(k_aux_inject, vgrid_rows(D_ - 1, c0, c1), kThreads, 0, s_, V(D_), Vrow(D_ - 1, c0));
+                break;
+            case 4: {
+                const double omega = d_.omega;
+                const bool pi = d_.variant == LZB_ADAFAC_PI;
+                for (int l = D_ - 1; l >= 0; --l) {
+                    const dim3 g = vgrid(l);
+                    if (pi && l > 0) {
+                        LZB_LAUNCH(k_aux_inject, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1));
+                        LZB_LAUNCH(k_aux_sub, g, kThreads, 0, s_, V(l), V(l - 1), omega);
+                    }
+                    LZB_LAUNCH(k_jacobi, g, kThreads, 0, s_, V(l), damping(l));
+                }
+                prolong_launches(D_ - 1);
+                if (pi) LZB_LAUNCH(k_scale_aux, vgrid(D_ - 1), kThreads, 0, s_, V(D_ - 1), omega, caux_.p);
+                LZB_LAUNCH(k_update_fine, vgrid_rows(D_, v0, v1), kThreads, 0, s_, Vrow(D_, v0), V(D_ - 1),
+                           pi ? caux_.p : nullptr, damping(D_));
+                LZB_LAUNCH(k_inject, vgrid_rows(D_ - 1, c0, c1), kThreads, 0, s_, V(D_), Vrow(D_ - 1, c0));
+                break;
+            }
+            case 5:
+                for (int l = D_ - 1; l >= 1; --l)
+                    LZB_LAUNCH(k_inject, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1));
+                sync_check();
+                break;
+            default: throw Error(LZB_ERR_INVALID, "unknown phase");
+        }
+    }
+
+    // Result of phase 2 for the host reduction: the slab's sum of r^2 and the
+    // 20 counter slots.
+    void dist_result(double* norm2, uint64_t* slots) const {
+        *norm2 = hres_->norm;
+        for (int k = 0; k < 20; ++k) slots[k] = hres_->s[k];
+    }
+
+    // The cycle report from the reduced norm^2 and counters (every rank gets
+    // the same); report.status tells whether phases 3-5 run.
+    lzb_cycle_report dist_report(double norm2, const uint64_t* slots) {
+        lzb_cycle_report rep;
+        std::memset(&rep, 0, sizeof rep);
+        rep.cycle = static_cast<int32_t>(cycle_);
+        Result r;
+        r.norm = std::sqrt(norm2);
+        for (int k = 0; k < 20; ++k) r.s[k] = slots[k];
+        front_report(rep, r);
+        finish_report(rep, r);
+        rep.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - dist_t0_).count();
         return rep;
     }
 
@@ -2701,6 +2848,8 @@ private:
     cudaGraphExec_t g_coarse_ = nullptr, g_front_ = nullptr, g_back_ = nullptr;
     uint64_t graph_kernels_[3] = {0, 0, 0};
     double first_residual_ = -1.0;
+    int slab_v0_ = 0, slab_v1_ = -1;  // leaf vertex rows of this rank's slab (-1: the whole level)
+    std::chrono::steady_clock::time_point dist_t0_{};
     std::vector<double> history_;
     uint64_t dof_total_ = 0;
     int64_t pending_ = 0;
@@ -2802,6 +2951,18 @@ int lzb_grid_stream_image(lzb_grid* g, uint8_t* out, int64_t cap, int64_t* size)
         }
         *size = g->g->image_into(out, cap);
     });
+}
+int lzb_grid_set_slab(lzb_grid* g, int v0, int v1) {
+    return guarded([&] { g->g->set_slab(v0, v1); });
+}
+int lzb_grid_dist_phase(lzb_grid* g, int phase, int flags) {
+    return guarded([&] { g->g->dist_phase(phase, flags); });
+}
+int lzb_grid_dist_result(lzb_grid* g, double* norm2, uint64_t* slots20) {
+    return guarded([&] { g->g->dist_result(norm2, slots20); });
+}
+int lzb_grid_dist_report(lzb_grid* g, double norm2, const uint64_t* slots20, lzb_cycle_report* rep) {
+    return guarded([&] { *rep = g->g->dist_report(norm2, slots20); });
 }
 int lzb_grid_time_kernel(lzb_grid* g, int what, int reps, double* avg_ms) {
     return guarded([&] { *avg_ms = g->g->time_kernel(what, reps); });

@@ -139,3 +139,199 @@ def sum_over_ranks(x, group=None, device=None):
     t = torch.tensor(arr, device=device or "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t.cpu().numpy()
+
+
+# ------------------------------------------------------ slab-distributed cycle
+# the leaf level's vertex rows are cut into slabs (multiples of
+# 3), one per rank; the coarse levels run replicated. Grid.dist_phase 0..5 do
+# the compute (csrc/grid.cu, Grid::dist_phase); this layer does the exchanges
+# in between: NCCL point-to-point halos and all-gathers of level-(D-1) rows
+# over torch.distributed (TorchComm), or device copies between several slabs
+# of one process (LoopbackComm, the one-GPU test of the same plan).
+
+# Result slots reduced by max (S_MAXN, S_MAXDELTA as non-negative double bits,
+# S_MAXSAMPLES); every other slot is a count, reduced by sum.
+MAX_SLOTS = (11, 14, 15)
+
+
+def slab_vertex_rows(n_cells: int, world: int, rank: int) -> tuple[int, int]:
+    """Leaf vertex rows [v0, v1) of `rank`: the cell-row slab of slab_rows
+    (boundaries at multiples of 3); the last rank also owns vertex row N."""
+    if n_cells // 3 < world:
+        raise ValueError(f"{world} slabs need at least {3 * world} cell rows")
+    r0, r1 = slab_rows(n_cells, world, rank)
+    return r0, (n_cells + 1 if r1 >= n_cells else r1)
+
+
+class Slab:
+    """One rank's view: its Grid (whole-grid storage) and its leaf rows."""
+
+    def __init__(self, grid, rank: int, world: int):
+        self.grid, self.rank, self.world = grid, rank, world
+        self.D = grid.depth
+        self.N = 3 ** self.D
+        self.v0, self.v1 = slab_vertex_rows(self.N, world, rank)
+        self.c0, self.c1 = self.v0 // 3, (self.v1 + 2) // 3  # owned rows of level D-1
+        grid.set_slab(self.v0, self.v1)
+
+    def field(self, level: int, fld: int):
+        n = 3 ** level + 1
+        return device_tensor(self.grid.device_view(level, fld), n * n, "<f8")
+
+
+def _row_ranges(slabs_or_plan, level_is_coarse: bool):
+    return [(s.c0, s.c1) if level_is_coarse else (s.v0, s.v1) for s in slabs_or_plan]
+
+
+class LoopbackComm:
+    """All ranks in this process (one GPU): exchanges are device copies on the
+    solve stream the slabs' kernels run on."""
+
+    def __init__(self, stream=None):
+        self.stream = stream
+
+    def _ctx(self):
+        import contextlib
+
+        import torch
+        return torch.cuda.stream(self.stream) if self.stream is not None else contextlib.nullcontext()
+
+    def halo(self, slabs, level, fld, depth):
+        n = 3 ** level + 1
+        with self._ctx():
+            for i, s in enumerate(slabs):
+                t = s.field(level, fld)
+                if i > 0:  # rows below the slab from the previous rank
+                    a = max(s.v0 - depth, 0)
+                    t[a * n:s.v0 * n].copy_(slabs[i - 1].field(level, fld)[a * n:s.v0 * n])
+                if i + 1 < len(slabs):
+                    b = min(s.v1 + depth, n)
+                    t[s.v1 * n:b * n].copy_(slabs[i + 1].field(level, fld)[s.v1 * n:b * n])
+
+    def allgather_rows(self, slabs, level, fld):
+        n = 3 ** level + 1
+        with self._ctx():
+            for s in slabs:
+                src = s.field(level, fld)[s.c0 * n:s.c1 * n]
+                for o in slabs:
+                    if o is not s:
+                        o.field(level, fld)[s.c0 * n:s.c1 * n].copy_(src)
+
+    def reduce(self, results):
+        norm2 = sum(r[0] for r in results)
+        slots = [max(r[1][k] for r in results) if k in MAX_SLOTS else sum(r[1][k] for r in results)
+                 for k in range(20)]
+        return norm2, slots
+
+
+class TorchComm:
+    """One slab per process over torch.distributed: point-to-point halos
+    (batch_isend_irecv) and padded all-gathers of level-(D-1) rows; NCCL on
+    the GPU box (tensors alias liblzb device memory), gloo for CPU tensors."""
+
+    def __init__(self, group=None, stream=None):
+        self.group, self.stream = group, stream
+
+    def _ctx(self):
+        import contextlib
+
+        import torch
+        return torch.cuda.stream(self.stream) if self.stream is not None else contextlib.nullcontext()
+
+    def halo_tensor(self, t, n, v0, v1, depth):
+        """Exchange `depth` rows (of n elements) of the flat row-major tensor t
+        with the neighbouring ranks: send own boundary rows, receive theirs."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
+        nrows = t.numel() // n
+        ops = []
+        if rank > 0:
+            a = max(v0 - depth, 0)
+            ops.append(dist.P2POp(dist.isend, t[v0 * n:min(v0 + depth, v1) * n], rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, t[a * n:v0 * n], rank - 1, self.group))
+        if rank + 1 < world:
+            b = min(v1 + depth, nrows)
+            ops.append(dist.P2POp(dist.isend, t[max(v1 - depth, v0) * n:v1 * n], rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, t[v1 * n:b * n], rank + 1, self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
+    def halo(self, slabs, level, fld, depth):
+        (s,) = slabs
+        with self._ctx():
+            self.halo_tensor(s.field(level, fld), 3 ** level + 1, s.v0, s.v1, depth)
+
+    def allgather_tensor(self, t, n, ranges):
+        """Every rank's rows [r0, r1) of t (n elements per row) into all ranks."""
+        import torch
+        import torch.distributed as dist
+        rank = dist.get_rank(self.group)
+        maxr = max(b - a for a, b in ranges)
+        send = torch.zeros(maxr * n, dtype=t.dtype, device=t.device)
+        a, b = ranges[rank]
+        send[:(b - a) * n] = t[a * n:b * n]
+        recv = torch.empty(len(ranges) * maxr * n, dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(recv, send, group=self.group)
+        for q, (a, b) in enumerate(ranges):
+            if q != rank and b > a:
+                t[a * n:b * n] = recv[q * maxr * n:q * maxr * n + (b - a) * n]
+
+    def allgather_rows(self, slabs, level, fld):
+        import torch.distributed as dist
+        (s,) = slabs
+        world = dist.get_world_size(self.group)
+        ranges = []
+        for r in range(world):
+            v0, v1 = slab_vertex_rows(s.N, world, r)
+            ranges.append((v0 // 3, (v1 + 2) // 3))
+        with self._ctx():
+            self.allgather_tensor(s.field(level, fld), 3 ** level + 1, ranges)
+
+    def reduce(self, results, device=None):
+        import torch
+        import torch.distributed as dist
+        ((norm2, slots),) = results
+        dev = device or ("cuda" if dist.get_backend(self.group) == "nccl" else "cpu")
+        sums = torch.tensor([0 if k in MAX_SLOTS else int(slots[k]) for k in range(20)], dtype=torch.int64,
+                            device=dev)
+        maxs = torch.tensor([int(slots[k]) if k in MAX_SLOTS else 0 for k in range(20)], dtype=torch.int64,
+                            device=dev)
+        n2 = torch.tensor([float(norm2)], dtype=torch.float64, device=dev)
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=self.group)
+        dist.all_reduce(maxs, op=dist.ReduceOp.MAX, group=self.group)
+        dist.all_reduce(n2, op=dist.ReduceOp.SUM, group=self.group)
+        s, m = sums.cpu().tolist(), maxs.cpu().tolist()
+        return float(n2.item()), [m[k] if k in MAX_SLOTS else s[k] for k in range(20)]
+
+
+def dist_cycle(slabs, comm, adafac_pi: bool) -> dict:
+    """One slab-distributed cycle (Grid::dist_phase 0..5 with the exchanges in
+    between); returns the cycle report (identical on every rank)."""
+    import paper_2005_03606_b200 as lzb
+
+    V = lzb.T
+    D = slabs[0].D
+    for s in slabs:
+        s.grid.dist_phase(0, 1 if s.rank == 0 else 0)
+    comm.halo(slabs, D, V.V_RHAT, 3)               # restriction reads r̂ 3 rows beyond the slab
+    for s in slabs:
+        s.grid.dist_phase(1)
+    comm.allgather_rows(slabs, D - 1, V.V_FL)      # restricted load of level D-1
+    for s in slabs:
+        s.grid.dist_phase(2)
+    norm2, slots = comm.reduce([s.grid.dist_result() for s in slabs])
+    reps = [s.grid.dist_report(norm2, slots) for s in slabs]
+    rep = reps[0]
+    if rep["status"] in (V.CONTINUE, V.TIMEOUT):
+        for s in slabs:
+            s.grid.dist_phase(3)
+        if adafac_pi:
+            comm.allgather_rows(slabs, D - 1, V.V_AUX)  # injected residual of level D-1
+        for s in slabs:
+            s.grid.dist_phase(4)
+        comm.allgather_rows(slabs, D - 1, V.V_U)        # injected solution of level D-1
+        for s in slabs:
+            s.grid.dist_phase(5)
+        comm.halo(slabs, D, V.V_U, 1)                   # leaf u one row beyond the slab
+    return rep
