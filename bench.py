@@ -361,7 +361,27 @@ def run_ours(args, world, rank, local):
                   "ms_per_step": 1e3 * ts / args.steps, "scaling": "strong", "ranks": world,
                   "what": "slab assembly of one 729^2 p=32 pass split over the ranks + NCCL all-gather "
                           "of the leaf operators/markers (replicated solve follows)"}
+        gs.close()
         del gs
+        # slab-distributed cycle (strong scaling on the 6561^2 grid): leaf rows split
+        # over the ranks, NCCL halos / all-gathers between the phases
+        gd = lzb.Grid(lzb.make_desc(depth=HBM_LEVEL, field=f, delta_max=1e-8, solver="adafac-pi", omega=0.6,
+                                    rhs_kind="sinprod", integration="fast", max_cycles=10 ** 6), 42, ctx)
+        gd.assemble_fixed(4)
+        slab = parallel.Slab(gd, rank, world)
+        comm = parallel.TorchComm(stream=stream)
+        for _ in range(2):
+            parallel.dist_cycle([slab], comm, True)
+        kd = max(3, args.steps)
+        td = timed_steps(lambda: parallel.dist_cycle([slab], comm, True), kd)
+        td = max_over_ranks(td, world)
+        dofd = (3 ** HBM_LEVEL - 1) ** 2
+        strong["smoother"] = {"value": dofd * kd / td, "unit": "DoF-updates/s", "ms_per_cycle": 1e3 * td / kd,
+                              "scaling": "strong", "ranks": world,
+                              "what": f"{3 ** HBM_LEVEL}^2 adaFAC-PI cycle, leaf rows in slabs, coarse levels "
+                                      "replicated, NCCL halo + all-gather exchanges (parallel.dist_cycle)"}
+        gd.close()
+        del gd
 
     # time to solution of the delayed-assembly solve (BASELINE configs[1]): p doubling
     # 1 -> 32 on the side stream while the adaFAC cycles run (termination-c = 0 forces
