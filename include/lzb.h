@@ -160,6 +160,10 @@ int lzb_grid_device_view(lzb_grid* g, int level, int field, void** ptr);
  * halo after 5). flags bit 0 on phase 0: count the coarse levels' stats
  * (one rank). Every vertex value is bit-identical to the one-GPU cycle. */
 int lzb_grid_set_slab(lzb_grid* g, int v0, int v1);
+/* The leaf level's compressed records read by the residual (desc.plane_width
+ * > 0; NULL otherwise): 16 slots of `width` bytes per cell, and the width
+ * each cell's slots hold (> width: the FP64 operator is read). */
+int lzb_grid_plane_arrays(lzb_grid* g, void** planes, void** cp3, int* width);
 int lzb_grid_dist_phase(lzb_grid* g, int phase, int flags);
 int lzb_grid_dist_result(lzb_grid* g, double* norm2, uint64_t* slots20);
 int lzb_grid_dist_report(lzb_grid* g, double norm2, const uint64_t* slots20, lzb_cycle_report* rep);

@@ -108,6 +108,12 @@ typedef struct lzb_grid_desc {
     uint64_t throttle;        /* tasks per cycle, 0 = unlimited                     */
     uint64_t noise_seed;
     double boundary_value;
+    /* extensions (no reference counterpart) */
+    int32_t plane_width;      /* 0: the residual reads the decoded FP64 operators; 2..8: it
+                                 decodes the leaf records' compressed surplus bytes (a slot of
+                                 plane_width bytes per entry; wider records fall back to FP64) */
+    int32_t fixed_p3;         /* 0: choose_precision per leaf record; 2..8: every leaf record
+                                 at this width (the mantissa-width sweep, BASELINE configs[4]) */
 } lzb_grid_desc;
 
 /* CycleReport, solver.hpp:41-61 (field for field). */

@@ -119,6 +119,7 @@ def lib():
         L.lzb_grid_device_view.argtypes = [vp, C.c_int, C.c_int, C.POINTER(vp)]
         L.lzb_grid_time_kernel.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.lzb_grid_set_slab.argtypes = [vp, C.c_int, C.c_int]
+        L.lzb_grid_plane_arrays.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(C.c_int)]
         L.lzb_grid_dist_phase.argtypes = [vp, C.c_int, C.c_int]
         L.lzb_grid_dist_result.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
         L.lzb_grid_dist_report.argtypes = [vp, C.c_double, C.POINTER(C.c_uint64), C.POINTER(CycleReport)]
@@ -322,7 +323,7 @@ def make_desc(depth=2, field: Field | None = None, rhs: float = 0.0, rhs_kind="c
               rhs_scale=2 * np.pi ** 2, delta_max=1e-8, solver="adafac-pi", omega=0.7, target=1e-10,
               divergence=1e2, max_cycles=500, assembly="adaptive", termination_c=0.01, schedule="increment",
               n_max=0, integration="exact", transfer="geometric", gating=True, throttle=0, seed=0,
-              concurrent=False) -> GridDesc:
+              concurrent=False, plane_width=0, fixed_p3=0) -> GridDesc:
     d = GridDesc()
     d.dim = 2
     d.depth = depth
@@ -344,6 +345,8 @@ def make_desc(depth=2, field: Field | None = None, rhs: float = 0.0, rhs_kind="c
     d.concurrent = 1 if concurrent else 0
     d.throttle = throttle
     d.noise_seed = seed
+    d.plane_width = plane_width
+    d.fixed_p3 = fixed_p3
     return d
 
 

@@ -65,6 +65,8 @@ class GridDesc(C.Structure):
         ("throttle", C.c_uint64),
         ("noise_seed", C.c_uint64),
         ("boundary_value", C.c_double),
+        ("plane_width", C.c_int32),
+        ("fixed_p3", C.c_int32),
     ]
 
 

@@ -328,6 +328,20 @@ struct WordSink {
     }
 };
 
+// The p3 bytes of an encode_word at d (p3 uniform per record: unrolled).
+__device__ __forceinline__ void put_bytes(uint8_t* d, unsigned long long w, int p3) {
+    switch (p3) {
+        case 8: d[7] = static_cast<uint8_t>(w >> 56); [[fallthrough]];
+        case 7: d[6] = static_cast<uint8_t>(w >> 48); [[fallthrough]];
+        case 6: d[5] = static_cast<uint8_t>(w >> 40); [[fallthrough]];
+        case 5: d[4] = static_cast<uint8_t>(w >> 32); [[fallthrough]];
+        case 4: d[3] = static_cast<uint8_t>(w >> 24); [[fallthrough]];
+        case 3: d[2] = static_cast<uint8_t>(w >> 16); [[fallthrough]];
+        case 2: d[1] = static_cast<uint8_t>(w >> 8); d[0] = static_cast<uint8_t>(w); break;
+        default: break;
+    }
+}
+
 // codec::roundtrip (codec.hpp:28-33) without the byte detour: the same
 // encode/decode arithmetic on registers. Returns false for non-finite.
 __device__ inline bool roundtrip_fast(double x, int p3, double& out) {
@@ -514,6 +528,13 @@ struct LevelView {
     // first vertex row of a row-range launch of the 2D vertex kernels
     // (blockIdx.y + row0); 0 for whole-level launches
     int row0;
+    // compressed leaf operators for the residual (plane_width > 0): per cell
+    // 16 slots of cw bytes (row-major entries) holding encode_value(surplus,
+    // cp3) in their first cp3 bytes; cp3 > cw: use the FP64 operator
+    uint8_t* cplanes;
+    int8_t* cp3;
+    int cw;
+    int fixed_p3;  // > 0: every leaf record at this width (desc.fixed_p3)
 };
 
 __device__ inline int32_t crank(const LevelView& L, int cx, int cy) { return L.rx[cx] + L.ry[cy]; }

@@ -92,6 +92,22 @@ __device__ inline void atomic_max_double_bits(unsigned long long* a, double v) {
     atomic_max_u64(a, static_cast<unsigned long long>(__double_as_longlong(v)));
 }
 
+// The compressed copy of a published leaf record for the residual
+// (plane_width > 0): entry k's encode_value bytes in slot k of the cell.
+__device__ __forceinline__ void store_slot(uint8_t* slot, double sur, int p3) {
+    put_bytes(slot, encode_word(sur, p3), p3);
+}
+__device__ inline void store_planes16(const LevelView& F, int c, const double* sur, int p3) {
+    if (!F.cplanes) return;
+    if (p3 > F.cw) {
+        F.cp3[c] = 9;  // wider than a slot: the residual reads the FP64 operator
+        return;
+    }
+    uint8_t* base = F.cplanes + static_cast<int64_t>(c) * 16 * F.cw;
+    for (int k = 0; k < 16; ++k) store_slot(base + k * F.cw, sur[k], p3);
+    F.cp3[c] = static_cast<int8_t>(p3);
+}
+
 // CellStream::publish_element (stream.cpp:100-132); caller stores p1.
 __device__ inline bool publish_leaf(const LevelView& F, int c, const double* m, int n, double e_c,
                                     double delta_max, uint32_t cycle, unsigned long long* stats) {
@@ -100,7 +116,7 @@ __device__ inline bool publish_leaf(const LevelView& F, int c, const double* m, 
         base[k] = baseline_entry(k, e_c);
         sur[k] = m[k] - base[k];
     }
-    int p3 = choose_precision(sur, 16, delta_max);
+    int p3 = F.fixed_p3 ? F.fixed_p3 : choose_precision(sur, 16, delta_max);
     if (p3 < 0) return false;
     double delta = 0.0;
     double* op = F.op + 16 * static_cast<int64_t>(c);
@@ -111,6 +127,7 @@ __device__ inline bool publish_leaf(const LevelView& F, int c, const double* m, 
         delta = delta < err ? err : delta;
         op[k] = base[k] + rt;
     }
+    store_planes16(F, c, sur, p3);
     atomic_max_double_bits(&stats[S_MAXDELTA], delta);
     atomic_max_u64(&stats[S_MAXSAMPLES], static_cast<unsigned long long>(n));
     F.n[c] = n;
@@ -136,7 +153,7 @@ __device__ inline bool publish_leaf_k9(const LevelView& F, int c, const double* 
         base9[i] = baseline_entry(k, e_c);
         sur9[i] = m16[k] - base9[i];
     }
-    const int p3 = choose_precision_k9(sur9, delta_max);
+    const int p3 = F.fixed_p3 ? F.fixed_p3 : choose_precision_k9(sur9, delta_max);
     if (p3 < 0) return false;
     double delta = 0.0, dec9[9];
 #pragma unroll
@@ -152,6 +169,11 @@ __device__ inline bool publish_leaf_k9(const LevelView& F, int c, const double* 
     double2* op = reinterpret_cast<double2*>(F.op + 16 * static_cast<int64_t>(c));
 #pragma unroll
     for (int q = 0; q < 8; ++q) op[q] = make_double2(dec[2 * q], dec[2 * q + 1]);
+    if (F.cplanes) {
+        double sur[16];
+        k9_expand(sur9, sur);
+        store_planes16(F, c, sur, p3);
+    }
     atomic_max_double_bits(&stats[S_MAXDELTA], delta);
     atomic_max_u64(&stats[S_MAXSAMPLES], static_cast<unsigned long long>(n));
     F.n[c] = n;
@@ -820,6 +842,130 @@ __global__ void __launch_bounds__(kThreads) k_residual(LevelView F, lzb_field f)
     F.v[LZB_V_DIAG][vi] = dg;
 }
 
+// ---- residual on the compressed leaf records (plane_width = W > 0)
+// Bytes [k*W, k*W + W) of a 4W-byte slot row held as W little-endian words.
+template <int W>
+__device__ __forceinline__ unsigned long long slot_bytes(const uint32_t* w, int k) {
+    unsigned long long r = 0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        const int b = k * W + j;
+        r |= static_cast<unsigned long long>((w[b >> 2] >> (8 * (b & 3))) & 0xffu) << (8 * j);
+    }
+    return r;
+}
+
+// decode_value (codec.cpp:47-63) of the p3 bytes in w (byte j at bits 8j),
+// built from the IEEE fields: the value codec::roundtrip returns.
+__device__ __forceinline__ double decode_word(unsigned long long w, int p3) {
+    if (p3 == 0) return 0.0;
+    if (p3 == 8) return __longlong_as_double(static_cast<long long>(w));
+    const int nb = 8 * (p3 - 1), m = nb - 1;
+    const unsigned long long lo = w & ((1ull << nb) - 1);
+    const unsigned l32 = static_cast<unsigned>(lo), h32 = static_cast<unsigned>(lo >> 32);
+    const unsigned long long sw = (static_cast<unsigned long long>(__byte_perm(l32, 0, 0x0123)) << 32) |
+                                  __byte_perm(h32, 0, 0x0123);
+    const unsigned long long packed = sw >> (64 - nb);  // the big-endian sign|fraction bytes
+    const unsigned long long sign = packed >> m, frac = packed & ((1ull << m) - 1);
+    const int e_hat = static_cast<int8_t>(static_cast<uint8_t>(w >> nb));
+    if (!sign && !frac && e_hat == -128) return 0.0;
+    return __longlong_as_double(static_cast<long long>((sign << 63) |
+                                                       (static_cast<unsigned long long>(e_hat + 1023) << 52) |
+                                                       (frac << (52 - m))));
+}
+
+// k_residual reading, per adjacent cell, the vertex's row of the compressed
+// record (4 slots of W bytes) instead of the 32-B FP64 row: the entry is
+// rebuilt as baseline(ε centre) + decode(bytes), which is the stored operator
+// bit for bit (publish stores baseline + roundtrip(surplus), stream.cpp:100-111).
+template <int W>
+__global__ void __launch_bounds__(kThreads) k_residual_comp(LevelView F, lzb_field f, const double* __restrict__ cxp,
+                                                            const double* __restrict__ cyp) {
+    int ix, iy;
+    int64_t vi;
+    if (!vertex_xy(F, ix, iy, vi)) return;
+    const int N = F.N, NV = N + 1;
+    bool has[4];
+    has[0] = ix >= 1 && iy >= 1;
+    has[1] = ix < N && iy >= 1;
+    has[2] = ix >= 1 && iy < N;
+    has[3] = ix < N && iy < N;
+    uint32_t rw[4][W];
+    int32_t p1[4];
+    int cp[4];
+    double ex[4], ey[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int a = q & 1, b = q >> 1, row = (1 - a) + 2 * (1 - b);
+        const int cx = has[q] ? ix - 1 + a : 0, cy = has[q] ? iy - 1 + b : 0;
+        const int64_t c = static_cast<int64_t>(cy) * N + cx;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(F.cplanes + (c * 16 + row * 4) * W);
+#pragma unroll
+        for (int j = 0; j < W; ++j) rw[q][j] = __ldcs(src + j);
+        p1[q] = F.p1[c];
+        cp[q] = F.cp3[c];
+        ex[q] = cxp[cx];
+        ey[q] = cyp[cy];
+    }
+    double uu[3][3], uh[3][3];
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+            const int x = min(max(ix - 1 + dx, 0), N), y = min(max(iy - 1 + dy, 0), N);
+            const int64_t cv = static_cast<int64_t>(y) * NV + x;
+            uu[dy][dx] = F.v[LZB_V_U][cv];
+            uh[dy][dx] = F.v[LZB_V_UHAT][cv];
+        }
+    const double fl = F.v[LZB_V_FL][vi];
+    const bool both = has[0] && has[3];
+    const bool swap12 = both && !(crank(F, ix, iy - 1) < crank(F, ix - 1, iy));
+    double au[4], auh[4], kd[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int a = q & 1, b = q >> 1, row = (1 - a) + 2 * (1 - b);
+        const double e = field_combine(f, ex[q], ey[q]);  // ε(centre), the n = 1 sample
+        double Kr[4];
+        if (has[q] && p1[q] == LZB_P1_BOTTOM) {
+            for (int col = 0; col < 4; ++col) Kr[col] = baseline_entry(row * 4 + col, e);
+        } else if (cp[q] <= W) {
+#pragma unroll
+            for (int col = 0; col < 4; ++col)
+                Kr[col] = baseline_entry(row * 4 + col, e) + decode_word(slot_bytes<W>(rw[q], col), cp[q]);
+        } else {  // record wider than a slot: the FP64 row
+            const int cx = has[q] ? ix - 1 + a : 0, cy = has[q] ? iy - 1 + b : 0;
+            const double* src = F.op + 16 * (static_cast<int64_t>(cy) * N + cx) + 4 * row;
+            for (int col = 0; col < 4; ++col) Kr[col] = src[col];
+        }
+        double s = 0.0, sh = 0.0;
+#pragma unroll
+        for (int col = 0; col < 4; ++col) {
+            const int dy = b + cdy(col), dx = a + cdx(col);
+            s += Kr[col] * uu[dy][dx];
+            sh += Kr[col] * uh[dy][dx];
+        }
+        au[q] = s;
+        auh[q] = sh;
+        kd[q] = Kr[row];
+    }
+    const double a1 = swap12 ? au[2] : au[1], a2 = swap12 ? au[1] : au[2];
+    const double h1 = swap12 ? auh[2] : auh[1], h2 = swap12 ? auh[1] : auh[2];
+    const double d1 = swap12 ? kd[2] : kd[1], d2 = swap12 ? kd[1] : kd[2];
+    const bool e1 = swap12 ? has[2] : has[1], e2 = swap12 ? has[1] : has[2];
+    double r = fl, rh = fl, dg = 0.0;
+    if (has[0]) { r -= au[0]; rh -= auh[0]; dg += kd[0]; }
+    if (e1) { r -= a1; rh -= h1; dg += d1; }
+    if (e2) { r -= a2; rh -= h2; dg += d2; }
+    if (has[3]) { r -= au[3]; rh -= auh[3]; dg += kd[3]; }
+    if (boundary(N, ix, iy)) {
+        r = 0.0;
+        rh = 0.0;
+    }
+    F.v[LZB_V_R][vi] = r;
+    F.v[LZB_V_RHAT][vi] = rh;
+    F.v[LZB_V_DIAG][vi] = dg;
+}
+
 // Restriction fl_{l-1} += P^T rhat_l over owned lattice vertices
 // (solver.cpp:177-200), gathered per coarse vertex in (cell rank, L) order.
 // mode 0: rhs restriction of rhat into fl; mode 1: adaFAC-Jac smoothed
@@ -1159,20 +1305,6 @@ struct AllLevels {
 
 __device__ __forceinline__ int record_size(int p1, int p3, bool leaf) {  // stream.cpp:227-237
     return (p1 == LZB_P1_BOTTOM || p3 == 0) ? 1 : 1 + p3 * (leaf ? 16 : 144);
-}
-
-// The p3 bytes of an encode_word at d (p3 uniform per record: unrolled).
-__device__ __forceinline__ void put_bytes(uint8_t* d, unsigned long long w, int p3) {
-    switch (p3) {
-        case 8: d[7] = static_cast<uint8_t>(w >> 56); [[fallthrough]];
-        case 7: d[6] = static_cast<uint8_t>(w >> 48); [[fallthrough]];
-        case 6: d[5] = static_cast<uint8_t>(w >> 40); [[fallthrough]];
-        case 5: d[4] = static_cast<uint8_t>(w >> 32); [[fallthrough]];
-        case 4: d[3] = static_cast<uint8_t>(w >> 24); [[fallthrough]];
-        case 3: d[2] = static_cast<uint8_t>(w >> 16); [[fallthrough]];
-        case 2: d[1] = static_cast<uint8_t>(w >> 8); d[0] = static_cast<uint8_t>(w); break;
-        default: break;
-    }
 }
 
 // CellStream::save records of level-(D-1) patches with their 9 leaves. In
@@ -1584,6 +1716,7 @@ __global__ void k_commit(LevelView F, LevelView S, const int32_t* list, const in
         for (int q = 0; q < 8; ++q) dst[q] = src[q];
         F.n[c] = S.n[c];
         F.p3[c] = S.p3[c];
+        if (F.cp3) F.cp3[c] = 9;  // no compressed copy staged: FP64 operator
         F.epoch[c] = S.epoch[c];
         F.chg[c] = cycle + 1;  // swapped in at this cycle's start: the walk sees it
     }
@@ -1686,6 +1819,8 @@ struct Level {
     DevBuf<uint8_t> p2, has_P;
     DevBuf<int8_t> p3;
     DevBuf<uint32_t> epoch, chg, seen;
+    DevBuf<uint8_t> cplanes;  // leaf level, plane_width > 0
+    DevBuf<int8_t> cp3;
     LevelView view(int depth) const {
         LevelView L{};
         L.N = N;
@@ -1705,6 +1840,8 @@ struct Level {
         L.chg = chg.p;
         L.seen = seen.p;
         L.has_P = has_P.p;
+        L.cplanes = cplanes.p;
+        L.cp3 = cp3.p;
         return L;
     }
 };
@@ -1785,6 +1922,16 @@ public:
         hist_.alloc(kNHist);
         partial_.alloc(kNormBlocks);
         if (d.variant == LZB_ADAFAC_PI && D_ >= 1) caux_.alloc(L_[D_ - 1].nv);
+        if (d.fixed_p3 != 0 && (d.fixed_p3 < 2 || d.fixed_p3 > 8))
+            throw Error(LZB_ERR_INVALID, "fixed_p3 must be 0 or 2..8");
+        if (d.plane_width != 0) {
+            if (d.plane_width < 2 || d.plane_width > 8) throw Error(LZB_ERR_INVALID, "plane_width must be 0 or 2..8");
+            if (d.concurrent) throw Error(LZB_ERR_INVALID, "plane_width needs the deterministic modes");
+            Level& F = L_[D_];
+            F.cplanes.alloc(static_cast<size_t>(F.nc) * 16 * d.plane_width);
+            F.cp3.alloc(F.nc);
+            LZB_CUDA(cudaMemsetAsync(F.cp3.p, 9, F.cp3.bytes(), s_));  // nothing compressed yet: FP64
+        }
         res_.alloc(1);
         LZB_CUDA(cudaMemsetAsync(res_.p, 0, sizeof(Result), s_));
         if (d.throttle) keys_.alloc(leaves_);
@@ -1860,7 +2007,14 @@ public:
             if (*e) cudaGraphExecDestroy(*e);
     }
 
-    LevelView V(int l) const { return L_[l].view(D_); }
+    LevelView V(int l) const {
+        LevelView v = L_[l].view(D_);
+        if (l == D_) {
+            v.cw = d_.plane_width;
+            v.fixed_p3 = d_.fixed_p3;
+        }
+        return v;
+    }
     // 2D launch geometry of the vertex kernels: x = column blocks, y = rows
     dim3 vgrid(int l) const { return dim3(blocks_for(L_[l].N + 1, kThreads), L_[l].N + 1); }
     const lzb_grid_desc& desc() const { return d_; }
@@ -2149,11 +2303,30 @@ public:
         rhs_ready_ = true;
     }
 
+    // The leaf level's residual on rows [r0, r1): FP64 operators, or the
+    // compressed records when plane_width > 0.
+    void leaf_residual(int r0, int r1) {
+        const dim3 g = vgrid_rows(D_, r0, r1);
+        const LevelView F = Vrow(D_, r0);
+        const double *cx = centre_[1].x.p, *cy = centre_[1].y.p;
+        switch (d_.plane_width) {
+            case 0: LZB_LAUNCH(k_residual, g, kThreads, 0, s_, F, d_.field); break;
+            case 2: LZB_LAUNCH(k_residual_comp<2>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
+            case 3: LZB_LAUNCH(k_residual_comp<3>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
+            case 4: LZB_LAUNCH(k_residual_comp<4>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
+            case 5: LZB_LAUNCH(k_residual_comp<5>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
+            case 6: LZB_LAUNCH(k_residual_comp<6>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
+            case 7: LZB_LAUNCH(k_residual_comp<7>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
+            default: LZB_LAUNCH(k_residual_comp<8>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
+        }
+    }
+
     void residual_launches() {  // solver.cpp:145-210
         for (int l = D_; l >= 0; --l) {
             const dim3 g = vgrid(l);
             LZB_LAUNCH(k_uhat, g, kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
-            LZB_LAUNCH(k_residual, g, kThreads, 0, s_, V(l), d_.field);
+            if (l == D_) leaf_residual(0, L_[D_].N + 1);
+            else LZB_LAUNCH(k_residual, g, kThreads, 0, s_, V(l), d_.field);
             if (l > 0)
                 LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l),
                            V(l - 1), 0, 0.0);
@@ -2404,7 +2577,7 @@ public:
                 ensure_rhs();
                 const int u0 = std::max(v0 - 1, 0), u1 = std::min(v1 + 1, N + 1);
                 LZB_LAUNCH(k_uhat, vgrid_rows(D_, u0, u1), kThreads, 0, s_, Vrow(D_, u0), V(D_ - 1), 1);
-                LZB_LAUNCH(k_residual, vgrid_rows(D_, v0, v1), kThreads, 0, s_, Vrow(D_, v0), d_.field);
+                leaf_residual(v0, v1);
                 LZB_LAUNCH(k_reset_stats, 1, 32, 0, s_, res_.p);
                 const int cr1 = std::min(v1, N);
                 if (cr1 > v0)
@@ -2678,9 +2851,7 @@ public:
                 case LZB_TK_UHAT:
                     LZB_LAUNCH(k_uhat, vgrid(l), kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
                     break;
-                case LZB_TK_RESIDUAL:
-                    LZB_LAUNCH(k_residual, vgrid(l), kThreads, 0, s_, V(l), d_.field);
-                    break;
+                case LZB_TK_RESIDUAL: leaf_residual(0, L_[D_].N + 1); break;
                 case LZB_TK_RESTRICT:
                     LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1), 0, 0.0);
                     break;
@@ -2767,6 +2938,12 @@ public:
     void invalidate() {
         LZB_CUDA(cudaStreamSynchronize(s_));
         all_top_ = false;
+    }
+
+    void plane_arrays(void** planes, void** cp3, int* width) {
+        *planes = L_[D_].cplanes.p;
+        *cp3 = L_[D_].cp3.p;
+        *width = d_.plane_width;
     }
 
     void cell_arrays(int level, void** op, void** p1, void** n, void** p3, void** epoch, void** chg) {
@@ -2951,6 +3128,9 @@ int lzb_grid_stream_image(lzb_grid* g, uint8_t* out, int64_t cap, int64_t* size)
         }
         *size = g->g->image_into(out, cap);
     });
+}
+int lzb_grid_plane_arrays(lzb_grid* g, void** planes, void** cp3, int* width) {
+    return guarded([&] { g->g->plane_arrays(planes, cp3, width); });
 }
 int lzb_grid_set_slab(lzb_grid* g, int v0, int v1) {
     return guarded([&] { g->g->set_slab(v0, v1); });

@@ -83,10 +83,16 @@ def leaf_tensors(grid):
     N = 3 ** grid.depth
     nc = N * N
     op, p1, n, p3, ep, chg = (p.value for p in ptrs)
-    return {"op": device_tensor(op, 16 * nc, "<f8"), "p1": device_tensor(p1, nc, "<i4"),
-            "n": device_tensor(n, nc, "<i4"), "p3": device_tensor(p3, nc, "|i1"),
-            # u32 arrays travel as i32 (same bits; torch's NCCL group has no uint32)
-            "epoch": device_tensor(ep, nc, "<i4"), "chg": device_tensor(chg, nc, "<i4")}
+    out = {"op": device_tensor(op, 16 * nc, "<f8"), "p1": device_tensor(p1, nc, "<i4"),
+           "n": device_tensor(n, nc, "<i4"), "p3": device_tensor(p3, nc, "|i1"),
+           # u32 arrays travel as i32 (same bits; torch's NCCL group has no uint32)
+           "epoch": device_tensor(ep, nc, "<i4"), "chg": device_tensor(chg, nc, "<i4")}
+    planes, cp3, width = C.c_void_p(), C.c_void_p(), C.c_int()
+    lzb._check(lzb.lib().lzb_grid_plane_arrays(grid.h, C.byref(planes), C.byref(cp3), C.byref(width)))
+    if width.value:  # the compressed records the residual reads
+        out["planes"] = device_tensor(planes.value, 16 * width.value * nc, "|u1")
+        out["cp3"] = device_tensor(cp3.value, nc, "|i1")
+    return out
 
 
 def distributed_assemble(grid, n: int, group=None):
@@ -109,9 +115,14 @@ def distributed_assemble(grid, n: int, group=None):
     for key, per_cell in (("op", 16), ("p1", 1), ("n", 1), ("epoch", 1), ("chg", 1)):
         gather_rows(None, t[key], per_cell * N, N, group)
     # i8 markers travel as i32 (NCCL has int8, but keep one code path for gloo)
-    p3 = t["p3"].to(torch.int32)
-    gather_rows(None, p3, N, N, group)
-    t["p3"].copy_(p3.to(torch.int8))
+    for key in ("p3", "cp3"):
+        if key in t:
+            v = t[key].to(torch.int32)
+            gather_rows(None, v, N, N, group)
+            t[key].copy_(v.to(torch.int8))
+    if "planes" in t:
+        w = t["planes"].numel() // (N * N)
+        gather_rows(None, t["planes"], w * N, N, group)
     torch.cuda.synchronize()
     lzb._check(lzb.lib().lzb_grid_invalidate(grid.h))
     return r0, r1

@@ -255,3 +255,77 @@ def test_concurrent_rejects_non_anarchic():
     d = lzb.make_desc(depth=2, assembly="adaptive", concurrent=True)
     with pytest.raises(lzb.LzbError):
         lzb.Grid(d)
+
+
+# ------------------------------------------- residual on compressed records
+def _cycles(d, n_asm, k, eager=False):
+    g = lzb.Grid(d, 42)
+    if eager:
+        g.eager_setup()
+    else:
+        g.assemble_fixed(n_asm)
+    reps = [g.step() for _ in range(k)]
+    return g, reps
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("width", [2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("solver", ["additive", "adafac-pi"])
+def test_compressed_residual_bit_identical(width, solver):
+    """The residual decoding the leaf records' surplus bytes (plane_width)
+    rebuilds the stored operator bit for bit: same u, r and residual history
+    as the FP64 residual, including records wider than a slot (FP64 fallback)."""
+    f = lzb.field_theta(16.0)
+    base = dict(depth=4, field=f, solver=solver, omega=0.6, rhs_kind="sinprod", max_cycles=100, delta_max=1e-8)
+    a, ra = _cycles(lzb.make_desc(**base), 3, 6)
+    b, rb = _cycles(lzb.make_desc(plane_width=width, **base), 3, 6)
+    assert [r["residual"] for r in ra] == [r["residual"] for r in rb]
+    for lvl in range(5):
+        assert np.array_equal(a.vertices(lvl, lzb.T.V_U), b.vertices(lvl, lzb.T.V_U))
+    assert np.array_equal(a.vertices(4, lzb.T.V_R), b.vertices(4, lzb.T.V_R))
+
+
+@pytest.mark.gpu
+def test_compressed_residual_adaptive_and_reload(tmp_path):
+    """Records published by the adaptive protocol and by a stream load feed the
+    compressed residual as they feed the FP64 one."""
+    f = lzb.checkerboard(3, 8)
+    base = dict(depth=3, field=f, solver="adafac-pi", omega=0.6, rhs=1.0, max_cycles=100)
+    a, ra = _cycles(lzb.make_desc(assembly="eager", **base), 0, 5, eager=True)
+    b, rb = _cycles(lzb.make_desc(assembly="eager", plane_width=4, **base), 0, 5, eager=True)
+    assert [r["residual"] for r in ra] == [r["residual"] for r in rb]
+    img = a.stream_image()
+    c = lzb.Grid(lzb.make_desc(plane_width=4, **base), 42)
+    c.load_image(img)
+    d0 = lzb.Grid(lzb.make_desc(**base), 42)
+    d0.load_image(img)
+    rc, rd = [c.step() for _ in range(4)], [d0.step() for _ in range(4)]
+    assert [r["residual"] for r in rc] == [r["residual"] for r in rd]
+    assert np.array_equal(c.vertices(3, lzb.T.V_U), d0.vertices(3, lzb.T.V_U))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p3", [2, 3, 4, 5, 6, 7, 8])
+def test_fixed_width_records(p3):
+    """fixed_p3: every leaf record at one mantissa width (the width sweep of
+    BASELINE configs[4]); the stored operator is baseline + roundtrip at that
+    width, and the compressed residual at plane_width = p3 agrees with the
+    FP64 one bit for bit."""
+    f = lzb.field_sinusoid(0.9, 6.0)
+    base = dict(depth=3, field=f, solver="additive", omega=0.6, rhs_kind="sinprod", max_cycles=100,
+                fixed_p3=p3)
+    a, ra = _cycles(lzb.make_desc(**base), 2, 4)
+    b, rb = _cycles(lzb.make_desc(plane_width=p3, **base), 2, 4)
+    st = a.stats()
+    assert st.p3_histogram[p3] == 27 * 27 and st.fine_stored_bytes == 27 * 27 * (1 + 16 * p3)
+    assert [r["residual"] for r in ra] == [r["residual"] for r in rb]
+    # stored entries = baseline + roundtrip(surplus, p3) of the n = 2 integration
+    cells = a.cells(3)
+    h = (1.0 / 3) ** 3  # mesh.hpp:87 on the host, x0 = cx * h
+    xs = np.array([cx * h for cy in range(27) for cx in range(27)])
+    ys = np.array([cy * h for cy in range(27) for cx in range(27)])
+    m = lzb.integrate_elements(f, xs, ys, h, 2)
+    basev = lzb.integrate_elements(f, xs, ys, h, 1)  # A(n=1) = eps(centre) K_unit, the baseline
+    for c in (0, 13, 400, 728):
+        want = basev[c] + lzb.codec.roundtrip(m[c] - basev[c], p3)
+        assert np.array_equal(cells["ops"][c], want), c
