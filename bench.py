@@ -345,6 +345,9 @@ def run_ours(args, world, rank, local):
                 "grid": f"{3 ** HBM_LEVEL}^2 (depth {HBM_LEVEL}), p = 4 assembly", "peak_source": hbm_src}
 
     smoother["roofline"] = hbm_roof("k_residual")
+    # mantissa-width sweep (BASELINE configs[4], here on the 2D 6561^2 grid): every
+    # leaf record at one width, the residual decoding the compressed records
+    smoother["width_sweep"] = measure.width_sweep(ctx, f, HBM_LEVEL, hbm_peak, reps=5, cycles=5)
     smoother["hbm_kernels"] = {k: v for k, v in hbm_tab.items() if k != "image_bytes"}
 
     # strong-scaling slab decomposition (§8e): each rank assembles 1/world of the rows,

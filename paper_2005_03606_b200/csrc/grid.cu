@@ -93,18 +93,27 @@ __device__ inline void atomic_max_double_bits(unsigned long long* a, double v) {
 }
 
 // The compressed copy of a published leaf record for the residual
-// (plane_width > 0): entry k's encode_value bytes in slot k of the cell.
-__device__ __forceinline__ void store_slot(uint8_t* slot, double sur, int p3) {
-    put_bytes(slot, encode_word(sur, p3), p3);
+// (plane_width > 0). A slot holds the p3-byte little-endian word of the
+// roundtrip value rt = codec::roundtrip(surplus, p3) in a register-friendly
+// order (sign | e_hat+128 | top m fraction bits; raw IEEE at p3 = 8; 0 <-> +0):
+// the same information as the LZMG bytes (stream.cpp:311-337), rebuilt into
+// the double with shifts and masks only.
+__device__ __forceinline__ unsigned long long plane_word(double rt, int p3) {
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(rt));
+    if (p3 == 8) return u;
+    if (rt == 0.0) return 0;
+    const int m = 8 * (p3 - 1) - 1;
+    const unsigned long long e8 = ((u >> 52) & 0x7ff) - 895;  // e_hat + 128 in [0, 255]
+    return ((u >> 63) << (8 * p3 - 1)) | (e8 << m) | ((u & 0xFFFFFFFFFFFFFull) >> (52 - m));
 }
-__device__ inline void store_planes16(const LevelView& F, int c, const double* sur, int p3) {
+__device__ __forceinline__ void store_planes_rt(const LevelView& F, int c, const double* rt, int p3) {
     if (!F.cplanes) return;
     if (p3 > F.cw) {
         F.cp3[c] = 9;  // wider than a slot: the residual reads the FP64 operator
         return;
     }
     uint8_t* base = F.cplanes + static_cast<int64_t>(c) * 16 * F.cw;
-    for (int k = 0; k < 16; ++k) store_slot(base + k * F.cw, sur[k], p3);
+    for (int k = 0; k < 16; ++k) put_bytes(base + k * F.cw, plane_word(rt[k], p3), p3);
     F.cp3[c] = static_cast<int8_t>(p3);
 }
 
@@ -118,7 +127,7 @@ __device__ inline bool publish_leaf(const LevelView& F, int c, const double* m, 
     }
     int p3 = F.fixed_p3 ? F.fixed_p3 : choose_precision(sur, 16, delta_max);
     if (p3 < 0) return false;
-    double delta = 0.0;
+    double delta = 0.0, rts[16];
     double* op = F.op + 16 * static_cast<int64_t>(c);
     for (int k = 0; k < 16; ++k) {
         double rt;
@@ -126,8 +135,9 @@ __device__ inline bool publish_leaf(const LevelView& F, int c, const double* m, 
         double err = fabs(rt - sur[k]);
         delta = delta < err ? err : delta;
         op[k] = base[k] + rt;
+        rts[k] = rt;
     }
-    store_planes16(F, c, sur, p3);
+    store_planes_rt(F, c, rts, p3);
     atomic_max_double_bits(&stats[S_MAXDELTA], delta);
     atomic_max_u64(&stats[S_MAXSAMPLES], static_cast<unsigned long long>(n));
     F.n[c] = n;
@@ -155,7 +165,7 @@ __device__ inline bool publish_leaf_k9(const LevelView& F, int c, const double* 
     }
     const int p3 = F.fixed_p3 ? F.fixed_p3 : choose_precision_k9(sur9, delta_max);
     if (p3 < 0) return false;
-    double delta = 0.0, dec9[9];
+    double delta = 0.0, dec9[9], rt9[9];
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
         double rt;
@@ -163,6 +173,7 @@ __device__ inline bool publish_leaf_k9(const LevelView& F, int c, const double* 
         const double err = fabs(rt - sur9[i]);
         delta = delta < err ? err : delta;
         dec9[i] = base9[i] + rt;
+        rt9[i] = rt;
     }
     double dec[16];
     k9_expand(dec9, dec);
@@ -170,9 +181,9 @@ __device__ inline bool publish_leaf_k9(const LevelView& F, int c, const double* 
 #pragma unroll
     for (int q = 0; q < 8; ++q) op[q] = make_double2(dec[2 * q], dec[2 * q + 1]);
     if (F.cplanes) {
-        double sur[16];
-        k9_expand(sur9, sur);
-        store_planes16(F, c, sur, p3);
+        double rt16[16];
+        k9_expand(rt9, rt16);
+        store_planes_rt(F, c, rt16, p3);
     }
     atomic_max_double_bits(&stats[S_MAXDELTA], delta);
     atomic_max_u64(&stats[S_MAXSAMPLES], static_cast<unsigned long long>(n));
@@ -855,31 +866,32 @@ __device__ __forceinline__ unsigned long long slot_bytes(const uint32_t* w, int 
     return r;
 }
 
-// decode_value (codec.cpp:47-63) of the p3 bytes in w (byte j at bits 8j),
-// built from the IEEE fields: the value codec::roundtrip returns.
-__device__ __forceinline__ double decode_word(unsigned long long w, int p3) {
-    if (p3 == 0) return 0.0;
-    if (p3 == 8) return __longlong_as_double(static_cast<long long>(w));
-    const int nb = 8 * (p3 - 1), m = nb - 1;
-    const unsigned long long lo = w & ((1ull << nb) - 1);
-    const unsigned l32 = static_cast<unsigned>(lo), h32 = static_cast<unsigned>(lo >> 32);
-    const unsigned long long sw = (static_cast<unsigned long long>(__byte_perm(l32, 0, 0x0123)) << 32) |
-                                  __byte_perm(h32, 0, 0x0123);
-    const unsigned long long packed = sw >> (64 - nb);  // the big-endian sign|fraction bytes
-    const unsigned long long sign = packed >> m, frac = packed & ((1ull << m) - 1);
-    const int e_hat = static_cast<int8_t>(static_cast<uint8_t>(w >> nb));
-    if (!sign && !frac && e_hat == -128) return 0.0;
-    return __longlong_as_double(static_cast<long long>((sign << 63) |
-                                                       (static_cast<unsigned long long>(e_hat + 1023) << 52) |
-                                                       (frac << (52 - m))));
-}
+// The roundtrip value from a plane word (the inverse of plane_word), with
+// the per-row constants of width p3 precomputed.
+struct PlaneDec {
+    int p3, m, sh_sign;
+    unsigned long long fmask;
+    __device__ __forceinline__ explicit PlaneDec(int p) : p3(p) {
+        m = 8 * (p - 1) - 1;
+        sh_sign = 8 * p - 1;
+        fmask = (1ull << (m > 0 ? m : 0)) - 1;
+    }
+    __device__ __forceinline__ double operator()(unsigned long long w) const {
+        if (p3 == 8) return __longlong_as_double(static_cast<long long>(w));
+        if (p3 == 0 || w == 0) return 0.0;
+        const unsigned long long sign = (w >> sh_sign) & 1, e8 = (w >> m) & 0xff;
+        return __longlong_as_double(static_cast<long long>((sign << 63) | ((e8 + 895) << 52) |
+                                                           ((w & fmask) << (52 - m))));
+    }
+};
 
 // k_residual reading, per adjacent cell, the vertex's row of the compressed
 // record (4 slots of W bytes) instead of the 32-B FP64 row: the entry is
-// rebuilt as baseline(ε centre) + decode(bytes), which is the stored operator
-// bit for bit (publish stores baseline + roundtrip(surplus), stream.cpp:100-111).
+// rebuilt as baseline(ε centre) + roundtrip value, which is the stored
+// operator bit for bit (publish stores baseline + roundtrip(surplus),
+// stream.cpp:100-111).
 template <int W>
-__global__ void __launch_bounds__(kThreads) k_residual_comp(LevelView F, lzb_field f, const double* __restrict__ cxp,
+__global__ void __launch_bounds__(kThreads, 3) k_residual_comp(LevelView F, lzb_field f, const double* __restrict__ cxp,
                                                             const double* __restrict__ cyp) {
     int ix, iy;
     int64_t vi;
@@ -891,9 +903,7 @@ __global__ void __launch_bounds__(kThreads) k_residual_comp(LevelView F, lzb_fie
     has[2] = ix >= 1 && iy < N;
     has[3] = ix < N && iy < N;
     uint32_t rw[4][W];
-    int32_t p1[4];
     int cp[4];
-    double ex[4], ey[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int a = q & 1, b = q >> 1, row = (1 - a) + 2 * (1 - b);
@@ -902,11 +912,11 @@ __global__ void __launch_bounds__(kThreads) k_residual_comp(LevelView F, lzb_fie
         const uint32_t* src = reinterpret_cast<const uint32_t*>(F.cplanes + (c * 16 + row * 4) * W);
 #pragma unroll
         for (int j = 0; j < W; ++j) rw[q][j] = __ldcs(src + j);
-        p1[q] = F.p1[c];
-        cp[q] = F.cp3[c];
-        ex[q] = cxp[cx];
-        ey[q] = cyp[cy];
+        cp[q] = F.cp3[c];  // -1: bottom (baseline), 0..W: slots, > W: FP64 row
     }
+    // centre field parts of the two cell columns / rows around the vertex
+    const double ex0 = cxp[max(ix - 1, 0)], ex1 = cxp[min(ix, N - 1)];
+    const double ey0 = cyp[max(iy - 1, 0)], ey1 = cyp[min(iy, N - 1)];
     double uu[3][3], uh[3][3];
 #pragma unroll
     for (int dy = 0; dy < 3; ++dy)
@@ -924,14 +934,15 @@ __global__ void __launch_bounds__(kThreads) k_residual_comp(LevelView F, lzb_fie
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int a = q & 1, b = q >> 1, row = (1 - a) + 2 * (1 - b);
-        const double e = field_combine(f, ex[q], ey[q]);  // ε(centre), the n = 1 sample
+        const double e = field_combine(f, a ? ex1 : ex0, b ? ey1 : ey0);  // ε(centre), the n = 1 sample
         double Kr[4];
-        if (has[q] && p1[q] == LZB_P1_BOTTOM) {
+        if (cp[q] < 0) {
             for (int col = 0; col < 4; ++col) Kr[col] = baseline_entry(row * 4 + col, e);
         } else if (cp[q] <= W) {
+            const PlaneDec dec(cp[q]);
 #pragma unroll
             for (int col = 0; col < 4; ++col)
-                Kr[col] = baseline_entry(row * 4 + col, e) + decode_word(slot_bytes<W>(rw[q], col), cp[q]);
+                Kr[col] = baseline_entry(row * 4 + col, e) + dec(slot_bytes<W>(rw[q], col));
         } else {  // record wider than a slot: the FP64 row
             const int cx = has[q] ? ix - 1 + a : 0, cy = has[q] ? iy - 1 + b : 0;
             const double* src = F.op + 16 * (static_cast<int64_t>(cy) * N + cx) + 4 * row;
@@ -1548,6 +1559,7 @@ __global__ void k_unpack(LevelView L, lzb_field f, int level, int leaf, SlotTabl
     L.p2[c] = static_cast<uint8_t>(p2);
     if (cls == 0) {
         L.p1[c] = LZB_P1_BOTTOM;
+        if (L.cp3) L.cp3[c] = -1;
         L.chg[c] = cycle + 1;  // the payload disappears: parents must see it
         return;
     }
@@ -1612,6 +1624,7 @@ __global__ void k_publish_one(LevelView F, lzb_field f, int c, const double* m, 
     double e = centre_eps(f, F, c % F.N, c / F.N);
     if (!publish_leaf(F, c, m, n, e, delta_max, cycle, stats)) atomicExch(err, 1);
     F.p1[c] = p1;
+    if (F.cp3 && p1 == LZB_P1_BOTTOM) F.cp3[c] = -1;
 }
 
 __global__ void k_step_one(LevelView F, lzb_field f, int c, int schedule, int n_max, double term_c,
@@ -1930,7 +1943,7 @@ public:
             Level& F = L_[D_];
             F.cplanes.alloc(static_cast<size_t>(F.nc) * 16 * d.plane_width);
             F.cp3.alloc(F.nc);
-            LZB_CUDA(cudaMemsetAsync(F.cp3.p, 9, F.cp3.bytes(), s_));  // nothing compressed yet: FP64
+            LZB_CUDA(cudaMemsetAsync(F.cp3.p, 0xff, F.cp3.bytes(), s_));  // -1: every leaf starts bottom
         }
         res_.alloc(1);
         LZB_CUDA(cudaMemsetAsync(res_.p, 0, sizeof(Result), s_));
@@ -2317,7 +2330,9 @@ public:
             case 5: LZB_LAUNCH(k_residual_comp<5>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
             case 6: LZB_LAUNCH(k_residual_comp<6>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
             case 7: LZB_LAUNCH(k_residual_comp<7>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
-            default: LZB_LAUNCH(k_residual_comp<8>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
+            case 8:
+            // W = 8: a slot row is as wide as the FP64 row, which the residual reads
+            default: LZB_LAUNCH(k_residual, g, kThreads, 0, s_, F, d_.field); break;
         }
     }
 

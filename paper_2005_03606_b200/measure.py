@@ -49,3 +49,49 @@ def hbm_kernel_table(grid, depth: int, peak_gbs: float, reps: int = 10) -> dict:
         out[name] = {"ms": ms, "bytes": ab[tk], "GB/s": gbs, "frac": gbs / peak_gbs}
     out["image_bytes"] = img
     return out
+
+
+MANTISSA_BITS = {2: 7, 3: 15, 4: 23, 5: 31, 6: 39, 7: 47, 8: 52}
+
+
+def width_sweep(ctx, field, depth: int, peak_gbs: float, widths=(2, 3, 4, 5, 6, 7, 8), reps=10, cycles=10):
+    """BASELINE configs[4] in 2D: every leaf record at one width p3 (fixed_p3)
+    and the residual reading the compressed records (plane_width = p3), plus
+    the delta-chosen widths with FP64 operators as the reference row. Per
+    width: LZMG bytes per leaf, residual bytes per cell, k_residual time and
+    roofline fraction, cycle time and DoF-updates/s."""
+    import torch
+
+    import paper_2005_03606_b200 as lzb
+    N = 3 ** depth
+    nc, nv = N * N, (N + 1) ** 2
+    stream = torch.cuda.ExternalStream(ctx.solve_stream)
+    rows = []
+    for p3 in (0,) + tuple(widths):
+        w = p3 if p3 < 8 else 0  # width 8 reads the FP64 rows
+        d = lzb.make_desc(depth=depth, field=field, solver="adafac-pi", omega=0.6, rhs_kind="sinprod",
+                          max_cycles=10 ** 6, delta_max=1e-8, integration="fast", fixed_p3=p3, plane_width=w)
+        g = lzb.Grid(d, 1, ctx)
+        g.assemble_fixed(4)
+        for _ in range(2):
+            g.step()
+        ms = g.time_kernel(T.TK_RESIDUAL, reps)
+        cell_b = (16 * w + 1) if w else (128 + 4)
+        nbytes = nv * 48 + nc * cell_b
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(cycles):
+            g.step()
+        b.record(stream)
+        b.synchronize()
+        cyc = a.elapsed_time(b) / cycles
+        st = g.stats()
+        rows.append({"p3": p3 if p3 else "chosen", "mantissa_bits": MANTISSA_BITS.get(p3),
+                     "lzmg_bytes_per_leaf": st.fine_stored_bytes / st.fine_cells,
+                     "residual_bytes_per_cell": cell_b, "k_residual_ms": ms,
+                     "k_residual_frac": nbytes / (ms * 1e-3) / 1e9 / peak_gbs,
+                     "cycle_ms": cyc, "dof_updates_per_s": (N - 1) ** 2 / (cyc * 1e-3)})
+        g.close()
+        del g
+        torch.cuda.empty_cache()
+    return rows
