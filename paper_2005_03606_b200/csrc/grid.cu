@@ -1318,6 +1318,82 @@ __device__ __forceinline__ int record_size(int p1, int p3, bool leaf) {  // stre
     return (p1 == LZB_P1_BOTTOM || p3 == 0) ? 1 : 1 + p3 * (leaf ? 16 : 144);
 }
 
+// ---- leaf record payload at a compile-time width
+// encode_word for normal values with exponent in [-128,127] at width P3 < 8
+// (constants folded); other values take the general path.
+template <int P3>
+__device__ __forceinline__ unsigned long long encode_word_w(double x) {
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(x));
+    if (P3 == 8) return u;
+    const int e = static_cast<int>((u >> 52) & 0x7ff) - 1023;
+    if (e < -128 || e > 127) return encode_word(x, P3);  // zero, subnormal, clamped exponent
+    const unsigned long long w = (u & 0x8000000000000000ull) | ((u << 11) & 0x7FFFFFFFFFFFF800ull);
+    const unsigned lo = static_cast<unsigned>(w), hi = static_cast<unsigned>(w >> 32);
+    const unsigned long long sw = (static_cast<unsigned long long>(__byte_perm(lo, 0, 0x0123)) << 32) |
+                                  __byte_perm(hi, 0, 0x0123);
+    constexpr int nb = 8 * (P3 - 1);
+    return (sw & ((1ull << nb) - 1)) | (static_cast<unsigned long long>(static_cast<uint8_t>(e)) << nb);
+}
+
+// The 16 encoded values of a leaf record (value k at bytes [k*P3, (k+1)*P3))
+// packed into 4*P3 little-endian words, then written at byte address dst of a
+// zeroed shared-memory window: aligned words, the two boundary words merged
+// with atomicOr (they may hold a neighbour's bytes).
+template <int P3>
+__device__ __forceinline__ void put_leaf_payload(uint8_t* dst, const unsigned long long* w16) {
+    constexpr int NW = 4 * P3;
+    uint32_t out[NW];
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+        uint32_t word = 0;
+        constexpr int VB = 8 * P3;  // bits per value
+#pragma unroll
+        for (int k = (32 * j) / VB; k <= (32 * j + 31) / VB && k < 16; ++k) {
+            const int sh = VB * k - 32 * j;
+            word |= sh >= 0 ? static_cast<uint32_t>(w16[k] << sh) : static_cast<uint32_t>(w16[k] >> (-sh));
+        }
+        out[j] = word;
+    }
+    const uintptr_t a = reinterpret_cast<uintptr_t>(dst);
+    uint32_t* wp = reinterpret_cast<uint32_t*>(a & ~uintptr_t{3});
+    const int s8 = 8 * static_cast<int>(a & 3);
+    if (s8 == 0) {
+        atomicOr(wp, out[0]);
+#pragma unroll
+        for (int j = 1; j < NW - 1; ++j) wp[j] = out[j];
+        atomicOr(wp + NW - 1, out[NW - 1]);
+    } else {
+        atomicOr(wp, out[0] << s8);
+#pragma unroll
+        for (int j = 1; j < NW; ++j) wp[j] = __funnelshift_l(out[j - 1], out[j], s8);
+        atomicOr(wp + NW, out[NW - 1] >> (32 - s8));
+    }
+}
+
+// Encode the 16 surplus values of a leaf at width P3 (9 encodes when the
+// record has the k9 symmetry of the integrated operators, else 16).
+template <int P3>
+__device__ __forceinline__ void leaf_payload(uint8_t* dst, const double* x, bool sym) {
+    unsigned long long w[16];
+    if (sym) {
+        constexpr int kpos[9] = {0, 5, 10, 15, 1, 11, 2, 7, 3};
+        unsigned long long w9[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) w9[i] = encode_word_w<P3>(x[kpos[i]]);
+        // k9_expand: 0,5,10,15 diagonal; 1=4; 11=14; 2=8; 7=13; 3=12=6=9
+        w[0] = w9[0]; w[5] = w9[1]; w[10] = w9[2]; w[15] = w9[3];
+        w[1] = w[4] = w9[4];
+        w[11] = w[14] = w9[5];
+        w[2] = w[8] = w9[6];
+        w[7] = w[13] = w9[7];
+        w[3] = w[12] = w[6] = w[9] = w9[8];
+    } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) w[k] = encode_word_w<P3>(x[k]);
+    }
+    put_leaf_payload<P3>(dst, w);
+}
+
 // CellStream::save records of level-(D-1) patches with their 9 leaves. In
 // pre-order a patch and its leaves are 10 consecutive records (slot sP, then
 // sP+1+ci, ci = lx*3+ly), and sibling patches (px, 3q+j), j = 0..2, follow
@@ -1408,16 +1484,26 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_pack_patches(AllLevels A, l
         double2 v[8];  // the whole operator in flight before any use
 #pragma unroll
         for (int h = 0; h < 8; ++h) v[h] = __ldcs(src + h);
-        WordSink sink(buf + shift + rel + 1);
+        double x[16];
 #pragma unroll
         for (int h = 0; h < 8; ++h) {
-            const double x0 = v[h].x - (0.0 + c_kunit[2 * h] * e);
-            const double x1 = v[h].y - (0.0 + c_kunit[2 * h + 1] * e);
-            ok = ok && dev_isfinite(x0) && dev_isfinite(x1);
-            sink.put(encode_word_sel(x0, p3), p3);
-            sink.put(encode_word_sel(x1, p3), p3);
+            x[2 * h] = v[h].x - (0.0 + c_kunit[2 * h] * e);
+            x[2 * h + 1] = v[h].y - (0.0 + c_kunit[2 * h + 1] * e);
+            ok = ok && dev_isfinite(x[2 * h]) && dev_isfinite(x[2 * h + 1]);
         }
-        sink.flush();
+        // the integrated operators repeat 9 values (k9_expand), and so does the baseline
+        const bool sym = x[1] == x[4] && x[11] == x[14] && x[2] == x[8] && x[7] == x[13] && x[3] == x[12] &&
+                         x[3] == x[6] && x[3] == x[9];
+        uint8_t* dst = buf + shift + rel + 1;
+        switch (p3) {
+            case 2: leaf_payload<2>(dst, x, sym); break;
+            case 3: leaf_payload<3>(dst, x, sym); break;
+            case 4: leaf_payload<4>(dst, x, sym); break;
+            case 5: leaf_payload<5>(dst, x, sym); break;
+            case 6: leaf_payload<6>(dst, x, sym); break;
+            case 7: leaf_payload<7>(dst, x, sym); break;
+            default: leaf_payload<8>(dst, x, sym); break;
+        }
     }
     __syncwarp();
     // refined records with a payload: the whole warp, lane = value
