@@ -1427,8 +1427,24 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_pack_patches(AllLevels A, l
     const int px = blockIdx.x * kPackWarps + warp, py0 = blockIdx.y * per;
     if (px >= C.N) return;
     const unsigned full = 0xffffffffu;
-    const int64_t s0 = slot_at(A.st, D - 1, px, py0);
+    // pre-order slot of patch (px, py0) from its base-3 digits (no table loads
+    // in front of the offsets load)
+    int64_t s0 = D - 1;
+    {
+        int x = px, y = py0;
+        for (int k = D - 1; k >= 1; --k) {
+            const int dx = x % 3, dy = y % 3;
+            x /= 3;
+            y /= 3;
+            s0 += (dx * 3 + dy) * A.st.subtree[k];
+        }
+    }
     const int nrec = 10 * per;
+    // the patch records' Â entries (lane < 16), loaded with everything else
+    double ra[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+        if (lane < 16 && j < per) ra[j] = __ldcs(C.op + 16 * (static_cast<int64_t>(py0 + j) * C.N + px) + lane);
     // lane r < nrec: record r of the range = patch r/10, then leaf (r%10)-1
     const int pj = lane / 10, k = lane % 10;
     const bool have = lane < nrec, leaf = have && k > 0;
@@ -1520,7 +1536,9 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_pack_patches(AllLevels A, l
             // geometric transfer: Â, then P̂ = R̂ = geo - geo = +0 -> (0, 0, -128),
             // whose only non-zero byte is the exponent (raw +0 at p3 = 8)
             if (lane < 16) {
-                const double x = C.op[16 * static_cast<int64_t>(rcell) + lane] - (0.0 + s_kunit[lane] * re);
+                const int j = r / 10;  // the patch of record lane r
+                const double xa = j == 0 ? ra[0] : (j == 1 ? ra[1] : ra[2]);
+                const double x = xa - (0.0 + s_kunit[lane] * re);
                 ok = ok && dev_isfinite(x);
                 put_bytes(dst + lane * rp3, encode_word(x, rp3), rp3);
             }
