@@ -172,6 +172,32 @@ int lzb_grid_dist_report(lzb_grid* g, double norm2, const uint64_t* slots20, lzb
  * No reference counterpart: the measurement hook behind bench.py's roofline. */
 int lzb_grid_time_kernel(lzb_grid* g, int what, int reps, double* avg_ms);
 
+/* -------------------------------------------------------------------- 3D
+ * Restated 3D extension (BASELINE configs[2..4]; no reference counterpart):
+ * trilinear hexahedra, corner a = ax + 2 ay + 4 az, 8x8 element matrices,
+ * eps sampled at the n^3 sub-cell centres, K = sum eps * K_sub with K_sub
+ * the exact sub-box stiffness (per-axis seg_int, element.cpp:8-32, in 3D).
+ * Records: 64 entries, the same codec and surplus-over-A(n=1) coding. */
+/* Gaussian random field g on a periodic n^3 grid (n a power of 2): Gaussian
+ * covariance sigma2 * exp(-r^2 / (2 ell^2)), spectral synthesis from seeded
+ * (splitmix64, Box-Muller) normals, inverse FFT; out: n^3 doubles. */
+int lzb_grf_table(uint64_t seed, int n, double ell, double sigma2, double* out);
+/* Batched 3D element integration (host buffers): count cells, out count*64. */
+int lzb_integrate_elements3(lzb_ctx* ctx, const lzb_field3* f, int64_t count, const double* x0,
+                            const double* y0, const double* z0, const double* h, const int32_t* n,
+                            double* out);
+typedef struct lzb_grid3 lzb_grid3;
+/* A regular 3D grid of depth `depth` (3^depth cells per axis), leaves only:
+ * fixed-p assembly + compression (fixed_p3 = 0: choose_precision per record). */
+int lzb_grid3_create(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3,
+                     lzb_grid3** out);
+int lzb_grid3_destroy(lzb_grid3* g);
+int lzb_grid3_assemble_fixed(lzb_grid3* g, int n);
+int lzb_grid3_stats(lzb_grid3* g, lzb_compression_stats* out);
+/* Cells [first, first+count) (index (cz*N + cy)*N + cx): stored operators
+ * (count*64) and widths. */
+int lzb_grid3_cells(lzb_grid3* g, int64_t first, int64_t count, double* ops, int32_t* p3);
+
 /* -------------------------------------------------------------- experiment */
 /* run_experiment(parse_config_file(path))               experiment.hpp:75,89
  * Writes the telemetry CSV when the config names one; returns the exit code

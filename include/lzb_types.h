@@ -57,6 +57,22 @@ typedef struct lzb_field {
     double table[LZB_CHECKER_MAX_BLOCKS * LZB_CHECKER_MAX_BLOCKS]; /* T[bx*blocks+by] */
 } lzb_field;
 
+/* --------------------------------------------------------------- 3D fields
+ * BASELINE configs[2..4] are 3D; the reference has no 3D code (types.hpp:13),
+ * so these are restated extensions (SURVEY.md §8c "3D: parity unpinned by the
+ * reference"). GRF: eps = exp(g), g trilinearly interpolated from a periodic
+ * n^3 table (lzb_grf_table), index (i*n + j)*n + k for (x, y, z). EXTRUDED:
+ * eps(x, y, z) = the 2D field at (x, y) (tensor-product checks). */
+enum lzb_field3_kind { LZB_F3_CONSTANT = 0, LZB_F3_GRF = 1, LZB_F3_EXTRUDED = 2 };
+
+typedef struct lzb_field3 {
+    int32_t kind;
+    int32_t grf_n;        /* GRF table points per axis (64 for BASELINE)        */
+    double value;         /* constant                                           */
+    const double* grf;    /* host pointer to grf_n^3 values of g (copied)       */
+    lzb_field xy;         /* EXTRUDED                                           */
+} lzb_field3;
+
 /* ------------------------------------------------------------ right-hand side */
 /* The reference only has f = rhs_constant (problem.hpp:38,42) and applies the
  * lumped load only when it is non-zero (solver.cpp:106). SINPROD is the

@@ -1,0 +1,163 @@
+"""Restated 3D oracle (numpy) — TEST INFRASTRUCTURE ONLY.
+
+The reference has no 3D code (proj/include/lazymg/types.hpp:13):
+parity of the 3D extension is unpinned by the reference and
+is checked against this restatement and against internal oracles instead:
+  * the trilinear element is the 3D form of reference_subcell_stiffness
+    (proj/src/element.cpp:8-32): per axis seg_int over the sub-interval for
+    the shape-function pair, the derivative factor +-(t1 - t0), and
+    K_sub_ab = h (Dx Sy Sz + Sx Dy Sz + Sx Sy Dz); K = sum eps(centre_ijk)
+    K_sub(i,j,k) over the n^3 sub-boxes (sample order i, j, k as
+    proj/include/lazymg/element.hpp:41-45), computed here literally per sample;
+  * constant eps: the analytic Q1 cube stiffness h/12 * (4 | 0 | -1 | -1)
+    by corner distance (0, 1, 2, 3 differing coordinates);
+  * z-independent eps: K3 = h (K2 (x) Mz + M2 (x) Dz) from the 2D element;
+  * the Gaussian random field generator restated with numpy's inverse FFT.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from paper_2005_03606_b200._types import splitmix64
+
+
+def seg_int(si: int, sj: int, a: float, b: float) -> float:
+    """proj/src/element.cpp:8-15: integral of X_si * X_sj over [a, b], X_0 = 1 - t, X_1 = t."""
+    a0, a1 = (0.0, 1.0) if si else (1.0, -1.0)
+    b0, b1 = (0.0, 1.0) if sj else (1.0, -1.0)
+    Fb = a0 * b0 * b + (a0 * b1 + a1 * b0) * b * b / 2.0 + a1 * b1 * b * b * b / 3.0
+    Fa = a0 * b0 * a + (a0 * b1 + a1 * b0) * a * a / 2.0 + a1 * b1 * a * a * a / 3.0
+    return Fb - Fa
+
+
+def corner(a: int):
+    return a & 1, (a >> 1) & 1, a >> 2
+
+
+def subcell_stiffness3(i, j, k, n, h):
+    """K_sub(i,j,k) (8 x 8) of the trilinear cube of size h."""
+    inv = 1.0 / n
+    iv = [(i * inv, (i + 1) * inv), (j * inv, (j + 1) * inv), (k * inv, (k + 1) * inv)]
+    K = np.zeros((8, 8))
+    for a in range(8):
+        ca = corner(a)
+        for b in range(8):
+            cb = corner(b)
+            S = [seg_int(ca[d], cb[d], *iv[d]) for d in range(3)]
+            Dd = [(1.0 if ca[d] == cb[d] else -1.0) * (iv[d][1] - iv[d][0]) for d in range(3)]
+            K[a, b] = h * (Dd[0] * S[1] * S[2] + S[0] * Dd[1] * S[2] + S[0] * S[1] * Dd[2])
+    return K
+
+
+def unit_stiffness3(h=1.0):
+    """Analytic Q1 stiffness of the cube [0,h]^3: h/12 * (4, 0, -1, -1)."""
+    K = np.zeros((8, 8))
+    for a in range(8):
+        for b in range(8):
+            d = sum(x != y for x, y in zip(corner(a), corner(b)))
+            K[a, b] = h * (4.0, 0.0, -1.0, -1.0)[d] / 12.0
+    return K
+
+
+def eps_grf(table: np.ndarray, x: float, y: float, z: float) -> float:
+    """exp of the periodic trilinear interpolant, lerp(a, b, t) = (1 - t) a + t b."""
+    n = table.shape[0]
+    u = [x * n, y * n, z * n]
+    f = [math.floor(v) for v in u]
+    t = [u[d] - f[d] for d in range(3)]
+    i0 = [int(f[d]) % n for d in range(3)]
+    i1 = [(i0[d] + 1) % n for d in range(3)]
+
+    def lerp(a, b, s):
+        return (1.0 - s) * a + s * b
+
+    def at(a, b, c):
+        return table[(i0[0], i1[0])[a], (i0[1], i1[1])[b], (i0[2], i1[2])[c]]
+
+    c00 = lerp(at(0, 0, 0), at(0, 0, 1), t[2])
+    c01 = lerp(at(0, 1, 0), at(0, 1, 1), t[2])
+    c10 = lerp(at(1, 0, 0), at(1, 0, 1), t[2])
+    c11 = lerp(at(1, 1, 0), at(1, 1, 1), t[2])
+    return math.exp(lerp(lerp(c00, c01, t[1]), lerp(c10, c11, t[1]), t[0]))
+
+
+def element3(eps, x0, y0, z0, h, n):
+    """sum_ijk eps(x_i, y_j, z_k) K_sub(i,j,k), samples x0 + (i + 0.5) inv h."""
+    inv = 1.0 / n
+    K = np.zeros((8, 8))
+    for i in range(n):
+        for j in range(n):
+            for k in range(n):
+                e = eps(x0 + (i + 0.5) * inv * h, y0 + (j + 0.5) * inv * h, z0 + (k + 0.5) * inv * h)
+                K += e * subcell_stiffness3(i, j, k, n, h)
+    return K
+
+
+def mass2(eps2, x0, y0, h, n):
+    """2D eps-weighted mass sum_ij eps_ij Sx Sy (4 x 4, corners SW,SE,NW,NE), h-free like K2."""
+    inv = 1.0 / n
+    M = np.zeros((4, 4))
+    for i in range(n):
+        for j in range(n):
+            e = eps2(x0 + (i + 0.5) * inv * h, y0 + (j + 0.5) * inv * h)
+            for a in range(4):
+                for b in range(4):
+                    M[a, b] += e * seg_int(a & 1, b & 1, i * inv, (i + 1) * inv) * \
+                        seg_int(a >> 1, b >> 1, j * inv, (j + 1) * inv)
+    return M
+
+
+def extruded_from_2d(K2, M2, h):
+    """K3 = h (K2 (x) Mz + M2 (x) Dz) for eps independent of z (a = a2 + 4 az)."""
+    Mz = np.array([[1.0 / 3, 1.0 / 6], [1.0 / 6, 1.0 / 3]])
+    Dz = np.array([[1.0, -1.0], [-1.0, 1.0]])
+    K = np.zeros((8, 8))
+    for a in range(8):
+        for b in range(8):
+            a2, az, b2, bz = a & 3, a >> 2, b & 3, b >> 2
+            K[a, b] = h * (K2[a2, b2] * Mz[az, bz] + M2[a2, b2] * Dz[az, bz])
+    return K
+
+
+def grf_table(seed: int, n: int, ell: float, sigma2: float) -> np.ndarray:
+    """The generator of lzb_grf_table restated: S_k = exp(-(2 pi |k| ell)^2 / 2),
+    Z = sum S_k / sigma2, c_k = sqrt(S_k / Z) (xi - i eta) with (xi, eta) from
+    Box-Muller on splitmix64 uniforms in k order, g = Re(unnormalised inverse DFT)."""
+    tpi = 2.0 * math.pi
+    freq = [i if i < n // 2 else i - n for i in range(n)]
+    S = np.zeros((n, n, n))
+    Z = 0.0
+    for i in range(n):
+        for j in range(n):
+            for l in range(n):
+                k2 = float(freq[i]) ** 2 + float(freq[j]) ** 2 + float(freq[l]) ** 2
+                s = math.exp(-0.5 * tpi * tpi * ell * ell * k2)
+                S[i, j, l] = s
+                Z += s
+    Z /= sigma2
+    c = np.zeros((n, n, n), complex)
+    st = seed
+    m = (1 << 64) - 1
+
+    def uniform():
+        nonlocal st
+        st = (st + 0x9E3779B97F4A7C15) & m
+        z = st
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+        z = z ^ (z >> 31)
+        return ((z >> 11) + 0.5) * 2.0 ** -53
+
+    flat = c.reshape(-1)
+    Sf = S.reshape(-1)
+    for q in range(n ** 3):
+        u1, u2 = uniform(), uniform()
+        r = math.sqrt(-2.0 * math.log(u1))
+        a = math.sqrt(Sf[q] / Z)
+        flat[q] = complex(a * r * math.cos(tpi * u2), -a * r * math.sin(tpi * u2))
+    return np.real(np.fft.ifftn(c)) * n ** 3
+
+
+assert splitmix64  # same generator family as the 2D checkerboard (problem.cpp:43-48)

@@ -119,6 +119,13 @@ def lib():
         L.lzb_grid_device_view.argtypes = [vp, C.c_int, C.c_int, C.POINTER(vp)]
         L.lzb_grid_time_kernel.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.lzb_grid_set_slab.argtypes = [vp, C.c_int, C.c_int]
+        L.lzb_grf_table.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, vp]
+        L.lzb_integrate_elements3.argtypes = [vp, C.POINTER(T.Field3), i64, vp, vp, vp, vp, vp, vp]
+        L.lzb_grid3_create.argtypes = [vp, C.c_int, C.POINTER(T.Field3), C.c_double, C.c_int, C.POINTER(vp)]
+        L.lzb_grid3_destroy.argtypes = [vp]
+        L.lzb_grid3_assemble_fixed.argtypes = [vp, C.c_int]
+        L.lzb_grid3_stats.argtypes = [vp, C.POINTER(CompressionStats)]
+        L.lzb_grid3_cells.argtypes = [vp, i64, i64, vp, vp]
         L.lzb_grid_plane_arrays.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(C.c_int)]
         L.lzb_grid_dist_phase.argtypes = [vp, C.c_int, C.c_int]
         L.lzb_grid_dist_result.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
@@ -516,6 +523,79 @@ class Grid:
         ms = C.c_double()
         _check(lib().lzb_grid_time_kernel(self.h, what, reps, C.byref(ms)))
         return ms.value
+
+
+# ---------------------------------------------------------------------- 3D
+# Restated 3D extension (BASELINE configs[2..4]; the reference is 2D only).
+def grf_table(seed=1, n=64, ell=0.05, sigma2=1.0) -> np.ndarray:
+    """Gaussian random field g on a periodic n^3 grid (lzb_grf_table)."""
+    out = np.zeros((n, n, n))
+    _check(lib().lzb_grf_table(seed, n, ell, sigma2, _ptr(out)))
+    return out
+
+
+def field3_grf(table: np.ndarray) -> "T.Field3":
+    """eps = exp(g), g trilinear in the periodic table (kept alive by the field)."""
+    t = np.ascontiguousarray(table, dtype=np.float64)
+    f = T.Field3(kind=T.F3_GRF, grf_n=t.shape[0], value=1.0, grf=t.ctypes.data)
+    f._table = t
+    return f
+
+
+def field3_constant(value=1.0) -> "T.Field3":
+    return T.Field3(kind=T.F3_CONSTANT, grf_n=0, value=value, grf=None)
+
+
+def field3_extruded(f2: Field) -> "T.Field3":
+    return T.Field3(kind=T.F3_EXTRUDED, grf_n=0, value=1.0, grf=None, xy=f2)
+
+
+def integrate_elements3(field, x0, y0, z0, h, n, ctx: Context | None = None) -> np.ndarray:
+    """Batched 3D element integration: (count, 8, 8) trilinear stiffness matrices."""
+    ctx = ctx or default_context()
+    x0 = np.ascontiguousarray(x0, dtype=np.float64).reshape(-1)
+    cnt = x0.size
+    y0, z0, h = (np.ascontiguousarray(np.broadcast_to(v, (cnt,)), dtype=np.float64) for v in (y0, z0, h))
+    n = np.ascontiguousarray(np.broadcast_to(n, (cnt,)), dtype=np.int32)
+    out = np.zeros((cnt, 8, 8))
+    _check(lib().lzb_integrate_elements3(ctx.h, C.byref(field), cnt, _ptr(x0), _ptr(y0), _ptr(z0), _ptr(h),
+                                         _ptr(n), _ptr(out)))
+    return out
+
+
+class Grid3:
+    """Leaves of a regular 3D grid (3^depth cells per axis): fixed-p assembly
+    with the 64-entry record coding (lzb_grid3_*)."""
+
+    def __init__(self, depth, field, delta_max=1e-8, fixed_p3=0, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.depth, self.field = depth, field
+        self.N = 3 ** depth
+        h = C.c_void_p()
+        _check(lib().lzb_grid3_create(self.ctx.h, depth, C.byref(field), delta_max, fixed_p3, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            if _lib is not None:
+                _lib.lzb_grid3_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def assemble_fixed(self, n):
+        _check(lib().lzb_grid3_assemble_fixed(self.h, n))
+
+    def stats(self) -> CompressionStats:
+        s = CompressionStats()
+        _check(lib().lzb_grid3_stats(self.h, C.byref(s)))
+        return s
+
+    def cells(self, first, count):
+        ops = np.zeros((count, 8, 8))
+        p3 = np.zeros(count, np.int32)
+        _check(lib().lzb_grid3_cells(self.h, first, count, _ptr(ops), _ptr(p3)))
+        return ops, p3
 
 
 # ------------------------------------------------------------------ experiment

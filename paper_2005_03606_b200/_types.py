@@ -37,6 +37,20 @@ class Field(C.Structure):
     ]
 
 
+# 3D field kinds (lzb_types.h, restated extension)
+F3_CONSTANT, F3_GRF, F3_EXTRUDED = range(3)
+
+
+class Field3(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32),
+        ("grf_n", C.c_int32),
+        ("value", C.c_double),
+        ("grf", C.c_void_p),
+        ("xy", Field),
+    ]
+
+
 class Rhs(C.Structure):
     _fields_ = [("kind", C.c_int32), ("pad_", C.c_int32), ("value", C.c_double)]
 

@@ -1,0 +1,460 @@
+// grid3.cu — the restated 3D extension of the delayed-assembly hot path
+// (BASELINE configs[2..4]). The reference is 2D only
+// (types.hpp:13), so this follows the survey's restatement:
+// trilinear hexahedra on regular 3^l grids, eps sampled at the n^3 sub-cell
+// centres, the exact sub-box stiffness of every sample (the 3D form of
+// reference_subcell_stiffness, element.cpp:19-32), and the 2D record coding
+// (surplus over A(n=1), codec widths, stream.cpp:82-132) on 64-entry records.
+//
+// Corner a = ax + 2 ay + 4 az, phi_a = X_ax(x) Y_ay(y) Z_az(z), X_0 = 1 - t,
+// X_1 = t on the unit cell. With S_c(i) = seg_int over sub-interval i for the
+// pair class c (00, 01, 11) and the derivative products s = +-1:
+//   K_ab = h/n * ( s_x A_yz[c_y][c_z] + s_y A_xz[c_x][c_z] + s_z A_xy[c_x][c_y] )
+//   A_yz = sum_ijk eps_ijk S_y(j) S_z(k), A_xz = sum eps S_x(i) S_z(k),
+//   A_xy = sum eps S_x(i) S_y(j)
+// accumulated with partial sums over the innermost axis (4 flops per sample,
+// not 27 per entry), so the per-sample cost is the eps evaluation.
+//
+// Layout in HBM: cell operators AoS, 64 doubles = 512 B per cell, index
+// (cz*N + cy)*N + cx; markers p3 (i8), n (i32).
+#include <complex>
+#include <memory>
+#include <vector>
+
+namespace lzb {
+namespace {
+
+constexpr int kMaxN3 = 16;
+
+struct Field3 {
+    int kind, n;
+    double value;
+    const double* grf;  // device, n^3
+    lzb_field xy;
+};
+
+// eps for the 3D kinds (lzb_field3); the GRF is exp of the periodic
+// trilinear interpolant of the table, lerp(a, b, t) = (1 - t) a + t b.
+__device__ inline double eps3(const Field3& F, double x, double y, double z) {
+    if (F.kind == LZB_F3_GRF) {
+        const int n = F.n;
+        const double ux = x * n, uy = y * n, uz = z * n;
+        const double fx = floor(ux), fy = floor(uy), fz = floor(uz);
+        const double tx = ux - fx, ty = uy - fy, tz = uz - fz;
+        int i0 = static_cast<int>(fx) % n, j0 = static_cast<int>(fy) % n, k0 = static_cast<int>(fz) % n;
+        i0 += i0 < 0 ? n : 0;
+        j0 += j0 < 0 ? n : 0;
+        k0 += k0 < 0 ? n : 0;
+        const int i1 = i0 + 1 == n ? 0 : i0 + 1, j1 = j0 + 1 == n ? 0 : j0 + 1, k1 = k0 + 1 == n ? 0 : k0 + 1;
+        const double* T = F.grf;
+        auto at = [&](int i, int j, int k) { return __ldg(T + (static_cast<int64_t>(i) * n + j) * n + k); };
+        auto lerp = [](double a, double b, double t) { return (1.0 - t) * a + t * b; };
+        const double c00 = lerp(at(i0, j0, k0), at(i0, j0, k1), tz), c01 = lerp(at(i0, j1, k0), at(i0, j1, k1), tz);
+        const double c10 = lerp(at(i1, j0, k0), at(i1, j0, k1), tz), c11 = lerp(at(i1, j1, k0), at(i1, j1, k1), tz);
+        const double g = lerp(lerp(c00, c01, ty), lerp(c10, c11, ty), tx);
+        return exp(g);
+    }
+    if (F.kind == LZB_F3_EXTRUDED) return field_eval(F.xy, x, y);
+    return F.value;
+}
+
+// Per-axis seg_int classes (00, 01, 11) of the n sub-intervals.
+struct AxisTab3 {
+    double s[kMaxN3][3];
+    int n;
+};
+
+AxisTab3 axis_tab3(int n) {
+    AxisTab3 T{};
+    T.n = n;
+    const double inv = 1.0 / n;
+    for (int i = 0; i < n; ++i) {
+        const AxisSeg a = axis_seg(i, inv);
+        T.s[i][0] = a.s0;
+        T.s[i][1] = a.s1;
+        T.s[i][2] = a.s2;
+    }
+    return T;
+}
+
+struct Acc3 {
+    double yz[9], xz[9], xy[9];
+};
+
+// The 27 class sums of one cell at n samples per axis.
+__device__ inline void accumulate3(const Field3& F, double x0, double y0, double z0, double h, const AxisTab3& T,
+                                   Acc3& A) {
+    const int n = T.n;
+    const double inv = 1.0 / n;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) A.yz[q] = A.xz[q] = A.xy[q] = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double x = x0 + (i + 0.5) * inv * h;
+        double B[3] = {0.0, 0.0, 0.0}, Cc[3] = {0.0, 0.0, 0.0};
+        for (int j = 0; j < n; ++j) {
+            const double y = y0 + (j + 0.5) * inv * h;
+            double G = 0.0, Dz[3] = {0.0, 0.0, 0.0};
+            for (int k = 0; k < n; ++k) {
+                const double z = z0 + (k + 0.5) * inv * h;
+                const double e = eps3(F, x, y, z);
+                G += e;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) Dz[c] += e * T.s[k][c];
+            }
+#pragma unroll
+            for (int cy = 0; cy < 3; ++cy) {
+#pragma unroll
+                for (int cz = 0; cz < 3; ++cz) A.yz[cy * 3 + cz] += T.s[j][cy] * Dz[cz];
+                Cc[cy] += T.s[j][cy] * G;
+                B[cy] += Dz[cy];
+            }
+        }
+#pragma unroll
+        for (int cx = 0; cx < 3; ++cx)
+#pragma unroll
+            for (int c2 = 0; c2 < 3; ++c2) {
+                A.xz[cx * 3 + c2] += T.s[i][cx] * B[c2];
+                A.xy[cx * 3 + c2] += T.s[i][cx] * Cc[c2];
+            }
+    }
+}
+
+// Entry (a, b) of h/n * (s_x A_yz + s_y A_xz + s_z A_xy).
+__device__ __forceinline__ double entry3(const Acc3& A, double hn, int a, int b) {
+    const int ax = a & 1, ay = (a >> 1) & 1, az = a >> 2, bx = b & 1, by = (b >> 1) & 1, bz = b >> 2;
+    const int cx = ax == bx ? 2 * ax : 1, cy = ay == by ? 2 * ay : 1, cz = az == bz ? 2 * az : 1;
+    const double sx = ax == bx ? 1.0 : -1.0, sy = ay == by ? 1.0 : -1.0, sz = az == bz ? 1.0 : -1.0;
+    return hn * (sx * A.yz[cy * 3 + cz] + sy * A.xz[cx * 3 + cz] + sz * A.xy[cx * 3 + cy]);
+}
+
+__global__ void k_elements3(Field3 F, int64_t count, const double* x0, const double* y0, const double* z0,
+                            const double* h, const int32_t* nn, AxisTab3 T, double* out) {
+    const int64_t t = gtid();
+    if (t >= count) return;
+    if (nn[t] != T.n) return;  // batches are grouped by n on the host
+    Acc3 A;
+    accumulate3(F, x0[t], y0[t], z0[t], h[t], T, A);
+    const double hn = h[t] * (1.0 / T.n);
+    for (int a = 0; a < 8; ++a)
+        for (int b = 0; b < 8; ++b) out[64 * t + 8 * a + b] = entry3(A, hn, a, b);
+}
+
+// Fixed-p assembly of every cell of a 3D level: integrate at n, code the
+// record against the n = 1 element (stream.cpp:82-111 in 3D), store the
+// decoded operator, width and n. One thread per cell.
+__global__ void __launch_bounds__(128) k_assemble3(Field3 F, int N, double h, AxisTab3 T, AxisTab3 T1,
+                                                   double delta_max, int fixed_p3, double* __restrict__ op,
+                                                   int8_t* __restrict__ p3o, int32_t* __restrict__ no,
+                                                   unsigned long long* stats, int* err) {
+    const int64_t c = gtid();
+    const int64_t nc = static_cast<int64_t>(N) * N * N;
+    if (c >= nc) return;
+    const int cx = static_cast<int>(c % N), cy = static_cast<int>((c / N) % N), cz = static_cast<int>(c / N / N);
+    const double x0 = cx * h, y0 = cy * h, z0 = cz * h;
+    Acc3 A, B;
+    accumulate3(F, x0, y0, z0, h, T, A);
+    accumulate3(F, x0, y0, z0, h, T1, B);  // A(n=1): eps(centre) * unit stiffness
+    const double hn = h * (1.0 / T.n), h1 = h * (1.0 / 1);
+    double sur[64];
+    for (int a = 0; a < 8; ++a)
+        for (int b = 0; b < 8; ++b) sur[8 * a + b] = entry3(A, hn, a, b) - entry3(B, h1, a, b);
+    const int p3 = fixed_p3 ? fixed_p3 : choose_precision(sur, 64, delta_max);
+    if (p3 < 0) {
+        atomicExch(err, 1);
+        return;
+    }
+    double delta = 0.0;
+    double* o = op + 64 * c;
+    for (int a = 0; a < 8; ++a)
+        for (int b = 0; b < 8; ++b) {
+            const int k = 8 * a + b;
+            double rt;
+            if (!roundtrip_fast(sur[k], p3, rt)) {
+                atomicExch(err, 1);
+                return;
+            }
+            const double d = fabs(rt - sur[k]);
+            delta = delta < d ? d : delta;
+            o[k] = entry3(B, h1, a, b) + rt;
+        }
+    p3o[c] = static_cast<int8_t>(p3);
+    no[c] = T.n;
+    atomic_max_double_bits(&stats[S_MAXDELTA], delta);
+}
+
+__global__ void k_stats3(const int8_t* __restrict__ p3, int64_t nc, unsigned long long* s) {
+    __shared__ unsigned long long sh[9];
+    if (threadIdx.x < 9) sh[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned h[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t c = gtid(); c < nc; c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int q = p3[c];
+#pragma unroll
+        for (int b = 0; b <= 8; ++b) h[b] += q == b ? 1u : 0u;
+    }
+#pragma unroll
+    for (int b = 0; b <= 8; ++b) {
+        const unsigned w = __reduce_add_sync(0xffffffffu, h[b]);
+        if ((threadIdx.x & 31) == 0 && w) atomicAdd(&sh[b], static_cast<unsigned long long>(w));
+    }
+    __syncthreads();
+    if (threadIdx.x < 9 && sh[threadIdx.x]) atomicAdd(&s[S_HIST + threadIdx.x], sh[threadIdx.x]);
+}
+
+// ------------------------------------------------------------ host side
+uint64_t splitmix64_host(uint64_t& z) {
+    z += 0x9e3779b97f4a7c15ull;
+    uint64_t r = z;
+    r = (r ^ (r >> 30)) * 0xbf58476d1ce4e5b9ull;
+    r = (r ^ (r >> 27)) * 0x94d049bb133111ebull;
+    return r ^ (r >> 31);
+}
+
+// In-place radix-2 complex FFT of length n (power of 2), stride st, sign
+// +1 (inverse, unnormalised) or -1.
+void fft1(std::complex<double>* a, int n, int st, int sign) {
+    for (int i = 1, j = 0; i < n; ++i) {
+        int bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) std::swap(a[i * st], a[j * st]);
+    }
+    for (int len = 2; len <= n; len <<= 1) {
+        const double ang = sign * 2.0 * 3.14159265358979323846 / len;
+        const std::complex<double> wl(std::cos(ang), std::sin(ang));
+        for (int i = 0; i < n; i += len) {
+            std::complex<double> w(1.0, 0.0);
+            for (int k = 0; k < len / 2; ++k) {
+                const std::complex<double> u = a[(i + k) * st], v = a[(i + k + len / 2) * st] * w;
+                a[(i + k) * st] = u + v;
+                a[(i + k + len / 2) * st] = u - v;
+                w *= wl;
+            }
+        }
+    }
+}
+
+// g(x) = sum_k sqrt(S_k / Z) (xi_k cos(2 pi k.x) + eta_k sin(2 pi k.x)) on
+// x = (i, j, l) / n, k in [-n/2, n/2)^3, S_k = exp(-(2 pi |k| ell)^2 / 2)
+// (the spectrum of sigma2 exp(-r^2 / 2 ell^2)), Z = sum_k S_k / sigma2 so that
+// Var g = sigma2; xi, eta ~ N(0,1) from splitmix64 + Box-Muller in k order.
+void grf_table(uint64_t seed, int n, double ell, double sigma2, double* out) {
+    if (n < 2 || (n & (n - 1))) throw Error(LZB_ERR_INVALID, "GRF table size must be a power of 2");
+    const size_t n3 = static_cast<size_t>(n) * n * n;
+    std::vector<std::complex<double>> c(n3);
+    const double tpi = 2.0 * 3.14159265358979323846;
+    double Z = 0.0;
+    std::vector<double> S(n3);
+    auto freq = [n](int i) { return i < n / 2 ? i : i - n; };
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j)
+            for (int l = 0; l < n; ++l) {
+                const double k2 = static_cast<double>(freq(i)) * freq(i) + static_cast<double>(freq(j)) * freq(j) +
+                                  static_cast<double>(freq(l)) * freq(l);
+                const double s = std::exp(-0.5 * tpi * tpi * ell * ell * k2);
+                S[(static_cast<size_t>(i) * n + j) * n + l] = s;
+                Z += s;
+            }
+    Z /= sigma2;
+    uint64_t st = seed;
+    auto uniform = [&st]() { return (static_cast<double>(splitmix64_host(st) >> 11) + 0.5) * 0x1.0p-53; };
+    for (size_t q = 0; q < n3; ++q) {
+        // Box-Muller: one pair (xi, eta) per mode
+        const double u1 = uniform(), u2 = uniform();
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        const double xi = r * std::cos(tpi * u2), eta = r * std::sin(tpi * u2);
+        const double a = std::sqrt(S[q] / Z);
+        c[q] = std::complex<double>(a * xi, -a * eta);  // Re(c e^{i th}) = a (xi cos th + eta sin th)
+    }
+    for (int j = 0; j < n; ++j)
+        for (int l = 0; l < n; ++l) fft1(c.data() + static_cast<size_t>(j) * n + l, n, n * n, +1);
+    for (int i = 0; i < n; ++i)
+        for (int l = 0; l < n; ++l) fft1(c.data() + static_cast<size_t>(i) * n * n + l, n, n, +1);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) fft1(c.data() + (static_cast<size_t>(i) * n + j) * n, n, 1, +1);
+    for (size_t q = 0; q < n3; ++q) out[q] = c[q].real();
+}
+
+Field3 to_device(const lzb_field3& f, DevBuf<double>& table) {
+    Field3 F{};
+    F.kind = f.kind;
+    F.n = f.grf_n;
+    F.value = f.value;
+    F.xy = f.xy;
+    if (f.kind == LZB_F3_GRF) {
+        if (!f.grf || f.grf_n < 2) throw Error(LZB_ERR_INVALID, "GRF field needs a table");
+        const size_t n3 = static_cast<size_t>(f.grf_n) * f.grf_n * f.grf_n;
+        table.alloc(n3);
+        LZB_CUDA(cudaMemcpy(table.p, f.grf, n3 * sizeof(double), cudaMemcpyHostToDevice));
+        F.grf = table.p;
+    } else if (f.kind != LZB_F3_CONSTANT && f.kind != LZB_F3_EXTRUDED) {
+        throw Error(LZB_ERR_INVALID, "unknown 3D field kind");
+    }
+    return F;
+}
+
+}  // namespace
+
+class Grid3 {
+public:
+    Grid3(lzb_ctx* ctx, int depth, const lzb_field3& f, double delta_max, int fixed_p3)
+        : ctx_(ctx), D_(depth), delta_(delta_max), fixed_(fixed_p3) {
+        if (depth < 0 || depth > 6) throw Error(LZB_ERR_INVALID, "3D depth must be in 0..6");
+        if (fixed_p3 != 0 && (fixed_p3 < 2 || fixed_p3 > 8)) throw Error(LZB_ERR_INVALID, "fixed_p3 must be 0 or 2..8");
+        LZB_CUDA(cudaSetDevice(ctx->device));
+        s_ = ctx->solve;
+        N_ = 1;
+        for (int i = 0; i < depth; ++i) N_ *= 3;
+        nc_ = static_cast<int64_t>(N_) * N_ * N_;
+        h_ = std::pow(1.0 / 3, depth);
+        F_ = to_device(f, table_);
+        op_.alloc(static_cast<size_t>(nc_) * 64);
+        p3_.alloc(nc_);
+        n_.alloc(nc_);
+        stats_.alloc(20);
+        LZB_CUDA(cudaMemsetAsync(p3_.p, 0, p3_.bytes(), s_));
+        LZB_CUDA(cudaMemsetAsync(n_.p, 0, n_.bytes(), s_));
+        LZB_CUDA(cudaMemsetAsync(stats_.p, 0, stats_.bytes(), s_));
+        LZB_CUDA(cudaStreamSynchronize(s_));
+    }
+
+    void assemble_fixed(int n) {
+        if (n < 1 || n > kMaxN3) throw Error(LZB_ERR_INVALID, "3D sub-samples per axis must be in 1..16");
+        const AxisTab3 T = axis_tab3(n), T1 = axis_tab3(1);
+        LZB_LAUNCH(k_assemble3, blocks_for(nc_, 128), 128, 0, s_, F_, N_, h_, T, T1, delta_, fixed_, op_.p, p3_.p,
+                   n_.p, stats_.p, ctx_->err.p);
+        n_last_ = n;
+    }
+
+    lzb_compression_stats stats() {
+        LZB_CUDA(cudaMemsetAsync(stats_.p + S_HIST, 0, 9 * sizeof(unsigned long long), s_));
+        LZB_LAUNCH(k_stats3, 148 * 4, 256, 0, s_, p3_.p, nc_, stats_.p);
+        unsigned long long s[20];
+        LZB_CUDA(cudaMemcpyAsync(s, stats_.p, sizeof s, cudaMemcpyDeviceToHost, s_));
+        sync();
+        lzb_compression_stats st;
+        std::memset(&st, 0, sizeof st);
+        st.fine_cells = static_cast<uint64_t>(nc_);
+        double ratio = 0.0;
+        for (int p = 0; p <= 8; ++p) {
+            st.p3_histogram[p] = s[S_HIST + p];
+            st.fine_stored_bytes += s[S_HIST + p] * (p == 0 ? 1ull : 1ull + 64ull * p);
+            ratio += static_cast<double>(s[S_HIST + p]) * (512.0 / (p == 0 ? 1.0 : 1.0 + 64.0 * p));
+        }
+        st.fine_uncompressed_bytes = 512ull * nc_;
+        st.fine_factor_totals = static_cast<double>(st.fine_uncompressed_bytes) / st.fine_stored_bytes;
+        st.fine_factor_mean = ratio / nc_;
+        st.max_n = n_last_;
+        st.avg_n = n_last_;
+        double md;
+        std::memcpy(&md, &s[S_MAXDELTA], sizeof md);
+        st.max_delta = md;
+        st.total_stored_bytes = st.fine_stored_bytes;
+        st.total_uncompressed_bytes = st.fine_uncompressed_bytes;
+        st.total_factor = st.fine_factor_totals;
+        return st;
+    }
+
+    void cells(int64_t first, int64_t count, double* ops, int32_t* p3) {
+        if (first < 0 || count < 0 || first + count > nc_) throw Error(LZB_ERR_INVALID, "bad cell range");
+        if (ops)
+            LZB_CUDA(cudaMemcpyAsync(ops, op_.p + 64 * first, count * 64 * sizeof(double), cudaMemcpyDeviceToHost, s_));
+        std::vector<int8_t> q(count);
+        if (p3) LZB_CUDA(cudaMemcpyAsync(q.data(), p3_.p + first, count, cudaMemcpyDeviceToHost, s_));
+        sync();
+        if (p3)
+            for (int64_t i = 0; i < count; ++i) p3[i] = q[i];
+    }
+
+    void sync() {
+        LZB_CUDA(cudaStreamSynchronize(s_));
+        int flag = 0;
+        LZB_CUDA(cudaMemcpy(&flag, ctx_->err.p, sizeof(int), cudaMemcpyDeviceToHost));
+        if (flag) {
+            LZB_CUDA(cudaMemset(ctx_->err.p, 0, sizeof(int)));
+            throw Error(LZB_ERR_PROTOCOL, "cannot encode non-finite operator entry");
+        }
+    }
+
+private:
+    lzb_ctx* ctx_;
+    cudaStream_t s_ = nullptr;
+    int D_, N_ = 1, n_last_ = 0, fixed_;
+    int64_t nc_ = 1;
+    double h_ = 1.0, delta_;
+    Field3 F_{};
+    DevBuf<double> table_, op_;
+    DevBuf<int8_t> p3_;
+    DevBuf<int32_t> n_;
+    DevBuf<unsigned long long> stats_;
+};
+
+}  // namespace lzb
+
+struct lzb_grid3 {
+    std::unique_ptr<lzb::Grid3> g;
+};
+
+extern "C" {
+
+int lzb_grf_table(uint64_t seed, int n, double ell, double sigma2, double* out) {
+    return lzb::guarded([&] { lzb::grf_table(seed, n, ell, sigma2, out); });
+}
+
+int lzb_integrate_elements3(lzb_ctx* ctx, const lzb_field3* f, int64_t count, const double* x0, const double* y0,
+                            const double* z0, const double* h, const int32_t* n, double* out) {
+    return lzb::guarded([&] {
+        using namespace lzb;
+        if (count <= 0) return;
+        LZB_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->solve;
+        DevBuf<double> table;
+        const Field3 F = to_device(*f, table);
+        DevBuf<double> dx, dy, dz, dh, dout;
+        DevBuf<int32_t> dn;
+        for (auto* b : {&dx, &dy, &dz, &dh}) b->alloc(count);
+        dn.alloc(count);
+        dout.alloc(static_cast<size_t>(count) * 64);
+        LZB_CUDA(cudaMemcpyAsync(dx.p, x0, count * 8, cudaMemcpyHostToDevice, s));
+        LZB_CUDA(cudaMemcpyAsync(dy.p, y0, count * 8, cudaMemcpyHostToDevice, s));
+        LZB_CUDA(cudaMemcpyAsync(dz.p, z0, count * 8, cudaMemcpyHostToDevice, s));
+        LZB_CUDA(cudaMemcpyAsync(dh.p, h, count * 8, cudaMemcpyHostToDevice, s));
+        LZB_CUDA(cudaMemcpyAsync(dn.p, n, count * 4, cudaMemcpyHostToDevice, s));
+        std::vector<int> seen(kMaxN3 + 1, 0);
+        for (int64_t i = 0; i < count; ++i) {
+            if (n[i] < 1 || n[i] > kMaxN3) throw Error(LZB_ERR_INVALID, "3D sub-samples per axis must be in 1..16");
+            seen[n[i]] = 1;
+        }
+        for (int q = 1; q <= kMaxN3; ++q)
+            if (seen[q])
+                LZB_LAUNCH(k_elements3, blocks_for(count, 128), 128, 0, s, F, count, dx.p, dy.p, dz.p, dh.p, dn.p,
+                           axis_tab3(q), dout.p);
+        LZB_CUDA(cudaMemcpyAsync(out, dout.p, static_cast<size_t>(count) * 64 * 8, cudaMemcpyDeviceToHost, s));
+        LZB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int lzb_grid3_create(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3, lzb_grid3** out) {
+    return lzb::guarded([&] {
+        auto g = std::make_unique<lzb_grid3>();
+        g->g = std::make_unique<lzb::Grid3>(ctx, depth, *f, delta_max, fixed_p3);
+        *out = g.release();
+    });
+}
+int lzb_grid3_destroy(lzb_grid3* g) {
+    return lzb::guarded([&] { delete g; });
+}
+int lzb_grid3_assemble_fixed(lzb_grid3* g, int n) {
+    return lzb::guarded([&] {
+        g->g->assemble_fixed(n);
+        g->g->sync();
+    });
+}
+int lzb_grid3_stats(lzb_grid3* g, lzb_compression_stats* out) {
+    return lzb::guarded([&] { *out = g->g->stats(); });
+}
+int lzb_grid3_cells(lzb_grid3* g, int64_t first, int64_t count, double* ops, int32_t* p3) {
+    return lzb::guarded([&] { g->g->cells(first, count, ops, p3); });
+}
+
+}  // extern "C"

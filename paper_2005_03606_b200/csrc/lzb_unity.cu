@@ -3,3 +3,4 @@
 // does on x86-64; the FAST integration path uses explicit __fma_rn.
 #include "runtime.cu"
 #include "grid.cu"
+#include "grid3.cu"

@@ -1,0 +1,74 @@
+"""The 3D extension on the GPU (BASELINE configs[2..4]) against the restated
+3D oracle (oracle/port3.py) and the codec: element matrices within 1e-12,
+records bit-exact given the product's own stencils."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2005_03606_b200 as lzb
+from oracle import port as orc
+from oracle import port3 as o3
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_constant_element3(n):
+    K = lzb.integrate_elements3(lzb.field3_constant(1.5), [0.0, 1 / 3], [0.0, 2 / 3], [0.0, 0.0], 1 / 3, n)
+    for k in K:
+        assert _rel(k, 1.5 * o3.unit_stiffness3(1 / 3)) < 1e-14
+
+
+def test_grf_element3_matches_restatement():
+    g = lzb.grf_table(5, 16, 0.05, 1.0)
+    f = lzb.field3_grf(g)
+    rng = np.random.default_rng(1)
+    h = 1 / 27
+    cells = rng.integers(0, 27, size=(6, 3))
+    for n in (1, 2, 4):
+        K = lzb.integrate_elements3(f, cells[:, 0] * h, cells[:, 1] * h, cells[:, 2] * h, h, n)
+        for c, k in zip(cells, K):
+            want = o3.element3(lambda x, y, z: o3.eps_grf(g, x, y, z), c[0] * h, c[1] * h, c[2] * h, h, n)
+            assert _rel(k, want) < 1e-12, (n, c)
+
+
+def test_extruded_element3_is_the_tensor_product_of_the_2d_element():
+    f2 = lzb.field_theta(16.0)
+    x0, y0, h, n = 4 / 27, 20 / 27, 1 / 27, 3
+    K3 = lzb.integrate_elements3(lzb.field3_extruded(f2), [x0], [y0], [13 / 27], h, n)[0]
+    K2 = lzb.integrate_elements(f2, [x0], [y0], [h], [n])[0].reshape(4, 4)
+    of = orc.field_from_keys({"setup": "theta", "theta": "16"})
+    M2 = o3.mass2(lambda x, y: orc.lib().orc_field_eval(ctypes.byref(of), x, y), x0, y0, h, n)
+    assert _rel(K3, o3.extruded_from_2d(K2, M2, h)) < 1e-12
+
+
+@pytest.mark.parametrize("fixed", [0, 2, 4, 8])
+def test_grid3_records_bit_exact(fixed):
+    """Stored operator = A(n=1) + roundtrip(A(n) - A(n=1), p3), p3 chosen by the
+    (reference-pinned) codec over the 64 entries, or forced."""
+    g = lzb.grf_table(9, 16, 0.05, 1.0)
+    f = lzb.field3_grf(g)
+    G = lzb.Grid3(2, f, delta_max=1e-8, fixed_p3=fixed)
+    G.assemble_fixed(3)
+    N, h = 9, (1.0 / 3) ** 2
+    ops, p3 = G.cells(0, N ** 3)
+    idx = np.arange(N ** 3)
+    cx, cy, cz = idx % N, (idx // N) % N, idx // (N * N)
+    K = lzb.integrate_elements3(f, cx * h, cy * h, cz * h, h, 3).reshape(-1, 64)
+    B = lzb.integrate_elements3(f, cx * h, cy * h, cz * h, h, 1).reshape(-1, 64)
+    for c in range(0, N ** 3, 37):
+        sur = K[c] - B[c]
+        want_p3 = fixed if fixed else orc.choose_precision(sur, 1e-8)
+        assert p3[c] == want_p3, c
+        want = B[c] + lzb.codec.roundtrip(sur, want_p3)
+        assert np.array_equal(ops[c].reshape(-1), want), c
+    st = G.stats()
+    assert st.fine_cells == N ** 3 and sum(st.p3_histogram) == N ** 3
+    assert st.fine_stored_bytes == sum(st.p3_histogram[q] * (1 if q == 0 else 1 + 64 * q) for q in range(9))
+    if fixed:
+        assert st.p3_histogram[fixed] == N ** 3

@@ -1,0 +1,56 @@
+"""The restated 3D oracle (oracle/port3.py) against its internal pins, on CPU
+(the reference has no 3D code: SURVEY.md §8c, "3D: parity unpinned by the
+reference"), and the product's GRF generator (host code) against the numpy
+restatement."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2005_03606_b200 as lzb
+from oracle import port as orc
+from oracle import port3 as o3
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_constant_eps_is_the_analytic_q1_stiffness(n):
+    for h in (1.0, 1.0 / 9):
+        K = o3.element3(lambda x, y, z: 2.5, 0.0, 0.0, 0.0, h, n)
+        assert np.allclose(K, 2.5 * o3.unit_stiffness3(h), rtol=0, atol=1e-15)
+
+
+def test_grf_element_symmetric_zero_row_sum():
+    g = o3.grf_table(3, 8, 0.1, 1.0)
+    K = o3.element3(lambda x, y, z: o3.eps_grf(g, x, y, z), 0.2, 0.4, 0.6, 1.0 / 27, 3)
+    assert np.allclose(K, K.T, rtol=0, atol=1e-15 * np.abs(K).max())
+    assert np.abs(K.sum(axis=1)).max() < 1e-13 * np.abs(K).max()
+    assert np.all(np.diag(K) > 0)
+
+
+def test_z_independent_eps_is_the_tensor_product_of_2d():
+    """K3 = h (K2 (x) Mz + M2 (x) Dz), K2 from the reference-pinned 2D oracle."""
+    f2 = orc.field_from_keys({"setup": "theta", "theta": "16"})
+    x0, y0, h, n = 2 / 9, 5 / 9, 1 / 9, 3
+    K2 = orc.integrate_element(f2, x0, y0, h, n).reshape(4, 4)
+    def eps2(x, y):
+        return orc.lib().orc_field_eval(ctypes.byref(f2), x, y)
+
+    M2 = o3.mass2(eps2, x0, y0, h, n)
+    K3 = o3.element3(lambda x, y, z: eps2(x, y), x0, y0, 0.3, h, n)
+    assert np.allclose(K3, o3.extruded_from_2d(K2, M2, h), rtol=0, atol=1e-14 * np.abs(K3).max())
+
+
+def test_grf_table_product_matches_restatement():
+    """lzb_grf_table (host C++ radix-2 FFT) against numpy's inverse FFT."""
+    want = o3.grf_table(7, 16, 0.05, 1.0)
+    got = lzb.grf_table(7, 16, 0.05, 1.0)
+    assert np.abs(got - want).max() < 1e-12
+
+
+def test_grf_table_statistics():
+    g = lzb.grf_table(11, 64, 0.05, 1.0)
+    assert abs(g.mean()) < 0.2 and 0.6 < g.var() < 1.4
+    # the covariance falls with the lag like exp(-r^2 / 2 ell^2): at r = ell about 0.6
+    lag = int(round(0.05 * 64))
+    c = np.mean(g * np.roll(g, lag, axis=0)) / g.var()
+    assert 0.35 < c < 0.85
