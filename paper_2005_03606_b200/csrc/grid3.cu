@@ -81,9 +81,98 @@ struct Acc3 {
     double yz[9], xz[9], xy[9];
 };
 
+// The GRF eps of a cell's samples, separably: a cell is smaller than a
+// table spacing (h n_g < 1), so its samples touch the table points b, b+1,
+// b+2 per axis. Per sample row i the 3x3 (y, z) points are interpolated in
+// x, per (i, j) the 3 z points in y, per sample the z lerp and the exp: 18
+// table loads per row instead of 8 per sample. The trilinear interpolant is
+// the same function as eps3's (the lerps run in x, y, z order instead of z, y, x).
+struct GrfCell {
+    const double* T;
+    int n, bx, by, bz;  // lower table point per axis
+    double X[3][3];     // at the current x: (y point, z point)
+    double Y[3];        // at the current (x, y): z point
+
+    __device__ GrfCell(const Field3& F, double x0, double y0, double z0) : T(F.grf), n(F.n) {
+        bx = static_cast<int>(floor(x0 * n));
+        by = static_cast<int>(floor(y0 * n));
+        bz = static_cast<int>(floor(z0 * n));
+    }
+    __device__ __forceinline__ int wrap(int i) const { return i >= n ? i - n : i; }
+    __device__ __forceinline__ static double lerp(double a, double b, double t) { return (1.0 - t) * a + t * b; }
+    __device__ __forceinline__ void set_x(double x) {
+        const double u = x * n, f = floor(u);
+        const int o = static_cast<int>(f) - bx;  // 0 or 1
+        const double t = u - f;
+        const int i0 = wrap(bx + o), i1 = wrap(bx + o + 1);
+#pragma unroll
+        for (int jy = 0; jy < 3; ++jy)
+#pragma unroll
+            for (int kz = 0; kz < 3; ++kz) {
+                const int64_t jk = static_cast<int64_t>(wrap(by + jy)) * n + wrap(bz + kz);
+                X[jy][kz] = lerp(__ldg(T + static_cast<int64_t>(i0) * n * n + jk),
+                                 __ldg(T + static_cast<int64_t>(i1) * n * n + jk), t);
+            }
+    }
+    __device__ __forceinline__ void set_y(double y) {
+        const double u = y * n, f = floor(u);
+        const bool o = static_cast<int>(f) != by;
+        const double t = u - f;
+#pragma unroll
+        for (int kz = 0; kz < 3; ++kz) Y[kz] = lerp(o ? X[1][kz] : X[0][kz], o ? X[2][kz] : X[1][kz], t);
+    }
+    __device__ __forceinline__ double eps(double z) const {
+        const double u = z * n, f = floor(u);
+        const bool o = static_cast<int>(f) != bz;
+        const double t = u - f;
+        return exp(lerp(o ? Y[1] : Y[0], o ? Y[2] : Y[1], t));
+    }
+};
+
+__device__ inline void accumulate3_grf(const Field3& F, double x0, double y0, double z0, double h,
+                                       const AxisTab3& T, Acc3& A) {
+    const int n = T.n;
+    const double inv = 1.0 / n;
+    GrfCell G3(F, x0, y0, z0);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) A.yz[q] = A.xz[q] = A.xy[q] = 0.0;
+    for (int i = 0; i < n; ++i) {
+        G3.set_x(x0 + (i + 0.5) * inv * h);
+        double B[3] = {0.0, 0.0, 0.0}, Cc[3] = {0.0, 0.0, 0.0};
+        for (int j = 0; j < n; ++j) {
+            G3.set_y(y0 + (j + 0.5) * inv * h);
+            double G = 0.0, Dz[3] = {0.0, 0.0, 0.0};
+            for (int k = 0; k < n; ++k) {
+                const double e = G3.eps(z0 + (k + 0.5) * inv * h);
+                G += e;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) Dz[c] += e * T.s[k][c];
+            }
+#pragma unroll
+            for (int cy = 0; cy < 3; ++cy) {
+#pragma unroll
+                for (int cz = 0; cz < 3; ++cz) A.yz[cy * 3 + cz] += T.s[j][cy] * Dz[cz];
+                Cc[cy] += T.s[j][cy] * G;
+                B[cy] += Dz[cy];
+            }
+        }
+#pragma unroll
+        for (int cx = 0; cx < 3; ++cx)
+#pragma unroll
+            for (int c2 = 0; c2 < 3; ++c2) {
+                A.xz[cx * 3 + c2] += T.s[i][cx] * B[c2];
+                A.xy[cx * 3 + c2] += T.s[i][cx] * Cc[c2];
+            }
+    }
+}
+
 // The 27 class sums of one cell at n samples per axis.
 __device__ inline void accumulate3(const Field3& F, double x0, double y0, double z0, double h, const AxisTab3& T,
                                    Acc3& A) {
+    if (F.kind == LZB_F3_GRF && h * F.n < 1.0) {
+        accumulate3_grf(F, x0, y0, z0, h, T, A);
+        return;
+    }
     const int n = T.n;
     const double inv = 1.0 / n;
 #pragma unroll
@@ -139,9 +228,26 @@ __global__ void k_elements3(Field3 F, int64_t count, const double* x0, const dou
         for (int b = 0; b < 8; ++b) out[64 * t + 8 * a + b] = entry3(A, hn, a, b);
 }
 
+// The 64 entries of a trilinear element take 27 values: entry (a, b)
+// depends only on the per-axis pair classes (c = 0: both 0, 1: different,
+// 2: both 1), the sign of each term being fixed by its class.
+__device__ __forceinline__ double class_value(const Acc3& A, double hn, int cx, int cy, int cz) {
+    const double sx = cx == 1 ? -1.0 : 1.0, sy = cy == 1 ? -1.0 : 1.0, sz = cz == 1 ? -1.0 : 1.0;
+    return hn * (sx * A.yz[cy * 3 + cz] + sy * A.xz[cx * 3 + cz] + sz * A.xy[cx * 3 + cy]);
+}
+
+// choose_precision over a record's distinct values (duplicates never change
+// it), all indices compile-time so the values stay in registers; the same
+// algorithm as the device choose_precision (codec.cpp:64-85 semantics).
+template <int COUNT>
+__device__ __noinline__ int choose_precision_set(const double* v, double delta) {
+    return choose_precision(v, COUNT, delta);
+}
+
 // Fixed-p assembly of every cell of a 3D level: integrate at n, code the
 // record against the n = 1 element (stream.cpp:82-111 in 3D), store the
-// decoded operator, width and n. One thread per cell.
+// decoded operator, width and n. One thread per cell; the record's 27
+// distinct surplus values are coded once and written to their 64 positions.
 __global__ void __launch_bounds__(128) k_assemble3(Field3 F, int N, double h, AxisTab3 T, AxisTab3 T1,
                                                    double delta_max, int fixed_p3, double* __restrict__ op,
                                                    int8_t* __restrict__ p3o, int32_t* __restrict__ no,
@@ -151,32 +257,48 @@ __global__ void __launch_bounds__(128) k_assemble3(Field3 F, int N, double h, Ax
     if (c >= nc) return;
     const int cx = static_cast<int>(c % N), cy = static_cast<int>((c / N) % N), cz = static_cast<int>(c / N / N);
     const double x0 = cx * h, y0 = cy * h, z0 = cz * h;
-    Acc3 A, B;
-    accumulate3(F, x0, y0, z0, h, T, A);
-    accumulate3(F, x0, y0, z0, h, T1, B);  // A(n=1): eps(centre) * unit stiffness
-    const double hn = h * (1.0 / T.n), h1 = h * (1.0 / 1);
-    double sur[64];
-    for (int a = 0; a < 8; ++a)
-        for (int b = 0; b < 8; ++b) sur[8 * a + b] = entry3(A, hn, a, b) - entry3(B, h1, a, b);
-    const int p3 = fixed_p3 ? fixed_p3 : choose_precision(sur, 64, delta_max);
+    double base[27], sur[27];
+    {
+        Acc3 B;
+        accumulate3(F, x0, y0, z0, h, T1, B);  // A(n=1): eps(centre) * unit stiffness
+        const double h1 = h * (1.0 / 1);
+#pragma unroll
+        for (int q = 0; q < 27; ++q) base[q] = class_value(B, h1, q / 9, (q / 3) % 3, q % 3);
+    }
+    {
+        Acc3 A;
+        accumulate3(F, x0, y0, z0, h, T, A);
+        const double hn = h * (1.0 / T.n);
+#pragma unroll
+        for (int q = 0; q < 27; ++q) sur[q] = class_value(A, hn, q / 9, (q / 3) % 3, q % 3) - base[q];
+    }
+    const int p3 = fixed_p3 ? fixed_p3 : choose_precision_set<27>(sur, delta_max);
     if (p3 < 0) {
         atomicExch(err, 1);
         return;
     }
-    double delta = 0.0;
-    double* o = op + 64 * c;
-    for (int a = 0; a < 8; ++a)
-        for (int b = 0; b < 8; ++b) {
-            const int k = 8 * a + b;
-            double rt;
-            if (!roundtrip_fast(sur[k], p3, rt)) {
-                atomicExch(err, 1);
-                return;
-            }
-            const double d = fabs(rt - sur[k]);
-            delta = delta < d ? d : delta;
-            o[k] = entry3(B, h1, a, b) + rt;
+    double delta = 0.0, dec[27];
+#pragma unroll
+    for (int q = 0; q < 27; ++q) {
+        double rt;
+        if (!roundtrip_fast(sur[q], p3, rt)) {
+            atomicExch(err, 1);
+            return;
         }
+        const double d = fabs(rt - sur[q]);
+        delta = delta < d ? d : delta;
+        dec[q] = base[q] + rt;
+    }
+    double2* o = reinterpret_cast<double2*>(op + 64 * c);
+#pragma unroll
+    for (int k = 0; k < 64; k += 2) {
+        const int a = k >> 3, b0 = k & 7, b1 = b0 + 1;
+        auto cls = [](int a, int b) {
+            const int ax = a & 1, ay = (a >> 1) & 1, az = a >> 2, bx = b & 1, by = (b >> 1) & 1, bz = b >> 2;
+            return 9 * (ax == bx ? 2 * ax : 1) + 3 * (ay == by ? 2 * ay : 1) + (az == bz ? 2 * az : 1);
+        };
+        o[k >> 1] = make_double2(dec[cls(a, b0)], dec[cls(a, b1)]);
+    }
     p3o[c] = static_cast<int8_t>(p3);
     no[c] = T.n;
     atomic_max_double_bits(&stats[S_MAXDELTA], delta);
