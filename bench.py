@@ -39,6 +39,10 @@ CELLS = N_AXIS * N_AXIS
 P = 32
 SAMPLES_PER_STEP = CELLS * P * P
 HBM_LEVEL = 8  # smoother / stream-pack roofline grid (6561^2, beyond L2)
+# C3 (3D) executed FP64 flops per sub-sample of the separable class sums
+# (grid3.cu): z lerp 4 + exp 20 (survey convention) + coordinates 2 + the
+# class partial sums 7 (G += e, Dz[3] += e * S)
+C3_FLOPS_PER_SAMPLE = 33
 # algorithmic FP64 flops per sub-sample of the tabulated integration:
 #   EXACT: 6 mul (K_sub from axis parts) + 9 add (K values) + 9 mul + 9 add (accumulate)
 #          + 2 (eps combine: 1 + (0.9 sin x) sin y)                                   = 35
@@ -350,6 +354,26 @@ def run_ours(args, world, rank, local):
     smoother["width_sweep"] = measure.width_sweep(ctx, f, HBM_LEVEL, hbm_peak, reps=5, cycles=5)
     smoother["hbm_kernels"] = {k: v for k, v in hbm_tab.items() if k != "image_bytes"}
 
+    # BASELINE configs[2] (C3): 243^3 cells, eps = exp(GRF 64^3, ell 0.05, var 1),
+    # fixed-p assembly (integrate + 64-entry record coding + store) at p = 1 and 8
+    g3 = lzb.Grid3(5, lzb.field3_grf(lzb.grf_table(1, 64, 0.05, 1.0)), delta_max=1e-8, ctx=ctx)
+    c3 = {"grid": "243^3 (depth 5), 14,348,907 cells", "eps": "exp(GRF), 64^3 periodic table, ell 0.05, sigma^2 1",
+          "flops_per_sample_survey": 172, "flops_per_sample_executed": C3_FLOPS_PER_SAMPLE}
+    for p3d in (1, 8):
+        g3.assemble_fixed(p3d)
+        k3 = max(3, args.steps // 2)
+        t3 = timed_steps(lambda: g3.assemble_fixed(p3d), k3) / k3
+        ns = 3 ** 15 * p3d ** 3
+        st3 = g3.stats()
+        c3[f"p{p3d}"] = {"ms": 1e3 * t3, "sub_samples_per_s": ns / t3,
+                         "fp64_tflops_executed": ns * C3_FLOPS_PER_SAMPLE / t3 / 1e12,
+                         "frac_executed": ns * C3_FLOPS_PER_SAMPLE / t3 / 1e12 / fp64_peak,
+                         "lzmg_bytes_per_cell": st3.fine_stored_bytes / st3.fine_cells,
+                         "store_GBs": 512 * 3 ** 15 / t3 / 1e9}
+    g3.close()
+    del g3
+    torch.cuda.empty_cache()
+
     # strong-scaling slab decomposition (§8e): each rank assembles 1/world of the rows,
     # then one all-gather of the leaf state (NCCL) makes the operator replicated
     strong = None
@@ -457,6 +481,7 @@ def run_ours(args, world, rank, local):
                        "ms_per_step": 1e3 * results["exact"]["t"] / args.steps, "roofline": roof("exact")},
         "smoother": smoother,
         "time_to_solution": tts,
+        "c3_assembly_3d": c3,
         "strong_slabs": strong,
         "compression": {"p3_histogram": r["p3_hist"], "fine_factor_totals": r["factor"],
                         "roofline": hbm_roof("k_pack_patches"), "image_bytes_depth8": hbm_tab["image_bytes"]},
