@@ -197,6 +197,14 @@ int lzb_grid3_stats(lzb_grid3* g, lzb_compression_stats* out);
 /* Cells [first, first+count) (index (cz*N + cy)*N + cx): stored operators
  * (count*64) and widths. */
 int lzb_grid3_cells(lzb_grid3* g, int64_t first, int64_t count, double* ops, int32_t* p3);
+/* The additive multilevel cycle on the 3D grid (solver.cpp:99-347 restated):
+ * levels 0..depth, Galerkin coarse operators from the assembled leaves,
+ * trilinear geometric transfer, variant additive or adafac-pi, load
+ * f = rhs_scale * prod sin(pi x_d) lumped with h^3/8, u0 = seeded noise. */
+int lzb_grid3_init_cycle(lzb_grid3* g, int variant, double omega, double rhs_scale, uint64_t noise_seed,
+                         int max_cycles, double target);
+int lzb_grid3_step(lzb_grid3* g, lzb_cycle_report* out);
+int lzb_grid3_vertices(lzb_grid3* g, int level, int field, double* out);  /* (N+1)^3 doubles */
 
 /* -------------------------------------------------------------- experiment */
 /* run_experiment(parse_config_file(path))               experiment.hpp:75,89

@@ -161,3 +161,191 @@ def grf_table(seed: int, n: int, ell: float, sigma2: float) -> np.ndarray:
 
 
 assert splitmix64  # same generator family as the 2D checkerboard (problem.cpp:43-48)
+
+
+# ------------------------------------------------------------------ 3D cycle
+def _mix(z):
+    m = (1 << 64) - 1
+    z = (z + 0x9E3779B97F4A7C15) & m
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    return z ^ (z >> 31)
+
+
+def pw3(L, a):
+    """Trilinear lattice weight w(L, a) = prod_d (a_d ? L_d : 3 - L_d) / 27."""
+    lx, ly, lz = L
+    return float(((lx if a & 1 else 3 - lx) * (ly if (a >> 1) & 1 else 3 - ly) * (lz if a >> 2 else 3 - lz))) / 27.0
+
+
+class Cycle3:
+    """The additive multilevel cycle of proj/src/solver.cpp:99-347 restated in 3D
+    (numpy, arrays indexed [z, y, x]): Galerkin coarse operators, trilinear
+    transfer with the lowest-coordinate owner patch, hierarchical residual,
+    restriction of r-hat, Jacobi, prolongation cascade, injection."""
+
+    def __init__(self, leaf_ops, depth, variant="adafac-pi", omega=0.6, rhs_scale=3 * math.pi ** 2, seed=42,
+                 target=1e-10, max_cycles=100):
+        self.D, self.omega, self.variant, self.target, self.max_cycles = depth, omega, variant, target, max_cycles
+        self.N = [3 ** l for l in range(depth + 1)]
+        N = self.N[depth]
+        self.ops = [None] * (depth + 1)
+        self.ops[depth] = np.asarray(leaf_ops, dtype=np.float64).reshape(N, N, N, 8, 8)  # [z, y, x]
+        for l in range(depth - 1, -1, -1):
+            self.ops[l] = self._galerkin(self.ops[l + 1])
+        self.v = []
+        for l in range(depth + 1):
+            n = self.N[l] + 1
+            f = {k: np.zeros((n, n, n)) for k in ("u", "fl", "r", "rh", "uh", "dg", "aux", "us")}
+            self.v.append(f)
+        for l in range(depth + 1):
+            n = self.N[l]
+            u = self.v[l]["u"]
+            for iz in range(n + 1):
+                for iy in range(n + 1):
+                    for ix in range(n + 1):
+                        if min(ix, iy, iz) == 0 or max(ix, iy, iz) == n:
+                            u[iz, iy, ix] = 0.0
+                        else:
+                            k = _mix(seed ^ _mix((l << 48) ^ (ix << 32) ^ (iy << 16) ^ iz))
+                            u[iz, iy, ix] = (4.0 / 3.0) * float(k >> 11) * 2.0 ** -53
+        self._inject()
+        # lumped load on the leaves: f(v) h^3 / 8 per adjacent leaf
+        n = N
+        h = (1.0 / 3) ** depth
+        fl = self.v[depth]["fl"]
+        w = h * h * h / 8.0
+        for iz in range(n + 1):
+            for iy in range(n + 1):
+                for ix in range(n + 1):
+                    adj = sum(1 for dz in (0, 1) for dy in (0, 1) for dx in (0, 1)
+                              if 0 <= ix - dx < n and 0 <= iy - dy < n and 0 <= iz - dz < n)
+                    term = w * (rhs_scale * math.sin(math.pi * (ix * h)) * math.sin(math.pi * (iy * h))
+                                * math.sin(math.pi * (iz * h)))
+                    acc = 0.0
+                    for _ in range(adj):
+                        acc += term
+                    fl[iz, iy, ix] = acc
+        self.history = []
+        self.cycle = 0
+
+    @staticmethod
+    def _galerkin(fine):
+        Nf = fine.shape[0]
+        Nc = Nf // 3
+        out = np.zeros((Nc, Nc, Nc, 8, 8))
+        for lz in range(3):
+            for ly in range(3):
+                for lx in range(3):
+                    Q = np.array([[pw3((lx + (i & 1), ly + ((i >> 1) & 1), lz + (i >> 2)), a) for a in range(8)]
+                                  for i in range(8)])
+                    K = fine[lz::3, ly::3, lx::3]
+                    out += np.einsum("ia,zyxij,jb->zyxab", Q, K, Q)
+        return out
+
+    def _corner_view(self, arr, n, a):
+        """arr[z + az, y + ay, x + ax] over the n^3 cells."""
+        ax, ay, az = a & 1, (a >> 1) & 1, a >> 2
+        return arr[az:az + n, ay:ay + n, ax:ax + n]
+
+    def _owner(self, l):
+        """Per fine vertex of level l: owner patch coordinate and lattice index per axis."""
+        n, nc = self.N[l], self.N[l - 1]
+        f = np.arange(n + 1)
+        x1 = f // 3
+        p = np.where((f - 3 * x1 == 0) & (x1 > 0), x1 - 1, x1)
+        p = np.minimum(p, nc - 1)
+        return p, f - 3 * p
+
+    def _interp(self, l, coarse):
+        """P coarse at every vertex of level l."""
+        p, L = self._owner(l)
+        out = 0.0
+        for a in range(8):
+            ax, ay, az = a & 1, (a >> 1) & 1, a >> 2
+            w = (np.where(ax, L, 3 - L)[None, None, :] * np.where(ay, L, 3 - L)[None, :, None]
+                 * np.where(az, L, 3 - L)[:, None, None]) / 27.0
+            cv = coarse[(p + az)[:, None, None], (p + ay)[None, :, None], (p + ax)[None, None, :]]
+            out = out + w * cv
+        return out
+
+    def _restrict(self, l, rh):
+        """fl_{l-1} = P^T r-hat over the owned lattice (each fine vertex through its owner patch)."""
+        p, L = self._owner(l)
+        nc = self.N[l - 1]
+        out = np.zeros((nc + 1,) * 3)
+        for a in range(8):
+            ax, ay, az = a & 1, (a >> 1) & 1, a >> 2
+            w = (np.where(ax, L, 3 - L)[None, None, :] * np.where(ay, L, 3 - L)[None, :, None]
+                 * np.where(az, L, 3 - L)[:, None, None]) / 27.0
+            np.add.at(out, ((p + az)[:, None, None], (p + ay)[None, :, None], (p + ax)[None, None, :]), w * rh)
+        return out
+
+    def _interior(self, n):
+        m = np.zeros((n + 1,) * 3, bool)
+        m[1:n, 1:n, 1:n] = True
+        return m
+
+    def _residual(self, l):
+        n = self.N[l]
+        K = self.ops[l]
+        V = self.v[l]
+        Au = np.zeros_like(V["u"])
+        Auh = np.zeros_like(V["u"])
+        dg = np.zeros_like(V["u"])
+        for row in range(8):
+            for col in range(8):
+                uc = self._corner_view(V["u"], n, col)
+                uhc = self._corner_view(V["uh"], n, col)
+                tgt = self._corner_view(Au, n, row)
+                tgt += K[..., row, col] * uc
+                self._corner_view(Auh, n, row)[...] += K[..., row, col] * uhc
+            self._corner_view(dg, n, row)[...] += K[..., row, row]
+        inner = self._interior(n)
+        V["r"] = np.where(inner, V["fl"] - Au, 0.0)
+        V["rh"] = np.where(inner, V["fl"] - Auh, 0.0)
+        V["dg"] = dg
+
+    def _inject(self):
+        for l in range(self.D, 0, -1):
+            self.v[l - 1]["u"] = self.v[l]["u"][::3, ::3, ::3].copy()
+
+    def step(self):
+        self.cycle += 1
+        for l in range(self.D, -1, -1):
+            V = self.v[l]
+            V["uh"] = V["u"] - self._interp(l, self.v[l - 1]["u"]) if l > 0 else V["u"].copy()
+            self._residual(l)
+            if l > 0:
+                self.v[l - 1]["fl"] = self._restrict(l, V["rh"])
+        n = self.N[self.D]
+        res = math.sqrt(float(np.sum(self.v[self.D]["r"][1:n, 1:n, 1:n] ** 2)))
+        if not self.history:
+            self.first = res if res > 0 else 1.0
+        self.history.append(res)
+        norm = res / self.first
+        status = 1 if norm <= self.target else (2 if norm >= 1e2 else (3 if self.cycle >= self.max_cycles else 0))
+        if status in (0, 3):
+            for l in range(self.D):
+                self.v[l]["us"] = self.v[l]["u"].copy()
+                self.v[l]["aux"] = np.zeros_like(self.v[l]["u"])
+            for l in range(self.D, -1, -1):
+                V = self.v[l]
+                inner = self._interior(self.N[l])
+                if self.variant == "adafac-pi" and l > 0:
+                    Cv = self.v[l - 1]
+                    Cv["aux"] = V["r"][::3, ::3, ::3].copy()
+                    cin = self._interior(self.N[l - 1])
+                    with np.errstate(divide="ignore", invalid="ignore"):
+                        caux = np.where(cin & (Cv["dg"] != 0), self.omega / Cv["dg"] * Cv["aux"], 0.0)
+                    V["u"] = np.where(inner, V["u"] - self._interp(l, caux), V["u"])
+                damping = self.omega ** (self.D - l + 1) if self.variant == "additive" else self.omega
+                with np.errstate(divide="ignore", invalid="ignore"):
+                    upd = np.where(V["dg"] != 0, damping / V["dg"] * V["r"], 0.0)
+                V["u"] = np.where(inner, V["u"] + upd, V["u"])
+            for l in range(1, self.D + 1):
+                V, Cv = self.v[l], self.v[l - 1]
+                inner = self._interior(self.N[l])
+                V["u"] = np.where(inner, V["u"] + self._interp(l, Cv["u"] - Cv["us"]), V["u"])
+            self._inject()
+        return {"cycle": self.cycle, "residual": res, "normalized": norm, "status": status}

@@ -126,6 +126,9 @@ def lib():
         L.lzb_grid3_assemble_fixed.argtypes = [vp, C.c_int]
         L.lzb_grid3_stats.argtypes = [vp, C.POINTER(CompressionStats)]
         L.lzb_grid3_cells.argtypes = [vp, i64, i64, vp, vp]
+        L.lzb_grid3_init_cycle.argtypes = [vp, C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_int, C.c_double]
+        L.lzb_grid3_step.argtypes = [vp, C.POINTER(CycleReport)]
+        L.lzb_grid3_vertices.argtypes = [vp, C.c_int, C.c_int, vp]
         L.lzb_grid_plane_arrays.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(C.c_int)]
         L.lzb_grid_dist_phase.argtypes = [vp, C.c_int, C.c_int]
         L.lzb_grid_dist_result.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
@@ -590,6 +593,22 @@ class Grid3:
         s = CompressionStats()
         _check(lib().lzb_grid3_stats(self.h, C.byref(s)))
         return s
+
+    def init_cycle(self, solver="adafac-pi", omega=0.6, rhs_scale=3 * np.pi ** 2, seed=42, max_cycles=100,
+                   target=1e-10):
+        variant = {"additive": T.ADDITIVE, "adafac-jac": T.ADAFAC_JAC, "adafac-pi": T.ADAFAC_PI}[solver]
+        _check(lib().lzb_grid3_init_cycle(self.h, variant, omega, rhs_scale, seed, max_cycles, target))
+
+    def step(self) -> dict:
+        r = CycleReport()
+        _check(lib().lzb_grid3_step(self.h, C.byref(r)))
+        return report_dict(r)
+
+    def vertices(self, level, field):
+        n = 3 ** level + 1
+        out = np.zeros((n, n, n))  # [z][y][x]
+        _check(lib().lzb_grid3_vertices(self.h, level, field, _ptr(out)))
+        return out
 
     def cells(self, first, count):
         ops = np.zeros((count, 8, 8))

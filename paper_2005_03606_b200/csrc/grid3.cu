@@ -323,6 +323,287 @@ __global__ void k_stats3(const int8_t* __restrict__ p3, int64_t nc, unsigned lon
     if (threadIdx.x < 9 && sh[threadIdx.x]) atomicAdd(&s[S_HIST + threadIdx.x], sh[threadIdx.x]);
 }
 
+// ------------------------------------------------------------ 3D cycle
+// The additive multilevel cycle of solver.cpp:99-347 restated on regular 3D
+// grids (the reference is 2D): hierarchical residual r̂ = fl - A û with
+// û = u - P u_c, restriction of r̂ into the coarse load, Jacobi on every
+// level, prolongation cascade, injection. Trilinear geometric transfer with
+// lattice weights w(L, a) = prod_d (a_d ? L_d : 3 - L_d) / 27 over the 4^3
+// lattice points of a patch; a fine vertex belongs to the patch with the
+// lowest coordinates that contains it (the 2D owner rule per axis,
+// solver.cpp:35-57); Galerkin coarse operators P^T A P (transfer.cpp:81-93).
+struct Lv3 {
+    int N;
+    double h;
+    double* v[LZB_V_NFIELDS];
+    const double* op;  // 64 per cell
+};
+
+__device__ __forceinline__ bool vxyz(const Lv3& L, int& ix, int& iy, int& iz, int64_t& vi) {
+    ix = blockIdx.x * blockDim.x + threadIdx.x;
+    iy = blockIdx.y;
+    iz = blockIdx.z;
+    if (ix > L.N) return false;
+    vi = (static_cast<int64_t>(iz) * (L.N + 1) + iy) * (L.N + 1) + ix;
+    return true;
+}
+__device__ __forceinline__ bool bnd3(int N, int ix, int iy, int iz) {
+    return ix == 0 || iy == 0 || iz == 0 || ix == N || iy == N || iz == N;
+}
+__device__ __forceinline__ int64_t vidx3(int N, int x, int y, int z) {
+    return (static_cast<int64_t>(z) * (N + 1) + y) * (N + 1) + x;
+}
+__device__ __forceinline__ double pw3(int lx, int ly, int lz, int a) {
+    return static_cast<double>(((a & 1) ? lx : 3 - lx) * (((a >> 1) & 1) ? ly : 3 - ly) * ((a >> 2) ? lz : 3 - lz)) /
+           27.0;
+}
+__device__ __forceinline__ int owner3(int f, int Nc) {
+    const int x1 = f / 3;
+    const int p = (f - 3 * x1 == 0 && x1 > 0) ? x1 - 1 : x1;
+    return p > Nc - 1 ? Nc - 1 : p;
+}
+
+// fl = sum over the adjacent leaves of f(v) h^3 / 8, f = scale prod sin(pi x_d)
+// (the lumped load of solver.cpp:99-118 in 3D; BASELINE f = 3 pi^2 prod sin)
+__global__ void k3_init_rhs(Lv3 F, double scale, double w) {
+    int ix, iy, iz;
+    int64_t vi;
+    if (!vxyz(F, ix, iy, iz, vi)) return;
+    int adj = 0;
+    for (int dz = 0; dz < 2; ++dz)
+        for (int dy = 0; dy < 2; ++dy)
+            for (int dx = 0; dx < 2; ++dx) {
+                const int cx = ix - dx, cy = iy - dy, cz = iz - dz;
+                adj += (cx >= 0 && cy >= 0 && cz >= 0 && cx < F.N && cy < F.N && cz < F.N);
+            }
+    const double x = ix * F.h, y = iy * F.h, z = iz * F.h;
+    const double term = w * (scale * sin(kPi * x) * sin(kPi * y) * sin(kPi * z));
+    double fl = 0.0;
+    for (int k = 0; k < adj; ++k) fl += term;
+    F.v[LZB_V_FL][vi] = fl;
+}
+
+__global__ void k3_noise(Lv3 L, int level, uint64_t seed, double gval) {
+    int ix, iy, iz;
+    int64_t vi;
+    if (!vxyz(L, ix, iy, iz, vi)) return;
+    if (bnd3(L.N, ix, iy, iz)) {
+        L.v[LZB_V_U][vi] = gval;
+        return;
+    }
+    auto mix = [](uint64_t z) {
+        z += 0x9e3779b97f4a7c15ull;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    };
+    const uint64_t k = mix(seed ^ mix((static_cast<uint64_t>(level) << 48) ^ (static_cast<uint64_t>(ix) << 32) ^
+                                      (static_cast<uint64_t>(iy) << 16) ^ static_cast<uint64_t>(iz)));
+    L.v[LZB_V_U][vi] = (4.0 / 3.0) * static_cast<double>(k >> 11) * 0x1.0p-53;
+}
+
+__global__ void k3_uhat(Lv3 F, Lv3 C, int has_coarse) {
+    int fx, fy, fz;
+    int64_t vi;
+    if (!vxyz(F, fx, fy, fz, vi)) return;
+    const double u = F.v[LZB_V_U][vi];
+    if (!has_coarse) {
+        F.v[LZB_V_UHAT][vi] = u;
+        return;
+    }
+    const int px = owner3(fx, C.N), py = owner3(fy, C.N), pz = owner3(fz, C.N);
+    const int lx = fx - 3 * px, ly = fy - 3 * py, lz = fz - 3 * pz;
+    double interp = 0.0;
+    for (int a = 0; a < 8; ++a)
+        interp += pw3(lx, ly, lz, a) * C.v[LZB_V_U][vidx3(C.N, px + (a & 1), py + ((a >> 1) & 1), pz + (a >> 2))];
+    F.v[LZB_V_UHAT][vi] = u - interp;
+}
+
+// r, r̂, diag per vertex, gathered over the 8 adjacent cells in (z, y, x) order.
+__global__ void __launch_bounds__(128) k3_residual(Lv3 F) {
+    int ix, iy, iz;
+    int64_t vi;
+    if (!vxyz(F, ix, iy, iz, vi)) return;
+    const int N = F.N;
+    const double fl = F.v[LZB_V_FL][vi];
+    double r = fl, rh = fl, dg = 0.0;
+    for (int q = 0; q < 8; ++q) {
+        const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;  // cell (ix-1+dx, ...)
+        const int cx = ix - 1 + dx, cy = iy - 1 + dy, cz = iz - 1 + dz;
+        if (cx < 0 || cy < 0 || cz < 0 || cx >= N || cy >= N || cz >= N) continue;
+        const int row = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
+        const double* K = F.op + 64 * ((static_cast<int64_t>(cz) * N + cy) * N + cx) + 8 * row;
+        double au = 0.0, auh = 0.0;
+        for (int col = 0; col < 8; ++col) {
+            const int64_t cv = vidx3(N, cx + (col & 1), cy + ((col >> 1) & 1), cz + (col >> 2));
+            au += K[col] * F.v[LZB_V_U][cv];
+            auh += K[col] * F.v[LZB_V_UHAT][cv];
+        }
+        r -= au;
+        rh -= auh;
+        dg += K[row];
+    }
+    if (bnd3(N, ix, iy, iz)) {
+        r = 0.0;
+        rh = 0.0;
+    }
+    F.v[LZB_V_R][vi] = r;
+    F.v[LZB_V_RHAT][vi] = rh;
+    F.v[LZB_V_DIAG][vi] = dg;
+}
+
+// fl_c = P^T r̂ over owned lattice points (adjacent patches in (z, y, x)
+// order, lattice points in (z, y, x) order). mode 1: r into aux (unused).
+__global__ void k3_restrict(Lv3 F, Lv3 C) {
+    int IX, IY, IZ;
+    int64_t vi;
+    if (!vxyz(C, IX, IY, IZ, vi)) return;
+    const int Nc = C.N;
+    double acc = 0.0;
+    for (int q = 0; q < 8; ++q) {
+        const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;
+        const int px = IX - 1 + dx, py = IY - 1 + dy, pz = IZ - 1 + dz;
+        if (px < 0 || py < 0 || pz < 0 || px >= Nc || py >= Nc || pz >= Nc) continue;
+        const int k = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);  // the vertex's corner in the patch
+        for (int lz = 0; lz < 4; ++lz) {
+            if (lz == 0 && pz != 0) continue;
+            for (int ly = 0; ly < 4; ++ly) {
+                if (ly == 0 && py != 0) continue;
+                for (int lx = 0; lx < 4; ++lx) {
+                    if (lx == 0 && px != 0) continue;
+                    const double w = pw3(lx, ly, lz, k);
+                    if (w == 0.0) continue;
+                    acc += w * F.v[LZB_V_RHAT][vidx3(F.N, 3 * px + lx, 3 * py + ly, 3 * pz + lz)];
+                }
+            }
+        }
+    }
+    C.v[LZB_V_FL][vi] = acc;
+}
+
+__global__ void k3_norm_partial(Lv3 F, double* partial) {
+    __shared__ double sh[256];
+    const int N = F.N;
+    double s = 0.0;
+    const int64_t rows = static_cast<int64_t>(N - 1) * (N - 1);  // interior (y, z) rows
+    for (int64_t rz = blockIdx.x; rz < rows; rz += gridDim.x) {
+        const int iy = 1 + static_cast<int>(rz % (N - 1)), iz = 1 + static_cast<int>(rz / (N - 1));
+        for (int ix = 1 + threadIdx.x; ix < N; ix += blockDim.x) {
+            const double r = F.v[LZB_V_R][vidx3(N, ix, iy, iz)];
+            s += r * r;
+        }
+    }
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void k3_snap(Lv3 L, int64_t nv) {
+    const int64_t i = gtid();
+    if (i >= nv) return;
+    L.v[LZB_V_USNAP][i] = L.v[LZB_V_U][i];
+    L.v[LZB_V_AUX][i] = 0.0;
+}
+
+__global__ void k3_aux_inject(Lv3 F, Lv3 C) {
+    int ix, iy, iz;
+    int64_t vi;
+    if (!vxyz(C, ix, iy, iz, vi)) return;
+    C.v[LZB_V_AUX][vi] = F.v[LZB_V_R][vidx3(F.N, 3 * ix, 3 * iy, 3 * iz)];
+}
+
+__global__ void k3_aux_sub(Lv3 F, Lv3 C, double omega) {
+    int fx, fy, fz;
+    int64_t vi;
+    if (!vxyz(F, fx, fy, fz, vi)) return;
+    if (bnd3(F.N, fx, fy, fz)) return;
+    const int px = owner3(fx, C.N), py = owner3(fy, C.N), pz = owner3(fz, C.N);
+    const int lx = fx - 3 * px, ly = fy - 3 * py, lz = fz - 3 * pz;
+    double p = 0.0;
+    for (int a = 0; a < 8; ++a) {
+        const int cx = px + (a & 1), cy = py + ((a >> 1) & 1), cz = pz + (a >> 2);
+        const int64_t ci = vidx3(C.N, cx, cy, cz);
+        const double dg = C.v[LZB_V_DIAG][ci];
+        const double caux = (!bnd3(C.N, cx, cy, cz) && dg != 0.0) ? omega / dg * C.v[LZB_V_AUX][ci] : 0.0;
+        p += pw3(lx, ly, lz, a) * caux;
+    }
+    F.v[LZB_V_U][vi] -= p;
+}
+
+__global__ void k3_jacobi(Lv3 F, double damping) {
+    int ix, iy, iz;
+    int64_t vi;
+    if (!vxyz(F, ix, iy, iz, vi)) return;
+    if (bnd3(F.N, ix, iy, iz)) return;
+    const double dg = F.v[LZB_V_DIAG][vi];
+    if (dg != 0.0) F.v[LZB_V_U][vi] += damping / dg * F.v[LZB_V_R][vi];
+}
+
+__global__ void k3_prolong(Lv3 F, Lv3 C) {
+    int fx, fy, fz;
+    int64_t vi;
+    if (!vxyz(F, fx, fy, fz, vi)) return;
+    if (bnd3(F.N, fx, fy, fz)) return;
+    const int px = owner3(fx, C.N), py = owner3(fy, C.N), pz = owner3(fz, C.N);
+    const int lx = fx - 3 * px, ly = fy - 3 * py, lz = fz - 3 * pz;
+    double d[8];
+    bool any = false;
+    for (int a = 0; a < 8; ++a) {
+        const int64_t ci = vidx3(C.N, px + (a & 1), py + ((a >> 1) & 1), pz + (a >> 2));
+        d[a] = C.v[LZB_V_U][ci] - C.v[LZB_V_USNAP][ci];
+        any |= d[a] != 0.0;
+    }
+    if (!any) return;
+    double p = 0.0;
+    for (int a = 0; a < 8; ++a) p += pw3(lx, ly, lz, a) * d[a];
+    F.v[LZB_V_U][vi] += p;
+}
+
+__global__ void k3_inject(Lv3 F, Lv3 C) {
+    int ix, iy, iz;
+    int64_t vi;
+    if (!vxyz(C, ix, iy, iz, vi)) return;
+    C.v[LZB_V_U][vi] = F.v[LZB_V_U][vidx3(F.N, 3 * ix, 3 * iy, 3 * iz)];
+}
+
+// Galerkin coarse element: sum over the 27 children (lz, ly, lx order) of
+// Q^T K_child Q, Q[i][a] = w(child lattice of corner i, a).
+__global__ void __launch_bounds__(64) k3_galerkin(double* __restrict__ cop, const double* __restrict__ fop, int Nc) {
+    const int64_t c = gtid();
+    if (c >= static_cast<int64_t>(Nc) * Nc * Nc) return;
+    const int px = static_cast<int>(c % Nc), py = static_cast<int>((c / Nc) % Nc), pz = static_cast<int>(c / Nc / Nc);
+    const int Nf = 3 * Nc;
+    double out[64];
+    for (int q = 0; q < 64; ++q) out[q] = 0.0;
+    for (int lz = 0; lz < 3; ++lz)
+        for (int ly = 0; ly < 3; ++ly)
+            for (int lx = 0; lx < 3; ++lx) {
+                const double* K =
+                    fop + 64 * ((static_cast<int64_t>(3 * pz + lz) * Nf + 3 * py + ly) * Nf + 3 * px + lx);
+                double Q[8][8];
+                for (int i = 0; i < 8; ++i)
+                    for (int a = 0; a < 8; ++a) Q[i][a] = pw3(lx + (i & 1), ly + ((i >> 1) & 1), lz + (i >> 2), a);
+                for (int i = 0; i < 8; ++i) {
+                    double T[8];  // row i of K Q
+                    for (int b = 0; b < 8; ++b) {
+                        double t = 0.0;
+                        for (int j = 0; j < 8; ++j) t += K[8 * i + j] * Q[j][b];
+                        T[b] = t;
+                    }
+                    for (int a = 0; a < 8; ++a) {
+                        const double qa = Q[i][a];
+                        if (qa == 0.0) continue;
+                        for (int b = 0; b < 8; ++b) out[8 * a + b] += qa * T[b];
+                    }
+                }
+            }
+    for (int q = 0; q < 64; ++q) cop[64 * c + q] = out[q];
+}
+
 // ------------------------------------------------------------ host side
 uint64_t splitmix64_host(uint64_t& z) {
     z += 0x9e3779b97f4a7c15ull;
@@ -442,6 +723,7 @@ public:
 
     void assemble_fixed(int n) {
         if (n < 1 || n > kMaxN3) throw Error(LZB_ERR_INVALID, "3D sub-samples per axis must be in 1..16");
+        ops_dirty_ = true;
         const AxisTab3 T = axis_tab3(n), T1 = axis_tab3(1);
         LZB_LAUNCH(k_assemble3, blocks_for(nc_, 128), 128, 0, s_, F_, N_, h_, T, T1, delta_, fixed_, op_.p, p3_.p,
                    n_.p, stats_.p, ctx_->err.p);
@@ -488,6 +770,104 @@ public:
             for (int64_t i = 0; i < count; ++i) p3[i] = q[i];
     }
 
+    // ------------------------------------------------------- 3D cycle
+    void init_cycle(int variant, double omega, double rhs_scale, uint64_t noise_seed, int max_cycles,
+                    double target) {
+        if (variant == LZB_ADAFAC_JAC) throw Error(LZB_ERR_INVALID, "the 3D cycle runs additive and adafac-pi");
+        variant_ = variant;
+        omega_ = omega;
+        max_cycles_ = max_cycles;
+        target_ = target;
+        L3_.resize(D_ + 1);
+        for (int l = 0; l <= D_; ++l) {
+            Lev& L = L3_[l];
+            L.N = 1;
+            for (int i = 0; i < l; ++i) L.N *= 3;
+            L.nv = static_cast<int64_t>(L.N + 1) * (L.N + 1) * (L.N + 1);
+            L.h = std::pow(1.0 / 3, l);
+            for (int f = 0; f < LZB_V_NFIELDS; ++f) {
+                L.v[f].alloc(L.nv);
+                LZB_CUDA(cudaMemsetAsync(L.v[f].p, 0, L.v[f].bytes(), s_));
+            }
+            if (l < D_) L.op.alloc(static_cast<size_t>(L.N) * L.N * L.N * 64);
+        }
+        partial3_.alloc(kNormBlocks3);
+        res3_.alloc(1);
+        for (int l = 0; l <= D_; ++l)
+            LZB_LAUNCH(k3_noise, vg(l), 128, 0, s_, lv(l), l, noise_seed, 0.0);
+        inject3();
+        LZB_LAUNCH(k3_init_rhs, vg(D_), 128, 0, s_, lv(D_), rhs_scale, L3_[D_].h * L3_[D_].h * L3_[D_].h / 8.0);
+        cycle_ = 0;
+        history_.clear();
+        sync();
+    }
+
+    // Coarse operators from the leaves (after an assembly): Galerkin, finest first.
+    void coarse_ops() {
+        for (int l = D_ - 1; l >= 0; --l) {
+            const int64_t ncl = static_cast<int64_t>(L3_[l].N) * L3_[l].N * L3_[l].N;
+            LZB_LAUNCH(k3_galerkin, blocks_for(ncl, 64), 64, 0, s_, L3_[l].op.p, l + 1 == D_ ? op_.p : L3_[l + 1].op.p,
+                       L3_[l].N);
+        }
+    }
+
+    lzb_cycle_report step() {
+        if (L3_.empty()) throw Error(LZB_ERR_INVALID, "call init_cycle first");
+        if (ops_dirty_) {
+            coarse_ops();
+            ops_dirty_ = false;
+        }
+        lzb_cycle_report rep;
+        std::memset(&rep, 0, sizeof rep);
+        rep.cycle = static_cast<int32_t>(++cycle_);
+        for (int l = D_; l >= 0; --l) {
+            LZB_LAUNCH(k3_uhat, vg(l), 128, 0, s_, lv(l), l > 0 ? lv(l - 1) : lv(l), l > 0 ? 1 : 0);
+            LZB_LAUNCH(k3_residual, vg(l), 128, 0, s_, lv(l));
+            if (l > 0) LZB_LAUNCH(k3_restrict, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
+        }
+        const int ng = L3_[D_].N > 1 ? kNormBlocks3 : 1;
+        LZB_CUDA(cudaMemsetAsync(partial3_.p, 0, partial3_.bytes(), s_));
+        if (L3_[D_].N > 1) LZB_LAUNCH(k3_norm_partial, ng, 256, 0, s_, lv(D_), partial3_.p);
+        std::vector<double> part(kNormBlocks3);
+        LZB_CUDA(cudaMemcpyAsync(part.data(), partial3_.p, kNormBlocks3 * sizeof(double), cudaMemcpyDeviceToHost, s_));
+        sync();
+        double s2 = 0.0;
+        for (double x : part) s2 += x;
+        rep.residual = std::sqrt(s2);
+        if (history_.empty()) first_ = rep.residual > 0.0 ? rep.residual : 1.0;
+        history_.push_back(rep.residual);
+        rep.normalized = rep.residual / first_;
+        rep.status = rep.normalized <= target_ ? LZB_CONVERGED
+                     : rep.normalized >= 1e2 ? LZB_DIVERGED
+                     : static_cast<int>(cycle_) >= max_cycles_ ? LZB_TIMEOUT : LZB_CONTINUE;
+        if (rep.status == LZB_CONTINUE || rep.status == LZB_TIMEOUT) {
+            for (int l = 0; l < D_; ++l) LZB_LAUNCH(k3_snap, blocks_for(L3_[l].nv, 256), 256, 0, s_, lv(l), L3_[l].nv);
+            for (int l = D_; l >= 0; --l) {
+                if (variant_ == LZB_ADAFAC_PI && l > 0) {
+                    LZB_LAUNCH(k3_aux_inject, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
+                    LZB_LAUNCH(k3_aux_sub, vg(l), 128, 0, s_, lv(l), lv(l - 1), omega_);
+                }
+                const double damping = variant_ == LZB_ADDITIVE ? std::pow(omega_, D_ - l + 1) : omega_;
+                LZB_LAUNCH(k3_jacobi, vg(l), 128, 0, s_, lv(l), damping);
+            }
+            for (int l = 1; l <= D_; ++l) LZB_LAUNCH(k3_prolong, vg(l), 128, 0, s_, lv(l), lv(l - 1));
+            inject3();
+            const uint64_t Nf = static_cast<uint64_t>(L3_[D_].N);
+            rep.dof_updates = (Nf - 1) * (Nf - 1) * (Nf - 1);
+        }
+        rep.levels = D_ + 1;
+        rep.cells = static_cast<uint64_t>(nc_);
+        sync();
+        return rep;
+    }
+
+    void vertices(int level, int field, double* out) {
+        if (L3_.empty() || level < 0 || level > D_ || field < 0 || field >= LZB_V_NFIELDS)
+            throw Error(LZB_ERR_INVALID, "bad level / field");
+        LZB_CUDA(cudaMemcpyAsync(out, L3_[level].v[field].p, L3_[level].v[field].bytes(), cudaMemcpyDeviceToHost, s_));
+        sync();
+    }
+
     void sync() {
         LZB_CUDA(cudaStreamSynchronize(s_));
         int flag = 0;
@@ -509,6 +889,35 @@ private:
     DevBuf<int8_t> p3_;
     DevBuf<int32_t> n_;
     DevBuf<unsigned long long> stats_;
+    // 3D cycle
+    struct Lev {
+        int N = 1;
+        int64_t nv = 8;
+        double h = 1.0;
+        DevBuf<double> v[LZB_V_NFIELDS];
+        DevBuf<double> op;  // coarse levels (the leaves use op_)
+    };
+    static constexpr int kNormBlocks3 = 148 * 2;
+    std::vector<Lev> L3_;
+    DevBuf<double> partial3_, res3_;
+    int variant_ = LZB_ADDITIVE, max_cycles_ = 100;
+    double omega_ = 0.6, target_ = 1e-10, first_ = 1.0;
+    uint32_t cycle_ = 0;
+    bool ops_dirty_ = true;
+    std::vector<double> history_;
+
+    Lv3 lv(int l) const {
+        Lv3 v{};
+        v.N = L3_[l].N;
+        v.h = L3_[l].h;
+        for (int f = 0; f < LZB_V_NFIELDS; ++f) v.v[f] = L3_[l].v[f].p;
+        v.op = l == D_ ? op_.p : L3_[l].op.p;
+        return v;
+    }
+    dim3 vg(int l) const { return dim3(blocks_for(L3_[l].N + 1, 128), L3_[l].N + 1, L3_[l].N + 1); }
+    void inject3() {
+        for (int l = D_; l >= 1; --l) LZB_LAUNCH(k3_inject, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
+    }
 };
 
 }  // namespace lzb
@@ -577,6 +986,16 @@ int lzb_grid3_stats(lzb_grid3* g, lzb_compression_stats* out) {
 }
 int lzb_grid3_cells(lzb_grid3* g, int64_t first, int64_t count, double* ops, int32_t* p3) {
     return lzb::guarded([&] { g->g->cells(first, count, ops, p3); });
+}
+int lzb_grid3_init_cycle(lzb_grid3* g, int variant, double omega, double rhs_scale, uint64_t noise_seed,
+                         int max_cycles, double target) {
+    return lzb::guarded([&] { g->g->init_cycle(variant, omega, rhs_scale, noise_seed, max_cycles, target); });
+}
+int lzb_grid3_step(lzb_grid3* g, lzb_cycle_report* out) {
+    return lzb::guarded([&] { *out = g->g->step(); });
+}
+int lzb_grid3_vertices(lzb_grid3* g, int level, int field, double* out) {
+    return lzb::guarded([&] { g->g->vertices(level, field, out); });
 }
 
 }  // extern "C"
