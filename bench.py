@@ -370,6 +370,18 @@ def run_ours(args, world, rank, local):
                          "frac_executed": ns * C3_FLOPS_PER_SAMPLE / t3 / 1e12 / fp64_peak,
                          "lzmg_bytes_per_cell": st3.fine_stored_bytes / st3.fine_cells,
                          "store_GBs": 512 * 3 ** 15 / t3 / 1e9}
+    # record bytes per cell across the mantissa widths (BASELINE configs[4] widths
+    # 4/8/16/23/32/52 bits -> nearest p3 2..8), 243^3 at p = 4
+    c3["width_sweep"] = []
+    for w3 in (2, 3, 4, 5, 6, 7, 8):
+        gw = lzb.Grid3(5, lzb.field3_grf(lzb.grf_table(1, 64, 0.05, 1.0)), delta_max=1e-8, fixed_p3=w3, ctx=ctx)
+        gw.assemble_fixed(4)
+        stw = gw.stats()
+        c3["width_sweep"].append({"p3": w3, "mantissa_bits": measure.MANTISSA_BITS[w3],
+                                  "record_bytes_per_cell": stw.fine_stored_bytes / stw.fine_cells,
+                                  "max_abs_error": stw.max_delta})
+        gw.close()
+        del gw
     # 10 adaFAC-PI cycles on the p = 8 operators (Galerkin coarse levels, trilinear transfer)
     g3.assemble_fixed(8)
     g3.init_cycle(solver="adafac-pi", omega=0.6, max_cycles=10 ** 6)
