@@ -15,7 +15,8 @@
 // accumulated with partial sums over the innermost axis (4 flops per sample,
 // not 27 per entry), so the per-sample cost is the eps evaluation.
 //
-// Layout in HBM: cell operators AoS, 64 doubles = 512 B per cell, index
+// Layout in HBM: cell operators as class records (the 27 distinct values of
+// the 8x8 matrix, padded to 28 doubles = 224 B per cell), index
 // (cz*N + cy)*N + cx; markers p3 (i8), n (i32).
 #include <complex>
 #include <memory>
@@ -228,6 +229,19 @@ __global__ void k_elements3(Field3 F, int64_t count, const double* x0, const dou
         for (int b = 0; b < 8; ++b) out[64 * t + 8 * a + b] = entry3(A, hn, a, b);
 }
 
+// Class index of entry (a, b): q = 9 c_x + 3 c_y + c_z, per axis c = 0 (both
+// corners 0), 1 (different), 2 (both 1).
+__host__ __device__ __forceinline__ int cls3(int a, int b) {
+    const int ax = a & 1, ay = (a >> 1) & 1, az = a >> 2, bx = b & 1, by = (b >> 1) & 1, bz = b >> 2;
+    return 9 * (ax == bx ? 2 * ax : 1) + 3 * (ay == by ? 2 * ay : 1) + (az == bz ? 2 * az : 1);
+}
+// Operators in HBM are class records: the 27 class values (padded to 28 for
+// 16-B stores), 224 B per cell instead of 512 — trilinear operators built
+// from tensor products of symmetric per-axis 2x2 matrices (the elements here
+// and their Galerkin products with the tensor-product P) take one value per
+// class for any eps.
+constexpr int kCls3 = 28;
+
 // The 64 entries of a trilinear element take 27 values: entry (a, b)
 // depends only on the per-axis pair classes (c = 0: both 0, 1: different,
 // 2: both 1), the sign of each term being fixed by its class.
@@ -289,16 +303,10 @@ __global__ void __launch_bounds__(128) k_assemble3(Field3 F, int N, double h, Ax
         delta = delta < d ? d : delta;
         dec[q] = base[q] + rt;
     }
-    double2* o = reinterpret_cast<double2*>(op + 64 * c);
+    double2* o = reinterpret_cast<double2*>(op + kCls3 * c);
 #pragma unroll
-    for (int k = 0; k < 64; k += 2) {
-        const int a = k >> 3, b0 = k & 7, b1 = b0 + 1;
-        auto cls = [](int a, int b) {
-            const int ax = a & 1, ay = (a >> 1) & 1, az = a >> 2, bx = b & 1, by = (b >> 1) & 1, bz = b >> 2;
-            return 9 * (ax == bx ? 2 * ax : 1) + 3 * (ay == by ? 2 * ay : 1) + (az == bz ? 2 * az : 1);
-        };
-        o[k >> 1] = make_double2(dec[cls(a, b0)], dec[cls(a, b1)]);
-    }
+    for (int q = 0; q < 26; q += 2) o[q >> 1] = make_double2(dec[q], dec[q + 1]);
+    o[13] = make_double2(dec[26], 0.0);
     p3o[c] = static_cast<int8_t>(p3);
     no[c] = T.n;
     atomic_max_double_bits(&stats[S_MAXDELTA], delta);
@@ -432,16 +440,17 @@ __global__ void __launch_bounds__(128) k3_residual(Lv3 F) {
         const int cx = ix - 1 + dx, cy = iy - 1 + dy, cz = iz - 1 + dz;
         if (cx < 0 || cy < 0 || cz < 0 || cx >= N || cy >= N || cz >= N) continue;
         const int row = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
-        const double* K = F.op + 64 * ((static_cast<int64_t>(cz) * N + cy) * N + cx) + 8 * row;
+        const double* K = F.op + kCls3 * ((static_cast<int64_t>(cz) * N + cy) * N + cx);
         double au = 0.0, auh = 0.0;
         for (int col = 0; col < 8; ++col) {
             const int64_t cv = vidx3(N, cx + (col & 1), cy + ((col >> 1) & 1), cz + (col >> 2));
-            au += K[col] * F.v[LZB_V_U][cv];
-            auh += K[col] * F.v[LZB_V_UHAT][cv];
+            const double k = __ldg(K + cls3(row, col));
+            au += k * F.v[LZB_V_U][cv];
+            auh += k * F.v[LZB_V_UHAT][cv];
         }
         r -= au;
         rh -= auh;
-        dg += K[row];
+        dg += __ldg(K + cls3(row, row));
     }
     if (bnd3(N, ix, iy, iz)) {
         r = 0.0;
@@ -571,37 +580,42 @@ __global__ void k3_inject(Lv3 F, Lv3 C) {
 }
 
 // Galerkin coarse element: sum over the 27 children (lz, ly, lx order) of
-// Q^T K_child Q, Q[i][a] = w(child lattice of corner i, a).
+// Q^T K_child Q, Q[i][a] = w(child lattice of corner i, a); the 27 class
+// values from their representative entries (per axis (0,0), (0,1), (1,1)).
 __global__ void __launch_bounds__(64) k3_galerkin(double* __restrict__ cop, const double* __restrict__ fop, int Nc) {
     const int64_t c = gtid();
     if (c >= static_cast<int64_t>(Nc) * Nc * Nc) return;
     const int px = static_cast<int>(c % Nc), py = static_cast<int>((c / Nc) % Nc), pz = static_cast<int>(c / Nc / Nc);
     const int Nf = 3 * Nc;
-    double out[64];
-    for (int q = 0; q < 64; ++q) out[q] = 0.0;
+    double out[27];
+    for (int q = 0; q < 27; ++q) out[q] = 0.0;
     for (int lz = 0; lz < 3; ++lz)
         for (int ly = 0; ly < 3; ++ly)
             for (int lx = 0; lx < 3; ++lx) {
-                const double* K =
-                    fop + 64 * ((static_cast<int64_t>(3 * pz + lz) * Nf + 3 * py + ly) * Nf + 3 * px + lx);
-                double Q[8][8];
-                for (int i = 0; i < 8; ++i)
-                    for (int a = 0; a < 8; ++a) Q[i][a] = pw3(lx + (i & 1), ly + ((i >> 1) & 1), lz + (i >> 2), a);
-                for (int i = 0; i < 8; ++i) {
-                    double T[8];  // row i of K Q
-                    for (int b = 0; b < 8; ++b) {
-                        double t = 0.0;
-                        for (int j = 0; j < 8; ++j) t += K[8 * i + j] * Q[j][b];
-                        T[b] = t;
-                    }
-                    for (int a = 0; a < 8; ++a) {
-                        const double qa = Q[i][a];
+                const double* K27 =
+                    fop + kCls3 * ((static_cast<int64_t>(3 * pz + lz) * Nf + 3 * py + ly) * Nf + 3 * px + lx);
+                double Kc[27];
+                for (int q = 0; q < 27; ++q) Kc[q] = __ldg(K27 + q);
+                for (int q = 0; q < 27; ++q) {
+                    // representative (a, b) of class q
+                    const int cx = q / 9, cy = (q / 3) % 3, cz = q % 3;
+                    const int a = (cx == 2) + 2 * (cy == 2) + 4 * (cz == 2);
+                    const int b = (cx >= 1) + 2 * (cy >= 1) + 4 * (cz >= 1);
+                    double acc = 0.0;
+                    for (int i = 0; i < 8; ++i) {
+                        const double qa = pw3(lx + (i & 1), ly + ((i >> 1) & 1), lz + (i >> 2), a);
                         if (qa == 0.0) continue;
-                        for (int b = 0; b < 8; ++b) out[8 * a + b] += qa * T[b];
+                        double t = 0.0;
+                        for (int j = 0; j < 8; ++j)
+                            t += Kc[cls3(i, j)] * pw3(lx + (j & 1), ly + ((j >> 1) & 1), lz + (j >> 2), b);
+                        acc += qa * t;
                     }
+                    out[q] += acc;
                 }
             }
-    for (int q = 0; q < 64; ++q) cop[64 * c + q] = out[q];
+    double2* o = reinterpret_cast<double2*>(cop + kCls3 * c);
+    for (int q = 0; q < 26; q += 2) o[q >> 1] = make_double2(out[q], out[q + 1]);
+    o[13] = make_double2(out[26], 0.0);
 }
 
 // ------------------------------------------------------------ host side
@@ -711,7 +725,7 @@ public:
         nc_ = static_cast<int64_t>(N_) * N_ * N_;
         h_ = std::pow(1.0 / 3, depth);
         F_ = to_device(f, table_);
-        op_.alloc(static_cast<size_t>(nc_) * 64);
+        op_.alloc(static_cast<size_t>(nc_) * kCls3);
         p3_.alloc(nc_);
         n_.alloc(nc_);
         stats_.alloc(20);
@@ -761,11 +775,17 @@ public:
 
     void cells(int64_t first, int64_t count, double* ops, int32_t* p3) {
         if (first < 0 || count < 0 || first + count > nc_) throw Error(LZB_ERR_INVALID, "bad cell range");
+        std::vector<double> cls(static_cast<size_t>(count) * kCls3);
         if (ops)
-            LZB_CUDA(cudaMemcpyAsync(ops, op_.p + 64 * first, count * 64 * sizeof(double), cudaMemcpyDeviceToHost, s_));
+            LZB_CUDA(cudaMemcpyAsync(cls.data(), op_.p + kCls3 * first, cls.size() * sizeof(double),
+                                     cudaMemcpyDeviceToHost, s_));
         std::vector<int8_t> q(count);
         if (p3) LZB_CUDA(cudaMemcpyAsync(q.data(), p3_.p + first, count, cudaMemcpyDeviceToHost, s_));
         sync();
+        if (ops)  // the 64 entries of each class record
+            for (int64_t i = 0; i < count; ++i)
+                for (int a = 0; a < 8; ++a)
+                    for (int b = 0; b < 8; ++b) ops[64 * i + 8 * a + b] = cls[kCls3 * i + cls3(a, b)];
         if (p3)
             for (int64_t i = 0; i < count; ++i) p3[i] = q[i];
     }
@@ -789,7 +809,7 @@ public:
                 L.v[f].alloc(L.nv);
                 LZB_CUDA(cudaMemsetAsync(L.v[f].p, 0, L.v[f].bytes(), s_));
             }
-            if (l < D_) L.op.alloc(static_cast<size_t>(L.N) * L.N * L.N * 64);
+            if (l < D_) L.op.alloc(static_cast<size_t>(L.N) * L.N * L.N * kCls3);
         }
         partial3_.alloc(kNormBlocks3);
         res3_.alloc(1);
