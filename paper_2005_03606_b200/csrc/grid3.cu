@@ -579,43 +579,62 @@ __global__ void k3_inject(Lv3 F, Lv3 C) {
     C.v[LZB_V_U][vi] = F.v[LZB_V_U][vidx3(F.N, 3 * ix, 3 * iy, 3 * iz)];
 }
 
-// Galerkin coarse element: sum over the 27 children (lz, ly, lx order) of
-// Q^T K_child Q, Q[i][a] = w(child lattice of corner i, a); the 27 class
-// values from their representative entries (per axis (0,0), (0,1), (1,1)).
-__global__ void __launch_bounds__(64) k3_galerkin(double* __restrict__ cop, const double* __restrict__ fop, int Nc) {
+// Galerkin coarse element (transfer.cpp:81-93 restated): in class form
+//   A_c[q] = sum_children sum_k K_child[k] W[child][k][q],
+//   W[child][k][q] = sum_{(i,j) in class k} Q_child[i][a_q] Q_child[j][b_q],
+// Q_child[i][a] = w(child lattice of corner i, a), (a_q, b_q) the
+// representative entry of class q. W (27^3 values) is a constant of the
+// trilinear transfer: computed once on the host, staged in shared memory.
+constexpr int kW3 = 27 * 27 * 27;
+__global__ void __launch_bounds__(256) k3_galerkin(double* __restrict__ cop, const double* __restrict__ fop, int Nc,
+                                                   const double* __restrict__ W) {
+    extern __shared__ double sW[];
+    for (int i = threadIdx.x; i < kW3; i += blockDim.x) sW[i] = W[i];
+    __syncthreads();
     const int64_t c = gtid();
     if (c >= static_cast<int64_t>(Nc) * Nc * Nc) return;
     const int px = static_cast<int>(c % Nc), py = static_cast<int>((c / Nc) % Nc), pz = static_cast<int>(c / Nc / Nc);
     const int Nf = 3 * Nc;
     double out[27];
+#pragma unroll
     for (int q = 0; q < 27; ++q) out[q] = 0.0;
-    for (int lz = 0; lz < 3; ++lz)
-        for (int ly = 0; ly < 3; ++ly)
-            for (int lx = 0; lx < 3; ++lx) {
-                const double* K27 =
-                    fop + kCls3 * ((static_cast<int64_t>(3 * pz + lz) * Nf + 3 * py + ly) * Nf + 3 * px + lx);
-                double Kc[27];
-                for (int q = 0; q < 27; ++q) Kc[q] = __ldg(K27 + q);
-                for (int q = 0; q < 27; ++q) {
-                    // representative (a, b) of class q
-                    const int cx = q / 9, cy = (q / 3) % 3, cz = q % 3;
-                    const int a = (cx == 2) + 2 * (cy == 2) + 4 * (cz == 2);
-                    const int b = (cx >= 1) + 2 * (cy >= 1) + 4 * (cz >= 1);
-                    double acc = 0.0;
-                    for (int i = 0; i < 8; ++i) {
-                        const double qa = pw3(lx + (i & 1), ly + ((i >> 1) & 1), lz + (i >> 2), a);
-                        if (qa == 0.0) continue;
-                        double t = 0.0;
-                        for (int j = 0; j < 8; ++j)
-                            t += Kc[cls3(i, j)] * pw3(lx + (j & 1), ly + ((j >> 1) & 1), lz + (j >> 2), b);
-                        acc += qa * t;
-                    }
-                    out[q] += acc;
-                }
-            }
+    for (int ch = 0; ch < 27; ++ch) {  // child (lz, ly, lx) = (ch / 9, (ch / 3) % 3, ch % 3)
+        const int lz = ch / 9, ly = (ch / 3) % 3, lx = ch % 3;
+        const double* K27 = fop + kCls3 * ((static_cast<int64_t>(3 * pz + lz) * Nf + 3 * py + ly) * Nf + 3 * px + lx);
+        const double* Wc = sW + ch * 27 * 27;
+        for (int k = 0; k < 27; ++k) {
+            const double kv = __ldg(K27 + k);
+#pragma unroll
+            for (int q = 0; q < 27; ++q) out[q] += kv * Wc[k * 27 + q];
+        }
+    }
     double2* o = reinterpret_cast<double2*>(cop + kCls3 * c);
+#pragma unroll
     for (int q = 0; q < 26; q += 2) o[q >> 1] = make_double2(out[q], out[q + 1]);
     o[13] = make_double2(out[26], 0.0);
+}
+
+std::vector<double> galerkin_weights3() {
+    std::vector<double> W(kW3, 0.0);
+    auto w = [](int lx, int ly, int lz, int a) {
+        return static_cast<double>(((a & 1) ? lx : 3 - lx) * (((a >> 1) & 1) ? ly : 3 - ly) * ((a >> 2) ? lz : 3 - lz)) /
+               27.0;
+    };
+    for (int ch = 0; ch < 27; ++ch) {
+        const int lz = ch / 9, ly = (ch / 3) % 3, lx = ch % 3;
+        for (int q = 0; q < 27; ++q) {
+            const int cx = q / 9, cy = (q / 3) % 3, cz = q % 3;
+            const int a = (cx == 2) + 2 * (cy == 2) + 4 * (cz == 2);
+            const int b = (cx >= 1) + 2 * (cy >= 1) + 4 * (cz >= 1);
+            for (int i = 0; i < 8; ++i)
+                for (int j = 0; j < 8; ++j) {
+                    const double qi = w(lx + (i & 1), ly + ((i >> 1) & 1), lz + (i >> 2), a);
+                    const double qj = w(lx + (j & 1), ly + ((j >> 1) & 1), lz + (j >> 2), b);
+                    W[(ch * 27 + cls3(i, j)) * 27 + q] += qi * qj;
+                }
+        }
+    }
+    return W;
 }
 
 // ------------------------------------------------------------ host side
@@ -812,6 +831,13 @@ public:
             if (l < D_) L.op.alloc(static_cast<size_t>(L.N) * L.N * L.N * kCls3);
         }
         partial3_.alloc(kNormBlocks3);
+        {
+            const std::vector<double> W = galerkin_weights3();
+            W3_.alloc(kW3);
+            LZB_CUDA(cudaMemcpy(W3_.p, W.data(), kW3 * sizeof(double), cudaMemcpyHostToDevice));
+            LZB_CUDA(cudaFuncSetAttribute(k3_galerkin, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kW3 * sizeof(double))));
+        }
         res3_.alloc(1);
         for (int l = 0; l <= D_; ++l)
             LZB_LAUNCH(k3_noise, vg(l), 128, 0, s_, lv(l), l, noise_seed, 0.0);
@@ -826,8 +852,8 @@ public:
     void coarse_ops() {
         for (int l = D_ - 1; l >= 0; --l) {
             const int64_t ncl = static_cast<int64_t>(L3_[l].N) * L3_[l].N * L3_[l].N;
-            LZB_LAUNCH(k3_galerkin, blocks_for(ncl, 64), 64, 0, s_, L3_[l].op.p, l + 1 == D_ ? op_.p : L3_[l + 1].op.p,
-                       L3_[l].N);
+            LZB_LAUNCH(k3_galerkin, blocks_for(ncl, 256), 256, kW3 * sizeof(double), s_, L3_[l].op.p,
+                       l + 1 == D_ ? op_.p : L3_[l + 1].op.p, L3_[l].N, W3_.p);
         }
     }
 
@@ -919,7 +945,7 @@ private:
     };
     static constexpr int kNormBlocks3 = 148 * 2;
     std::vector<Lev> L3_;
-    DevBuf<double> partial3_, res3_;
+    DevBuf<double> partial3_, res3_, W3_;
     int variant_ = LZB_ADDITIVE, max_cycles_ = 100;
     double omega_ = 0.6, target_ = 1e-10, first_ = 1.0;
     uint32_t cycle_ = 0;
