@@ -427,30 +427,45 @@ __global__ void k3_uhat(Lv3 F, Lv3 C, int has_coarse) {
     F.v[LZB_V_UHAT][vi] = u - interp;
 }
 
-// r, r̂, diag per vertex, gathered over the 8 adjacent cells in (z, y, x) order.
+// r, r̂, diag per vertex, gathered over the 8 adjacent cells in (z, y, x)
+// order; the 3x3x3 u / û neighbourhood and the 8 class values of the
+// vertex's row in each cell are all loaded before use.
 __global__ void __launch_bounds__(128) k3_residual(Lv3 F) {
     int ix, iy, iz;
     int64_t vi;
     if (!vxyz(F, ix, iy, iz, vi)) return;
     const int N = F.N;
+    double uu[27], uh[27];
+#pragma unroll
+    for (int d = 0; d < 27; ++d) {
+        const int x = min(max(ix - 1 + d % 3, 0), N), y = min(max(iy - 1 + (d / 3) % 3, 0), N),
+                  z = min(max(iz - 1 + d / 9, 0), N);
+        const int64_t cv = vidx3(N, x, y, z);
+        uu[d] = F.v[LZB_V_U][cv];
+        uh[d] = F.v[LZB_V_UHAT][cv];
+    }
     const double fl = F.v[LZB_V_FL][vi];
     double r = fl, rh = fl, dg = 0.0;
+#pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;  // cell (ix-1+dx, ...)
         const int cx = ix - 1 + dx, cy = iy - 1 + dy, cz = iz - 1 + dz;
         if (cx < 0 || cy < 0 || cz < 0 || cx >= N || cy >= N || cz >= N) continue;
         const int row = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
         const double* K = F.op + kCls3 * ((static_cast<int64_t>(cz) * N + cy) * N + cx);
+        double k8[8];
+#pragma unroll
+        for (int col = 0; col < 8; ++col) k8[col] = __ldg(K + cls3(row, col));
         double au = 0.0, auh = 0.0;
+#pragma unroll
         for (int col = 0; col < 8; ++col) {
-            const int64_t cv = vidx3(N, cx + (col & 1), cy + ((col >> 1) & 1), cz + (col >> 2));
-            const double k = __ldg(K + cls3(row, col));
-            au += k * F.v[LZB_V_U][cv];
-            auh += k * F.v[LZB_V_UHAT][cv];
+            const int d = (dz + (col >> 2)) * 9 + (dy + ((col >> 1) & 1)) * 3 + dx + (col & 1);
+            au += k8[col] * uu[d];
+            auh += k8[col] * uh[d];
         }
         r -= au;
         rh -= auh;
-        dg += __ldg(K + cls3(row, row));
+        dg += k8[row];
     }
     if (bnd3(N, ix, iy, iz)) {
         r = 0.0;
