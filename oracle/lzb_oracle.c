@@ -408,6 +408,7 @@ typedef struct {
     int32_t* n;
     uint32_t* epoch;
     uint8_t* has_P;
+    uint8_t* dirty; /* CellStream slot dirty[2] as bits 0/1 (stream.cpp:240-260) */
     double* v[LZB_V_NFIELDS];
 } orc_level;
 
@@ -426,6 +427,9 @@ struct orc_grid {
     /* TaskPool with workers = 1 (scheduler.cpp:88-111): FIFO of leaf cells */
     int32_t* queue;
     int64_t qhead, qtail, qcap;
+    /* the high-priority class: coarse_recompute tasks (level, cell), FIFO */
+    int32_t* hq;
+    int64_t hhead, htail, hcap;
     uint64_t spawned, completed;
     double geo[64];
     double kunit[16];
@@ -467,6 +471,7 @@ orc_grid* orc_grid_create(const lzb_grid_desc* d) {
         L->n = calloc(nc, sizeof(int32_t));
         L->epoch = calloc(nc, sizeof(uint32_t));
         L->has_P = calloc(nc, 1);
+        L->dirty = calloc(nc, 1);
         if (l < g->D) L->P = calloc(nc * 64, sizeof(double));
         for (int f = 0; f < LZB_V_NFIELDS; ++f) L->v[f] = calloc(nv, sizeof(double));
         for (int c = 0; c < N; ++c) {
@@ -506,12 +511,13 @@ void orc_grid_destroy(orc_grid* g) {
     for (int l = 0; l <= g->D; ++l) {
         orc_level* L = &g->L[l];
         free(L->order); free(L->vorder); free(L->rx); free(L->ry); free(L->op); free(L->P);
-        free(L->p1); free(L->p2); free(L->p3); free(L->n); free(L->epoch); free(L->has_P);
+        free(L->p1); free(L->p2); free(L->p3); free(L->n); free(L->epoch); free(L->has_P); free(L->dirty);
         for (int f = 0; f < LZB_V_NFIELDS; ++f) free(L->v[f]);
     }
     free(g->L);
     free(g->history);
     free(g->queue);
+    free(g->hq);
     free(g);
 }
 
@@ -533,6 +539,16 @@ static void element_or_baseline(const orc_grid* g, int l, int c, double* out) {
 static const double* transfer_or_geometric(const orc_grid* g, int l, int c) {
     const orc_level* L = &g->L[l];
     return L->has_P[c] ? L->P + 64 * c : g->geo; /* stream.cpp:212-216 */
+}
+
+/* CellStream::mark_parent_dirty (stream.cpp:240-245): the parent's flag of
+ * the parity (cycle + 1) & 1, taken by the walk of the next cycle */
+static void mark_parent_dirty(orc_grid* g, int l, int c) {
+    if (l == 0) return;
+    const orc_level* L = &g->L[l];
+    int cx = c % L->N, cy = c / L->N;
+    orc_level* P = &g->L[l - 1];
+    P->dirty[(cy / 3) * P->N + cx / 3] |= (uint8_t)(1u << ((g->cycle + 1) & 1u));
 }
 
 /* stream.cpp:100-132 (caller sets p1, assembly.cpp) */
@@ -557,6 +573,7 @@ static int publish_element(orc_grid* g, int l, int c, const double* m, int n) {
     L->n[c] = n;
     L->epoch[c] = g->cycle;
     L->p3[c] = p3;
+    mark_parent_dirty(g, l, c);
     return 0;
 }
 
@@ -596,6 +613,7 @@ static int publish_coarse(orc_grid* g, int l, int c, const double* m, const doub
     L->epoch[c] = g->cycle;
     L->p3[c] = p3;
     L->p1[c] = LZB_P1_TOP;
+    mark_parent_dirty(g, l, c);
     return 1;
 }
 
@@ -674,15 +692,42 @@ static void spawn(orc_grid* g, int c) {
     g->spawned++;
 }
 
-/* TaskPool::begin_cycle with workers == 1: FIFO, <= throttle (scheduler.cpp:88-111) */
+/* A coarse_recompute task (solver.cpp:86-90) in the high-priority class. */
+static void spawn_coarse(orc_grid* g, int l, int c) {
+    if (g->htail + 2 > g->hcap) {
+        int64_t live = g->htail - g->hhead;
+        g->hcap = g->hcap ? 2 * g->hcap : 1024;
+        int32_t* q = malloc(g->hcap * sizeof(int32_t));
+        memcpy(q, g->hq + g->hhead, live * sizeof(int32_t));
+        free(g->hq);
+        g->hq = q;
+        g->hhead = 0;
+        g->htail = live;
+    }
+    g->hq[g->htail++] = l;
+    g->hq[g->htail++] = c;
+    g->spawned++;
+}
+
+static int recompute_coarse(orc_grid* g, int l, int c, int* published);
+
+/* TaskPool::begin_cycle with workers == 1: the high class first, then the
+ * leaf tasks, FIFO, <= throttle tasks in all (scheduler.cpp:88-111) */
 static int pool_begin_cycle(orc_grid* g) {
     uint64_t budget = g->d.throttle == 0 ? UINT64_MAX : g->d.throttle;
-    while (g->qhead < g->qtail) {
+    while (g->hhead < g->htail || g->qhead < g->qtail) {
         if (budget == 0) break;
         if (budget != UINT64_MAX) --budget;
-        int c = g->queue[g->qhead++];
-        int rc = adaptive_step(g, c);
-        g->L[g->D].p2[c] = 0;
+        int rc;
+        if (g->hhead < g->htail) {
+            int l = g->hq[g->hhead], c = g->hq[g->hhead + 1], pub;
+            g->hhead += 2;
+            rc = recompute_coarse(g, l, c, &pub);
+        } else {
+            int c = g->queue[g->qhead++];
+            rc = adaptive_step(g, c);
+            g->L[g->D].p2[c] = 0;
+        }
         g->completed++;
         if (rc) return rc;
     }
@@ -748,11 +793,25 @@ static int walk(orc_grid* g, int l, int cx, int cy, visit_fn fn, void* ctx) {
     return 0;
 }
 
-static int visit_assembly(orc_grid* g, int l, int c, void* ctx) {
+/* take_dirty (stream.cpp:247-250): the flag of the current cycle's parity */
+static int take_dirty(orc_grid* g, int l, int c) {
+    uint8_t bit = (uint8_t)(1u << (g->cycle & 1u));
+    int set = (g->L[l].dirty[c] & bit) != 0;
+    g->L[l].dirty[c] &= (uint8_t)~bit;
+    return set;
+}
+
+static int visit_assembly(orc_grid* g, int l, int c, void* ctx) { /* solver.cpp:79-97 */
     (void)ctx;
     if (l < g->D) {
+        if (g->d.policy == LZB_RIPPLE) {
+            if (take_dirty(g, l, c)) spawn_coarse(g, l, c);
+            return 0;
+        }
         int pub;
-        return recompute_coarse(g, l, c, &pub); /* policy always, solver.cpp:83-85 */
+        int rc = recompute_coarse(g, l, c, &pub); /* policy always */
+        take_dirty(g, l, c);                      /* consumed implicitly */
+        return rc;
     }
     return request_stencil(g, c);
 }
@@ -1146,7 +1205,7 @@ int orc_step(orc_grid* g, lzb_cycle_report* rep) {
     }
     g->dof_updates_total += rep->dof_updates;
     rep->dof_updates_total = g->dof_updates_total;
-    rep->pending_tasks = (uint64_t)(g->qtail - g->qhead);
+    rep->pending_tasks = (uint64_t)(g->qtail - g->qhead) + (uint64_t)(g->htail - g->hhead) / 2;
     lzb_compression_stats cs;
     orc_stats(g, &cs);
     rep->max_n = cs.max_n;
