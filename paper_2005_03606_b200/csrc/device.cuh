@@ -535,6 +535,12 @@ struct LevelView {
     int8_t* cp3;
     int cw;
     int fixed_p3;  // > 0: every leaf record at this width (desc.fixed_p3)
+    // coarse-recompute = ripple (solver.cpp:86-90): this level's dirty flags
+    // (bit = cycle parity, stream.cpp:240-260) and pending coarse_recompute
+    // tasks, and the parent level's dirty flags; nullptr with policy always
+    uint32_t* dirty;
+    uint8_t* pend;
+    uint32_t* pdirty;
 };
 
 __device__ inline int32_t crank(const LevelView& L, int cx, int cy) { return L.rx[cx] + L.ry[cy]; }

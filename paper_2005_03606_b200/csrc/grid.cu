@@ -117,6 +117,14 @@ __device__ __forceinline__ void store_planes_rt(const LevelView& F, int c, const
     F.cp3[c] = static_cast<int8_t>(p3);
 }
 
+// CellStream::mark_parent_dirty (stream.cpp:240-245) under ripple: the
+// parent's flag of parity (cycle + 1) & 1, taken by the next cycle's walk.
+__device__ __forceinline__ void mark_parent(const LevelView& L, int64_t c, uint32_t cycle) {
+    if (!L.pdirty) return;
+    const int cx = static_cast<int>(c % L.N), cy = static_cast<int>(c / L.N);
+    atomicOr(L.pdirty + static_cast<int64_t>(cy / 3) * (L.N / 3) + cx / 3, 1u << ((cycle + 1) & 1u));
+}
+
 // CellStream::publish_element (stream.cpp:100-132); caller stores p1.
 __device__ inline bool publish_leaf(const LevelView& F, int c, const double* m, int n, double e_c,
                                     double delta_max, uint32_t cycle, unsigned long long* stats) {
@@ -138,6 +146,7 @@ __device__ inline bool publish_leaf(const LevelView& F, int c, const double* m, 
         rts[k] = rt;
     }
     store_planes_rt(F, c, rts, p3);
+    mark_parent(F, c, cycle);
     atomic_max_double_bits(&stats[S_MAXDELTA], delta);
     atomic_max_u64(&stats[S_MAXSAMPLES], static_cast<unsigned long long>(n));
     F.n[c] = n;
@@ -185,6 +194,7 @@ __device__ inline bool publish_leaf_k9(const LevelView& F, int c, const double* 
         k9_expand(rt9, rt16);
         store_planes_rt(F, c, rt16, p3);
     }
+    mark_parent(F, c, cycle);
     atomic_max_double_bits(&stats[S_MAXDELTA], delta);
     atomic_max_u64(&stats[S_MAXSAMPLES], static_cast<unsigned long long>(n));
     F.n[c] = n;
@@ -498,11 +508,16 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_geo(LevelView C, Leve
     if (c >= static_cast<int64_t>(C.N) * C.N) return;
     const int cx = static_cast<int>(c % C.N), cy = static_cast<int>(c / C.N);
 
-    // policy `always` recomputes every refined cell each cycle (solver.cpp:83-85);
-    // recomputing a patch none of whose children changed since the last attempt
-    // reproduces the stored result bit for bit and publish_coarse would be a
-    // no-op (stream.cpp:153-158), so those patches are skipped
-    {
+    // ripple: only the pending coarse_recompute tasks, each consumed
+    // (solver.cpp:86-90); policy `always` recomputes every refined cell each
+    // cycle (solver.cpp:83-85): recomputing a patch none of whose children
+    // changed since the last attempt reproduces the stored result bit for bit
+    // and publish_coarse would be a no-op (stream.cpp:153-158), so those
+    // patches are skipped
+    if (C.pend) {
+        if (!C.pend[c]) return;
+        C.pend[c] = 0;
+    } else {
         const uint32_t seen = C.seen[c];
         if (seen != 0) {
             uint32_t mx = 0;
@@ -605,6 +620,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_geo(LevelView C, Leve
     C.chg[c] = cycle + 1;
     C.p3[c] = static_cast<int8_t>(p3);
     C.p1[c] = LZB_P1_TOP;
+    mark_parent(C, c, cycle);
 }
 
 // recompute_coarse + publish_coarse with BoxMG transfer (needs the full patch
@@ -617,11 +633,16 @@ __global__ void __launch_bounds__(64) k_coarse(LevelView C, LevelView F, lzb_fie
     if (c >= static_cast<int64_t>(C.N) * C.N) return;
     int cx = static_cast<int>(c % C.N), cy = static_cast<int>(c / C.N);
 
-    // policy `always` recomputes every refined cell each cycle (solver.cpp:83-85);
-    // recomputing a patch none of whose children changed since the last attempt
-    // reproduces the stored result bit for bit and publish_coarse would be a
-    // no-op (stream.cpp:153-158), so those patches are skipped
-    {
+    // ripple: only the pending coarse_recompute tasks, each consumed
+    // (solver.cpp:86-90); policy `always` recomputes every refined cell each
+    // cycle (solver.cpp:83-85): recomputing a patch none of whose children
+    // changed since the last attempt reproduces the stored result bit for bit
+    // and publish_coarse would be a no-op (stream.cpp:153-158), so those
+    // patches are skipped
+    if (C.pend) {
+        if (!C.pend[c]) return;
+        C.pend[c] = 0;
+    } else {
         const uint32_t seen = C.seen[c];
         if (seen != 0) {
             uint32_t mx = 0;
@@ -685,6 +706,7 @@ __global__ void __launch_bounds__(64) k_coarse(LevelView C, LevelView F, lzb_fie
     C.chg[c] = cycle + 1;
     C.p3[c] = static_cast<int8_t>(p3);
     C.p1[c] = LZB_P1_TOP;
+    mark_parent(C, c, cycle);
 }
 
 // ------------------------------------------------------------------ cycle
@@ -1081,6 +1103,7 @@ __global__ void __launch_bounds__(kThreads) k_stats(LevelView L, int leaf, unsig
         const int p3raw = L.p3[c];
         const int p3 = p1 != LZB_P1_BOTTOM ? p3raw : 0;
         bytes += p1 == LZB_P1_BOTTOM ? 1u : 1u + p3 * (leaf ? 16u : 144u);
+        if (!leaf && L.pend) pend += L.pend[c] ? 1u : 0u;  // pending coarse_recompute tasks
         if (leaf) {
             const unsigned n = p1 != LZB_P1_BOTTOM ? static_cast<unsigned>(L.n[c]) : 0u;
             nsum += n;
@@ -1104,18 +1127,33 @@ __global__ void __launch_bounds__(kThreads) k_stats(LevelView L, int leaf, unsig
             const unsigned cnt = __reduce_add_sync(full, h[b]);
             if (lead && cnt) atomicAdd(&sh[S_HIST + b], static_cast<unsigned long long>(cnt));
         }
-        const unsigned wmax = __reduce_max_sync(full, nmax), wp = __reduce_add_sync(full, pend);
+        const unsigned wmax = __reduce_max_sync(full, nmax);
         if (lead) {
             if (bytes) atomicAdd(&sh[S_FINE_BYTES], bytes);
             if (nsum) atomicAdd(&sh[S_NSUM], nsum);
             if (wmax) atomicMax(&sh[S_MAXN], static_cast<unsigned long long>(wmax));
-            if (wp) atomicAdd(&sh[S_PENDING], static_cast<unsigned long long>(wp));
         }
+    }
+    {
+        const unsigned wp = __reduce_add_sync(full, pend);
+        if (lead && wp) atomicAdd(&sh[S_PENDING], static_cast<unsigned long long>(wp));
     }
     __syncthreads();
     if ((threadIdx.x < 13 || threadIdx.x == S_PENDING) && sh[threadIdx.x]) {
         if (threadIdx.x == S_MAXN) atomic_max_u64(&s[S_MAXN], sh[S_MAXN]);
         else atomicAdd(&s[threadIdx.x], sh[threadIdx.x]);
+    }
+}
+
+// The walk's take_dirty (stream.cpp:247-250) for every refined cell of a
+// level: the flag of the current parity spawns a coarse_recompute task.
+__global__ void k_take_dirty(LevelView L, uint32_t cycle) {
+    const int64_t c = gtid();
+    if (c >= static_cast<int64_t>(L.N) * L.N) return;
+    const uint32_t bit = 1u << (cycle & 1u), d = L.dirty[c];
+    if (d & bit) {
+        L.dirty[c] = d & ~bit;
+        L.pend[c] = 1;
     }
 }
 
@@ -1938,6 +1976,8 @@ struct Level {
     DevBuf<uint32_t> epoch, chg, seen;
     DevBuf<uint8_t> cplanes;  // leaf level, plane_width > 0
     DevBuf<int8_t> cp3;
+    DevBuf<uint32_t> dirty;  // refined levels, coarse-recompute = ripple
+    DevBuf<uint8_t> pend;
     LevelView view(int depth) const {
         LevelView L{};
         L.N = N;
@@ -1959,6 +1999,8 @@ struct Level {
         L.has_P = has_P.p;
         L.cplanes = cplanes.p;
         L.cp3 = cp3.p;
+        L.dirty = dirty.p;
+        L.pend = pend.p;
         return L;
     }
 };
@@ -2039,6 +2081,16 @@ public:
         hist_.alloc(kNHist);
         partial_.alloc(kNormBlocks);
         if (d.variant == LZB_ADAFAC_PI && D_ >= 1) caux_.alloc(L_[D_ - 1].nv);
+        if (d.policy == LZB_RIPPLE) {
+            if (d.throttle) throw Error(LZB_ERR_INVALID, "coarse-recompute = ripple runs every task (throttle = 0)");
+            if (d.concurrent) throw Error(LZB_ERR_INVALID, "coarse-recompute = ripple needs the deterministic modes");
+            for (int l = 0; l < D_; ++l) {
+                L_[l].dirty.alloc(L_[l].nc);
+                L_[l].pend.alloc(L_[l].nc);
+                LZB_CUDA(cudaMemsetAsync(L_[l].dirty.p, 0, L_[l].dirty.bytes(), s_));
+                LZB_CUDA(cudaMemsetAsync(L_[l].pend.p, 0, L_[l].pend.bytes(), s_));
+            }
+        }
         if (d.fixed_p3 != 0 && (d.fixed_p3 < 2 || d.fixed_p3 > 8))
             throw Error(LZB_ERR_INVALID, "fixed_p3 must be 0 or 2..8");
         if (d.plane_width != 0) {
@@ -2130,6 +2182,7 @@ public:
             v.cw = d_.plane_width;
             v.fixed_p3 = d_.fixed_p3;
         }
+        if (l > 0) v.pdirty = L_[l - 1].dirty.p;  // nullptr unless ripple
         return v;
     }
     // 2D launch geometry of the vertex kernels: x = column blocks, y = rows
@@ -2234,6 +2287,7 @@ public:
     // TaskPool::drain_all (scheduler.cpp:125-141): finish every pending task.
     void drain() {
         if (d_.concurrent) try_commit(true);
+        if (ripple()) ripple_tasks();  // the high class first (scheduler.cpp:125-141)
         if (d_.mode == LZB_ANARCHIC) {
             while (count_pending() > 0) round(1, true);
         }
@@ -2377,9 +2431,38 @@ public:
         round(1, true, limit);
     }
 
+    bool ripple() const { return d_.policy == LZB_RIPPLE; }
+
+    // The high-priority class of TaskPool::begin_cycle (scheduler.cpp:95-111):
+    // every pending coarse_recompute task, in pre-order = level by level from
+    // the root (siblings are independent; a task reads its children before
+    // their own pending recompute, as the pre-order FIFO does).
+    void ripple_tasks() {
+        *hcycle_ = cycle_;
+        LZB_CUDA(cudaMemcpyAsync(dcycle_.p, hcycle_, sizeof(uint32_t), cudaMemcpyHostToDevice, s_));
+        for (int l = 0; l < D_; ++l) {
+            if (d_.transfer == LZB_BOXMG)
+                LZB_LAUNCH(k_coarse, blocks_for(L_[l].nc, 64), 64, 0, s_, V(l), V(l + 1), d_.field, 1, d_.delta_max,
+                           dcycle_.p, res_.p->s, ctx_->err.p);
+            else
+                LZB_LAUNCH(k_coarse_geo, blocks_for(L_[l].nc, kCoarseThreads), kCoarseThreads, 0, s_, V(l), V(l + 1),
+                           d_.field, d_.delta_max, dcycle_.p, res_.p->s, ctx_->err.p);
+        }
+    }
+    // The walk's refined cells under ripple: take_dirty -> spawn (solver.cpp:86-90).
+    void ripple_walk() {
+        for (int l = 0; l < D_; ++l)
+            LZB_LAUNCH(k_take_dirty, blocks_for(L_[l].nc, kThreads), kThreads, 0, s_, V(l), cycle_);
+    }
+    void begin_cycle_tasks() {
+        if (ripple()) ripple_tasks();
+        pool_begin_cycle();
+    }
+
     void assembly_pass() {  // solver.cpp:79-97
         *hcycle_ = cycle_;
-        coarse_pass();
+        if (ripple()) ripple_walk();
+        else coarse_pass();
         leaves_pass();
     }
 
@@ -2583,9 +2666,10 @@ public:
         ++cycle_;
         *hcycle_ = cycle_;
         if (d_.concurrent) try_commit(false);  // swap in a finished batch before the walk
-        else pool_begin_cycle();
+        else begin_cycle_tasks();
         rep.cycle = static_cast<int32_t>(cycle_);
-        run_graph(g_coarse_, &Grid::coarse_pass);
+        if (ripple()) ripple_walk();
+        else run_graph(g_coarse_, &Grid::coarse_pass);
         leaves_pass();
         if (d_.concurrent && !batch_inflight_ && (cycle_ == 1 || pending_ > 0)) launch_batch();
         ensure_rhs();
@@ -2628,7 +2712,8 @@ public:
     void finish_report(lzb_cycle_report& rep, const Result& r) {
         dof_total_ += rep.dof_updates;
         rep.dof_updates_total = dof_total_;
-        pending_ = d_.mode == LZB_ANARCHIC ? static_cast<int64_t>(r.s[S_PENDING]) : 0;
+        // leaf tasks (anarchic p2) + pending coarse_recompute tasks (ripple)
+        pending_ = static_cast<int64_t>(r.s[S_PENDING]);
         // anarchic: no task pending and nothing bottom means every leaf is top
         // (request_stencil spawns a task for every other leaf)
         if (d_.mode == LZB_ANARCHIC && pending_ == 0 && !batch_inflight_) all_top_ = true;
@@ -2797,7 +2882,7 @@ public:
             case 3: prolong_launches(); sync_check(); return 0.0;
             case 4: inject(); sync_check(); return 0.0;
             case 5: return 0.0;
-            case 6: pool_begin_cycle(); sync_check(); pending_ = count_pending(); return 0.0;
+            case 6: begin_cycle_tasks(); sync_check(); pending_ = count_pending(); return 0.0;
             case 7: drain(); sync_check(); return static_cast<double>(pending_);
             default: throw Error(LZB_ERR_INVALID, "unknown pass");
         }

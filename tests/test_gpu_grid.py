@@ -94,6 +94,24 @@ def test_cycle_bit_identical_to_oracle(f, solver, asm):
     assert g.stream_image() == o.stream_image()
 
 
+RIPPLE = [(f, s, a, t) for f in ["setup = quadrant\neps-low = 0.001", "setup = checkerboard\nfield-seed = 1"]
+          for s in ["additive", "adafac-pi"] for a in ["eager", "adaptive", "anarchic"] for t in ["geometric", "boxmg"]]
+
+
+@pytest.mark.parametrize("f,solver,asm,transfer", RIPPLE)
+def test_ripple_bit_identical_to_oracle(f, solver, asm, transfer):
+    """coarse-recompute = ripple on the device (dirty flags by cycle parity,
+    coarse_recompute tasks in the high-priority class) against the oracle,
+    itself pinned to the unmodified reference (test_oracle_pin.py)."""
+    text = (f"{f}\ndepth = 3\nsolver = {solver}\nassembly = {asm}\nmax-cycles = 10\nomega = 0.6\nrhs = 1\n"
+            f"seed = 42\ncoarse-recompute = ripple\ntransfer = {transfer}\n")
+    g, o, d = grid_pair(text)
+    assert d.policy == lzb.T.RIPPLE
+    assert_reports(g.run(), o.run())
+    assert_state(g, o, d.depth)
+    assert g.stream_image() == o.stream_image()
+
+
 @pytest.mark.parametrize("setup", ["setup = theta\ntheta = 16", "setup = sinusoid"])
 def test_cycle_transcendental_fields_within_tolerance(setup):
     text = f"{setup}\ndepth = 3\nsolver = additive\nassembly = eager\nmax-cycles = 10\nomega = 0.6\nseed = 42\n"
