@@ -205,6 +205,14 @@ int lzb_grid3_init_cycle(lzb_grid3* g, int variant, double omega, double rhs_sca
                          int max_cycles, double target);
 int lzb_grid3_step(lzb_grid3* g, lzb_cycle_report* out);
 int lzb_grid3_vertices(lzb_grid3* g, int level, int field, double* out);  /* (N+1)^3 doubles */
+/* Slab-distributed 3D cycle: z-slabs of leaf vertex planes, coarse levels
+ * replicated; phases 0..5 and exchanges as lzb_grid_dist_phase (driven by
+ * paper_2005_03606_b200/parallel.py dist_cycle3). */
+int lzb_grid3_set_slab(lzb_grid3* g, int v0, int v1);
+int lzb_grid3_dist_phase(lzb_grid3* g, int phase);
+int lzb_grid3_dist_result(lzb_grid3* g, double* norm2);
+int lzb_grid3_dist_report(lzb_grid3* g, double norm2, lzb_cycle_report* out);
+int lzb_grid3_device_view(lzb_grid3* g, int level, int field, void** ptr);
 
 /* -------------------------------------------------------------- experiment */
 /* run_experiment(parse_config_file(path))               experiment.hpp:75,89

@@ -129,6 +129,11 @@ def lib():
         L.lzb_grid3_init_cycle.argtypes = [vp, C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_int, C.c_double]
         L.lzb_grid3_step.argtypes = [vp, C.POINTER(CycleReport)]
         L.lzb_grid3_vertices.argtypes = [vp, C.c_int, C.c_int, vp]
+        L.lzb_grid3_set_slab.argtypes = [vp, C.c_int, C.c_int]
+        L.lzb_grid3_dist_phase.argtypes = [vp, C.c_int]
+        L.lzb_grid3_dist_result.argtypes = [vp, C.POINTER(C.c_double)]
+        L.lzb_grid3_dist_report.argtypes = [vp, C.c_double, C.POINTER(CycleReport)]
+        L.lzb_grid3_device_view.argtypes = [vp, C.c_int, C.c_int, C.POINTER(vp)]
         L.lzb_grid_plane_arrays.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(C.c_int)]
         L.lzb_grid_dist_phase.argtypes = [vp, C.c_int, C.c_int]
         L.lzb_grid_dist_result.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
@@ -603,6 +608,28 @@ class Grid3:
         r = CycleReport()
         _check(lib().lzb_grid3_step(self.h, C.byref(r)))
         return report_dict(r)
+
+    # slab-distributed cycle (parallel.dist_cycle3)
+    def set_slab(self, v0, v1):
+        _check(lib().lzb_grid3_set_slab(self.h, v0, v1))
+
+    def dist_phase(self, phase, flags=0):
+        _check(lib().lzb_grid3_dist_phase(self.h, phase))
+
+    def dist_result(self):
+        n2 = C.c_double()
+        _check(lib().lzb_grid3_dist_result(self.h, C.byref(n2)))
+        return n2.value, [0] * 20
+
+    def dist_report(self, norm2, slots=None) -> dict:
+        r = CycleReport()
+        _check(lib().lzb_grid3_dist_report(self.h, float(norm2), C.byref(r)))
+        return report_dict(r)
+
+    def device_view(self, level, field) -> int:
+        p = C.c_void_p()
+        _check(lib().lzb_grid3_device_view(self.h, level, field, C.byref(p)))
+        return p.value
 
     def vertices(self, level, field):
         n = 3 ** level + 1

@@ -344,13 +344,14 @@ struct Lv3 {
     int N;
     double h;
     double* v[LZB_V_NFIELDS];
-    const double* op;  // 64 per cell
+    const double* op;  // class records, kCls3 per cell
+    int z0;            // first vertex plane of a z-range launch (blockIdx.z + z0)
 };
 
 __device__ __forceinline__ bool vxyz(const Lv3& L, int& ix, int& iy, int& iz, int64_t& vi) {
     ix = blockIdx.x * blockDim.x + threadIdx.x;
     iy = blockIdx.y;
-    iz = blockIdx.z;
+    iz = blockIdx.z + L.z0;
     if (ix > L.N) return false;
     vi = (static_cast<int64_t>(iz) * (L.N + 1) + iy) * (L.N + 1) + ix;
     return true;
@@ -505,13 +506,15 @@ __global__ void k3_restrict(Lv3 F, Lv3 C) {
     C.v[LZB_V_FL][vi] = acc;
 }
 
-__global__ void k3_norm_partial(Lv3 F, double* partial) {
+__global__ void k3_norm_partial(Lv3 F, double* partial, int zlo, int zhi) {
     __shared__ double sh[256];
     const int N = F.N;
     double s = 0.0;
-    const int64_t rows = static_cast<int64_t>(N - 1) * (N - 1);  // interior (y, z) rows
+    // interior (y, z) rows with z in [max(zlo,1), min(zhi,N))
+    const int za = max(zlo, 1), zb = min(zhi, N);
+    const int64_t rows = zb > za ? static_cast<int64_t>(N - 1) * (zb - za) : 0;
     for (int64_t rz = blockIdx.x; rz < rows; rz += gridDim.x) {
-        const int iy = 1 + static_cast<int>(rz % (N - 1)), iz = 1 + static_cast<int>(rz / (N - 1));
+        const int iy = 1 + static_cast<int>(rz % (N - 1)), iz = za + static_cast<int>(rz / (N - 1));
         for (int ix = 1 + threadIdx.x; ix < N; ix += blockDim.x) {
             const double r = F.v[LZB_V_R][vidx3(N, ix, iy, iz)];
             s += r * r;
@@ -888,7 +891,7 @@ public:
         }
         const int ng = L3_[D_].N > 1 ? kNormBlocks3 : 1;
         LZB_CUDA(cudaMemsetAsync(partial3_.p, 0, partial3_.bytes(), s_));
-        if (L3_[D_].N > 1) LZB_LAUNCH(k3_norm_partial, ng, 256, 0, s_, lv(D_), partial3_.p);
+        if (L3_[D_].N > 1) LZB_LAUNCH(k3_norm_partial, ng, 256, 0, s_, lv(D_), partial3_.p, 0, L3_[D_].N + 1);
         std::vector<double> part(kNormBlocks3);
         LZB_CUDA(cudaMemcpyAsync(part.data(), partial3_.p, kNormBlocks3 * sizeof(double), cudaMemcpyDeviceToHost, s_));
         sync();
@@ -920,6 +923,127 @@ public:
         rep.cells = static_cast<uint64_t>(nc_);
         sync();
         return rep;
+    }
+
+    // ---------------------------------------- slab-distributed 3D cycle
+    // The 2D scheme of Grid::dist_phase on z-slabs of leaf vertex planes
+    // [v0, v1) (multiples of 3; the last slab ends at N+1), the coarse levels
+    // replicated; phases 0..5 with the host exchanges in between
+    // (parallel.dist_cycle3): 0 leaf û (slab +-1 plane), residual, norm^2
+    // partial -> r̂ halo (3 planes); 1 restriction into the slab's level-(D-1)
+    // planes -> all-gather fl_{D-1}; 2 residual pass of the coarse levels ->
+    // all-reduce norm^2, report; 3 snapshots, adaFAC-PI injection of the slab's
+    // aux_{D-1} planes -> all-gather; 4 coarse updates, prolongation to D-1,
+    // the slab's leaf aux correction / Jacobi / prolongation, injection of its
+    // u_{D-1} planes -> all-gather; 5 coarse injections -> u halo (1 plane).
+    void set_slab(int v0, int v1) {
+        if (L3_.empty()) throw Error(LZB_ERR_INVALID, "call init_cycle first");
+        const int NV = L3_[D_].N + 1;
+        if (D_ < 1 || v0 < 0 || v1 > NV || v0 >= v1 || v0 % 3 != 0 || (v1 % 3 != 0 && v1 != NV))
+            throw Error(LZB_ERR_INVALID, "bad slab planes");
+        sv0_ = v0;
+        sv1_ = v1;
+    }
+    Lv3 lvz(int l, int z0) const {
+        Lv3 v = lv(l);
+        v.z0 = z0;
+        return v;
+    }
+    dim3 vgz(int l, int z0, int z1) const { return dim3(blocks_for(L3_[l].N + 1, 128), L3_[l].N + 1, z1 - z0); }
+
+    void dist_phase(int phase) {
+        if (L3_.empty()) throw Error(LZB_ERR_INVALID, "call init_cycle first");
+        const int N = L3_[D_].N, v0 = sv0_, v1 = sv1_ < 0 ? N + 1 : sv1_;
+        const int c0 = v0 / 3, c1 = (v1 + 2) / 3;
+        switch (phase) {
+            case 0: {
+                if (ops_dirty_) {
+                    coarse_ops();
+                    ops_dirty_ = false;
+                }
+                ++cycle_;
+                const int u0 = std::max(v0 - 1, 0), u1 = std::min(v1 + 1, N + 1);
+                LZB_LAUNCH(k3_uhat, vgz(D_, u0, u1), 128, 0, s_, lvz(D_, u0), lv(D_ - 1), 1);
+                LZB_LAUNCH(k3_residual, vgz(D_, v0, v1), 128, 0, s_, lvz(D_, v0));
+                LZB_CUDA(cudaMemsetAsync(partial3_.p, 0, partial3_.bytes(), s_));
+                LZB_LAUNCH(k3_norm_partial, kNormBlocks3, 256, 0, s_, lv(D_), partial3_.p, v0, v1);
+                break;
+            }
+            case 1:
+                LZB_LAUNCH(k3_restrict, vgz(D_ - 1, c0, c1), 128, 0, s_, lv(D_), lvz(D_ - 1, c0));
+                break;
+            case 2: {
+                for (int l = D_ - 1; l >= 0; --l) {
+                    LZB_LAUNCH(k3_uhat, vg(l), 128, 0, s_, lv(l), l > 0 ? lv(l - 1) : lv(l), l > 0 ? 1 : 0);
+                    LZB_LAUNCH(k3_residual, vg(l), 128, 0, s_, lv(l));
+                    if (l > 0) LZB_LAUNCH(k3_restrict, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
+                }
+                std::vector<double> part(kNormBlocks3);
+                LZB_CUDA(cudaMemcpyAsync(part.data(), partial3_.p, kNormBlocks3 * sizeof(double),
+                                         cudaMemcpyDeviceToHost, s_));
+                sync();
+                dist_norm2_ = 0.0;
+                for (double x : part) dist_norm2_ += x;
+                break;
+            }
+            case 3:
+                for (int l = 0; l < D_; ++l)
+                    LZB_LAUNCH(k3_snap, blocks_for(L3_[l].nv, 256), 256, 0, s_, lv(l), L3_[l].nv);
+                if (variant_ == LZB_ADAFAC_PI)
+                    LZB_LAUNCH(k3_aux_inject, vgz(D_ - 1, c0, c1), 128, 0, s_, lv(D_), lvz(D_ - 1, c0));
+                break;
+            case 4: {
+                for (int l = D_ - 1; l >= 0; --l) {
+                    if (variant_ == LZB_ADAFAC_PI && l > 0) {
+                        LZB_LAUNCH(k3_aux_inject, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
+                        LZB_LAUNCH(k3_aux_sub, vg(l), 128, 0, s_, lv(l), lv(l - 1), omega_);
+                    }
+                    const double damping = variant_ == LZB_ADDITIVE ? std::pow(omega_, D_ - l + 1) : omega_;
+                    LZB_LAUNCH(k3_jacobi, vg(l), 128, 0, s_, lv(l), damping);
+                }
+                for (int l = 1; l < D_; ++l) LZB_LAUNCH(k3_prolong, vg(l), 128, 0, s_, lv(l), lv(l - 1));
+                // the slab's leaf planes: aux correction, Jacobi, prolongation (the one-GPU order)
+                if (variant_ == LZB_ADAFAC_PI)
+                    LZB_LAUNCH(k3_aux_sub, vgz(D_, v0, v1), 128, 0, s_, lvz(D_, v0), lv(D_ - 1), omega_);
+                LZB_LAUNCH(k3_jacobi, vgz(D_, v0, v1), 128, 0, s_, lvz(D_, v0), omega_);  // damping of level D
+                LZB_LAUNCH(k3_prolong, vgz(D_, v0, v1), 128, 0, s_, lvz(D_, v0), lv(D_ - 1));
+                LZB_LAUNCH(k3_inject, vgz(D_ - 1, c0, c1), 128, 0, s_, lv(D_), lvz(D_ - 1, c0));
+                break;
+            }
+            case 5:
+                for (int l = D_ - 1; l >= 1; --l) LZB_LAUNCH(k3_inject, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
+                sync();
+                break;
+            default: throw Error(LZB_ERR_INVALID, "unknown phase");
+        }
+    }
+
+    double dist_norm2() const { return dist_norm2_; }
+
+    lzb_cycle_report dist_report(double norm2) {
+        lzb_cycle_report rep;
+        std::memset(&rep, 0, sizeof rep);
+        rep.cycle = static_cast<int32_t>(cycle_);
+        rep.residual = std::sqrt(norm2);
+        if (history_.empty()) first_ = rep.residual > 0.0 ? rep.residual : 1.0;
+        history_.push_back(rep.residual);
+        rep.normalized = rep.residual / first_;
+        rep.status = rep.normalized <= target_ ? LZB_CONVERGED
+                     : rep.normalized >= 1e2 ? LZB_DIVERGED
+                     : static_cast<int>(cycle_) >= max_cycles_ ? LZB_TIMEOUT : LZB_CONTINUE;
+        if (rep.status == LZB_CONTINUE || rep.status == LZB_TIMEOUT) {
+            const uint64_t Nf = static_cast<uint64_t>(L3_[D_].N);
+            rep.dof_updates = (Nf - 1) * (Nf - 1) * (Nf - 1);
+        }
+        rep.levels = D_ + 1;
+        rep.cells = static_cast<uint64_t>(nc_);
+        return rep;
+    }
+
+    void* device_field(int level, int field) const {
+        if (L3_.empty() || level < 0 || level > D_ || field < 0 || field >= LZB_V_NFIELDS)
+            throw Error(LZB_ERR_INVALID, "bad level / field");
+        return L3_[level].v[field].p;
     }
 
     void vertices(int level, int field, double* out) {
@@ -966,6 +1090,8 @@ private:
     uint32_t cycle_ = 0;
     bool ops_dirty_ = true;
     std::vector<double> history_;
+    int sv0_ = 0, sv1_ = -1;
+    double dist_norm2_ = 0.0;
 
     Lv3 lv(int l) const {
         Lv3 v{};
@@ -1057,6 +1183,21 @@ int lzb_grid3_step(lzb_grid3* g, lzb_cycle_report* out) {
 }
 int lzb_grid3_vertices(lzb_grid3* g, int level, int field, double* out) {
     return lzb::guarded([&] { g->g->vertices(level, field, out); });
+}
+int lzb_grid3_set_slab(lzb_grid3* g, int v0, int v1) {
+    return lzb::guarded([&] { g->g->set_slab(v0, v1); });
+}
+int lzb_grid3_dist_phase(lzb_grid3* g, int phase) {
+    return lzb::guarded([&] { g->g->dist_phase(phase); });
+}
+int lzb_grid3_dist_result(lzb_grid3* g, double* norm2) {
+    return lzb::guarded([&] { *norm2 = g->g->dist_norm2(); });
+}
+int lzb_grid3_dist_report(lzb_grid3* g, double norm2, lzb_cycle_report* out) {
+    return lzb::guarded([&] { *out = g->g->dist_report(norm2); });
+}
+int lzb_grid3_device_view(lzb_grid3* g, int level, int field, void** ptr) {
+    return lzb::guarded([&] { *ptr = g->g->device_field(level, field); });
 }
 
 }  // extern "C"

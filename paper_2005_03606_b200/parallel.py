@@ -185,9 +185,21 @@ class Slab:
         self.c0, self.c1 = self.v0 // 3, (self.v1 + 2) // 3  # owned rows of level D-1
         grid.set_slab(self.v0, self.v1)
 
+    dims = 2
+
+    def row_elems(self, level: int) -> int:
+        """Elements of one slab unit (a vertex row in 2D, a vertex plane in 3D)."""
+        return (3 ** level + 1) ** (self.dims - 1)
+
     def field(self, level: int, fld: int):
         n = 3 ** level + 1
-        return device_tensor(self.grid.device_view(level, fld), n * n, "<f8")
+        return device_tensor(self.grid.device_view(level, fld), n ** self.dims, "<f8")
+
+
+class Slab3(Slab):
+    """One rank's view of a Grid3: z-slabs of leaf vertex planes."""
+
+    dims = 3
 
 
 def _row_ranges(slabs_or_plan, level_is_coarse: bool):
@@ -208,7 +220,8 @@ class LoopbackComm:
         return torch.cuda.stream(self.stream) if self.stream is not None else contextlib.nullcontext()
 
     def halo(self, slabs, level, fld, depth):
-        n = 3 ** level + 1
+        n = slabs[0].row_elems(level)
+        nrows = 3 ** level + 1
         with self._ctx():
             for i, s in enumerate(slabs):
                 t = s.field(level, fld)
@@ -216,11 +229,11 @@ class LoopbackComm:
                     a = max(s.v0 - depth, 0)
                     t[a * n:s.v0 * n].copy_(slabs[i - 1].field(level, fld)[a * n:s.v0 * n])
                 if i + 1 < len(slabs):
-                    b = min(s.v1 + depth, n)
+                    b = min(s.v1 + depth, nrows)
                     t[s.v1 * n:b * n].copy_(slabs[i + 1].field(level, fld)[s.v1 * n:b * n])
 
     def allgather_rows(self, slabs, level, fld):
-        n = 3 ** level + 1
+        n = slabs[0].row_elems(level)
         with self._ctx():
             for s in slabs:
                 src = s.field(level, fld)[s.c0 * n:s.c1 * n]
@@ -271,7 +284,7 @@ class TorchComm:
     def halo(self, slabs, level, fld, depth):
         (s,) = slabs
         with self._ctx():
-            self.halo_tensor(s.field(level, fld), 3 ** level + 1, s.v0, s.v1, depth)
+            self.halo_tensor(s.field(level, fld), s.row_elems(level), s.v0, s.v1, depth)
 
     def allgather_tensor(self, t, n, ranges):
         """Every rank's rows [r0, r1) of t (n elements per row) into all ranks."""
@@ -297,7 +310,7 @@ class TorchComm:
             v0, v1 = slab_vertex_rows(s.N, world, r)
             ranges.append((v0 // 3, (v1 + 2) // 3))
         with self._ctx():
-            self.allgather_tensor(s.field(level, fld), 3 ** level + 1, ranges)
+            self.allgather_tensor(s.field(level, fld), s.row_elems(level), ranges)
 
     def reduce(self, results, device=None):
         import torch
@@ -345,4 +358,36 @@ def dist_cycle(slabs, comm, adafac_pi: bool) -> dict:
         for s in slabs:
             s.grid.dist_phase(5)
         comm.halo(slabs, D, V.V_U, 1)                   # leaf u one row beyond the slab
+    return rep
+
+
+def dist_cycle3(slabs, comm, adafac_pi: bool) -> dict:
+    """One slab-distributed 3D cycle (Grid3.dist_phase 0..5 with the exchanges
+    in between, z-slabs of vertex planes); returns the cycle report."""
+    import paper_2005_03606_b200 as lzb
+
+    V = lzb.T
+    D = slabs[0].D
+    for s in slabs:
+        s.grid.dist_phase(0)
+    comm.halo(slabs, D, V.V_RHAT, 3)
+    for s in slabs:
+        s.grid.dist_phase(1)
+    comm.allgather_rows(slabs, D - 1, V.V_FL)
+    for s in slabs:
+        s.grid.dist_phase(2)
+    norm2, _ = comm.reduce([s.grid.dist_result() for s in slabs])
+    reps = [s.grid.dist_report(norm2) for s in slabs]
+    rep = reps[0]
+    if rep["status"] in (V.CONTINUE, V.TIMEOUT):
+        for s in slabs:
+            s.grid.dist_phase(3)
+        if adafac_pi:
+            comm.allgather_rows(slabs, D - 1, V.V_AUX)
+        for s in slabs:
+            s.grid.dist_phase(4)
+        comm.allgather_rows(slabs, D - 1, V.V_U)
+        for s in slabs:
+            s.grid.dist_phase(5)
+        comm.halo(slabs, D, V.V_U, 1)
     return rep
