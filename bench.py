@@ -421,9 +421,42 @@ def run_ours(args, world, rank, local):
         c5["cycles"] = {"mode": "one GPU"}
     t5c = max_over_ranks(t5c, world)
     c5["cycles"].update({"ms_per_cycle": 1e3 * t5c, "dof_updates_per_s": (3 ** 6 - 1) ** 3 / t5c})
+    nv5, nc5 = (3 ** 6 + 1) ** 3, 3 ** 18
+    if world == 1:
+        # the leaf residual (k3_residual_z, cell-centric z-march over FP64 class planes)
+        # against HBM: 48 B per vertex (fl, u, û read; r, r̂, diag written) + 216 B per cell
+        tr5 = g5.time_kernel(lzb.TK_RESIDUAL, 3)
+        ab5 = nv5 * 48 + nc5 * 216
+        c5["residual_roofline"] = {"bound": "hbm", "kernel": "k3_residual_z", "ms": tr5, "algorithmic_bytes": ab5,
+                                   "achieved": ab5 / tr5 / 1e6, "peak": hbm_peak, "unit": "GB/s",
+                                   "frac": ab5 / tr5 / 1e6 / hbm_peak, "traffic": traffic_of("k3_residual_z")}
     g5.close()
     del g5
     torch.cuda.empty_cache()
+    if world == 1:
+        # BASELINE configs[4] mantissa-width sweep at 729^3: the leaf operators held only
+        # as compressed class planes of W = p3 bytes per class value (+ eps(centre), p3),
+        # decoded by the residual and the Galerkin product; bit-identical operators
+        c5["width_sweep"] = []
+        for w5 in (2, 3, 4, 5, 6, 7, 8):
+            gw5 = lzb.Grid3(6, lzb.field3_grf(lzb.grf_table(1, 64, 0.05, 1.0)), delta_max=1e-8, fixed_p3=w5,
+                            plane_width=w5, ctx=ctx)
+            gw5.assemble_fixed(2)
+            stw5 = gw5.stats()
+            gw5.init_cycle(solver="adafac-pi", omega=0.6, max_cycles=10 ** 6)
+            gw5.step()  # builds the coarse operators from the decoded planes
+            trw = gw5.time_kernel(lzb.TK_RESIDUAL, 3)
+            tcw = timed_steps(lambda: gw5.step(), 2) / 2
+            abw = nv5 * 48 + nc5 * gw5.leaf_bytes_per_cell()
+            c5["width_sweep"].append({
+                "p3": w5, "mantissa_bits": measure.MANTISSA_BITS[w5],
+                "lzmg_bytes_per_cell": stw5.fine_stored_bytes / stw5.fine_cells,
+                "resident_bytes_per_cell": gw5.leaf_bytes_per_cell(), "max_abs_error": stw5.max_delta,
+                "residual_ms": trw, "residual_GBs": abw / trw / 1e6, "ms_per_cycle": 1e3 * tcw,
+                "dof_updates_per_s": (3 ** 6 - 1) ** 3 / tcw})
+            gw5.close()
+            del gw5
+            torch.cuda.empty_cache()
 
     # strong-scaling slab decomposition (§8e): each rank assembles 1/world of the rows,
     # then one all-gather of the leaf state (NCCL) makes the operator replicated

@@ -191,6 +191,13 @@ typedef struct lzb_grid3 lzb_grid3;
  * fixed-p assembly + compression (fixed_p3 = 0: choose_precision per record). */
 int lzb_grid3_create(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3,
                      lzb_grid3** out);
+/* The same with the leaf operators held only as compressed class planes of
+ * plane_width W bytes per class value (2..8; 0 = FP64 class planes): the
+ * residual and the Galerkin product decode them (BASELINE configs[4] width
+ * sweep). A record whose p3 exceeds W fails the assembly with
+ * LZB_ERR_RESOURCE. Restated 3D form of stream.cpp:82-111 + solver.cpp:145-175. */
+int lzb_grid3_create_planes(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3,
+                            int plane_width, lzb_grid3** out);
 int lzb_grid3_destroy(lzb_grid3* g);
 int lzb_grid3_assemble_fixed(lzb_grid3* g, int n);
 int lzb_grid3_stats(lzb_grid3* g, lzb_compression_stats* out);
@@ -212,6 +219,8 @@ int lzb_grid3_set_slab(lzb_grid3* g, int v0, int v1);
 int lzb_grid3_dist_phase(lzb_grid3* g, int phase);
 int lzb_grid3_dist_result(lzb_grid3* g, double* norm2);
 int lzb_grid3_dist_report(lzb_grid3* g, double norm2, lzb_cycle_report* out);
+/* Average device ms of one leaf-level 3D cycle kernel (LZB_TK_UHAT .. LZB_TK_PROLONG). */
+int lzb_grid3_time_kernel(lzb_grid3* g, int what, int reps, double* avg_ms);
 int lzb_grid3_device_view(lzb_grid3* g, int level, int field, void** ptr);
 
 /* -------------------------------------------------------------- experiment */

@@ -122,6 +122,8 @@ def lib():
         L.lzb_grf_table.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, vp]
         L.lzb_integrate_elements3.argtypes = [vp, C.POINTER(T.Field3), i64, vp, vp, vp, vp, vp, vp]
         L.lzb_grid3_create.argtypes = [vp, C.c_int, C.POINTER(T.Field3), C.c_double, C.c_int, C.POINTER(vp)]
+        L.lzb_grid3_create_planes.argtypes = [vp, C.c_int, C.POINTER(T.Field3), C.c_double, C.c_int, C.c_int,
+                                               C.POINTER(vp)]
         L.lzb_grid3_destroy.argtypes = [vp]
         L.lzb_grid3_assemble_fixed.argtypes = [vp, C.c_int]
         L.lzb_grid3_stats.argtypes = [vp, C.POINTER(CompressionStats)]
@@ -133,6 +135,7 @@ def lib():
         L.lzb_grid3_dist_phase.argtypes = [vp, C.c_int]
         L.lzb_grid3_dist_result.argtypes = [vp, C.POINTER(C.c_double)]
         L.lzb_grid3_dist_report.argtypes = [vp, C.c_double, C.POINTER(CycleReport)]
+        L.lzb_grid3_time_kernel.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.lzb_grid3_device_view.argtypes = [vp, C.c_int, C.c_int, C.POINTER(vp)]
         L.lzb_grid_plane_arrays.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(C.c_int)]
         L.lzb_grid_dist_phase.argtypes = [vp, C.c_int, C.c_int]
@@ -575,13 +578,26 @@ class Grid3:
     """Leaves of a regular 3D grid (3^depth cells per axis): fixed-p assembly
     with the 64-entry record coding (lzb_grid3_*)."""
 
-    def __init__(self, depth, field, delta_max=1e-8, fixed_p3=0, ctx: Context | None = None):
+    def __init__(self, depth, field, delta_max=1e-8, fixed_p3=0, plane_width=0, ctx: Context | None = None):
         self.ctx = ctx or default_context()
         self.depth, self.field = depth, field
         self.N = 3 ** depth
+        self.plane_width = plane_width
         h = C.c_void_p()
-        _check(lib().lzb_grid3_create(self.ctx.h, depth, C.byref(field), delta_max, fixed_p3, C.byref(h)))
+        _check(lib().lzb_grid3_create_planes(self.ctx.h, depth, C.byref(field), delta_max, fixed_p3, plane_width,
+                                             C.byref(h)))
         self.h = h
+
+    def time_kernel(self, what, reps=10) -> float:
+        """Average device ms of one leaf-level cycle kernel (TK_* id), CUDA events on the solve stream."""
+        ms = C.c_double()
+        _check(lib().lzb_grid3_time_kernel(self.h, what, reps, C.byref(ms)))
+        return ms.value
+
+    def leaf_bytes_per_cell(self) -> int:
+        """Resident bytes of one leaf operator: 27 FP64 class values, or 27
+        plane words of plane_width bytes + eps(centre) + p3."""
+        return 27 * 8 if not self.plane_width else 27 * self.plane_width + 8 + 1
 
     def close(self):
         if getattr(self, "h", None):

@@ -235,12 +235,14 @@ __host__ __device__ __forceinline__ int cls3(int a, int b) {
     const int ax = a & 1, ay = (a >> 1) & 1, az = a >> 2, bx = b & 1, by = (b >> 1) & 1, bz = b >> 2;
     return 9 * (ax == bx ? 2 * ax : 1) + 3 * (ay == by ? 2 * ay : 1) + (az == bz ? 2 * az : 1);
 }
-// Operators in HBM are class records: the 27 class values (padded to 28 for
-// 16-B stores), 224 B per cell instead of 512 — trilinear operators built
-// from tensor products of symmetric per-axis 2x2 matrices (the elements here
-// and their Galerkin products with the tensor-product P) take one value per
-// class for any eps.
-constexpr int kCls3 = 28;
+// Operators in HBM are class planes: the 27 class values of a cell (the
+// distinct values of its 8x8 matrix; trilinear operators built from tensor
+// products of symmetric per-axis 2x2 matrices — the elements here and their
+// Galerkin products with the tensor-product P — take one value per class for
+// any eps), stored plane by plane, value q of cell c at q * nc + c: 216 B per
+// cell instead of 512, and the per-vertex gathers of the cycle read whole
+// 128-B lines across a warp (consecutive vertices, consecutive cells).
+constexpr int kCls3 = 27;
 
 // The 64 entries of a trilinear element take 27 values: entry (a, b)
 // depends only on the per-axis pair classes (c = 0: both 0, 1: different,
@@ -249,6 +251,127 @@ __device__ __forceinline__ double class_value(const Acc3& A, double hn, int cx, 
     const double sx = cx == 1 ? -1.0 : 1.0, sy = cy == 1 ? -1.0 : 1.0, sz = cz == 1 ? -1.0 : 1.0;
     return hn * (sx * A.yz[cy * 3 + cz] + sy * A.xz[cx * 3 + cz] + sz * A.xy[cx * 3 + cy]);
 }
+
+// eps at the n = 1 sample of a cell, evaluated exactly as accumulate3 does at
+// n = 1 (the GrfCell path for GRF cells smaller than a table spacing).
+__device__ __forceinline__ double centre_eps3(const Field3& F, double x0, double y0, double z0, double h) {
+    const double inv = 1.0 / 1;
+    const double x = x0 + (0 + 0.5) * inv * h, y = y0 + (0 + 0.5) * inv * h, z = z0 + (0 + 0.5) * inv * h;
+    if (F.kind == LZB_F3_GRF && h * F.n < 1.0) {
+        GrfCell G3(F, x0, y0, z0);
+        G3.set_x(x);
+        G3.set_y(y);
+        return G3.eps(z);
+    }
+    return eps3(F, x, y, z);
+}
+
+// A(n=1) in class form from eps(centre): at n = 1 the three class sums of
+// accumulate3 are all M[a][b] = s_a (e s_b) (every "0 +" of the loop is exact
+// for these positive terms), so class (cx, cy, cz) is
+// h (sx M[cy][cz] + sy M[cx][cz] + sz M[cx][cy]) — the bits of class_value on
+// the n = 1 sums. The stream baseline (stream.cpp:82-84 in 3D), rebuilt by
+// the compressed-plane readers from the stored eps(centre).
+struct Base3 {
+    double m[3][3];
+    double h;
+    __device__ __forceinline__ Base3(double e, const double* s, double h_) : h(h_) {
+        double es[3];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) es[b] = e * s[b];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) m[a][b] = s[a] * es[b];
+    }
+    __device__ __forceinline__ double operator()(int cx, int cy, int cz) const {
+        const double tx = cx == 1 ? -m[cy][cz] : m[cy][cz];
+        const double ty = cy == 1 ? -m[cx][cz] : m[cx][cz];
+        const double tz = cz == 1 ? -m[cx][cy] : m[cx][cy];
+        return h * (tx + ty + tz);
+    }
+};
+
+// ---- compressed class planes (plane_width W > 0, BASELINE configs[4])
+// Class q of a leaf is held as the W-byte plane word (grid.cu plane_word) of
+// rt = roundtrip(surplus_q, p3): lossless at any W >= p3 (rt has at most the
+// m(p3) fraction bits), decoded with the compile-time constants of W. The
+// word is split into power-of-two pieces (8 | 4, 2, 1 bytes), each piece an
+// array of 27 planes of nc words, so a warp reads 2..8 consecutive bytes per
+// cell per piece. The stored operator is Base3(eps centre) + rt, bit for bit
+// the FP64 class value (k_assemble3 stores exactly that).
+struct Planes3 {
+    uint8_t* base;  // piece arrays back to back, largest piece first
+    double* ec;     // eps at the cell centre
+    int64_t nc;
+    double h;
+    double s1[3];  // seg_int classes of the n = 1 sub-interval
+};
+
+template <int W>
+__device__ __forceinline__ unsigned long long plane_load3(const Planes3& P, int64_t c, int q) {
+    const int64_t i = q * P.nc + c;
+    if (W == 8) return __ldg(reinterpret_cast<const unsigned long long*>(P.base) + i);
+    unsigned long long w = 0;
+    int64_t off = 0;
+    int sh = 0;
+    if (W & 4) {
+        w = __ldg(reinterpret_cast<const uint32_t*>(P.base) + i);
+        off += 4 * 27 * P.nc;
+        sh = 32;
+    }
+    if (W & 2) {
+        w |= static_cast<unsigned long long>(__ldg(reinterpret_cast<const uint16_t*>(P.base + off) + i)) << sh;
+        off += 2 * 27 * P.nc;
+        sh += 16;
+    }
+    if (W & 1) w |= static_cast<unsigned long long>(__ldg(P.base + off + i)) << sh;
+    return w;
+}
+__device__ __forceinline__ void plane_store3(const Planes3& P, int W, int64_t c, int q, unsigned long long w) {
+    const int64_t i = q * P.nc + c;
+    if (W == 8) {
+        reinterpret_cast<unsigned long long*>(P.base)[i] = w;
+        return;
+    }
+    int64_t off = 0;
+    if (W & 4) {
+        reinterpret_cast<uint32_t*>(P.base)[i] = static_cast<uint32_t>(w);
+        w >>= 32;
+        off += 4 * 27 * P.nc;
+    }
+    if (W & 2) {
+        reinterpret_cast<uint16_t*>(P.base + off)[i] = static_cast<uint16_t>(w);
+        w >>= 16;
+        off += 2 * 27 * P.nc;
+    }
+    if (W & 1) P.base[off + i] = static_cast<uint8_t>(w);
+}
+
+// Leaf class sources of the cycle kernels: FP64 planes, or compressed planes
+// at width W (27 values of one cell: load(c, out)).
+struct Src64 {
+    const double* op;
+    int64_t nc;
+    __device__ __forceinline__ double at(int64_t c, int q) const { return __ldg(op + q * nc + c); }
+    __device__ __forceinline__ void load27(int64_t c, double* v) const {
+#pragma unroll
+        for (int q = 0; q < 27; ++q) v[q] = at(c, q);
+    }
+};
+template <int W>
+struct SrcComp {
+    Planes3 P;
+    __device__ __forceinline__ void load27(int64_t c, double* v) const {
+        unsigned long long w[27];
+#pragma unroll
+        for (int q = 0; q < 27; ++q) w[q] = plane_load3<W>(P, c, q);
+        const Base3 B(__ldg(P.ec + c), P.s1, P.h);
+        const PlaneDec dec(W);
+#pragma unroll
+        for (int q = 0; q < 27; ++q) v[q] = B(q / 9, (q / 3) % 3, q % 3) + dec(w[q]);
+    }
+};
 
 // choose_precision over a record's distinct values (duplicates never change
 // it), all indices compile-time so the values stay in registers; the same
@@ -260,24 +383,24 @@ __device__ __noinline__ int choose_precision_set(const double* v, double delta) 
 
 // Fixed-p assembly of every cell of a 3D level: integrate at n, code the
 // record against the n = 1 element (stream.cpp:82-111 in 3D), store the
-// decoded operator, width and n. One thread per cell; the record's 27
-// distinct surplus values are coded once and written to their 64 positions.
-__global__ void __launch_bounds__(128) k_assemble3(Field3 F, int N, double h, AxisTab3 T, AxisTab3 T1,
-                                                   double delta_max, int fixed_p3, double* __restrict__ op,
+// decoded operator (FP64 class planes, or eps(centre) + the compressed
+// planes of width W), width and n. One thread per cell; the record's 27
+// distinct surplus values are coded once (they stand for its 64 entries).
+__global__ void __launch_bounds__(128) k_assemble3(Field3 F, int N, double h, AxisTab3 T, double delta_max,
+                                                   int fixed_p3, double* __restrict__ op, Planes3 PL, int W,
                                                    int8_t* __restrict__ p3o, int32_t* __restrict__ no,
-                                                   unsigned long long* stats, int* err) {
+                                                   unsigned long long* stats, int* err, int* wide) {
     const int64_t c = gtid();
     const int64_t nc = static_cast<int64_t>(N) * N * N;
     if (c >= nc) return;
     const int cx = static_cast<int>(c % N), cy = static_cast<int>((c / N) % N), cz = static_cast<int>(c / N / N);
     const double x0 = cx * h, y0 = cy * h, z0 = cz * h;
     double base[27], sur[27];
+    const double e = centre_eps3(F, x0, y0, z0, h);
     {
-        Acc3 B;
-        accumulate3(F, x0, y0, z0, h, T1, B);  // A(n=1): eps(centre) * unit stiffness
-        const double h1 = h * (1.0 / 1);
+        const Base3 B(e, PL.s1, h);  // A(n=1): eps(centre) * unit stiffness
 #pragma unroll
-        for (int q = 0; q < 27; ++q) base[q] = class_value(B, h1, q / 9, (q / 3) % 3, q % 3);
+        for (int q = 0; q < 27; ++q) base[q] = B(q / 9, (q / 3) % 3, q % 3);
     }
     {
         Acc3 A;
@@ -291,7 +414,7 @@ __global__ void __launch_bounds__(128) k_assemble3(Field3 F, int N, double h, Ax
         atomicExch(err, 1);
         return;
     }
-    double delta = 0.0, dec[27];
+    double delta = 0.0, rts[27];
 #pragma unroll
     for (int q = 0; q < 27; ++q) {
         double rt;
@@ -301,15 +424,32 @@ __global__ void __launch_bounds__(128) k_assemble3(Field3 F, int N, double h, Ax
         }
         const double d = fabs(rt - sur[q]);
         delta = delta < d ? d : delta;
-        dec[q] = base[q] + rt;
+        rts[q] = rt;
     }
-    double2* o = reinterpret_cast<double2*>(op + kCls3 * c);
+    if (W == 0) {
 #pragma unroll
-    for (int q = 0; q < 26; q += 2) o[q >> 1] = make_double2(dec[q], dec[q + 1]);
-    o[13] = make_double2(dec[26], 0.0);
+        for (int q = 0; q < 27; ++q) op[q * nc + c] = base[q] + rts[q];
+    } else if (p3 > W) {
+        atomicExch(wide, 1);  // record wider than the planes
+    } else {
+        PL.ec[c] = e;
+#pragma unroll
+        for (int q = 0; q < 27; ++q) plane_store3(PL, W, c, q, plane_word(rts[q], W));
+    }
     p3o[c] = static_cast<int8_t>(p3);
     no[c] = T.n;
     atomic_max_double_bits(&stats[S_MAXDELTA], delta);
+}
+
+// The 27 class values of cells [first, first + count) (AoS, 27 per cell).
+template <class Src>
+__global__ void k3_read_cls(Src S, int64_t first, int64_t count, double* __restrict__ out) {
+    const int64_t t = gtid();
+    if (t >= count) return;
+    double v[27];
+    S.load27(first + t, v);
+#pragma unroll
+    for (int q = 0; q < 27; ++q) out[27 * t + q] = v[q];
 }
 
 __global__ void k_stats3(const int8_t* __restrict__ p3, int64_t nc, unsigned long long* s) {
@@ -362,9 +502,14 @@ __device__ __forceinline__ bool bnd3(int N, int ix, int iy, int iz) {
 __device__ __forceinline__ int64_t vidx3(int N, int x, int y, int z) {
     return (static_cast<int64_t>(z) * (N + 1) + y) * (N + 1) + x;
 }
+// k / 27 for the integer weight products k = 0..27 (the divisions of the
+// trilinear lattice weights, tabulated: the same correctly rounded quotients)
+__device__ const double g_w27[28] = {
+    0 / 27.0,  1 / 27.0,  2 / 27.0,  3 / 27.0,  4 / 27.0,  5 / 27.0,  6 / 27.0,  7 / 27.0,  8 / 27.0,  9 / 27.0,
+    10 / 27.0, 11 / 27.0, 12 / 27.0, 13 / 27.0, 14 / 27.0, 15 / 27.0, 16 / 27.0, 17 / 27.0, 18 / 27.0, 19 / 27.0,
+    20 / 27.0, 21 / 27.0, 22 / 27.0, 23 / 27.0, 24 / 27.0, 25 / 27.0, 26 / 27.0, 27 / 27.0};
 __device__ __forceinline__ double pw3(int lx, int ly, int lz, int a) {
-    return static_cast<double>(((a & 1) ? lx : 3 - lx) * (((a >> 1) & 1) ? ly : 3 - ly) * ((a >> 2) ? lz : 3 - lz)) /
-           27.0;
+    return g_w27[((a & 1) ? lx : 3 - lx) * (((a >> 1) & 1) ? ly : 3 - ly) * ((a >> 2) ? lz : 3 - lz)];
 }
 __device__ __forceinline__ int owner3(int f, int Nc) {
     const int x1 = f / 3;
@@ -428,53 +573,112 @@ __global__ void k3_uhat(Lv3 F, Lv3 C, int has_coarse) {
     F.v[LZB_V_UHAT][vi] = u - interp;
 }
 
-// r, r̂, diag per vertex, gathered over the 8 adjacent cells in (z, y, x)
-// order; the 3x3x3 u / û neighbourhood and the 8 class values of the
-// vertex's row in each cell are all loaded before use.
-__global__ void __launch_bounds__(128) k3_residual(Lv3 F) {
-    int ix, iy, iz;
-    int64_t vi;
-    if (!vxyz(F, ix, iy, iz, vi)) return;
-    const int N = F.N;
-    double uu[27], uh[27];
+// r, r̂, diag per vertex over the 8 adjacent cells in (z, y, x) order
+// (solver.cpp:145-175 restated), cell-centric and z-marching: a block owns a tile of
+// 31 x 7 vertex columns and a range of vertex planes; per cell layer every
+// thread loads one cell's 27 class values (decoded once, not once per
+// adjacent vertex), forms the 8 row products K_a. u and K_a. û of the 8x8
+// operator and its diagonal, and stages them in shared memory; the vertex
+// threads then subtract them in the gather kernel's order (cells q = dx +
+// 2 dy + 4 dz: the 4 cells below a vertex plane while the previous layer is
+// staged, the 4 above in this layer) — the per-vertex gather's order. The
+// u / û corners of the layer below stay in registers.
+constexpr int kRzX = 32, kRzY = 8, kRzChunk = 32;
+template <class Src>
+__global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_z(Lv3 F, Src S, int zbeg, int zend) {
+    __shared__ double sy[3][8][kRzX * kRzY];  // [u, û, diag][corner][cell of the tile]
+    const int tx = threadIdx.x % kRzX, ty = threadIdx.x / kRzX, t = threadIdx.x;
+    const int N = F.N, NV = N + 1;
+    const int X0 = blockIdx.x * (kRzX - 1), Y0 = blockIdx.y * (kRzY - 1);
+    const int zs = zbeg + blockIdx.z * kRzChunk, ze = min(zs + kRzChunk, zend);
+    if (zs >= ze) return;
+    const int cx = X0 - 1 + tx, cy = Y0 - 1 + ty;  // this thread's cell column
+    const bool colok = cx >= 0 && cy >= 0 && cx < N && cy < N;
+    const int ix = X0 + tx, iy = Y0 + ty;  // this thread's vertex column (tx < 31, ty < 7)
+    const bool vthr = tx < kRzX - 1 && ty < kRzY - 1 && ix <= N && iy <= N;
+    const double* __restrict__ U = F.v[LZB_V_U];
+    const double* __restrict__ UH = F.v[LZB_V_UHAT];
+    auto vid = [&](int x, int y, int z) {
+        return (static_cast<int64_t>(min(max(z, 0), N)) * NV + min(max(y, 0), N)) * NV + min(max(x, 0), N);
+    };
+    double ul[4], uhl[4];  // corners of the current layer's lower plane
 #pragma unroll
-    for (int d = 0; d < 27; ++d) {
-        const int x = min(max(ix - 1 + d % 3, 0), N), y = min(max(iy - 1 + (d / 3) % 3, 0), N),
-                  z = min(max(iz - 1 + d / 9, 0), N);
-        const int64_t cv = vidx3(N, x, y, z);
-        uu[d] = F.v[LZB_V_U][cv];
-        uh[d] = F.v[LZB_V_UHAT][cv];
+    for (int k = 0; k < 4; ++k) {
+        const int64_t v = vid(cx + (k & 1), cy + (k >> 1), zs - 1);
+        ul[k] = U[v];
+        uhl[k] = UH[v];
     }
-    const double fl = F.v[LZB_V_FL][vi];
-    double r = fl, rh = fl, dg = 0.0;
+    double rp = 0.0, rhp = 0.0, dgp = 0.0;  // partial sums of the vertex plane being completed
+    for (int cz = zs - 1; cz < ze; ++cz) {
+        // 1. this thread's cell of layer cz: row products into shared memory
+        double uu[8], uh[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;  // cell (ix-1+dx, ...)
-        const int cx = ix - 1 + dx, cy = iy - 1 + dy, cz = iz - 1 + dz;
-        if (cx < 0 || cy < 0 || cz < 0 || cx >= N || cy >= N || cz >= N) continue;
-        const int row = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
-        const double* K = F.op + kCls3 * ((static_cast<int64_t>(cz) * N + cy) * N + cx);
-        double k8[8];
-#pragma unroll
-        for (int col = 0; col < 8; ++col) k8[col] = __ldg(K + cls3(row, col));
-        double au = 0.0, auh = 0.0;
-#pragma unroll
-        for (int col = 0; col < 8; ++col) {
-            const int d = (dz + (col >> 2)) * 9 + (dy + ((col >> 1) & 1)) * 3 + dx + (col & 1);
-            au += k8[col] * uu[d];
-            auh += k8[col] * uh[d];
+        for (int k = 0; k < 4; ++k) {
+            uu[k] = ul[k];
+            uh[k] = uhl[k];
+            const int64_t v = vid(cx + (k & 1), cy + (k >> 1), cz + 1);
+            uu[4 + k] = U[v];
+            uh[4 + k] = UH[v];
+            ul[k] = uu[4 + k];
+            uhl[k] = uh[4 + k];
         }
-        r -= au;
-        rh -= auh;
-        dg += k8[row];
+        const bool ok = colok && cz >= 0 && cz < N;
+        if (ok) {
+            double K[27];
+            S.load27((static_cast<int64_t>(cz) * N + cy) * N + cx, K);
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+                double au = 0.0, auh = 0.0;
+#pragma unroll
+                for (int col = 0; col < 8; ++col) {  // explicit FMA (the 3D cycle is restated, not pinned bitwise)
+                    au = __fma_rn(K[cls3(a, col)], uu[col], au);
+                    auh = __fma_rn(K[cls3(a, col)], uh[col], auh);
+                }
+                sy[0][a][t] = au;
+                sy[1][a][t] = auh;
+                sy[2][a][t] = K[cls3(a, a)];
+            }
+        }
+        __syncthreads();
+        // 2. vertex threads: plane cz (cells above it, q = 4..7) is completed,
+        // plane cz + 1 starts (cells below it, q = 0..3)
+        if (vthr) {
+            auto sub = [&](int q, double& r, double& rh, double& dg) {
+                const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;
+                const int row = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
+                const int ccx = ix - 1 + dx, ccy = iy - 1 + dy;
+                if (ccx < 0 || ccy < 0 || ccx >= N || ccy >= N) return;
+                const int c = (ty + dy) * kRzX + tx + dx;
+                r -= sy[0][row][c];
+                rh -= sy[1][row][c];
+                dg += sy[2][row][c];
+            };
+            if (cz >= zs && cz < N) {  // layer cz lies above plane cz
+#pragma unroll
+                for (int q = 4; q < 8; ++q) sub(q, rp, rhp, dgp);
+            }
+            if (cz >= zs) {
+                double r = rp, rh = rhp;
+                if (bnd3(N, ix, iy, cz)) {
+                    r = 0.0;
+                    rh = 0.0;
+                }
+                const int64_t vi = (static_cast<int64_t>(cz) * NV + iy) * NV + ix;
+                F.v[LZB_V_R][vi] = r;
+                F.v[LZB_V_RHAT][vi] = rh;
+                F.v[LZB_V_DIAG][vi] = dgp;
+            }
+            if (cz + 1 < ze) {  // plane cz + 1: fl, then the cells of layer cz below it
+                rp = rhp = F.v[LZB_V_FL][(static_cast<int64_t>(cz + 1) * NV + iy) * NV + ix];
+                dgp = 0.0;
+                if (cz >= 0) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) sub(q, rp, rhp, dgp);
+                }
+            }
+        }
+        __syncthreads();
     }
-    if (bnd3(N, ix, iy, iz)) {
-        r = 0.0;
-        rh = 0.0;
-    }
-    F.v[LZB_V_R][vi] = r;
-    F.v[LZB_V_RHAT][vi] = rh;
-    F.v[LZB_V_DIAG][vi] = dg;
 }
 
 // fl_c = P^T r̂ over owned lattice points (adjacent patches in (z, y, x)
@@ -604,13 +808,15 @@ __global__ void k3_inject(Lv3 F, Lv3 C) {
 // representative entry of class q. W (27^3 values) is a constant of the
 // trilinear transfer: computed once on the host, staged in shared memory.
 constexpr int kW3 = 27 * 27 * 27;
-__global__ void __launch_bounds__(256) k3_galerkin(double* __restrict__ cop, const double* __restrict__ fop, int Nc,
+template <class Src>
+__global__ void __launch_bounds__(256) k3_galerkin(double* __restrict__ cop, Src S, int Nc,
                                                    const double* __restrict__ W) {
     extern __shared__ double sW[];
     for (int i = threadIdx.x; i < kW3; i += blockDim.x) sW[i] = W[i];
     __syncthreads();
     const int64_t c = gtid();
-    if (c >= static_cast<int64_t>(Nc) * Nc * Nc) return;
+    const int64_t ncc = static_cast<int64_t>(Nc) * Nc * Nc;
+    if (c >= ncc) return;
     const int px = static_cast<int>(c % Nc), py = static_cast<int>((c / Nc) % Nc), pz = static_cast<int>(c / Nc / Nc);
     const int Nf = 3 * Nc;
     double out[27];
@@ -618,18 +824,18 @@ __global__ void __launch_bounds__(256) k3_galerkin(double* __restrict__ cop, con
     for (int q = 0; q < 27; ++q) out[q] = 0.0;
     for (int ch = 0; ch < 27; ++ch) {  // child (lz, ly, lx) = (ch / 9, (ch / 3) % 3, ch % 3)
         const int lz = ch / 9, ly = (ch / 3) % 3, lx = ch % 3;
-        const double* K27 = fop + kCls3 * ((static_cast<int64_t>(3 * pz + lz) * Nf + 3 * py + ly) * Nf + 3 * px + lx);
+        double K27[27];
+        S.load27((static_cast<int64_t>(3 * pz + lz) * Nf + 3 * py + ly) * Nf + 3 * px + lx, K27);
         const double* Wc = sW + ch * 27 * 27;
+#pragma unroll
         for (int k = 0; k < 27; ++k) {
-            const double kv = __ldg(K27 + k);
+            const double kv = K27[k];
 #pragma unroll
             for (int q = 0; q < 27; ++q) out[q] += kv * Wc[k * 27 + q];
         }
     }
-    double2* o = reinterpret_cast<double2*>(cop + kCls3 * c);
 #pragma unroll
-    for (int q = 0; q < 26; q += 2) o[q >> 1] = make_double2(out[q], out[q + 1]);
-    o[13] = make_double2(out[26], 0.0);
+    for (int q = 0; q < 27; ++q) cop[q * ncc + c] = out[q];
 }
 
 std::vector<double> galerkin_weights3() {
@@ -751,10 +957,14 @@ Field3 to_device(const lzb_field3& f, DevBuf<double>& table) {
 
 class Grid3 {
 public:
-    Grid3(lzb_ctx* ctx, int depth, const lzb_field3& f, double delta_max, int fixed_p3)
-        : ctx_(ctx), D_(depth), delta_(delta_max), fixed_(fixed_p3) {
+    Grid3(lzb_ctx* ctx, int depth, const lzb_field3& f, double delta_max, int fixed_p3, int plane_width = 0)
+        : ctx_(ctx), D_(depth), fixed_(fixed_p3), W_(plane_width), delta_(delta_max) {
         if (depth < 0 || depth > 6) throw Error(LZB_ERR_INVALID, "3D depth must be in 0..6");
         if (fixed_p3 != 0 && (fixed_p3 < 2 || fixed_p3 > 8)) throw Error(LZB_ERR_INVALID, "fixed_p3 must be 0 or 2..8");
+        if (plane_width != 0 && (plane_width < 2 || plane_width > 8))
+            throw Error(LZB_ERR_INVALID, "plane_width must be 0 or 2..8");
+        if (plane_width != 0 && fixed_p3 > plane_width)
+            throw Error(LZB_ERR_INVALID, "fixed_p3 wider than plane_width");
         LZB_CUDA(cudaSetDevice(ctx->device));
         s_ = ctx->solve;
         N_ = 1;
@@ -762,7 +972,14 @@ public:
         nc_ = static_cast<int64_t>(N_) * N_ * N_;
         h_ = std::pow(1.0 / 3, depth);
         F_ = to_device(f, table_);
-        op_.alloc(static_cast<size_t>(nc_) * kCls3);
+        if (W_ == 0) {
+            op_.alloc(static_cast<size_t>(nc_) * kCls3);
+        } else {  // compressed class planes + eps(centre); no FP64 leaf operators
+            planes_.alloc(static_cast<size_t>(nc_) * kCls3 * W_);
+            ec_.alloc(nc_);
+        }
+        wide_.alloc(1);
+        LZB_CUDA(cudaMemsetAsync(wide_.p, 0, sizeof(int), s_));
         p3_.alloc(nc_);
         n_.alloc(nc_);
         stats_.alloc(20);
@@ -775,9 +992,9 @@ public:
     void assemble_fixed(int n) {
         if (n < 1 || n > kMaxN3) throw Error(LZB_ERR_INVALID, "3D sub-samples per axis must be in 1..16");
         ops_dirty_ = true;
-        const AxisTab3 T = axis_tab3(n), T1 = axis_tab3(1);
-        LZB_LAUNCH(k_assemble3, blocks_for(nc_, 128), 128, 0, s_, F_, N_, h_, T, T1, delta_, fixed_, op_.p, p3_.p,
-                   n_.p, stats_.p, ctx_->err.p);
+        const AxisTab3 T = axis_tab3(n);
+        LZB_LAUNCH(k_assemble3, blocks_for(nc_, 128), 128, 0, s_, F_, N_, h_, T, delta_, fixed_, op_.p, planes(), W_,
+                   p3_.p, n_.p, stats_.p, ctx_->err.p, wide_.p);
         n_last_ = n;
     }
 
@@ -813,9 +1030,15 @@ public:
     void cells(int64_t first, int64_t count, double* ops, int32_t* p3) {
         if (first < 0 || count < 0 || first + count > nc_) throw Error(LZB_ERR_INVALID, "bad cell range");
         std::vector<double> cls(static_cast<size_t>(count) * kCls3);
-        if (ops)
-            LZB_CUDA(cudaMemcpyAsync(cls.data(), op_.p + kCls3 * first, cls.size() * sizeof(double),
-                                     cudaMemcpyDeviceToHost, s_));
+        if (ops && count > 0) {
+            DevBuf<double> tmp;
+            tmp.alloc(cls.size());
+            leaf_cls([&](auto S) {
+                LZB_LAUNCH(k3_read_cls<decltype(S)>, blocks_for(count, 128), 128, 0, s_, S, first, count, tmp.p);
+            });
+            LZB_CUDA(cudaMemcpyAsync(cls.data(), tmp.p, cls.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
+            LZB_CUDA(cudaStreamSynchronize(s_));
+        }
         std::vector<int8_t> q(count);
         if (p3) LZB_CUDA(cudaMemcpyAsync(q.data(), p3_.p + first, count, cudaMemcpyDeviceToHost, s_));
         sync();
@@ -853,8 +1076,15 @@ public:
             const std::vector<double> W = galerkin_weights3();
             W3_.alloc(kW3);
             LZB_CUDA(cudaMemcpy(W3_.p, W.data(), kW3 * sizeof(double), cudaMemcpyHostToDevice));
-            LZB_CUDA(cudaFuncSetAttribute(k3_galerkin, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(kW3 * sizeof(double))));
+            for (int w = 0; w <= 8; ++w)
+                if (w == 0 || w == W_)
+                    leaf_cls(
+                        [&](auto S) {
+                            LZB_CUDA(cudaFuncSetAttribute(k3_galerkin<decltype(S)>,
+                                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                          static_cast<int>(kW3 * sizeof(double))));
+                        },
+                        w);
         }
         res3_.alloc(1);
         for (int l = 0; l <= D_; ++l)
@@ -870,8 +1100,16 @@ public:
     void coarse_ops() {
         for (int l = D_ - 1; l >= 0; --l) {
             const int64_t ncl = static_cast<int64_t>(L3_[l].N) * L3_[l].N * L3_[l].N;
-            LZB_LAUNCH(k3_galerkin, blocks_for(ncl, 256), 256, kW3 * sizeof(double), s_, L3_[l].op.p,
-                       l + 1 == D_ ? op_.p : L3_[l + 1].op.p, L3_[l].N, W3_.p);
+            if (l + 1 == D_) {
+                leaf_cls([&](auto S) {
+                    LZB_LAUNCH(k3_galerkin<decltype(S)>, blocks_for(ncl, 256), 256, kW3 * sizeof(double), s_,
+                               L3_[l].op.p, S, L3_[l].N, W3_.p);
+                });
+            } else {
+                const Src64 S{L3_[l + 1].op.p, static_cast<int64_t>(L3_[l + 1].N) * L3_[l + 1].N * L3_[l + 1].N};
+                LZB_LAUNCH(k3_galerkin<Src64>, blocks_for(ncl, 256), 256, kW3 * sizeof(double), s_, L3_[l].op.p, S,
+                           L3_[l].N, W3_.p);
+            }
         }
     }
 
@@ -886,7 +1124,7 @@ public:
         rep.cycle = static_cast<int32_t>(++cycle_);
         for (int l = D_; l >= 0; --l) {
             LZB_LAUNCH(k3_uhat, vg(l), 128, 0, s_, lv(l), l > 0 ? lv(l - 1) : lv(l), l > 0 ? 1 : 0);
-            LZB_LAUNCH(k3_residual, vg(l), 128, 0, s_, lv(l));
+            residual3(l, 0, L3_[l].N + 1);
             if (l > 0) LZB_LAUNCH(k3_restrict, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
         }
         const int ng = L3_[D_].N > 1 ? kNormBlocks3 : 1;
@@ -964,7 +1202,7 @@ public:
                 ++cycle_;
                 const int u0 = std::max(v0 - 1, 0), u1 = std::min(v1 + 1, N + 1);
                 LZB_LAUNCH(k3_uhat, vgz(D_, u0, u1), 128, 0, s_, lvz(D_, u0), lv(D_ - 1), 1);
-                LZB_LAUNCH(k3_residual, vgz(D_, v0, v1), 128, 0, s_, lvz(D_, v0));
+                residual3(D_, v0, v1);
                 LZB_CUDA(cudaMemsetAsync(partial3_.p, 0, partial3_.bytes(), s_));
                 LZB_LAUNCH(k3_norm_partial, kNormBlocks3, 256, 0, s_, lv(D_), partial3_.p, v0, v1);
                 break;
@@ -975,7 +1213,7 @@ public:
             case 2: {
                 for (int l = D_ - 1; l >= 0; --l) {
                     LZB_LAUNCH(k3_uhat, vg(l), 128, 0, s_, lv(l), l > 0 ? lv(l - 1) : lv(l), l > 0 ? 1 : 0);
-                    LZB_LAUNCH(k3_residual, vg(l), 128, 0, s_, lv(l));
+                    residual3(l, 0, L3_[l].N + 1);
                     if (l > 0) LZB_LAUNCH(k3_restrict, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
                 }
                 std::vector<double> part(kNormBlocks3);
@@ -1020,6 +1258,43 @@ public:
 
     double dist_norm2() const { return dist_norm2_; }
 
+    // Average device ms of one leaf-level cycle kernel (LZB_TK_UHAT, _RESIDUAL,
+    // _RESTRICT, _JACOBI, _PROLONG) over `reps` back-to-back launches, CUDA
+    // events on the solve stream.
+    double time_kernel(int what, int reps) {
+        if (L3_.empty()) throw Error(LZB_ERR_INVALID, "call init_cycle first");
+        if (reps < 1) throw Error(LZB_ERR_INVALID, "reps must be >= 1");
+        if (D_ < 1) throw Error(LZB_ERR_INVALID, "needs depth >= 1");
+        if (ops_dirty_) {
+            coarse_ops();
+            ops_dirty_ = false;
+        }
+        auto launch = [&] {
+            switch (what) {
+                case LZB_TK_UHAT: LZB_LAUNCH(k3_uhat, vg(D_), 128, 0, s_, lv(D_), lv(D_ - 1), 1); break;
+                case LZB_TK_RESIDUAL: residual3(D_, 0, L3_[D_].N + 1); break;
+                case LZB_TK_RESTRICT: LZB_LAUNCH(k3_restrict, vg(D_ - 1), 128, 0, s_, lv(D_), lv(D_ - 1)); break;
+                case LZB_TK_JACOBI: LZB_LAUNCH(k3_jacobi, vg(D_), 128, 0, s_, lv(D_), 0.0); break;
+                case LZB_TK_PROLONG: LZB_LAUNCH(k3_prolong, vg(D_), 128, 0, s_, lv(D_), lv(D_ - 1)); break;
+                default: throw Error(LZB_ERR_INVALID, "unknown kernel id");
+            }
+        };
+        launch();
+        cudaEvent_t a, b;
+        LZB_CUDA(cudaEventCreate(&a));
+        LZB_CUDA(cudaEventCreate(&b));
+        LZB_CUDA(cudaEventRecord(a, s_));
+        for (int i = 0; i < reps; ++i) launch();
+        LZB_CUDA(cudaEventRecord(b, s_));
+        LZB_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        LZB_CUDA(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        sync();
+        return static_cast<double>(ms) / reps;
+    }
+
     lzb_cycle_report dist_report(double norm2) {
         lzb_cycle_report rep;
         std::memset(&rep, 0, sizeof rep);
@@ -1061,16 +1336,25 @@ public:
             LZB_CUDA(cudaMemset(ctx_->err.p, 0, sizeof(int)));
             throw Error(LZB_ERR_PROTOCOL, "cannot encode non-finite operator entry");
         }
+        if (W_) {
+            LZB_CUDA(cudaMemcpy(&flag, wide_.p, sizeof(int), cudaMemcpyDeviceToHost));
+            if (flag) {
+                LZB_CUDA(cudaMemset(wide_.p, 0, sizeof(int)));
+                throw Error(LZB_ERR_RESOURCE, "a record's p3 exceeds plane_width");
+            }
+        }
     }
 
 private:
     lzb_ctx* ctx_;
     cudaStream_t s_ = nullptr;
-    int D_, N_ = 1, n_last_ = 0, fixed_;
+    int D_, N_ = 1, n_last_ = 0, fixed_, W_ = 0;
     int64_t nc_ = 1;
     double h_ = 1.0, delta_;
     Field3 F_{};
-    DevBuf<double> table_, op_;
+    DevBuf<double> table_, op_, ec_;
+    DevBuf<uint8_t> planes_;
+    DevBuf<int> wide_;
     DevBuf<int8_t> p3_;
     DevBuf<int32_t> n_;
     DevBuf<unsigned long long> stats_;
@@ -1100,6 +1384,44 @@ private:
         for (int f = 0; f < LZB_V_NFIELDS; ++f) v.v[f] = L3_[l].v[f].p;
         v.op = l == D_ ? op_.p : L3_[l].op.p;
         return v;
+    }
+    Planes3 planes() const {
+        Planes3 P{};
+        P.base = planes_.p;
+        P.ec = ec_.p;
+        P.nc = nc_;
+        P.h = h_;
+        const AxisTab3 T1 = axis_tab3(1);
+        for (int c = 0; c < 3; ++c) P.s1[c] = T1.s[0][c];
+        return P;
+    }
+    // fn(source of the leaves' 27 class values) for width w (default: this grid's)
+    template <class Fn>
+    void leaf_cls(Fn&& fn, int w = -1) const {
+        switch (w < 0 ? W_ : w) {
+            case 0: fn(Src64{op_.p, nc_}); break;
+            case 2: fn(SrcComp<2>{planes()}); break;
+            case 3: fn(SrcComp<3>{planes()}); break;
+            case 4: fn(SrcComp<4>{planes()}); break;
+            case 5: fn(SrcComp<5>{planes()}); break;
+            case 6: fn(SrcComp<6>{planes()}); break;
+            case 7: fn(SrcComp<7>{planes()}); break;
+            default: fn(SrcComp<8>{planes()}); break;
+        }
+    }
+    // the residual kernel of level l on vertex planes [z0, z1) (the leaves
+    // read this grid's leaf source): the cell-centric z-marching form
+    void residual3(int l, int z0, int z1) {
+        const int N = L3_[l].N;
+        const dim3 grid((N + kRzX - 1) / (kRzX - 1), (N + kRzY - 1) / (kRzY - 1),
+                        (z1 - z0 + kRzChunk - 1) / kRzChunk);
+        const Lv3 v = lv(l);
+        if (l < D_ || W_ == 0) {
+            const Src64 S{l < D_ ? L3_[l].op.p : op_.p, static_cast<int64_t>(N) * N * N};
+            LZB_LAUNCH(k3_residual_z<Src64>, grid, kRzX * kRzY, 0, s_, v, S, z0, z1);
+            return;
+        }
+        leaf_cls([&](auto S) { LZB_LAUNCH(k3_residual_z<decltype(S)>, grid, kRzX * kRzY, 0, s_, v, S, z0, z1); });
     }
     dim3 vg(int l) const { return dim3(blocks_for(L3_[l].N + 1, 128), L3_[l].N + 1, L3_[l].N + 1); }
     void inject3() {
@@ -1153,9 +1475,13 @@ int lzb_integrate_elements3(lzb_ctx* ctx, const lzb_field3* f, int64_t count, co
 }
 
 int lzb_grid3_create(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3, lzb_grid3** out) {
+    return lzb_grid3_create_planes(ctx, depth, f, delta_max, fixed_p3, 0, out);
+}
+int lzb_grid3_create_planes(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3,
+                            int plane_width, lzb_grid3** out) {
     return lzb::guarded([&] {
         auto g = std::make_unique<lzb_grid3>();
-        g->g = std::make_unique<lzb::Grid3>(ctx, depth, *f, delta_max, fixed_p3);
+        g->g = std::make_unique<lzb::Grid3>(ctx, depth, *f, delta_max, fixed_p3, plane_width);
         *out = g.release();
     });
 }
@@ -1195,6 +1521,9 @@ int lzb_grid3_dist_result(lzb_grid3* g, double* norm2) {
 }
 int lzb_grid3_dist_report(lzb_grid3* g, double norm2, lzb_cycle_report* out) {
     return lzb::guarded([&] { *out = g->g->dist_report(norm2); });
+}
+int lzb_grid3_time_kernel(lzb_grid3* g, int what, int reps, double* avg_ms) {
+    return lzb::guarded([&] { *avg_ms = g->g->time_kernel(what, reps); });
 }
 int lzb_grid3_device_view(lzb_grid3* g, int level, int field, void** ptr) {
     return lzb::guarded([&] { *ptr = g->g->device_field(level, field); });

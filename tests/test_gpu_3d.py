@@ -139,3 +139,35 @@ def test_dist_cycle3_loopback_bit_identical(world, solver):
             assert np.array_equal(s.grid.vertices(lvl, lzb.T.V_U), ref.vertices(lvl, lzb.T.V_U)), lvl
         a, b = s.grid.vertices(depth, lzb.T.V_U), ref.vertices(depth, lzb.T.V_U)
         assert np.array_equal(a[s.v0:min(s.v1, N + 1)], b[s.v0:min(s.v1, N + 1)])
+
+
+@pytest.mark.parametrize("width,fixed", [(2, 2), (3, 3), (4, 0), (5, 4), (6, 6), (7, 7), (8, 0), (8, 8)])
+def test_grid3_compressed_planes_bit_identical(width, fixed):
+    """Leaf operators held only as compressed class planes (BASELINE
+    configs[4]): the decoded operators, and the cycle that reads them (the
+    residual and the Galerkin coarse operators decode the planes), are bit
+    for bit those of the FP64 grid."""
+    g = lzb.grf_table(3, 16, 0.05, 1.0)
+    f = lzb.field3_grf(g)
+    grids = [lzb.Grid3(2, f, delta_max=1e-4, fixed_p3=fixed),
+             lzb.Grid3(2, f, delta_max=1e-4, fixed_p3=fixed, plane_width=width)]
+    for G in grids:
+        G.assemble_fixed(3)
+        G.init_cycle(solver="adafac-pi", omega=0.6, seed=7, max_cycles=100)
+    (a_ops, a_p3), (b_ops, b_p3) = (G.cells(0, 9 ** 3) for G in grids)
+    assert np.array_equal(a_p3, b_p3) and np.array_equal(a_ops, b_ops)
+    for _ in range(4):
+        ra, rb = (G.step() for G in grids)
+        assert ra["residual"] == rb["residual"] and ra["status"] == rb["status"]
+    for lvl in range(3):
+        assert np.array_equal(grids[0].vertices(lvl, lzb.T.V_U), grids[1].vertices(lvl, lzb.T.V_U)), lvl
+    assert grids[1].leaf_bytes_per_cell() == 27 * width + 9
+
+
+def test_grid3_planes_reject_wide_records():
+    g = lzb.grf_table(3, 16, 0.05, 1.0)
+    G = lzb.Grid3(2, lzb.field3_grf(g), delta_max=0.0, plane_width=3)  # exact records need p3 = 8
+    with pytest.raises(lzb.ResourceError):
+        G.assemble_fixed(3)
+    with pytest.raises(lzb.LzbError):
+        lzb.Grid3(2, lzb.field3_grf(g), fixed_p3=5, plane_width=4)
