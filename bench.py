@@ -40,9 +40,14 @@ P = 32
 SAMPLES_PER_STEP = CELLS * P * P
 HBM_LEVEL = 8  # smoother / stream-pack roofline grid (6561^2, beyond L2)
 # C3 (3D) executed FP64 flops per sub-sample of the separable class sums
-# (grid3.cu): z lerp 4 + exp 20 (survey convention) + coordinates 2 + the
-# class partial sums 7 (G += e, Dz[3] += e * S)
-C3_FLOPS_PER_SAMPLE = 33
+# (grid3.cu accumulate3_grf): per sample the geometric exp step 1 + the class
+# partial sums 7 (G += e, Dz[3] += e * S); per sample row (p samples) two
+# exps (first value and ratio, 20 each, survey convention), their lerp /
+# difference 6, the y interpolation 9, the row sums 5 -> 8 + 60 / p
+
+
+def c3_flops_per_sample(p):
+    return 8 + 60 / p
 # algorithmic FP64 flops per sub-sample of the tabulated integration:
 #   EXACT: 6 mul (K_sub from axis parts) + 9 add (K values) + 9 mul + 9 add (accumulate)
 #          + 2 (eps combine: 1 + (0.9 sin x) sin y)                                   = 35
@@ -358,7 +363,7 @@ def run_ours(args, world, rank, local):
     # fixed-p assembly (integrate + 64-entry record coding + store) at p = 1 and 8
     g3 = lzb.Grid3(5, lzb.field3_grf(lzb.grf_table(1, 64, 0.05, 1.0)), delta_max=1e-8, ctx=ctx)
     c3 = {"grid": "243^3 (depth 5), 14,348,907 cells", "eps": "exp(GRF), 64^3 periodic table, ell 0.05, sigma^2 1",
-          "flops_per_sample_survey": 172, "flops_per_sample_executed": C3_FLOPS_PER_SAMPLE}
+          "flops_per_sample_survey": 172, "flops_per_sample_executed": "8 + 60 / p"}
     for p3d in (1, 8):
         g3.assemble_fixed(p3d)
         k3 = max(3, args.steps // 2)
@@ -366,10 +371,11 @@ def run_ours(args, world, rank, local):
         ns = 3 ** 15 * p3d ** 3
         st3 = g3.stats()
         c3[f"p{p3d}"] = {"ms": 1e3 * t3, "sub_samples_per_s": ns / t3,
-                         "fp64_tflops_executed": ns * C3_FLOPS_PER_SAMPLE / t3 / 1e12,
-                         "frac_executed": ns * C3_FLOPS_PER_SAMPLE / t3 / 1e12 / fp64_peak,
+                         "fp64_tflops_executed": ns * c3_flops_per_sample(p3d) / t3 / 1e12,
+                         "frac_executed": ns * c3_flops_per_sample(p3d) / t3 / 1e12 / fp64_peak,
+                         "survey_def_tflops": ns * 172 / t3 / 1e12,
                          "lzmg_bytes_per_cell": st3.fine_stored_bytes / st3.fine_cells,
-                         "store_GBs": 512 * 3 ** 15 / t3 / 1e9}
+                         "store_GBs": 216 * 3 ** 15 / t3 / 1e9}
     # record bytes per cell across the mantissa widths (BASELINE configs[4] widths
     # 4/8/16/23/32/52 bits -> nearest p3 2..8), 243^3 at p = 4
     c3["width_sweep"] = []

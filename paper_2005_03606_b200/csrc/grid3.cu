@@ -130,11 +130,30 @@ struct GrfCell {
     }
 };
 
+// Along a sample row (fixed x, y) the interpolant g is linear in z inside
+// each table interval, so exp(g) at the equally spaced z samples is a
+// geometric sequence: per row and interval one exp for the first sample and
+// one for the ratio exp(dg), then a multiply per sample (a cell spans at most
+// two z intervals). Relative error <= n ulps against one exp per sample.
 __device__ inline void accumulate3_grf(const Field3& F, double x0, double y0, double z0, double h,
                                        const AxisTab3& T, Acc3& A) {
     const int n = T.n;
     const double inv = 1.0 / n;
     GrfCell G3(F, x0, y0, z0);
+    // first z sample in the upper table interval (n if none), and the z
+    // parameters of the first sample of each interval
+    int ks = n;
+    for (int k = 0; k < n; ++k)
+        if (static_cast<int>(floor((z0 + (k + 0.5) * inv * h) * F.n)) != G3.bz) {
+            ks = k;
+            break;
+        }
+    auto tz = [&](int k) {
+        const double u = (z0 + (k + 0.5) * inv * h) * F.n;
+        return u - floor(u);
+    };
+    const double t0 = tz(0), t1 = ks < n ? tz(ks) : 0.0;
+    const double dt = inv * h * F.n;  // the z parameter step between samples
 #pragma unroll
     for (int q = 0; q < 9; ++q) A.yz[q] = A.xz[q] = A.xy[q] = 0.0;
     for (int i = 0; i < n; ++i) {
@@ -143,11 +162,17 @@ __device__ inline void accumulate3_grf(const Field3& F, double x0, double y0, do
         for (int j = 0; j < n; ++j) {
             G3.set_y(y0 + (j + 0.5) * inv * h);
             double G = 0.0, Dz[3] = {0.0, 0.0, 0.0};
+            double e = exp(GrfCell::lerp(G3.Y[0], G3.Y[1], t0));
+            double r = exp((G3.Y[1] - G3.Y[0]) * dt);
             for (int k = 0; k < n; ++k) {
-                const double e = G3.eps(z0 + (k + 0.5) * inv * h);
+                if (k == ks) {
+                    e = exp(GrfCell::lerp(G3.Y[1], G3.Y[2], t1));
+                    r = exp((G3.Y[2] - G3.Y[1]) * dt);
+                }
                 G += e;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) Dz[c] += e * T.s[k][c];
+                e *= r;
             }
 #pragma unroll
             for (int cy = 0; cy < 3; ++cy) {
@@ -794,6 +819,57 @@ __global__ void k3_prolong(Lv3 F, Lv3 C) {
     F.v[LZB_V_U][vi] += p;
 }
 
+// The leaf level's three u updates of a cycle in one pass (bit-identical to
+// k3_aux_sub, k3_jacobi, k3_prolong run in that order): the adaFAC-PI aux
+// correction, damped Jacobi, the prolongated coarse correction. The coarse
+// levels are updated first; nothing there reads the leaf u.
+__global__ void k3_update_fine(Lv3 F, Lv3 C, int pi, double omega, double damping) {
+    int fx, fy, fz;
+    int64_t vi;
+    if (!vxyz(F, fx, fy, fz, vi)) return;
+    if (bnd3(F.N, fx, fy, fz)) return;
+    const int px = owner3(fx, C.N), py = owner3(fy, C.N), pz = owner3(fz, C.N);
+    const int lx = fx - 3 * px, ly = fy - 3 * py, lz = fz - 3 * pz;
+    double cu[8], cs[8], ca[8], cd[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        const int64_t ci = vidx3(C.N, px + (a & 1), py + ((a >> 1) & 1), pz + (a >> 2));
+        cu[a] = C.v[LZB_V_U][ci];
+        cs[a] = C.v[LZB_V_USNAP][ci];
+        if (pi) {
+            ca[a] = C.v[LZB_V_AUX][ci];
+            cd[a] = C.v[LZB_V_DIAG][ci];
+        }
+    }
+    double u = F.v[LZB_V_U][vi];
+    const double dg = F.v[LZB_V_DIAG][vi], r = F.v[LZB_V_R][vi];
+    if (pi) {
+        double p = 0.0;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const int cx = px + (a & 1), cy = py + ((a >> 1) & 1), cz = pz + (a >> 2);
+            const double caux = (!bnd3(C.N, cx, cy, cz) && cd[a] != 0.0) ? omega / cd[a] * ca[a] : 0.0;
+            p += pw3(lx, ly, lz, a) * caux;
+        }
+        u -= p;
+    }
+    if (dg != 0.0) u += damping / dg * r;
+    double d[8];
+    bool any = false;
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        d[a] = cu[a] - cs[a];
+        any |= d[a] != 0.0;
+    }
+    if (any) {
+        double p = 0.0;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) p += pw3(lx, ly, lz, a) * d[a];
+        u += p;
+    }
+    F.v[LZB_V_U][vi] = u;
+}
+
 __global__ void k3_inject(Lv3 F, Lv3 C) {
     int ix, iy, iz;
     int64_t vi;
@@ -1143,16 +1219,23 @@ public:
                      : rep.normalized >= 1e2 ? LZB_DIVERGED
                      : static_cast<int>(cycle_) >= max_cycles_ ? LZB_TIMEOUT : LZB_CONTINUE;
         if (rep.status == LZB_CONTINUE || rep.status == LZB_TIMEOUT) {
+            // the update pass (solver.cpp:212-313) and the prolongation cascade
+            // (solver.cpp:315-342); the leaf level's three updates run last, fused
             for (int l = 0; l < D_; ++l) LZB_LAUNCH(k3_snap, blocks_for(L3_[l].nv, 256), 256, 0, s_, lv(l), L3_[l].nv);
-            for (int l = D_; l >= 0; --l) {
-                if (variant_ == LZB_ADAFAC_PI && l > 0) {
+            const bool pi = variant_ == LZB_ADAFAC_PI;
+            if (pi && D_ > 0) LZB_LAUNCH(k3_aux_inject, vg(D_ - 1), 128, 0, s_, lv(D_), lv(D_ - 1));
+            for (int l = D_ - 1; l >= 0; --l) {
+                if (pi && l > 0) {
                     LZB_LAUNCH(k3_aux_inject, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
                     LZB_LAUNCH(k3_aux_sub, vg(l), 128, 0, s_, lv(l), lv(l - 1), omega_);
                 }
-                const double damping = variant_ == LZB_ADDITIVE ? std::pow(omega_, D_ - l + 1) : omega_;
-                LZB_LAUNCH(k3_jacobi, vg(l), 128, 0, s_, lv(l), damping);
+                LZB_LAUNCH(k3_jacobi, vg(l), 128, 0, s_, lv(l), damping3(l));
             }
-            for (int l = 1; l <= D_; ++l) LZB_LAUNCH(k3_prolong, vg(l), 128, 0, s_, lv(l), lv(l - 1));
+            for (int l = 1; l < D_; ++l) LZB_LAUNCH(k3_prolong, vg(l), 128, 0, s_, lv(l), lv(l - 1));
+            if (D_ > 0)
+                LZB_LAUNCH(k3_update_fine, vg(D_), 128, 0, s_, lv(D_), lv(D_ - 1), pi ? 1 : 0, omega_, damping3(D_));
+            else
+                LZB_LAUNCH(k3_jacobi, vg(0), 128, 0, s_, lv(0), damping3(0));
             inject3();
             const uint64_t Nf = static_cast<uint64_t>(L3_[D_].N);
             rep.dof_updates = (Nf - 1) * (Nf - 1) * (Nf - 1);
@@ -1236,15 +1319,12 @@ public:
                         LZB_LAUNCH(k3_aux_inject, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
                         LZB_LAUNCH(k3_aux_sub, vg(l), 128, 0, s_, lv(l), lv(l - 1), omega_);
                     }
-                    const double damping = variant_ == LZB_ADDITIVE ? std::pow(omega_, D_ - l + 1) : omega_;
-                    LZB_LAUNCH(k3_jacobi, vg(l), 128, 0, s_, lv(l), damping);
+                    LZB_LAUNCH(k3_jacobi, vg(l), 128, 0, s_, lv(l), damping3(l));
                 }
                 for (int l = 1; l < D_; ++l) LZB_LAUNCH(k3_prolong, vg(l), 128, 0, s_, lv(l), lv(l - 1));
-                // the slab's leaf planes: aux correction, Jacobi, prolongation (the one-GPU order)
-                if (variant_ == LZB_ADAFAC_PI)
-                    LZB_LAUNCH(k3_aux_sub, vgz(D_, v0, v1), 128, 0, s_, lvz(D_, v0), lv(D_ - 1), omega_);
-                LZB_LAUNCH(k3_jacobi, vgz(D_, v0, v1), 128, 0, s_, lvz(D_, v0), omega_);  // damping of level D
-                LZB_LAUNCH(k3_prolong, vgz(D_, v0, v1), 128, 0, s_, lvz(D_, v0), lv(D_ - 1));
+                // the slab's leaf planes: aux correction, Jacobi, prolongation (fused, the one-GPU kernel)
+                LZB_LAUNCH(k3_update_fine, vgz(D_, v0, v1), 128, 0, s_, lvz(D_, v0), lv(D_ - 1),
+                           variant_ == LZB_ADAFAC_PI ? 1 : 0, omega_, damping3(D_));
                 LZB_LAUNCH(k3_inject, vgz(D_ - 1, c0, c1), 128, 0, s_, lv(D_), lvz(D_ - 1, c0));
                 break;
             }
@@ -1276,6 +1356,9 @@ public:
                 case LZB_TK_RESTRICT: LZB_LAUNCH(k3_restrict, vg(D_ - 1), 128, 0, s_, lv(D_), lv(D_ - 1)); break;
                 case LZB_TK_JACOBI: LZB_LAUNCH(k3_jacobi, vg(D_), 128, 0, s_, lv(D_), 0.0); break;
                 case LZB_TK_PROLONG: LZB_LAUNCH(k3_prolong, vg(D_), 128, 0, s_, lv(D_), lv(D_ - 1)); break;
+                case LZB_TK_BACK:  // the fused leaf update (u drifts by the prolongated correction)
+                    LZB_LAUNCH(k3_update_fine, vg(D_), 128, 0, s_, lv(D_), lv(D_ - 1), 1, omega_, 0.0);
+                    break;
                 default: throw Error(LZB_ERR_INVALID, "unknown kernel id");
             }
         };
@@ -1423,6 +1506,7 @@ private:
         }
         leaf_cls([&](auto S) { LZB_LAUNCH(k3_residual_z<decltype(S)>, grid, kRzX * kRzY, 0, s_, v, S, z0, z1); });
     }
+    double damping3(int l) const { return variant_ == LZB_ADDITIVE ? std::pow(omega_, D_ - l + 1) : omega_; }
     dim3 vg(int l) const { return dim3(blocks_for(L3_[l].N + 1, 128), L3_[l].N + 1, L3_[l].N + 1); }
     void inject3() {
         for (int l = D_; l >= 1; --l) LZB_LAUNCH(k3_inject, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
