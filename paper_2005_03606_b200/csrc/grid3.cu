@@ -405,41 +405,64 @@ template <int COUNT>
 __device__ __noinline__ int choose_precision_set(const double* v, double delta) {
     return choose_precision(v, COUNT, delta);
 }
+// The same result in registers for records whose values are all regular
+// (finite, normal, exponent in [-128, 127], or +-0: the passing widths of
+// each value are upward closed): the running maximum P of the
+// per-value smallest passing widths, each value testing only widths >= P.
+// Other records take the general routine.
+template <int COUNT>
+__device__ __forceinline__ int choose_precision_regular(const double* v, double delta) {
+    bool all_small = true, regular = true;
+#pragma unroll
+    for (int i = 0; i < COUNT; ++i) {
+        all_small = all_small && !(fabs(v[i]) > delta);
+        regular = regular && codec_regular(v[i]);
+    }
+    if (all_small) return 0;
+    if (!regular) return choose_precision_set<COUNT>(v, delta);
+    int P = 2;
+#pragma unroll
+    for (int i = 0; i < COUNT; ++i)
+        while (P < 8 && fabs(rt_bits(v[i], mantissa_bits(P)) - v[i]) > delta) ++P;
+    return P;
+}
 
 // Fixed-p assembly of every cell of a 3D level: integrate at n, code the
 // record against the n = 1 element (stream.cpp:82-111 in 3D), store the
 // decoded operator (FP64 class planes, or eps(centre) + the compressed
 // planes of width W), width and n. One thread per cell; the record's 27
 // distinct surplus values are coded once (they stand for its 64 entries).
-__global__ void __launch_bounds__(128) k_assemble3(Field3 F, int N, double h, AxisTab3 T, double delta_max,
-                                                   int fixed_p3, double* __restrict__ op, Planes3 PL, int W,
-                                                   int8_t* __restrict__ p3o, int32_t* __restrict__ no,
-                                                   unsigned long long* stats, int* err, int* wide) {
+__global__ void __launch_bounds__(128, 4) k_assemble3(Field3 F, int N, double h, AxisTab3 T, double delta_max,
+                                                      int fixed_p3, double* __restrict__ op, Planes3 PL, int W,
+                                                      int8_t* __restrict__ p3o, int32_t* __restrict__ no,
+                                                      unsigned long long* stats, int* err, int* wide) {
     const int64_t c = gtid();
     const int64_t nc = static_cast<int64_t>(N) * N * N;
     if (c >= nc) return;
     const int cx = static_cast<int>(c % N), cy = static_cast<int>((c / N) % N), cz = static_cast<int>(c / N / N);
     const double x0 = cx * h, y0 = cy * h, z0 = cz * h;
-    double base[27], sur[27];
     const double e = centre_eps3(F, x0, y0, z0, h);
-    {
-        const Base3 B(e, PL.s1, h);  // A(n=1): eps(centre) * unit stiffness
-#pragma unroll
-        for (int q = 0; q < 27; ++q) base[q] = B(q / 9, (q / 3) % 3, q % 3);
-    }
+    const Base3 B(e, PL.s1, h);  // A(n=1): eps(centre) * unit stiffness, recomputed per class (9 products)
+    double sur[27];
     {
         Acc3 A;
         accumulate3(F, x0, y0, z0, h, T, A);
         const double hn = h * (1.0 / T.n);
 #pragma unroll
-        for (int q = 0; q < 27; ++q) sur[q] = class_value(A, hn, q / 9, (q / 3) % 3, q % 3) - base[q];
+        for (int q = 0; q < 27; ++q)
+            sur[q] = class_value(A, hn, q / 9, (q / 3) % 3, q % 3) - B(q / 9, (q / 3) % 3, q % 3);
     }
-    const int p3 = fixed_p3 ? fixed_p3 : choose_precision_set<27>(sur, delta_max);
+    const int p3 = fixed_p3 ? fixed_p3 : choose_precision_regular<27>(sur, delta_max);
     if (p3 < 0) {
         atomicExch(err, 1);
         return;
     }
-    double delta = 0.0, rts[27];
+    if (W != 0 && p3 > W) {
+        atomicExch(wide, 1);  // record wider than the planes
+        return;
+    }
+    if (W != 0) PL.ec[c] = e;
+    double delta = 0.0;
 #pragma unroll
     for (int q = 0; q < 27; ++q) {
         double rt;
@@ -449,17 +472,8 @@ __global__ void __launch_bounds__(128) k_assemble3(Field3 F, int N, double h, Ax
         }
         const double d = fabs(rt - sur[q]);
         delta = delta < d ? d : delta;
-        rts[q] = rt;
-    }
-    if (W == 0) {
-#pragma unroll
-        for (int q = 0; q < 27; ++q) op[q * nc + c] = base[q] + rts[q];
-    } else if (p3 > W) {
-        atomicExch(wide, 1);  // record wider than the planes
-    } else {
-        PL.ec[c] = e;
-#pragma unroll
-        for (int q = 0; q < 27; ++q) plane_store3(PL, W, c, q, plane_word(rts[q], W));
+        if (W == 0) op[q * nc + c] = B(q / 9, (q / 3) % 3, q % 3) + rt;
+        else plane_store3(PL, W, c, q, plane_word(rt, W));
     }
     p3o[c] = static_cast<int8_t>(p3);
     no[c] = T.n;
