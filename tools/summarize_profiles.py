@@ -1,6 +1,8 @@
 """Summarise an ncu launch list + a `--set full` report into profiles/<tag>_*.
 
-usage: python tools/summarize_profiles.py <tag> <launches.csv | -> <full.ncu-rep>
+usage: python tools/summarize_profiles.py <tag> <launches.csv | -> <full.ncu-rep | raw.csv>
+(raw.csv: `ncu -i <rep> --page raw --csv`, written on the GPU box when the
+report itself is too large to bring back)
 Also merges the per-launch DRAM traffic of every captured kernel into
 profiles/traffic.json (read by bench.py for roofline.traffic).
 """
@@ -42,7 +44,8 @@ if launches != "-":
         for name, v in seq:
             f.write(f"{name},{v:.3f}\n")
 
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+raw = (open(rep).read() if rep.endswith(".csv") else
+       subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)
 rr = list(csv.reader(io.StringIO(raw)))
 hdr, units, vals = rr[0], rr[1], rr[2:]
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -59,6 +62,7 @@ lines = [f"# {tag}: ncu --set full (selected metrics per captured launch)", "",
          "|---|" + "---|" * len(col)]
 for v in vals:
     name = v[kn].split("(")[0].replace("lzb::<unnamed>::", "").replace("(anonymous namespace)::", "")
+    name = name.replace("void ", "").replace("unnamed>::", "").split("<")[0]
     cells = []
     for w, i in col.items():
         u = units[i]
@@ -73,7 +77,8 @@ tpath = os.path.join(out_dir, "traffic.json")
 traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
 ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
 for v in vals:
-    name = v[kn].split("(")[0].split("::")[-1].replace("void ", "").split("<")[0].strip()
+    name = v[kn].split("(")[0].replace("void ", "").replace("lzb::<unnamed>::", "")
+    name = name.replace("(anonymous namespace)::", "").replace("unnamed>::", "").split("<")[0].strip()
     b = float(v[ir].replace(",", "")) * scale.get(units[ir], 1) + float(v[iw].replace(",", "")) * scale.get(units[iw], 1)
     traffic[name] = {"dram_bytes_per_launch": b, "report": os.path.basename(rep), "tag": tag}
 json.dump(traffic, open(tpath, "w"), indent=1, sort_keys=True)
