@@ -29,13 +29,49 @@ inline void cuda_check(cudaError_t e, const char* what) {
         throw Error(LZB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 #define LZB_CUDA(x) ::lzb::cuda_check((x), #x)
+// Programmatic dependent launch (PDL) for the cycle's kernel chains: while
+// g_pdl is set (the captured cycle bodies), launches carry the programmatic
+// stream-serialisation attribute, so a kernel's CTAs are scheduled as soon as
+// its predecessor's have all started, and wait in lzb_pdl_enter (every
+// grid.cu kernel's first statement: griddepcontrol.wait, a no-op without a
+// programmatic predecessor) until the predecessor has completed and its
+// writes are visible.
+extern thread_local bool g_pdl;
+// Kernels called with their default arguments take the plain launch.
+template <typename... KArgs, typename... Args>
+constexpr bool pdl_arity(void (*)(KArgs...), const Args&...) {
+    return sizeof...(KArgs) == sizeof...(Args);
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    if constexpr (sizeof...(KArgs) != sizeof...(Args)) {
+        return cudaErrorInvalidValue;  // not reached: see pdl_arity
+    } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+    }
+}
 // Every kernel launch goes through this: counts launches and surfaces
 // launch-configuration errors immediately.
-#define LZB_LAUNCH(kernel, grid, block, smem, stream, ...)                         \
-    do {                                                                           \
-        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                \
-        ::lzb::g_launches.fetch_add(1, std::memory_order_relaxed);                 \
-        ::lzb::cuda_check(cudaGetLastError(), #kernel);                            \
+#define LZB_LAUNCH(kernel, grid, block, smem, stream, ...)                                          \
+    do {                                                                                            \
+        if (::lzb::g_pdl && ::lzb::pdl_arity(kernel, __VA_ARGS__))                                  \
+            ::lzb::cuda_check(::lzb::launch_pdl(kernel, dim3(grid), dim3(block), (smem), (stream),  \
+                                                __VA_ARGS__),                                       \
+                              #kernel);                                                             \
+        else                                                                                        \
+            kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                             \
+        ::lzb::g_launches.fetch_add(1, std::memory_order_relaxed);                                  \
+        ::lzb::cuda_check(cudaGetLastError(), #kernel);                                             \
     } while (0)
 
 template <typename F>

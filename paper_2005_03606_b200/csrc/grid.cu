@@ -88,6 +88,10 @@ __device__ inline void element_or_baseline(const lzb_field& f, const LevelView& 
 __device__ inline void atomic_max_u64(unsigned long long* a, unsigned long long v) {
     if (v > *reinterpret_cast<volatile unsigned long long*>(a)) atomicMax(a, v);
 }
+__device__ __forceinline__ void lzb_pdl_enter() {  // see LZB_LAUNCH (engine.hpp)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 __device__ inline void atomic_max_double_bits(unsigned long long* a, double v) {  // v >= 0
     atomic_max_u64(a, static_cast<unsigned long long>(__double_as_longlong(v)));
 }
@@ -220,6 +224,7 @@ constexpr int kCompactThreads = 256;
 
 __global__ void k_compact_count(LevelView F, int selector, const long long* keys, long long key_limit,
                                 int* block_counts) {
+    lzb_pdl_enter();
     __shared__ int warp_n[kCompactThreads / 32];
     int64_t c = gtid();
     int32_t p1;
@@ -236,6 +241,7 @@ __global__ void k_compact_count(LevelView F, int selector, const long long* keys
 
 // Exclusive scan of the block counts in one CTA; total into *count.
 __global__ void k_compact_scan(int* block_counts, int nblocks, int* count) {
+    lzb_pdl_enter();
     __shared__ int carry;
     __shared__ int warp_sum[32];
     if (threadIdx.x == 0) carry = 0;
@@ -270,6 +276,7 @@ __global__ void k_compact_scan(int* block_counts, int nblocks, int* count) {
 
 __global__ void k_compact_scatter(LevelView F, int selector, const long long* keys, long long key_limit,
                                   const int* block_offsets, int32_t* list, int32_t* snap, unsigned* hist) {
+    lzb_pdl_enter();
     __shared__ int warp_off[kCompactThreads / 32];
     int64_t c = gtid();
     int32_t p1 = 0;
@@ -300,6 +307,7 @@ __global__ void k_compact_scatter(LevelView F, int selector, const long long* ke
 __global__ void k_bottom(LevelView F, lzb_field f, const int32_t* list, const int32_t* snap,
                          int count, double delta_max, uint32_t cycle, int clear_p2,
                          unsigned long long* stats, int* err) {
+    lzb_pdl_enter();
     int64_t t = gtid();
     if (t >= count || snap[t] != LZB_P1_BOTTOM) return;
     int c = list[t], cx = c % F.N, cy = c / F.N;
@@ -323,6 +331,7 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_step(LevelView F, LevelView 
                                                          int n_cap_top, IntTables T, double term_c,
                                                          double delta_max, uint32_t cycle, int clear_p2,
                                                          unsigned long long* stats, int* err) {
+    lzb_pdl_enter();
     extern __shared__ double sm[];
     const int count = *count_ptr;
     const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x * kCPT;
@@ -389,6 +398,7 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_step(LevelView F, LevelView 
 // Anarchic request_stencil for non-bottom leaves: spawn if not top and not in
 // flight (assembly.cpp:95-106); key = FIFO position (spawn cycle, pre-order).
 __global__ void k_spawn(LevelView F, uint32_t cycle, long long leaf_count, long long* keys) {
+    lzb_pdl_enter();
     int64_t c = gtid();
     if (c >= static_cast<int64_t>(F.N) * F.N) return;
     if (F.p1[c] == LZB_P1_TOP || F.p2[c]) return;
@@ -402,6 +412,7 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_fixed(LevelView F, lzb_field
                                                           double delta_max, uint32_t cycle,
                                                           unsigned long long* stats, int* err,
                                                           int64_t cbeg, int64_t cend) {
+    lzb_pdl_enter();
     extern __shared__ double sm[];
     stage_common(sm, f, T);
     const int64_t ncell = cend;  // cells [cbeg, cend): a slab of whole rows
@@ -444,6 +455,7 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_fixed_res(LevelView F, lzb_f
                                                               double delta_max, uint32_t cycle,
                                                               unsigned long long* stats, int* err,
                                                               int64_t cbeg, int64_t cend) {
+    lzb_pdl_enter();
     extern __shared__ double sm[];
     stage_common(sm, f, T);
     if (!FAST) {
@@ -503,6 +515,7 @@ constexpr int kCoarseThreads = 128;
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_geo(LevelView C, LevelView F, lzb_field f,
                                                                double delta_max, const uint32_t* cycle_ptr,
                                                                unsigned long long* stats, int* err) {
+    lzb_pdl_enter();
     const uint32_t cycle = *cycle_ptr;  // device-resident: the cycle is replayed as a CUDA graph
     int64_t c = gtid();
     if (c >= static_cast<int64_t>(C.N) * C.N) return;
@@ -628,6 +641,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_geo(LevelView C, Leve
 __global__ void __launch_bounds__(64) k_coarse(LevelView C, LevelView F, lzb_field f, int boxmg,
                                                double delta_max, const uint32_t* cycle_ptr,
                                                unsigned long long* stats, int* err) {
+    lzb_pdl_enter();
     const uint32_t cycle = *cycle_ptr;
     int64_t c = gtid();
     if (c >= static_cast<int64_t>(C.N) * C.N) return;
@@ -719,6 +733,18 @@ __device__ inline bool vertex_xy(const LevelView& L, int& ix, int& iy, int64_t& 
     vi = static_cast<int64_t>(iy) * (L.N + 1) + ix;
     return true;
 }
+// The same for a linear vertex index of a whole level (the fused small-level
+// kernels: one block walks every vertex of a level).
+template <bool LIN>
+__device__ __forceinline__ bool vertex_at(int64_t lin, const LevelView& L, int& ix, int& iy, int64_t& vi) {
+    if (!LIN) return vertex_xy(L, ix, iy, vi);
+    const int NV = L.N + 1;
+    if (lin >= static_cast<int64_t>(NV) * NV) return false;
+    iy = static_cast<int>(lin / NV);
+    ix = static_cast<int>(lin - static_cast<int64_t>(iy) * NV);
+    vi = lin;
+    return true;
+}
 __device__ inline bool boundary(int N, int ix, int iy) {
     return ix == 0 || iy == 0 || ix == N || iy == N;
 }
@@ -758,6 +784,7 @@ __device__ inline Adj adjacent_cells(const LevelView& L, int ix, int iy) {
 // init_level_rhs on the leaf level (solver.cpp:99-118): fl = sum over
 // adjacent leaves of w * f(v) (identical terms, so order-free).
 __global__ void k_init_rhs(LevelView F, lzb_rhs rhs, double w) {
+    lzb_pdl_enter();
     int ix, iy;
     int64_t vi;
     if (!vertex_xy(F, ix, iy, vi)) return;
@@ -775,10 +802,11 @@ __global__ void k_init_rhs(LevelView F, lzb_rhs rhs, double w) {
 }
 
 // compute_uhat (solver.cpp:120-143).
-__global__ void k_uhat(LevelView F, LevelView C, int has_coarse) {
+template <bool LIN>
+__device__ __forceinline__ void k_uhat_body(int64_t lin, LevelView F, LevelView C, int has_coarse) {
     int fx, fy, px, py;
     int64_t vi;
-    if (!vertex_xy(F, fx, fy, vi)) return;
+    if (!vertex_at<LIN>(lin, F, fx, fy, vi)) return;
     double u = F.v[LZB_V_U][vi];
     if (!has_coarse) {
         F.v[LZB_V_UHAT][vi] = u;
@@ -792,6 +820,10 @@ __global__ void k_uhat(LevelView F, LevelView C, int has_coarse) {
         interp += P[L * 4 + k] * C.v[LZB_V_U][(py + cdy(k)) * (C.N + 1) + px + cdx(k)];
     F.v[LZB_V_UHAT][vi] = u - interp;
 }
+__global__ void k_uhat(LevelView F, LevelView C, int has_coarse) {
+    lzb_pdl_enter();
+    k_uhat_body<false>(0, F, C, has_coarse);
+}
 
 // residual_pass cell mat-vec, as a gather (solver.cpp:149-175).
 //
@@ -800,10 +832,11 @@ __global__ void k_uhat(LevelView F, LevelView C, int has_coarse) {
 // load (four 32-B operator rows, p1, the 3x3 u / uhat neighbourhood) is
 // issued up front, independent of the creation-rank order, which only picks
 // the accumulation order of positions 1 and 2 afterwards.
-__global__ void __launch_bounds__(kThreads) k_residual(LevelView F, lzb_field f) {
+template <bool LIN>
+__device__ __forceinline__ void k_residual_body(int64_t lin, LevelView F, lzb_field f) {
     int ix, iy;
     int64_t vi;
-    if (!vertex_xy(F, ix, iy, vi)) return;
+    if (!vertex_at<LIN>(lin, F, ix, iy, vi)) return;
     const int N = F.N, NV = N + 1;
     bool has[4];
     has[0] = ix >= 1 && iy >= 1;
@@ -874,6 +907,10 @@ __global__ void __launch_bounds__(kThreads) k_residual(LevelView F, lzb_field f)
     F.v[LZB_V_RHAT][vi] = rh;
     F.v[LZB_V_DIAG][vi] = dg;
 }
+__global__ void __launch_bounds__(kThreads) k_residual(LevelView F, lzb_field f) {
+    lzb_pdl_enter();
+    k_residual_body<false>(0, F, f);
+}
 
 // ---- residual on the compressed leaf records (plane_width = W > 0)
 // Bytes [k*W, k*W + W) of a 4W-byte slot row held as W little-endian words.
@@ -915,6 +952,7 @@ struct PlaneDec {
 template <int W>
 __global__ void __launch_bounds__(kThreads, 3) k_residual_comp(LevelView F, lzb_field f, const double* __restrict__ cxp,
                                                             const double* __restrict__ cyp) {
+    lzb_pdl_enter();
     int ix, iy;
     int64_t vi;
     if (!vertex_xy(F, ix, iy, vi)) return;
@@ -1003,10 +1041,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_residual_comp(LevelView F, lzb_
 // (solver.cpp:177-200), gathered per coarse vertex in (cell rank, L) order.
 // mode 0: rhs restriction of rhat into fl; mode 1: adaFAC-Jac smoothed
 // residual into aux (solver.cpp:250-268).
-__global__ void k_restrict(LevelView F, LevelView C, int mode, double omega) {
+template <bool LIN>
+__device__ __forceinline__ void k_restrict_body(int64_t lin, LevelView F, LevelView C, int mode, double omega) {
     int IX, IY;
     int64_t vi;
-    if (!vertex_xy(C, IX, IY, vi)) return;
+    if (!vertex_at<LIN>(lin, C, IX, IY, vi)) return;
     const int NV = F.N + 1;
     Adj a = adjacent_cells(C, IX, IY);
     double acc_v = 0.0;
@@ -1035,12 +1074,17 @@ __global__ void k_restrict(LevelView F, LevelView C, int mode, double omega) {
     if (mode == 0) C.v[LZB_V_FL][vi] = acc_v;
     else C.v[LZB_V_AUX][vi] = acc_v;
 }
+__global__ void k_restrict(LevelView F, LevelView C, int mode, double omega) {
+    lzb_pdl_enter();
+    k_restrict_body<false>(0, F, C, mode, omega);
+}
 
 // Residual norm partials (solver.cpp:202-209): fine interior vertices. Block
 // b sums rows 1+b, 1+b+G, ... four rows per step (independent loads in
 // flight), then a fixed-order tree; k_norm_final adds the kNormBlocks partials.
 constexpr int kNormBlocks = 148 * 4;
 __global__ void __launch_bounds__(kThreads) k_norm_partial(LevelView F, int y0, int y1, double* partial) {
+    lzb_pdl_enter();
     __shared__ double sh[kThreads];
     const int N = F.N;
     const double* r = F.v[LZB_V_R];
@@ -1074,6 +1118,7 @@ __global__ void __launch_bounds__(kThreads) k_norm_partial(LevelView F, int y0, 
 constexpr int kNormFinalThreads = 1024;
 __global__ void __launch_bounds__(kNormFinalThreads) k_norm_final(const double* partial, int n, Result* res,
                                                                    int squared = 0) {
+    lzb_pdl_enter();
     __shared__ double sh[kNormFinalThreads];
     double s = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) s += partial[i];
@@ -1092,6 +1137,7 @@ __global__ void __launch_bounds__(kNormFinalThreads) k_norm_final(const double* 
 constexpr int kStatsBlocks = 148 * 4;
 __global__ void __launch_bounds__(kThreads) k_stats(LevelView L, int leaf, unsigned long long* s,
                                                     int64_t cbeg = 0, int64_t cend = -1) {
+    lzb_pdl_enter();
     __shared__ unsigned long long sh[20];
     if (threadIdx.x < 20) sh[threadIdx.x] = 0;
     __syncthreads();
@@ -1148,6 +1194,7 @@ __global__ void __launch_bounds__(kThreads) k_stats(LevelView L, int leaf, unsig
 // The walk's take_dirty (stream.cpp:247-250) for every refined cell of a
 // level: the flag of the current parity spawns a coarse_recompute task.
 __global__ void k_take_dirty(LevelView L, uint32_t cycle) {
+    lzb_pdl_enter();
     const int64_t c = gtid();
     if (c >= static_cast<int64_t>(L.N) * L.N) return;
     const uint32_t bit = 1u << (cycle & 1u), d = L.dirty[c];
@@ -1158,6 +1205,7 @@ __global__ void k_take_dirty(LevelView L, uint32_t cycle) {
 }
 
 __global__ void k_count_p2(LevelView L, unsigned long long* out) {
+    lzb_pdl_enter();
     int64_t c = gtid();
     bool on = c < static_cast<int64_t>(L.N) * L.N && L.p2[c];
     unsigned m = __ballot_sync(0xffffffffu, on);
@@ -1165,22 +1213,33 @@ __global__ void k_count_p2(LevelView L, unsigned long long* out) {
 }
 
 // update_pass pieces (solver.cpp:212-313)
-__global__ void k_snap(LevelView L) {
-    int64_t vi = gtid();
+template <bool LIN>
+__device__ __forceinline__ void k_snap_body(int64_t lin, LevelView L) {
+    int64_t vi = (LIN ? lin : gtid());
     if (vi >= static_cast<int64_t>(L.N + 1) * (L.N + 1)) return;
     L.v[LZB_V_USNAP][vi] = L.v[LZB_V_U][vi];
     L.v[LZB_V_AUX][vi] = 0.0;
 }
-__global__ void k_aux_inject(LevelView F, LevelView C) {  // adaFAC-PI: R~ = injection
+__global__ void k_snap(LevelView L) {
+    lzb_pdl_enter();
+    k_snap_body<false>(0, L);
+}
+template <bool LIN>
+__device__ __forceinline__ void k_aux_inject_body(int64_t lin, LevelView F, LevelView C) {  // adaFAC-PI: R~ = injection
     int ix, iy;
     int64_t vi;
-    if (!vertex_xy(C, ix, iy, vi)) return;
+    if (!vertex_at<LIN>(lin, C, ix, iy, vi)) return;
     C.v[LZB_V_AUX][vi] = F.v[LZB_V_R][static_cast<int64_t>(3 * iy) * (F.N + 1) + 3 * ix];
 }
-__global__ void k_aux_Ar(LevelView F, lzb_field f) {  // adaFAC-Jac: aux = A r on level l
+__global__ void k_aux_inject(LevelView F, LevelView C) {
+    lzb_pdl_enter();
+    k_aux_inject_body<false>(0, F, C);
+}
+template <bool LIN>
+__device__ __forceinline__ void k_aux_Ar_body(int64_t lin, LevelView F, lzb_field f) {  // adaFAC-Jac: aux = A r on level l
     int ix, iy;
     int64_t vi;
-    if (!vertex_xy(F, ix, iy, vi)) return;
+    if (!vertex_at<LIN>(lin, F, ix, iy, vi)) return;
     const int NV = F.N + 1;
     Adj a = adjacent_cells(F, ix, iy);
     double aux = 0.0;
@@ -1195,11 +1254,16 @@ __global__ void k_aux_Ar(LevelView F, lzb_field f) {  // adaFAC-Jac: aux = A r o
     }
     F.v[LZB_V_AUX][vi] = aux;
 }
+__global__ void k_aux_Ar(LevelView F, lzb_field f) {
+    lzb_pdl_enter();
+    k_aux_Ar_body<false>(0, F, f);
+}
 // u_l -= P (omega/diag_c aux_c) on interior fine vertices (solver.cpp:271-297)
-__global__ void k_aux_sub(LevelView F, LevelView C, double omega) {
+template <bool LIN>
+__device__ __forceinline__ void k_aux_sub_body(int64_t lin, LevelView F, LevelView C, double omega) {
     int fx, fy, px, py;
     int64_t vi;
-    if (!vertex_xy(F, fx, fy, vi)) return;
+    if (!vertex_at<LIN>(lin, F, fx, fy, vi)) return;
     if (boundary(F.N, fx, fy)) return;
     owner_patch(C, fx, fy, px, py);
     const double* P = transfer_of(C, py * C.N + px);
@@ -1214,19 +1278,29 @@ __global__ void k_aux_sub(LevelView F, LevelView C, double omega) {
     }
     F.v[LZB_V_U][vi] -= p;
 }
-__global__ void k_jacobi(LevelView F, double damping) {
+__global__ void k_aux_sub(LevelView F, LevelView C, double omega) {
+    lzb_pdl_enter();
+    k_aux_sub_body<false>(0, F, C, omega);
+}
+template <bool LIN>
+__device__ __forceinline__ void k_jacobi_body(int64_t lin, LevelView F, double damping) {
     int ix, iy;
     int64_t vi;
-    if (!vertex_xy(F, ix, iy, vi)) return;
+    if (!vertex_at<LIN>(lin, F, ix, iy, vi)) return;
     if (boundary(F.N, ix, iy)) return;
     double dg = F.v[LZB_V_DIAG][vi];
     if (dg != 0.0) F.v[LZB_V_U][vi] += damping / dg * F.v[LZB_V_R][vi];
 }
+__global__ void k_jacobi(LevelView F, double damping) {
+    lzb_pdl_enter();
+    k_jacobi_body<false>(0, F, damping);
+}
 // prolong_corrections (solver.cpp:315-342)
-__global__ void k_prolong(LevelView F, LevelView C) {
+template <bool LIN>
+__device__ __forceinline__ void k_prolong_body(int64_t lin, LevelView F, LevelView C) {
     int fx, fy, px, py;
     int64_t vi;
-    if (!vertex_xy(F, fx, fy, vi)) return;
+    if (!vertex_at<LIN>(lin, F, fx, fy, vi)) return;
     if (boundary(F.N, fx, fy)) return;
     owner_patch(C, fx, fy, px, py);
     double delta[4];
@@ -1243,6 +1317,10 @@ __global__ void k_prolong(LevelView F, LevelView C) {
     for (int k = 0; k < 4; ++k) p += P[L * 4 + k] * delta[k];
     F.v[LZB_V_U][vi] += p;
 }
+__global__ void k_prolong(LevelView F, LevelView C) {
+    lzb_pdl_enter();
+    k_prolong_body<false>(0, F, C);
+}
 // The leaf level's three updates of one cycle in one pass over u (u is
 // touched by nothing else in between): the adaFAC-PI aux correction
 // (k_aux_sub, when caux_c is given), the damped Jacobi step (k_jacobi) and the
@@ -1253,6 +1331,7 @@ __global__ void k_prolong(LevelView F, LevelView C) {
 // and where diag_c = 0), once per coarse vertex instead of four times per
 // fine vertex; same expression, same bits.
 __global__ void k_scale_aux(LevelView C, double omega, double* __restrict__ out) {
+    lzb_pdl_enter();
     int cx, cy;
     int64_t ci;
     if (!vertex_xy(C, cx, cy, ci)) return;
@@ -1261,6 +1340,7 @@ __global__ void k_scale_aux(LevelView C, double omega, double* __restrict__ out)
 }
 
 __global__ void k_update_fine(LevelView F, LevelView C, const double* __restrict__ caux_c, double damping) {
+    lzb_pdl_enter();
     int fx, fy, px, py;
     int64_t vi;
     if (!vertex_xy(F, fx, fy, vi)) return;
@@ -1298,14 +1378,20 @@ __global__ void k_update_fine(LevelView F, LevelView C, const double* __restrict
     F.v[LZB_V_U][vi] = u;
 }
 // inject_solution (mesh.cpp:226-234)
-__global__ void k_inject(LevelView F, LevelView C) {
+template <bool LIN>
+__device__ __forceinline__ void k_inject_body(int64_t lin, LevelView F, LevelView C) {
     int ix, iy;
     int64_t vi;
-    if (!vertex_xy(C, ix, iy, vi)) return;
+    if (!vertex_at<LIN>(lin, C, ix, iy, vi)) return;
     C.v[LZB_V_U][vi] = F.v[LZB_V_U][static_cast<int64_t>(3 * iy) * (F.N + 1) + 3 * ix];
+}
+__global__ void k_inject(LevelView F, LevelView C) {
+    lzb_pdl_enter();
+    k_inject_body<false>(0, F, C);
 }
 // init_noise (problem.cpp:50-68), before the injection.
 __global__ void k_noise(LevelView L, int level, uint64_t seed, double gval) {
+    lzb_pdl_enter();
     int ix, iy;
     int64_t vi;
     if (!vertex_xy(L, ix, iy, vi)) return;
@@ -1452,6 +1538,7 @@ struct PackArgs {
 __global__ void __launch_bounds__(kPackWarps * 32) k_pack_patches(AllLevels A, lzb_field f, PackArgs T, int per,
                                                                   const int64_t* __restrict__ offsets,
                                                                   uint8_t* __restrict__ out, int* err) {
+    lzb_pdl_enter();
     __shared__ __align__(16) uint8_t wbuf[kPackWarps][kPackWindow];
     __shared__ double s_geo[64], s_kunit[16];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1614,6 +1701,7 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_pack_patches(AllLevels A, l
 // value, bytes straight to global memory.
 __global__ void k_pack_upper(AllLevels A, lzb_field f, int64_t ncells, const int64_t* __restrict__ offsets,
                              uint8_t* __restrict__ out, int* err) {
+    lzb_pdl_enter();
     const int lane = threadIdx.x & 31;
     int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (t >= ncells) return;
@@ -1655,6 +1743,7 @@ __global__ void k_pack_upper(AllLevels A, lzb_field f, int64_t ncells, const int
 // level-(D-1) patch writes its record and its 9 leaves' (10 consecutive
 // slots); one thread per cell of the levels above.
 __global__ void k_record_sizes_patches(AllLevels A, int64_t* __restrict__ sizes) {
+    lzb_pdl_enter();
     const int D = A.D;
     const LevelView& C = A.L[D - 1];
     const LevelView& F = A.L[D];
@@ -1672,6 +1761,7 @@ __global__ void k_record_sizes_patches(AllLevels A, int64_t* __restrict__ sizes)
     }
 }
 __global__ void k_record_sizes_upper(AllLevels A, int64_t ncells, int64_t* __restrict__ sizes) {
+    lzb_pdl_enter();
     int64_t t = gtid();
     if (t >= ncells) return;
     int l = 0;
@@ -1688,10 +1778,81 @@ __global__ void k_record_sizes_upper(AllLevels A, int64_t ncells, int64_t* __res
     sizes[slot_at(A.st, l, cx, cy)] = record_size(p1, p1 != LZB_P1_BOTTOM ? L.p3[c] : 0, false);
 }
 
+// ---- the small levels of the cycle in one block: levels 0..lc ((N+1)^2 <=
+// 100 vertices each) run the per-vertex bodies of the per-level kernels in
+// the same order, a block barrier between passes (global writes of the block
+// are visible to it after __syncthreads). Bit-identical to the per-level
+// launches.
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallMaxN = 9;
+struct Damp {
+    double d[kMaxLevels];
+};
+#define LZB_FOR_VERTS(L, i) for (int64_t i = threadIdx.x; i < static_cast<int64_t>((L).N + 1) * ((L).N + 1); i += blockDim.x)
+
+// residual_pass of levels lc..0 (uhat, residual, restriction per level)
+__global__ void __launch_bounds__(kSmallThreads) k_small_front(AllLevels A, int lc, lzb_field f) {
+    lzb_pdl_enter();
+    for (int l = lc; l >= 0; --l) {
+        const LevelView F = A.L[l], C = A.L[l > 0 ? l - 1 : 0];
+        LZB_FOR_VERTS(F, i) k_uhat_body<true>(i, F, C, l > 0 ? 1 : 0);
+        __syncthreads();
+        LZB_FOR_VERTS(F, i) k_residual_body<true>(i, F, f);
+        __syncthreads();
+        if (l > 0) {
+            LZB_FOR_VERTS(C, i) k_restrict_body<true>(i, F, C, 0, 0.0);
+            __syncthreads();
+        }
+    }
+}
+// snapshots of levels 0..lc (update_pass prologue)
+__global__ void __launch_bounds__(kSmallThreads) k_small_snap(AllLevels A, int lc) {
+    lzb_pdl_enter();
+    for (int l = 0; l <= lc; ++l) LZB_FOR_VERTS(A.L[l], i) k_snap_body<true>(i, A.L[l]);
+}
+// update_pass of levels lc..0, then the prolongation of levels 1..lc
+__global__ void __launch_bounds__(kSmallThreads) k_small_back(AllLevels A, int lc, int variant, double omega,
+                                                               Damp dm, lzb_field f) {
+    lzb_pdl_enter();
+    for (int l = lc; l >= 0; --l) {
+        const LevelView F = A.L[l];
+        if (variant != LZB_ADDITIVE && l > 0) {
+            const LevelView C = A.L[l - 1];
+            if (variant == LZB_ADAFAC_PI) {
+                LZB_FOR_VERTS(C, i) k_aux_inject_body<true>(i, F, C);
+                __syncthreads();
+            } else {
+                LZB_FOR_VERTS(F, i) k_aux_Ar_body<true>(i, F, f);
+                __syncthreads();
+                LZB_FOR_VERTS(C, i) k_restrict_body<true>(i, F, C, 1, omega);
+                __syncthreads();
+            }
+            LZB_FOR_VERTS(F, i) k_aux_sub_body<true>(i, F, C, omega);
+            __syncthreads();
+        }
+        LZB_FOR_VERTS(F, i) k_jacobi_body<true>(i, F, dm.d[l]);
+        __syncthreads();
+    }
+    for (int l = 1; l <= lc; ++l) {
+        LZB_FOR_VERTS(A.L[l], i) k_prolong_body<true>(i, A.L[l], A.L[l - 1]);
+        __syncthreads();
+    }
+}
+// injection of levels lc..1 into lc-1..0
+__global__ void __launch_bounds__(kSmallThreads) k_small_inject(AllLevels A, int lc) {
+    lzb_pdl_enter();
+    for (int l = lc; l >= 1; --l) {
+        LZB_FOR_VERTS(A.L[l - 1], i) k_inject_body<true>(i, A.L[l], A.L[l - 1]);
+        __syncthreads();
+    }
+}
+#undef LZB_FOR_VERTS
+
 // CellStream::load record (stream.cpp:355-392); offsets from the host parse.
 __global__ void k_unpack(LevelView L, lzb_field f, int level, int leaf, SlotTable st,
                          const int64_t* __restrict__ offsets, const uint8_t* __restrict__ in,
                          double delta_max, uint32_t cycle, unsigned long long* stats, int* err) {
+    lzb_pdl_enter();
     int64_t c = gtid();
     if (c >= static_cast<int64_t>(L.N) * L.N) return;
     int cx = static_cast<int>(c % L.N), cy = static_cast<int>(c / L.N);
@@ -1762,6 +1923,7 @@ __global__ void k_unpack(LevelView L, lzb_field f, int level, int leaf, SlotTabl
 // Single-cell protocol ops for the per-cell compatibility API.
 __global__ void k_publish_one(LevelView F, lzb_field f, int c, const double* m, int n, int32_t p1,
                               double delta_max, uint32_t cycle, unsigned long long* stats, int* err) {
+    lzb_pdl_enter();
     if (gtid() != 0) return;
     double e = centre_eps(f, F, c % F.N, c / F.N);
     if (!publish_leaf(F, c, m, n, e, delta_max, cycle, stats)) atomicExch(err, 1);
@@ -1772,6 +1934,7 @@ __global__ void k_publish_one(LevelView F, lzb_field f, int c, const double* m, 
 __global__ void k_step_one(LevelView F, lzb_field f, int c, int schedule, int n_max, double term_c,
                            double delta_max, uint32_t cycle, int fast, unsigned long long* stats,
                            int* err) {
+    lzb_pdl_enter();
     if (gtid() != 0) return;
     int cx = c % F.N, cy = c / F.N;
     int32_t p1 = F.p1[c];
@@ -1813,6 +1976,7 @@ __global__ void k_step_one(LevelView F, lzb_field f, int c, int schedule, int n_
 }
 
 __global__ void k_clear_p2(LevelView F, const int32_t* list, int count) {
+    lzb_pdl_enter();
     int64_t t = gtid();
     if (t < count) F.p2[list[t]] = 0;
 }
@@ -1823,6 +1987,7 @@ __global__ void k_step_generic(LevelView F, LevelView D, lzb_field f, const int3
                                const int32_t* snap, const int* count_ptr, int n_main, int schedule,
                                int n_max, int fast, double term_c, double delta_max, uint32_t cycle,
                                unsigned long long* stats, int* err) {
+    lzb_pdl_enter();
     int64_t t = gtid();
     if (t >= *count_ptr) return;
     const int32_t p1 = snap[t];
@@ -1861,6 +2026,7 @@ __global__ void k_step_generic(LevelView F, LevelView D, lzb_field f, const int3
 // completes (p2 cleared, assembly.cpp:66-68).
 __global__ void k_commit(LevelView F, LevelView S, const int32_t* list, const int* count_ptr,
                          uint32_t cycle) {
+    lzb_pdl_enter();
     int64_t t = gtid();
     if (t >= *count_ptr) return;
     const int c = list[t];
@@ -1880,6 +2046,7 @@ __global__ void k_commit(LevelView F, LevelView S, const int32_t* list, const in
 }
 
 __global__ void k_reset_stats(Result* r) {
+    lzb_pdl_enter();
     // per-cycle slots; the norm is written by k_norm_final
     if (threadIdx.x < 13 || threadIdx.x == S_PENDING) r->s[threadIdx.x] = 0;
 }
@@ -2370,8 +2537,14 @@ public:
     // residual pass + stats + result copy) and (update + prolongation +
     // injection). All kernel arguments are stable per grid; the epoch and the
     // result travel through pinned host memory read/written at replay time.
+    struct PdlScope {  // programmatic dependent launches for the cycle bodies
+        bool prev;
+        PdlScope() : prev(g_pdl) { g_pdl = std::getenv("LZB_NO_PDL") == nullptr; }
+        ~PdlScope() { g_pdl = prev; }
+    };
     void run_graph(cudaGraphExec_t& exec, void (Grid::*body)()) {
         if (!use_graphs_) {
+            PdlScope pdl;
             (this->*body)();
             return;
         }
@@ -2381,6 +2554,7 @@ public:
             const uint64_t l0 = g_launches.load();
             LZB_CUDA(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal));
             try {
+                PdlScope pdl;
                 (this->*body)();
             } catch (...) {
                 cudaStreamEndCapture(s_, &g);
@@ -2403,8 +2577,9 @@ public:
         LZB_CUDA(cudaMemcpyAsync(herr_, ctx_->err.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
     }
     void back_body() {  // update + prolongation + injection
-        update_launches(true);
-        prolong_launches(D_ - 1);
+        update_launches(true, true);
+        for (int l = std::max(small_lc(), 0) + 1; l <= D_ - 1; ++l)
+            LZB_LAUNCH(k_prolong, vgrid(l), kThreads, 0, s_, V(l), V(l - 1));
         const bool pi = d_.variant == LZB_ADAFAC_PI;
         if (pi) LZB_LAUNCH(k_scale_aux, vgrid(D_ - 1), kThreads, 0, s_, V(D_ - 1), d_.omega, caux_.p);
         LZB_LAUNCH(k_update_fine, vgrid(D_), kThreads, 0, s_, V(D_), V(D_ - 1), pi ? caux_.p : nullptr,
@@ -2523,8 +2698,17 @@ public:
         }
     }
 
+    // levels 0..small_lc() run fused in one block (k_small_*); -1: none
+    int small_lc() const {
+        static const int maxn = std::getenv("LZB_SMALL_MAXN") ? std::atoi(std::getenv("LZB_SMALL_MAXN")) : kSmallMaxN;
+        int lc = -1;
+        while (lc + 1 <= D_ - 1 && L_[lc + 1].N <= maxn) ++lc;
+        return lc;
+    }
+
     void residual_launches() {  // solver.cpp:145-210
-        for (int l = D_; l >= 0; --l) {
+        const int lc = small_lc();
+        for (int l = D_; l > lc; --l) {
             const dim3 g = vgrid(l);
             LZB_LAUNCH(k_uhat, g, kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
             if (l == D_) leaf_residual(0, L_[D_].N + 1);
@@ -2533,6 +2717,7 @@ public:
                 LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l),
                            V(l - 1), 0, 0.0);
         }
+        if (lc >= 0) LZB_LAUNCH(k_small_front, 1, kSmallThreads, 0, s_, all_levels(), lc, d_.field);
         LZB_LAUNCH(k_norm_partial, kNormBlocks, kThreads, 0, s_, V(D_), 0, L_[D_].N + 1, partial_.p);
         LZB_LAUNCH(k_norm_final, 1, kNormFinalThreads, 0, s_, partial_.p, kNormBlocks, res_.p);
     }
@@ -2550,13 +2735,17 @@ public:
 
     // fuse_fine: the leaf level's Jacobi step (and, for adaFAC-PI, its aux
     // correction) is left to k_update_fine at the end of the back graph.
-    void update_launches(bool fuse_fine = false) {  // solver.cpp:212-313
+    // small: levels 0..small_lc() in k_small_snap / k_small_back, which also
+    // prolongates levels 1..small_lc() (the caller prolongates the rest).
+    void update_launches(bool fuse_fine = false, bool small = false) {  // solver.cpp:212-313
         const double omega = d_.omega;
+        const int lc = small ? small_lc() : -1;
         // usnap / aux of the leaf level are never read (prolongation reads the
         // coarse snapshots; adaFAC-Jac rewrites the leaf aux before use)
-        for (int l = 0; l < D_; ++l)
+        if (lc >= 0) LZB_LAUNCH(k_small_snap, 1, kSmallThreads, 0, s_, all_levels(), lc);
+        for (int l = lc + 1; l < D_; ++l)
             LZB_LAUNCH(k_snap, blocks_for(L_[l].nv, kThreads), kThreads, 0, s_, V(l));
-        for (int l = D_; l >= 0; --l) {
+        for (int l = D_; l > lc; --l) {
             bool aux = d_.variant != LZB_ADDITIVE && l > 0;
             const dim3 g = vgrid(l);
             if (aux) {
@@ -2572,6 +2761,12 @@ public:
             }
             if (!(fuse_fine && l == D_)) LZB_LAUNCH(k_jacobi, g, kThreads, 0, s_, V(l), damping(l));
         }
+        if (lc >= 0) {
+            Damp dm{};
+            for (int l = 0; l <= lc; ++l) dm.d[l] = damping(l);
+            LZB_LAUNCH(k_small_back, 1, kSmallThreads, 0, s_, all_levels(), lc, static_cast<int>(d_.variant), omega,
+                       dm, d_.field);
+        }
     }
 
     void prolong_launches(int lmax = -1) {
@@ -2581,8 +2776,10 @@ public:
     }
 
     void inject() {
-        for (int l = D_; l >= 1; --l)
+        const int lc = small_lc();
+        for (int l = D_; l >= std::max(lc, 0) + 1; --l)
             LZB_LAUNCH(k_inject, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1));
+        if (lc >= 1) LZB_LAUNCH(k_small_inject, 1, kSmallThreads, 0, s_, all_levels(), lc);
     }
 
     void fetch_result() {

@@ -14,6 +14,7 @@
 namespace lzb {
 
 std::atomic<uint64_t> g_launches{0};
+thread_local bool g_pdl = false;
 static thread_local std::string t_last_error;
 
 void set_last_error(const std::string& msg) { t_last_error = msg; }
