@@ -219,6 +219,16 @@ int lzb_grid3_set_slab(lzb_grid3* g, int v0, int v1);
 int lzb_grid3_dist_phase(lzb_grid3* g, int phase);
 int lzb_grid3_dist_result(lzb_grid3* g, double* norm2);
 int lzb_grid3_dist_report(lzb_grid3* g, double norm2, lzb_cycle_report* out);
+/* z-slab sharded 3D assembly (parallel.distributed_assemble3): fixed-p
+ * assembly of the leaf cells in z planes [cz0, cz1); the Galerkin coarse
+ * operators of `level` for its coarse cells in z planes [pz0, pz1); every
+ * coarse level below `level` from it; the device class planes of a level
+ * (27 planes of N^3 doubles, value q of cell c at q * N^3 + c) for the
+ * all-gather. Restated 3D form of assembly.cpp:111-118 / solver.cpp:59-77. */
+int lzb_grid3_assemble_planes(lzb_grid3* g, int n, int cz0, int cz1);
+int lzb_grid3_galerkin_planes(lzb_grid3* g, int level, int pz0, int pz1);
+int lzb_grid3_coarse_below(lzb_grid3* g, int level);
+int lzb_grid3_level_ops(lzb_grid3* g, int level, void** ptr);
 /* Average device ms of one leaf-level 3D cycle kernel (LZB_TK_UHAT .. LZB_TK_PROLONG). */
 int lzb_grid3_time_kernel(lzb_grid3* g, int what, int reps, double* avg_ms);
 int lzb_grid3_device_view(lzb_grid3* g, int level, int field, void** ptr);

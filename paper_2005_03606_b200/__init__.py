@@ -135,6 +135,10 @@ def lib():
         L.lzb_grid3_dist_phase.argtypes = [vp, C.c_int]
         L.lzb_grid3_dist_result.argtypes = [vp, C.POINTER(C.c_double)]
         L.lzb_grid3_dist_report.argtypes = [vp, C.c_double, C.POINTER(CycleReport)]
+        L.lzb_grid3_assemble_planes.argtypes = [vp, C.c_int, C.c_int, C.c_int]
+        L.lzb_grid3_galerkin_planes.argtypes = [vp, C.c_int, C.c_int, C.c_int]
+        L.lzb_grid3_coarse_below.argtypes = [vp, C.c_int]
+        L.lzb_grid3_level_ops.argtypes = [vp, C.c_int, C.POINTER(vp)]
         L.lzb_grid3_time_kernel.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.lzb_grid3_device_view.argtypes = [vp, C.c_int, C.c_int, C.POINTER(vp)]
         L.lzb_grid_plane_arrays.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(C.c_int)]
@@ -587,6 +591,20 @@ class Grid3:
         _check(lib().lzb_grid3_create_planes(self.ctx.h, depth, C.byref(field), delta_max, fixed_p3, plane_width,
                                              C.byref(h)))
         self.h = h
+
+    def assemble_planes(self, n, cz0, cz1):
+        _check(lib().lzb_grid3_assemble_planes(self.h, n, cz0, cz1))
+
+    def galerkin_planes(self, level, pz0, pz1):
+        _check(lib().lzb_grid3_galerkin_planes(self.h, level, pz0, pz1))
+
+    def coarse_below(self, level):
+        _check(lib().lzb_grid3_coarse_below(self.h, level))
+
+    def level_ops_ptr(self, level) -> int:
+        p = C.c_void_p()
+        _check(lib().lzb_grid3_level_ops(self.h, level, C.byref(p)))
+        return p.value
 
     def time_kernel(self, what, reps=10) -> float:
         """Average device ms of one leaf-level cycle kernel (TK_* id), CUDA events on the solve stream."""

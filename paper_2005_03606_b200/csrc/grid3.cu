@@ -435,10 +435,11 @@ __device__ __forceinline__ int choose_precision_regular(const double* v, double 
 __global__ void __launch_bounds__(128, 4) k_assemble3(Field3 F, int N, double h, AxisTab3 T, double delta_max,
                                                       int fixed_p3, double* __restrict__ op, Planes3 PL, int W,
                                                       int8_t* __restrict__ p3o, int32_t* __restrict__ no,
-                                                      unsigned long long* stats, int* err, int* wide) {
-    const int64_t c = gtid();
+                                                      unsigned long long* stats, int* err, int* wide,
+                                                      int64_t cbeg, int64_t cend) {
+    const int64_t c = cbeg + gtid();  // cells [cbeg, cend): whole z planes
     const int64_t nc = static_cast<int64_t>(N) * N * N;
-    if (c >= nc) return;
+    if (c >= cend) return;
     const int cx = static_cast<int>(c % N), cy = static_cast<int>((c / N) % N), cz = static_cast<int>(c / N / N);
     const double x0 = cx * h, y0 = cy * h, z0 = cz * h;
     const double e = centre_eps3(F, x0, y0, z0, h);
@@ -900,13 +901,13 @@ __global__ void k3_inject(Lv3 F, Lv3 C) {
 constexpr int kW3 = 27 * 27 * 27;
 template <class Src>
 __global__ void __launch_bounds__(256) k3_galerkin(double* __restrict__ cop, Src S, int Nc,
-                                                   const double* __restrict__ W) {
+                                                   const double* __restrict__ W, int64_t cbeg, int64_t cend) {
     extern __shared__ double sW[];
     for (int i = threadIdx.x; i < kW3; i += blockDim.x) sW[i] = W[i];
     __syncthreads();
-    const int64_t c = gtid();
+    const int64_t c = cbeg + gtid();  // coarse cells [cbeg, cend)
     const int64_t ncc = static_cast<int64_t>(Nc) * Nc * Nc;
-    if (c >= ncc) return;
+    if (c >= cend) return;
     const int px = static_cast<int>(c % Nc), py = static_cast<int>((c / Nc) % Nc), pz = static_cast<int>(c / Nc / Nc);
     const int Nf = 3 * Nc;
     double out[27];
@@ -1079,13 +1080,57 @@ public:
         LZB_CUDA(cudaStreamSynchronize(s_));
     }
 
-    void assemble_fixed(int n) {
+    void assemble_fixed(int n) { assemble_planes(n, 0, N_); }
+
+    // Fixed-p assembly of the leaf cells in z planes [cz0, cz1) (a z-slab of
+    // the distributed assembly; cells are independent, no exchange).
+    void assemble_planes(int n, int cz0, int cz1) {
         if (n < 1 || n > kMaxN3) throw Error(LZB_ERR_INVALID, "3D sub-samples per axis must be in 1..16");
+        if (cz0 < 0 || cz1 > N_ || cz0 > cz1) throw Error(LZB_ERR_INVALID, "bad z plane range");
         ops_dirty_ = true;
         const AxisTab3 T = axis_tab3(n);
-        LZB_LAUNCH(k_assemble3, blocks_for(nc_, 128), 128, 0, s_, F_, N_, h_, T, delta_, fixed_, op_.p, planes(), W_,
-                   p3_.p, n_.p, stats_.p, ctx_->err.p, wide_.p);
+        const int64_t cb = static_cast<int64_t>(cz0) * N_ * N_, ce = static_cast<int64_t>(cz1) * N_ * N_;
+        if (ce > cb)
+            LZB_LAUNCH(k_assemble3, blocks_for(ce - cb, 128), 128, 0, s_, F_, N_, h_, T, delta_, fixed_, op_.p,
+                       planes(), W_, p3_.p, n_.p, stats_.p, ctx_->err.p, wide_.p, cb, ce);
         n_last_ = n;
+    }
+
+    // Galerkin coarse operators of `level` (from level + 1) for the coarse
+    // cells in z planes [pz0, pz1).
+    void galerkin_planes(int level, int pz0, int pz1) {
+        if (L3_.empty()) throw Error(LZB_ERR_INVALID, "call init_cycle first");
+        if (level < 0 || level >= D_) throw Error(LZB_ERR_INVALID, "bad coarse level");
+        const int N = L3_[level].N;
+        if (pz0 < 0 || pz1 > N || pz0 > pz1) throw Error(LZB_ERR_INVALID, "bad z plane range");
+        const int64_t cb = static_cast<int64_t>(pz0) * N * N, ce = static_cast<int64_t>(pz1) * N * N;
+        if (ce <= cb) return;
+        if (level + 1 == D_) {
+            leaf_cls([&](auto S) {
+                LZB_LAUNCH(k3_galerkin<decltype(S)>, blocks_for(ce - cb, 256), 256, kW3 * sizeof(double), s_,
+                           L3_[level].op.p, S, N, W3_.p, cb, ce);
+            });
+        } else {
+            const Src64 S{L3_[level + 1].op.p,
+                          static_cast<int64_t>(L3_[level + 1].N) * L3_[level + 1].N * L3_[level + 1].N};
+            LZB_LAUNCH(k3_galerkin<Src64>, blocks_for(ce - cb, 256), 256, kW3 * sizeof(double), s_, L3_[level].op.p,
+                       S, N, W3_.p, cb, ce);
+        }
+    }
+
+    // The coarse operators of levels below `level` from it (Galerkin chain);
+    // level D: every coarse level from the leaves. Clears the dirty mark.
+    void coarse_below(int level) {
+        if (L3_.empty()) throw Error(LZB_ERR_INVALID, "call init_cycle first");
+        if (level < 0 || level > D_) throw Error(LZB_ERR_INVALID, "bad level");
+        for (int l = level - 1; l >= 0; --l) galerkin_planes(l, 0, L3_[l].N);
+        ops_dirty_ = false;
+    }
+
+    double* level_ops(int level) const {
+        if (L3_.empty() || level < 0 || level > D_) throw Error(LZB_ERR_INVALID, "bad level");
+        if (level == D_ && W_) throw Error(LZB_ERR_INVALID, "leaf operators are compressed planes");
+        return level == D_ ? op_.p : L3_[level].op.p;
     }
 
     lzb_compression_stats stats() {
@@ -1188,19 +1233,7 @@ public:
 
     // Coarse operators from the leaves (after an assembly): Galerkin, finest first.
     void coarse_ops() {
-        for (int l = D_ - 1; l >= 0; --l) {
-            const int64_t ncl = static_cast<int64_t>(L3_[l].N) * L3_[l].N * L3_[l].N;
-            if (l + 1 == D_) {
-                leaf_cls([&](auto S) {
-                    LZB_LAUNCH(k3_galerkin<decltype(S)>, blocks_for(ncl, 256), 256, kW3 * sizeof(double), s_,
-                               L3_[l].op.p, S, L3_[l].N, W3_.p);
-                });
-            } else {
-                const Src64 S{L3_[l + 1].op.p, static_cast<int64_t>(L3_[l + 1].N) * L3_[l + 1].N * L3_[l + 1].N};
-                LZB_LAUNCH(k3_galerkin<Src64>, blocks_for(ncl, 256), 256, kW3 * sizeof(double), s_, L3_[l].op.p, S,
-                           L3_[l].N, W3_.p);
-            }
-        }
+        for (int l = D_ - 1; l >= 0; --l) galerkin_planes(l, 0, L3_[l].N);
     }
 
     lzb_cycle_report step() {
@@ -1619,6 +1652,27 @@ int lzb_grid3_dist_result(lzb_grid3* g, double* norm2) {
 }
 int lzb_grid3_dist_report(lzb_grid3* g, double norm2, lzb_cycle_report* out) {
     return lzb::guarded([&] { *out = g->g->dist_report(norm2); });
+}
+int lzb_grid3_assemble_planes(lzb_grid3* g, int n, int cz0, int cz1) {
+    return lzb::guarded([&] {
+        g->g->assemble_planes(n, cz0, cz1);
+        g->g->sync();
+    });
+}
+int lzb_grid3_galerkin_planes(lzb_grid3* g, int level, int pz0, int pz1) {
+    return lzb::guarded([&] {
+        g->g->galerkin_planes(level, pz0, pz1);
+        g->g->sync();
+    });
+}
+int lzb_grid3_coarse_below(lzb_grid3* g, int level) {
+    return lzb::guarded([&] {
+        g->g->coarse_below(level);
+        g->g->sync();
+    });
+}
+int lzb_grid3_level_ops(lzb_grid3* g, int level, void** ptr) {
+    return lzb::guarded([&] { *ptr = g->g->level_ops(level); });
 }
 int lzb_grid3_time_kernel(lzb_grid3* g, int what, int reps, double* avg_ms) {
     return lzb::guarded([&] { *avg_ms = g->g->time_kernel(what, reps); });

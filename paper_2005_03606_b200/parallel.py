@@ -241,6 +241,17 @@ class LoopbackComm:
                     if o is not s:
                         o.field(level, fld)[s.c0 * n:s.c1 * n].copy_(src)
 
+    def allgather_planes(self, slabs, level):
+        Nc = 3 ** level
+        views = [device_tensor(s.grid.level_ops_ptr(level), 27 * Nc ** 3, "<f8").view(27, Nc, Nc * Nc)
+                 for s in slabs]
+        with self._ctx():
+            for s, v in zip(slabs, views):
+                p0, p1 = coarse_cell_planes(s)
+                for o in views:
+                    if o is not v:
+                        o[:, p0:p1].copy_(v[:, p0:p1])
+
     def reduce(self, results):
         norm2 = sum(r[0] for r in results)
         slots = [max(r[1][k] for r in results) if k in MAX_SLOTS else sum(r[1][k] for r in results)
@@ -312,6 +323,20 @@ class TorchComm:
         with self._ctx():
             self.allgather_tensor(s.field(level, fld), s.row_elems(level), ranges)
 
+    def allgather_planes(self, slabs, level):
+        import torch.distributed as dist
+        (s,) = slabs
+        world = dist.get_world_size(self.group)
+        Nc = 3 ** level
+        ranges = []
+        for r in range(world):
+            v0, v1 = slab_vertex_rows(s.N, world, r)
+            ranges.append((v0 // 3, min(v1, s.N) // 3))
+        ops = device_tensor(s.grid.level_ops_ptr(level), 27 * Nc ** 3, "<f8")
+        with self._ctx():
+            for q in range(27):  # class plane q: rows of Nc^2 cells, one per coarse z plane
+                self.allgather_tensor(ops[q * Nc ** 3:(q + 1) * Nc ** 3], Nc * Nc, ranges)
+
     def reduce(self, results, device=None):
         import torch
         import torch.distributed as dist
@@ -359,6 +384,26 @@ def dist_cycle(slabs, comm, adafac_pi: bool) -> dict:
             s.grid.dist_phase(5)
         comm.halo(slabs, D, V.V_U, 1)                   # leaf u one row beyond the slab
     return rep
+
+
+def coarse_cell_planes(s) -> tuple[int, int]:
+    """Level-(D-1) cell planes [p0, p1) whose 27 children lie in slab s's leaf cells."""
+    return s.v0 // 3, min(s.v1, s.N) // 3
+
+
+def distributed_assemble3(slabs, comm, n: int):
+    """z-slab sharded 3D assembly (assembly needs no exchange):
+    each slab assembles the leaf cell planes its cycle reads (its vertex
+    planes' cells and one layer below), the Galerkin operators of its
+    level-(D-1) cell planes; one all-gather of the level-(D-1) class planes,
+    then every rank recomputes the (small) levels below. After init_cycle;
+    the result is bit-identical to a one-GPU assembly on the planes read."""
+    for s in slabs:
+        s.grid.assemble_planes(n, max(s.v0 - 1, 0), min(s.v1, s.N))
+        s.grid.galerkin_planes(s.D - 1, *coarse_cell_planes(s))
+    comm.allgather_planes(slabs, slabs[0].D - 1)
+    for s in slabs:
+        s.grid.coarse_below(s.D - 1)
 
 
 def dist_cycle3(slabs, comm, adafac_pi: bool) -> dict:
