@@ -402,6 +402,33 @@ def run_ours(args, world, rank, local):
     del g3
     torch.cuda.empty_cache()
 
+    # BASELINE configs[3] (C4), the assembly half: the adaptive spacetree (level 6 where a
+    # cell meets the ball r = 0.25 about the centre, level 4 elsewhere; hanging nodes
+    # between the leaf levels), eps 100 / 1 with a tanh interface of width 0.01; fixed-p
+    # assembly of every leaf, then the delayed re-assembly of the interface shell at p
+    # doubling 2 -> 16 (the cycle on the adaptive tree is not built yet: DESIGN.md §9)
+    t4 = lzb.Tree3(4, 6, lzb.field3_sphere(), delta_max=1e-8, ctx=ctx)
+    c4 = {"tree": "k=3 spacetree, level 6 where a cell meets |x - (0.5,0.5,0.5)| <= 0.25, level 4 elsewhere",
+          "eps": "100 inside, 1 outside, tanh interface (10-90 %) over 0.01",
+          "leaves": t4.n_leaves, "leaves_per_level": {str(lv): int(t4.per_level[lv]) for lv in (4, 5, 6)},
+          "assembly": [], "shell_delayed": []}
+    for p4 in (1, 2, 4):
+        t4.assemble(p4)
+        tt = timed_steps(lambda: t4.assemble(p4), 2) / 2
+        c4["assembly"].append({"p": p4, "ms": 1e3 * tt, "sub_samples_per_s": t4.n_leaves * p4 ** 3 / tt})
+    t4.assemble(1)
+    c4["shell_leaves"] = t4.set_shell(0.01)
+    for p4 in (2, 4, 8, 16):
+        tt = timed_steps(lambda: t4.assemble_shell(p4), 1)
+        c4["shell_delayed"].append({"p": p4, "ms": 1e3 * tt, "sub_samples_per_s": c4["shell_leaves"] * p4 ** 3 / tt})
+    st4 = t4.stats()
+    c4["p3_histogram"] = list(st4.p3_histogram)
+    c4["record_factor"] = st4.fine_factor_totals
+    c4["not_built"] = "the additive cycle on the adaptive tree (hanging-node interpolation) and its re-refinement"
+    t4.close()
+    del t4
+    torch.cuda.empty_cache()
+
     # BASELINE configs[4] (C5) at its full size: 729^3 = 387 M cells on one GPU
     # (class records: 224 B/cell, ~115 GB resident), GRF eps, p = 2 assembly and
     # adaFAC-PI cycles; under torchrun the cycle runs z-slab distributed (NCCL)
@@ -581,6 +608,7 @@ def run_ours(args, world, rank, local):
         "smoother": smoother,
         "time_to_solution": tts,
         "c3_assembly_3d": c3,
+        "c4_adaptive_assembly": c4,
         "c5_729cubed": c5,
         "strong_slabs": strong,
         "compression": {"p3_histogram": r["p3_hist"], "fine_factor_totals": r["factor"],

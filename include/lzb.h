@@ -229,6 +229,25 @@ int lzb_grid3_assemble_planes(lzb_grid3* g, int n, int cz0, int cz1);
 int lzb_grid3_galerkin_planes(lzb_grid3* g, int level, int pz0, int pz1);
 int lzb_grid3_coarse_below(lzb_grid3* g, int level);
 int lzb_grid3_level_ops(lzb_grid3* g, int level, void** ptr);
+/* BASELINE configs[3] (C4), assembly: a 3D adaptive spacetree refined to
+ * level lmax where a cell meets the ball |x - f->centre| <= f->radius and to
+ * lbase elsewhere (leaves on up to three levels, hanging nodes between them;
+ * the adaptive mesh of mesh.cpp:66-129,236-312 restated in 3D), fixed-p
+ * assembly + 27-class record coding of every leaf, and the delayed
+ * re-assembly of the leaves meeting the interface shell | |x - c| - r | <=
+ * band. Leaves: (level, cx, cy, cz), level-major. */
+typedef struct lzb_tree3 lzb_tree3;
+int lzb_tree3_create(lzb_ctx* ctx, int lbase, int lmax, const lzb_field3* f, double delta_max, int fixed_p3,
+                     lzb_tree3** out);
+int lzb_tree3_destroy(lzb_tree3* t);
+int lzb_tree3_counts(lzb_tree3* t, int64_t* per_level /* [8] */, int64_t* total);
+int lzb_tree3_assemble(lzb_tree3* t, int n);
+int lzb_tree3_set_shell(lzb_tree3* t, double band, int64_t* count);
+int lzb_tree3_assemble_shell(lzb_tree3* t, int n);
+int lzb_tree3_stats(lzb_tree3* t, lzb_compression_stats* out);
+/* leaves [first, first + count): 64 entries (8x8 row-major), p3, n, (level, cx, cy, cz) */
+int lzb_tree3_cells(lzb_tree3* t, int64_t first, int64_t count, double* ops, int32_t* p3, int32_t* n,
+                    int32_t* lxyz);
 /* Average device ms of one leaf-level 3D cycle kernel (LZB_TK_UHAT .. LZB_TK_PROLONG). */
 int lzb_grid3_time_kernel(lzb_grid3* g, int what, int reps, double* avg_ms);
 int lzb_grid3_device_view(lzb_grid3* g, int level, int field, void** ptr);

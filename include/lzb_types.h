@@ -63,14 +63,19 @@ typedef struct lzb_field {
  * reference"). GRF: eps = exp(g), g trilinearly interpolated from a periodic
  * n^3 table (lzb_grf_table), index (i*n + j)*n + k for (x, y, z). EXTRUDED:
  * eps(x, y, z) = the 2D field at (x, y) (tensor-product checks). */
-enum lzb_field3_kind { LZB_F3_CONSTANT = 0, LZB_F3_GRF = 1, LZB_F3_EXTRUDED = 2 };
+enum lzb_field3_kind { LZB_F3_CONSTANT = 0, LZB_F3_GRF = 1, LZB_F3_EXTRUDED = 2, LZB_F3_SPHERE = 3 };
 
+/* SPHERE (BASELINE configs[3]): eps = eps_out + (eps_in - eps_out) s(t),
+ * t = (radius - |x - centre|) / width, s(t) = (1 + tanh(2 atanh(0.8) t)) / 2,
+ * so eps passes from 10 % to 90 % of the jump across the interface width. */
 typedef struct lzb_field3 {
     int32_t kind;
     int32_t grf_n;        /* GRF table points per axis (64 for BASELINE)        */
     double value;         /* constant                                           */
     const double* grf;    /* host pointer to grf_n^3 values of g (copied)       */
     lzb_field xy;         /* EXTRUDED                                           */
+    double centre[3];     /* SPHERE                                             */
+    double radius, width, eps_in, eps_out;
 } lzb_field3;
 
 /* ------------------------------------------------------------ right-hand side */

@@ -83,6 +83,38 @@ def eps_grf(table: np.ndarray, x: float, y: float, z: float) -> float:
     return math.exp(lerp(lerp(c00, c01, t[1]), lerp(c10, c11, t[1]), t[0]))
 
 
+def eps_sphere(x, y, z, centre=(0.5, 0.5, 0.5), radius=0.25, width=0.01, eps_in=100.0, eps_out=1.0):
+    """BASELINE configs[3] field (lzb_types.h LZB_F3_SPHERE): eps_out + (eps_in -
+    eps_out) (1 + tanh(2 atanh(0.8) t)) / 2, t = (radius - r) / width."""
+    r = math.sqrt((x - centre[0]) ** 2 + (y - centre[1]) ** 2 + (z - centre[2]) ** 2)
+    t = (radius - r) / width
+    return eps_out + (eps_in - eps_out) * (0.5 * (1.0 + math.tanh(2.1972245773362196 * t)))
+
+
+def sphere_tree_leaves(lbase, lmax, centre=(0.5, 0.5, 0.5), radius=0.25):
+    """Leaves (level, cx, cy, cz) of the adaptive spacetree of BASELINE
+    configs[3]: every cell below lbase refined; below lmax the cells whose box
+    meets the ball |x - centre| <= radius (the restated 3D form of the
+    reference's refine/apply_refinement, mesh.cpp:236-312)."""
+    c = np.asarray(centre, dtype=np.float64)
+    cur = np.zeros((1, 3), np.int64)
+    out = []
+    for lvl in range(lmax + 1):
+        h = (1.0 / 3) ** lvl
+        lo = cur * h
+        near = np.clip(c, lo, lo + h)
+        dist = np.sqrt(((near - c) ** 2).sum(axis=1))
+        refine = np.full(len(cur), lvl < lbase) | ((lvl < lmax) & (dist <= radius))
+        leaves = cur[~refine]
+        out.append(np.column_stack([np.full(len(leaves), lvl), leaves]))
+        par = cur[refine]
+        if not len(par):
+            break
+        d = np.array([(dx, dy, dz) for dz in range(3) for dy in range(3) for dx in range(3)], np.int64)
+        cur = (3 * par[:, None, :] + d[None, :, :]).reshape(-1, 3)
+    return np.concatenate(out)
+
+
 def element3(eps, x0, y0, z0, h, n):
     """sum_ijk eps(x_i, y_j, z_k) K_sub(i,j,k), samples x0 + (i + 0.5) inv h."""
     inv = 1.0 / n

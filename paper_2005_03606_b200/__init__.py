@@ -139,6 +139,14 @@ def lib():
         L.lzb_grid3_galerkin_planes.argtypes = [vp, C.c_int, C.c_int, C.c_int]
         L.lzb_grid3_coarse_below.argtypes = [vp, C.c_int]
         L.lzb_grid3_level_ops.argtypes = [vp, C.c_int, C.POINTER(vp)]
+        L.lzb_tree3_create.argtypes = [vp, C.c_int, C.c_int, C.POINTER(T.Field3), C.c_double, C.c_int, C.POINTER(vp)]
+        L.lzb_tree3_destroy.argtypes = [vp]
+        L.lzb_tree3_counts.argtypes = [vp, vp, C.POINTER(i64)]
+        L.lzb_tree3_assemble.argtypes = [vp, C.c_int]
+        L.lzb_tree3_set_shell.argtypes = [vp, C.c_double, C.POINTER(i64)]
+        L.lzb_tree3_assemble_shell.argtypes = [vp, C.c_int]
+        L.lzb_tree3_stats.argtypes = [vp, C.POINTER(CompressionStats)]
+        L.lzb_tree3_cells.argtypes = [vp, i64, i64, vp, vp, vp, vp]
         L.lzb_grid3_time_kernel.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.lzb_grid3_device_view.argtypes = [vp, C.c_int, C.c_int, C.POINTER(vp)]
         L.lzb_grid_plane_arrays.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(C.c_int)]
@@ -563,6 +571,62 @@ def field3_constant(value=1.0) -> "T.Field3":
 
 def field3_extruded(f2: Field) -> "T.Field3":
     return T.Field3(kind=T.F3_EXTRUDED, grf_n=0, value=1.0, grf=None, xy=f2)
+
+
+def field3_sphere(centre=(0.5, 0.5, 0.5), radius=0.25, width=0.01, eps_in=100.0, eps_out=1.0) -> "T.Field3":
+    """BASELINE configs[3]: eps_in inside the sphere, eps_out outside, a tanh
+    interface whose 10-90 % transition spans `width` (lzb_types.h)."""
+    f = T.Field3(kind=T.F3_SPHERE, grf_n=0, value=1.0, grf=None)
+    f.centre[:] = [float(c) for c in centre]
+    f.radius, f.width, f.eps_in, f.eps_out = radius, width, eps_in, eps_out
+    return f
+
+
+class Tree3:
+    """BASELINE configs[3] assembly on a 3D adaptive spacetree (lzb_tree3_*):
+    level lmax where a cell meets the field's sphere, lbase elsewhere."""
+
+    def __init__(self, lbase, lmax, field, delta_max=1e-8, fixed_p3=0, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.field = field
+        h = C.c_void_p()
+        _check(lib().lzb_tree3_create(self.ctx.h, lbase, lmax, C.byref(field), delta_max, fixed_p3, C.byref(h)))
+        self.h = h
+        per = np.zeros(8, np.int64)
+        tot = C.c_int64()
+        _check(lib().lzb_tree3_counts(self.h, _ptr(per), C.byref(tot)))
+        self.per_level, self.n_leaves = per, tot.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            if _lib is not None:
+                _lib.lzb_tree3_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def assemble(self, n):
+        _check(lib().lzb_tree3_assemble(self.h, n))
+
+    def set_shell(self, band) -> int:
+        c = C.c_int64()
+        _check(lib().lzb_tree3_set_shell(self.h, band, C.byref(c)))
+        return c.value
+
+    def assemble_shell(self, n):
+        _check(lib().lzb_tree3_assemble_shell(self.h, n))
+
+    def stats(self) -> CompressionStats:
+        s = CompressionStats()
+        _check(lib().lzb_tree3_stats(self.h, C.byref(s)))
+        return s
+
+    def cells(self, first, count):
+        ops = np.zeros((count, 8, 8))
+        p3, n = np.zeros(count, np.int32), np.zeros(count, np.int32)
+        lxyz = np.zeros((count, 4), np.int32)
+        _check(lib().lzb_tree3_cells(self.h, first, count, _ptr(ops), _ptr(p3), _ptr(n), _ptr(lxyz)))
+        return ops, p3, n, lxyz
 
 
 def integrate_elements3(field, x0, y0, z0, h, n, ctx: Context | None = None) -> np.ndarray:

@@ -38,7 +38,7 @@ class Field(C.Structure):
 
 
 # 3D field kinds (lzb_types.h, restated extension)
-F3_CONSTANT, F3_GRF, F3_EXTRUDED = range(3)
+F3_CONSTANT, F3_GRF, F3_EXTRUDED, F3_SPHERE = range(4)
 
 
 class Field3(C.Structure):
@@ -48,6 +48,11 @@ class Field3(C.Structure):
         ("value", C.c_double),
         ("grf", C.c_void_p),
         ("xy", Field),
+        ("centre", C.c_double * 3),
+        ("radius", C.c_double),
+        ("width", C.c_double),
+        ("eps_in", C.c_double),
+        ("eps_out", C.c_double),
     ]
 
 

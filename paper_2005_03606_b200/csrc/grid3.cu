@@ -32,7 +32,11 @@ struct Field3 {
     double value;
     const double* grf;  // device, n^3
     lzb_field xy;
+    double cx, cy, cz, radius, width, eps_in, eps_out;  // SPHERE
 };
+
+// 2 atanh(0.8): s(t) = (1 + tanh(k t)) / 2 goes from 0.1 to 0.9 over t in [-1/2, 1/2]
+constexpr double kSphereK = 2.1972245773362196;
 
 // eps for the 3D kinds (lzb_field3); the GRF is exp of the periodic
 // trilinear interpolant of the table, lerp(a, b, t) = (1 - t) a + t b.
@@ -56,6 +60,11 @@ __device__ inline double eps3(const Field3& F, double x, double y, double z) {
         return exp(g);
     }
     if (F.kind == LZB_F3_EXTRUDED) return field_eval(F.xy, x, y);
+    if (F.kind == LZB_F3_SPHERE) {
+        const double dx = x - F.cx, dy = y - F.cy, dz = z - F.cz;
+        const double t = (F.radius - sqrt(dx * dx + dy * dy + dz * dz)) / F.width;
+        return F.eps_out + (F.eps_in - F.eps_out) * (0.5 * (1.0 + tanh(kSphereK * t)));
+    }
     return F.value;
 }
 
@@ -922,7 +931,7 @@ __global__ void __launch_bounds__(256) k3_galerkin(double* __restrict__ cop, Src
         for (int k = 0; k < 27; ++k) {
             const double kv = K27[k];
 #pragma unroll
-            for (int q = 0; q < 27; ++q) out[q] += kv * Wc[k * 27 + q];
+            for (int q = 0; q < 27; ++q) out[q] = __fma_rn(kv, Wc[k * 27 + q], out[q]);  // restated: FMA allowed
         }
     }
 #pragma unroll
@@ -1032,13 +1041,21 @@ Field3 to_device(const lzb_field3& f, DevBuf<double>& table) {
     F.n = f.grf_n;
     F.value = f.value;
     F.xy = f.xy;
+    F.cx = f.centre[0];
+    F.cy = f.centre[1];
+    F.cz = f.centre[2];
+    F.radius = f.radius;
+    F.width = f.width;
+    F.eps_in = f.eps_in;
+    F.eps_out = f.eps_out;
+    if (f.kind == LZB_F3_SPHERE && !(f.width > 0.0)) throw Error(LZB_ERR_INVALID, "sphere interface width must be > 0");
     if (f.kind == LZB_F3_GRF) {
         if (!f.grf || f.grf_n < 2) throw Error(LZB_ERR_INVALID, "GRF field needs a table");
         const size_t n3 = static_cast<size_t>(f.grf_n) * f.grf_n * f.grf_n;
         table.alloc(n3);
         LZB_CUDA(cudaMemcpy(table.p, f.grf, n3 * sizeof(double), cudaMemcpyHostToDevice));
         F.grf = table.p;
-    } else if (f.kind != LZB_F3_CONSTANT && f.kind != LZB_F3_EXTRUDED) {
+    } else if (f.kind != LZB_F3_CONSTANT && f.kind != LZB_F3_EXTRUDED && f.kind != LZB_F3_SPHERE) {
         throw Error(LZB_ERR_INVALID, "unknown 3D field kind");
     }
     return F;

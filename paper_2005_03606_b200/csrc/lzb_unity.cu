@@ -4,3 +4,4 @@
 #include "runtime.cu"
 #include "grid.cu"
 #include "grid3.cu"
+#include "tree3.cu"

@@ -2,6 +2,7 @@
 3D oracle (oracle/port3.py) and the codec: element matrices within 1e-12,
 records bit-exact given the product's own stencils."""
 import ctypes
+import math
 
 import numpy as np
 import pytest
@@ -203,3 +204,40 @@ def test_distributed_assemble3_loopback(world):
             assert np.array_equal(s.grid.vertices(lvl, lzb.T.V_U), ref.vertices(lvl, lzb.T.V_U)), lvl
         a, b = s.grid.vertices(depth, lzb.T.V_U), ref.vertices(depth, lzb.T.V_U)
         assert np.array_equal(a[s.v0:min(s.v1, N + 1)], b[s.v0:min(s.v1, N + 1)])
+
+
+def test_tree3_sphere_leaves_and_elements():
+    """BASELINE configs[3] assembly on the adaptive spacetree: the leaf set of
+    the restated construction (oracle/port3.py sphere_tree_leaves), element
+    matrices of leaves on every level against the literal per-sample
+    restatement (1e-12), records bit-exact given the product's stencils, and
+    the delayed shell re-assembly touching only the interface leaves."""
+    f = lzb.field3_sphere()
+    T3 = lzb.Tree3(1, 3, f, delta_max=1e-8)
+    want = o3.sphere_tree_leaves(1, 3)
+    assert T3.n_leaves == len(want)
+    assert list(T3.per_level[:4]) == list(np.bincount(want[:, 0], minlength=4))
+    T3.assemble(2)
+    ops, p3, n, lxyz = T3.cells(0, T3.n_leaves)
+    assert np.array_equal(lxyz, want.astype(np.int32)) and (n == 2).all()
+    rng = np.random.default_rng(3)
+    pick = np.concatenate([rng.choice(np.where(lxyz[:, 0] == lv)[0], 4, replace=False) for lv in (1, 2, 3)])
+    h = np.array([math.pow(1.0 / 3, lv) for lv in range(8)])[lxyz[pick, 0]]  # libm pow, as the host side
+    x0, y0, z0 = (lxyz[pick, d + 1] * h for d in range(3))
+    K = lzb.integrate_elements3(f, x0, y0, z0, h, 2).reshape(-1, 64)
+    B = lzb.integrate_elements3(f, x0, y0, z0, h, 1).reshape(-1, 64)
+    for i, c in enumerate(pick):
+        lit = o3.element3(o3.eps_sphere, x0[i], y0[i], z0[i], h[i], 2)
+        assert _rel(K[i].reshape(8, 8), lit) < 1e-12
+        sur = K[i] - B[i]
+        assert p3[c] == orc.choose_precision(sur, 1e-8)
+        assert np.array_equal(ops[c].reshape(-1), B[i] + lzb.codec.roundtrip(sur, p3[c]))
+    cnt = T3.set_shell(0.02)
+    assert 0 < cnt < T3.n_leaves
+    T3.assemble_shell(4)
+    ops2, _, n2, _ = T3.cells(0, T3.n_leaves)
+    moved = n2 == 4
+    assert moved.sum() == cnt
+    assert np.array_equal(ops2[~moved], ops[~moved])
+    st = T3.stats()
+    assert st.fine_cells == T3.n_leaves and sum(st.p3_histogram) == T3.n_leaves and st.max_n == 4

@@ -54,3 +54,14 @@ def test_grf_table_statistics():
     lag = int(round(0.05 * 64))
     c = np.mean(g * np.roll(g, lag, axis=0)) / g.var()
     assert 0.35 < c < 0.85
+
+
+def test_sphere_tree_counts():
+    """Leaf counts of the restated adaptive spacetree (level 2 inside the ball,
+    level 1 elsewhere): the 27 level-1 cells all meet the r = 0.25 ball except
+    the 8 corners; the others refine into level-2 leaves."""
+    from oracle import port3 as o3
+    L = o3.sphere_tree_leaves(1, 2)
+    per = np.bincount(L[:, 0], minlength=3)
+    assert per[0] == 0 and per[1] == 8 and per[2] == 19 * 27
+    assert o3.eps_sphere(0.5, 0.5, 0.5) == pytest.approx(100.0) and o3.eps_sphere(0.0, 0.0, 0.0) == pytest.approx(1.0)
