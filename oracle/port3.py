@@ -381,3 +381,237 @@ class Cycle3:
                 V["u"] = np.where(inner, V["u"] + self._interp(l, Cv["u"] - Cv["us"]), V["u"])
             self._inject()
         return {"cycle": self.cycle, "residual": res, "normalized": norm, "status": status}
+
+
+class Cycle3A:
+    """The additive cycle of proj/src/solver.cpp:99-347 on a 3D ADAPTIVE
+    spacetree (BASELINE configs[3]), restated from the reference's 2D adaptive
+    semantics (numpy, dense levels with masks, arrays indexed [z, y, x]):
+    - cells exist under refined parents; a vertex exists at a corner of an
+      existing cell; kinds (mesh.cpp:115-138): dirichlet on the boundary,
+      interior when all 8 surrounding cells of its level exist, else hanging;
+      fine_grid = corner of a leaf;
+    - operators: leaves' element matrices, refined cells' Galerkin products;
+    - fl = the level's own lumped load f h^3/8 per adjacent leaf
+      (solver.cpp:99-118), plus the restricted r-hat of the level above;
+    - a fine vertex belongs to the first REFINED patch in the order of its
+      candidate patches (z, then y, then x, lower coordinate first), the 3D
+      restatement's owner rule (solver.cpp:39-57);
+    - r, r-hat over every existing vertex (hanging ones keep partial sums),
+      zero at dirichlet; restriction of r-hat from owned lattice vertices;
+      norm over fine_grid interior vertices; Jacobi / aux correction /
+      prolongation on interior vertices only;
+    - after a cycle: injection where the fine vertex exists, then hanging
+      vertices from the parent interpolant of the first existing host cell
+      (mesh.cpp:182-224)."""
+
+    def __init__(self, leaves, leaf_ops, lmax, variant="adafac-pi", omega=0.6, rhs_scale=3 * math.pi ** 2, seed=42,
+                 target=1e-10, max_cycles=100):
+        self.D, self.omega, self.variant, self.target, self.max_cycles = lmax, omega, variant, target, max_cycles
+        self.N = [3 ** l for l in range(lmax + 1)]
+        leaves = np.asarray(leaves)
+        leaf_ops = np.asarray(leaf_ops, dtype=np.float64).reshape(-1, 8, 8)
+        self.exist, self.refined = [], []
+        for l in range(lmax + 1):
+            n = self.N[l]
+            self.exist.append(np.zeros((n, n, n), bool))
+            self.refined.append(np.zeros((n, n, n), bool))
+        self.ops = [np.zeros((n, n, n, 8, 8)) for n in self.N]
+        for l in range(lmax + 1):
+            sel = leaves[:, 0] == l
+            cx, cy, cz = leaves[sel, 1], leaves[sel, 2], leaves[sel, 3]
+            self.exist[l][cz, cy, cx] = True
+            self.ops[l][cz, cy, cx] = leaf_ops[sel]
+        # refined cells: the parents of existing cells, level by level from the finest
+        for l in range(lmax, 0, -1):
+            z, y, x = np.nonzero(self.exist[l])
+            self.refined[l - 1][z // 3, y // 3, x // 3] = True
+            self.exist[l - 1][z // 3, y // 3, x // 3] = True
+        for l in range(lmax - 1, -1, -1):
+            self.ops[l] = np.where(self.refined[l][..., None, None], Cycle3._galerkin(self.ops[l + 1]), self.ops[l])
+        self.vexist, self.kind, self.fine = [], [], []
+        for l in range(lmax + 1):
+            n = self.N[l]
+            ve = np.zeros((n + 1,) * 3, bool)
+            cnt = np.zeros((n + 1,) * 3, np.int32)
+            fg = np.zeros((n + 1,) * 3, bool)
+            leaf = self.exist[l] & ~self.refined[l]
+            for a in range(8):
+                ax, ay, az = a & 1, (a >> 1) & 1, a >> 2
+                ve[az:az + n, ay:ay + n, ax:ax + n] |= self.exist[l]
+                cnt[az:az + n, ay:ay + n, ax:ax + n] += self.exist[l]
+                fg[az:az + n, ay:ay + n, ax:ax + n] |= leaf
+            bnd = np.zeros((n + 1,) * 3, bool)
+            bnd[[0, n], :, :] = bnd[:, [0, n], :] = bnd[:, :, [0, n]] = True
+            kind = np.where(~ve, 0, np.where(bnd, 2, np.where(cnt == 8, 1, 3)))
+            self.vexist.append(ve)
+            self.kind.append(kind)
+            self.fine.append(fg)
+        self.own = [None] + [self._owner(l) for l in range(1, lmax + 1)]
+        self.v = []
+        for l in range(lmax + 1):
+            n = self.N[l]
+            self.v.append({k: np.zeros((n + 1,) * 3) for k in ("u", "fl", "r", "rh", "uh", "dg", "aux", "us", "load")})
+        for l in range(lmax + 1):
+            n = self.N[l]
+            u = self.v[l]["u"]
+            for iz, iy, ix in zip(*np.nonzero(self.vexist[l] & (self.kind[l] != 2))):
+                k = _mix(seed ^ _mix((l << 48) ^ (int(ix) << 32) ^ (int(iy) << 16) ^ int(iz)))
+                u[iz, iy, ix] = (4.0 / 3.0) * float(k >> 11) * 2.0 ** -53
+        self._finish()
+        for l in range(lmax + 1):
+            n = self.N[l]
+            h = (1.0 / 3) ** l
+            w = h * h * h / 8.0
+            leaf = self.exist[l] & ~self.refined[l]
+            adj = np.zeros((n + 1,) * 3, np.int32)
+            for a in range(8):
+                ax, ay, az = a & 1, (a >> 1) & 1, a >> 2
+                adj[az:az + n, ay:ay + n, ax:ax + n] += leaf
+            g = np.arange(n + 1) * h
+            term = w * (rhs_scale * np.sin(math.pi * g)[None, None, :] * np.sin(math.pi * g)[None, :, None]
+                        * np.sin(math.pi * g)[:, None, None])
+            self.v[l]["load"] = adj * term
+        self.history = []
+        self.cycle = 0
+
+    def _owner(self, l):
+        """Per vertex of level l: (pz, py, px) of its owner patch, lattice (Lz, Ly, Lx), has-owner."""
+        n, nc = self.N[l], self.N[l - 1]
+        f = np.arange(n + 1)
+        # the patches containing lattice coordinate f: f // 3 - 1 (on a patch
+        # boundary) and f // 3, within [0, nc)
+        x0 = np.where((f % 3 == 0) & (f > 0), f // 3 - 1, f // 3)
+        x1 = np.minimum(f // 3, nc - 1)
+        Z, Y, X = np.meshgrid(f, f, f, indexing="ij")
+        shape = (n + 1,) * 3
+        op = [np.zeros(shape, np.int64) for _ in range(3)]
+        has = np.zeros(shape, bool)
+        for cz in (x0, x1):
+            for cy in (x0, x1):
+                for cx in (x0, x1):
+                    pz, py, px = cz[Z], cy[Y], cx[X]
+                    ok = self.refined[l - 1][pz, py, px] & ~has
+                    op[0] = np.where(ok, pz, op[0])
+                    op[1] = np.where(ok, py, op[1])
+                    op[2] = np.where(ok, px, op[2])
+                    has |= ok
+        return op[0], op[1], op[2], Z - 3 * op[0], Y - 3 * op[1], X - 3 * op[2], has
+
+    def _w(self, l, a):
+        pz, py, px, Lz, Ly, Lx, has = self.own[l]
+        ax, ay, az = a & 1, (a >> 1) & 1, a >> 2
+        return (np.where(ax, Lx, 3 - Lx) * np.where(ay, Ly, 3 - Ly) * np.where(az, Lz, 3 - Lz)) / 27.0
+
+    def _interp(self, l, coarse):
+        pz, py, px, Lz, Ly, Lx, has = self.own[l]
+        out = np.zeros_like(coarse, shape=pz.shape)
+        for a in range(8):
+            ax, ay, az = a & 1, (a >> 1) & 1, a >> 2
+            out = out + self._w(l, a) * coarse[pz + az, py + ay, px + ax]
+        return out, has
+
+    def _residual(self, l):
+        n = self.N[l]
+        K = np.where(self.exist[l][..., None, None], self.ops[l], 0.0)
+        V = self.v[l]
+        Au, Auh, dg = (np.zeros_like(V["u"]) for _ in range(3))
+        for row in range(8):
+            rx, ry, rz = row & 1, (row >> 1) & 1, row >> 2
+            for col in range(8):
+                cx, cy, cz = col & 1, (col >> 1) & 1, col >> 2
+                Au[rz:rz + n, ry:ry + n, rx:rx + n] += K[..., row, col] * V["u"][cz:cz + n, cy:cy + n, cx:cx + n]
+                Auh[rz:rz + n, ry:ry + n, rx:rx + n] += K[..., row, col] * V["uh"][cz:cz + n, cy:cy + n, cx:cx + n]
+            dg[rz:rz + n, ry:ry + n, rx:rx + n] += K[..., row, row]
+        keep = self.vexist[l] & (self.kind[l] != 2)
+        V["r"] = np.where(keep, V["fl"] - Au, 0.0)
+        V["rh"] = np.where(keep, V["fl"] - Auh, 0.0)
+        V["dg"] = dg
+
+    def _restrict(self, l):
+        pz, py, px, Lz, Ly, Lx, has = self.own[l]
+        rh = np.where(has, self.v[l]["rh"], 0.0)
+        out = self.v[l - 1]["fl"]
+        for a in range(8):
+            ax, ay, az = a & 1, (a >> 1) & 1, a >> 2
+            np.add.at(out, (pz + az, py + ay, px + ax), self._w(l, a) * rh)
+
+    def _finish(self):
+        for l in range(self.D, 0, -1):  # inject where the fine vertex exists
+            C, F = self.v[l - 1], self.v[l]
+            fe = self.vexist[l][::3, ::3, ::3]
+            C["u"] = np.where(self.vexist[l - 1] & fe, F["u"][::3, ::3, ::3], C["u"])
+        for l in range(1, self.D + 1):  # hanging vertices from the first existing host cell
+            n, nc = self.N[l], self.N[l - 1]
+            u, cu = self.v[l]["u"], self.v[l - 1]["u"]
+            for iz, iy, ix in zip(*np.nonzero(self.kind[l] == 3)):
+                cand = []
+                for i in (ix, iy, iz):
+                    c1 = min(i // 3, nc - 1)
+                    c0 = c1 - 1 if (i % 3 == 0 and c1 > 0) else c1
+                    cand.append((c0, c1))
+                host = None
+                for hx in cand[0]:
+                    for hy in cand[1]:
+                        for hz in cand[2]:
+                            if host is None and self.exist[l - 1][hz, hy, hx]:
+                                host = (hx, hy, hz)
+                hx, hy, hz = host
+                fx, fy, fz = (ix - 3.0 * hx) / 3.0, (iy - 3.0 * hy) / 3.0, (iz - 3.0 * hz) / 3.0
+                val = 0.0
+                for a in range(8):
+                    ax, ay, az = a & 1, (a >> 1) & 1, a >> 2
+                    w = (fx if ax else 1.0 - fx) * (fy if ay else 1.0 - fy) * (fz if az else 1.0 - fz)
+                    if w == 0.0:
+                        continue
+                    val += w * cu[hz + az, hy + ay, hx + ax]
+                u[iz, iy, ix] = val
+
+    def step(self):
+        self.cycle += 1
+        for l in range(self.D + 1):
+            self.v[l]["fl"] = self.v[l]["load"].copy()
+        for l in range(self.D, -1, -1):
+            V = self.v[l]
+            if l > 0:
+                interp, has = self._interp(l, self.v[l - 1]["u"])
+                V["uh"] = np.where(has, V["u"] - interp, V["u"])
+            else:
+                V["uh"] = V["u"].copy()
+            self._residual(l)
+            if l > 0:
+                self._restrict(l)
+        sq = sum(float(np.sum(np.where(self.fine[l] & (self.kind[l] == 1), self.v[l]["r"], 0.0) ** 2))
+                 for l in range(self.D + 1))
+        res = math.sqrt(sq)
+        if not self.history:
+            self.first = res if res > 0 else 1.0
+        self.history.append(res)
+        norm = res / self.first
+        status = 1 if norm <= self.target else (2 if norm >= 1e2 else (3 if self.cycle >= self.max_cycles else 0))
+        if status in (0, 3):
+            for l in range(self.D + 1):
+                self.v[l]["us"] = self.v[l]["u"].copy()
+                self.v[l]["aux"] = np.zeros_like(self.v[l]["u"])
+            for l in range(self.D, -1, -1):
+                V = self.v[l]
+                inner = self.kind[l] == 1
+                if self.variant == "adafac-pi" and l > 0:
+                    Cv = self.v[l - 1]
+                    fe = self.vexist[l][::3, ::3, ::3]
+                    Cv["aux"] = np.where(self.vexist[l - 1] & fe, V["r"][::3, ::3, ::3], 0.0)
+                    cin = self.kind[l - 1] == 1
+                    with np.errstate(divide="ignore", invalid="ignore"):
+                        caux = np.where(cin & (Cv["dg"] != 0), self.omega / Cv["dg"] * Cv["aux"], 0.0)
+                    p, has = self._interp(l, caux)
+                    V["u"] = np.where(inner & has, V["u"] - p, V["u"])
+                damping = self.omega ** (self.D - l + 1) if self.variant == "additive" else self.omega
+                with np.errstate(divide="ignore", invalid="ignore"):
+                    upd = np.where(V["dg"] != 0, damping / V["dg"] * V["r"], 0.0)
+                V["u"] = np.where(inner, V["u"] + upd, V["u"])
+            for l in range(1, self.D + 1):
+                V, Cv = self.v[l], self.v[l - 1]
+                p, has = self._interp(l, Cv["u"] - Cv["us"])
+                V["u"] = np.where((self.kind[l] == 1) & has, V["u"] + p, V["u"])
+            self._finish()
+        return {"cycle": self.cycle, "residual": res, "normalized": norm, "status": status}

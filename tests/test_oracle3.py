@@ -65,3 +65,37 @@ def test_sphere_tree_counts():
     per = np.bincount(L[:, 0], minlength=3)
     assert per[0] == 0 and per[1] == 8 and per[2] == 19 * 27
     assert o3.eps_sphere(0.5, 0.5, 0.5) == pytest.approx(100.0) and o3.eps_sphere(0.0, 0.0, 0.0) == pytest.approx(1.0)
+
+
+def _unit_ops(leaves, eps):
+    """n = 1 trilinear elements eps(centre) K_unit(h) per leaf."""
+    out = np.zeros((len(leaves), 8, 8))
+    for i, (lv, cx, cy, cz) in enumerate(leaves):
+        h = (1.0 / 3) ** lv
+        out[i] = eps((cx + 0.5) * h, (cy + 0.5) * h, (cz + 0.5) * h) * o3.unit_stiffness3(h)
+    return out
+
+
+def test_cycle3a_without_adaptivity_is_cycle3():
+    """The adaptive restatement on a tree refined uniformly to depth 2 is the
+    regular 3D cycle: residual history and u on every level within 1e-12."""
+    leaves = o3.sphere_tree_leaves(2, 2)
+    ops = _unit_ops(leaves, lambda x, y, z: 1.0 + x + 2 * y * z)
+    order = np.lexsort((leaves[:, 1], leaves[:, 2], leaves[:, 3]))  # [z, y, x] raster for Cycle3
+    a = o3.Cycle3A(leaves, ops, 2, seed=7)
+    b = o3.Cycle3(ops[order], 2, seed=7)
+    for _ in range(4):
+        ra, rb = a.step(), b.step()
+        assert ra["residual"] == pytest.approx(rb["residual"], rel=1e-12)
+    for lvl in range(3):
+        assert np.abs(a.v[lvl]["u"] - b.v[lvl]["u"]).max() <= 1e-12
+
+
+def test_cycle3a_sphere_tree_converges():
+    """On the sphere tree (level 3 in the ball, 1 elsewhere, hanging nodes)
+    the adaptive cycle reduces the residual."""
+    leaves = o3.sphere_tree_leaves(1, 3)
+    a = o3.Cycle3A(leaves, _unit_ops(leaves, o3.eps_sphere), 3, seed=3)
+    assert (a.kind[3] == 3).any() and (a.kind[2] == 3).any()
+    reps = [a.step() for _ in range(25)]
+    assert reps[-1]["normalized"] < 0.05, [r["normalized"] for r in reps[::6]]
