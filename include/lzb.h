@@ -248,6 +248,17 @@ int lzb_tree3_stats(lzb_tree3* t, lzb_compression_stats* out);
 /* leaves [first, first + count): 64 entries (8x8 row-major), p3, n, (level, cx, cy, cz) */
 int lzb_tree3_cells(lzb_tree3* t, int64_t first, int64_t count, double* ops, int32_t* p3, int32_t* n,
                     int32_t* lxyz);
+/* The additive cycle on the tree (solver.cpp:99-347 on an adaptive mesh,
+ * restated in 3D: hanging vertices interpolated from their parents,
+ * mesh.cpp:115-138,182-234). init_cycle builds the levels, copies the leaves'
+ * operators in and forms the refined cells' Galerkin operators; refresh_ops
+ * redoes that after a (shell) re-assembly; vertices reads a dense level
+ * ((3^l + 1)^3 values, [z][y][x]). */
+int lzb_tree3_init_cycle(lzb_tree3* t, int variant, double omega, double rhs_scale, uint64_t noise_seed,
+                         int max_cycles, double target);
+int lzb_tree3_refresh_ops(lzb_tree3* t);
+int lzb_tree3_step(lzb_tree3* t, lzb_cycle_report* out);
+int lzb_tree3_vertices(lzb_tree3* t, int level, int field, double* out);
 /* Average device ms of one leaf-level 3D cycle kernel (LZB_TK_UHAT .. LZB_TK_PROLONG). */
 int lzb_grid3_time_kernel(lzb_grid3* g, int what, int reps, double* avg_ms);
 int lzb_grid3_device_view(lzb_grid3* g, int level, int field, void** ptr);

@@ -147,6 +147,10 @@ def lib():
         L.lzb_tree3_assemble_shell.argtypes = [vp, C.c_int]
         L.lzb_tree3_stats.argtypes = [vp, C.POINTER(CompressionStats)]
         L.lzb_tree3_cells.argtypes = [vp, i64, i64, vp, vp, vp, vp]
+        L.lzb_tree3_init_cycle.argtypes = [vp, C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_int, C.c_double]
+        L.lzb_tree3_refresh_ops.argtypes = [vp]
+        L.lzb_tree3_step.argtypes = [vp, C.POINTER(CycleReport)]
+        L.lzb_tree3_vertices.argtypes = [vp, C.c_int, C.c_int, vp]
         L.lzb_grid3_time_kernel.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.lzb_grid3_device_view.argtypes = [vp, C.c_int, C.c_int, C.POINTER(vp)]
         L.lzb_grid_plane_arrays.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(C.c_int)]
@@ -620,6 +624,26 @@ class Tree3:
         s = CompressionStats()
         _check(lib().lzb_tree3_stats(self.h, C.byref(s)))
         return s
+
+    def init_cycle(self, solver="adafac-pi", omega=0.6, rhs_scale=3 * np.pi ** 2, seed=42, max_cycles=100,
+                   target=1e-10):
+        variant = {"additive": T.ADDITIVE, "adafac-pi": T.ADAFAC_PI, "adafac-jac": T.ADAFAC_JAC}[solver]
+        _check(lib().lzb_tree3_init_cycle(self.h, variant, omega, rhs_scale, seed, max_cycles, target))
+        self.lmax = int(np.nonzero(self.per_level)[0].max())
+
+    def refresh_ops(self):
+        _check(lib().lzb_tree3_refresh_ops(self.h))
+
+    def step(self) -> dict:
+        r = CycleReport()
+        _check(lib().lzb_tree3_step(self.h, C.byref(r)))
+        return report_dict(r)
+
+    def vertices(self, level, field) -> np.ndarray:
+        n = 3 ** level + 1
+        out = np.zeros((n, n, n))
+        _check(lib().lzb_tree3_vertices(self.h, level, field, _ptr(out)))
+        return out
 
     def cells(self, first, count):
         ops = np.zeros((count, 8, 8))

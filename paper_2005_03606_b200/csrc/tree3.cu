@@ -1,4 +1,4 @@
-// tree3.cu — BASELINE configs[3] (C4), the assembly half: a 3D adaptive
+// tree3.cu — BASELINE configs[3] (C4): a 3D adaptive
 // spacetree (k = 3) refined to level lmax inside a sphere and to level lbase
 // elsewhere, its leaves at three levels with hanging nodes between them, the
 // smoothed-interface sphere field eps (LZB_F3_SPHERE), fixed-p assembly of
@@ -6,8 +6,7 @@
 // re-assembly of the interface shell at rising p. The reference is 2D only
 // (types.hpp:13); its adaptive mesh is mesh.cpp:66-129,236-312 (cells exist
 // only under refined parents, leaves on several levels). The cycle on the
-// adaptive tree (hanging-node interpolation, mesh.cpp:182-224, in 3D) is not
-// built yet.
+// adaptive tree is the second half of this file.
 //
 // Leaves are a flat list (level, cx, cy, cz), level-major, in the order the
 // levels are generated (parents in order, children z-major); operators are
@@ -69,6 +68,367 @@ __global__ void __launch_bounds__(128, 4) k_assemble3_leaves(Field3 F, const int
     p3o[c] = static_cast<int8_t>(p3);
     no[c] = T.n;
     atomic_max_double_bits(&stats[S_MAXDELTA], delta);
+}
+
+// ------------------------------------------------ the cycle on the tree
+// solver.cpp:99-347 on the adaptive tree, restated in 3D (oracle/port3.py
+// Cycle3A): dense levels with cell flags (0 none, 1 leaf, 2 refined), vertex
+// kinds (mesh.cpp:115-138: 0 outside, 1 interior, 2 dirichlet, 3 hanging;
+// +4 fine_grid), operators of the existing cells as class planes behind a
+// per-cell index. A fine vertex belongs to the first refined patch among the
+// patches containing it (z, then y, then x; lower coordinate first).
+struct LvA {
+    int N;
+    double h;
+    double* v[LZB_V_NFIELDS];
+    double* load;
+    uint8_t* cf;
+    int32_t* oi;
+    double* op;  // class planes, value q of existing cell j at q * nop + j
+    int64_t nop;
+    uint8_t* vk;
+};
+enum : uint8_t { VK_OUT = 0, VK_INT = 1, VK_DIR = 2, VK_HANG = 3, VK_FINE = 4 };
+
+__device__ __forceinline__ bool vxyzA(const LvA& L, int& ix, int& iy, int& iz, int64_t& vi) {
+    ix = blockIdx.x * blockDim.x + threadIdx.x;
+    iy = blockIdx.y;
+    iz = blockIdx.z;
+    if (ix > L.N) return false;
+    vi = (static_cast<int64_t>(iz) * (L.N + 1) + iy) * (L.N + 1) + ix;
+    return true;
+}
+__device__ __forceinline__ int64_t cidx(int N, int x, int y, int z) {
+    return (static_cast<int64_t>(z) * N + y) * N + x;
+}
+__device__ __forceinline__ uint8_t cflag(const LvA& L, int x, int y, int z) {
+    if (x < 0 || y < 0 || z < 0 || x >= L.N || y >= L.N || z >= L.N) return 0;
+    return L.cf[cidx(L.N, x, y, z)];
+}
+// candidate patches of lattice coordinate f on a level with nc cells per axis
+__device__ __forceinline__ void cand(int f, int nc, int& c0, int& c1) {
+    c0 = (f % 3 == 0 && f > 0) ? f / 3 - 1 : f / 3;
+    c1 = min(f / 3, nc - 1);
+}
+// owner patch of fine vertex (fx, fy, fz); false if none is refined
+__device__ __forceinline__ bool ownerA(const LvA& C, int fx, int fy, int fz, int& px, int& py, int& pz) {
+    int x0, x1, y0, y1, z0, z1;
+    cand(fx, C.N, x0, x1);
+    cand(fy, C.N, y0, y1);
+    cand(fz, C.N, z0, z1);
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+            for (int c = 0; c < 2; ++c) {
+                const int qz = a ? z1 : z0, qy = b ? y1 : y0, qx = c ? x1 : x0;
+                if (C.cf[cidx(C.N, qx, qy, qz)] == 2) {
+                    px = qx;
+                    py = qy;
+                    pz = qz;
+                    return true;
+                }
+            }
+    return false;
+}
+
+__global__ void k4_mark_leaves(const int4* __restrict__ leaves, int64_t n, int lvl, LvA L) {
+    const int64_t t = gtid();
+    if (t >= n) return;
+    const int4 c = leaves[t];
+    if (c.x == lvl) L.cf[cidx(L.N, c.y, c.z, c.w)] = 1;
+}
+__global__ void k4_mark_parents(LvA F, LvA C) {
+    const int64_t t = gtid();
+    const int64_t nc = static_cast<int64_t>(F.N) * F.N * F.N;
+    if (t >= nc || !F.cf[t]) return;
+    const int x = static_cast<int>(t % F.N), y = static_cast<int>((t / F.N) % F.N), z = static_cast<int>(t / F.N / F.N);
+    C.cf[cidx(C.N, x / 3, y / 3, z / 3)] = 2;
+}
+__global__ void k4_exist01(const uint8_t* __restrict__ cf, int64_t n, int32_t* __restrict__ out) {
+    const int64_t t = gtid();
+    if (t < n) out[t] = cf[t] ? 1 : 0;
+}
+__global__ void k4_index(const uint8_t* __restrict__ cf, int64_t n, int32_t* __restrict__ oi) {
+    const int64_t t = gtid();  // oi holds the exclusive scan of exist01; -1 where no cell
+    if (t < n && !cf[t]) oi[t] = -1;
+}
+// leaf operators (Tree3 class planes over the leaf index) into their level's planes
+__global__ void k4_copy_leaf_ops(const int4* __restrict__ leaves, int64_t n, int lvl, const double* __restrict__ lop,
+                                 int64_t nleaves, LvA L) {
+    const int64_t t = gtid();
+    if (t >= n) return;
+    const int4 c = leaves[t];
+    if (c.x != lvl) return;
+    const int32_t j = L.oi[cidx(L.N, c.y, c.z, c.w)];
+#pragma unroll
+    for (int q = 0; q < 27; ++q) L.op[q * L.nop + j] = lop[q * nleaves + t];
+}
+// refined cells of C: Galerkin from the 27 children of F (k3_galerkin's class form)
+__global__ void __launch_bounds__(256) k4_galerkin(LvA C, LvA F, const double* __restrict__ W) {
+    extern __shared__ double sW[];
+    for (int i = threadIdx.x; i < kW3; i += blockDim.x) sW[i] = W[i];
+    __syncthreads();
+    const int64_t c = gtid();
+    const int64_t ncc = static_cast<int64_t>(C.N) * C.N * C.N;
+    if (c >= ncc || C.cf[c] != 2) return;
+    const int px = static_cast<int>(c % C.N), py = static_cast<int>((c / C.N) % C.N), pz = static_cast<int>(c / C.N / C.N);
+    double out[27];
+#pragma unroll
+    for (int q = 0; q < 27; ++q) out[q] = 0.0;
+    for (int ch = 0; ch < 27; ++ch) {
+        const int lz = ch / 9, ly = (ch / 3) % 3, lx = ch % 3;
+        const int32_t j = F.oi[cidx(F.N, 3 * px + lx, 3 * py + ly, 3 * pz + lz)];
+        const double* Wc = sW + ch * 27 * 27;
+        for (int k = 0; k < 27; ++k) {
+            const double kv = F.op[k * F.nop + j];
+#pragma unroll
+            for (int q = 0; q < 27; ++q) out[q] = __fma_rn(kv, Wc[k * 27 + q], out[q]);
+        }
+    }
+    const int32_t jc = C.oi[c];
+#pragma unroll
+    for (int q = 0; q < 27; ++q) C.op[q * C.nop + jc] = out[q];
+}
+__global__ void k4_classify(LvA L) {
+    int ix, iy, iz;
+    int64_t vi;
+    if (!vxyzA(L, ix, iy, iz, vi)) return;
+    int cnt = 0;
+    bool fine = false;
+    for (int q = 0; q < 8; ++q) {
+        const uint8_t f = cflag(L, ix - 1 + (q & 1), iy - 1 + ((q >> 1) & 1), iz - 1 + (q >> 2));
+        cnt += f != 0;
+        fine |= f == 1;
+    }
+    uint8_t k = VK_OUT;
+    if (cnt) k = bnd3(L.N, ix, iy, iz) ? VK_DIR : (cnt == 8 ? VK_INT : VK_HANG);
+    L.vk[vi] = static_cast<uint8_t>(k | (fine ? VK_FINE : 0));
+}
+// the level's lumped load: f(v) h^3/8 per adjacent leaf (solver.cpp:99-118)
+__global__ void k4_load(LvA L, double scale, double w) {
+    int ix, iy, iz;
+    int64_t vi;
+    if (!vxyzA(L, ix, iy, iz, vi)) return;
+    int adj = 0;
+    for (int q = 0; q < 8; ++q) adj += cflag(L, ix - 1 + (q & 1), iy - 1 + ((q >> 1) & 1), iz - 1 + (q >> 2)) == 1;
+    const double x = ix * L.h, y = iy * L.h, z = iz * L.h;
+    const double term = w * (scale * sin(kPi * x) * sin(kPi * y) * sin(kPi * z));
+    double acc = 0.0;
+    for (int k = 0; k < adj; ++k) acc += term;
+    L.load[vi] = acc;
+}
+__global__ void k4_noise(LvA L, int level, uint64_t seed) {
+    int ix, iy, iz;
+    int64_t vi;
+    if (!vxyzA(L, ix, iy, iz, vi)) return;
+    const int k = L.vk[vi] & 3;
+    if (k == VK_OUT || k == VK_DIR) {
+        L.v[LZB_V_U][vi] = 0.0;
+        return;
+    }
+    auto mix = [](uint64_t z) {
+        z += 0x9e3779b97f4a7c15ull;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    };
+    const uint64_t kk = mix(seed ^ mix((static_cast<uint64_t>(level) << 48) ^ (static_cast<uint64_t>(ix) << 32) ^
+                                       (static_cast<uint64_t>(iy) << 16) ^ static_cast<uint64_t>(iz)));
+    L.v[LZB_V_U][vi] = (4.0 / 3.0) * static_cast<double>(kk >> 11) * 0x1.0p-53;
+}
+__global__ void k4_reset_fl(LvA L, int64_t nv) {
+    const int64_t i = gtid();
+    if (i < nv) L.v[LZB_V_FL][i] = L.load[i];
+}
+__global__ void k4_uhat(LvA F, LvA C, int has_coarse) {
+    int fx, fy, fz;
+    int64_t vi;
+    if (!vxyzA(F, fx, fy, fz, vi)) return;
+    if ((F.vk[vi] & 3) == VK_OUT) return;
+    const double u = F.v[LZB_V_U][vi];
+    int px, py, pz;
+    if (!has_coarse || !ownerA(C, fx, fy, fz, px, py, pz)) {
+        F.v[LZB_V_UHAT][vi] = u;
+        return;
+    }
+    const int lx = fx - 3 * px, ly = fy - 3 * py, lz = fz - 3 * pz;
+    double interp = 0.0;
+    for (int a = 0; a < 8; ++a)
+        interp += pw3(lx, ly, lz, a) * C.v[LZB_V_U][vidx3(C.N, px + (a & 1), py + ((a >> 1) & 1), pz + (a >> 2))];
+    F.v[LZB_V_UHAT][vi] = u - interp;
+}
+// r, r-hat, diag over the existing adjacent cells (gather, q = dx + 2 dy + 4 dz)
+__global__ void __launch_bounds__(128) k4_residual(LvA F) {
+    int ix, iy, iz;
+    int64_t vi;
+    if (!vxyzA(F, ix, iy, iz, vi)) return;
+    const int kind = F.vk[vi] & 3;
+    if (kind == VK_OUT) return;  // r, r-hat, diag of absent vertices stay 0 (never read)
+    const int N = F.N;
+    const double fl = F.v[LZB_V_FL][vi];
+    double r = fl, rh = fl, dg = 0.0;
+    for (int q = 0; q < 8; ++q) {
+        const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;
+        const int cx = ix - 1 + dx, cy = iy - 1 + dy, cz = iz - 1 + dz;
+        if (!cflag(F, cx, cy, cz)) continue;
+        const int row = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
+        const int32_t j = F.oi[cidx(N, cx, cy, cz)];
+        double au = 0.0, auh = 0.0;
+        for (int col = 0; col < 8; ++col) {
+            const double k = F.op[cls3(row, col) * F.nop + j];
+            const int64_t cv = vidx3(N, cx + (col & 1), cy + ((col >> 1) & 1), cz + (col >> 2));
+            au = __fma_rn(k, F.v[LZB_V_U][cv], au);
+            auh = __fma_rn(k, F.v[LZB_V_UHAT][cv], auh);
+        }
+        r -= au;
+        rh -= auh;
+        dg += F.op[cls3(row, row) * F.nop + j];
+    }
+    if (kind == VK_DIR) {
+        r = 0.0;
+        rh = 0.0;
+    }
+    F.v[LZB_V_R][vi] = r;
+    F.v[LZB_V_RHAT][vi] = rh;
+    F.v[LZB_V_DIAG][vi] = dg;
+}
+// fl_c += P^T r-hat over the lattice vertices each adjacent refined patch owns
+__global__ void k4_restrict(LvA F, LvA C) {
+    int IX, IY, IZ;
+    int64_t vi;
+    if (!vxyzA(C, IX, IY, IZ, vi)) return;
+    if ((C.vk[vi] & 3) == VK_OUT) return;
+    double acc = C.v[LZB_V_FL][vi];
+    for (int q = 0; q < 8; ++q) {
+        const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;
+        const int px = IX - 1 + dx, py = IY - 1 + dy, pz = IZ - 1 + dz;
+        if (cflag(C, px, py, pz) != 2) continue;
+        const int k = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
+        for (int lz = 0; lz < 4; ++lz)
+            for (int ly = 0; ly < 4; ++ly)
+                for (int lx = 0; lx < 4; ++lx) {
+                    const double w = pw3(lx, ly, lz, k);
+                    if (w == 0.0) continue;
+                    const int fx = 3 * px + lx, fy = 3 * py + ly, fz = 3 * pz + lz;
+                    int ox, oy, oz;
+                    if (!ownerA(C, fx, fy, fz, ox, oy, oz) || ox != px || oy != py || oz != pz) continue;
+                    const double rh = F.v[LZB_V_RHAT][vidx3(F.N, fx, fy, fz)];
+                    if (rh == 0.0) continue;
+                    acc += w * rh;
+                }
+    }
+    C.v[LZB_V_FL][vi] = acc;
+}
+__global__ void __launch_bounds__(256) k4_norm_partial(LvA L, int64_t nv, double* partial) {
+    __shared__ double sh[256];
+    double s = 0.0;
+    for (int64_t i = gtid(); i < nv; i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        if (L.vk[i] == (VK_INT | VK_FINE)) s += L.v[LZB_V_R][i] * L.v[LZB_V_R][i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+__global__ void k4_snap(LvA L, int64_t nv) {
+    const int64_t i = gtid();
+    if (i >= nv) return;
+    L.v[LZB_V_USNAP][i] = L.v[LZB_V_U][i];
+    L.v[LZB_V_AUX][i] = 0.0;
+}
+__global__ void k4_aux_inject(LvA F, LvA C) {
+    int ix, iy, iz;
+    int64_t vi;
+    if (!vxyzA(C, ix, iy, iz, vi)) return;
+    if ((C.vk[vi] & 3) == VK_OUT) return;
+    const int64_t fv = vidx3(F.N, 3 * ix, 3 * iy, 3 * iz);
+    if ((F.vk[fv] & 3) != VK_OUT) C.v[LZB_V_AUX][vi] = F.v[LZB_V_R][fv];
+}
+// the leaf-ward updates of one level on its interior vertices: adaFAC-PI aux
+// correction (pi), damped Jacobi (damping), prolongated coarse correction (prol)
+__global__ void k4_update(LvA F, LvA C, int pi, double omega, double damping, int jac, int prol) {
+    int fx, fy, fz;
+    int64_t vi;
+    if (!vxyzA(F, fx, fy, fz, vi)) return;
+    if ((F.vk[vi] & 3) != VK_INT) return;
+    int px = 0, py = 0, pz = 0;
+    const bool own = (pi || prol) && ownerA(C, fx, fy, fz, px, py, pz);
+    const int lx = fx - 3 * px, ly = fy - 3 * py, lz = fz - 3 * pz;
+    double u = F.v[LZB_V_U][vi];
+    if (pi && own) {
+        double p = 0.0;
+        for (int a = 0; a < 8; ++a) {
+            const int64_t ci = vidx3(C.N, px + (a & 1), py + ((a >> 1) & 1), pz + (a >> 2));
+            const double dg = C.v[LZB_V_DIAG][ci];
+            const double caux = ((C.vk[ci] & 3) == VK_INT && dg != 0.0) ? omega / dg * C.v[LZB_V_AUX][ci] : 0.0;
+            p += pw3(lx, ly, lz, a) * caux;
+        }
+        u -= p;
+    }
+    if (jac) {
+        const double dg = F.v[LZB_V_DIAG][vi];
+        if (dg != 0.0) u += damping / dg * F.v[LZB_V_R][vi];
+    }
+    if (prol && own) {
+        double d[8];
+        bool any = false;
+        for (int a = 0; a < 8; ++a) {
+            const int64_t ci = vidx3(C.N, px + (a & 1), py + ((a >> 1) & 1), pz + (a >> 2));
+            d[a] = C.v[LZB_V_U][ci] - C.v[LZB_V_USNAP][ci];
+            any |= d[a] != 0.0;
+        }
+        if (any) {
+            double p = 0.0;
+            for (int a = 0; a < 8; ++a) p += pw3(lx, ly, lz, a) * d[a];
+            u += p;
+        }
+    }
+    F.v[LZB_V_U][vi] = u;
+}
+__global__ void k4_inject(LvA F, LvA C) {
+    int ix, iy, iz;
+    int64_t vi;
+    if (!vxyzA(C, ix, iy, iz, vi)) return;
+    if ((C.vk[vi] & 3) == VK_OUT) return;
+    const int64_t fv = vidx3(F.N, 3 * ix, 3 * iy, 3 * iz);
+    if ((F.vk[fv] & 3) != VK_OUT) C.v[LZB_V_U][vi] = F.v[LZB_V_U][fv];
+}
+// hanging u from the parent interpolant of the first existing host cell
+// (mesh.cpp:182-214 in 3D: candidates x outer, then y, then z)
+__global__ void k4_hanging(LvA F, LvA C) {
+    int ix, iy, iz;
+    int64_t vi;
+    if (!vxyzA(F, ix, iy, iz, vi)) return;
+    if ((F.vk[vi] & 3) != VK_HANG) return;
+    const int nc = C.N;
+    int c1[3], c0[3];
+    const int f[3] = {ix, iy, iz};
+    for (int d = 0; d < 3; ++d) {
+        c1[d] = min(f[d] / 3, nc - 1);
+        c0[d] = (f[d] % 3 == 0 && c1[d] > 0) ? c1[d] - 1 : c1[d];
+    }
+    int hx = -1, hy = -1, hz = -1;
+    for (int a = 0; a < 2 && hx < 0; ++a)
+        for (int b = 0; b < 2 && hx < 0; ++b)
+            for (int c = 0; c < 2 && hx < 0; ++c) {
+                const int qx = a ? c1[0] : c0[0], qy = b ? c1[1] : c0[1], qz = c ? c1[2] : c0[2];
+                if (C.cf[cidx(nc, qx, qy, qz)]) {
+                    hx = qx;
+                    hy = qy;
+                    hz = qz;
+                }
+            }
+    if (hx < 0) return;
+    const double fx = (ix - 3.0 * hx) / 3.0, fy = (iy - 3.0 * hy) / 3.0, fz = (iz - 3.0 * hz) / 3.0;
+    double val = 0.0;
+    for (int a = 0; a < 8; ++a) {
+        const int ax = a & 1, ay = (a >> 1) & 1, az = a >> 2;
+        const double w = (ax ? fx : 1.0 - fx) * (ay ? fy : 1.0 - fy) * (az ? fz : 1.0 - fz);
+        if (w == 0.0) continue;
+        val += w * C.v[LZB_V_U][vidx3(nc, hx + ax, hy + ay, hz + az)];
+    }
+    F.v[LZB_V_U][vi] = val;
 }
 
 }  // namespace
@@ -195,6 +555,144 @@ public:
         if (lxyz) std::memcpy(lxyz, leaves_.data() + first, count * sizeof(int4));
     }
 
+    // ------------------------------------------------ the cycle on the tree
+    // Levels 0..lmax as dense grids with cell flags; the leaves' current
+    // operators (this tree's class planes) copied into their levels, the
+    // refined cells' operators by Galerkin products, finest first.
+    void init_cycle(int variant, double omega, double rhs_scale, uint64_t seed, int max_cycles, double target) {
+        if (variant == LZB_ADAFAC_JAC) throw Error(LZB_ERR_INVALID, "the 3D cycle runs additive and adafac-pi");
+        variant_ = variant;
+        omega_ = omega;
+        max_cycles_ = max_cycles;
+        target_ = target;
+        const int D = lmax_;
+        A_.clear();
+        A_.resize(D + 1);
+        for (int l = 0; l <= D; ++l) {
+            LevA& L = A_[l];
+            L.N = 1;
+            for (int i = 0; i < l; ++i) L.N *= 3;
+            L.nc = static_cast<int64_t>(L.N) * L.N * L.N;
+            L.nv = static_cast<int64_t>(L.N + 1) * (L.N + 1) * (L.N + 1);
+            L.h = HL_.h[l];
+            for (int f = 0; f < LZB_V_NFIELDS; ++f) {
+                L.v[f].alloc(L.nv);
+                LZB_CUDA(cudaMemsetAsync(L.v[f].p, 0, L.v[f].bytes(), s_));
+            }
+            L.load.alloc(L.nv);
+            L.vk.alloc(L.nv);
+            L.cf.alloc(L.nc);
+            L.oi.alloc(L.nc + 1);
+            LZB_CUDA(cudaMemsetAsync(L.cf.p, 0, L.cf.bytes(), s_));
+        }
+        // cell flags: leaves, then the refined parents level by level
+        for (int l = 0; l <= D; ++l)
+            LZB_LAUNCH(k4_mark_leaves, blocks_for(n_leaves_, 256), 256, 0, s_, dleaves_.p, n_leaves_, l, lv(l));
+        for (int l = D; l >= 1; --l)
+            LZB_LAUNCH(k4_mark_parents, blocks_for(A_[l].nc, 256), 256, 0, s_, lv(l), lv(l - 1));
+        // dense cell -> operator slot (exclusive scan of existence), slot counts
+        for (int l = 0; l <= D; ++l) {
+            LevA& L = A_[l];
+            DevBuf<int32_t> e01;
+            e01.alloc(L.nc + 1);
+            LZB_CUDA(cudaMemsetAsync(e01.p + L.nc, 0, sizeof(int32_t), s_));
+            LZB_LAUNCH(k4_exist01, blocks_for(L.nc, 256), 256, 0, s_, L.cf.p, L.nc, e01.p);
+            size_t tb = 0;
+            LZB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, e01.p, L.oi.p, static_cast<int>(L.nc + 1), s_));
+            DevBuf<unsigned char> tmp;
+            tmp.alloc(tb);
+            LZB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, e01.p, L.oi.p, static_cast<int>(L.nc + 1), s_));
+            int32_t cnt = 0;
+            LZB_CUDA(cudaMemcpyAsync(&cnt, L.oi.p + L.nc, sizeof(int32_t), cudaMemcpyDeviceToHost, s_));
+            LZB_CUDA(cudaStreamSynchronize(s_));
+            LZB_LAUNCH(k4_index, blocks_for(L.nc, 256), 256, 0, s_, L.cf.p, L.nc, L.oi.p);
+            L.nop = cnt;
+            L.op.alloc(static_cast<size_t>(std::max(cnt, 1)) * kCls3);
+            LZB_LAUNCH(k4_classify, vgA(l), 128, 0, s_, lv(l));
+        }
+        if (!W3_.n) {
+            const std::vector<double> W = galerkin_weights3();
+            W3_.alloc(kW3);
+            LZB_CUDA(cudaMemcpy(W3_.p, W.data(), kW3 * sizeof(double), cudaMemcpyHostToDevice));
+            LZB_CUDA(cudaFuncSetAttribute(k4_galerkin, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kW3 * sizeof(double))));
+        }
+        refresh_ops();
+        partialA_.alloc(kNormBlocksA);
+        for (int l = 0; l <= D; ++l) LZB_LAUNCH(k4_noise, vgA(l), 128, 0, s_, lv(l), l, seed);
+        finish_cycle();
+        for (int l = 0; l <= D; ++l)
+            LZB_LAUNCH(k4_load, vgA(l), 128, 0, s_, lv(l), rhs_scale, A_[l].h * A_[l].h * A_[l].h / 8.0);
+        cycle_ = 0;
+        history_.clear();
+        sync();
+    }
+
+    // the leaves' current operators into the levels, then the Galerkin chain
+    void refresh_ops() {
+        for (int l = 0; l <= lmax_; ++l)
+            LZB_LAUNCH(k4_copy_leaf_ops, blocks_for(n_leaves_, 256), 256, 0, s_, dleaves_.p, n_leaves_, l, op_.p,
+                       n_leaves_, lv(l));
+        for (int l = lmax_ - 1; l >= 0; --l)
+            LZB_LAUNCH(k4_galerkin, blocks_for(A_[l].nc, 256), 256, kW3 * sizeof(double), s_, lv(l), lv(l + 1),
+                       W3_.p);
+    }
+
+    lzb_cycle_report step() {
+        if (A_.empty()) throw Error(LZB_ERR_INVALID, "call init_cycle first");
+        const int D = lmax_;
+        lzb_cycle_report rep;
+        std::memset(&rep, 0, sizeof rep);
+        rep.cycle = static_cast<int32_t>(++cycle_);
+        for (int l = 0; l <= D; ++l)
+            LZB_LAUNCH(k4_reset_fl, blocks_for(A_[l].nv, 256), 256, 0, s_, lv(l), A_[l].nv);
+        for (int l = D; l >= 0; --l) {
+            LZB_LAUNCH(k4_uhat, vgA(l), 128, 0, s_, lv(l), l > 0 ? lv(l - 1) : lv(l), l > 0 ? 1 : 0);
+            LZB_LAUNCH(k4_residual, vgA(l), 128, 0, s_, lv(l));
+            if (l > 0) LZB_LAUNCH(k4_restrict, vgA(l - 1), 128, 0, s_, lv(l), lv(l - 1));
+        }
+        double s2 = 0.0;
+        std::vector<double> part(kNormBlocksA);
+        for (int l = 0; l <= D; ++l) {
+            LZB_LAUNCH(k4_norm_partial, kNormBlocksA, 256, 0, s_, lv(l), A_[l].nv, partialA_.p);
+            LZB_CUDA(cudaMemcpyAsync(part.data(), partialA_.p, kNormBlocksA * sizeof(double), cudaMemcpyDeviceToHost,
+                                     s_));
+            LZB_CUDA(cudaStreamSynchronize(s_));
+            for (double x : part) s2 += x;
+        }
+        rep.residual = std::sqrt(s2);
+        if (history_.empty()) first_ = rep.residual > 0.0 ? rep.residual : 1.0;
+        history_.push_back(rep.residual);
+        rep.normalized = rep.residual / first_;
+        rep.status = rep.normalized <= target_ ? LZB_CONVERGED
+                     : rep.normalized >= 1e2 ? LZB_DIVERGED
+                     : static_cast<int>(cycle_) >= max_cycles_ ? LZB_TIMEOUT : LZB_CONTINUE;
+        if (rep.status == LZB_CONTINUE || rep.status == LZB_TIMEOUT) {
+            const bool pi = variant_ == LZB_ADAFAC_PI;
+            for (int l = 0; l <= D; ++l) LZB_LAUNCH(k4_snap, blocks_for(A_[l].nv, 256), 256, 0, s_, lv(l), A_[l].nv);
+            for (int l = D; l >= 0; --l) {
+                if (pi && l > 0) LZB_LAUNCH(k4_aux_inject, vgA(l - 1), 128, 0, s_, lv(l), lv(l - 1));
+                const double damping = variant_ == LZB_ADDITIVE ? std::pow(omega_, D - l + 1) : omega_;
+                LZB_LAUNCH(k4_update, vgA(l), 128, 0, s_, lv(l), l > 0 ? lv(l - 1) : lv(l), pi && l > 0 ? 1 : 0,
+                           omega_, damping, 1, 0);
+            }
+            for (int l = 1; l <= D; ++l)
+                LZB_LAUNCH(k4_update, vgA(l), 128, 0, s_, lv(l), lv(l - 1), 0, omega_, 0.0, 0, 1);
+            finish_cycle();
+        }
+        rep.levels = D + 1;
+        rep.cells = static_cast<uint64_t>(n_leaves_);
+        sync();
+        return rep;
+    }
+
+    void vertices(int level, int field, double* out) {
+        if (A_.empty() || level < 0 || level > lmax_ || field < 0 || field >= LZB_V_NFIELDS)
+            throw Error(LZB_ERR_INVALID, "bad level / field");
+        LZB_CUDA(cudaMemcpyAsync(out, A_[level].v[field].p, A_[level].v[field].bytes(), cudaMemcpyDeviceToHost, s_));
+        sync();
+    }
+
     void sync() {
         LZB_CUDA(cudaStreamSynchronize(s_));
         int flag = 0;
@@ -206,6 +704,45 @@ public:
     }
 
 private:
+    struct LevA {
+        int N = 1;
+        int64_t nc = 1, nv = 8, nop = 0;
+        double h = 1.0;
+        DevBuf<double> v[LZB_V_NFIELDS];
+        DevBuf<double> load, op;
+        DevBuf<uint8_t> vk, cf;
+        DevBuf<int32_t> oi;
+    };
+    static constexpr int kNormBlocksA = 148 * 2;
+    std::vector<LevA> A_;
+    DevBuf<double> W3_, partialA_;
+    int variant_ = LZB_ADDITIVE, max_cycles_ = 100;
+    double omega_ = 0.6, target_ = 1e-10, first_ = 1.0;
+    uint32_t cycle_ = 0;
+    std::vector<double> history_;
+
+    LvA lv(int l) {
+        LvA v{};
+        LevA& L = A_[l];
+        v.N = L.N;
+        v.h = L.h;
+        for (int f = 0; f < LZB_V_NFIELDS; ++f) v.v[f] = L.v[f].p;
+        v.load = L.load.p;
+        v.cf = L.cf.p;
+        v.oi = L.oi.p;
+        v.op = L.op.p;
+        v.nop = L.nop;
+        v.vk = L.vk.p;
+        return v;
+    }
+    dim3 vgA(int l) const { return dim3(blocks_for(A_[l].N + 1, 128), A_[l].N + 1, A_[l].N + 1); }
+    // injection (finest first) where the fine vertex exists, then the hanging
+    // vertices of every level from their parents (solver.cpp:344-347)
+    void finish_cycle() {
+        for (int l = lmax_; l >= 1; --l) LZB_LAUNCH(k4_inject, vgA(l - 1), 128, 0, s_, lv(l), lv(l - 1));
+        for (int l = 1; l <= lmax_; ++l) LZB_LAUNCH(k4_hanging, vgA(l), 128, 0, s_, lv(l), lv(l - 1));
+    }
+
     // distance range [lo, hi] from the sphere centre to the points of a box
     void box_range(double x0, double y0, double z0, double h, double& lo, double& hi) const {
         const double b[3][2] = {{x0, x0 + h}, {y0, y0 + h}, {z0, z0 + h}};
@@ -310,6 +847,22 @@ int lzb_tree3_stats(lzb_tree3* t, lzb_compression_stats* out) {
 int lzb_tree3_cells(lzb_tree3* t, int64_t first, int64_t count, double* ops, int32_t* p3, int32_t* n,
                     int32_t* lxyz) {
     return lzb::guarded([&] { t->t->cells(first, count, ops, p3, n, lxyz); });
+}
+int lzb_tree3_init_cycle(lzb_tree3* t, int variant, double omega, double rhs_scale, uint64_t noise_seed,
+                         int max_cycles, double target) {
+    return lzb::guarded([&] { t->t->init_cycle(variant, omega, rhs_scale, noise_seed, max_cycles, target); });
+}
+int lzb_tree3_refresh_ops(lzb_tree3* t) {
+    return lzb::guarded([&] {
+        t->t->refresh_ops();
+        t->t->sync();
+    });
+}
+int lzb_tree3_step(lzb_tree3* t, lzb_cycle_report* out) {
+    return lzb::guarded([&] { *out = t->t->step(); });
+}
+int lzb_tree3_vertices(lzb_tree3* t, int level, int field, double* out) {
+    return lzb::guarded([&] { t->t->vertices(level, field, out); });
 }
 
 }  // extern "C"
