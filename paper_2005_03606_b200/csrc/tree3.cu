@@ -87,14 +87,15 @@ struct LvA {
     double* op;  // class planes, value q of existing cell j at q * nop + j
     int64_t nop;
     uint8_t* vk;
+    int bx0, bx1, by0, by1, bz0, bz1;  // vertex box holding every existing vertex (launch domain)
 };
 enum : uint8_t { VK_OUT = 0, VK_INT = 1, VK_DIR = 2, VK_HANG = 3, VK_FINE = 4 };
 
 __device__ __forceinline__ bool vxyzA(const LvA& L, int& ix, int& iy, int& iz, int64_t& vi) {
-    ix = blockIdx.x * blockDim.x + threadIdx.x;
-    iy = blockIdx.y;
-    iz = blockIdx.z;
-    if (ix > L.N) return false;
+    ix = L.bx0 + blockIdx.x * blockDim.x + threadIdx.x;
+    iy = L.by0 + blockIdx.y;
+    iz = L.bz0 + blockIdx.z;
+    if (ix >= L.bx1) return false;
     vi = (static_cast<int64_t>(iz) * (L.N + 1) + iy) * (L.N + 1) + ix;
     return true;
 }
@@ -235,9 +236,10 @@ __global__ void k4_noise(LvA L, int level, uint64_t seed) {
                                        (static_cast<uint64_t>(iy) << 16) ^ static_cast<uint64_t>(iz)));
     L.v[LZB_V_U][vi] = (4.0 / 3.0) * static_cast<double>(kk >> 11) * 0x1.0p-53;
 }
-__global__ void k4_reset_fl(LvA L, int64_t nv) {
-    const int64_t i = gtid();
-    if (i < nv) L.v[LZB_V_FL][i] = L.load[i];
+__global__ void k4_reset_fl(LvA L) {
+    int ix, iy, iz;
+    int64_t vi;
+    if (vxyzA(L, ix, iy, iz, vi)) L.v[LZB_V_FL][vi] = L.load[vi];
 }
 __global__ void k4_uhat(LvA F, LvA C, int has_coarse) {
     int fx, fy, fz;
@@ -318,11 +320,17 @@ __global__ void k4_restrict(LvA F, LvA C) {
     }
     C.v[LZB_V_FL][vi] = acc;
 }
-__global__ void __launch_bounds__(256) k4_norm_partial(LvA L, int64_t nv, double* partial) {
+__global__ void __launch_bounds__(256) k4_norm_partial(LvA L, double* partial) {
     __shared__ double sh[256];
     double s = 0.0;
-    for (int64_t i = gtid(); i < nv; i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    const int wx = L.bx1 - L.bx0, wy = L.by1 - L.by0;
+    const int64_t nb = static_cast<int64_t>(wx) * wy * (L.bz1 - L.bz0);
+    for (int64_t t = gtid(); t < nb; t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int ix = L.bx0 + static_cast<int>(t % wx), iy = L.by0 + static_cast<int>((t / wx) % wy),
+                  iz = L.bz0 + static_cast<int>(t / wx / wy);
+        const int64_t i = vidx3(L.N, ix, iy, iz);
         if (L.vk[i] == (VK_INT | VK_FINE)) s += L.v[LZB_V_R][i] * L.v[LZB_V_R][i];
+    }
     sh[threadIdx.x] = s;
     __syncthreads();
     for (int w = blockDim.x / 2; w > 0; w >>= 1) {
@@ -331,9 +339,10 @@ __global__ void __launch_bounds__(256) k4_norm_partial(LvA L, int64_t nv, double
     }
     if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
 }
-__global__ void k4_snap(LvA L, int64_t nv) {
-    const int64_t i = gtid();
-    if (i >= nv) return;
+__global__ void k4_snap(LvA L) {
+    int ix, iy, iz;
+    int64_t i;
+    if (!vxyzA(L, ix, iy, iz, i)) return;
     L.v[LZB_V_USNAP][i] = L.v[LZB_V_U][i];
     L.v[LZB_V_AUX][i] = 0.0;
 }
@@ -579,6 +588,23 @@ public:
                 L.v[f].alloc(L.nv);
                 LZB_CUDA(cudaMemsetAsync(L.v[f].p, 0, L.v[f].bytes(), s_));
             }
+            // the vertex box of the level's existing cells: the leaves of level l
+            // and the ancestors at level l of every deeper leaf
+            int lo[3] = {L.N, L.N, L.N}, hi[3] = {-1, -1, -1};
+            for (const int4& c : leaves_) {
+                if (c.x < l) continue;
+                int sh = 1;
+                for (int k = l; k < c.x; ++k) sh *= 3;
+                const int q[3] = {c.y / sh, c.z / sh, c.w / sh};
+                for (int d = 0; d < 3; ++d) {
+                    lo[d] = std::min(lo[d], q[d]);
+                    hi[d] = std::max(hi[d], q[d]);
+                }
+            }
+            for (int d = 0; d < 3; ++d) {
+                L.box[2 * d] = hi[d] < 0 ? 0 : lo[d];
+                L.box[2 * d + 1] = hi[d] < 0 ? 1 : hi[d] + 2;  // empty level: one (absent) vertex
+            }
             L.load.alloc(L.nv);
             L.vk.alloc(L.nv);
             L.cf.alloc(L.nc);
@@ -644,8 +670,7 @@ public:
         lzb_cycle_report rep;
         std::memset(&rep, 0, sizeof rep);
         rep.cycle = static_cast<int32_t>(++cycle_);
-        for (int l = 0; l <= D; ++l)
-            LZB_LAUNCH(k4_reset_fl, blocks_for(A_[l].nv, 256), 256, 0, s_, lv(l), A_[l].nv);
+        for (int l = 0; l <= D; ++l) LZB_LAUNCH(k4_reset_fl, vgA(l), 128, 0, s_, lv(l));
         for (int l = D; l >= 0; --l) {
             LZB_LAUNCH(k4_uhat, vgA(l), 128, 0, s_, lv(l), l > 0 ? lv(l - 1) : lv(l), l > 0 ? 1 : 0);
             LZB_LAUNCH(k4_residual, vgA(l), 128, 0, s_, lv(l));
@@ -654,7 +679,7 @@ public:
         double s2 = 0.0;
         std::vector<double> part(kNormBlocksA);
         for (int l = 0; l <= D; ++l) {
-            LZB_LAUNCH(k4_norm_partial, kNormBlocksA, 256, 0, s_, lv(l), A_[l].nv, partialA_.p);
+            LZB_LAUNCH(k4_norm_partial, kNormBlocksA, 256, 0, s_, lv(l), partialA_.p);
             LZB_CUDA(cudaMemcpyAsync(part.data(), partialA_.p, kNormBlocksA * sizeof(double), cudaMemcpyDeviceToHost,
                                      s_));
             LZB_CUDA(cudaStreamSynchronize(s_));
@@ -669,7 +694,7 @@ public:
                      : static_cast<int>(cycle_) >= max_cycles_ ? LZB_TIMEOUT : LZB_CONTINUE;
         if (rep.status == LZB_CONTINUE || rep.status == LZB_TIMEOUT) {
             const bool pi = variant_ == LZB_ADAFAC_PI;
-            for (int l = 0; l <= D; ++l) LZB_LAUNCH(k4_snap, blocks_for(A_[l].nv, 256), 256, 0, s_, lv(l), A_[l].nv);
+            for (int l = 0; l <= D; ++l) LZB_LAUNCH(k4_snap, vgA(l), 128, 0, s_, lv(l));
             for (int l = D; l >= 0; --l) {
                 if (pi && l > 0) LZB_LAUNCH(k4_aux_inject, vgA(l - 1), 128, 0, s_, lv(l), lv(l - 1));
                 const double damping = variant_ == LZB_ADDITIVE ? std::pow(omega_, D - l + 1) : omega_;
@@ -712,6 +737,7 @@ private:
         DevBuf<double> load, op;
         DevBuf<uint8_t> vk, cf;
         DevBuf<int32_t> oi;
+        int box[6] = {0, 2, 0, 2, 0, 2};  // vertex ranges [x0, x1), [y0, y1), [z0, z1)
     };
     static constexpr int kNormBlocksA = 148 * 2;
     std::vector<LevA> A_;
@@ -733,9 +759,18 @@ private:
         v.op = L.op.p;
         v.nop = L.nop;
         v.vk = L.vk.p;
+        v.bx0 = L.box[0];
+        v.bx1 = L.box[1];
+        v.by0 = L.box[2];
+        v.by1 = L.box[3];
+        v.bz0 = L.box[4];
+        v.bz1 = L.box[5];
         return v;
     }
-    dim3 vgA(int l) const { return dim3(blocks_for(A_[l].N + 1, 128), A_[l].N + 1, A_[l].N + 1); }
+    dim3 vgA(int l) const {
+        const LevA& L = A_[l];
+        return dim3(blocks_for(L.box[1] - L.box[0], 128), L.box[3] - L.box[2], L.box[5] - L.box[4]);
+    }
     // injection (finest first) where the fine vertex exists, then the hanging
     // vertices of every level from their parents (solver.cpp:344-347)
     void finish_cycle() {
