@@ -583,15 +583,19 @@ def run_ours(args, world, rank, local):
     host = torch.empty(len(img) + (1 << 20), dtype=torch.uint8, pin_memory=True).numpy()
 
     def e2e_step():
-        g.assemble_fixed(P)
-        g.stream_image(host)
+        # assembly + the compressed LZMG stream into pinned host memory, the copy of
+        # each band of level-1 subtrees overlapping the next band's assembly
+        g.assemble_stream(P, host)
+
+    e2e_step()  # allocations and events of the pipelined path (untimed)
 
     te = timed_steps(e2e_step, args.steps)
     te = max_over_ranks(te, world)
     e2e = {"value": world * SAMPLES_PER_STEP * args.steps / te, "unit": "sub-samples/s",
            "h2d_bytes_per_step": 560, "d2h_bytes_per_step": len(img) + 16,
            "ms_per_step": 1e3 * te / args.steps,
-           "path": "lzb_grid_assemble_fixed + lzb_grid_stream_image into pinned host memory (LZMG bytes)"}
+           "path": "lzb_grid_assemble_stream: fixed-p assembly + LZMG stream into pinned host memory, "
+                   "3 bands of level-1 subtrees pipelined (assemble + pack | D2H copy)"}
 
     if rank != 0:
         return

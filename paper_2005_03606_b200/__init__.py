@@ -122,6 +122,7 @@ def lib():
         L.lzb_grf_table.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, vp]
         L.lzb_integrate_elements3.argtypes = [vp, C.POINTER(T.Field3), i64, vp, vp, vp, vp, vp, vp]
         L.lzb_grid3_create.argtypes = [vp, C.c_int, C.POINTER(T.Field3), C.c_double, C.c_int, C.POINTER(vp)]
+        L.lzb_grid_assemble_stream.argtypes = [vp, C.c_int, vp, i64, C.POINTER(i64), vp]
         L.lzb_grid3_create_planes.argtypes = [vp, C.c_int, C.POINTER(T.Field3), C.c_double, C.c_int, C.c_int,
                                                C.POINTER(vp)]
         L.lzb_grid3_destroy.argtypes = [vp]
@@ -521,6 +522,14 @@ class Grid:
         buf = np.zeros(size.value, np.uint8)
         _check(lib().lzb_grid_stream_image(self.h, _ptr(buf), buf.size, C.byref(size)))
         return buf[: size.value].tobytes()
+
+    def assemble_stream(self, n, out: np.ndarray, timeline: np.ndarray | None = None) -> int:
+        """assemble_fixed(n) + stream_image(out), pipelined per band of level-1
+        subtrees (lzb_grid_assemble_stream); returns the image size."""
+        size = C.c_int64()
+        _check(lib().lzb_grid_assemble_stream(self.h, n, _ptr(out), out.size, C.byref(size),
+                                              None if timeline is None else _ptr(timeline)))
+        return size.value
 
     def stream_image_size(self) -> int:
         size = C.c_int64()

@@ -406,20 +406,29 @@ __global__ void k_spawn(LevelView F, uint32_t cycle, long long leaf_count, long 
     if (keys) keys[c] = static_cast<long long>(cycle) * leaf_count + crank(F, c % F.N, c / F.N);
 }
 
+// A rectangle of leaf cells [x0, x0 + w) x [y0, ...): the fixed-p kernels
+// walk a linear range of its cells (rect-local index cy' * w + cx'); the
+// whole level is {0, N, 0}.
+struct CellRect {
+    int x0, w, y0;
+    __device__ __forceinline__ int cx(int64_t cl) const { return x0 + static_cast<int>(cl % w); }
+    __device__ __forceinline__ int cy(int64_t cl) const { return y0 + static_cast<int>(cl / w); }
+};
+
 // Fixed-p assembly: every leaf integrated at n, published, p1 = top.
 template <int KIND, bool FAST>
 __global__ void __launch_bounds__(kIntThreads, 2) k_fixed(LevelView F, lzb_field f, int n, IntTables T,
                                                           double delta_max, uint32_t cycle,
                                                           unsigned long long* stats, int* err,
-                                                          int64_t cbeg, int64_t cend) {
+                                                          int64_t cbeg, int64_t cend, CellRect R) {
     lzb_pdl_enter();
     extern __shared__ double sm[];
     stage_common(sm, f, T);
-    const int64_t ncell = cend;  // cells [cbeg, cend): a slab of whole rows
+    const int64_t ncell = cend;  // rect-local cells [cbeg, cend)
     const int64_t c0 = cbeg + static_cast<int64_t>(blockIdx.x) * blockDim.x * kCPT;
     const int64_t c1 = (c0 + static_cast<int64_t>(blockDim.x) * kCPT < ncell
                             ? c0 + static_cast<int64_t>(blockDim.x) * kCPT : ncell) - 1;
-    const int row_lo = static_cast<int>(c0 / F.N), rows = static_cast<int>(c1 / F.N) - row_lo + 1;
+    const int row_lo = R.cy(c0), rows = R.cy(c1) - row_lo + 1;
     const double* s_fy = stage_rows(sm, T, row_lo, rows);
     bool mine[kCPT];
     int64_t cc[kCPT];
@@ -429,8 +438,9 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_fixed(LevelView F, lzb_field
     for (int q = 0; q < kCPT; ++q) {
         const int64_t c = c0 + threadIdx.x + q * blockDim.x;
         mine[q] = c < ncell;
-        cc[q] = mine[q] ? c : c0;
-        const int cx = static_cast<int>(cc[q] % F.N), cy = static_cast<int>(cc[q] / F.N);
+        const int64_t cl = mine[q] ? c : c0;
+        const int cx = R.cx(cl), cy = R.cy(cl);
+        cc[q] = static_cast<int64_t>(cy) * F.N + cx;
         fxc[q] = T.fx + static_cast<int64_t>(cx) * n;
         fyc[q] = s_fy ? s_fy + static_cast<int64_t>(cy - row_lo) * n : T.fy + static_cast<int64_t>(cy) * n;
     }
@@ -454,7 +464,7 @@ template <int KIND, bool FAST>
 __global__ void __launch_bounds__(kIntThreads, 2) k_fixed_res(LevelView F, lzb_field f, int n, IntTables T,
                                                               double delta_max, uint32_t cycle,
                                                               unsigned long long* stats, int* err,
-                                                              int64_t cbeg, int64_t cend) {
+                                                              int64_t cbeg, int64_t cend, CellRect R) {
     lzb_pdl_enter();
     extern __shared__ double sm[];
     stage_common(sm, f, T);
@@ -466,8 +476,8 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_fixed_res(LevelView F, lzb_f
     const int64_t total = cend - cbeg;
     const int64_t b0 = cbeg + blockIdx.x * total / gridDim.x;
     const int64_t b1 = cbeg + (blockIdx.x + 1) * total / gridDim.x;
-    const int row_lo = static_cast<int>(b0 / F.N);
-    const int rows = b1 > b0 ? static_cast<int>((b1 - 1) / F.N) - row_lo + 1 : 0;
+    const int row_lo = R.cy(b0);
+    const int rows = b1 > b0 ? R.cy(b1 - 1) - row_lo + 1 : 0;
     double* s_fy = nullptr;
     if (rows > 0 && rows <= kFyRows) {
         s_fy = res_fy_region(sm, n);
@@ -484,8 +494,9 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_fixed_res(LevelView F, lzb_f
         for (int q = 0; q < kCPT; ++q) {
             const int64_t c = base + static_cast<int64_t>(q) * blockDim.x;
             mine[q] = c < b1;
-            cc[q] = mine[q] ? c : base;
-            const int cx = static_cast<int>(cc[q] % F.N), cy = static_cast<int>(cc[q] / F.N);
+            const int64_t cl = mine[q] ? c : base;
+            const int cx = R.cx(cl), cy = R.cy(cl);
+            cc[q] = static_cast<int64_t>(cy) * F.N + cx;
             fxc[q] = T.fx + static_cast<int64_t>(cx) * n;
             fyc[q] = s_fy ? s_fy + static_cast<int64_t>(cy - row_lo) * n : T.fy + static_cast<int64_t>(cy) * n;
         }
@@ -1537,7 +1548,9 @@ struct PackArgs {
 
 __global__ void __launch_bounds__(kPackWarps * 32) k_pack_patches(AllLevels A, lzb_field f, PackArgs T, int per,
                                                                   const int64_t* __restrict__ offsets,
-                                                                  uint8_t* __restrict__ out, int* err) {
+                                                                  uint8_t* __restrict__ out, int* err, int px0,
+                                                                  int pxn, int py_base,
+                                                                  const int64_t* __restrict__ basep) {
     lzb_pdl_enter();
     __shared__ __align__(16) uint8_t wbuf[kPackWarps][kPackWindow];
     __shared__ double s_geo[64], s_kunit[16];
@@ -1548,9 +1561,12 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_pack_patches(AllLevels A, l
     const int D = A.D;
     const LevelView C = A.L[D - 1];
     const LevelView F = A.L[D];
-    // 2D grid: x = patch columns (kPackWarps per block), y = groups of `per` sibling patches
-    const int px = blockIdx.x * kPackWarps + warp, py0 = blockIdx.y * per;
-    if (px >= C.N) return;
+    // 2D grid: x = patch columns (kPackWarps per block), y = groups of `per` sibling patches;
+    // patches [px0, px0 + pxn) x [py_base, ...) (a band of level-1 subtrees, or the whole
+    // level), offsets relative to *basep when given
+    const int px = px0 + blockIdx.x * kPackWarps + warp, py0 = py_base + blockIdx.y * per;
+    if (px >= px0 + pxn) return;
+    const int64_t obase = basep ? *basep : 0;
     const unsigned full = 0xffffffffu;
     // pre-order slot of patch (px, py0) from its base-3 digits (no table loads
     // in front of the offsets load)
@@ -1595,7 +1611,7 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_pack_patches(AllLevels A, l
         const int32_t p1 = p1a[cell];
         const int p3raw = p3a[cell];
         const uint8_t p2 = p2a[cell];
-        off = offsets[s0 + lane];
+        off = offsets[s0 + lane] + obase;
         const double ex = leaf ? T.cxF[cx] : T.cxC[cx], ey = leaf ? T.cyF[cy] : T.cyC[cy];
         p3 = p1 != LZB_P1_BOTTOM ? p3raw : 0;
         hdr = pack_header(p1, p2, p3);
@@ -1699,26 +1715,37 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_pack_patches(AllLevels A, l
 
 // Records of levels 0..D-2 (1/80 of the image): one warp per record, lane =
 // value, bytes straight to global memory.
-__global__ void k_pack_upper(AllLevels A, lzb_field f, int64_t ncells, const int64_t* __restrict__ offsets,
-                             uint8_t* __restrict__ out, int* err) {
-    lzb_pdl_enter();
-    const int lane = threadIdx.x & 31;
-    int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (t >= ncells) return;
-    int l = 0;
+// Cell t of the upper levels in the walk order of k_pack_upper /
+// k_record_sizes_upper: levels 0..D-2 (ca < 0), or levels 1..D-2 of the
+// level-1 subtree (ca, cb) (9^(l-1) cells at level l).
+__device__ __forceinline__ void upper_cell(const AllLevels& A, int64_t t, int ca, int cb, int& l, int& cx, int& cy) {
+    l = ca < 0 ? 0 : 1;
     int64_t n = 1;
     while (t >= n) {
         t -= n;
         ++l;
         n *= 9;
     }
+    const int w = ca < 0 ? A.L[l].N : A.L[l].N / 3;
+    cx = (ca < 0 ? 0 : ca * w) + static_cast<int>(t % w);
+    cy = (cb < 0 ? 0 : cb * w) + static_cast<int>(t / w);
+}
+
+__global__ void k_pack_upper(AllLevels A, lzb_field f, int64_t ncells, const int64_t* __restrict__ offsets,
+                             uint8_t* __restrict__ out, int* err, int ca, int cb,
+                             const int64_t* __restrict__ basep) {
+    lzb_pdl_enter();
+    const int lane = threadIdx.x & 31;
+    int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (t >= ncells) return;
+    int l, cx, cy;
+    upper_cell(A, t, ca, cb, l, cx, cy);
     const LevelView& L = A.L[l];
-    const int cx = static_cast<int>(t % L.N), cy = static_cast<int>(t / L.N);
     const int c = cy * L.N + cx;
     const int32_t p1 = L.p1[c];
     const int p3 = p1 != LZB_P1_BOTTOM ? L.p3[c] : 0;
     const int size = record_size(p1, p3, false);
-    uint8_t* rec = out + 12 + offsets[slot_at(A.st, l, cx, cy)];
+    uint8_t* rec = out + 12 + offsets[slot_at(A.st, l, cx, cy)] + (basep ? *basep : 0);
     if (lane == 0) rec[0] = pack_header(p1, L.p2[c], p3);
     if (size == 1) return;
     const double e = centre_eps(f, L, cx, cy);
@@ -1742,13 +1769,13 @@ __global__ void k_pack_upper(AllLevels A, lzb_field f, int64_t ncells, const int
 // Record sizes in slot order (stream.cpp:227-237): one thread per
 // level-(D-1) patch writes its record and its 9 leaves' (10 consecutive
 // slots); one thread per cell of the levels above.
-__global__ void k_record_sizes_patches(AllLevels A, int64_t* __restrict__ sizes) {
+__global__ void k_record_sizes_patches(AllLevels A, int64_t* __restrict__ sizes, int px0, int pxn, int py_base) {
     lzb_pdl_enter();
     const int D = A.D;
     const LevelView& C = A.L[D - 1];
     const LevelView& F = A.L[D];
-    const int px = blockIdx.x * blockDim.x + threadIdx.x, py = blockIdx.y;
-    if (px >= C.N) return;
+    const int px = px0 + blockIdx.x * blockDim.x + threadIdx.x, py = py_base + blockIdx.y;
+    if (px >= px0 + pxn) return;
     const int64_t sP = slot_at(A.st, D - 1, px, py);
     int c = py * C.N + px;
     int32_t p1 = C.p1[c];
@@ -1760,19 +1787,13 @@ __global__ void k_record_sizes_patches(AllLevels A, int64_t* __restrict__ sizes)
         sizes[sP + 1 + ci] = record_size(p1, p1 != LZB_P1_BOTTOM ? F.p3[c] : 0, true);
     }
 }
-__global__ void k_record_sizes_upper(AllLevels A, int64_t ncells, int64_t* __restrict__ sizes) {
+__global__ void k_record_sizes_upper(AllLevels A, int64_t ncells, int64_t* __restrict__ sizes, int ca, int cb) {
     lzb_pdl_enter();
     int64_t t = gtid();
     if (t >= ncells) return;
-    int l = 0;
-    int64_t n = 1;
-    while (t >= n) {
-        t -= n;
-        ++l;
-        n *= 9;
-    }
+    int l, cx, cy;
+    upper_cell(A, t, ca, cb, l, cx, cy);
     const LevelView& L = A.L[l];
-    const int cx = static_cast<int>(t % L.N), cy = static_cast<int>(t / L.N);
     const int c = cy * L.N + cx;
     const int32_t p1 = L.p1[c];
     sizes[slot_at(A.st, l, cx, cy)] = record_size(p1, p1 != LZB_P1_BOTTOM ? L.p3[c] : 0, false);
@@ -1847,6 +1868,19 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_inject(AllLevels A, int
     }
 }
 #undef LZB_FOR_VERTS
+
+// Running image offset of the bands of level-1 subtrees (assemble_stream):
+// base[1] = base[0] + the band's bytes (its last local offset plus its last record).
+__global__ void k_chunk_base(const int64_t* __restrict__ sizes, const int64_t* __restrict__ offs, int64_t n,
+                             int64_t* base) {
+    lzb_pdl_enter();
+    base[1] = base[0] + offs[n - 1] + sizes[n - 1];
+}
+__global__ void k_root_base(const int64_t* __restrict__ sizes, int64_t* __restrict__ offs, int64_t* base) {
+    lzb_pdl_enter();
+    offs[0] = 0;
+    base[0] = sizes[0];
+}
 
 // CellStream::load record (stream.cpp:355-392); offsets from the host parse.
 __global__ void k_unpack(LevelView L, lzb_field f, int level, int leaf, SlotTable st,
@@ -2093,7 +2127,7 @@ inline void dispatch_step(bool fast, cudaStream_t s, const LevelView& F, const L
 template <int KIND, bool FAST>
 void launch_fixed_k(cudaStream_t s, const LevelView& F, const lzb_field& f, int n, const IntTables& T,
                     double dmax, uint32_t cycle, unsigned long long* stats, int* err, int64_t cbeg,
-                    int64_t cend) {
+                    int64_t cend, CellRect R) {
     const size_t rsmem = res_smem_bytes(n);
     if (rsmem <= kResidentSmemMax) {  // persistent: K_sub table resident, one range per block
         static int grid = 0;          // per instantiation: resident blocks x SMs
@@ -2110,21 +2144,21 @@ void launch_fixed_k(cudaStream_t s, const LevelView& F, const lzb_field& f, int 
         const int64_t want = (cend - cbeg + kCPT - 1) / kCPT;
         const unsigned g = static_cast<unsigned>(want < grid ? (want > 0 ? want : 1) : grid);
         LZB_LAUNCH((k_fixed_res<KIND, FAST>), g, kIntThreads, rsmem, s, F, f, n, T, dmax, cycle, stats, err,
-                   cbeg, cend);
+                   cbeg, cend, R);
         return;
     }
     size_t smem = int_smem_bytes(n);
     set_smem(k_fixed<KIND, FAST>, smem);
     LZB_LAUNCH((k_fixed<KIND, FAST>), blocks_for(cend - cbeg, kIntThreads * kCPT), kIntThreads, smem, s, F,
-               f, n, T, dmax, cycle, stats, err, cbeg, cend);
+               f, n, T, dmax, cycle, stats, err, cbeg, cend, R);
 }
 
 template <int KIND>
 void launch_fixed(bool fast, cudaStream_t s, const LevelView& F, const lzb_field& f, int n,
                   const IntTables& T, double dmax, uint32_t cycle, unsigned long long* stats, int* err,
-                  int64_t cbeg, int64_t cend) {
-    if (fast) launch_fixed_k<KIND, true>(s, F, f, n, T, dmax, cycle, stats, err, cbeg, cend);
-    else launch_fixed_k<KIND, false>(s, F, f, n, T, dmax, cycle, stats, err, cbeg, cend);
+                  int64_t cbeg, int64_t cend, CellRect R) {
+    if (fast) launch_fixed_k<KIND, true>(s, F, f, n, T, dmax, cycle, stats, err, cbeg, cend, R);
+    else launch_fixed_k<KIND, false>(s, F, f, n, T, dmax, cycle, stats, err, cbeg, cend, R);
 }
 
 }  // namespace
@@ -2341,6 +2375,18 @@ public:
         if (herr_) cudaFreeHost(herr_);
         for (cudaGraphExec_t* e : {&g_coarse_, &g_front_, &g_back_})
             if (*e) cudaGraphExecDestroy(*e);
+        if (st_ready_) {
+            cudaStreamSynchronize(cp_);
+            cudaStreamDestroy(cp_);
+            cudaFreeHost(hbase_);
+            for (int k = 0; k < 3; ++k) {
+                cudaEventDestroy(ev_asm_[k]);
+                cudaEventDestroy(ev_pack_[k]);
+                cudaEventDestroy(ev_copy_[k]);
+            }
+            cudaEventDestroy(ev_root_);
+            cudaEventDestroy(ev_start_);
+        }
     }
 
     LevelView V(int l) const {
@@ -2503,19 +2549,26 @@ public:
     void assemble_fixed_rows(int n, int row0, int row1) {
         if (n < 1) throw Error(LZB_ERR_INVALID, "n must be >= 1");
         if (row0 < 0 || row1 > L_[D_].N || row0 >= row1) throw Error(LZB_ERR_INVALID, "bad row range");
-        const int64_t cbeg = static_cast<int64_t>(row0) * L_[D_].N, cend = static_cast<int64_t>(row1) * L_[D_].N;
         // the whole level ends at p1 = top only when every row is assembled here
         all_top_ = row0 == 0 && row1 == L_[D_].N;
         ensure_tables(n);
+        assemble_rect(n, CellRect{0, L_[D_].N, row0}, static_cast<int64_t>(row1 - row0) * L_[D_].N, s_);
+    }
+
+    // Fixed-p assembly launch over the leaf cells of rectangle R (count cells) on stream st (tables ready).
+    void assemble_rect(int n, CellRect R, int64_t count, cudaStream_t st) {
         LevelView F = V(D_);
         bool fast = d_.integration == LZB_INTEGRATE_FAST;
         unsigned long long* stats = res_.p->s;
+        const IntTables T = tables_.view();
+        int* err = ctx_->err.p;
+        const double dm = d_.delta_max;
         switch (d_.field.kind) {
-            case LZB_FIELD_THETA: launch_fixed<LZB_FIELD_THETA>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p, cbeg, cend); break;
-            case LZB_FIELD_QUADRANT: launch_fixed<LZB_FIELD_QUADRANT>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p, cbeg, cend); break;
-            case LZB_FIELD_CHECKER: launch_fixed<LZB_FIELD_CHECKER>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p, cbeg, cend); break;
-            case LZB_FIELD_SINUSOID: launch_fixed<LZB_FIELD_SINUSOID>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p, cbeg, cend); break;
-            default: launch_fixed<LZB_FIELD_CONSTANT>(fast, s_, F, d_.field, n, tables_.view(), d_.delta_max, cycle_, stats, ctx_->err.p, cbeg, cend); break;
+            case LZB_FIELD_THETA: launch_fixed<LZB_FIELD_THETA>(fast, st, F, d_.field, n, T, dm, cycle_, stats, err, 0, count, R); break;
+            case LZB_FIELD_QUADRANT: launch_fixed<LZB_FIELD_QUADRANT>(fast, st, F, d_.field, n, T, dm, cycle_, stats, err, 0, count, R); break;
+            case LZB_FIELD_CHECKER: launch_fixed<LZB_FIELD_CHECKER>(fast, st, F, d_.field, n, T, dm, cycle_, stats, err, 0, count, R); break;
+            case LZB_FIELD_SINUSOID: launch_fixed<LZB_FIELD_SINUSOID>(fast, st, F, d_.field, n, T, dm, cycle_, stats, err, 0, count, R); break;
+            default: launch_fixed<LZB_FIELD_CONSTANT>(fast, st, F, d_.field, n, T, dm, cycle_, stats, err, 0, count, R); break;
         }
     }
 
@@ -3174,11 +3227,11 @@ public:
 
     void record_sizes(int64_t* sizes) {
         const dim3 grid(blocks_for(L_[D_ - 1].N, 64), L_[D_ - 1].N);
-        LZB_LAUNCH(k_record_sizes_patches, grid, 64, 0, s_, all_levels(), sizes);
+        LZB_LAUNCH(k_record_sizes_patches, grid, 64, 0, s_, all_levels(), sizes, 0, L_[D_ - 1].N, 0);
         const int64_t upper = total_cells_ - L_[D_].nc - L_[D_ - 1].nc;
         if (upper > 0)
             LZB_LAUNCH(k_record_sizes_upper, blocks_for(upper, kThreads), kThreads, 0, s_, all_levels(), upper,
-                       sizes);
+                       sizes, -1, -1);
     }
 
     // Record sizes -> device exclusive scan (cub) -> total. Returns the image size.
@@ -3212,11 +3265,114 @@ public:
         const int per = L_[D_ - 1].N >= 3 ? 3 : 1;  // sibling patches per warp
         const dim3 grid(blocks_for(L_[D_ - 1].N, kPackWarps), L_[D_ - 1].N / per);
         LZB_LAUNCH(k_pack_patches, grid, kPackWarps * 32, 0, s_, all_levels(), d_.field, T, per, rec_offs_.p, img,
-                   ctx_->err.p);
+                   ctx_->err.p, 0, L_[D_ - 1].N, 0, nullptr);
         const int64_t upper = total_cells_ - L_[D_].nc - L_[D_ - 1].nc;
         if (upper > 0)
             LZB_LAUNCH(k_pack_upper, blocks_for(upper, kThreads / 32), kThreads, 0, s_, all_levels(), d_.field,
-                       upper, rec_offs_.p, img, ctx_->err.p);
+                       upper, rec_offs_.p, img, ctx_->err.p, -1, -1, nullptr);
+    }
+
+    // assemble_fixed(n) followed by image_into(out, cap), pipelined: the LZMG
+    // image is a root record followed by the 9 level-1 subtrees in child
+    // order lx * 3 + ly (pre-order, mesh.cpp:152-157), so each x band of 3
+    // subtrees is one contiguous byte range. Band by band the solve stream
+    // assembles the leaves, then sizes, scans and packs its records (offsets chained through a
+    // device running base) and the copy stream moves its bytes to the host
+    // while the next band assembles (a band is ~600 cells per resident
+    // block; a single subtree would leave the persistent assembly kernel
+    // under one iteration per block). Same bytes as the sequential calls.
+    // timeline: NULL or 9 floats, device ms of each band's assembly, pack
+    // and copy end after the start.
+    int64_t assemble_stream(int n, uint8_t* out, int64_t cap, float* timeline) {
+        if (n < 1) throw Error(LZB_ERR_INVALID, "n must be >= 1");
+        if (D_ < 2) {
+            assemble_fixed(n);
+            return image_into(out, cap);
+        }
+        if (cap < 12) throw Error(LZB_ERR_INVALID, "stream image buffer too small");
+        all_top_ = true;
+        ensure_tables(n);
+        if (rec_sizes_.n < static_cast<size_t>(total_cells_)) scan_records();  // allocates the scan buffers
+        const int64_t leaves = L_[D_].nc, refined = total_cells_ - leaves;
+        const size_t cap_dev = static_cast<size_t>(12 + total_cells_ + leaves * 128 + refined * 1152);
+        if (img_.n < cap_dev) img_.alloc(cap_dev);
+        if (!st_ready_) {
+            stream_base_.alloc(4);
+            LZB_CUDA(cudaMallocHost(&hbase_, 4 * sizeof(int64_t)));
+            LZB_CUDA(cudaStreamCreateWithFlags(&cp_, cudaStreamNonBlocking));
+            for (int k = 0; k < 3; ++k) {
+                LZB_CUDA(cudaEventCreate(&ev_asm_[k]));
+                LZB_CUDA(cudaEventCreate(&ev_pack_[k]));
+                LZB_CUDA(cudaEventCreate(&ev_copy_[k]));
+            }
+            LZB_CUDA(cudaEventCreate(&ev_root_));
+            LZB_CUDA(cudaEventCreate(&ev_start_));
+            st_ready_ = true;
+        }
+        const int N = L_[D_].N, Nc = L_[D_ - 1].N, w = N / 3, pw = Nc / 3;
+        const int64_t S1 = slots_.subtree[1];
+        int64_t nup = 0;  // cells of levels 1..D-2 in one subtree
+        for (int l = 1, q = 1; l <= D_ - 2; ++l, q *= 9) nup += q;
+        const AllLevels AL = all_levels();
+        const PackArgs T{centre_[1].x.p, centre_[1].y.p, centre_[0].x.p, centre_[0].y.p};
+        LZB_CUDA(cudaEventRecord(ev_start_, s_));
+        // the root record (slot 0, offset 0): its size starts the running base
+        LZB_LAUNCH(k_record_sizes_upper, 1, 32, 0, s_, AL, 1, rec_sizes_.p, -1, -1);
+        LZB_LAUNCH(k_root_base, 1, 1, 0, s_, rec_sizes_.p, rec_offs_.p, stream_base_.p);
+        LZB_LAUNCH(k_pack_upper, 1, 32, 0, s_, AL, d_.field, 1, rec_offs_.p, img_.p, ctx_->err.p, -1, -1, nullptr);
+        LZB_CUDA(cudaEventRecord(ev_root_, s_));
+        const int per = Nc >= 3 ? 3 : 1;
+        // band a (subtrees (a, 0..2), leaf columns [a w, (a + 1) w)): assembly, then
+        // its sizes / scan / pack, all on the solve stream (the persistent assembly
+        // kernel holds every SM while it runs, so a pack beside it would starve)
+        for (int a = 0; a < 3; ++a) {
+            const int64_t s0 = 1 + 3 * a * S1;
+            assemble_rect(n, CellRect{a * w, w, 0}, static_cast<int64_t>(w) * N, s_);
+            LZB_CUDA(cudaEventRecord(ev_asm_[a], s_));
+            LZB_LAUNCH(k_record_sizes_patches, dim3(blocks_for(pw, 64), Nc), 64, 0, s_, AL, rec_sizes_.p, a * pw, pw, 0);
+            for (int b = 0; b < 3 && nup > 0; ++b)
+                LZB_LAUNCH(k_record_sizes_upper, blocks_for(nup, kThreads), kThreads, 0, s_, AL, nup, rec_sizes_.p,
+                           a, b);
+            size_t tb = scan_tmp_.n;
+            LZB_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp_.p, tb, rec_sizes_.p + s0, rec_offs_.p + s0,
+                                                  static_cast<int>(3 * S1), s_));
+            LZB_LAUNCH(k_chunk_base, 1, 1, 0, s_, rec_sizes_.p + s0, rec_offs_.p + s0, 3 * S1, stream_base_.p + a);
+            LZB_LAUNCH(k_pack_patches, dim3(blocks_for(pw, kPackWarps), Nc / per), kPackWarps * 32, 0, s_, AL,
+                       d_.field, T, per, rec_offs_.p, img_.p, ctx_->err.p, a * pw, pw, 0, stream_base_.p + a);
+            for (int b = 0; b < 3 && nup > 0; ++b)
+                LZB_LAUNCH(k_pack_upper, blocks_for(nup, kThreads / 32), kThreads, 0, s_, AL, d_.field, nup,
+                           rec_offs_.p, img_.p, ctx_->err.p, a, b, stream_base_.p + a);
+            LZB_CUDA(cudaMemcpyAsync(hbase_ + a, stream_base_.p + a + 1, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                     s_));
+            LZB_CUDA(cudaEventRecord(ev_pack_[a], s_));
+        }
+        // host: as each band's byte range becomes known, queue its copy (copy
+        // engine, concurrent with the next bands' assembly)
+        bool overflow = false;
+        int64_t lo = 12;
+        for (int a = 0; a < 3; ++a) {
+            LZB_CUDA(cudaEventSynchronize(ev_pack_[a]));
+            const int64_t hi = 12 + hbase_[a];
+            if (hi > cap) overflow = true;
+            if (!overflow) {
+                LZB_CUDA(cudaStreamWaitEvent(cp_, ev_pack_[a], 0));
+                LZB_CUDA(cudaMemcpyAsync(out + lo, img_.p + lo, hi - lo, cudaMemcpyDeviceToHost, cp_));
+            }
+            LZB_CUDA(cudaEventRecord(ev_copy_[a], cp_));
+            lo = hi;
+        }
+        LZB_CUDA(cudaStreamSynchronize(cp_));
+        if (timeline)
+            for (int a = 0; a < 3; ++a) {
+                LZB_CUDA(cudaEventElapsedTime(&timeline[a], ev_start_, ev_asm_[a]));
+                LZB_CUDA(cudaEventElapsedTime(&timeline[3 + a], ev_start_, ev_pack_[a]));
+                LZB_CUDA(cudaEventElapsedTime(&timeline[6 + a], ev_start_, ev_copy_[a]));
+            }
+        sync_check();
+        if (overflow) throw Error(LZB_ERR_INVALID, "stream image buffer too small");
+        const uint32_t hdr[3] = {0x4c5a4d47u, 1u, static_cast<uint32_t>(total_cells_)};
+        std::memcpy(out, hdr, 12);
+        return lo;
     }
 
     // CellStream::save byte image: packed on the device (k_pack_patches) from the
@@ -3405,7 +3561,11 @@ public:
     int64_t batches_committed() const { return batches_committed_; }
 
 private:
-    DevBuf<int64_t> rec_sizes_, rec_offs_;
+    DevBuf<int64_t> rec_sizes_, rec_offs_, stream_base_;
+    int64_t* hbase_ = nullptr;  // pinned: the running image base per band
+    cudaStream_t cp_ = nullptr;
+    cudaEvent_t ev_asm_[3] = {}, ev_pack_[3] = {}, ev_copy_[3] = {}, ev_root_ = nullptr, ev_start_ = nullptr;
+    bool st_ready_ = false;
     DevBuf<unsigned char> scan_tmp_;
     DevBuf<uint8_t> img_;
     Result* hres_ = nullptr;
@@ -3544,6 +3704,9 @@ int lzb_grid_dist_result(lzb_grid* g, double* norm2, uint64_t* slots20) {
 }
 int lzb_grid_dist_report(lzb_grid* g, double norm2, const uint64_t* slots20, lzb_cycle_report* rep) {
     return guarded([&] { *rep = g->g->dist_report(norm2, slots20); });
+}
+int lzb_grid_assemble_stream(lzb_grid* g, int n, uint8_t* out, int64_t cap, int64_t* size, float* timeline) {
+    return guarded([&] { *size = g->g->assemble_stream(n, out, cap, timeline); });
 }
 int lzb_grid_time_kernel(lzb_grid* g, int what, int reps, double* avg_ms) {
     return guarded([&] { *avg_ms = g->g->time_kernel(what, reps); });

@@ -607,6 +607,9 @@ public:
             }
             L.load.alloc(L.nv);
             L.vk.alloc(L.nv);
+            // kinds outside the launch box stay "outside" (read by injection across levels)
+            LZB_CUDA(cudaMemsetAsync(L.vk.p, 0, L.vk.bytes(), s_));
+            LZB_CUDA(cudaMemsetAsync(L.load.p, 0, L.load.bytes(), s_));
             L.cf.alloc(L.nc);
             L.oi.alloc(L.nc + 1);
             LZB_CUDA(cudaMemsetAsync(L.cf.p, 0, L.cf.bytes(), s_));

@@ -347,3 +347,33 @@ def test_fixed_width_records(p3):
     for c in (0, 13, 400, 728):
         want = basev[c] + lzb.codec.roundtrip(m[c] - basev[c], p3)
         assert np.array_equal(cells["ops"][c], want), c
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("depth,kind,dmax,n", [(2, "checker", 1e-8, 3), (3, "sinusoid", 1e-8, 4),
+                                               (4, "checker", 0.0, 2), (5, "sinusoid", 1e-4, 5)])
+def test_assemble_stream_matches_sequential(depth, kind, dmax, n):
+    """lzb_grid_assemble_stream (assembly + pack + copy pipelined over the
+    three bands of level-1 subtrees) gives the bytes of assemble_fixed
+    followed by stream_image and leaves the same grid state; a too-small
+    buffer fails without writing past it."""
+    import torch
+    f = lzb.checkerboard(1, 8) if kind == "checker" else lzb.field_sinusoid(0.9, 6.0)
+    desc = lzb.make_desc(depth=depth, field=f, solver="adafac-pi", omega=0.6, max_cycles=100, delta_max=dmax)
+    a, b = lzb.Grid(desc, 1), lzb.Grid(desc, 1)
+    a.assemble_fixed(n)
+    a.step()  # refined records with payloads
+    b.assemble_fixed(n)
+    b.step()
+    want = a.stream_image()
+    out = torch.full((len(want) + 64,), 0xAB, dtype=torch.uint8, pin_memory=True).numpy()
+    tl = np.zeros(9, np.float32)
+    size = b.assemble_stream(n, out, tl)
+    assert size == len(want) and out[:size].tobytes() == want
+    assert (out[size:] == 0xAB).all() and (np.diff(tl[:3]) > 0).all()
+    assert np.array_equal(a.cells(depth)["ops"], b.cells(depth)["ops"])
+    assert [r["residual"] for r in (a.step(), a.step())] == [r["residual"] for r in (b.step(), b.step())]
+    guard = np.full(len(want), 0xCD, np.uint8)
+    with pytest.raises(lzb.LzbError):
+        b.assemble_stream(n, guard[: len(want) // 2])
+    assert (guard[len(want) // 2:] == 0xCD).all()
