@@ -905,15 +905,79 @@ __global__ void k3_inject(Lv3 F, Lv3 C) {
 //   A_c[q] = sum_children sum_k K_child[k] W[child][k][q],
 //   W[child][k][q] = sum_{(i,j) in class k} Q_child[i][a_q] Q_child[j][b_q],
 // Q_child[i][a] = w(child lattice of corner i, a), (a_q, b_q) the
-// representative entry of class q. W (27^3 values) is a constant of the
-// trilinear transfer: computed once on the host, staged in shared memory.
-constexpr int kW3 = 27 * 27 * 27;
+// representative entry of class q. Q is a tensor product of per-axis
+// factors and a class is a per-axis product of pair classes, so W factors:
+// W[child][k][q] = prod_d wa[l_d][k_d][q_d], wa[l][kd][qd] = sum over the
+// axis pairs (i, j) of class kd of qax(l + i, a(qd)) qax(l + j, b(qd)),
+// qax(L, a) = (a ? L : 3 - L) / 3. The product is contracted axis by axis
+// (x, then y, then z): 243 FMA per child instead of 729, no weight table in
+// shared memory.
+__constant__ double c_wa[27];  // wa[l][kd][qd] at l * 9 + kd * 3 + qd
+
+std::vector<double> galerkin_axis_weights() {
+    std::vector<double> w(27, 0.0);
+    auto qax = [](int L, int a) { return static_cast<double>(a ? L : 3 - L) / 3.0; };
+    for (int l = 0; l < 3; ++l)
+        for (int kd = 0; kd < 3; ++kd)
+            for (int qd = 0; qd < 3; ++qd) {
+                const int a = qd == 2, b = qd >= 1;  // class representative (a, b) per axis
+                double acc = 0.0;
+                for (int i = 0; i < 2; ++i)
+                    for (int j = 0; j < 2; ++j) {
+                        const int cls = i == j ? 2 * i : 1;
+                        if (cls == kd) acc += qax(l + i, a) * qax(l + j, b);
+                    }
+                w[l * 9 + kd * 3 + qd] = acc;
+            }
+    return w;
+}
+void upload_galerkin_weights() {
+    static bool done = false;  // per process (one device per process)
+    if (done) return;
+    const std::vector<double> w = galerkin_axis_weights();
+    LZB_CUDA(cudaMemcpyToSymbol(c_wa, w.data(), 27 * sizeof(double)));
+    done = true;
+}
+
+// out[9 qx + 3 qy + qz] += sum_k K[9 kx + 3 ky + kz] wx[kx][qx] wy[ky][qy] wz[kz][qz]
+__device__ __forceinline__ void galerkin_child(const double* K, int lx, int ly, int lz, double* out) {
+    const double* wx = c_wa + lx * 9;
+    const double* wy = c_wa + ly * 9;
+    const double* wz = c_wa + lz * 9;
+#pragma unroll
+    for (int kz = 0; kz < 3; ++kz) {
+        double t1[3][3], t2[3][3];
+#pragma unroll
+        for (int qx = 0; qx < 3; ++qx)
+#pragma unroll
+            for (int ky = 0; ky < 3; ++ky) {
+                double acc = 0.0;
+#pragma unroll
+                for (int kx = 0; kx < 3; ++kx) acc = __fma_rn(K[9 * kx + 3 * ky + kz], wx[kx * 3 + qx], acc);
+                t1[qx][ky] = acc;
+            }
+#pragma unroll
+        for (int qx = 0; qx < 3; ++qx)
+#pragma unroll
+            for (int qy = 0; qy < 3; ++qy) {
+                double acc = 0.0;
+#pragma unroll
+                for (int ky = 0; ky < 3; ++ky) acc = __fma_rn(t1[qx][ky], wy[ky * 3 + qy], acc);
+                t2[qx][qy] = acc;
+            }
+#pragma unroll
+        for (int qx = 0; qx < 3; ++qx)
+#pragma unroll
+            for (int qy = 0; qy < 3; ++qy)
+#pragma unroll
+                for (int qz = 0; qz < 3; ++qz)
+                    out[9 * qx + 3 * qy + qz] = __fma_rn(t2[qx][qy], wz[kz * 3 + qz], out[9 * qx + 3 * qy + qz]);
+    }
+}
+
 template <class Src>
-__global__ void __launch_bounds__(256) k3_galerkin(double* __restrict__ cop, Src S, int Nc,
-                                                   const double* __restrict__ W, int64_t cbeg, int64_t cend) {
-    extern __shared__ double sW[];
-    for (int i = threadIdx.x; i < kW3; i += blockDim.x) sW[i] = W[i];
-    __syncthreads();
+__global__ void __launch_bounds__(256) k3_galerkin(double* __restrict__ cop, Src S, int Nc, int64_t cbeg,
+                                                   int64_t cend) {
     const int64_t c = cbeg + gtid();  // coarse cells [cbeg, cend)
     const int64_t ncc = static_cast<int64_t>(Nc) * Nc * Nc;
     if (c >= cend) return;
@@ -926,39 +990,10 @@ __global__ void __launch_bounds__(256) k3_galerkin(double* __restrict__ cop, Src
         const int lz = ch / 9, ly = (ch / 3) % 3, lx = ch % 3;
         double K27[27];
         S.load27((static_cast<int64_t>(3 * pz + lz) * Nf + 3 * py + ly) * Nf + 3 * px + lx, K27);
-        const double* Wc = sW + ch * 27 * 27;
-#pragma unroll
-        for (int k = 0; k < 27; ++k) {
-            const double kv = K27[k];
-#pragma unroll
-            for (int q = 0; q < 27; ++q) out[q] = __fma_rn(kv, Wc[k * 27 + q], out[q]);  // restated: FMA allowed
-        }
+        galerkin_child(K27, lx, ly, lz, out);
     }
 #pragma unroll
     for (int q = 0; q < 27; ++q) cop[q * ncc + c] = out[q];
-}
-
-std::vector<double> galerkin_weights3() {
-    std::vector<double> W(kW3, 0.0);
-    auto w = [](int lx, int ly, int lz, int a) {
-        return static_cast<double>(((a & 1) ? lx : 3 - lx) * (((a >> 1) & 1) ? ly : 3 - ly) * ((a >> 2) ? lz : 3 - lz)) /
-               27.0;
-    };
-    for (int ch = 0; ch < 27; ++ch) {
-        const int lz = ch / 9, ly = (ch / 3) % 3, lx = ch % 3;
-        for (int q = 0; q < 27; ++q) {
-            const int cx = q / 9, cy = (q / 3) % 3, cz = q % 3;
-            const int a = (cx == 2) + 2 * (cy == 2) + 4 * (cz == 2);
-            const int b = (cx >= 1) + 2 * (cy >= 1) + 4 * (cz >= 1);
-            for (int i = 0; i < 8; ++i)
-                for (int j = 0; j < 8; ++j) {
-                    const double qi = w(lx + (i & 1), ly + ((i >> 1) & 1), lz + (i >> 2), a);
-                    const double qj = w(lx + (j & 1), ly + ((j >> 1) & 1), lz + (j >> 2), b);
-                    W[(ch * 27 + cls3(i, j)) * 27 + q] += qi * qj;
-                }
-        }
-    }
-    return W;
 }
 
 // ------------------------------------------------------------ host side
@@ -1124,14 +1159,13 @@ public:
         if (ce <= cb) return;
         if (level + 1 == D_) {
             leaf_cls([&](auto S) {
-                LZB_LAUNCH(k3_galerkin<decltype(S)>, blocks_for(ce - cb, 256), 256, kW3 * sizeof(double), s_,
-                           L3_[level].op.p, S, N, W3_.p, cb, ce);
+                LZB_LAUNCH(k3_galerkin<decltype(S)>, blocks_for(ce - cb, 256), 256, 0, s_, L3_[level].op.p, S, N,
+                           cb, ce);
             });
         } else {
             const Src64 S{L3_[level + 1].op.p,
                           static_cast<int64_t>(L3_[level + 1].N) * L3_[level + 1].N * L3_[level + 1].N};
-            LZB_LAUNCH(k3_galerkin<Src64>, blocks_for(ce - cb, 256), 256, kW3 * sizeof(double), s_, L3_[level].op.p,
-                       S, N, W3_.p, cb, ce);
+            LZB_LAUNCH(k3_galerkin<Src64>, blocks_for(ce - cb, 256), 256, 0, s_, L3_[level].op.p, S, N, cb, ce);
         }
     }
 
@@ -1224,20 +1258,7 @@ public:
             if (l < D_) L.op.alloc(static_cast<size_t>(L.N) * L.N * L.N * kCls3);
         }
         partial3_.alloc(kNormBlocks3);
-        {
-            const std::vector<double> W = galerkin_weights3();
-            W3_.alloc(kW3);
-            LZB_CUDA(cudaMemcpy(W3_.p, W.data(), kW3 * sizeof(double), cudaMemcpyHostToDevice));
-            for (int w = 0; w <= 8; ++w)
-                if (w == 0 || w == W_)
-                    leaf_cls(
-                        [&](auto S) {
-                            LZB_CUDA(cudaFuncSetAttribute(k3_galerkin<decltype(S)>,
-                                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                          static_cast<int>(kW3 * sizeof(double))));
-                        },
-                        w);
-        }
+        upload_galerkin_weights();
         res3_.alloc(1);
         for (int l = 0; l <= D_; ++l)
             LZB_LAUNCH(k3_noise, vg(l), 128, 0, s_, lv(l), l, noise_seed, 0.0);
@@ -1515,7 +1536,7 @@ private:
     };
     static constexpr int kNormBlocks3 = 148 * 2;
     std::vector<Lev> L3_;
-    DevBuf<double> partial3_, res3_, W3_;
+    DevBuf<double> partial3_, res3_;
     int variant_ = LZB_ADDITIVE, max_cycles_ = 100;
     double omega_ = 0.6, target_ = 1e-10, first_ = 1.0;
     uint32_t cycle_ = 0;

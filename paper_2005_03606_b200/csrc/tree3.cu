@@ -164,10 +164,7 @@ __global__ void k4_copy_leaf_ops(const int4* __restrict__ leaves, int64_t n, int
     for (int q = 0; q < 27; ++q) L.op[q * L.nop + j] = lop[q * nleaves + t];
 }
 // refined cells of C: Galerkin from the 27 children of F (k3_galerkin's class form)
-__global__ void __launch_bounds__(256) k4_galerkin(LvA C, LvA F, const double* __restrict__ W) {
-    extern __shared__ double sW[];
-    for (int i = threadIdx.x; i < kW3; i += blockDim.x) sW[i] = W[i];
-    __syncthreads();
+__global__ void __launch_bounds__(256) k4_galerkin(LvA C, LvA F) {
     const int64_t c = gtid();
     const int64_t ncc = static_cast<int64_t>(C.N) * C.N * C.N;
     if (c >= ncc || C.cf[c] != 2) return;
@@ -178,12 +175,10 @@ __global__ void __launch_bounds__(256) k4_galerkin(LvA C, LvA F, const double* _
     for (int ch = 0; ch < 27; ++ch) {
         const int lz = ch / 9, ly = (ch / 3) % 3, lx = ch % 3;
         const int32_t j = F.oi[cidx(F.N, 3 * px + lx, 3 * py + ly, 3 * pz + lz)];
-        const double* Wc = sW + ch * 27 * 27;
-        for (int k = 0; k < 27; ++k) {
-            const double kv = F.op[k * F.nop + j];
+        double K27[27];
 #pragma unroll
-            for (int q = 0; q < 27; ++q) out[q] = __fma_rn(kv, Wc[k * 27 + q], out[q]);
-        }
+        for (int k = 0; k < 27; ++k) K27[k] = F.op[k * F.nop + j];
+        galerkin_child(K27, lx, ly, lz, out);
     }
     const int32_t jc = C.oi[c];
 #pragma unroll
@@ -639,13 +634,7 @@ public:
             L.op.alloc(static_cast<size_t>(std::max(cnt, 1)) * kCls3);
             LZB_LAUNCH(k4_classify, vgA(l), 128, 0, s_, lv(l));
         }
-        if (!W3_.n) {
-            const std::vector<double> W = galerkin_weights3();
-            W3_.alloc(kW3);
-            LZB_CUDA(cudaMemcpy(W3_.p, W.data(), kW3 * sizeof(double), cudaMemcpyHostToDevice));
-            LZB_CUDA(cudaFuncSetAttribute(k4_galerkin, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(kW3 * sizeof(double))));
-        }
+        upload_galerkin_weights();
         refresh_ops();
         partialA_.alloc(kNormBlocksA);
         for (int l = 0; l <= D; ++l) LZB_LAUNCH(k4_noise, vgA(l), 128, 0, s_, lv(l), l, seed);
@@ -663,8 +652,7 @@ public:
             LZB_LAUNCH(k4_copy_leaf_ops, blocks_for(n_leaves_, 256), 256, 0, s_, dleaves_.p, n_leaves_, l, op_.p,
                        n_leaves_, lv(l));
         for (int l = lmax_ - 1; l >= 0; --l)
-            LZB_LAUNCH(k4_galerkin, blocks_for(A_[l].nc, 256), 256, kW3 * sizeof(double), s_, lv(l), lv(l + 1),
-                       W3_.p);
+            LZB_LAUNCH(k4_galerkin, blocks_for(A_[l].nc, 256), 256, 0, s_, lv(l), lv(l + 1));
     }
 
     lzb_cycle_report step() {
@@ -744,7 +732,7 @@ private:
     };
     static constexpr int kNormBlocksA = 148 * 2;
     std::vector<LevA> A_;
-    DevBuf<double> W3_, partialA_;
+    DevBuf<double> partialA_;
     int variant_ = LZB_ADDITIVE, max_cycles_ = 100;
     double omega_ = 0.6, target_ = 1e-10, first_ = 1.0;
     uint32_t cycle_ = 0;
