@@ -1568,18 +1568,8 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_pack_patches(AllLevels A, l
     if (px >= px0 + pxn) return;
     const int64_t obase = basep ? *basep : 0;
     const unsigned full = 0xffffffffu;
-    // pre-order slot of patch (px, py0) from its base-3 digits (no table loads
-    // in front of the offsets load)
-    int64_t s0 = D - 1;
-    {
-        int x = px, y = py0;
-        for (int k = D - 1; k >= 1; --k) {
-            const int dx = x % 3, dy = y % 3;
-            x /= 3;
-            y /= 3;
-            s0 += (dx * 3 + dy) * A.st.subtree[k];
-        }
-    }
+    // pre-order slot of patch (px, py0)
+    const int64_t s0 = slot_at(A.st, D - 1, px, py0);  // digit tables (L1/L2-resident)
     const int nrec = 10 * per;
     // the patch records' Â entries (lane < 16), loaded with everything else
     double ra[3] = {0.0, 0.0, 0.0};
@@ -1646,7 +1636,7 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_pack_patches(AllLevels A, l
         for (int h = 0; h < 8; ++h) {
             x[2 * h] = v[h].x - (0.0 + c_kunit[2 * h] * e);
             x[2 * h + 1] = v[h].y - (0.0 + c_kunit[2 * h + 1] * e);
-            ok = ok && dev_isfinite(x[2 * h]) && dev_isfinite(x[2 * h + 1]);
+            ok &= dev_isfinite(x[2 * h]) & dev_isfinite(x[2 * h + 1]);  // no short-circuit branches
         }
         // the integrated operators repeat 9 values (k9_expand), and so does the baseline
         const bool sym = x[1] == x[4] && x[11] == x[14] && x[2] == x[8] && x[7] == x[13] && x[3] == x[12] &&
