@@ -759,21 +759,33 @@ __global__ void k3_restrict(Lv3 F, Lv3 C) {
     C.v[LZB_V_FL][vi] = acc;
 }
 
+// Per-block partial sums of r^2 over the interior vertices of planes
+// [max(zlo, 1), min(zhi, N)): block b takes rows b, b + G, ... four rows per
+// step (four independent loads in flight per thread), then a fixed-order tree.
 __global__ void k3_norm_partial(Lv3 F, double* partial, int zlo, int zhi) {
     __shared__ double sh[256];
     const int N = F.N;
-    double s = 0.0;
-    // interior (y, z) rows with z in [max(zlo,1), min(zhi,N))
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
     const int za = max(zlo, 1), zb = min(zhi, N);
     const int64_t rows = zb > za ? static_cast<int64_t>(N - 1) * (zb - za) : 0;
-    for (int64_t rz = blockIdx.x; rz < rows; rz += gridDim.x) {
-        const int iy = 1 + static_cast<int>(rz % (N - 1)), iz = za + static_cast<int>(rz / (N - 1));
+    const int64_t G = gridDim.x;
+    for (int64_t r0 = blockIdx.x; r0 < rows; r0 += 4 * G) {
+        int64_t base[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t rz = r0 + k * G;
+            base[k] = rz < rows ? vidx3(N, 0, 1 + static_cast<int>(rz % (N - 1)), za + static_cast<int>(rz / (N - 1)))
+                                : -1;
+        }
         for (int ix = 1 + threadIdx.x; ix < N; ix += blockDim.x) {
-            const double r = F.v[LZB_V_R][vidx3(N, ix, iy, iz)];
-            s += r * r;
+            double r[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) r[k] = base[k] >= 0 ? F.v[LZB_V_R][base[k] + ix] : 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) s[k] += r[k] * r[k];
         }
     }
-    sh[threadIdx.x] = s;
+    sh[threadIdx.x] = (s[0] + s[1]) + (s[2] + s[3]);
     __syncthreads();
     for (int w = blockDim.x / 2; w > 0; w >>= 1) {
         if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
@@ -1534,7 +1546,7 @@ private:
         DevBuf<double> v[LZB_V_NFIELDS];
         DevBuf<double> op;  // coarse levels (the leaves use op_)
     };
-    static constexpr int kNormBlocks3 = 148 * 2;
+    static constexpr int kNormBlocks3 = 148 * 4;
     std::vector<Lev> L3_;
     DevBuf<double> partial3_, res3_;
     int variant_ = LZB_ADDITIVE, max_cycles_ = 100;
