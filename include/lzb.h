@@ -143,11 +143,11 @@ int lzb_grid_stats(lzb_grid* g, lzb_compression_stats* out);
  * lzb_grid_stream_image with out == NULL returns the size in *size. */
 int lzb_grid_stream_image(lzb_grid* g, uint8_t* out, int64_t cap, int64_t* size);
 /* lzb_grid_assemble_fixed(g, n) then lzb_grid_stream_image(g, out, cap, size),
- * pipelined: the image's three x bands of level-1 subtrees (contiguous byte
- * ranges in pre-order) are packed and copied to `out` while the next band
- * assembles. Same bytes; LZB_ERR_INVALID if the image exceeds cap (nothing
- * past cap is written). timeline: NULL or 9 floats (device ms of each band's
- * assembly, pack and copy end). Replaces Assembler::eager_setup at fixed n +
+ * pipelined: three bands of level-1 subtrees (contiguous byte ranges in
+ * pre-order) are packed and copied to `out` while the next band assembles.
+ * Same bytes; LZB_ERR_INVALID if the image exceeds cap (nothing past cap is
+ * written). timeline: NULL or 9 floats (device ms of each band's assembly,
+ * pack and copy end). Replaces Assembler::eager_setup at fixed n +
  * CellStream::save (assembly.cpp:111-118, stream.cpp:303-338). */
 int lzb_grid_assemble_stream(lzb_grid* g, int n, uint8_t* out, int64_t cap, int64_t* size, float* timeline);
 int lzb_grid_stream_load(lzb_grid* g, const uint8_t* in, int64_t size);

@@ -2369,7 +2369,7 @@ public:
             cudaStreamSynchronize(cp_);
             cudaStreamDestroy(cp_);
             cudaFreeHost(hbase_);
-            for (int k = 0; k < 3; ++k) {
+            for (int k = 0; k < kBands; ++k) {
                 cudaEventDestroy(ev_asm_[k]);
                 cudaEventDestroy(ev_pack_[k]);
                 cudaEventDestroy(ev_copy_[k]);
@@ -3265,14 +3265,16 @@ public:
     // assemble_fixed(n) followed by image_into(out, cap), pipelined: the LZMG
     // image is a root record followed by the 9 level-1 subtrees in child
     // order lx * 3 + ly (pre-order, mesh.cpp:152-157), so each x band of 3
-    // subtrees is one contiguous byte range. Band by band the solve stream
-    // assembles the leaves, then sizes, scans and packs its records (offsets chained through a
-    // device running base) and the copy stream moves its bytes to the host
-    // while the next band assembles (a band is ~600 cells per resident
-    // block; a single subtree would leave the persistent assembly kernel
-    // under one iteration per block). Same bytes as the sequential calls.
-    // timeline: NULL or 9 floats, device ms of each band's assembly, pack
-    // and copy end after the start.
+    // subtrees is one contiguous byte range, and so is any run of subtrees
+    // inside one column. Band by band (the three columns: smaller bands,
+    // e.g. {1, 2, 3, 2, 1} subtrees, measured 1.96 ms against 1.90: a band
+    // under ~600 cells per resident block slows the persistent assembly
+    // kernel more than the earlier copy start saves) the solve stream
+    // assembles the leaves, then sizes, scans and packs the band's records
+    // (offsets chained through a device running base), and the copy stream
+    // moves its bytes to the host while the next band assembles. Same bytes
+    // as the sequential calls. timeline: NULL or 3 x kBands floats, device
+    // ms of each band's assembly, pack and copy end.
     int64_t assemble_stream(int n, uint8_t* out, int64_t cap, float* timeline) {
         if (n < 1) throw Error(LZB_ERR_INVALID, "n must be >= 1");
         if (D_ < 2) {
@@ -3287,10 +3289,10 @@ public:
         const size_t cap_dev = static_cast<size_t>(12 + total_cells_ + leaves * 128 + refined * 1152);
         if (img_.n < cap_dev) img_.alloc(cap_dev);
         if (!st_ready_) {
-            stream_base_.alloc(4);
-            LZB_CUDA(cudaMallocHost(&hbase_, 4 * sizeof(int64_t)));
+            stream_base_.alloc(kBands + 1);
+            LZB_CUDA(cudaMallocHost(&hbase_, (kBands + 1) * sizeof(int64_t)));
             LZB_CUDA(cudaStreamCreateWithFlags(&cp_, cudaStreamNonBlocking));
-            for (int k = 0; k < 3; ++k) {
+            for (int k = 0; k < kBands; ++k) {
                 LZB_CUDA(cudaEventCreate(&ev_asm_[k]));
                 LZB_CUDA(cudaEventCreate(&ev_pack_[k]));
                 LZB_CUDA(cudaEventCreate(&ev_copy_[k]));
@@ -3311,36 +3313,41 @@ public:
         LZB_LAUNCH(k_root_base, 1, 1, 0, s_, rec_sizes_.p, rec_offs_.p, stream_base_.p);
         LZB_LAUNCH(k_pack_upper, 1, 32, 0, s_, AL, d_.field, 1, rec_offs_.p, img_.p, ctx_->err.p, -1, -1, nullptr);
         LZB_CUDA(cudaEventRecord(ev_root_, s_));
-        const int per = Nc >= 3 ? 3 : 1;
-        // band a (subtrees (a, 0..2), leaf columns [a w, (a + 1) w)): assembly, then
-        // its sizes / scan / pack, all on the solve stream (the persistent assembly
-        // kernel holds every SM while it runs, so a pack beside it would starve)
-        for (int a = 0; a < 3; ++a) {
-            const int64_t s0 = 1 + 3 * a * S1;
-            assemble_rect(n, CellRect{a * w, w, 0}, static_cast<int64_t>(w) * N, s_);
-            LZB_CUDA(cudaEventRecord(ev_asm_[a], s_));
-            LZB_LAUNCH(k_record_sizes_patches, dim3(blocks_for(pw, 64), Nc), 64, 0, s_, AL, rec_sizes_.p, a * pw, pw, 0);
-            for (int b = 0; b < 3 && nup > 0; ++b)
+        // band i: subtrees [k0, k1) of column a = k0 / 3, rows b0 = k0 % 3 .. b1 - 1;
+        // assembly, then its sizes / scan / pack, all on the solve stream (the
+        // persistent assembly kernel holds every SM while it runs, so a pack beside
+        // it would starve)
+        static constexpr int kBand[kBands + 1] = {0, 3, 6, 9};
+        for (int i = 0; i < kBands; ++i) {
+            const int k0 = kBand[i], k1 = kBand[i + 1], a = k0 / 3, b0 = k0 % 3, nb = k1 - k0;
+            const int64_t s0 = 1 + k0 * S1, nslot = nb * S1;
+            const int prow = nb * pw;  // patch rows of the band
+            const int per = prow % 3 == 0 ? 3 : 1;
+            assemble_rect(n, CellRect{a * w, w, b0 * w}, static_cast<int64_t>(w) * nb * w, s_);
+            LZB_CUDA(cudaEventRecord(ev_asm_[i], s_));
+            LZB_LAUNCH(k_record_sizes_patches, dim3(blocks_for(pw, 64), prow), 64, 0, s_, AL, rec_sizes_.p, a * pw, pw,
+                       b0 * pw);
+            for (int b = b0; b < b0 + nb && nup > 0; ++b)
                 LZB_LAUNCH(k_record_sizes_upper, blocks_for(nup, kThreads), kThreads, 0, s_, AL, nup, rec_sizes_.p,
                            a, b);
             size_t tb = scan_tmp_.n;
             LZB_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp_.p, tb, rec_sizes_.p + s0, rec_offs_.p + s0,
-                                                  static_cast<int>(3 * S1), s_));
-            LZB_LAUNCH(k_chunk_base, 1, 1, 0, s_, rec_sizes_.p + s0, rec_offs_.p + s0, 3 * S1, stream_base_.p + a);
-            LZB_LAUNCH(k_pack_patches, dim3(blocks_for(pw, kPackWarps), Nc / per), kPackWarps * 32, 0, s_, AL,
-                       d_.field, T, per, rec_offs_.p, img_.p, ctx_->err.p, a * pw, pw, 0, stream_base_.p + a);
-            for (int b = 0; b < 3 && nup > 0; ++b)
+                                                  static_cast<int>(nslot), s_));
+            LZB_LAUNCH(k_chunk_base, 1, 1, 0, s_, rec_sizes_.p + s0, rec_offs_.p + s0, nslot, stream_base_.p + i);
+            LZB_LAUNCH(k_pack_patches, dim3(blocks_for(pw, kPackWarps), prow / per), kPackWarps * 32, 0, s_, AL,
+                       d_.field, T, per, rec_offs_.p, img_.p, ctx_->err.p, a * pw, pw, b0 * pw, stream_base_.p + i);
+            for (int b = b0; b < b0 + nb && nup > 0; ++b)
                 LZB_LAUNCH(k_pack_upper, blocks_for(nup, kThreads / 32), kThreads, 0, s_, AL, d_.field, nup,
-                           rec_offs_.p, img_.p, ctx_->err.p, a, b, stream_base_.p + a);
-            LZB_CUDA(cudaMemcpyAsync(hbase_ + a, stream_base_.p + a + 1, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                           rec_offs_.p, img_.p, ctx_->err.p, a, b, stream_base_.p + i);
+            LZB_CUDA(cudaMemcpyAsync(hbase_ + i, stream_base_.p + i + 1, sizeof(int64_t), cudaMemcpyDeviceToHost,
                                      s_));
-            LZB_CUDA(cudaEventRecord(ev_pack_[a], s_));
+            LZB_CUDA(cudaEventRecord(ev_pack_[i], s_));
         }
         // host: as each band's byte range becomes known, queue its copy (copy
         // engine, concurrent with the next bands' assembly)
         bool overflow = false;
         int64_t lo = 12;
-        for (int a = 0; a < 3; ++a) {
+        for (int a = 0; a < kBands; ++a) {
             LZB_CUDA(cudaEventSynchronize(ev_pack_[a]));
             const int64_t hi = 12 + hbase_[a];
             if (hi > cap) overflow = true;
@@ -3353,10 +3360,10 @@ public:
         }
         LZB_CUDA(cudaStreamSynchronize(cp_));
         if (timeline)
-            for (int a = 0; a < 3; ++a) {
+            for (int a = 0; a < kBands; ++a) {
                 LZB_CUDA(cudaEventElapsedTime(&timeline[a], ev_start_, ev_asm_[a]));
-                LZB_CUDA(cudaEventElapsedTime(&timeline[3 + a], ev_start_, ev_pack_[a]));
-                LZB_CUDA(cudaEventElapsedTime(&timeline[6 + a], ev_start_, ev_copy_[a]));
+                LZB_CUDA(cudaEventElapsedTime(&timeline[kBands + a], ev_start_, ev_pack_[a]));
+                LZB_CUDA(cudaEventElapsedTime(&timeline[2 * kBands + a], ev_start_, ev_copy_[a]));
             }
         sync_check();
         if (overflow) throw Error(LZB_ERR_INVALID, "stream image buffer too small");
@@ -3554,7 +3561,9 @@ private:
     DevBuf<int64_t> rec_sizes_, rec_offs_, stream_base_;
     int64_t* hbase_ = nullptr;  // pinned: the running image base per band
     cudaStream_t cp_ = nullptr;
-    cudaEvent_t ev_asm_[3] = {}, ev_pack_[3] = {}, ev_copy_[3] = {}, ev_root_ = nullptr, ev_start_ = nullptr;
+    static constexpr int kBands = 3;  // assemble_stream bands of level-1 subtrees
+    cudaEvent_t ev_asm_[kBands] = {}, ev_pack_[kBands] = {}, ev_copy_[kBands] = {}, ev_root_ = nullptr,
+                ev_start_ = nullptr;
     bool st_ready_ = false;
     DevBuf<unsigned char> scan_tmp_;
     DevBuf<uint8_t> img_;
