@@ -99,3 +99,36 @@ def test_cycle3a_sphere_tree_converges():
     assert (a.kind[3] == 3).any() and (a.kind[2] == 3).any()
     reps = [a.step() for _ in range(25)]
     assert reps[-1]["normalized"] < 0.05, [r["normalized"] for r in reps[::6]]
+
+
+def test_galerkin_class_weights_factor_per_axis():
+    """The class-form Galerkin weights W[child][k][q] (sum over the (i, j) of
+    class k of Q_child[i][a_q] Q_child[j][b_q], trilinear Q) equal the product
+    of per-axis factors wa[l][kd][qd] that k3_galerkin contracts axis by axis."""
+    def qax(L, a):
+        return (L if a else 3 - L) / 3.0
+
+    wa = np.zeros((3, 3, 3))
+    for l in range(3):
+        for kd in range(3):
+            for qd in range(3):
+                a, b = int(qd == 2), int(qd >= 1)
+                wa[l, kd, qd] = sum(qax(l + i, a) * qax(l + j, b) for i in (0, 1) for j in (0, 1)
+                                    if (2 * i if i == j else 1) == kd)
+
+    def cls(i, j):
+        return tuple(2 * ((i >> d) & 1) if ((i >> d) & 1) == ((j >> d) & 1) else 1 for d in range(3))
+
+    for lx, ly, lz in [(0, 0, 0), (1, 2, 0), (2, 1, 1), (2, 2, 2)]:
+        for q in range(27):
+            qx, qy, qz = q // 9, (q // 3) % 3, q % 3
+            a = (qx == 2) + 2 * (qy == 2) + 4 * (qz == 2)
+            b = (qx >= 1) + 2 * (qy >= 1) + 4 * (qz >= 1)
+            W = np.zeros((3, 3, 3))
+            for i in range(8):
+                for j in range(8):
+                    Li = (lx + (i & 1), ly + ((i >> 1) & 1), lz + (i >> 2))
+                    Lj = (lx + (j & 1), ly + ((j >> 1) & 1), lz + (j >> 2))
+                    W[cls(i, j)] += o3.pw3(Li, a) * o3.pw3(Lj, b)
+            want = np.einsum("i,j,k->ijk", wa[lx, :, qx], wa[ly, :, qy], wa[lz, :, qz])
+            assert np.allclose(W, want, rtol=1e-14, atol=1e-16)
