@@ -419,21 +419,57 @@ __device__ __noinline__ int choose_precision_set(const double* v, double delta) 
 // each value are upward closed): the running maximum P of the
 // per-value smallest passing widths, each value testing only widths >= P.
 // Other records take the general routine.
+//
+// Values with exponent e in [-127, 127] (or +-0) are "plain": no clamp and no
+// (0, 0, -128) decode apply, so truncation to m fraction bits is a mask and
+// the error is exactly the dropped fraction bits F_low * 2^(e - 52) (rt and v
+// share the exponent: the subtraction of the reference test is exact); the
+// test |rt - v| <= delta is then F_low <= delta * 2^(52 - e), an integer
+// comparison against one exact product per value.
+__device__ __forceinline__ bool codec_plain(unsigned long long u) {
+    const int E = static_cast<int>((u >> 52) & 0x7ff);
+    return (u << 1) == 0 || (E >= 1023 - 127 && E <= 1023 + 127);
+}
+// the smallest width in [P, 7] a plain value passes, else 8
+__device__ __forceinline__ int min_width_plain(unsigned long long u, double delta, int P) {
+    if ((u << 1) == 0) return P;  // +-0: error 0 at every width
+    const int E = static_cast<int>((u >> 52) & 0x7ff);
+    const double T = delta * __longlong_as_double(static_cast<long long>(2098 - E) << 52);  // delta 2^(1075 - E)
+    const unsigned long long F = u & 0xFFFFFFFFFFFFFull;
+    while (P < 8 && static_cast<double>(F & ((1ull << (52 - mantissa_bits(P))) - 1)) > T) ++P;
+    return P;
+}
+// roundtrip at width p3 in 2..7 of a plain value: the low fraction bits cleared
+__device__ __forceinline__ double rt_plain(unsigned long long u, int p3) {
+    if ((u << 1) == 0) return 0.0;  // -0 encodes as +0
+    return __longlong_as_double(static_cast<long long>(u & ~((1ull << (52 - mantissa_bits(p3))) - 1)));
+}
+
+// plain: every value plain (then the caller may roundtrip with rt_plain)
 template <int COUNT>
-__device__ __forceinline__ int choose_precision_regular(const double* v, double delta) {
-    bool all_small = true, regular = true;
+__device__ __forceinline__ int choose_precision_regular(const double* v, double delta, bool& plain) {
+    bool all_small = true;
+    plain = true;
 #pragma unroll
     for (int i = 0; i < COUNT; ++i) {
         all_small = all_small && !(fabs(v[i]) > delta);
-        regular = regular && codec_regular(v[i]);
+        plain = plain && codec_plain(static_cast<unsigned long long>(__double_as_longlong(v[i])));
     }
     if (all_small) return 0;
-    if (!regular) return choose_precision_set<COUNT>(v, delta);
+    if (!plain) return choose_precision_set<COUNT>(v, delta);
     int P = 2;
 #pragma unroll
     for (int i = 0; i < COUNT; ++i)
-        while (P < 8 && fabs(rt_bits(v[i], mantissa_bits(P)) - v[i]) > delta) ++P;
+        P = min_width_plain(static_cast<unsigned long long>(__double_as_longlong(v[i])), delta, P);
     return P;
+}
+// codec::roundtrip for one value of a record coded at p3 (plain: rt_plain)
+__device__ __forceinline__ bool roundtrip_rec(double x, int p3, bool plain, double& rt) {
+    if (plain && p3 >= 2 && p3 <= 7) {
+        rt = rt_plain(static_cast<unsigned long long>(__double_as_longlong(x)), p3);
+        return true;
+    }
+    return roundtrip_fast(x, p3, rt);
 }
 
 // Fixed-p assembly of every cell of a 3D level: integrate at n, code the
@@ -462,7 +498,8 @@ __global__ void __launch_bounds__(128, 4) k_assemble3(Field3 F, int N, double h,
         for (int q = 0; q < 27; ++q)
             sur[q] = class_value(A, hn, q / 9, (q / 3) % 3, q % 3) - B(q / 9, (q / 3) % 3, q % 3);
     }
-    const int p3 = fixed_p3 ? fixed_p3 : choose_precision_regular<27>(sur, delta_max);
+    bool plain = false;
+    const int p3 = fixed_p3 ? fixed_p3 : choose_precision_regular<27>(sur, delta_max, plain);
     if (p3 < 0) {
         atomicExch(err, 1);
         return;
@@ -476,7 +513,7 @@ __global__ void __launch_bounds__(128, 4) k_assemble3(Field3 F, int N, double h,
 #pragma unroll
     for (int q = 0; q < 27; ++q) {
         double rt;
-        if (!roundtrip_fast(sur[q], p3, rt)) {
+        if (!roundtrip_rec(sur[q], p3, plain, rt)) {
             atomicExch(err, 1);
             return;
         }

@@ -48,7 +48,8 @@ __global__ void __launch_bounds__(128, 4) k_assemble3_leaves(Field3 F, const int
         for (int q = 0; q < 27; ++q)
             sur[q] = class_value(A, hn, q / 9, (q / 3) % 3, q % 3) - B(q / 9, (q / 3) % 3, q % 3);
     }
-    const int p3 = fixed_p3 ? fixed_p3 : choose_precision_regular<27>(sur, delta_max);
+    bool plain = false;
+    const int p3 = fixed_p3 ? fixed_p3 : choose_precision_regular<27>(sur, delta_max, plain);
     if (p3 < 0) {
         atomicExch(err, 1);
         return;
@@ -57,7 +58,7 @@ __global__ void __launch_bounds__(128, 4) k_assemble3_leaves(Field3 F, const int
 #pragma unroll
     for (int q = 0; q < 27; ++q) {
         double rt;
-        if (!roundtrip_fast(sur[q], p3, rt)) {
+        if (!roundtrip_rec(sur[q], p3, plain, rt)) {
             atomicExch(err, 1);
             return;
         }
