@@ -377,3 +377,25 @@ def test_assemble_stream_matches_sequential(depth, kind, dmax, n):
     with pytest.raises(lzb.LzbError):
         b.assemble_stream(n, guard[: len(want) // 2])
     assert (guard[len(want) // 2:] == 0xCD).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("text,exact", [
+    ("setup = theta\ntheta = 16\nrhs = 1\ndepth = 5\nsolver = additive\nassembly = anarchic\nmax-cycles = 3\n",
+     False),
+    ("setup = quadrant\neps-low = 0.001\nrhs = 1\ndepth = 6\nsolver = adafac-pi\nassembly = anarchic\n"
+     "max-cycles = 2\n", True),
+])
+def test_deep_grids_match_oracle(text, exact):
+    """Depths 5 and 6 (the survey's gate depths; the oracle is pinned to the
+    unmodified reference there): the quadrant field bit-identical (u on every
+    level, operators, markers, LZMG bytes); the theta field through CUDA libm
+    within the transcendental-field tolerances."""
+    text += "omega = 0.6\nseed = 42\n"
+    d = port.desc_from_keys(port.parse_keys(text))
+    g, o = lzb.Grid(d, 42), port.Grid(d, 42)
+    rg, ro = g.run(), o.run()
+    assert_reports(rg, ro, rel=1e-13 if exact else 1e-10)
+    assert_state(g, o, d.depth, exact=exact)
+    if exact:
+        assert g.stream_image() == o.stream_image()
