@@ -219,6 +219,10 @@ int lzb_grid3_cells(lzb_grid3* g, int64_t first, int64_t count, double* ops, int
 int lzb_grid3_init_cycle(lzb_grid3* g, int variant, double omega, double rhs_scale, uint64_t noise_seed,
                          int max_cycles, double target);
 int lzb_grid3_step(lzb_grid3* g, lzb_cycle_report* out);
+/* One multiplicative V(nu, nu) cycle with damped Jacobi (omega of
+ * init_cycle) on the same levels, Galerkin operators and transfers
+ * (BASELINE configs[1..2] V-cycles; restated, the reference is additive only). */
+int lzb_grid3_vcycle(lzb_grid3* g, int nu, lzb_cycle_report* out);
 int lzb_grid3_vertices(lzb_grid3* g, int level, int field, double* out);  /* (N+1)^3 doubles */
 /* Slab-distributed 3D cycle: z-slabs of leaf vertex planes, coarse levels
  * replicated; phases 0..5 and exchanges as lzb_grid_dist_phase (driven by

@@ -383,6 +383,54 @@ class Cycle3:
         return {"cycle": self.cycle, "residual": res, "normalized": norm, "status": status}
 
 
+def _cycle3_vstep(self, nu=2):
+    """One multiplicative V(nu, nu) cycle (restated extension; device:
+    lzb_grid3_vcycle): per level from the leaves nu damped-Jacobi sweeps, the
+    residual restricted (P^T over owned lattice vertices) into the next
+    level's rhs with a zero start; back up: u_l += P u_{l-1}, nu sweeps.
+    Returns the report of the leaf residual before the cycle."""
+    D = self.D
+
+    def residual(l):
+        V = self.v[l]
+        V["uh"] = V["u"].copy()
+        self._residual(l)
+
+    def smooth(l, k):
+        for _ in range(k):
+            residual(l)
+            V = self.v[l]
+            inner = self._interior(self.N[l])
+            with np.errstate(divide="ignore", invalid="ignore"):
+                upd = np.where(V["dg"] != 0, self.omega / V["dg"] * V["r"], 0.0)
+            V["u"] = np.where(inner, V["u"] + upd, V["u"])
+
+    self.cycle += 1
+    residual(D)
+    n = self.N[D]
+    res = math.sqrt(float(np.sum(self.v[D]["r"][1:n, 1:n, 1:n] ** 2)))
+    if not self.history:
+        self.first = res if res > 0 else 1.0
+    self.history.append(res)
+    norm = res / self.first
+    status = 1 if norm <= self.target else (2 if norm >= 1e2 else (3 if self.cycle >= self.max_cycles else 0))
+    if status in (0, 3):
+        for l in range(D, 0, -1):
+            smooth(l, nu)
+            residual(l)
+            self.v[l - 1]["fl"] = self._restrict(l, self.v[l]["rh"])
+            self.v[l - 1]["u"] = np.zeros_like(self.v[l - 1]["u"])
+        for l in range(1, D + 1):
+            V = self.v[l]
+            inner = self._interior(self.N[l])
+            V["u"] = np.where(inner, V["u"] + self._interp(l, self.v[l - 1]["u"]), V["u"])
+            smooth(l, nu)
+    return {"cycle": self.cycle, "residual": res, "normalized": norm, "status": status}
+
+
+Cycle3.vstep = _cycle3_vstep
+
+
 class Cycle3A:
     """The additive cycle of proj/src/solver.cpp:99-347 on a 3D ADAPTIVE
     spacetree (BASELINE configs[3]), restated from the reference's 2D adaptive

@@ -131,6 +131,7 @@ def lib():
         L.lzb_grid3_cells.argtypes = [vp, i64, i64, vp, vp]
         L.lzb_grid3_init_cycle.argtypes = [vp, C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_int, C.c_double]
         L.lzb_grid3_step.argtypes = [vp, C.POINTER(CycleReport)]
+        L.lzb_grid3_vcycle.argtypes = [vp, C.c_int, C.POINTER(CycleReport)]
         L.lzb_grid3_vertices.argtypes = [vp, C.c_int, C.c_int, vp]
         L.lzb_grid3_set_slab.argtypes = [vp, C.c_int, C.c_int]
         L.lzb_grid3_dist_phase.argtypes = [vp, C.c_int]
@@ -738,6 +739,12 @@ class Grid3:
     def step(self) -> dict:
         r = CycleReport()
         _check(lib().lzb_grid3_step(self.h, C.byref(r)))
+        return report_dict(r)
+
+    def vcycle(self, nu=2) -> dict:
+        """One multiplicative V(nu, nu) cycle (lzb_grid3_vcycle)."""
+        r = CycleReport()
+        _check(lib().lzb_grid3_vcycle(self.h, nu, C.byref(r)))
         return report_dict(r)
 
     # slab-distributed cycle (parallel.dist_cycle3)

@@ -1323,6 +1323,73 @@ public:
         for (int l = D_ - 1; l >= 0; --l) galerkin_planes(l, 0, L3_[l].N);
     }
 
+    // A multiplicative V(nu, nu) cycle on the same hierarchy (BASELINE
+    // configs[1..2] name V(1,1) / V(2,2) cycles; the reference has only the
+    // additive cycle, so this is a restated extension, oracle/port3.py
+    // Cycle3.vstep): per level from the leaves, nu damped-Jacobi sweeps,
+    // the residual restricted (R = P^T, the restriction of the additive
+    // cycle) into the next level's right-hand side with a zero start; at the
+    // bottom back up, the coarse correction prolongated (P, the additive
+    // cycle's interpolation) and nu sweeps. The report's residual is the
+    // leaf residual before the cycle.
+    lzb_cycle_report vcycle(int nu) {
+        if (L3_.empty()) throw Error(LZB_ERR_INVALID, "call init_cycle first");
+        if (nu < 0) throw Error(LZB_ERR_INVALID, "nu must be >= 0");
+        if (ops_dirty_) {
+            coarse_ops();
+            ops_dirty_ = false;
+        }
+        lzb_cycle_report rep;
+        std::memset(&rep, 0, sizeof rep);
+        rep.cycle = static_cast<int32_t>(++cycle_);
+        auto residual_plain = [&](int l) {  // r (and r-hat = r) of level l from its fl
+            LZB_LAUNCH(k3_uhat, vg(l), 128, 0, s_, lv(l), lv(l), 0);
+            residual3(l, 0, L3_[l].N + 1);
+        };
+        auto smooth = [&](int l, int k) {
+            for (int i = 0; i < k; ++i) {
+                residual_plain(l);
+                LZB_LAUNCH(k3_jacobi, vg(l), 128, 0, s_, lv(l), omega_);
+            }
+        };
+        residual_plain(D_);
+        LZB_CUDA(cudaMemsetAsync(partial3_.p, 0, partial3_.bytes(), s_));
+        if (L3_[D_].N > 1)
+            LZB_LAUNCH(k3_norm_partial, kNormBlocks3, 256, 0, s_, lv(D_), partial3_.p, 0, L3_[D_].N + 1);
+        std::vector<double> part(kNormBlocks3);
+        LZB_CUDA(cudaMemcpyAsync(part.data(), partial3_.p, kNormBlocks3 * sizeof(double), cudaMemcpyDeviceToHost, s_));
+        sync();
+        double s2 = 0.0;
+        for (double x : part) s2 += x;
+        rep.residual = std::sqrt(s2);
+        if (history_.empty()) first_ = rep.residual > 0.0 ? rep.residual : 1.0;
+        history_.push_back(rep.residual);
+        rep.normalized = rep.residual / first_;
+        rep.status = rep.normalized <= target_ ? LZB_CONVERGED
+                     : rep.normalized >= 1e2 ? LZB_DIVERGED
+                     : static_cast<int>(cycle_) >= max_cycles_ ? LZB_TIMEOUT : LZB_CONTINUE;
+        if (rep.status == LZB_CONTINUE || rep.status == LZB_TIMEOUT) {
+            for (int l = D_; l >= 1; --l) {
+                smooth(l, nu);
+                residual_plain(l);
+                LZB_LAUNCH(k3_restrict, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));  // fl_{l-1} = P^T r_l
+                LZB_CUDA(cudaMemsetAsync(L3_[l - 1].v[LZB_V_U].p, 0, L3_[l - 1].v[LZB_V_U].bytes(), s_));
+            }
+            for (int l = 1; l <= D_; ++l) {
+                // u_l += P u_{l-1}: the additive cycle's prolongation with a zero snapshot
+                LZB_CUDA(cudaMemsetAsync(L3_[l - 1].v[LZB_V_USNAP].p, 0, L3_[l - 1].v[LZB_V_USNAP].bytes(), s_));
+                LZB_LAUNCH(k3_prolong, vg(l), 128, 0, s_, lv(l), lv(l - 1));
+                smooth(l, nu);
+            }
+            const uint64_t Nf = static_cast<uint64_t>(L3_[D_].N);
+            rep.dof_updates = static_cast<uint64_t>(2 * nu) * (Nf - 1) * (Nf - 1) * (Nf - 1);
+        }
+        rep.levels = D_ + 1;
+        rep.cells = static_cast<uint64_t>(nc_);
+        sync();
+        return rep;
+    }
+
     lzb_cycle_report step() {
         if (L3_.empty()) throw Error(LZB_ERR_INVALID, "call init_cycle first");
         if (ops_dirty_) {
@@ -1724,6 +1791,9 @@ int lzb_grid3_init_cycle(lzb_grid3* g, int variant, double omega, double rhs_sca
 }
 int lzb_grid3_step(lzb_grid3* g, lzb_cycle_report* out) {
     return lzb::guarded([&] { *out = g->g->step(); });
+}
+int lzb_grid3_vcycle(lzb_grid3* g, int nu, lzb_cycle_report* out) {
+    return lzb::guarded([&] { *out = g->g->vcycle(nu); });
 }
 int lzb_grid3_vertices(lzb_grid3* g, int level, int field, double* out) {
     return lzb::guarded([&] { g->g->vertices(level, field, out); });
