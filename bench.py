@@ -329,6 +329,33 @@ def run_ours(args, world, rank, local):
                           "restriction + Jacobi + prolongation + injection + stats)",
                 "value": world * dof * cycles / tc, "ms_per_cycle": 1e3 * tc / cycles, "cycles": cycles,
                 "launches_per_cycle": cyc_launches / cycles, "dof_per_cycle": dof}
+    # BASELINE configs[1] names V(1,1) cycles: the multiplicative cycle on the same grid
+    gv = make(head)
+    gv.assemble_fixed(P)
+    for _ in range(2):
+        gv.vcycle(1)
+    repv2 = []
+    tv2 = max_over_ranks(timed_steps(lambda: repv2.append(gv.vcycle(1)), cycles), world)
+    smoother["vcycles"] = {"what": "V(1,1), damped Jacobi omega 0.6, Galerkin coarse operators (lzb_grid_vcycle)",
+                           "ms_per_cycle": 1e3 * tv2 / cycles, "cycles": cycles,
+                           "fine_dof_updates_per_s": world * 2 * dof * cycles / tv2,
+                           "rate_per_cycle": (repv2[-1]["residual"] / repv2[0]["residual"]) ** (1 / (cycles - 1))}
+    gv.close()
+    del gv
+    try:  # BASELINE configs[0] (C1): 243^2 checkerboard, eager assembly at p = 16, 20 V(1,1) cycles
+        g1 = lzb.Grid(lzb.make_desc(depth=5, field=lzb.checkerboard(1, 8), solver="additive", omega=0.6,
+                                    rhs_kind="sinprod", max_cycles=10 ** 6), 42, ctx)
+        g1.assemble_fixed(16)
+        g1.vcycle(1)
+        t1a = timed_steps(lambda: g1.assemble_fixed(16), 3) / 3
+        rep1 = []
+        t1 = timed_steps(lambda: rep1.append(g1.vcycle(1)), 20)
+        smoother["c1"] = {"grid": "243^2 (depth 5), 8x8 checkerboard 10^U(-2,2)", "assembly_p": 16,
+                          "assembly_ms": 1e3 * t1a, "vcycles": 20, "vcycle_ms": 1e3 * t1 / 20,
+                          "normalized_after": rep1[-1]["residual"] / rep1[0]["residual"]}
+        g1.close()
+    except Exception as e:  # noqa: BLE001
+        smoother["c1"] = {"error": repr(e)}
 
     # HBM-bound regime: the 729^2 working set (~150 MB) is largely L2-resident
     # (SURVEY.md §8d), so the smoother and stream-pack rooflines are measured on

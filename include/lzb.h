@@ -120,6 +120,10 @@ int lzb_grid_invalidate(lzb_grid* g);
 /* AdditiveSolver::step / run_cycles                             solver.hpp:78-79 */
 int lzb_grid_step(lzb_grid* g, lzb_cycle_report* out);
 int lzb_grid_run(lzb_grid* g, lzb_cycle_report* out, int cap, int* count);
+/* One multiplicative V(nu, nu) cycle with damped Jacobi (omega of the desc)
+ * on the same levels, operators and transfers (BASELINE configs[1] names
+ * V(1,1); restated extension, the reference's cycle is additive only). */
+int lzb_grid_vcycle(lzb_grid* g, int nu, lzb_cycle_report* out);
 /* Individual passes (solver.hpp:91-98): 0 assembly, 1 residual (value = norm),
  * 2 update, 3 prolong, 4 finish_cycle_sync, 5 stream begin_cycle, 6 pool begin_cycle,
  * 7 drain every pending assembly task (TaskPool::drain_all, scheduler.hpp:59). */

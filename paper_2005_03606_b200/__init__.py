@@ -101,6 +101,7 @@ def lib():
         L.lzb_grid_eager_setup.argtypes = [vp]
         L.lzb_grid_assemble_fixed.argtypes = [vp, C.c_int]
         L.lzb_grid_step.argtypes = [vp, C.POINTER(CycleReport)]
+        L.lzb_grid_vcycle.argtypes = [vp, C.c_int, C.POINTER(CycleReport)]
         L.lzb_grid_run.argtypes = [vp, vp, C.c_int, C.POINTER(C.c_int)]
         L.lzb_grid_pass.argtypes = [vp, C.c_int, C.POINTER(dbl)]
         L.lzb_grid_cycle.argtypes = [vp]
@@ -432,6 +433,12 @@ class Grid:
     def step(self) -> dict:
         r = CycleReport()
         _check(lib().lzb_grid_step(self.h, C.byref(r)))
+        return report_dict(r)
+
+    def vcycle(self, nu=1) -> dict:
+        """One multiplicative V(nu, nu) cycle (lzb_grid_vcycle)."""
+        r = CycleReport()
+        _check(lib().lzb_grid_vcycle(self.h, nu, C.byref(r)))
         return report_dict(r)
 
     def run(self, cap=100000):

@@ -2928,6 +2928,79 @@ public:
         return rep;
     }
 
+    // A multiplicative V(nu, nu) cycle on the same levels (BASELINE configs[1]
+    // names V(1,1); the reference has only the additive cycle, so this is a
+    // restated extension, oracle/port2v.py): the coarse operators are brought
+    // up to date as in step() (coarse pass / ripple walk; no leaf assembly
+    // tasks), then per level from the leaves nu damped-Jacobi sweeps (omega),
+    // the residual restricted into the next level's rhs (k_restrict mode 0,
+    // the owned-lattice P^T of the additive cycle) with a zero start; at the
+    // bottom back up, u_l += P u_{l-1} (k_prolong against a zero snapshot)
+    // and nu sweeps. The report's residual is the leaf residual before the cycle.
+    lzb_cycle_report vcycle(int nu) {
+        if (nu < 0) throw Error(LZB_ERR_INVALID, "nu must be >= 0");
+        if (d_.concurrent) throw Error(LZB_ERR_INVALID, "vcycle is not available with concurrent assembly");
+        auto t0 = std::chrono::steady_clock::now();
+        lzb_cycle_report rep;
+        std::memset(&rep, 0, sizeof rep);
+        ++cycle_;
+        *hcycle_ = cycle_;
+        rep.cycle = static_cast<int32_t>(cycle_);
+        if (ripple()) ripple_walk();
+        else run_graph(g_coarse_, &Grid::coarse_pass);
+        ensure_rhs();
+        auto residual = [&](int l) {  // r, r-hat (u-hat = u) and the diagonal of level l
+            LZB_LAUNCH(k_uhat, vgrid(l), kThreads, 0, s_, V(l), V(l), 0);
+            if (l == D_) leaf_residual(0, L_[D_].N + 1);
+            else LZB_LAUNCH(k_residual, vgrid(l), kThreads, 0, s_, V(l), d_.field);
+        };
+        auto smooth = [&](int l, int k) {
+            for (int i = 0; i < k; ++i) {
+                residual(l);
+                LZB_LAUNCH(k_jacobi, vgrid(l), kThreads, 0, s_, V(l), d_.omega);
+            }
+        };
+        residual(D_);
+        LZB_LAUNCH(k_norm_partial, kNormBlocks, kThreads, 0, s_, V(D_), 0, L_[D_].N + 1, partial_.p);
+        LZB_LAUNCH(k_norm_final, 1, kNormFinalThreads, 0, s_, partial_.p, kNormBlocks, res_.p);
+        fetch_result();
+        rep.residual = hres_->norm;
+        if (first_residual_ < 0.0) first_residual_ = rep.residual > 0.0 ? rep.residual : 1.0;
+        rep.normalized = rep.residual / first_residual_;
+        history_.push_back(rep.residual);
+        rep.status = check_termination();
+        if (rep.status == LZB_CONTINUE || rep.status == LZB_TIMEOUT) {
+            for (int l = D_; l >= 1; --l) {
+                smooth(l, nu);
+                residual(l);
+                LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1), 0, 0.0);  // fl = P^T r
+                LZB_CUDA(cudaMemsetAsync(L_[l - 1].v[LZB_V_U].p, 0, L_[l - 1].v[LZB_V_U].bytes(), s_));
+            }
+            for (int l = 1; l <= D_; ++l) {
+                LZB_CUDA(cudaMemsetAsync(L_[l - 1].v[LZB_V_USNAP].p, 0, L_[l - 1].v[LZB_V_USNAP].bytes(), s_));
+                LZB_LAUNCH(k_prolong, vgrid(l), kThreads, 0, s_, V(l), V(l - 1));
+                smooth(l, nu);
+            }
+            const uint64_t Nf = static_cast<uint64_t>(L_[D_].N);
+            rep.dof_updates = static_cast<uint64_t>(2 * nu) * (Nf - 1) * (Nf - 1);
+            for (int l = 0; l < D_; ++l) {
+                const uint64_t N = static_cast<uint64_t>(L_[l].N);
+                rep.coarse_updates += N > 1 ? static_cast<uint64_t>(2 * nu) * (N - 1) * (N - 1) : 0;
+            }
+        }
+        dof_total_ += rep.dof_updates;
+        rep.dof_updates_total = dof_total_;
+        rep.levels = D_ + 1;
+        rep.cells = static_cast<uint64_t>(total_cells_);
+        for (int l = 0; l <= D_ && l < 32; ++l) rep.enabled_mask |= 1u << l;
+        const uint64_t Nf = static_cast<uint64_t>(L_[D_].N);
+        rep.dofs_fine_interior = (Nf - 1) * (Nf - 1);
+        rep.grid_points_total = static_cast<uint64_t>(total_vertices_);
+        sync_check();
+        rep.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return rep;
+    }
+
     // step() bookkeeping after the residual pass (solver.cpp:359-370): history,
     // normalisation, termination; true when the update passes run.
     bool front_report(lzb_cycle_report& rep, const Result& r) {
@@ -3646,6 +3719,9 @@ int lzb_grid_assemble_fixed(lzb_grid* g, int n) {
     });
 }
 int lzb_grid_step(lzb_grid* g, lzb_cycle_report* out) { return guarded([&] { *out = g->g->step(); }); }
+int lzb_grid_vcycle(lzb_grid* g, int nu, lzb_cycle_report* out) {
+    return guarded([&] { *out = g->g->vcycle(nu); });
+}
 int lzb_grid_run(lzb_grid* g, lzb_cycle_report* out, int cap, int* count) {
     return guarded([&] {
         auto reps = g->g->run();
