@@ -2363,7 +2363,7 @@ public:
         if (hhist_) cudaFreeHost(hhist_);
         if (hcycle_) cudaFreeHost(hcycle_);
         if (herr_) cudaFreeHost(herr_);
-        for (cudaGraphExec_t* e : {&g_coarse_, &g_front_, &g_back_})
+        for (cudaGraphExec_t* e : {&g_coarse_, &g_front_, &g_back_, &g_vcoarse_})
             if (*e) cudaGraphExecDestroy(*e);
         if (st_ready_) {
             cudaStreamSynchronize(cp_);
@@ -2562,10 +2562,14 @@ public:
         }
     }
 
-    void coarse_pass() {  // pre-order semantics: coarse levels first, each reads l+1
+    // pre-order semantics: coarse levels first, each reads l+1 (post_order:
+    // finest first, each level reads the l+1 written in the same pass -- the
+    // V-cycle's consistent Galerkin hierarchy)
+    void coarse_pass_order(bool post_order) {
         // the epoch comes from pinned host memory at execution time (graph-replayable)
         LZB_CUDA(cudaMemcpyAsync(dcycle_.p, hcycle_, sizeof(uint32_t), cudaMemcpyHostToDevice, s_));
-        for (int l = 0; l < D_; ++l) {
+        for (int i = 0; i < D_; ++i) {
+            const int l = post_order ? D_ - 1 - i : i;
             if (d_.transfer == LZB_BOXMG)
                 LZB_LAUNCH(k_coarse, blocks_for(L_[l].nc, 64), 64, 0, s_, V(l), V(l + 1), d_.field, 1,
                            d_.delta_max, dcycle_.p, res_.p->s, ctx_->err.p);
@@ -2574,6 +2578,8 @@ public:
                            V(l), V(l + 1), d_.field, d_.delta_max, dcycle_.p, res_.p->s, ctx_->err.p);
         }
     }
+    void coarse_pass() { coarse_pass_order(false); }
+    void coarse_pass_post() { coarse_pass_order(true); }
 
     // ------------------------------------------------------------ CUDA graphs
     // The fixed part of a cycle is replayed as two graphs: (coarse recompute +
@@ -2591,7 +2597,7 @@ public:
             (this->*body)();
             return;
         }
-        const int slot = &exec == &g_coarse_ ? 0 : (&exec == &g_front_ ? 1 : 2);
+        const int slot = &exec == &g_coarse_ ? 0 : &exec == &g_front_ ? 1 : &exec == &g_back_ ? 2 : 3;
         if (!exec) {
             cudaGraph_t g = nullptr;
             const uint64_t l0 = g_launches.load();
@@ -2931,7 +2937,10 @@ public:
     // A multiplicative V(nu, nu) cycle on the same levels (BASELINE configs[1]
     // names V(1,1); the reference has only the additive cycle, so this is a
     // restated extension, oracle/port2v.py): the coarse operators are brought
-    // up to date as in step() (coarse pass / ripple walk; no leaf assembly
+    // up to date (the coarse pass finest level first, so every level is the
+    // Galerkin product of the current level below it -- the additive cycle's
+    // pre-order pass lags one level per cycle, which a multiplicative cycle
+    // does not tolerate; ripple mode: the ripple walk; no leaf assembly
     // tasks), then per level from the leaves nu damped-Jacobi sweeps (omega),
     // the residual restricted into the next level's rhs (k_restrict mode 0,
     // the owned-lattice P^T of the additive cycle) with a zero start; at the
@@ -2947,7 +2956,7 @@ public:
         *hcycle_ = cycle_;
         rep.cycle = static_cast<int32_t>(cycle_);
         if (ripple()) ripple_walk();
-        else run_graph(g_coarse_, &Grid::coarse_pass);
+        else run_graph(g_vcoarse_, &Grid::coarse_pass_post);
         ensure_rhs();
         auto residual = [&](int l) {  // r, r-hat (u-hat = u) and the diagonal of level l
             LZB_LAUNCH(k_uhat, vgrid(l), kThreads, 0, s_, V(l), V(l), 0);
@@ -3655,8 +3664,8 @@ private:
     DevBuf<double> caux_;         // scaled aux of level D-1 (k_update_fine)
     bool rhs_ready_ = false;      // leaf-level lumped load in place
     bool all_top_ = false;        // every leaf converged (no request_stencil work left)
-    cudaGraphExec_t g_coarse_ = nullptr, g_front_ = nullptr, g_back_ = nullptr;
-    uint64_t graph_kernels_[3] = {0, 0, 0};
+    cudaGraphExec_t g_coarse_ = nullptr, g_front_ = nullptr, g_back_ = nullptr, g_vcoarse_ = nullptr;
+    uint64_t graph_kernels_[4] = {0, 0, 0, 0};
     double first_residual_ = -1.0;
     int slab_v0_ = 0, slab_v1_ = -1;  // leaf vertex rows of this rank's slab (-1: the whole level)
     std::chrono::steady_clock::time_point dist_t0_{};
