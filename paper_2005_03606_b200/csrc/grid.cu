@@ -2363,7 +2363,7 @@ public:
         if (hhist_) cudaFreeHost(hhist_);
         if (hcycle_) cudaFreeHost(hcycle_);
         if (herr_) cudaFreeHost(herr_);
-        for (cudaGraphExec_t* e : {&g_coarse_, &g_front_, &g_back_, &g_vcoarse_})
+        for (cudaGraphExec_t* e : {&g_coarse_, &g_front_, &g_back_, &g_vfront_, &g_vback_})
             if (*e) cudaGraphExecDestroy(*e);
         if (st_ready_) {
             cudaStreamSynchronize(cp_);
@@ -2386,6 +2386,7 @@ public:
             v.fixed_p3 = d_.fixed_p3;
         }
         if (l > 0) v.pdirty = L_[l - 1].dirty.p;  // nullptr unless ripple
+        if (uhat_is_u_) v.v[LZB_V_UHAT] = v.v[LZB_V_U];  // V-cycle: u-hat = u without a copy
         return v;
     }
     // 2D launch geometry of the vertex kernels: x = column blocks, y = rows
@@ -2597,7 +2598,7 @@ public:
             (this->*body)();
             return;
         }
-        const int slot = &exec == &g_coarse_ ? 0 : &exec == &g_front_ ? 1 : &exec == &g_back_ ? 2 : 3;
+        const int slot = &exec == &g_coarse_ ? 0 : &exec == &g_front_ ? 1 : &exec == &g_back_ ? 2 : &exec == &g_vfront_ ? 3 : 4;
         if (!exec) {
             cudaGraph_t g = nullptr;
             const uint64_t l0 = g_launches.load();
@@ -2956,40 +2957,21 @@ public:
         *hcycle_ = cycle_;
         rep.cycle = static_cast<int32_t>(cycle_);
         if (ripple()) ripple_walk();
-        else run_graph(g_vcoarse_, &Grid::coarse_pass_post);
         ensure_rhs();
-        auto residual = [&](int l) {  // r, r-hat (u-hat = u) and the diagonal of level l
-            LZB_LAUNCH(k_uhat, vgrid(l), kThreads, 0, s_, V(l), V(l), 0);
-            if (l == D_) leaf_residual(0, L_[D_].N + 1);
-            else LZB_LAUNCH(k_residual, vgrid(l), kThreads, 0, s_, V(l), d_.field);
-        };
-        auto smooth = [&](int l, int k) {
-            for (int i = 0; i < k; ++i) {
-                residual(l);
-                LZB_LAUNCH(k_jacobi, vgrid(l), kThreads, 0, s_, V(l), d_.omega);
-            }
-        };
-        residual(D_);
-        LZB_LAUNCH(k_norm_partial, kNormBlocks, kThreads, 0, s_, V(D_), 0, L_[D_].N + 1, partial_.p);
-        LZB_LAUNCH(k_norm_final, 1, kNormFinalThreads, 0, s_, partial_.p, kNormBlocks, res_.p);
-        fetch_result();
+        run_graph(g_vfront_, &Grid::vfront_body);  // (coarse pass) + leaf residual + norm -> host
+        LZB_CUDA(cudaStreamSynchronize(s_));
         rep.residual = hres_->norm;
         if (first_residual_ < 0.0) first_residual_ = rep.residual > 0.0 ? rep.residual : 1.0;
         rep.normalized = rep.residual / first_residual_;
         history_.push_back(rep.residual);
         rep.status = check_termination();
         if (rep.status == LZB_CONTINUE || rep.status == LZB_TIMEOUT) {
-            for (int l = D_; l >= 1; --l) {
-                smooth(l, nu);
-                residual(l);
-                LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1), 0, 0.0);  // fl = P^T r
-                LZB_CUDA(cudaMemsetAsync(L_[l - 1].v[LZB_V_U].p, 0, L_[l - 1].v[LZB_V_U].bytes(), s_));
+            if (nu != vnu_ && g_vback_) {  // the sweep counts are baked into the graph
+                LZB_CUDA(cudaGraphExecDestroy(g_vback_));
+                g_vback_ = nullptr;
             }
-            for (int l = 1; l <= D_; ++l) {
-                LZB_CUDA(cudaMemsetAsync(L_[l - 1].v[LZB_V_USNAP].p, 0, L_[l - 1].v[LZB_V_USNAP].bytes(), s_));
-                LZB_LAUNCH(k_prolong, vgrid(l), kThreads, 0, s_, V(l), V(l - 1));
-                smooth(l, nu);
-            }
+            vnu_ = nu;
+            run_graph(g_vback_, &Grid::vback_body);
             const uint64_t Nf = static_cast<uint64_t>(L_[D_].N);
             rep.dof_updates = static_cast<uint64_t>(2 * nu) * (Nf - 1) * (Nf - 1);
             for (int l = 0; l < D_; ++l) {
@@ -3008,6 +2990,46 @@ public:
         sync_check();
         rep.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         return rep;
+    }
+    // r, r-hat (= r: the views alias u-hat to u) and the diagonal of level l
+    void vresidual(int l) {
+        if (l == D_) leaf_residual(0, L_[D_].N + 1);
+        else LZB_LAUNCH(k_residual, vgrid(l), kThreads, 0, s_, V(l), d_.field);
+    }
+    void vsmooth(int l, int k) {
+        for (int i = 0; i < k; ++i) {
+            vresidual(l);
+            LZB_LAUNCH(k_jacobi, vgrid(l), kThreads, 0, s_, V(l), d_.omega);
+        }
+    }
+    void vfront_body() {
+        if (!ripple()) coarse_pass_post();
+        {
+            UhatAlias alias(uhat_is_u_);
+            vresidual(D_);
+        }
+        LZB_LAUNCH(k_norm_partial, kNormBlocks, kThreads, 0, s_, V(D_), 0, L_[D_].N + 1, partial_.p);
+        LZB_LAUNCH(k_norm_final, 1, kNormFinalThreads, 0, s_, partial_.p, kNormBlocks, res_.p);
+        LZB_CUDA(cudaMemcpyAsync(hres_, res_.p, sizeof(Result), cudaMemcpyDeviceToHost, s_));
+    }
+    struct UhatAlias {  // scoped: V(l) views alias u-hat to u
+        bool& f;
+        explicit UhatAlias(bool& x) : f(x) { f = true; }
+        ~UhatAlias() { f = false; }
+    };
+    void vback_body() {
+        UhatAlias alias(uhat_is_u_);
+        for (int l = D_; l >= 1; --l) {
+            vsmooth(l, vnu_);
+            vresidual(l);
+            LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1), 0, 0.0);  // fl = P^T r
+            LZB_CUDA(cudaMemsetAsync(L_[l - 1].v[LZB_V_U].p, 0, L_[l - 1].v[LZB_V_U].bytes(), s_));
+        }
+        for (int l = 1; l <= D_; ++l) {
+            LZB_CUDA(cudaMemsetAsync(L_[l - 1].v[LZB_V_USNAP].p, 0, L_[l - 1].v[LZB_V_USNAP].bytes(), s_));
+            LZB_LAUNCH(k_prolong, vgrid(l), kThreads, 0, s_, V(l), V(l - 1));
+            vsmooth(l, vnu_);
+        }
     }
 
     // step() bookkeeping after the residual pass (solver.cpp:359-370): history,
@@ -3664,8 +3686,11 @@ private:
     DevBuf<double> caux_;         // scaled aux of level D-1 (k_update_fine)
     bool rhs_ready_ = false;      // leaf-level lumped load in place
     bool all_top_ = false;        // every leaf converged (no request_stencil work left)
-    cudaGraphExec_t g_coarse_ = nullptr, g_front_ = nullptr, g_back_ = nullptr, g_vcoarse_ = nullptr;
-    uint64_t graph_kernels_[4] = {0, 0, 0, 0};
+    cudaGraphExec_t g_coarse_ = nullptr, g_front_ = nullptr, g_back_ = nullptr;
+    cudaGraphExec_t g_vfront_ = nullptr, g_vback_ = nullptr;  // V-cycle: front, sweeps (for vnu_)
+    int vnu_ = -1;
+    bool uhat_is_u_ = false;
+    uint64_t graph_kernels_[5] = {0, 0, 0, 0, 0};
     double first_residual_ = -1.0;
     int slab_v0_ = 0, slab_v1_ = -1;  // leaf vertex rows of this rank's slab (-1: the whole level)
     std::chrono::steady_clock::time_point dist_t0_{};

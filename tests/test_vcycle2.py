@@ -95,3 +95,34 @@ def test_vcycle_rejects_bad_nu():
     G = lzb.Grid(lzb.make_desc(depth=2, solver="additive"), 1)
     with pytest.raises(Exception):
         G.vcycle(-1)
+
+
+@pytest.mark.gpu
+def test_vcycle_sweep_count_change_and_compressed_leaves():
+    """Changing nu between cycles re-captures the sweep graph (the restatement
+    follows the same nu sequence); the compressed leaf records (plane_width)
+    give the FP64 residual history bit for bit."""
+    def grid(width):
+        d = lzb.make_desc(depth=4, field=lzb.field_theta(16.0), solver="additive", omega=0.6,
+                          rhs_kind="sinprod", max_cycles=100, plane_width=width)
+        G = lzb.Grid(d, 42)
+        G.assemble_fixed(3)
+        return G
+
+    seq = [1, 2, 1, 3, 1]
+    G = grid(0)
+    u0 = G.vertices(4, lzb.T.V_U).copy()
+    a = [G.vcycle(seq[0])]
+    fl = G.vertices(4, lzb.T.V_FL)
+    ops = [G.cells(l)["ops"] for l in range(5)]
+    P = [np.array([[G.transfer(l, cx, cy) for cx in range(3 ** l)] for cy in range(3 ** l)]) for l in range(4)]
+    ref = VCycle2(ops, P, fl, u0, omega=0.6, max_cycles=100)
+    b = [ref.vstep(seq[0])]
+    for nu in seq[1:]:
+        a.append(G.vcycle(nu))
+        b.append(ref.vstep(nu))
+    for x, y in zip(a, b):
+        assert x["residual"] == pytest.approx(y["residual"], rel=1e-10)
+    H = grid(4)
+    c = [H.vcycle(nu) for nu in seq]
+    assert [x["residual"] for x in a] == [x["residual"] for x in c]
