@@ -1342,10 +1342,12 @@ public:
         lzb_cycle_report rep;
         std::memset(&rep, 0, sizeof rep);
         rep.cycle = static_cast<int32_t>(++cycle_);
-        auto residual_plain = [&](int l) {  // r (and r-hat = r) of level l from its fl
-            LZB_LAUNCH(k3_uhat, vg(l), 128, 0, s_, lv(l), lv(l), 0);
-            residual3(l, 0, L3_[l].N + 1);
-        };
+        struct Alias {  // the level views alias u-hat to u for this cycle
+            bool& f;
+            explicit Alias(bool& x) : f(x) { f = true; }
+            ~Alias() { f = false; }
+        } alias(uhat_is_u_);
+        auto residual_plain = [&](int l) { residual3(l, 0, L3_[l].N + 1); };  // r (and r-hat = r) from fl
         auto smooth = [&](int l, int k) {
             for (int i = 0; i < k; ++i) {
                 residual_plain(l);
@@ -1667,6 +1669,7 @@ private:
         v.h = L3_[l].h;
         for (int f = 0; f < LZB_V_NFIELDS; ++f) v.v[f] = L3_[l].v[f].p;
         v.op = l == D_ ? op_.p : L3_[l].op.p;
+        if (uhat_is_u_) v.v[LZB_V_UHAT] = v.v[LZB_V_U];  // V-cycle: u-hat = u without a copy
         return v;
     }
     Planes3 planes() const {
@@ -1707,6 +1710,7 @@ private:
         }
         leaf_cls([&](auto S) { LZB_LAUNCH(k3_residual_z<decltype(S)>, grid, kRzX * kRzY, 0, s_, v, S, z0, z1); });
     }
+    bool uhat_is_u_ = false;
     double damping3(int l) const { return variant_ == LZB_ADDITIVE ? std::pow(omega_, D_ - l + 1) : omega_; }
     dim3 vg(int l) const { return dim3(blocks_for(L3_[l].N + 1, 128), L3_[l].N + 1, L3_[l].N + 1); }
     void inject3() {
