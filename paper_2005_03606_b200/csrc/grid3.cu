@@ -669,14 +669,14 @@ __global__ void k3_uhat(Lv3 F, Lv3 C, int has_coarse) {
 // 2 dy + 4 dz: the 4 cells below a vertex plane while the previous layer is
 // staged, the 4 above in this layer) — the per-vertex gather's order. The
 // u / û corners of the layer below stay in registers.
-constexpr int kRzX = 32, kRzY = 8, kRzChunk = 32;
+constexpr int kRzX = 32, kRzY = 8, kRzChunk = 32;  // chunk: vertex planes per block (at most)
 template <class Src>
-__global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_z(Lv3 F, Src S, int zbeg, int zend) {
+__global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_z(Lv3 F, Src S, int zbeg, int zend, int zc) {
     __shared__ double sy[3][8][kRzX * kRzY];  // [u, û, diag][corner][cell of the tile]
     const int tx = threadIdx.x % kRzX, ty = threadIdx.x / kRzX, t = threadIdx.x;
     const int N = F.N, NV = N + 1;
     const int X0 = blockIdx.x * (kRzX - 1), Y0 = blockIdx.y * (kRzY - 1);
-    const int zs = zbeg + blockIdx.z * kRzChunk, ze = min(zs + kRzChunk, zend);
+    const int zs = zbeg + blockIdx.z * zc, ze = min(zs + zc, zend);
     if (zs >= ze) return;
     const int cx = X0 - 1 + tx, cy = Y0 - 1 + ty;  // this thread's cell column
     const bool colok = cx >= 0 && cy >= 0 && cx < N && cy < N;
@@ -1700,15 +1700,21 @@ private:
     // read this grid's leaf source): the cell-centric z-marching form
     void residual3(int l, int z0, int z1) {
         const int N = L3_[l].N;
-        const dim3 grid((N + kRzX - 1) / (kRzX - 1), (N + kRzY - 1) / (kRzY - 1),
-                        (z1 - z0 + kRzChunk - 1) / kRzChunk);
+        // planes per block: kRzChunk, halved (down to 2) while the grid is under
+        // four waves of the 2 resident blocks per SM -- the coarse levels are
+        // latency-bound marches otherwise (81^3: 108 blocks of 32 planes)
+        const int bx = (N + kRzX - 1) / (kRzX - 1), by = (N + kRzY - 1) / (kRzY - 1);
+        int zc = kRzChunk;
+        while (zc > 2 && static_cast<int64_t>(bx) * by * ((z1 - z0 + zc - 1) / zc) < 4 * 2 * 148)
+            zc /= 2;
+        const dim3 grid(bx, by, (z1 - z0 + zc - 1) / zc);
         const Lv3 v = lv(l);
         if (l < D_ || W_ == 0) {
             const Src64 S{l < D_ ? L3_[l].op.p : op_.p, static_cast<int64_t>(N) * N * N};
-            LZB_LAUNCH(k3_residual_z<Src64>, grid, kRzX * kRzY, 0, s_, v, S, z0, z1);
+            LZB_LAUNCH(k3_residual_z<Src64>, grid, kRzX * kRzY, 0, s_, v, S, z0, z1, zc);
             return;
         }
-        leaf_cls([&](auto S) { LZB_LAUNCH(k3_residual_z<decltype(S)>, grid, kRzX * kRzY, 0, s_, v, S, z0, z1); });
+        leaf_cls([&](auto S) { LZB_LAUNCH(k3_residual_z<decltype(S)>, grid, kRzX * kRzY, 0, s_, v, S, z0, z1, zc); });
     }
     bool uhat_is_u_ = false;
     double damping3(int l) const { return variant_ == LZB_ADDITIVE ? std::pow(omega_, D_ - l + 1) : omega_; }
