@@ -812,10 +812,20 @@ __global__ void k_init_rhs(LevelView F, lzb_rhs rhs, double w) {
     F.v[LZB_V_FL][vi] = fl;
 }
 
-// compute_uhat (solver.cpp:120-143).
+// compute_uhat (solver.cpp:120-143): P u_c at fine vertex (fx, fy).
+__device__ __forceinline__ double uhat_interp(const LevelView& C, int fx, int fy) {
+    int px, py;
+    owner_patch(C, fx, fy, px, py);
+    const double* P = transfer_of(C, py * C.N + px);
+    int L = (fy - 3 * py) * 4 + (fx - 3 * px);
+    double interp = 0.0;
+    for (int k = 0; k < 4; ++k)
+        interp += P[L * 4 + k] * C.v[LZB_V_U][(py + cdy(k)) * (C.N + 1) + px + cdx(k)];
+    return interp;
+}
 template <bool LIN>
 __device__ __forceinline__ void k_uhat_body(int64_t lin, LevelView F, LevelView C, int has_coarse) {
-    int fx, fy, px, py;
+    int fx, fy;
     int64_t vi;
     if (!vertex_at<LIN>(lin, F, fx, fy, vi)) return;
     double u = F.v[LZB_V_U][vi];
@@ -823,17 +833,25 @@ __device__ __forceinline__ void k_uhat_body(int64_t lin, LevelView F, LevelView 
         F.v[LZB_V_UHAT][vi] = u;
         return;
     }
-    owner_patch(C, fx, fy, px, py);
-    const double* P = transfer_of(C, py * C.N + px);
-    int L = (fy - 3 * py) * 4 + (fx - 3 * px);
-    double interp = 0.0;
-    for (int k = 0; k < 4; ++k)
-        interp += P[L * 4 + k] * C.v[LZB_V_U][(py + cdy(k)) * (C.N + 1) + px + cdx(k)];
-    F.v[LZB_V_UHAT][vi] = u - interp;
+    F.v[LZB_V_UHAT][vi] = u - uhat_interp(C, fx, fy);
 }
+// The grid kernel takes two adjacent vertices per thread: N = 3^l is odd, so
+// a row holds an even number of vertices, (2t, 2t+1) never straddles a row
+// and is 16-byte aligned (the planes are cudaMalloc'd), so u is read and u-hat
+// written as one 128-bit access each. Per vertex the arithmetic is the body's.
 __global__ void k_uhat(LevelView F, LevelView C, int has_coarse) {
     lzb_pdl_enter();
-    k_uhat_body<false>(0, F, C, has_coarse);
+    const int fx = 2 * static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x);
+    const int fy = blockIdx.y + F.row0;
+    if (fx > F.N) return;
+    const int64_t vi = static_cast<int64_t>(fy) * (F.N + 1) + fx;
+    const double2 u = *reinterpret_cast<const double2*>(F.v[LZB_V_U] + vi);
+    double2 out = u;
+    if (has_coarse) {
+        out.x = u.x - uhat_interp(C, fx, fy);
+        out.y = u.y - uhat_interp(C, fx + 1, fy);
+    }
+    *reinterpret_cast<double2*>(F.v[LZB_V_UHAT] + vi) = out;
 }
 
 // residual_pass cell mat-vec, as a gather (solver.cpp:149-175).
@@ -2391,6 +2409,9 @@ public:
     }
     // 2D launch geometry of the vertex kernels: x = column blocks, y = rows
     dim3 vgrid(int l) const { return dim3(blocks_for(L_[l].N + 1, kThreads), L_[l].N + 1); }
+    // k_uhat: one thread per vertex pair of a row
+    dim3 ugrid(int l) const { return dim3(blocks_for((L_[l].N + 1) / 2, kThreads), L_[l].N + 1); }
+    dim3 ugrid_rows(int l, int r0, int r1) const { return dim3(blocks_for((L_[l].N + 1) / 2, kThreads), r1 - r0); }
     const lzb_grid_desc& desc() const { return d_; }
     int depth() const { return D_; }
     uint32_t cycle() const { return cycle_; }
@@ -2760,7 +2781,7 @@ public:
         const int lc = small_lc();
         for (int l = D_; l > lc; --l) {
             const dim3 g = vgrid(l);
-            LZB_LAUNCH(k_uhat, g, kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
+            LZB_LAUNCH(k_uhat, ugrid(l), kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
             if (l == D_) leaf_residual(0, L_[D_].N + 1);
             else LZB_LAUNCH(k_residual, g, kThreads, 0, s_, V(l), d_.field);
             if (l > 0)
@@ -3124,7 +3145,7 @@ public:
                 leaves_pass();
                 ensure_rhs();
                 const int u0 = std::max(v0 - 1, 0), u1 = std::min(v1 + 1, N + 1);
-                LZB_LAUNCH(k_uhat, vgrid_rows(D_, u0, u1), kThreads, 0, s_, Vrow(D_, u0), V(D_ - 1), 1);
+                LZB_LAUNCH(k_uhat, ugrid_rows(D_, u0, u1), kThreads, 0, s_, Vrow(D_, u0), V(D_ - 1), 1);
                 leaf_residual(v0, v1);
                 LZB_LAUNCH(k_reset_stats, 1, 32, 0, s_, res_.p);
                 const int cr1 = std::min(v1, N);
@@ -3146,7 +3167,7 @@ public:
             case 2:
                 for (int l = D_ - 1; l >= 0; --l) {
                     const dim3 g = vgrid(l);
-                    LZB_LAUNCH(k_uhat, g, kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
+                    LZB_LAUNCH(k_uhat, ugrid(l), kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
                     LZB_LAUNCH(k_residual, g, kThreads, 0, s_, V(l), d_.field);
                     if (l > 0) LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1), 0, 0.0);
                 }
@@ -3507,7 +3528,7 @@ public:
         auto launch = [&] {
             switch (what) {
                 case LZB_TK_UHAT:
-                    LZB_LAUNCH(k_uhat, vgrid(l), kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
+                    LZB_LAUNCH(k_uhat, ugrid(l), kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
                     break;
                 case LZB_TK_RESIDUAL: leaf_residual(0, L_[D_].N + 1); break;
                 case LZB_TK_RESTRICT:
