@@ -1346,9 +1346,42 @@ __device__ __forceinline__ void k_prolong_body(int64_t lin, LevelView F, LevelVi
     for (int k = 0; k < 4; ++k) p += P[L * 4 + k] * delta[k];
     F.v[LZB_V_U][vi] += p;
 }
+// P u_c - P u_c,snap at an interior fine vertex (the body's arithmetic).
+__device__ __forceinline__ bool prolong_delta(const LevelView& F, const LevelView& C, int fx, int fy, double& p) {
+    if (boundary(F.N, fx, fy)) return false;
+    int px, py;
+    owner_patch(C, fx, fy, px, py);
+    double delta[4];
+    bool any = false;
+    for (int k = 0; k < 4; ++k) {
+        int64_t ci = static_cast<int64_t>(py + cdy(k)) * (C.N + 1) + px + cdx(k);
+        delta[k] = C.v[LZB_V_U][ci] - C.v[LZB_V_USNAP][ci];
+        any |= delta[k] != 0.0;
+    }
+    if (!any) return false;
+    const double* P = transfer_of(C, py * C.N + px);
+    int L = (fy - 3 * py) * 4 + (fx - 3 * px);
+    p = 0.0;
+    for (int k = 0; k < 4; ++k) p += P[L * 4 + k] * delta[k];
+    return true;
+}
+// Vertex pairs per thread as in k_uhat. u is only written when a correction
+// applies, exactly where the body adds (its += stays even when p == 0).
 __global__ void k_prolong(LevelView F, LevelView C) {
     lzb_pdl_enter();
-    k_prolong_body<false>(0, F, C);
+    const int fx = 2 * static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x);
+    const int fy = blockIdx.y + F.row0;
+    if (fx > F.N) return;
+    const int64_t vi = static_cast<int64_t>(fy) * (F.N + 1) + fx;
+    double px = 0.0, py = 0.0;
+    const bool ax = prolong_delta(F, C, fx, fy, px), ay = prolong_delta(F, C, fx + 1, fy, py);
+    double2* up = reinterpret_cast<double2*>(F.v[LZB_V_U] + vi);
+    if (ax || ay) {
+        double2 u = *up;
+        if (ax) u.x += px;
+        if (ay) u.y += py;
+        *up = u;
+    }
 }
 // The leaf level's three updates of one cycle in one pass over u (u is
 // touched by nothing else in between): the adaFAC-PI aux correction
@@ -2650,7 +2683,7 @@ public:
     void back_body() {  // update + prolongation + injection
         update_launches(true, true);
         for (int l = std::max(small_lc(), 0) + 1; l <= D_ - 1; ++l)
-            LZB_LAUNCH(k_prolong, vgrid(l), kThreads, 0, s_, V(l), V(l - 1));
+            LZB_LAUNCH(k_prolong, ugrid(l), kThreads, 0, s_, V(l), V(l - 1));
         const bool pi = d_.variant == LZB_ADAFAC_PI;
         if (pi) LZB_LAUNCH(k_scale_aux, vgrid(D_ - 1), kThreads, 0, s_, V(D_ - 1), d_.omega, caux_.p);
         LZB_LAUNCH(k_update_fine, vgrid(D_), kThreads, 0, s_, V(D_), V(D_ - 1), pi ? caux_.p : nullptr,
@@ -2843,7 +2876,7 @@ public:
     void prolong_launches(int lmax = -1) {
         if (lmax < 0) lmax = D_;
         for (int l = 1; l <= lmax; ++l)
-            LZB_LAUNCH(k_prolong, vgrid(l), kThreads, 0, s_, V(l), V(l - 1));
+            LZB_LAUNCH(k_prolong, ugrid(l), kThreads, 0, s_, V(l), V(l - 1));
     }
 
     void inject() {
@@ -3048,7 +3081,7 @@ public:
         }
         for (int l = 1; l <= D_; ++l) {
             LZB_CUDA(cudaMemsetAsync(L_[l - 1].v[LZB_V_USNAP].p, 0, L_[l - 1].v[LZB_V_USNAP].bytes(), s_));
-            LZB_LAUNCH(k_prolong, vgrid(l), kThreads, 0, s_, V(l), V(l - 1));
+            LZB_LAUNCH(k_prolong, ugrid(l), kThreads, 0, s_, V(l), V(l - 1));
             vsmooth(l, vnu_);
         }
     }
@@ -3535,7 +3568,7 @@ public:
                     LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1), 0, 0.0);
                     break;
                 case LZB_TK_JACOBI: LZB_LAUNCH(k_jacobi, vgrid(l), kThreads, 0, s_, V(l), 0.0); break;
-                case LZB_TK_PROLONG: LZB_LAUNCH(k_prolong, vgrid(l), kThreads, 0, s_, V(l), V(l - 1)); break;
+                case LZB_TK_PROLONG: LZB_LAUNCH(k_prolong, ugrid(l), kThreads, 0, s_, V(l), V(l - 1)); break;
                 case LZB_TK_PACK:
                     pack_launches(img_.p);
                     break;
