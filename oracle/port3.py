@@ -425,6 +425,7 @@ def _cycle3_vstep(self, nu=2):
             inner = self._interior(self.N[l])
             V["u"] = np.where(inner, V["u"] + self._interp(l, self.v[l - 1]["u"]), V["u"])
             smooth(l, nu)
+        self._inject()  # coarse u held corrections: back to the additive invariant
     return {"cycle": self.cycle, "residual": res, "normalized": norm, "status": status}
 
 

@@ -133,6 +133,7 @@ struct DevBuf {
 
 struct lzb_ctx {
     int device = 0;
+    int sms = 148;  // multiprocessor count of `device` (cudaDevAttrMultiProcessorCount)
     cudaStream_t solve = nullptr;
     cudaStream_t assembly = nullptr;
     lzb::DevBuf<int> err;  // device error flag (non-finite encode etc.)

@@ -88,10 +88,6 @@ __device__ inline void element_or_baseline(const lzb_field& f, const LevelView& 
 __device__ inline void atomic_max_u64(unsigned long long* a, unsigned long long v) {
     if (v > *reinterpret_cast<volatile unsigned long long*>(a)) atomicMax(a, v);
 }
-__device__ __forceinline__ void lzb_pdl_enter() {  // see LZB_LAUNCH (engine.hpp)
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
 __device__ inline void atomic_max_double_bits(unsigned long long* a, double v) {  // v >= 0
     atomic_max_u64(a, static_cast<unsigned long long>(__double_as_longlong(v)));
 }
@@ -3084,6 +3080,10 @@ public:
             LZB_LAUNCH(k_prolong, ugrid(l), kThreads, 0, s_, V(l), V(l - 1));
             vsmooth(l, vnu_);
         }
+        // the coarse u held corrections: restore the additive cycle's invariant
+        // (coarse u = injected fine u, finish_cycle_sync solver.cpp:344-347) so a
+        // later step() forms u-hat = u - P u_c from the solution, not from them
+        inject();
     }
 
     // step() bookkeeping after the residual pass (solver.cpp:359-370): history,

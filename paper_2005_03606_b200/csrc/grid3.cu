@@ -253,6 +253,7 @@ __device__ __forceinline__ double entry3(const Acc3& A, double hn, int a, int b)
 
 __global__ void k_elements3(Field3 F, int64_t count, const double* x0, const double* y0, const double* z0,
                             const double* h, const int32_t* nn, AxisTab3 T, double* out) {
+    lzb_pdl_enter();
     const int64_t t = gtid();
     if (t >= count) return;
     if (nn[t] != T.n) return;  // batches are grouped by n on the host
@@ -482,6 +483,7 @@ __global__ void __launch_bounds__(128, 4) k_assemble3(Field3 F, int N, double h,
                                                       int8_t* __restrict__ p3o, int32_t* __restrict__ no,
                                                       unsigned long long* stats, int* err, int* wide,
                                                       int64_t cbeg, int64_t cend) {
+    lzb_pdl_enter();
     const int64_t c = cbeg + gtid();  // cells [cbeg, cend): whole z planes
     const int64_t nc = static_cast<int64_t>(N) * N * N;
     if (c >= cend) return;
@@ -530,6 +532,7 @@ __global__ void __launch_bounds__(128, 4) k_assemble3(Field3 F, int N, double h,
 // The 27 class values of cells [first, first + count) (AoS, 27 per cell).
 template <class Src>
 __global__ void k3_read_cls(Src S, int64_t first, int64_t count, double* __restrict__ out) {
+    lzb_pdl_enter();
     const int64_t t = gtid();
     if (t >= count) return;
     double v[27];
@@ -539,6 +542,7 @@ __global__ void k3_read_cls(Src S, int64_t first, int64_t count, double* __restr
 }
 
 __global__ void k_stats3(const int8_t* __restrict__ p3, int64_t nc, unsigned long long* s) {
+    lzb_pdl_enter();
     __shared__ unsigned long long sh[9];
     if (threadIdx.x < 9) sh[threadIdx.x] = 0;
     __syncthreads();
@@ -606,6 +610,7 @@ __device__ __forceinline__ int owner3(int f, int Nc) {
 // fl = sum over the adjacent leaves of f(v) h^3 / 8, f = scale prod sin(pi x_d)
 // (the lumped load of solver.cpp:99-118 in 3D; BASELINE f = 3 pi^2 prod sin)
 __global__ void k3_init_rhs(Lv3 F, double scale, double w) {
+    lzb_pdl_enter();
     int ix, iy, iz;
     int64_t vi;
     if (!vxyz(F, ix, iy, iz, vi)) return;
@@ -624,6 +629,7 @@ __global__ void k3_init_rhs(Lv3 F, double scale, double w) {
 }
 
 __global__ void k3_noise(Lv3 L, int level, uint64_t seed, double gval) {
+    lzb_pdl_enter();
     int ix, iy, iz;
     int64_t vi;
     if (!vxyz(L, ix, iy, iz, vi)) return;
@@ -643,6 +649,7 @@ __global__ void k3_noise(Lv3 L, int level, uint64_t seed, double gval) {
 }
 
 __global__ void k3_uhat(Lv3 F, Lv3 C, int has_coarse) {
+    lzb_pdl_enter();
     int fx, fy, fz;
     int64_t vi;
     if (!vxyz(F, fx, fy, fz, vi)) return;
@@ -672,6 +679,7 @@ __global__ void k3_uhat(Lv3 F, Lv3 C, int has_coarse) {
 constexpr int kRzX = 32, kRzY = 8, kRzChunk = 32;  // chunk: vertex planes per block (at most)
 template <class Src>
 __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_z(Lv3 F, Src S, int zbeg, int zend, int zc) {
+    lzb_pdl_enter();
     __shared__ double sy[3][8][kRzX * kRzY];  // [u, û, diag][corner][cell of the tile]
     const int tx = threadIdx.x % kRzX, ty = threadIdx.x / kRzX, t = threadIdx.x;
     const int N = F.N, NV = N + 1;
@@ -770,6 +778,7 @@ __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_z(Lv3 F, Src S, in
 // fl_c = P^T r̂ over owned lattice points (adjacent patches in (z, y, x)
 // order, lattice points in (z, y, x) order). mode 1: r into aux (unused).
 __global__ void k3_restrict(Lv3 F, Lv3 C) {
+    lzb_pdl_enter();
     int IX, IY, IZ;
     int64_t vi;
     if (!vxyz(C, IX, IY, IZ, vi)) return;
@@ -800,6 +809,7 @@ __global__ void k3_restrict(Lv3 F, Lv3 C) {
 // [max(zlo, 1), min(zhi, N)): block b takes rows b, b + G, ... four rows per
 // step (four independent loads in flight per thread), then a fixed-order tree.
 __global__ void k3_norm_partial(Lv3 F, double* partial, int zlo, int zhi) {
+    lzb_pdl_enter();
     __shared__ double sh[256];
     const int N = F.N;
     double s[4] = {0.0, 0.0, 0.0, 0.0};
@@ -832,6 +842,7 @@ __global__ void k3_norm_partial(Lv3 F, double* partial, int zlo, int zhi) {
 }
 
 __global__ void k3_snap(Lv3 L, int64_t nv) {
+    lzb_pdl_enter();
     const int64_t i = gtid();
     if (i >= nv) return;
     L.v[LZB_V_USNAP][i] = L.v[LZB_V_U][i];
@@ -839,6 +850,7 @@ __global__ void k3_snap(Lv3 L, int64_t nv) {
 }
 
 __global__ void k3_aux_inject(Lv3 F, Lv3 C) {
+    lzb_pdl_enter();
     int ix, iy, iz;
     int64_t vi;
     if (!vxyz(C, ix, iy, iz, vi)) return;
@@ -846,6 +858,7 @@ __global__ void k3_aux_inject(Lv3 F, Lv3 C) {
 }
 
 __global__ void k3_aux_sub(Lv3 F, Lv3 C, double omega) {
+    lzb_pdl_enter();
     int fx, fy, fz;
     int64_t vi;
     if (!vxyz(F, fx, fy, fz, vi)) return;
@@ -864,6 +877,7 @@ __global__ void k3_aux_sub(Lv3 F, Lv3 C, double omega) {
 }
 
 __global__ void k3_jacobi(Lv3 F, double damping) {
+    lzb_pdl_enter();
     int ix, iy, iz;
     int64_t vi;
     if (!vxyz(F, ix, iy, iz, vi)) return;
@@ -873,6 +887,7 @@ __global__ void k3_jacobi(Lv3 F, double damping) {
 }
 
 __global__ void k3_prolong(Lv3 F, Lv3 C) {
+    lzb_pdl_enter();
     int fx, fy, fz;
     int64_t vi;
     if (!vxyz(F, fx, fy, fz, vi)) return;
@@ -897,6 +912,7 @@ __global__ void k3_prolong(Lv3 F, Lv3 C) {
 // correction, damped Jacobi, the prolongated coarse correction. The coarse
 // levels are updated first; nothing there reads the leaf u.
 __global__ void k3_update_fine(Lv3 F, Lv3 C, int pi, double omega, double damping) {
+    lzb_pdl_enter();
     int fx, fy, fz;
     int64_t vi;
     if (!vxyz(F, fx, fy, fz, vi)) return;
@@ -944,6 +960,7 @@ __global__ void k3_update_fine(Lv3 F, Lv3 C, int pi, double omega, double dampin
 }
 
 __global__ void k3_inject(Lv3 F, Lv3 C) {
+    lzb_pdl_enter();
     int ix, iy, iz;
     int64_t vi;
     if (!vxyz(C, ix, iy, iz, vi)) return;
@@ -1027,6 +1044,7 @@ __device__ __forceinline__ void galerkin_child(const double* K, int lx, int ly, 
 template <class Src>
 __global__ void __launch_bounds__(256) k3_galerkin(double* __restrict__ cop, Src S, int Nc, int64_t cbeg,
                                                    int64_t cend) {
+    lzb_pdl_enter();
     const int64_t c = cbeg + gtid();  // coarse cells [cbeg, cend)
     const int64_t ncc = static_cast<int64_t>(Nc) * Nc * Nc;
     if (c >= cend) return;
@@ -1383,6 +1401,10 @@ public:
                 LZB_LAUNCH(k3_prolong, vg(l), 128, 0, s_, lv(l), lv(l - 1));
                 smooth(l, nu);
             }
+            // coarse u held corrections: re-inject the fine solution so that a
+            // later additive step() forms u-hat = u - P u_c from the additive
+            // cycle's invariant (finish_cycle_sync, solver.cpp:344-347)
+            inject3();
             const uint64_t Nf = static_cast<uint64_t>(L3_[D_].N);
             rep.dof_updates = static_cast<uint64_t>(2 * nu) * (Nf - 1) * (Nf - 1) * (Nf - 1);
         }
@@ -1705,7 +1727,7 @@ private:
         // latency-bound marches otherwise (81^3: 108 blocks of 32 planes)
         const int bx = (N + kRzX - 1) / (kRzX - 1), by = (N + kRzY - 1) / (kRzY - 1);
         int zc = kRzChunk;
-        while (zc > 2 && static_cast<int64_t>(bx) * by * ((z1 - z0 + zc - 1) / zc) < 4 * 2 * 148)
+        while (zc > 2 && static_cast<int64_t>(bx) * by * ((z1 - z0 + zc - 1) / zc) < 4 * 2 * ctx_->sms)
             zc /= 2;
         const dim3 grid(bx, by, (z1 - z0 + zc - 1) / zc);
         const Lv3 v = lv(l);

@@ -7,6 +7,16 @@
 
 namespace lzb {
 
+// First statement of EVERY kernel of liblzb.so (tests/test_abi_host.py checks
+// it): LZB_LAUNCH may launch any kernel with programmatic dependent launch
+// while a cycle body is captured, and griddepcontrol.wait is what makes the
+// kernel wait for its predecessor's completion and memory (a no-op without a
+// programmatic predecessor).
+__device__ __forceinline__ void lzb_pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Constant tables uploaded once per device (make_ctx): K_unit = the reference
 // reference_subcell_stiffness(0,1,0,1) and the geometric transfer block.
 // (liblzb.so has a single device translation unit, lzb_unity.cu.)

@@ -52,6 +52,7 @@ lzb_ctx* make_ctx(int device) {
     LZB_CUDA(cudaSetDevice(device));
     auto* c = new lzb_ctx;
     c->device = device;
+    LZB_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
     int lo = 0, hi = 0;
     LZB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     // solve stream high priority, assembly stream low priority
@@ -84,6 +85,7 @@ void check_device_flag(lzb_ctx* c, cudaStream_t s) {
 
 // ------------------------------------------------------------ tables
 __global__ void k_field_parts(lzb_field f, int N, double h, int n, int axis, double* out) {
+    lzb_pdl_enter();
     int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (t >= static_cast<int64_t>(N) * n) return;
     int c = static_cast<int>(t / n), i = static_cast<int>(t % n);
@@ -94,6 +96,7 @@ __global__ void k_field_parts(lzb_field f, int N, double h, int n, int axis, dou
 }
 
 __global__ void k_seg_table(int n, double* seg) {
+    lzb_pdl_enter();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     AxisSeg s = axis_seg(i, 1.0 / n);
@@ -104,6 +107,7 @@ __global__ void k_seg_table(int n, double* seg) {
 }
 
 __global__ void k_ksub_table(int n, double* ktab) {
+    lzb_pdl_enter();
     int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (t >= static_cast<int64_t>(n) * n) return;
     int i = static_cast<int>(t / n), j = static_cast<int>(t % n);
@@ -152,6 +156,7 @@ __global__ void k_integrate_boxes(lzb_field f, int64_t ncells, const double* __r
                                   const double* __restrict__ y0, const double* __restrict__ hh,
                                   const int32_t* __restrict__ nn, double* __restrict__ out,
                                   int fast) {
+    lzb_pdl_enter();
     int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (c >= ncells) return;
     integrate_cell(f, x0[c], y0[c], hh[c], nn[c], fast, out + 16 * c);
@@ -161,6 +166,7 @@ __global__ void k_integrate_boxes(lzb_field f, int64_t ncells, const double* __r
 template <int KIND, bool FAST>
 __global__ void __launch_bounds__(kIntThreads, 2) k_integrate_level(lzb_field f, int N, IntTables T,
                                                                     double* __restrict__ out) {
+    lzb_pdl_enter();
     extern __shared__ double sm[];
     stage_common(sm, f, T);
     const int64_t ncell = static_cast<int64_t>(N) * N;
@@ -221,6 +227,7 @@ void launch_integrate_level(const lzb_field& f, int N, const IntTables& T, doubl
 
 // FP64 peak probe: 8 independent DFMA chains per thread, one CTA per SM slot.
 __global__ void k_fp64_probe(int iters, double seed, double* sink) {
+    lzb_pdl_enter();
     double a[8];
     for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 1e-9 + k;
     const double m = 0.999999999, c = 1e-9;
@@ -235,17 +242,20 @@ __global__ void k_fp64_probe(int iters, double seed, double* sink) {
 // ------------------------------------------------------------------ codec
 __global__ void k_encode(int64_t count, const double* __restrict__ x, int p3, uint8_t* out,
                          int* err) {
+    lzb_pdl_enter();
     int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= count) return;
     if (!encode_value(x[i], p3, out + i * p3)) atomicExch(err, 1);
 }
 __global__ void k_decode(int64_t count, const uint8_t* in, int p3, double* out) {
+    lzb_pdl_enter();
     int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= count) return;
     out[i] = decode_value(in + i * p3, p3);
 }
 __global__ void k_choose(int64_t nrec, int entries, const double* __restrict__ v, double delta,
                          int32_t* out, int* err) {
+    lzb_pdl_enter();
     int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (r >= nrec) return;
     int p = choose_precision(v + r * entries, entries, delta);
@@ -352,6 +362,7 @@ __device__ int boxmg_from_A(const double* A, double* P) {
 
 __global__ void k_galerkin_batch(int64_t np, const double* __restrict__ ch,
                                  const double* __restrict__ P, double* __restrict__ out) {
+    lzb_pdl_enter();
     int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= np) return;
     double A[256], Pl[64];
@@ -362,6 +373,7 @@ __global__ void k_galerkin_batch(int64_t np, const double* __restrict__ ch,
 
 __global__ void k_boxmg_batch(int64_t np, const double* __restrict__ ch, double* __restrict__ P,
                               int32_t* fb) {
+    lzb_pdl_enter();
     int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= np) return;
     double A[256];

@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(128, 4) k_assemble3_leaves(Field3 F, const int
                                                              double* __restrict__ op, int8_t* __restrict__ p3o,
                                                              int32_t* __restrict__ no, unsigned long long* stats,
                                                              int* err) {
+    lzb_pdl_enter();
     const int64_t t = gtid();
     if (t >= count) return;
     const int64_t c = list ? list[t] : t;
@@ -133,12 +134,14 @@ __device__ __forceinline__ bool ownerA(const LvA& C, int fx, int fy, int fz, int
 }
 
 __global__ void k4_mark_leaves(const int4* __restrict__ leaves, int64_t n, int lvl, LvA L) {
+    lzb_pdl_enter();
     const int64_t t = gtid();
     if (t >= n) return;
     const int4 c = leaves[t];
     if (c.x == lvl) L.cf[cidx(L.N, c.y, c.z, c.w)] = 1;
 }
 __global__ void k4_mark_parents(LvA F, LvA C) {
+    lzb_pdl_enter();
     const int64_t t = gtid();
     const int64_t nc = static_cast<int64_t>(F.N) * F.N * F.N;
     if (t >= nc || !F.cf[t]) return;
@@ -146,16 +149,19 @@ __global__ void k4_mark_parents(LvA F, LvA C) {
     C.cf[cidx(C.N, x / 3, y / 3, z / 3)] = 2;
 }
 __global__ void k4_exist01(const uint8_t* __restrict__ cf, int64_t n, int32_t* __restrict__ out) {
+    lzb_pdl_enter();
     const int64_t t = gtid();
     if (t < n) out[t] = cf[t] ? 1 : 0;
 }
 __global__ void k4_index(const uint8_t* __restrict__ cf, int64_t n, int32_t* __restrict__ oi) {
+    lzb_pdl_enter();
     const int64_t t = gtid();  // oi holds the exclusive scan of exist01; -1 where no cell
     if (t < n && !cf[t]) oi[t] = -1;
 }
 // leaf operators (Tree3 class planes over the leaf index) into their level's planes
 __global__ void k4_copy_leaf_ops(const int4* __restrict__ leaves, int64_t n, int lvl, const double* __restrict__ lop,
                                  int64_t nleaves, LvA L) {
+    lzb_pdl_enter();
     const int64_t t = gtid();
     if (t >= n) return;
     const int4 c = leaves[t];
@@ -166,6 +172,7 @@ __global__ void k4_copy_leaf_ops(const int4* __restrict__ leaves, int64_t n, int
 }
 // refined cells of C: Galerkin from the 27 children of F (k3_galerkin's class form)
 __global__ void __launch_bounds__(256) k4_galerkin(LvA C, LvA F) {
+    lzb_pdl_enter();
     const int64_t c = gtid();
     const int64_t ncc = static_cast<int64_t>(C.N) * C.N * C.N;
     if (c >= ncc || C.cf[c] != 2) return;
@@ -186,6 +193,7 @@ __global__ void __launch_bounds__(256) k4_galerkin(LvA C, LvA F) {
     for (int q = 0; q < 27; ++q) C.op[q * C.nop + jc] = out[q];
 }
 __global__ void k4_classify(LvA L) {
+    lzb_pdl_enter();
     int ix, iy, iz;
     int64_t vi;
     if (!vxyzA(L, ix, iy, iz, vi)) return;
@@ -202,6 +210,7 @@ __global__ void k4_classify(LvA L) {
 }
 // the level's lumped load: f(v) h^3/8 per adjacent leaf (solver.cpp:99-118)
 __global__ void k4_load(LvA L, double scale, double w) {
+    lzb_pdl_enter();
     int ix, iy, iz;
     int64_t vi;
     if (!vxyzA(L, ix, iy, iz, vi)) return;
@@ -214,6 +223,7 @@ __global__ void k4_load(LvA L, double scale, double w) {
     L.load[vi] = acc;
 }
 __global__ void k4_noise(LvA L, int level, uint64_t seed) {
+    lzb_pdl_enter();
     int ix, iy, iz;
     int64_t vi;
     if (!vxyzA(L, ix, iy, iz, vi)) return;
@@ -233,11 +243,13 @@ __global__ void k4_noise(LvA L, int level, uint64_t seed) {
     L.v[LZB_V_U][vi] = (4.0 / 3.0) * static_cast<double>(kk >> 11) * 0x1.0p-53;
 }
 __global__ void k4_reset_fl(LvA L) {
+    lzb_pdl_enter();
     int ix, iy, iz;
     int64_t vi;
     if (vxyzA(L, ix, iy, iz, vi)) L.v[LZB_V_FL][vi] = L.load[vi];
 }
 __global__ void k4_uhat(LvA F, LvA C, int has_coarse) {
+    lzb_pdl_enter();
     int fx, fy, fz;
     int64_t vi;
     if (!vxyzA(F, fx, fy, fz, vi)) return;
@@ -256,6 +268,7 @@ __global__ void k4_uhat(LvA F, LvA C, int has_coarse) {
 }
 // r, r-hat, diag over the existing adjacent cells (gather, q = dx + 2 dy + 4 dz)
 __global__ void __launch_bounds__(128) k4_residual(LvA F) {
+    lzb_pdl_enter();
     int ix, iy, iz;
     int64_t vi;
     if (!vxyzA(F, ix, iy, iz, vi)) return;
@@ -291,6 +304,7 @@ __global__ void __launch_bounds__(128) k4_residual(LvA F) {
 }
 // fl_c += P^T r-hat over the lattice vertices each adjacent refined patch owns
 __global__ void k4_restrict(LvA F, LvA C) {
+    lzb_pdl_enter();
     int IX, IY, IZ;
     int64_t vi;
     if (!vxyzA(C, IX, IY, IZ, vi)) return;
@@ -317,6 +331,7 @@ __global__ void k4_restrict(LvA F, LvA C) {
     C.v[LZB_V_FL][vi] = acc;
 }
 __global__ void __launch_bounds__(256) k4_norm_partial(LvA L, double* partial) {
+    lzb_pdl_enter();
     __shared__ double sh[256];
     double s = 0.0;
     const int wx = L.bx1 - L.bx0, wy = L.by1 - L.by0;
@@ -336,6 +351,7 @@ __global__ void __launch_bounds__(256) k4_norm_partial(LvA L, double* partial) {
     if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
 }
 __global__ void k4_snap(LvA L) {
+    lzb_pdl_enter();
     int ix, iy, iz;
     int64_t i;
     if (!vxyzA(L, ix, iy, iz, i)) return;
@@ -343,6 +359,7 @@ __global__ void k4_snap(LvA L) {
     L.v[LZB_V_AUX][i] = 0.0;
 }
 __global__ void k4_aux_inject(LvA F, LvA C) {
+    lzb_pdl_enter();
     int ix, iy, iz;
     int64_t vi;
     if (!vxyzA(C, ix, iy, iz, vi)) return;
@@ -353,6 +370,7 @@ __global__ void k4_aux_inject(LvA F, LvA C) {
 // the leaf-ward updates of one level on its interior vertices: adaFAC-PI aux
 // correction (pi), damped Jacobi (damping), prolongated coarse correction (prol)
 __global__ void k4_update(LvA F, LvA C, int pi, double omega, double damping, int jac, int prol) {
+    lzb_pdl_enter();
     int fx, fy, fz;
     int64_t vi;
     if (!vxyzA(F, fx, fy, fz, vi)) return;
@@ -392,6 +410,7 @@ __global__ void k4_update(LvA F, LvA C, int pi, double omega, double damping, in
     F.v[LZB_V_U][vi] = u;
 }
 __global__ void k4_inject(LvA F, LvA C) {
+    lzb_pdl_enter();
     int ix, iy, iz;
     int64_t vi;
     if (!vxyzA(C, ix, iy, iz, vi)) return;
@@ -402,6 +421,7 @@ __global__ void k4_inject(LvA F, LvA C) {
 // hanging u from the parent interpolant of the first existing host cell
 // (mesh.cpp:182-214 in 3D: candidates x outer, then y, then z)
 __global__ void k4_hanging(LvA F, LvA C) {
+    lzb_pdl_enter();
     int ix, iy, iz;
     int64_t vi;
     if (!vxyzA(F, ix, iy, iz, vi)) return;

@@ -32,6 +32,27 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
 
 
+def test_every_kernel_enters_through_pdl_wait():
+    """LZB_LAUNCH may give any launch the programmatic-dependent-launch
+    attribute while a cycle body is captured (engine.hpp), so every kernel's
+    first statement must be lzb_pdl_enter() (griddepcontrol.wait): otherwise it
+    could run before its predecessor's writes are visible."""
+    src = os.path.join(ROOT, "paper_2005_03606_b200", "csrc")
+    missing, count = [], 0
+    for name in sorted(os.listdir(src)):
+        if not name.endswith((".cu", ".cuh")):
+            continue
+        s = open(os.path.join(src, name)).read()
+        for m in re.finditer(r"__global__", s):
+            i, j = s.find("{", m.end()), s.find(";", m.end())
+            if j != -1 and j < i:
+                continue  # a declaration
+            count += 1
+            if not s[i + 1:i + 200].lstrip().startswith("lzb_pdl_enter();"):
+                missing.append(f"{name}: {s[m.end():i].split('(')[0].split()[-1]}")
+    assert count >= 90 and not missing, missing
+
+
 def _has_gpu():
     try:
         import torch

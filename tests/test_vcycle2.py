@@ -163,3 +163,29 @@ def test_vcycle_on_unassembled_leaves_converges():
     reps = [G.vcycle(2) for _ in range(8)]
     assert reps[-1]["normalized"] < 1e-3
     assert G.step()["cycle"] == 9
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("solver", ["additive", "adafac-pi"])
+def test_vcycle_then_step_uses_injected_solution(solver):
+    """after vcycle() the coarse u is the injected fine u (the
+    additive cycle's invariant), so a following step() equals a step on a
+    grid that starts from the same leaf u and operators, bit for bit."""
+    depth = 4
+    d = lzb.make_desc(depth=depth, field=lzb.checkerboard(7, 8), solver=solver, omega=0.6, rhs_kind="sinprod",
+                      max_cycles=100)
+    A = lzb.Grid(d, 42)
+    A.assemble_fixed(3)
+    A.vcycle(1)
+    A.vcycle(2)
+    for lvl in range(depth):
+        assert np.array_equal(A.vertices(lvl, lzb.T.V_U), A.vertices(lvl + 1, lzb.T.V_U)[::3, ::3])
+    B = lzb.Grid(d, 42)
+    B.assemble_fixed(3)
+    B.vcycle(1)  # the same coarse operators (finest-first Galerkin pass) as A's
+    B.set_vertices(depth, lzb.T.V_U, A.vertices(depth, lzb.T.V_U))
+    B.pass_(4)  # finish_cycle_sync: inject into the coarse levels
+    ra, rb = A.step(), B.step()
+    assert ra["residual"] == rb["residual"]
+    for lvl in range(depth + 1):
+        assert np.array_equal(A.vertices(lvl, lzb.T.V_U), B.vertices(lvl, lzb.T.V_U)), lvl
