@@ -107,6 +107,14 @@ int lzb_grid_init_noise(lzb_grid* g, uint64_t seed);
 int lzb_grid_eager_setup(lzb_grid* g);
 /* Fixed-p assembly (BASELINE config 1): every leaf integrated at n, published, p1 = top. */
 int lzb_grid_assemble_fixed(lzb_grid* g, int n);
+/* lzb_grid_assemble_fixed through the same fused integrate + compress +
+ * publish kernel, also returning each leaf's integrated element matrix before
+ * compression (host_raw: N*N*16 doubles, cy*N+cx): integrate_element
+ * (element.hpp:36-49) of every leaf, for parity checks of the benched kernel. */
+int lzb_grid_assemble_fixed_raw(lzb_grid* g, int n, double* host_raw);
+/* CellStream::publish_element + p1 store for every leaf (stream.cpp:100-132,
+ * batched): mats N*N*16 doubles, n per cell (host buffers). */
+int lzb_grid_publish_level(lzb_grid* g, int level, const double* mats, const int32_t* n, int32_t p1);
 /* Same for the leaf cell rows [row0, row1) only: one slab of a multi-GPU
  * decomposition (cells are independent). */
 int lzb_grid_assemble_rows(lzb_grid* g, int n, int row0, int row1);

@@ -17,12 +17,15 @@
  * identical (compiled with -ffp-contract=off).
  */
 #define _POSIX_C_SOURCE 200809L
+#define _DEFAULT_SOURCE
 #include "lzb_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
 
 #ifndef M_PI
 #define M_PI 3.14159265358979323846
@@ -119,18 +122,74 @@ void orc_subcell_stiffness(double a, double b, double c, double d, double* K) {
         }
 }
 
+/* K_sub(i, j) of integrate_element at sub-sample count n (element.hpp:42-45):
+ * reference_subcell_stiffness(i*inv, (i+1)*inv, j*inv, (j+1)*inv). It is a
+ * pure function of (n, i, j), so it is tabulated once per n and per thread
+ * with the very same call -- the bits are those of the per-sample call. */
+static const double* ksub_table(int n) {
+    static _Thread_local double* tab = NULL;
+    static _Thread_local int tab_n = 0;
+    if (tab_n != n) {
+        free(tab);
+        tab = malloc((size_t)n * n * 16 * sizeof(double));
+        double inv = 1.0 / n;
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j)
+                orc_subcell_stiffness(i * inv, (i + 1) * inv, j * inv, (j + 1) * inv, tab + ((size_t)i * n + j) * 16);
+        tab_n = n;
+    }
+    return tab;
+}
+
 /* element.hpp:36-49: i (x) outer, j (y) inner, out += eps * K_sub. */
 void orc_integrate_element(const lzb_field* f, double x0, double y0, double h, int n,
                            double* out) {
     double inv = 1.0 / n;
-    double K[16];
+    const double* tab = ksub_table(n);
     for (int k = 0; k < 16; ++k) out[k] = 0.0;
     for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j) {
             double e = orc_field_eval(f, x0 + (i + 0.5) * inv * h, y0 + (j + 0.5) * inv * h);
-            orc_subcell_stiffness(i * inv, (i + 1) * inv, j * inv, (j + 1) * inv, K);
+            const double* K = tab + ((size_t)i * n + j) * 16;
             for (int k = 0; k < 16; ++k) out[k] += e * K[k];
         }
+}
+
+/* integrate_element over every cell of a regular level (boxes as cell_box,
+ * element.hpp:29-32, h = pow(1/3, level) as mesh.hpp:87), cells split into
+ * contiguous ranges over `threads` POSIX threads (the reference's pure
+ * function on disjoint cells). out: N*N*16, cy*N+cx. */
+typedef struct {
+    const lzb_field* f;
+    int N, n;
+    double h;
+    int64_t c0, c1;
+    double* out;
+} level_job;
+static void* level_worker(void* arg) {
+    level_job* j = (level_job*)arg;
+    for (int64_t c = j->c0; c < j->c1; ++c)
+        orc_integrate_element(j->f, (c % j->N) * j->h, (c / j->N) * j->h, j->h, j->n, j->out + 16 * c);
+    return NULL;
+}
+void orc_integrate_level(const lzb_field* f, int level, int n, double* out, int threads) {
+    int N = 1;
+    for (int l = 0; l < level; ++l) N *= 3;
+    double h = pow(1.0 / 3, level);
+    int64_t nc = (int64_t)N * N;
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    pthread_t tid[256];
+    level_job jobs[256];
+    for (int t = 0; t < threads; ++t) {
+        jobs[t] = (level_job){f, N, n, h, nc * t / threads, nc * (t + 1) / threads, out};
+        if (pthread_create(&tid[t], NULL, level_worker, &jobs[t]) != 0) {
+            level_worker(&jobs[t]);
+            tid[t] = 0;
+        }
+    }
+    for (int t = 0; t < threads; ++t)
+        if (tid[t]) pthread_join(tid[t], NULL);
 }
 
 /* ================================================================ codec */
@@ -634,7 +693,11 @@ static int next_n(const orc_grid* g, int n) {
 }
 
 /* assembly.cpp:10-60 (n -> n+1; LZB_SCHEDULE_DOUBLE is the BASELINE knob) */
-static int adaptive_step(orc_grid* g, int c) {
+/* pre: NULL, or the integration at next_n(p1) computed ahead (a pure
+ * function of the cell and n, see prefetch_integrations) */
+static int adaptive_step_pre(orc_grid* g, int c, const double* pre);
+static int adaptive_step(orc_grid* g, int c) { return adaptive_step_pre(g, c, NULL); }
+static int adaptive_step_pre(orc_grid* g, int c, const double* pre) {
     orc_level* L = &g->L[g->D];
     int32_t p1 = L->p1[c];
     if (p1 == LZB_P1_TOP) return 0;
@@ -653,7 +716,8 @@ static int adaptive_step(orc_grid* g, int c) {
         return 0;
     }
     double fresh[16], diff[16];
-    orc_integrate_element(&g->d.field, cx * L->h, cy * L->h, L->h, nn, fresh);
+    if (pre) memcpy(fresh, pre, sizeof fresh);
+    else orc_integrate_element(&g->d.field, cx * L->h, cy * L->h, L->h, nn, fresh);
     const double* old = L->op + 16 * c;
     double denom = max_abs16(old), ratio = 0.0;
     if (denom == 0.0) {
@@ -713,8 +777,60 @@ static int recompute_coarse(orc_grid* g, int l, int c, int* published);
 
 /* TaskPool::begin_cycle with workers == 1: the high class first, then the
  * leaf tasks, FIFO, <= throttle tasks in all (scheduler.cpp:88-111) */
+/* The leaf tasks a begin_cycle will run integrate at next_n(p1) of their
+ * cell; p1 of a queued leaf cannot change before its task runs (p2 allows one
+ * task per cell, coarse tasks do not touch leaves), so those integrations are
+ * computed ahead on host threads, in any order -- each is the same pure
+ * function call as inside adaptive_step. The protocol itself then runs
+ * strictly in FIFO order. (A speed-up of the checker only.) */
+typedef struct {
+    const orc_grid* g;
+    const int32_t* cells;
+    int64_t k0, k1;
+    double* out;
+} pre_job;
+static void* pre_worker(void* arg) {
+    pre_job* j = (pre_job*)arg;
+    const orc_level* L = &j->g->L[j->g->D];
+    for (int64_t k = j->k0; k < j->k1; ++k) {
+        int c = j->cells[k], p1 = L->p1[c];
+        if (p1 == LZB_P1_TOP || p1 == LZB_P1_BOTTOM) continue;
+        if (j->g->d.n_max > 0 && p1 >= j->g->d.n_max) continue;
+        orc_integrate_element(&j->g->d.field, (c % L->N) * L->h, (c / L->N) * L->h, L->h, next_n(j->g, p1),
+                              j->out + 16 * k);
+    }
+    return NULL;
+}
+static double* prefetch_integrations(orc_grid* g, int64_t count) {
+    if (count < 4096) return NULL;
+    double* out = malloc((size_t)count * 16 * sizeof(double));
+    if (!out) return NULL;
+    long nt = sysconf(_SC_NPROCESSORS_ONLN);
+    int threads = nt < 1 ? 1 : (nt > 256 ? 256 : (int)nt);
+    pthread_t tid[256];
+    pre_job jobs[256];
+    for (int t = 0; t < threads; ++t) {
+        jobs[t] = (pre_job){g, g->queue + g->qhead, count * t / threads, count * (t + 1) / threads, out};
+        if (pthread_create(&tid[t], NULL, pre_worker, &jobs[t]) != 0) {
+            pre_worker(&jobs[t]);
+            tid[t] = 0;
+        }
+    }
+    for (int t = 0; t < threads; ++t)
+        if (tid[t]) pthread_join(tid[t], NULL);
+    return out;
+}
+
 static int pool_begin_cycle(orc_grid* g) {
     uint64_t budget = g->d.throttle == 0 ? UINT64_MAX : g->d.throttle;
+    /* leaf tasks this call will run: those the budget leaves after the high class */
+    int64_t nleaf = g->qtail - g->qhead, nhigh = (g->htail - g->hhead) / 2;
+    if (budget != UINT64_MAX) {
+        int64_t left = (int64_t)budget - nhigh;
+        if (left < nleaf) nleaf = left < 0 ? 0 : left;
+    }
+    const int64_t qbase = g->qhead;
+    double* pre = prefetch_integrations(g, nleaf);
     while (g->hhead < g->htail || g->qhead < g->qtail) {
         if (budget == 0) break;
         if (budget != UINT64_MAX) --budget;
@@ -724,13 +840,18 @@ static int pool_begin_cycle(orc_grid* g) {
             g->hhead += 2;
             rc = recompute_coarse(g, l, c, &pub);
         } else {
+            int64_t k = g->qhead - qbase;
             int c = g->queue[g->qhead++];
-            rc = adaptive_step(g, c);
+            rc = adaptive_step_pre(g, c, pre && k < nleaf ? pre + 16 * k : NULL);
             g->L[g->D].p2[c] = 0;
         }
         g->completed++;
-        if (rc) return rc;
+        if (rc) {
+            free(pre);
+            return rc;
+        }
     }
+    free(pre);
     return 0;
 }
 
@@ -1293,6 +1414,18 @@ int orc_publish_element(orc_grid* g, int level, int cx, int cy, const double* m,
     int rc = publish_element(g, level, c, m, n);
     if (rc) return rc;
     L->p1[c] = p1;
+    return 0;
+}
+
+/* CellStream::publish_element + p1 store for every cell of a level, in cell
+ * index order (a loop of the per-cell call; mats: N*N*16, n per cell). */
+int orc_publish_level(orc_grid* g, int level, const double* mats, const int32_t* n, int32_t p1) {
+    orc_level* L = &g->L[level];
+    for (int64_t c = 0; c < (int64_t)L->N * L->N; ++c) {
+        int rc = publish_element(g, level, (int)c, mats + 16 * c, n[c]);
+        if (rc) return rc;
+        L->p1[c] = p1;
+    }
     return 0;
 }
 

@@ -24,6 +24,8 @@ uint64_t orc_splitmix64(uint64_t z);
 void orc_subcell_stiffness(double a, double b, double c, double d, double* out16);
 void orc_integrate_element(const lzb_field* f, double x0, double y0, double h, int n,
                            double* out16);
+/* every cell of a regular level, threaded over disjoint cell ranges */
+void orc_integrate_level(const lzb_field* f, int level, int n, double* out, int threads);
 int orc_encode_value(double x, int p3, uint8_t* out); /* 0 ok, LZB_ERR_PROTOCOL */
 double orc_decode_value(const uint8_t* in, int p3);
 int orc_choose_precision(const double* v, int64_t count, double delta); /* <0: error */
@@ -50,6 +52,7 @@ int orc_cells(orc_grid* g, int level, double* ops, int32_t* p1, int32_t* n, int3
               uint32_t* epoch);
 int orc_publish_element(orc_grid* g, int level, int cx, int cy, const double* m, int n,
                         int32_t p1);
+int orc_publish_level(orc_grid* g, int level, const double* mats, const int32_t* n, int32_t p1);
 int orc_adaptive_step(orc_grid* g, int level, int cx, int cy);
 int orc_stats(orc_grid* g, lzb_compression_stats* out);
 int64_t orc_stream_image(orc_grid* g, uint8_t* out, int64_t cap);

@@ -38,6 +38,8 @@ def lib():
         L.orc_splitmix64.argtypes = [C.c_uint64]
         L.orc_subcell_stiffness.argtypes = [C.c_double] * 4 + [vp]
         L.orc_integrate_element.argtypes = [C.POINTER(Field), C.c_double, C.c_double, C.c_double, C.c_int, vp]
+        L.orc_integrate_level.argtypes = [C.POINTER(Field), C.c_int, C.c_int, vp, C.c_int]
+        L.orc_publish_level.argtypes = [vp, C.c_int, vp, vp, C.c_int32]
         L.orc_encode_value.argtypes = [C.c_double, C.c_int, vp]
         L.orc_decode_value.restype = C.c_double
         L.orc_decode_value.argtypes = [vp, C.c_int]
@@ -158,6 +160,15 @@ def integrate_element(field: Field, x0, y0, h, n):
     return out
 
 
+def integrate_level(field: Field, level, n, threads=None):
+    """Every cell of a regular level (cy*N+cx, 16 doubles each), the
+    reference's integrate_element over disjoint cell ranges on host threads."""
+    N = 3 ** level
+    out = np.zeros((N * N, 16))
+    lib().orc_integrate_level(C.byref(field), level, n, _ptr(out), int(threads or os.cpu_count() or 1))
+    return out
+
+
 def encode_value(x, p3):
     out = np.zeros(8, np.uint8)
     _check(lib().orc_encode_value(float(x), p3, _ptr(out)))
@@ -268,6 +279,11 @@ class Grid:
     def publish_element(self, level, cx, cy, m, n, p1):
         m = np.ascontiguousarray(m, dtype=np.float64)
         _check(lib().orc_publish_element(self.h, level, cx, cy, _ptr(m), n, p1))
+
+    def publish_level(self, level, mats, n, p1):
+        m = np.ascontiguousarray(mats, dtype=np.float64).reshape(-1)
+        nn = np.ascontiguousarray(np.broadcast_to(np.asarray(n, np.int32), (9 ** level,)))
+        _check(lib().orc_publish_level(self.h, level, _ptr(m), _ptr(nn), p1))
 
     def adaptive_step(self, level, cx, cy):
         _check(lib().orc_adaptive_step(self.h, level, cx, cy))

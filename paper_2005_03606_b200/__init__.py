@@ -109,6 +109,8 @@ def lib():
         L.lzb_grid_cells.argtypes = [vp, C.c_int, vp, vp, vp, vp, vp]
         L.lzb_grid_transfer.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp]
         L.lzb_grid_publish_element.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, i32]
+        L.lzb_grid_publish_level.argtypes = [vp, C.c_int, vp, vp, i32]
+        L.lzb_grid_assemble_fixed_raw.argtypes = [vp, C.c_int, vp]
         L.lzb_grid_adaptive_step.argtypes = [vp, C.c_int, C.c_int, C.c_int]
         L.lzb_grid_stats.argtypes = [vp, C.POINTER(CompressionStats)]
         L.lzb_grid_stream_image.argtypes = [vp, vp, i64, C.POINTER(i64)]
@@ -506,6 +508,19 @@ class Grid:
         out = np.zeros(64)
         _check(lib().lzb_grid_transfer(self.h, level, cx, cy, _ptr(out)))
         return out
+
+    def assemble_fixed_raw(self, n):
+        """assemble_fixed(n) through the same fused kernel; returns the
+        integrated leaf matrices before compression, (N*N, 16)."""
+        N = 3 ** self.desc.depth
+        out = np.zeros((N * N, 16))
+        _check(lib().lzb_grid_assemble_fixed_raw(self.h, n, _ptr(out)))
+        return out
+
+    def publish_level(self, level, mats, n, p1):
+        m = np.ascontiguousarray(mats, dtype=np.float64).reshape(-1)
+        nn = np.ascontiguousarray(np.broadcast_to(np.asarray(n, np.int32), (9 ** level,)))
+        _check(lib().lzb_grid_publish_level(self.h, level, _ptr(m), _ptr(nn), p1))
 
     def publish_element(self, level, cx, cy, m, n, p1):
         m = np.ascontiguousarray(m, dtype=np.float64)

@@ -411,12 +411,20 @@ struct CellRect {
     __device__ __forceinline__ int cy(int64_t cl) const { return y0 + static_cast<int>(cl / w); }
 };
 
+// The integrated (pre-compression) element matrix of a cell, for the parity
+// tests of the fused assembly kernels (lzb_grid_assemble_fixed_raw); raw is
+// null on every other path.
+__device__ __forceinline__ void store_raw(double* out, const double* m) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) out[k] = m[k];
+}
+
 // Fixed-p assembly: every leaf integrated at n, published, p1 = top.
 template <int KIND, bool FAST>
 __global__ void __launch_bounds__(kIntThreads, 2) k_fixed(LevelView F, lzb_field f, int n, IntTables T,
                                                           double delta_max, uint32_t cycle,
                                                           unsigned long long* stats, int* err,
-                                                          int64_t cbeg, int64_t cend, CellRect R) {
+                                                          int64_t cbeg, int64_t cend, CellRect R, double* __restrict__ raw) {
     lzb_pdl_enter();
     extern __shared__ double sm[];
     stage_common(sm, f, T);
@@ -447,6 +455,7 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_fixed(LevelView F, lzb_field
         if (!mine[q]) continue;
         const int cx = static_cast<int>(cc[q] % F.N), cy = static_cast<int>(cc[q] / F.N);
         const double e_c = combine_k<KIND>(T.cxp[cx], T.cyp[cy], f.value, f.eps_low, f.blocks, sm);
+        if (raw) store_raw(raw + 16 * cc[q], m[q]);
         if (!publish_leaf_k9(F, static_cast<int>(cc[q]), m[q], n, e_c, delta_max, cycle, stats))
             atomicExch(err, 1);
         F.p1[cc[q]] = LZB_P1_TOP;
@@ -460,7 +469,7 @@ template <int KIND, bool FAST>
 __global__ void __launch_bounds__(kIntThreads, 2) k_fixed_res(LevelView F, lzb_field f, int n, IntTables T,
                                                               double delta_max, uint32_t cycle,
                                                               unsigned long long* stats, int* err,
-                                                              int64_t cbeg, int64_t cend, CellRect R) {
+                                                              int64_t cbeg, int64_t cend, CellRect R, double* __restrict__ raw) {
     lzb_pdl_enter();
     extern __shared__ double sm[];
     stage_common(sm, f, T);
@@ -503,6 +512,7 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_fixed_res(LevelView F, lzb_f
             if (!mine[q]) continue;
             const int cx = static_cast<int>(cc[q] % F.N), cy = static_cast<int>(cc[q] / F.N);
             const double e_c = combine_k<KIND>(T.cxp[cx], T.cyp[cy], f.value, f.eps_low, f.blocks, sm);
+            if (raw) store_raw(raw + 16 * cc[q], m[q]);
             if (!publish_leaf_k9(F, static_cast<int>(cc[q]), m[q], n, e_c, delta_max, cycle, stats))
                 atomicExch(err, 1);
             F.p1[cc[q]] = LZB_P1_TOP;
@@ -2002,6 +2012,22 @@ __global__ void k_publish_one(LevelView F, lzb_field f, int c, const double* m, 
     if (F.cp3 && p1 == LZB_P1_BOTTOM) F.cp3[c] = -1;
 }
 
+// CellStream::publish_element + marker store for every leaf cell (the batched
+// form of k_publish_one; mats: 16 doubles per cell, n per cell).
+__global__ void k_publish_level(LevelView F, lzb_field f, const double* __restrict__ mats,
+                                const int32_t* __restrict__ nn, int32_t p1, double delta_max, uint32_t cycle,
+                                unsigned long long* stats, int* err) {
+    lzb_pdl_enter();
+    const int64_t c = gtid();
+    if (c >= static_cast<int64_t>(F.N) * F.N) return;
+    double m[16];
+    for (int k = 0; k < 16; ++k) m[k] = mats[16 * c + k];
+    const double e = centre_eps(f, F, static_cast<int>(c % F.N), static_cast<int>(c / F.N));
+    if (!publish_leaf(F, static_cast<int>(c), m, nn[c], e, delta_max, cycle, stats)) atomicExch(err, 1);
+    F.p1[c] = p1;
+    if (F.cp3 && p1 == LZB_P1_BOTTOM) F.cp3[c] = -1;
+}
+
 __global__ void k_step_one(LevelView F, lzb_field f, int c, int schedule, int n_max, double term_c,
                            double delta_max, uint32_t cycle, int fast, unsigned long long* stats,
                            int* err) {
@@ -2164,7 +2190,7 @@ inline void dispatch_step(bool fast, cudaStream_t s, const LevelView& F, const L
 template <int KIND, bool FAST>
 void launch_fixed_k(cudaStream_t s, const LevelView& F, const lzb_field& f, int n, const IntTables& T,
                     double dmax, uint32_t cycle, unsigned long long* stats, int* err, int64_t cbeg,
-                    int64_t cend, CellRect R) {
+                    int64_t cend, CellRect R, double* raw) {
     const size_t rsmem = res_smem_bytes(n);
     if (rsmem <= kResidentSmemMax) {  // persistent: K_sub table resident, one range per block
         static int grid = 0;          // per instantiation: resident blocks x SMs
@@ -2181,21 +2207,21 @@ void launch_fixed_k(cudaStream_t s, const LevelView& F, const lzb_field& f, int 
         const int64_t want = (cend - cbeg + kCPT - 1) / kCPT;
         const unsigned g = static_cast<unsigned>(want < grid ? (want > 0 ? want : 1) : grid);
         LZB_LAUNCH((k_fixed_res<KIND, FAST>), g, kIntThreads, rsmem, s, F, f, n, T, dmax, cycle, stats, err,
-                   cbeg, cend, R);
+                   cbeg, cend, R, raw);
         return;
     }
     size_t smem = int_smem_bytes(n);
     set_smem(k_fixed<KIND, FAST>, smem);
     LZB_LAUNCH((k_fixed<KIND, FAST>), blocks_for(cend - cbeg, kIntThreads * kCPT), kIntThreads, smem, s, F,
-               f, n, T, dmax, cycle, stats, err, cbeg, cend, R);
+               f, n, T, dmax, cycle, stats, err, cbeg, cend, R, raw);
 }
 
 template <int KIND>
 void launch_fixed(bool fast, cudaStream_t s, const LevelView& F, const lzb_field& f, int n,
                   const IntTables& T, double dmax, uint32_t cycle, unsigned long long* stats, int* err,
-                  int64_t cbeg, int64_t cend, CellRect R) {
-    if (fast) launch_fixed_k<KIND, true>(s, F, f, n, T, dmax, cycle, stats, err, cbeg, cend, R);
-    else launch_fixed_k<KIND, false>(s, F, f, n, T, dmax, cycle, stats, err, cbeg, cend, R);
+                  int64_t cbeg, int64_t cend, CellRect R, double* raw) {
+    if (fast) launch_fixed_k<KIND, true>(s, F, f, n, T, dmax, cycle, stats, err, cbeg, cend, R, raw);
+    else launch_fixed_k<KIND, false>(s, F, f, n, T, dmax, cycle, stats, err, cbeg, cend, R, raw);
 }
 
 }  // namespace
@@ -2605,11 +2631,11 @@ public:
         int* err = ctx_->err.p;
         const double dm = d_.delta_max;
         switch (d_.field.kind) {
-            case LZB_FIELD_THETA: launch_fixed<LZB_FIELD_THETA>(fast, st, F, d_.field, n, T, dm, cycle_, stats, err, 0, count, R); break;
-            case LZB_FIELD_QUADRANT: launch_fixed<LZB_FIELD_QUADRANT>(fast, st, F, d_.field, n, T, dm, cycle_, stats, err, 0, count, R); break;
-            case LZB_FIELD_CHECKER: launch_fixed<LZB_FIELD_CHECKER>(fast, st, F, d_.field, n, T, dm, cycle_, stats, err, 0, count, R); break;
-            case LZB_FIELD_SINUSOID: launch_fixed<LZB_FIELD_SINUSOID>(fast, st, F, d_.field, n, T, dm, cycle_, stats, err, 0, count, R); break;
-            default: launch_fixed<LZB_FIELD_CONSTANT>(fast, st, F, d_.field, n, T, dm, cycle_, stats, err, 0, count, R); break;
+            case LZB_FIELD_THETA: launch_fixed<LZB_FIELD_THETA>(fast, st, F, d_.field, n, T, dm, cycle_, stats, err, 0, count, R, raw_); break;
+            case LZB_FIELD_QUADRANT: launch_fixed<LZB_FIELD_QUADRANT>(fast, st, F, d_.field, n, T, dm, cycle_, stats, err, 0, count, R, raw_); break;
+            case LZB_FIELD_CHECKER: launch_fixed<LZB_FIELD_CHECKER>(fast, st, F, d_.field, n, T, dm, cycle_, stats, err, 0, count, R, raw_); break;
+            case LZB_FIELD_SINUSOID: launch_fixed<LZB_FIELD_SINUSOID>(fast, st, F, d_.field, n, T, dm, cycle_, stats, err, 0, count, R, raw_); break;
+            default: launch_fixed<LZB_FIELD_CONSTANT>(fast, st, F, d_.field, n, T, dm, cycle_, stats, err, 0, count, R, raw_); break;
         }
     }
 
@@ -3354,6 +3380,36 @@ public:
         sync_check();
     }
 
+    // lzb_grid_publish_level: every leaf published from host matrices
+    void publish_level(int level, const double* mats, const int32_t* n, int32_t p1) {
+        if (level != D_) throw Error(LZB_ERR_INVALID, "publish_level is for the leaf level");
+        all_top_ = false;
+        const int64_t nc = L_[D_].nc;
+        DevBuf<double> dm(static_cast<size_t>(nc) * 16);
+        DevBuf<int32_t> dn(static_cast<size_t>(nc));
+        LZB_CUDA(cudaMemcpyAsync(dm.p, mats, dm.bytes(), cudaMemcpyHostToDevice, s_));
+        LZB_CUDA(cudaMemcpyAsync(dn.p, n, dn.bytes(), cudaMemcpyHostToDevice, s_));
+        LZB_LAUNCH(k_publish_level, blocks_for(nc, kThreads), kThreads, 0, s_, V(D_), d_.field, dm.p, dn.p, p1,
+                   d_.delta_max, cycle_, res_.p->s, ctx_->err.p);
+        sync_check();
+    }
+
+    // assemble_fixed through the same fused kernel, also writing each cell's
+    // integrated matrix (before compression) to host_raw (nc x 16)
+    void assemble_fixed_raw(int n, double* host_raw) {
+        DevBuf<double> raw(static_cast<size_t>(L_[D_].nc) * 16);
+        raw_ = raw.p;
+        try {
+            assemble_fixed(n);
+        } catch (...) {
+            raw_ = nullptr;
+            throw;
+        }
+        raw_ = nullptr;
+        LZB_CUDA(cudaMemcpyAsync(host_raw, raw.p, raw.bytes(), cudaMemcpyDeviceToHost, s_));
+        sync_check();
+    }
+
     void adaptive_step(int level, int cx, int cy) {
         check_cell(level, cx, cy);
         all_top_ = false;
@@ -3688,6 +3744,7 @@ private:
     lzb_grid_desc d_;
     int D_;
     cudaStream_t s_;
+    double* raw_ = nullptr;  // assemble_fixed_raw: integrated matrices out of the fused kernel
     std::vector<Level> L_;
     int64_t leaves_ = 0, total_cells_ = 0, total_vertices_ = 0;
     DevBuf<int32_t> list_, snap_;
@@ -3792,6 +3849,12 @@ int lzb_grid_assemble_rows(lzb_grid* g, int n, int row0, int row1) {
         g->g->assemble_fixed_rows(n, row0, row1);
         g->g->sync_check();
     });
+}
+int lzb_grid_assemble_fixed_raw(lzb_grid* g, int n, double* host_raw) {
+    return guarded([&] { g->g->assemble_fixed_raw(n, host_raw); });
+}
+int lzb_grid_publish_level(lzb_grid* g, int level, const double* mats, const int32_t* n, int32_t p1) {
+    return guarded([&] { g->g->publish_level(level, mats, n, p1); });
 }
 int lzb_grid_invalidate(lzb_grid* g) {
     return guarded([&] { g->g->invalidate(); });
