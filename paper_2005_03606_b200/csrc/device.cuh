@@ -26,7 +26,13 @@ __host__ __device__ inline int cdy(int c) { return c >> 1; }  // types.hpp:15
 //   sinusoid: 1.0 + ((amp * sx) * sy),   sx = sin(freq pi x)
 //   quadrant: (x >= c) == (y >= c) ? 1 : eps_low
 //   checker:  T[min(B-1, int(B x))][min(B-1, int(B y))]
-__device__ inline double field_xpart(const lzb_field& f, double x) {
+// The transcendental parts (exp, cos, sin) are evaluated on the HOST for every
+// table the kernels read (host_field_parts, runtime.cu): the reference's libm
+// (glibc, x86-64) gives the bits, so the EXACT paths are bit-identical to the
+// reference on every field, not only on the polynomial ones. The device
+// evaluation below remains for arbitrary boxes (lzb_integrate_elements) and
+// the off-lockstep adaptive steps of the concurrent mode.
+__host__ __device__ inline double field_xpart(const lzb_field& f, double x) {
     switch (f.kind) {
         case LZB_FIELD_THETA: {
             const double amplitude = 0.3 / 2.0;
@@ -42,7 +48,7 @@ __device__ inline double field_xpart(const lzb_field& f, double x) {
         default: return 0.0;
     }
 }
-__device__ inline double field_ypart(const lzb_field& f, double y) {
+__host__ __device__ inline double field_ypart(const lzb_field& f, double y) {
     switch (f.kind) {
         case LZB_FIELD_THETA: return exp(-f.theta * y) * cos(kPi * f.theta * y);
         case LZB_FIELD_QUADRANT: return y >= kQuadCentre ? 1.0 : 0.0;
@@ -54,7 +60,7 @@ __device__ inline double field_ypart(const lzb_field& f, double y) {
         default: return 0.0;
     }
 }
-__device__ inline double field_combine(const lzb_field& f, double xp, double yp) {
+__host__ __device__ inline double field_combine(const lzb_field& f, double xp, double yp) {
     switch (f.kind) {
         case LZB_FIELD_THETA:
         case LZB_FIELD_SINUSOID: return 1.0 + xp * yp;
@@ -541,6 +547,12 @@ struct LevelView {
     uint32_t* dirty;
     uint8_t* pend;
     uint32_t* pdirty;
+    // host-evaluated centre parts of the field (the n = 1 sample of cell
+    // (cx, cy): field_combine(f, cex[cx], cey[cy])) and, on the leaf level,
+    // sin(pi ix / 3^l) of the BASELINE load f = s sin(pi x) sin(pi y)
+    const double* cex;
+    const double* cey;
+    const double* rsin;
 };
 
 __device__ inline int32_t crank(const LevelView& L, int cx, int cy) { return L.rx[cx] + L.ry[cy]; }

@@ -57,9 +57,9 @@ __device__ inline int64_t gtid() { return blockIdx.x * static_cast<int64_t>(bloc
 __device__ inline double baseline_entry(int k, double e) { return 0.0 + c_kunit[k] * e; }
 
 __device__ inline double centre_eps(const lzb_field& f, const LevelView& L, int cx, int cy) {
-    // integrate_element(box, eps, 1): sample at x0 + ((0+0.5)*1.0)*h (element.hpp:44)
-    double x0 = cx * L.h, y0 = cy * L.h;
-    return field_eval(f, x0 + (0 + 0.5) * 1.0 * L.h, y0 + (0 + 0.5) * 1.0 * L.h);
+    // integrate_element(box, eps, 1): the sample at x0 + ((0+0.5)*1.0)*h
+    // (element.hpp:44), its axis parts evaluated on the host (Level::cex/cey)
+    return field_combine(f, L.cex[cx], L.cey[cy]);
 }
 
 __device__ inline const double* transfer_of(const LevelView& C, int c) {
@@ -811,8 +811,8 @@ __global__ void k_init_rhs(LevelView F, lzb_rhs rhs, double w) {
             int cx = ix - dx, cy = iy - dy;
             adj += (cx >= 0 && cy >= 0 && cx < F.N && cy < F.N);
         }
-    double x = ix / F.pow3l, y = iy / F.pow3l;
-    double fv = rhs.kind == LZB_RHS_SINPROD ? rhs.value * sin(kPi * x) * sin(kPi * y) : rhs.value;
+    // rsin[i] = sin(pi * (i / 3^l)) from the host libm (Grid constructor)
+    double fv = rhs.kind == LZB_RHS_SINPROD ? rhs.value * F.rsin[ix] * F.rsin[iy] : rhs.value;
     double term = w * fv, fl = 0.0;
     for (int k = 0; k < adj; ++k) fl += term;
     F.v[LZB_V_FL][vi] = fl;
@@ -2242,6 +2242,7 @@ struct Level {
     DevBuf<int8_t> cp3;
     DevBuf<uint32_t> dirty;  // refined levels, coarse-recompute = ripple
     DevBuf<uint8_t> pend;
+    DevBuf<double> cex, cey, rsin;  // host-libm centre parts; leaf-level load sines
     LevelView view(int depth) const {
         LevelView L{};
         L.N = N;
@@ -2265,6 +2266,9 @@ struct Level {
         L.cp3 = cp3.p;
         L.dirty = dirty.p;
         L.pend = pend.p;
+        L.cex = cex.p;
+        L.cey = cey.p;
+        L.rsin = rsin.p;
         return L;
     }
 };
@@ -2327,15 +2331,28 @@ public:
                 LZB_CUDA(cudaMemsetAsync(L.P.p, 0, L.P.bytes(), s_));
             }
         }
-        // centre field parts (the n = 1 sample) of the patch and leaf levels
+        // centre field parts (the n = 1 sample) of every level, host libm; the
+        // patch and leaf levels' also as centre_ (read by the pack / residual kernels)
+        for (int l = 0; l <= D_; ++l) {
+            Level& L = L_[l];
+            L.cex.alloc(L.N);
+            L.cey.alloc(L.N);
+            upload_field_parts(d.field, L.N, L.h, 1, L.cex.p, L.cey.p, s_);
+        }
         for (int k = 0; k < 2; ++k) {
             const Level& L = L_[D_ - 1 + k];
             centre_[k].x.alloc(L.N);
             centre_[k].y.alloc(L.N);
-            LZB_LAUNCH(k_field_parts, blocks_for(L.N, kThreads), kThreads, 0, s_, d.field, L.N, L.h, 1, 0,
-                       centre_[k].x.p);
-            LZB_LAUNCH(k_field_parts, blocks_for(L.N, kThreads), kThreads, 0, s_, d.field, L.N, L.h, 1, 1,
-                       centre_[k].y.p);
+            LZB_CUDA(cudaMemcpyAsync(centre_[k].x.p, L.cex.p, L.cex.bytes(), cudaMemcpyDeviceToDevice, s_));
+            LZB_CUDA(cudaMemcpyAsync(centre_[k].y.p, L.cey.p, L.cey.bytes(), cudaMemcpyDeviceToDevice, s_));
+        }
+        {  // sin(pi x) of the leaf vertices for the BASELINE load (k_init_rhs)
+            Level& L = L_[D_];
+            std::vector<double> sv(static_cast<size_t>(L.N) + 1);
+            for (int i = 0; i <= L.N; ++i) sv[i] = std::sin(kPi * (i / L.pow3l));
+            L.rsin.alloc(sv.size());
+            LZB_CUDA(cudaMemcpyAsync(L.rsin.p, sv.data(), sv.size() * sizeof(double), cudaMemcpyHostToDevice, s_));
+            LZB_CUDA(cudaStreamSynchronize(s_));
         }
         leaves_ = L_[D_].nc;
         list_.alloc(leaves_);

@@ -32,6 +32,10 @@ struct TableSet {
     void build(const lzb_field& f, int N, double h, int n, cudaStream_t s);
     IntTables view() const { return IntTables{fx.p, fy.p, seg.p, ktab.p, cxp.p, cyp.p, n}; }
 };
+// Host-libm field parts of the N cells' n samples per axis (k_field_parts
+// arithmetic) and their upload to device arrays on stream s.
+void host_field_parts(const lzb_field& f, int N, double h, int n, int axis, double* out);
+void upload_field_parts(const lzb_field& f, int N, double h, int n, double* dx, double* dy, cudaStream_t s);
 template <typename K>
 void set_smem(K kernel, size_t bytes);
 void host_kunit(double* out16);

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <mutex>
+#include <vector>
 
 #include "engine.hpp"
 #include "kernels.cuh"
@@ -118,6 +119,29 @@ __global__ void k_ksub_table(int n, double* ktab) {
     o[5] = k.k23; o[6] = k.k02; o[7] = k.k13; o[8] = k.k03; o[9] = 0.0;
 }
 
+void host_field_parts(const lzb_field& f, int N, double h, int n, int axis, double* out) {
+    // the same arithmetic as k_field_parts (cell_box element.hpp:29-32, the
+    // sample element.hpp:44), the transcendentals from the host libm
+    const double inv = 1.0 / n;
+    for (int c = 0; c < N; ++c) {
+        const double x0 = c * h;
+        for (int i = 0; i < n; ++i) {
+            const double x = x0 + (i + 0.5) * inv * h;
+            out[static_cast<int64_t>(c) * n + i] = axis == 0 ? field_xpart(f, x) : field_ypart(f, x);
+        }
+    }
+}
+
+void upload_field_parts(const lzb_field& f, int N, double h, int n, double* dx, double* dy, cudaStream_t s) {
+    std::vector<double> hx(static_cast<size_t>(N) * n), hy(static_cast<size_t>(N) * n);
+    host_field_parts(f, N, h, n, 0, hx.data());
+    host_field_parts(f, N, h, n, 1, hy.data());
+    // pageable source: the call returns once the bytes are staged
+    LZB_CUDA(cudaMemcpyAsync(dx, hx.data(), hx.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    LZB_CUDA(cudaMemcpyAsync(dy, hy.data(), hy.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    LZB_CUDA(cudaStreamSynchronize(s));
+}
+
 void TableSet::build(const lzb_field& f, int N_, double h, int n_, cudaStream_t s) {
     size_t nf = static_cast<size_t>(N_) * n_;
     if (fx.n < nf) {
@@ -138,12 +162,10 @@ void TableSet::build(const lzb_field& f, int N_, double h, int n_, cudaStream_t 
         cxp.alloc(N_);
         cyp.alloc(N_);
     }
-    // cell-centre parts: the n = 1 sample, x0 + ((0+0.5)*1.0)*h (element.hpp:44)
-    LZB_LAUNCH(k_field_parts, blocks_for(N_, 256), 256, 0, s, f, N_, h, 1, 0, cxp.p);
-    LZB_LAUNCH(k_field_parts, blocks_for(N_, 256), 256, 0, s, f, N_, h, 1, 1, cyp.p);
-    unsigned g = blocks_for(static_cast<int64_t>(nf), 256);
-    LZB_LAUNCH(k_field_parts, g, 256, 0, s, f, N_, h, n_, 0, fx.p);
-    LZB_LAUNCH(k_field_parts, g, 256, 0, s, f, N_, h, n_, 1, fy.p);
+    // cell-centre parts: the n = 1 sample, x0 + ((0+0.5)*1.0)*h (element.hpp:44);
+    // sample parts at n -- host libm (see field_xpart)
+    upload_field_parts(f, N_, h, 1, cxp.p, cyp.p, s);
+    upload_field_parts(f, N_, h, n_, fx.p, fy.p, s);
     LZB_LAUNCH(k_seg_table, blocks_for(n_, 128), 128, 0, s, n_, seg.p);
     LZB_LAUNCH(k_ksub_table, blocks_for(static_cast<int64_t>(n_) * n_, 256), 256, 0, s, n_, ktab.p);
     n = n_;
