@@ -135,6 +135,17 @@ typedef struct lzb_grid_desc {
                                  plane_width bytes per entry; wider records fall back to FP64) */
     int32_t fixed_p3;         /* 0: choose_precision per leaf record; 2..8: every leaf record
                                  at this width (the mantissa-width sweep, BASELINE configs[4]) */
+    int32_t start_geometric;  /* 1: a leaf not yet integrated (p1 = bottom) reads the geometric
+                                 stencil (eps = 1) instead of its n = 1 sample, and in anarchic
+                                 mode its first integration is deferred to a task too -- the
+                                 "delayed assembly starting from the geometric stencil" of
+                                 BASELINE configs[1]; 0: the reference start (assembly.cpp:26-33,
+                                 stream.cpp:82-84). The codec baseline stays A(n = 1). */
+    int32_t forced_n;         /* spawn_forced sub-sample count (forced-task-n, experiment.hpp:56) */
+    double forced_fraction;   /* forced-task-fraction (experiment.hpp:55, experiment.cpp:260-270):
+                                 at every cycle start the leaves whose roll
+                                 splitmix64(0x6f4ce1a3 ^ cell id) falls below it get a forced
+                                 integrate task (Assembler::spawn_forced, assembly.cpp:138-154) */
 } lzb_grid_desc;
 
 /* CycleReport, solver.hpp:41-61 (field for field). */

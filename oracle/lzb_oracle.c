@@ -593,6 +593,7 @@ static void baseline(const orc_grid* g, int l, int cx, int cy, double* out) {
 static void element_or_baseline(const orc_grid* g, int l, int c, double* out) {
     const orc_level* L = &g->L[l];
     if (L->p1[c] != LZB_P1_BOTTOM) memcpy(out, L->op + 16 * c, 128);
+    else if (g->d.start_geometric) memcpy(out, g->kunit, 128); /* extension: the geometric stencil (eps = 1) */
     else baseline(g, l, c % L->N, c / L->N, out);
 }
 static const double* transfer_or_geometric(const orc_grid* g, int l, int c) {
@@ -756,6 +757,15 @@ static void spawn(orc_grid* g, int c) {
     g->spawned++;
 }
 
+/* Assembler::spawn_forced (assembly.cpp:138-154): an integrate task that only
+ * occupies the pool (its result is discarded); queued as -(c + 1). */
+static void spawn_forced(orc_grid* g, int c) {
+    orc_level* L = &g->L[g->D];
+    if (L->p2[c]) return; /* assembly.cpp:140 */
+    spawn(g, c);
+    g->queue[g->qtail - 1] = -c - 1;
+}
+
 /* A coarse_recompute task (solver.cpp:86-90) in the high-priority class. */
 static void spawn_coarse(orc_grid* g, int l, int c) {
     if (g->htail + 2 > g->hcap) {
@@ -793,7 +803,9 @@ static void* pre_worker(void* arg) {
     pre_job* j = (pre_job*)arg;
     const orc_level* L = &j->g->L[j->g->D];
     for (int64_t k = j->k0; k < j->k1; ++k) {
-        int c = j->cells[k], p1 = L->p1[c];
+        int c = j->cells[k];
+        if (c < 0) continue; /* a forced task */
+        int p1 = L->p1[c];
         if (p1 == LZB_P1_TOP || p1 == LZB_P1_BOTTOM) continue;
         if (j->g->d.n_max > 0 && p1 >= j->g->d.n_max) continue;
         orc_integrate_element(&j->g->d.field, (c % L->N) * L->h, (c / L->N) * L->h, L->h, next_n(j->g, p1),
@@ -842,8 +854,12 @@ static int pool_begin_cycle(orc_grid* g) {
         } else {
             int64_t k = g->qhead - qbase;
             int c = g->queue[g->qhead++];
-            rc = adaptive_step_pre(g, c, pre && k < nleaf ? pre + 16 * k : NULL);
-            g->L[g->D].p2[c] = 0;
+            if (c < 0) { /* spawn_forced's task: integrate_element(box, eps, fixed_n), result discarded */
+                g->L[g->D].p2[-c - 1] = 0;
+            } else {
+                rc = adaptive_step_pre(g, c, pre && k < nleaf ? pre + 16 * k : NULL);
+                g->L[g->D].p2[c] = 0;
+            }
         }
         g->completed++;
         if (rc) {
@@ -853,6 +869,29 @@ static int pool_begin_cycle(orc_grid* g) {
     }
     free(pre);
     return 0;
+}
+
+/* TaskPool::try_run_one (scheduler.cpp:113-128): the oldest task, high class
+ * first, regardless of the cycle budget */
+static int try_run_one(orc_grid* g) {
+    int rc = 0;
+    if (g->hhead < g->htail) {
+        int l = g->hq[g->hhead], c = g->hq[g->hhead + 1], pub;
+        g->hhead += 2;
+        rc = recompute_coarse(g, l, c, &pub);
+    } else if (g->qhead < g->qtail) {
+        int c = g->queue[g->qhead++];
+        if (c < 0) {
+            g->L[g->D].p2[-c - 1] = 0;
+        } else {
+            rc = adaptive_step(g, c);
+            g->L[g->D].p2[c] = 0;
+        }
+    } else {
+        return 0;
+    }
+    g->completed++;
+    return rc;
 }
 
 /* assembly.cpp:76-109 */
@@ -866,10 +905,18 @@ static int request_stencil(orc_grid* g, int c) {
                 if ((rc = adaptive_step(g, c))) return rc;
             return 0;
         case LZB_ADAPTIVE:
-            /* p2 is never set outside anarchic mode with workers = 1 */
+            /* block while a task of this cell is queued, running queued work
+             * (assembly.cpp:86-93); only forced tasks set p2 in this mode */
+            while (L->p2[c])
+                if ((rc = try_run_one(g))) return rc;
             if (L->p1[c] != LZB_P1_TOP) rc = adaptive_step(g, c);
             return rc;
         case LZB_ANARCHIC:
+            if (L->p1[c] == LZB_P1_BOTTOM && g->d.start_geometric) {
+                /* extension: the first integration is deferred too */
+                if (!L->p2[c]) spawn(g, c);
+                return 0;
+            }
             if (L->p1[c] == LZB_P1_BOTTOM) {
                 if ((rc = adaptive_step(g, c))) return rc;
                 spawn(g, c);
@@ -1309,6 +1356,16 @@ int orc_step(orc_grid* g, lzb_cycle_report* rep) {
     int rc = pool_begin_cycle(g);
     if (rc) return rc;
     rep->cycle = (int32_t)g->cycle;
+    if (g->d.forced_fraction > 0.0) { /* on_cycle_start of run_experiment, experiment.cpp:260-270 */
+        orc_level* L = &g->L[g->D];
+        int64_t id0 = 0; /* cell ids: level by level in creation order (mesh.cpp:66-102, 253-272) */
+        for (int l = 0; l < g->D; ++l) id0 += (int64_t)g->L[l].N * g->L[l].N;
+        for (int64_t q = 0; q < (int64_t)L->N * L->N; ++q) {
+            uint64_t id = (uint64_t)(id0 + q);
+            double roll = (double)(orc_splitmix64(0x6f4ce1a3ull ^ id) >> 11) * 0x1.0p-53;
+            if (roll < g->d.forced_fraction) spawn_forced(g, L->order[q]);
+        }
+    }
     if ((rc = walk(g, 0, 0, 0, visit_assembly, NULL))) return rc;
     rep->residual = residual_pass(g);
     if (g->first_residual < 0.0) g->first_residual = rep->residual > 0.0 ? rep->residual : 1.0;

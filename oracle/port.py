@@ -150,6 +150,9 @@ def desc_from_keys(k: dict) -> T.GridDesc:
     d.throttle = int(k["throttle"])
     d.noise_seed = int(k["seed"])
     d.boundary_value = 0.0
+    d.start_geometric = 1 if k.get("start", "sample") == "geometric" else 0
+    d.forced_fraction = float(k.get("forced-task-fraction", "0"))
+    d.forced_n = int(k.get("forced-task-n", "8"))
     return d
 
 

@@ -110,7 +110,20 @@ struct Rig {
           pool(c.scheduler_config()),
           assembler(stream, c.assembly_config(), pool),
           solver(mesh, stream, assembler, pool, problem, c.solver_config(),
-                 c.multilevel_config()) {}
+                 c.multilevel_config()) {
+        // run_experiment's forced-task workload hook (experiment.cpp:260-270),
+        // installed the same way through the public on_cycle_start member
+        if (cfg.forced_task_fraction > 0.0) {
+            solver.on_cycle_start = [this] {
+                for (std::size_t id = 0; id < mesh.cell_count(); ++id) {
+                    const Cell& cell = mesh.cell(static_cast<int32_t>(id));
+                    if (cell.refined) continue;
+                    const double roll = static_cast<double>(splitmix64(0x6f4ce1a3u ^ id) >> 11) * 0x1.0p-53;
+                    if (roll < cfg.forced_task_fraction) assembler.spawn_forced(cell.id, cfg.forced_task_n);
+                }
+            };
+        }
+    }
 };
 
 void fill_report(const CycleReport& r, lzb_cycle_report* o) {

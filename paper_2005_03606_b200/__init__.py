@@ -362,7 +362,8 @@ def make_desc(depth=2, field: Field | None = None, rhs: float = 0.0, rhs_kind="c
               rhs_scale=2 * np.pi ** 2, delta_max=1e-8, solver="adafac-pi", omega=0.7, target=1e-10,
               divergence=1e2, max_cycles=500, assembly="adaptive", termination_c=0.01, schedule="increment",
               n_max=0, integration="exact", transfer="geometric", gating=True, throttle=0, seed=0,
-              concurrent=False, plane_width=0, fixed_p3=0) -> GridDesc:
+              concurrent=False, plane_width=0, fixed_p3=0, start_geometric=False, forced_fraction=0.0,
+              forced_n=8) -> GridDesc:
     d = GridDesc()
     d.dim = 2
     d.depth = depth
@@ -386,6 +387,9 @@ def make_desc(depth=2, field: Field | None = None, rhs: float = 0.0, rhs_kind="c
     d.noise_seed = seed
     d.plane_width = plane_width
     d.fixed_p3 = fixed_p3
+    d.start_geometric = 1 if start_geometric else 0
+    d.forced_fraction = forced_fraction
+    d.forced_n = forced_n
     return d
 
 

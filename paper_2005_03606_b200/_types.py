@@ -86,6 +86,9 @@ class GridDesc(C.Structure):
         ("boundary_value", C.c_double),
         ("plane_width", C.c_int32),
         ("fixed_p3", C.c_int32),
+        ("start_geometric", C.c_int32),
+        ("forced_n", C.c_int32),
+        ("forced_fraction", C.c_double),
     ]
 
 

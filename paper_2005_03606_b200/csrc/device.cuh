@@ -19,6 +19,14 @@ constexpr double kQuadCentre = 0.5 + 1.0 / (2.0 * 2187.0);
 __host__ __device__ inline int cdx(int c) { return c & 1; }   // types.hpp:14
 __host__ __device__ inline int cdy(int c) { return c >> 1; }  // types.hpp:15
 
+// problem.cpp:43-48
+__host__ __device__ inline uint64_t splitmix64(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
 // ------------------------------------------------------------------ eps parts
 // eps(x, y) = combine(xpart(x), ypart(y)) reproduces the reference expression
 // tree exactly (problem.cpp:9-31 for kinds 0-2; BASELINE kinds 3-4):
@@ -553,6 +561,9 @@ struct LevelView {
     const double* cex;
     const double* cey;
     const double* rsin;
+    // desc.start_geometric on the leaf level: a cell at p1 = bottom reads the
+    // geometric stencil (eps = 1) instead of its n = 1 sample
+    int geo0;
 };
 
 __device__ inline int32_t crank(const LevelView& L, int cx, int cy) { return L.rx[cx] + L.ry[cy]; }

@@ -69,6 +69,7 @@ struct ExperimentConfig {
     std::string schedule = "increment";
     int n_max = 0;
     std::string integration = "exact";
+    std::string start = "sample";  // "geometric": BASELINE configs[1]'s eps = 1 start
     int device = 0;
 
     std::map<std::string, std::string> to_keys() const {
@@ -113,6 +114,7 @@ struct ExperimentConfig {
         if (schedule != d.schedule) k["schedule"] = schedule;
         if (n_max != d.n_max) k["n-max"] = std::to_string(n_max);
         if (integration != d.integration) k["integration"] = integration;
+        if (start != d.start) k["start"] = start;
         return k;
     }
 
@@ -163,6 +165,7 @@ struct ExperimentConfig {
             else if (key == "schedule") schedule = value;
             else if (key == "n-max") n_max = std::stoi(value);
             else if (key == "integration") integration = value;
+            else if (key == "start") start = value;
             else if (key == "device") device = std::stoi(value);
             else throw Fail(LZB_ERR_IO, "unknown config key: " + key);
         } catch (const std::invalid_argument&) {
@@ -242,6 +245,11 @@ struct ExperimentConfig {
         d.throttle = throttle;
         d.noise_seed = seed;
         d.boundary_value = 0.0;
+        if (start == "geometric") d.start_geometric = 1;
+        else if (start != "sample") throw Fail(LZB_ERR_IO, "unknown start: " + start);
+        // run_experiment's forced-task hook (experiment.cpp:260-270) on the device
+        d.forced_fraction = forced_task_fraction;
+        d.forced_n = forced_task_n;
         return d;
     }
 };
@@ -322,8 +330,6 @@ void check(int rc) {
 int run(const ExperimentConfig& cfg) {
     if (cfg.amr)
         throw Fail(LZB_ERR_INVALID, "amr = on: adaptive refinement is not on the device path (SURVEY §8f)");
-    if (cfg.forced_task_fraction > 0.0)
-        throw Fail(LZB_ERR_INVALID, "forced-task workload emulation is not on the device path");
     lzb_grid_desc d = cfg.desc();
     Ctx ctx;
     check(lzb_ctx_create(cfg.device, &ctx.c));

@@ -77,7 +77,7 @@ __device__ inline void element_or_baseline(const lzb_field& f, const LevelView& 
             K[2 * k + 1] = t.y;
         }
     } else {
-        double e = centre_eps(f, L, cx, cy);
+        double e = L.geo0 ? 1.0 : centre_eps(f, L, cx, cy);
         for (int k = 0; k < 16; ++k) K[k] = baseline_entry(k, e);
     }
 }
@@ -208,11 +208,18 @@ __device__ inline bool publish_leaf_k9(const LevelView& F, int c, const double* 
 // Order-preserving compaction of the selected leaves (ascending cell index,
 // so a block of list entries covers few cell rows): count per block, scan,
 // scatter. selector: 0 unconverged, 1 tasks (p2 set, FIFO key <= limit), 2 bottom.
+// p2 = 1: a step task (spawn_step_task); p2 = 2: a forced task (spawn_forced),
+// listed with snap = kForcedSnap so that no step kernel takes it.
+constexpr int32_t kForcedSnap = INT32_MIN;
 __device__ inline bool selected(const LevelView& F, int64_t c, int selector, const long long* keys,
                                 long long key_limit, int32_t& p1) {
     p1 = F.p1[c];
     if (selector == 0) return p1 != LZB_P1_TOP;
-    if (selector == 1) return F.p2[c] != 0 && (!keys || keys[c] <= key_limit);  // a task on a top cell still completes
+    if (selector == 1) {
+        const uint8_t t = F.p2[c];
+        if (t == 2) p1 = kForcedSnap;
+        return t != 0 && (!keys || keys[c] <= key_limit);  // a task on a top cell still completes
+    }
     return p1 == LZB_P1_BOTTOM;
 }
 
@@ -294,18 +301,21 @@ __global__ void k_compact_scatter(LevelView F, int selector, const long long* ke
         int pos = warp_off[w] + __popc(mask & ((1u << lane) - 1));
         list[pos] = static_cast<int32_t>(c);
         snap[pos] = p1;
-        int bin = p1 == LZB_P1_TOP ? kNHist - 1 : (p1 < kNHist - 1 ? p1 : kNHist - 1);
-        atomicAdd(&hist[bin], 1u);
+        if (p1 != kForcedSnap) {
+            int bin = p1 == LZB_P1_TOP ? kNHist - 1 : (p1 < kNHist - 1 ? p1 : kNHist - 1);
+            atomicAdd(&hist[bin], 1u);
+        }
     }
 }
 
 // p1 = bottom -> integrate with n = 1, publish, p1 = 1 (assembly.cpp:26-34).
+// count_ptr: the count on the device (concurrent batches), else `count`.
 __global__ void k_bottom(LevelView F, lzb_field f, const int32_t* list, const int32_t* snap,
-                         int count, double delta_max, uint32_t cycle, int clear_p2,
+                         int count, const int* count_ptr, double delta_max, uint32_t cycle, int clear_p2,
                          unsigned long long* stats, int* err) {
     lzb_pdl_enter();
     int64_t t = gtid();
-    if (t >= count || snap[t] != LZB_P1_BOTTOM) return;
+    if (t >= (count_ptr ? *count_ptr : count) || snap[t] != LZB_P1_BOTTOM) return;
     int c = list[t], cx = c % F.N, cy = c / F.N;
     double e = centre_eps(f, F, cx, cy), m[16];
     for (int k = 0; k < 16; ++k) m[k] = baseline_entry(k, e);
@@ -393,13 +403,48 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_step(LevelView F, LevelView 
 
 // Anarchic request_stencil for non-bottom leaves: spawn if not top and not in
 // flight (assembly.cpp:95-106); key = FIFO position (spawn cycle, pre-order).
+// Keys: cycle k's forced tasks (spawned at cycle start) precede its step tasks
+// (spawned by the assembly pass): 2k and 2k + 1 blocks of leaf_count.
 __global__ void k_spawn(LevelView F, uint32_t cycle, long long leaf_count, long long* keys) {
     lzb_pdl_enter();
     int64_t c = gtid();
     if (c >= static_cast<int64_t>(F.N) * F.N) return;
     if (F.p1[c] == LZB_P1_TOP || F.p2[c]) return;
     F.p2[c] = 1;
-    if (keys) keys[c] = static_cast<long long>(cycle) * leaf_count + crank(F, c % F.N, c / F.N);
+    if (keys) keys[c] = (2ll * cycle + 1) * leaf_count + crank(F, c % F.N, c / F.N);
+}
+
+// run_experiment's on_cycle_start (experiment.cpp:260-270): a forced task for
+// every leaf whose roll splitmix64(0x6f4ce1a3 ^ id) * 2^-53 is below the
+// fraction, unless a task of the cell is in flight (Assembler::spawn_forced,
+// assembly.cpp:138-154). Cell ids are level by level in creation order, so a
+// leaf's id is id0 + its creation rank.
+__global__ void k_spawn_forced(LevelView F, uint32_t cycle, long long leaf_count, long long* keys,
+                               long long id0, double fraction) {
+    lzb_pdl_enter();
+    int64_t c = gtid();
+    if (c >= static_cast<int64_t>(F.N) * F.N) return;
+    const long long rank = crank(F, static_cast<int>(c % F.N), static_cast<int>(c / F.N));
+    const double roll = static_cast<double>(splitmix64(0x6f4ce1a3ull ^ static_cast<uint64_t>(id0 + rank)) >> 11) *
+                        0x1.0p-53;
+    if (!(roll < fraction) || F.p2[c]) return;
+    F.p2[c] = 2;
+    keys[c] = 2ll * cycle * leaf_count + rank;
+}
+
+// A forced task's body: integrate_element(box, eps, fixed_n) whose result only
+// feeds a sink (workload emulation; the markers are untouched).
+__global__ void k_forced_work(LevelView F, lzb_field f, const int32_t* list, const int32_t* snap, int count,
+                              int n, double* sink) {
+    lzb_pdl_enter();
+    int64_t t = gtid();
+    if (t >= count || snap[t] != kForcedSnap) return;
+    const int c = list[t];
+    double m[16];
+    integrate_cell(f, (c % F.N) * F.h, (c / F.N) * F.h, F.h, n, 0, m);
+    double mx = 0.0;
+    for (int k = 0; k < 16; ++k) mx = fmax(mx, fabs(m[k]));
+    if (mx == -1.0) sink[0] = mx;  // never taken; keeps the integration live
 }
 
 // A rectangle of leaf cells [x0, x0 + w) x [y0, ...): the fixed-p kernels
@@ -910,7 +955,7 @@ __device__ __forceinline__ void k_residual_body(int64_t lin, LevelView F, lzb_fi
         const int a = q & 1, b = q >> 1, row = (1 - a) + 2 * (1 - b);
         double Kr[4] = {k01[q].x, k01[q].y, k23[q].x, k23[q].y};
         if (has[q] && p1[q] == LZB_P1_BOTTOM) {
-            const double e = centre_eps(f, F, ix - 1 + a, iy - 1 + b);
+            const double e = F.geo0 ? 1.0 : centre_eps(f, F, ix - 1 + a, iy - 1 + b);
             for (int col = 0; col < 4; ++col) Kr[col] = baseline_entry(row * 4 + col, e);
         }
         double s = 0.0, sh = 0.0;
@@ -1032,7 +1077,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_residual_comp(LevelView F, lzb_
         const double e = field_combine(f, a ? ex1 : ex0, b ? ey1 : ey0);  // ε(centre), the n = 1 sample
         double Kr[4];
         if (cp[q] < 0) {
-            for (int col = 0; col < 4; ++col) Kr[col] = baseline_entry(row * 4 + col, e);
+            for (int col = 0; col < 4; ++col) Kr[col] = baseline_entry(row * 4 + col, F.geo0 ? 1.0 : e);
         } else if (cp[q] <= W) {
             const PlaneDec dec(cp[q]);
 #pragma unroll
@@ -2088,7 +2133,7 @@ __global__ void k_step_generic(LevelView F, LevelView D, lzb_field f, const int3
     int64_t t = gtid();
     if (t >= *count_ptr) return;
     const int32_t p1 = snap[t];
-    if (p1 == n_main || p1 == LZB_P1_BOTTOM) return;  // main kernel / inline bottom round
+    if (p1 == n_main || p1 == LZB_P1_BOTTOM || p1 == kForcedSnap) return;  // main kernel / bottoms / forced
     const int c = list[t], cx = c % F.N, cy = c / F.N;
     if (p1 == LZB_P1_TOP || (n_max > 0 && p1 >= n_max)) {
         D.p1[c] = LZB_P1_TOP;
@@ -2384,7 +2429,14 @@ public:
         }
         res_.alloc(1);
         LZB_CUDA(cudaMemsetAsync(res_.p, 0, sizeof(Result), s_));
-        if (d.throttle) keys_.alloc(leaves_);
+        if (d.forced_fraction > 0.0) {
+            if (d.concurrent) throw Error(LZB_ERR_INVALID, "forced tasks need the deterministic modes (workers = 1)");
+            if (d.mode == LZB_ADAPTIVE && d.policy == LZB_RIPPLE)
+                throw Error(LZB_ERR_INVALID, "forced tasks with assembly = adaptive need coarse-recompute = always");
+            if (d.forced_n < 1) throw Error(LZB_ERR_INVALID, "forced-task-n must be >= 1");
+            sink_.alloc(1);
+        }
+        if (d.throttle || d.forced_fraction > 0.0) keys_.alloc(leaves_);
         if (d.concurrent) {
             if (d.mode != LZB_ANARCHIC)
                 throw Error(LZB_ERR_INVALID, "concurrent assembly needs assembly = anarchic");
@@ -2474,6 +2526,7 @@ public:
         if (l == D_) {
             v.cw = d_.plane_width;
             v.fixed_p3 = d_.fixed_p3;
+            v.geo0 = d_.start_geometric;
         }
         if (l > 0) v.pdirty = L_[l - 1].dirty.p;  // nullptr unless ripple
         if (uhat_is_u_) v.v[LZB_V_UHAT] = v.v[LZB_V_U];  // V-cycle: u-hat = u without a copy
@@ -2553,6 +2606,12 @@ public:
             atables_.build(d_.field, L_[D_].N, L_[D_].h, nn, a_);
         const bool fast = d_.integration == LZB_INTEGRATE_FAST;
         unsigned long long* stats = res_.p->s;
+        // geometric start: the first batch holds the deferred bottom -> 1 steps
+        const bool bottoms = d_.start_geometric && batches_launched_ == 0;
+        if (bottoms)
+            LZB_LAUNCH(k_bottom, blocks_for(leaves_, kThreads), kThreads, 0, a_, staging(), d_.field, alist_.p,
+                       asnap_.p, static_cast<int>(leaves_), static_cast<const int*>(acounter_.p), d_.delta_max,
+                       cycle_, 0, stats, ctx_->err.p);
         dispatch_step(fast, a_, V(D_), staging(), d_.field, alist_.p, asnap_.p, acounter_.p, leaves_, n, nn,
                       cap, atables_.view(), d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p);
         LZB_LAUNCH(k_step_generic, blocks_for(leaves_, kThreads), kThreads, 0, a_, V(D_), staging(), d_.field,
@@ -2560,7 +2619,7 @@ public:
                    d_.delta_max, cycle_, stats, ctx_->err.p);
         LZB_CUDA(cudaEventRecord(ev_batch_, a_));
         batch_inflight_ = true;
-        batch_n_ = cap ? n : nn;
+        if (!bottoms) batch_n_ = cap ? n : nn;
         ++batches_launched_;
     }
 
@@ -2585,7 +2644,7 @@ public:
     void drain() {
         if (d_.concurrent) try_commit(true);
         if (ripple()) ripple_tasks();  // the high class first (scheduler.cpp:125-141)
-        if (d_.mode == LZB_ANARCHIC) {
+        if (d_.mode == LZB_ANARCHIC || d_.forced_fraction > 0.0) {
             while (count_pending() > 0) round(1, true);
         }
         pending_ = count_pending();
@@ -2605,7 +2664,11 @@ public:
         unsigned long long* stats = res_.p->s;
         if (hhist_[0])
             LZB_LAUNCH(k_bottom, blocks_for(count, kThreads), kThreads, 0, s_, F, d_.field, list_.p,
-                       snap_.p, count, d_.delta_max, cycle_, 0, stats, ctx_->err.p);
+                       snap_.p, count, static_cast<const int*>(nullptr), d_.delta_max, cycle_, 0, stats,
+                       ctx_->err.p);
+        if (d_.forced_fraction > 0.0 && selector == 1)  // forced tasks: the integration, discarded
+            LZB_LAUNCH(k_forced_work, blocks_for(count, 128), 128, 0, s_, F, d_.field, list_.p, snap_.p, count,
+                       d_.forced_n, sink_.p);
         for (int n = 1; n < kNHist - 1; ++n) {
             if (!hhist_[n]) continue;
             bool cap = d_.n_max > 0 && n >= d_.n_max;
@@ -2731,7 +2794,8 @@ public:
     }
 
     void pool_begin_cycle() {  // TaskPool::begin_cycle, workers = 1 (scheduler.cpp:88-111)
-        if (d_.mode != LZB_ANARCHIC || pending_ == 0) return;
+        // step tasks (anarchic) and forced tasks (any mode) are the leaf tasks
+        if (pending_ == 0 || (d_.mode != LZB_ANARCHIC && d_.forced_fraction <= 0.0)) return;
         long long limit = -1;
         if (d_.throttle && static_cast<uint64_t>(pending_) > d_.throttle) {
             // FIFO: only the `throttle` oldest spawns run this cycle
@@ -2788,6 +2852,11 @@ public:
     // round has found every leaf converged (p1 = top) nothing can change until a
     // publish / load / adaptive_step, so the compaction is skipped.
     void leaves_pass() {
+        // adaptive_sync request_stencil runs queued work while the cell's task is
+        // in flight (assembly.cpp:86-93): every queued task (only forced tasks
+        // exist in this mode) has run by the end of the pass, and none changes a
+        // marker, so they run first
+        if (d_.mode == LZB_ADAPTIVE && d_.forced_fraction > 0.0) round(1, true);
         if (all_top_) return;
         switch (d_.mode) {
             case LZB_EAGER:
@@ -2800,7 +2869,9 @@ public:
                 if (round(0, false) == 0) all_top_ = true;
                 break;
             case LZB_ANARCHIC:
-                round(2, false);  // the initial stencil computation is not deferred
+                // the initial stencil computation is not deferred (assembly.cpp:98-103),
+                // unless the grid starts from the geometric stencil
+                if (!d_.start_geometric) round(2, false);
                 LZB_LAUNCH(k_spawn, blocks_for(leaves_, kThreads), kThreads, 0, s_, V(D_), cycle_,
                            static_cast<long long>(leaves_), keys_.p);
                 break;
@@ -3008,6 +3079,12 @@ public:
         if (d_.concurrent) try_commit(false);  // swap in a finished batch before the walk
         else begin_cycle_tasks();
         rep.cycle = static_cast<int32_t>(cycle_);
+        if (d_.forced_fraction > 0.0) {  // on_cycle_start (experiment.cpp:260-270)
+            long long id0 = 0;
+            for (int l = 0; l < D_; ++l) id0 += L_[l].nc;
+            LZB_LAUNCH(k_spawn_forced, blocks_for(leaves_, kThreads), kThreads, 0, s_, V(D_), cycle_,
+                       static_cast<long long>(leaves_), keys_.p, id0, d_.forced_fraction);
+        }
         if (ripple()) ripple_walk();
         else run_graph(g_coarse_, &Grid::coarse_pass);
         leaves_pass();
@@ -3762,6 +3839,7 @@ private:
     int D_;
     cudaStream_t s_;
     double* raw_ = nullptr;  // assemble_fixed_raw: integrated matrices out of the fused kernel
+    DevBuf<double> sink_;    // forced tasks' discarded results
     std::vector<Level> L_;
     int64_t leaves_ = 0, total_cells_ = 0, total_vertices_ = 0;
     DevBuf<int32_t> list_, snap_;
