@@ -561,8 +561,9 @@ struct LevelView {
     const double* cex;
     const double* cey;
     const double* rsin;
-    // desc.start_geometric on the leaf level: a cell at p1 = bottom reads the
-    // geometric stencil (eps = 1) instead of its n = 1 sample
+    // desc.start_geometric: a cell at p1 = bottom (a leaf not yet integrated, a
+    // coarse cell not yet recomputed) reads the geometric stencil (eps = 1)
+    // instead of its n = 1 sample
     int geo0;
 };
 

@@ -2526,8 +2526,8 @@ public:
         if (l == D_) {
             v.cw = d_.plane_width;
             v.fixed_p3 = d_.fixed_p3;
-            v.geo0 = d_.start_geometric;
         }
+        v.geo0 = d_.start_geometric;  // every level: unassembled cells read the eps = 1 stencil
         if (l > 0) v.pdirty = L_[l - 1].dirty.p;  // nullptr unless ripple
         if (uhat_is_u_) v.v[LZB_V_UHAT] = v.v[LZB_V_U];  // V-cycle: u-hat = u without a copy
         return v;
@@ -3443,8 +3443,9 @@ public:
                 } else {  // baseline, evaluated on the host only for this debug view
                     int cx = static_cast<int>(c % L.N), cy = static_cast<int>(c / L.N);
                     double x0 = cx * L.h, y0 = cy * L.h;
-                    double e = lzb_field_eval_host(&d_.field, x0 + (0 + 0.5) * 1.0 * L.h,
-                                                   y0 + (0 + 0.5) * 1.0 * L.h);
+                    double e = d_.start_geometric ? 1.0  // the geometric stencil (eps = 1)
+                                                  : lzb_field_eval_host(&d_.field, x0 + (0 + 0.5) * 1.0 * L.h,
+                                                                        y0 + (0 + 0.5) * 1.0 * L.h);
                     for (int k = 0; k < 16; ++k) ops[16 * c + k] = 0.0 + kunit[k] * e;
                 }
             }
