@@ -50,6 +50,18 @@ inline void check(int rc) {
 using Mat4 = std::array<double, 16>;
 using TransferBlock = std::array<double, 64>;  // w[L*4 + c] (types.hpp:62-66)
 
+/// Assembled 3x3 vertex stencil, index (dy+1)*3 + (dx+1) (types.hpp:53-58).
+struct Stencil9 {
+    std::array<double, 9> s{};
+    double& at(int dx, int dy) { return s[(dy + 1) * 3 + (dx + 1)]; }
+    double at(int dx, int dy) const { return s[(dy + 1) * 3 + (dx + 1)]; }
+    double centre() const { return at(0, 0); }
+};
+/// scatter_row (element.hpp:53)
+inline void scatter_row(const Mat4& element, int corner, Stencil9& stencil) {
+    check(lzb_scatter_row(element.data(), corner, stencil.s.data()));
+}
+
 struct ElementMatrix {  // element.hpp:12-15
     Mat4 m{};
     int n = 0;
@@ -209,6 +221,16 @@ public:
         std::vector<double> v(static_cast<size_t>(N + 1) * (N + 1));
         check(lzb_grid_vertices(g_, level, field, v.data(), 0));
         return v;
+    }
+    /// assemble_vertex_stencil (assembly.hpp:69-71) of vertex (ix, iy) of a level.
+    Stencil9 assemble_vertex_stencil(int level, int ix, int iy, bool require_payload = false) {
+        int N = 1;
+        for (int i = 0; i < level; ++i) N *= 3;
+        std::vector<double> all(static_cast<size_t>(N + 1) * (N + 1) * 9);
+        check(lzb_grid_vertex_stencils(g_, level, require_payload ? 1 : 0, all.data()));
+        Stencil9 st;
+        for (int k = 0; k < 9; ++k) st.s[k] = all[9 * (static_cast<size_t>(iy) * (N + 1) + ix) + k];
+        return st;
     }
     lzb_grid* raw() const { return g_; }
 

@@ -142,6 +142,14 @@ int lzb_grid_vertices(lzb_grid* g, int level, int field, double* buf, int write)
 /* Dense per-level cells, index cy*N+cx: element_or_baseline (16 doubles), markers. */
 int lzb_grid_cells(lzb_grid* g, int level, double* ops, int32_t* p1, int32_t* n, int32_t* p3,
                    uint32_t* epoch);
+/* assemble_vertex_stencil (assembly.hpp:69-71, assembly.cpp:120-136) for every
+ * vertex of a level: out (N+1)^2 x 9 doubles, vertex iy*(N+1)+ix, entry
+ * (dy+1)*3+(dx+1) (Stencil9, types.hpp:53-58); missing cells contribute zero;
+ * require_payload != 0 and a bottom neighbour -> LZB_ERR_PROTOCOL. */
+int lzb_grid_vertex_stencils(lzb_grid* g, int level, int require_payload, double* out);
+/* scatter_row (element.hpp:53, element.cpp:39-45): stencil9 += row `corner`
+ * of element16 placed relative to that corner. Host only. */
+int lzb_scatter_row(const double* element16, int corner, double* stencil9);
 /* Transfer block of a refined cell (transfer_or_geometric, stream.hpp:106). */
 int lzb_grid_transfer(lzb_grid* g, int level, int cx, int cy, double* out64);
 /* CellStream::publish_element + marker store (stream.hpp:88, assembly protocol). */

@@ -110,6 +110,8 @@ def lib():
         L.lzb_grid_transfer.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp]
         L.lzb_grid_publish_element.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, i32]
         L.lzb_grid_publish_level.argtypes = [vp, C.c_int, vp, vp, i32]
+        L.lzb_grid_vertex_stencils.argtypes = [vp, C.c_int, C.c_int, vp]
+        L.lzb_scatter_row.argtypes = [vp, C.c_int, vp]
         L.lzb_grid_assemble_fixed_raw.argtypes = [vp, C.c_int, vp]
         L.lzb_grid_adaptive_step.argtypes = [vp, C.c_int, C.c_int, C.c_int]
         L.lzb_grid_stats.argtypes = [vp, C.POINTER(CompressionStats)]
@@ -321,6 +323,14 @@ class codec:
         return int(codec.choose_precision_records(v, v.size, delta_max, ctx)[0])
 
 
+def scatter_row(element, corner, stencil=None) -> np.ndarray:
+    """scatter_row (element.cpp:39-45): stencil9 += the element row of `corner`."""
+    e = np.ascontiguousarray(element, dtype=np.float64).reshape(16)
+    st = np.zeros(9) if stencil is None else stencil
+    _check(lib().lzb_scatter_row(_ptr(e), corner, _ptr(st)))
+    return st
+
+
 def pack_header(p1, p2, p3) -> int:
     return lib().lzb_pack_header(p1, 1 if p2 else 0, p3)
 
@@ -519,6 +529,13 @@ class Grid:
         N = 3 ** self.desc.depth
         out = np.zeros((N * N, 16))
         _check(lib().lzb_grid_assemble_fixed_raw(self.h, n, _ptr(out)))
+        return out
+
+    def vertex_stencils(self, level, require_payload=False):
+        """assemble_vertex_stencil of every vertex: ((N+1)^2, 9), Stencil9 order."""
+        N = 3 ** level
+        out = np.zeros(((N + 1) * (N + 1), 9))
+        _check(lib().lzb_grid_vertex_stencils(self.h, level, 1 if require_payload else 0, _ptr(out)))
         return out
 
     def publish_level(self, level, mats, n, p1):

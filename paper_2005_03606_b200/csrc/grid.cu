@@ -2046,6 +2046,34 @@ __global__ void k_unpack(LevelView L, lzb_field f, int level, int leaf, SlotTabl
     L.p3[c] = static_cast<int8_t>(p3);
 }
 
+// assemble_vertex_stencil (assembly.cpp:120-136) for every vertex of a level:
+// the adjacent cells (stepping c = SW, SE, NW, NE) contribute, through
+// scatter_row (element.cpp:39-45), the row of the corner diagonally opposite
+// to the step; missing cells contribute zero. out: 9 per vertex, index
+// (dy+1)*3 + (dx+1) (Stencil9, types.hpp:53-58). require_payload: a bottom
+// neighbour raises *err (protocol_error).
+__global__ void k_vertex_stencils(LevelView F, lzb_field f, double* __restrict__ out, int require_payload,
+                                  int* err) {
+    lzb_pdl_enter();
+    int ix, iy;
+    int64_t vi;
+    if (!vertex_xy(F, ix, iy, vi)) return;
+    double st[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int c = 0; c < 4; ++c) {
+        const int cx = ix - 1 + cdx(c), cy = iy - 1 + cdy(c);
+        if (cx < 0 || cy < 0 || cx >= F.N || cy >= F.N) continue;
+        if (require_payload && F.p1[static_cast<int64_t>(cy) * F.N + cx] == LZB_P1_BOTTOM) atomicExch(err, 1);
+        const int corner = (1 - cdx(c)) | ((1 - cdy(c)) << 1);
+        double K[16];
+        element_or_baseline(f, F, cx, cy, K);
+        for (int k = 0; k < 4; ++k) {
+            const int dx = cdx(k) - cdx(corner), dy = cdy(k) - cdy(corner);
+            st[(dy + 1) * 3 + (dx + 1)] += K[corner * 4 + k];
+        }
+    }
+    for (int k = 0; k < 9; ++k) out[9 * vi + k] = st[k];
+}
+
 // Single-cell protocol ops for the per-cell compatibility API.
 __global__ void k_publish_one(LevelView F, lzb_field f, int c, const double* m, int n, int32_t p1,
                               double delta_max, uint32_t cycle, unsigned long long* stats, int* err) {
@@ -3475,6 +3503,22 @@ public:
         sync_check();
     }
 
+    // lzb_grid_vertex_stencils: assemble_vertex_stencil of every vertex of a level
+    void vertex_stencils(int level, int require_payload, double* host_out) {
+        check_level(level);
+        const Level& L = L_[level];
+        DevBuf<double> out(static_cast<size_t>(L.nv) * 9);
+        DevBuf<int> flag(1);
+        LZB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s_));
+        LZB_LAUNCH(k_vertex_stencils, vgrid(level), kThreads, 0, s_, V(level), d_.field, out.p, require_payload,
+                   flag.p);
+        int hflag = 0;
+        LZB_CUDA(cudaMemcpyAsync(host_out, out.p, out.bytes(), cudaMemcpyDeviceToHost, s_));
+        LZB_CUDA(cudaMemcpyAsync(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
+        sync_check();
+        if (hflag) throw Error(LZB_ERR_PROTOCOL, "adjacent cell has no assembled operator (p1 = bottom)");
+    }
+
     // lzb_grid_publish_level: every leaf published from host matrices
     void publish_level(int level, const double* mats, const int32_t* n, int32_t p1) {
         if (level != D_) throw Error(LZB_ERR_INVALID, "publish_level is for the leaf level");
@@ -3951,6 +3995,20 @@ int lzb_grid_assemble_fixed_raw(lzb_grid* g, int n, double* host_raw) {
 }
 int lzb_grid_publish_level(lzb_grid* g, int level, const double* mats, const int32_t* n, int32_t p1) {
     return guarded([&] { g->g->publish_level(level, mats, n, p1); });
+}
+int lzb_grid_vertex_stencils(lzb_grid* g, int level, int require_payload, double* out) {
+    return guarded([&] { g->g->vertex_stencils(level, require_payload, out); });
+}
+int lzb_scatter_row(const double* element16, int corner, double* stencil9) {
+    if (corner < 0 || corner > 3) {
+        lzb::set_last_error("corner must be 0..3");
+        return LZB_ERR_INVALID;
+    }
+    for (int c = 0; c < 4; ++c) {  // element.cpp:39-45
+        const int dx = lzb::cdx(c) - lzb::cdx(corner), dy = lzb::cdy(c) - lzb::cdy(corner);
+        stencil9[(dy + 1) * 3 + (dx + 1)] += element16[corner * 4 + c];
+    }
+    return LZB_OK;
 }
 int lzb_grid_invalidate(lzb_grid* g) {
     return guarded([&] { g->g->invalidate(); });

@@ -74,6 +74,14 @@ int main(int argc, char** argv) {
         CHECK(reps.size() == 67);  // golden exp_cmp_eager.csv: 67 cycles
         auto st = g.compression_stats();
         CHECK(st.fine_cells == 81 && st.fine_factor_totals == 128.0);
+        // assembled interior stencil on the eps = 1 mesh (test_element.cpp:83-107)
+        lm::Stencil9 s9 = g.assemble_vertex_stencil(2, 4, 4, true);
+        for (int dx = -1; dx <= 1; ++dx)
+            for (int dy = -1; dy <= 1; ++dy)
+                CHECK(std::fabs(s9.at(dx, dy) - ((dx == 0 && dy == 0) ? 8.0 / 3.0 : -1.0 / 3.0)) <= 1e-12);
+        lm::Stencil9 byhand;
+        for (int c = 0; c < 4; ++c) lm::scatter_row(lm::Mat4(em.m), 3 - c, byhand);  // the 4 cells around a vertex
+        for (int k = 0; k < 9; ++k) CHECK(std::fabs(byhand.s[k] - s9.s[k]) <= 1e-12);
     }
     // the experiment layer (config file -> CSV -> table)
     if (argc > 2) {

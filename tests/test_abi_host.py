@@ -141,3 +141,19 @@ def test_compare_runs_on_golden_telemetry():
     assert d["a"]["cycles_to_target"] == 67 and d["b"]["final_status"] == "converged"
     with pytest.raises(lzb.LzbError):
         lzb.compare_runs(os.path.join(GOLDEN, "exp_cmp_a.csv"), os.path.join(GOLDEN, "exp_cmp_b.csv"))
+
+
+def test_scatter_row_host():
+    """scatter_row (element.cpp:39-45): the row of `corner` lands relative to
+    that corner in the Stencil9 layout (dy+1)*3 + (dx+1) (types.hpp:53-58)."""
+    rng = np.random.default_rng(4)
+    m = rng.standard_normal(16)
+    for corner in range(4):
+        st = lzb.scatter_row(m, corner, np.ones(9))
+        want = np.ones(9)
+        for c in range(4):
+            dx, dy = (c & 1) - (corner & 1), (c >> 1) - (corner >> 1)
+            want[(dy + 1) * 3 + dx + 1] += m[corner * 4 + c]
+        assert np.array_equal(st, want)
+    with pytest.raises(lzb.LzbError):
+        lzb.scatter_row(m, 4)

@@ -475,3 +475,58 @@ def test_geometric_start_concurrent_converges_to_deterministic_solution():
     assert np.array_equal(ca["ops"], cb["ops"]) and np.array_equal(ca["n"], cb["n"])
     ua, ub = con.vertices(4, lzb.T.V_U), det.vertices(4, lzb.T.V_U)
     assert np.abs(ua - ub).max() <= 1e-8 * np.abs(ub).max()
+
+
+def _stencils_restated(ops, N):
+    """assemble_vertex_stencil (assembly.cpp:120-136) over the product's cells."""
+    out = np.zeros(((N + 1) * (N + 1), 9))
+    for iy in range(N + 1):
+        for ix in range(N + 1):
+            st = np.zeros(9)
+            for c in range(4):
+                cx, cy = ix - 1 + (c & 1), iy - 1 + (c >> 1)
+                if not (0 <= cx < N and 0 <= cy < N):
+                    continue
+                corner = (1 - (c & 1)) | ((1 - (c >> 1)) << 1)
+                K = ops[cy * N + cx]
+                for k in range(4):
+                    dx, dy = (k & 1) - (corner & 1), (k >> 1) - (corner >> 1)
+                    st[(dy + 1) * 3 + dx + 1] += K[corner * 4 + k]
+            out[iy * (N + 1) + ix] = st
+    return out
+
+
+def test_vertex_stencil_known_answer_and_protocol():
+    """test_element.cpp:83-140: the eps = 1 interior stencil is 8/3 and -1/3
+    (centre = the cell-wise Jacobi diagonal); zero matrices give a zero
+    stencil; a bottom neighbour with require_payload is a protocol_error."""
+    d = lzb.make_desc(depth=1, field=lzb.field_constant(1.0), assembly="lazy", delta_max=0.0)
+    g = lzb.Grid(d, 0)
+    with pytest.raises(lzb.ProtocolError):
+        g.vertex_stencils(1, require_payload=True)
+    g.pass_(0)  # request_stencil on every leaf (lazy: converge now)
+    st = g.vertex_stencils(1, require_payload=True).reshape(4, 4, 9)
+    want = np.full(9, -1.0 / 3.0)
+    want[4] = 8.0 / 3.0
+    assert np.allclose(st[1, 1], want, rtol=1e-12, atol=0)
+    g.step()
+    assert st[1, 1, 4] == pytest.approx(g.vertices(1, lzb.T.V_DIAG)[1, 1], rel=1e-14)
+    z = lzb.Grid(d, 0)
+    for cy in range(3):
+        for cx in range(3):
+            z.publish_element(1, cx, cy, np.zeros(16), 1, 1)
+    assert not np.any(z.vertex_stencils(1)[5])
+    z.vertex_stencils(1)  # boundary vertices: missing cells contribute zero, no throw
+
+
+def test_vertex_stencils_match_restatement():
+    """Every vertex of every level of an assembled grid (leaves, Galerkin
+    coarse levels, unassembled bottom cells) against the restated loop."""
+    d = lzb.make_desc(depth=3, field=lzb.field_theta(16.0), assembly="adaptive", solver="adafac-pi")
+    g = lzb.Grid(d, 1)
+    g.step()
+    g.step()
+    for lvl in range(4):
+        N = 3 ** lvl
+        got = g.vertex_stencils(lvl)
+        assert np.array_equal(got, _stencils_restated(g.cells(lvl)["ops"], N)), lvl
