@@ -48,11 +48,17 @@ HBM_LEVEL = 8  # smoother / stream-pack roofline grid (6561^2, beyond L2)
 
 def c3_flops_per_sample(p):
     return 8 + 60 / p
-# algorithmic FP64 flops per sub-sample of the tabulated integration:
-#   EXACT: 6 mul (K_sub from axis parts) + 9 add (K values) + 9 mul + 9 add (accumulate)
-#          + 2 (eps combine: 1 + (0.9 sin x) sin y)                                   = 35
-#   FAST : 4 FMA (row/column partial sums) + 1 FMA (eps combine)                       = 10
-FLOPS_PER_SAMPLE = {"exact": 35, "fast": 10}
+# FP64 instructions EXECUTED per sub-sample by the integration kernel's inner
+# loop (SASS of k_fixed_res, tools/sass_loops.py: the EXACT loop body is 40 DMUL
+# + 40 DADD for 2 cells x 2 samples; K_sub comes from the shared-memory table):
+#   EXACT: eps combine 1 + (0.9 sin x) sin y (DMUL + DADD) + 9 x (DMUL K*e, DADD a += .) = 20
+#   FAST : 5 DFMA (row partial sums + the combine)                                        = 5
+# The FP64 pipe issues one warp DP instruction (DADD, DMUL or DFMA alike) per
+# slot, so the pipe-bound roofline is DP instructions/s against the DFMA rate
+# of the probe; it is reported in DFMA-equivalent TFLOP/s (2 flops per DP slot)
+# so that frac = the fraction of the FP64 pipe's issue slots used.
+DP_INSTR_PER_SAMPLE = {"exact": 20, "fast": 5}
+EXEC_FLOPS_PER_SAMPLE = {"exact": 20, "fast": 10}  # DMUL / DADD = 1 flop, DFMA = 2
 SURVEY_FLOPS_PER_SAMPLE = 77  # SURVEY.md §8d for C2 (2E + F_eps, sin counted per sample)
 METRIC = "eps sub-sample integrations/s; smoother DoF-updates/s; % FP64/HBM roofline"
 
@@ -65,6 +71,17 @@ def traffic_of(kernel):
             t = json.load(f).get(kernel)
         return None if t is None else t["dram_bytes_per_launch"]
     except (OSError, ValueError, KeyError):
+        return None
+
+
+def ncu_metric(kernel, key):
+    """A per-kernel figure of the committed ncu --set full summaries
+    (profiles/traffic.json, tools/summarize_profiles.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f).get(kernel)
+        return None if t is None else t.get(key)
+    except (OSError, ValueError):
         return None
 
 
@@ -204,6 +221,25 @@ def cpu_baseline(seconds=10.0, threads=None):
             "sample": f"{k} level-6 cells at p={P}, oracle/lzb_oracle.c single thread, {dt:.1f} s"}
 
 
+def cpu_delayed_solve(level, pmax):
+    """The delayed solve of BASELINE configs[1] (geometric start, p doubling
+    1 -> pmax, adaFAC-PI to 1e-10) on the host through the oracle restatement."""
+    from oracle import port
+    from oracle.types import field_sinusoid
+    import paper_2005_03606_b200 as lzb
+    d = lzb.make_desc(depth=level, field=field_sinusoid(0.9, 6.0), delta_max=1e-8, solver="adafac-pi", omega=0.6,
+                      assembly="anarchic", rhs_kind="sinprod", schedule="double", n_max=pmax, termination_c=0.0,
+                      target=1e-10, max_cycles=2000, start_geometric=True)
+    t0 = time.perf_counter()
+    o = port.Grid(d, 42)
+    reps = o.run()
+    dt = time.perf_counter() - t0
+    return {"seconds": dt, "cycles": len(reps), "final_normalized": reps[-1]["normalized"],
+            "status": lzb.T.STATUS_NAMES[reps[-1]["status"]], "cores": os.cpu_count() or 1, "kind": "port",
+            "how": "oracle/lzb_oracle.c (pinned to the unmodified reference): deterministic anarchic solve, task "
+                   "integrations on all host threads, cycles single-threaded (solver.cpp has no threads)"}
+
+
 def cpu_cycle_seconds(cycles=2):
     """One AdditiveSolver::step of the unmodified reference on the 729^2 grid
     (single-threaded by construction, solver.cpp has no threads); the cycle
@@ -306,14 +342,23 @@ def run_ours(args, world, rank, local):
 
     def roof(mode):
         per_launch_s = results[mode]["t"] / args.steps
-        achieved = SAMPLES_PER_STEP * FLOPS_PER_SAMPLE[mode] / per_launch_s / 1e12
+        dp_rate = SAMPLES_PER_STEP * DP_INSTR_PER_SAMPLE[mode] / per_launch_s / 1e12  # T DP instr/s
+        achieved = 2.0 * dp_rate  # DFMA-equivalent TFLOP/s
+        executed = SAMPLES_PER_STEP * EXEC_FLOPS_PER_SAMPLE[mode] / per_launch_s / 1e12
         return {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak, "kernel": "k_fixed_res",
+                "what": "FP64-pipe issue fraction: executed DP instructions/s x 2 (DFMA-equivalent) over the "
+                        "DFMA-chain peak; DADD / DMUL / DFMA each take one DP issue slot",
                 # ncu capture of the EXACT instantiation (k_fixed_res<4, 0>)
                 "traffic": traffic_of("k_fixed_res") if mode == "exact" else None,
-                "flops_per_sample": FLOPS_PER_SAMPLE[mode],
+                "ncu_fp64_pipe_active": ncu_metric("k_fixed_res", "fp64_pipe_active_pct") if mode == "exact"
+                else None,
+                "dp_instr_per_sample": DP_INSTR_PER_SAMPLE[mode], "dp_instr_per_s": dp_rate * 1e12,
+                "executed_tflops": executed, "executed_flops_per_sample": EXEC_FLOPS_PER_SAMPLE[mode],
                 "peak_source": "measured: lzb_probe_fp64_tflops (DFMA chains, this GPU)",
-                "survey_def_achieved": SAMPLES_PER_STEP * SURVEY_FLOPS_PER_SAMPLE / per_launch_s / 1e12}
+                "survey_def_achieved": SAMPLES_PER_STEP * SURVEY_FLOPS_PER_SAMPLE / per_launch_s / 1e12,
+                "survey_def_note": "SURVEY §8d counts 77 flops per sample (two sines each); the per-axis sine "
+                                   "tables take them out of the kernel, so that figure exceeds the peak"}
 
     # smoother: full additive cycles on the assembled 729^2 grid (DoF-updates/s)
     g = results[head]["grid"]
@@ -598,15 +643,17 @@ def run_ours(args, world, rank, local):
         gd.close()
         del gd
 
-    # time to solution of the delayed-assembly solve (BASELINE configs[1]): p doubling
-    # 1 -> 32 on the side stream while the adaFAC cycles run (termination-c = 0 forces
-    # the whole ladder; with the reference's C = 0.01 every cell of this smooth field is
-    # accepted at the n = 2 check), vs assembling the same ladder first (eager)
-    tts = {}
-    for label, mode, conc in (("eager", "eager", False), ("delayed_concurrent", "anarchic", True)):
-        d = lzb.make_desc(depth=LEVEL, field=f, delta_max=1e-8, solver="adafac-pi", omega=0.6,
-                          assembly=mode, rhs_kind="sinprod", schedule="double", n_max=P, termination_c=0.0,
-                          target=1e-10, max_cycles=2000, concurrent=conc, integration=args.integration)
+    # time to solution of the delayed-assembly solve (BASELINE configs[1]): from the
+    # geometric stencil (eps = 1), p doubling 1 -> 32 on the assembly stream while the
+    # adaFAC cycles run (termination-c = 0 forces the whole ladder; with the reference's
+    # C = 0.01 every cell of this smooth field is accepted at the n = 2 check), vs the
+    # same ladder deterministically interleaved (workers = 1 semantics) and vs assembling
+    # it first (eager); BASELINE configs[0] (243^2 checkerboard, ladder to 16) likewise
+    def tts_solve(depth, field, pmax, mode, conc, start_geo):
+        d = lzb.make_desc(depth=depth, field=field, delta_max=1e-8, solver="adafac-pi", omega=0.6,
+                          assembly=mode, rhs_kind="sinprod", schedule="double", n_max=pmax, termination_c=0.0,
+                          target=1e-10, max_cycles=2000, concurrent=conc, integration=args.integration,
+                          start_geometric=start_geo)
         gt = lzb.Grid(d, 42, ctx)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -615,12 +662,26 @@ def run_ours(args, world, rank, local):
         b.record(stream)
         b.synchronize()
         t_s = max_over_ranks(a.elapsed_time(b) * 1e-3, world)
-        tts[label] = {"seconds": t_s, "cycles": len(reps), "final_normalized": reps[-1]["normalized"],
-                      "status": lzb.T.STATUS_NAMES[reps[-1]["status"]], "max_n": reps[-1]["max_n"],
-                      "factor_totals": reps[-1]["factor_totals"]}
+        out = {"seconds": t_s, "cycles": len(reps), "final_normalized": reps[-1]["normalized"],
+               "status": lzb.T.STATUS_NAMES[reps[-1]["status"]], "max_n": reps[-1]["max_n"],
+               "factor_totals": reps[-1]["factor_totals"]}
         del gt
-    tts["setup"] = (f"729^2 sinusoid eps, f = 2 pi^2 sin sin, adaFAC-PI omega 0.6, target 1e-10, p doubling "
-                    f"1->{P} (C = 0), delta_max 1e-8; device timeline (CUDA events) incl. host round trips")
+        return out
+
+    tts = {}
+    for label, mode, conc, geo in (("eager", "eager", False, False),
+                                   ("delayed_deterministic", "anarchic", False, True),
+                                   ("delayed_concurrent", "anarchic", True, True)):
+        tts[label] = tts_solve(LEVEL, f, P, mode, conc, geo)
+    tts["setup"] = (f"729^2 sinusoid eps, f = 2 pi^2 sin sin, adaFAC-PI omega 0.6, target 1e-10, delayed runs start "
+                    f"from the geometric stencil (eps = 1), p doubling 1->{P} (C = 0), delta_max 1e-8; device "
+                    f"timeline (CUDA events) incl. host round trips")
+    tts_c1 = {label: tts_solve(5, lzb.checkerboard(1, 8), 16, mode, conc, geo)
+              for label, mode, conc, geo in (("eager", "eager", False, False),
+                                             ("delayed_concurrent", "anarchic", True, True))}
+    tts_c1["setup"] = ("243^2 8x8 checkerboard 10^U(-2,2), f = 2 pi^2 sin sin, adaFAC-PI omega 0.6, target 1e-10, "
+                       "p doubling 1->16 (C = 0); eager = the ladder assembled first")
+    tts["c1"] = tts_c1
 
     # end to end through the C-ABI: assemble, then the compressed LZMG stream to a host buffer
     img = g.stream_image()
@@ -645,17 +706,12 @@ def run_ours(args, world, rank, local):
         return
     base = cpu_baseline(seconds=args.cpu_seconds) if not args.no_cpu_baseline else None
     if base is not None:
-        # time to solution of the same delayed solve on the host, projected from the
-        # measured reference components: the p-doubling ladder at the all-core
-        # integrate_element rate + the measured per-cycle cost x the cycles needed
-        cyc = cpu_cycle_seconds()
-        ladder = CELLS * sum(k * k for k in (1, 2, 4, 8, 16, 32))
-        if cyc is not None:
-            tts["cpu_reference_projected"] = {
-                "seconds": ladder / base["value"] + cyc * tts["eager"]["cycles"],
-                "cycle_seconds": cyc, "cycles": tts["eager"]["cycles"], "ladder_sub_samples": ladder,
-                "how": "unmodified reference: AdditiveSolver::step on the 729^2 mesh (1 thread) x cycles + "
-                       "ladder / measured all-core integrate_element rate"}
+        # time to solution of the same delayed solve on the host, MEASURED: the C
+        # restatement (oracle/lzb_oracle.c, pinned to the unmodified reference) runs
+        # the deterministic delayed solve (workers = 1 task semantics; each cycle's
+        # task integrations on all host threads, the cycle itself single-threaded as
+        # the reference's solver is)
+        tts["cpu_measured"] = cpu_delayed_solve(LEVEL, P)
     mp = peaks()
     line = {
         "metric": METRIC, "value": value, "unit": "sub-samples/s", "n_gpus": world, "steps": args.steps,

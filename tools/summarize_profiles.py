@@ -15,6 +15,8 @@ import subprocess
 import sys
 
 tag, launches, rep = sys.argv[1], sys.argv[2], sys.argv[3]
+# optional: a suffix for the traffic.json keys (e.g. "@729^3" for a per-config capture)
+key_suffix = sys.argv[4] if len(sys.argv) > 4 else ""
 out_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
 rows = list(csv.reader(open(launches))) if launches != "-" else [["Kernel Name", "Metric Value", "Metric Unit"]]
 hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
@@ -80,5 +82,18 @@ for v in vals:
     name = v[kn].split("(")[0].replace("void ", "").replace("lzb::<unnamed>::", "")
     name = name.replace("(anonymous namespace)::", "").replace("unnamed>::", "").split("<")[0].strip()
     b = float(v[ir].replace(",", "")) * scale.get(units[ir], 1) + float(v[iw].replace(",", "")) * scale.get(units[iw], 1)
-    traffic[name] = {"dram_bytes_per_launch": b, "report": os.path.basename(rep), "tag": tag}
+    entry = {"dram_bytes_per_launch": b, "report": os.path.basename(rep), "tag": tag}
+    for key, metric in (("fp64_pipe_active_pct", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                        ("dram_throughput_pct", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                        ("issue_active_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                        ("duration_us", "gpu__time_duration.sum")):
+        if metric in hdr:
+            try:
+                x = float(v[hdr.index(metric)].replace(",", ""))
+                if key == "duration_us":
+                    x *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(units[hdr.index(metric)], 1.0)
+                entry[key] = x
+            except ValueError:
+                pass
+    traffic[name + key_suffix] = entry
 json.dump(traffic, open(tpath, "w"), indent=1, sort_keys=True)
