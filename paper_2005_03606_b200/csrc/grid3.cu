@@ -907,56 +907,114 @@ __global__ void k3_prolong(Lv3 F, Lv3 C) {
     F.v[LZB_V_U][vi] += p;
 }
 
-// The leaf level's three u updates of a cycle in one pass (bit-identical to
-// k3_aux_sub, k3_jacobi, k3_prolong run in that order): the adaFAC-PI aux
-// correction, damped Jacobi, the prolongated coarse correction. The coarse
-// levels are updated first; nothing there reads the leaf u.
-__global__ void k3_update_fine(Lv3 F, Lv3 C, int pi, double omega, double damping) {
+// ---- staged leaf-level vertex kernels
+// A block is a row of 128 fine vertices along x at one (y, z): the owner
+// patch's (y, z) coordinates and lattice offsets are uniform over the block,
+// so the coarse values the row needs are the x-range of its owner patches
+// (<= 45 coarse x) on 4 coarse (y, z) lines. They are staged once per block in
+// shared memory (instead of 8 strided loads per fine vertex), with the k / 27
+// weight table; the fine arrays stream coalesced. k3_uhat_st is bit-identical
+// to k3_uhat (same expressions, same summation order); k3_update_fine_st is the
+// leaf level's three u updates of a cycle in one pass, bit-identical to
+// k3_aux_sub, k3_jacobi, k3_prolong run in that order (the adaFAC-PI aux
+// correction, damped Jacobi, the prolongated coarse correction; the coarse
+// levels are updated first, nothing there reads the leaf u).
+constexpr int kStX = 48;  // staged coarse x per line (128 / 3 + 3 rounded up)
+struct RowStage {
+    int px0, nx, py, pz, ly, lz;
+};
+__device__ __forceinline__ RowStage row_stage(const Lv3& F, const Lv3& C, int fy, int fz) {
+    RowStage r;
+    const int fx0 = blockIdx.x * blockDim.x;
+    const int fx1 = min(fx0 + static_cast<int>(blockDim.x) - 1, F.N);
+    r.px0 = owner3(fx0, C.N);
+    r.nx = owner3(fx1, C.N) + 2 - r.px0;  // owner patches' x corners px .. px + 1
+    r.py = owner3(fy, C.N);
+    r.pz = owner3(fz, C.N);
+    r.ly = fy - 3 * r.py;
+    r.lz = fz - 3 * r.pz;
+    return r;
+}
+
+// Per coarse vertex of the level below the leaves, once per cycle: the
+// adaFAC-PI aux correction factor omega / diag * aux (0 on the boundary and
+// where diag = 0) and the prolongated correction u - usnap.
+__global__ void k3_coarse_pre(Lv3 C, double omega, int pi, double2* __restrict__ pre) {
     lzb_pdl_enter();
-    int fx, fy, fz;
-    int64_t vi;
-    if (!vxyz(F, fx, fy, fz, vi)) return;
-    if (bnd3(F.N, fx, fy, fz)) return;
-    const int px = owner3(fx, C.N), py = owner3(fy, C.N), pz = owner3(fz, C.N);
-    const int lx = fx - 3 * px, ly = fy - 3 * py, lz = fz - 3 * pz;
-    double cu[8], cs[8], ca[8], cd[8];
-#pragma unroll
-    for (int a = 0; a < 8; ++a) {
-        const int64_t ci = vidx3(C.N, px + (a & 1), py + ((a >> 1) & 1), pz + (a >> 2));
-        cu[a] = C.v[LZB_V_U][ci];
-        cs[a] = C.v[LZB_V_USNAP][ci];
-        if (pi) {
-            ca[a] = C.v[LZB_V_AUX][ci];
-            cd[a] = C.v[LZB_V_DIAG][ci];
-        }
+    int cx, cy, cz;
+    int64_t ci;
+    if (!vxyz(C, cx, cy, cz, ci)) return;
+    double caux = 0.0;
+    if (pi) {
+        const double dg = C.v[LZB_V_DIAG][ci];
+        caux = (!bnd3(C.N, cx, cy, cz) && dg != 0.0) ? omega / dg * C.v[LZB_V_AUX][ci] : 0.0;
     }
+    pre[ci] = make_double2(caux, C.v[LZB_V_U][ci] - C.v[LZB_V_USNAP][ci]);
+}
+
+__global__ void __launch_bounds__(128) k3_update_fine_st(Lv3 F, Lv3 C, const double2* __restrict__ pre, int pi,
+                                                          double damping) {
+    lzb_pdl_enter();
+    __shared__ double2 s_pre[4][kStX];
+    __shared__ double s_w[28];
+    const int fx = blockIdx.x * blockDim.x + threadIdx.x, fy = blockIdx.y, fz = blockIdx.z + F.z0;
+    const RowStage R = row_stage(F, C, fy, fz);
+    if (threadIdx.x < 28) s_w[threadIdx.x] = g_w27[threadIdx.x];
+    for (int t = threadIdx.x; t < 4 * R.nx; t += blockDim.x) {
+        const int q = t / R.nx, j = t - q * R.nx, cx = min(R.px0 + j, C.N);
+        s_pre[q][j] = pre[vidx3(C.N, cx, R.py + (q & 1), R.pz + (q >> 1))];
+    }
+    __syncthreads();
+    if (fx > F.N || bnd3(F.N, fx, fy, fz)) return;
+    const int64_t vi = vidx3(F.N, fx, fy, fz);
+    const int px = owner3(fx, C.N), lx = fx - 3 * px, jx = px - R.px0;
+    const int wx[2] = {3 - lx, lx}, wy[2] = {3 - R.ly, R.ly}, wz[2] = {3 - R.lz, R.lz};
     double u = F.v[LZB_V_U][vi];
     const double dg = F.v[LZB_V_DIAG][vi], r = F.v[LZB_V_R][vi];
+    double2 c[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) c[a] = s_pre[((a >> 1) & 1) | ((a >> 2) << 1)][jx + (a & 1)];
     if (pi) {
         double p = 0.0;
 #pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            const int cx = px + (a & 1), cy = py + ((a >> 1) & 1), cz = pz + (a >> 2);
-            const double caux = (!bnd3(C.N, cx, cy, cz) && cd[a] != 0.0) ? omega / cd[a] * ca[a] : 0.0;
-            p += pw3(lx, ly, lz, a) * caux;
-        }
+        for (int a = 0; a < 8; ++a) p += s_w[wx[a & 1] * wy[(a >> 1) & 1] * wz[a >> 2]] * c[a].x;
         u -= p;
     }
     if (dg != 0.0) u += damping / dg * r;
-    double d[8];
     bool any = false;
 #pragma unroll
-    for (int a = 0; a < 8; ++a) {
-        d[a] = cu[a] - cs[a];
-        any |= d[a] != 0.0;
-    }
+    for (int a = 0; a < 8; ++a) any |= c[a].y != 0.0;
     if (any) {
         double p = 0.0;
 #pragma unroll
-        for (int a = 0; a < 8; ++a) p += pw3(lx, ly, lz, a) * d[a];
+        for (int a = 0; a < 8; ++a) p += s_w[wx[a & 1] * wy[(a >> 1) & 1] * wz[a >> 2]] * c[a].y;
         u += p;
     }
     F.v[LZB_V_U][vi] = u;
+}
+
+__global__ void __launch_bounds__(128) k3_uhat_st(Lv3 F, Lv3 C) {
+    lzb_pdl_enter();
+    __shared__ double s_u[4][kStX];
+    __shared__ double s_w[28];
+    const int fx = blockIdx.x * blockDim.x + threadIdx.x, fy = blockIdx.y, fz = blockIdx.z + F.z0;
+    const RowStage R = row_stage(F, C, fy, fz);
+    if (threadIdx.x < 28) s_w[threadIdx.x] = g_w27[threadIdx.x];
+    for (int t = threadIdx.x; t < 4 * R.nx; t += blockDim.x) {
+        const int q = t / R.nx, j = t - q * R.nx, cx = min(R.px0 + j, C.N);
+        s_u[q][j] = C.v[LZB_V_U][vidx3(C.N, cx, R.py + (q & 1), R.pz + (q >> 1))];
+    }
+    __syncthreads();
+    if (fx > F.N) return;
+    const int64_t vi = vidx3(F.N, fx, fy, fz);
+    const int px = owner3(fx, C.N), lx = fx - 3 * px, jx = px - R.px0;
+    const int wx[2] = {3 - lx, lx}, wy[2] = {3 - R.ly, R.ly}, wz[2] = {3 - R.lz, R.lz};
+    const double u = F.v[LZB_V_U][vi];
+    double interp = 0.0;
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+        interp += s_w[wx[a & 1] * wy[(a >> 1) & 1] * wz[a >> 2]] * s_u[((a >> 1) & 1) | ((a >> 2) << 1)][jx + (a & 1)];
+    F.v[LZB_V_UHAT][vi] = u - interp;
 }
 
 __global__ void k3_inject(Lv3 F, Lv3 C) {
@@ -1424,7 +1482,7 @@ public:
         std::memset(&rep, 0, sizeof rep);
         rep.cycle = static_cast<int32_t>(++cycle_);
         for (int l = D_; l >= 0; --l) {
-            LZB_LAUNCH(k3_uhat, vg(l), 128, 0, s_, lv(l), l > 0 ? lv(l - 1) : lv(l), l > 0 ? 1 : 0);
+            uhat3(l, 0, L3_[l].N + 1);
             residual3(l, 0, L3_[l].N + 1);
             if (l > 0) LZB_LAUNCH(k3_restrict, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
         }
@@ -1458,7 +1516,7 @@ public:
             }
             for (int l = 1; l < D_; ++l) LZB_LAUNCH(k3_prolong, vg(l), 128, 0, s_, lv(l), lv(l - 1));
             if (D_ > 0)
-                LZB_LAUNCH(k3_update_fine, vg(D_), 128, 0, s_, lv(D_), lv(D_ - 1), pi ? 1 : 0, omega_, damping3(D_));
+                update_fine3(0, L3_[D_].N + 1, pi, damping3(D_));
             else
                 LZB_LAUNCH(k3_jacobi, vg(0), 128, 0, s_, lv(0), damping3(0));
             inject3();
@@ -1509,7 +1567,7 @@ public:
                 }
                 ++cycle_;
                 const int u0 = std::max(v0 - 1, 0), u1 = std::min(v1 + 1, N + 1);
-                LZB_LAUNCH(k3_uhat, vgz(D_, u0, u1), 128, 0, s_, lvz(D_, u0), lv(D_ - 1), 1);
+                uhat3(D_, u0, u1);
                 residual3(D_, v0, v1);
                 LZB_CUDA(cudaMemsetAsync(partial3_.p, 0, partial3_.bytes(), s_));
                 LZB_LAUNCH(k3_norm_partial, kNormBlocks3, 256, 0, s_, lv(D_), partial3_.p, v0, v1);
@@ -1520,7 +1578,7 @@ public:
                 break;
             case 2: {
                 for (int l = D_ - 1; l >= 0; --l) {
-                    LZB_LAUNCH(k3_uhat, vg(l), 128, 0, s_, lv(l), l > 0 ? lv(l - 1) : lv(l), l > 0 ? 1 : 0);
+                    uhat3(l, 0, L3_[l].N + 1);
                     residual3(l, 0, L3_[l].N + 1);
                     if (l > 0) LZB_LAUNCH(k3_restrict, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
                 }
@@ -1548,8 +1606,7 @@ public:
                 }
                 for (int l = 1; l < D_; ++l) LZB_LAUNCH(k3_prolong, vg(l), 128, 0, s_, lv(l), lv(l - 1));
                 // the slab's leaf planes: aux correction, Jacobi, prolongation (fused, the one-GPU kernel)
-                LZB_LAUNCH(k3_update_fine, vgz(D_, v0, v1), 128, 0, s_, lvz(D_, v0), lv(D_ - 1),
-                           variant_ == LZB_ADAFAC_PI ? 1 : 0, omega_, damping3(D_));
+                update_fine3(v0, v1, variant_ == LZB_ADAFAC_PI, damping3(D_));
                 LZB_LAUNCH(k3_inject, vgz(D_ - 1, c0, c1), 128, 0, s_, lv(D_), lvz(D_ - 1, c0));
                 break;
             }
@@ -1576,13 +1633,13 @@ public:
         }
         auto launch = [&] {
             switch (what) {
-                case LZB_TK_UHAT: LZB_LAUNCH(k3_uhat, vg(D_), 128, 0, s_, lv(D_), lv(D_ - 1), 1); break;
+                case LZB_TK_UHAT: uhat3(D_, 0, L3_[D_].N + 1); break;
                 case LZB_TK_RESIDUAL: residual3(D_, 0, L3_[D_].N + 1); break;
                 case LZB_TK_RESTRICT: LZB_LAUNCH(k3_restrict, vg(D_ - 1), 128, 0, s_, lv(D_), lv(D_ - 1)); break;
                 case LZB_TK_JACOBI: LZB_LAUNCH(k3_jacobi, vg(D_), 128, 0, s_, lv(D_), 0.0); break;
                 case LZB_TK_PROLONG: LZB_LAUNCH(k3_prolong, vg(D_), 128, 0, s_, lv(D_), lv(D_ - 1)); break;
                 case LZB_TK_BACK:  // the fused leaf update (u drifts by the prolongated correction)
-                    LZB_LAUNCH(k3_update_fine, vg(D_), 128, 0, s_, lv(D_), lv(D_ - 1), 1, omega_, 0.0);
+                    update_fine3(0, L3_[D_].N + 1, true, 0.0);
                     break;
                 default: throw Error(LZB_ERR_INVALID, "unknown kernel id");
             }
@@ -1741,6 +1798,22 @@ private:
     bool uhat_is_u_ = false;
     double damping3(int l) const { return variant_ == LZB_ADDITIVE ? std::pow(omega_, D_ - l + 1) : omega_; }
     dim3 vg(int l) const { return dim3(blocks_for(L3_[l].N + 1, 128), L3_[l].N + 1, L3_[l].N + 1); }
+    // u-hat of level l on vertex planes [z0, z1): the leaf level (and any level
+    // with a coarse level below) through the staged row kernel
+    void uhat3(int l, int z0, int z1) {
+        if (l == 0) LZB_LAUNCH(k3_uhat, vgz(0, z0, z1), 128, 0, s_, lvz(0, z0), lv(0), 0);
+        else LZB_LAUNCH(k3_uhat_st, vgz(l, z0, z1), 128, 0, s_, lvz(l, z0), lv(l - 1));
+    }
+    // the leaf level's fused update on vertex planes [z0, z1): the coarse
+    // factors (aux correction, prolongated correction) once per coarse vertex,
+    // then the staged row kernel
+    void update_fine3(int z0, int z1, bool pi, double damping) {
+        if (pre3_.n < static_cast<size_t>(L3_[D_ - 1].nv)) pre3_.alloc(L3_[D_ - 1].nv);
+        LZB_LAUNCH(k3_coarse_pre, vg(D_ - 1), 128, 0, s_, lv(D_ - 1), omega_, pi ? 1 : 0, pre3_.p);
+        LZB_LAUNCH(k3_update_fine_st, vgz(D_, z0, z1), 128, 0, s_, lvz(D_, z0), lv(D_ - 1), pre3_.p, pi ? 1 : 0,
+                   damping);
+    }
+    DevBuf<double2> pre3_;
     void inject3() {
         for (int l = D_; l >= 1; --l) LZB_LAUNCH(k3_inject, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
     }
