@@ -908,33 +908,43 @@ __global__ void k3_prolong(Lv3 F, Lv3 C) {
 }
 
 // ---- staged leaf-level vertex kernels
-// A block is a row of 128 fine vertices along x at one (y, z): the owner
-// patch's (y, z) coordinates and lattice offsets are uniform over the block,
-// so the coarse values the row needs are the x-range of its owner patches
-// (<= 45 coarse x) on 4 coarse (y, z) lines. They are staged once per block in
-// shared memory (instead of 8 strided loads per fine vertex), with the k / 27
-// weight table; the fine arrays stream coalesced. k3_uhat_st is bit-identical
-// to k3_uhat (same expressions, same summation order); k3_update_fine_st is the
-// leaf level's three u updates of a cycle in one pass, bit-identical to
-// k3_aux_sub, k3_jacobi, k3_prolong run in that order (the adaFAC-PI aux
-// correction, damped Jacobi, the prolongated coarse correction; the coarse
-// levels are updated first, nothing there reads the leaf u).
-constexpr int kStX = 48;  // staged coarse x per line (128 / 3 + 3 rounded up)
+// A block is a row segment of 256 fine vertices along x on kStY consecutive
+// rows along y of one vertex plane z (rows of one plane are 8 (N+1) bytes
+// apart: the block's loads stay within a page or two per array, where a z
+// chunk would touch a page per plane). The owner patch's z coordinate and
+// lattice offset are uniform over the block, so the coarse values the block
+// needs are the x-range of its owner patches (<= 88 coarse x) on the <= 5
+// coarse y lines its rows' owners span and 2 coarse z planes; they are staged
+// once in shared memory. The trilinear interpolation is then evaluated
+// separably: per fine row the block contracts y and z for every staged coarse
+// x, and each fine vertex takes the x contraction of two of those -- 2 FMA per
+// vertex instead of 8 weights x 8 corners. The 3D cycle is a restatement
+// (oracle/port3.py sums the 8 corners with k / 27 weights): the regrouping
+// changes the last bits only (tests: 1e-12 on u).
+constexpr int kStThreads = 256;  // fine x per block
+constexpr int kStX = 96;  // staged coarse x per line (256 / 3 + 3 rounded up)
+constexpr int kStY = 8;   // fine rows per block
+constexpr int kStCy = 5;  // coarse y lines the rows' owner patches span (<= kStY / 3 + 3)
 struct RowStage {
-    int px0, nx, py, pz, ly, lz;
+    int px0, nx, pz, lz, py0, ny, fy0, fy1, fz;
 };
-__device__ __forceinline__ RowStage row_stage(const Lv3& F, const Lv3& C, int fy, int fz) {
+__device__ __forceinline__ RowStage row_stage(const Lv3& F, const Lv3& C) {
     RowStage r;
     const int fx0 = blockIdx.x * blockDim.x;
     const int fx1 = min(fx0 + static_cast<int>(blockDim.x) - 1, F.N);
     r.px0 = owner3(fx0, C.N);
     r.nx = owner3(fx1, C.N) + 2 - r.px0;  // owner patches' x corners px .. px + 1
-    r.py = owner3(fy, C.N);
-    r.pz = owner3(fz, C.N);
-    r.ly = fy - 3 * r.py;
-    r.lz = fz - 3 * r.pz;
+    r.fz = blockIdx.z + F.z0;
+    r.pz = owner3(r.fz, C.N);
+    r.lz = r.fz - 3 * r.pz;
+    r.fy0 = blockIdx.y * kStY;
+    r.fy1 = min(r.fy0 + kStY, F.N + 1);
+    r.py0 = owner3(r.fy0, C.N);
+    r.ny = owner3(r.fy1 - 1, C.N) + 2 - r.py0;
     return r;
 }
+// per-axis lattice weights (a ? L : 3 - L) / 3
+__device__ __forceinline__ double wax(int L, int a) { return static_cast<double>(a ? L : 3 - L) / 3.0; }
 
 // Per coarse vertex of the level below the leaves, once per cycle: the
 // adaFAC-PI aux correction factor omega / diag * aux (0 on the boundary and
@@ -952,69 +962,105 @@ __global__ void k3_coarse_pre(Lv3 C, double omega, int pi, double2* __restrict__
     pre[ci] = make_double2(caux, C.v[LZB_V_U][ci] - C.v[LZB_V_USNAP][ci]);
 }
 
-__global__ void __launch_bounds__(128) k3_update_fine_st(Lv3 F, Lv3 C, const double2* __restrict__ pre, int pi,
+// The leaf level's three u updates of a cycle in one pass (the adaFAC-PI aux
+// correction, damped Jacobi, the prolongated coarse correction -- k3_aux_sub,
+// k3_jacobi, k3_prolong in that order; the coarse levels are updated first,
+// nothing there reads the leaf u).
+__global__ void __launch_bounds__(kStThreads) k3_update_fine_st(Lv3 F, Lv3 C, const double2* __restrict__ pre, int pi,
                                                           double damping) {
     lzb_pdl_enter();
-    __shared__ double2 s_pre[4][kStX];
-    __shared__ double s_w[28];
-    const int fx = blockIdx.x * blockDim.x + threadIdx.x, fy = blockIdx.y, fz = blockIdx.z + F.z0;
-    const RowStage R = row_stage(F, C, fy, fz);
-    if (threadIdx.x < 28) s_w[threadIdx.x] = g_w27[threadIdx.x];
-    for (int t = threadIdx.x; t < 4 * R.nx; t += blockDim.x) {
-        const int q = t / R.nx, j = t - q * R.nx, cx = min(R.px0 + j, C.N);
-        s_pre[q][j] = pre[vidx3(C.N, cx, R.py + (q & 1), R.pz + (q >> 1))];
+    __shared__ double2 s_pre[kStCy][2][kStX];
+    __shared__ double2 s_g[kStY][kStX];  // per row, per coarse x: (aux, correction) contracted over y, z
+    __shared__ unsigned char s_nz[kStY][kStX];
+    const int fx = blockIdx.x * blockDim.x + threadIdx.x;
+    const RowStage R = row_stage(F, C);
+    const bool act = fx < F.N && fx > 0 && R.fz > 0 && R.fz < F.N;
+    // the fine vertices' loads first: they stream from HBM while the block stages
+    double u[kStY], dg[kStY], r[kStY];
+    const int64_t vi0 = vidx3(F.N, min(fx, F.N), R.fy0, R.fz);
+#pragma unroll
+    for (int k = 0; k < kStY; ++k) {
+        const int fy = R.fy0 + k;
+        if (act && fy < R.fy1 && fy > 0 && fy < F.N) {
+            const int64_t vi = vi0 + static_cast<int64_t>(k) * (F.N + 1);
+            u[k] = __ldcs(F.v[LZB_V_U] + vi);
+            dg[k] = __ldcs(F.v[LZB_V_DIAG] + vi);
+            r[k] = __ldcs(F.v[LZB_V_R] + vi);
+        }
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    for (int q = warp; q < 2 * R.ny; q += nwarp) {  // a warp per staged coarse line
+        const int az = q & 1, iy = q >> 1;
+        const int64_t base = vidx3(C.N, 0, min(R.py0 + iy, C.N), R.pz + az);
+        for (int j = lane; j < R.nx; j += 32) s_pre[iy][az][j] = pre[base + min(R.px0 + j, C.N)];
     }
     __syncthreads();
-    if (fx > F.N || bnd3(F.N, fx, fy, fz)) return;
-    const int64_t vi = vidx3(F.N, fx, fy, fz);
+    const double wz0 = wax(R.lz, 0), wz1 = wax(R.lz, 1);
+    for (int k = warp; k < kStY; k += nwarp)  // a warp per fine row, lanes over the coarse x
+        for (int j = lane; j < R.nx; j += 32) {
+            const int fy = min(R.fy0 + k, F.N);
+            const int py = owner3(fy, C.N), ly = fy - 3 * py, jy = py - R.py0;
+            const double wy0 = wax(ly, 0), wy1 = wax(ly, 1);
+            const double2 c00 = s_pre[jy][0][j], c10 = s_pre[jy + 1][0][j], c01 = s_pre[jy][1][j],
+                          c11 = s_pre[jy + 1][1][j];
+            s_g[k][j] = make_double2(wz0 * (wy0 * c00.x + wy1 * c10.x) + wz1 * (wy0 * c01.x + wy1 * c11.x),
+                                     wz0 * (wy0 * c00.y + wy1 * c10.y) + wz1 * (wy0 * c01.y + wy1 * c11.y));
+            s_nz[k][j] = (c00.y != 0.0) | (c10.y != 0.0) | (c01.y != 0.0) | (c11.y != 0.0);
+        }
+    __syncthreads();
+    if (!act) return;
     const int px = owner3(fx, C.N), lx = fx - 3 * px, jx = px - R.px0;
-    const int wx[2] = {3 - lx, lx}, wy[2] = {3 - R.ly, R.ly}, wz[2] = {3 - R.lz, R.lz};
-    double u = F.v[LZB_V_U][vi];
-    const double dg = F.v[LZB_V_DIAG][vi], r = F.v[LZB_V_R][vi];
-    double2 c[8];
+    const double wx0 = wax(lx, 0), wx1 = wax(lx, 1);
 #pragma unroll
-    for (int a = 0; a < 8; ++a) c[a] = s_pre[((a >> 1) & 1) | ((a >> 2) << 1)][jx + (a & 1)];
-    if (pi) {
-        double p = 0.0;
-#pragma unroll
-        for (int a = 0; a < 8; ++a) p += s_w[wx[a & 1] * wy[(a >> 1) & 1] * wz[a >> 2]] * c[a].x;
-        u -= p;
+    for (int k = 0; k < kStY; ++k) {
+        const int fy = R.fy0 + k;
+        if (!(fy < R.fy1 && fy > 0 && fy < F.N)) continue;
+        const double2 g0 = s_g[k][jx], g1 = s_g[k][jx + 1];
+        double uu = u[k];
+        if (pi) uu -= wx0 * g0.x + wx1 * g1.x;
+        if (dg[k] != 0.0) uu += damping / dg[k] * r[k];
+        if (s_nz[k][jx] | s_nz[k][jx + 1]) uu += wx0 * g0.y + wx1 * g1.y;
+        __stcs(F.v[LZB_V_U] + vi0 + static_cast<int64_t>(k) * (F.N + 1), uu);
     }
-    if (dg != 0.0) u += damping / dg * r;
-    bool any = false;
-#pragma unroll
-    for (int a = 0; a < 8; ++a) any |= c[a].y != 0.0;
-    if (any) {
-        double p = 0.0;
-#pragma unroll
-        for (int a = 0; a < 8; ++a) p += s_w[wx[a & 1] * wy[(a >> 1) & 1] * wz[a >> 2]] * c[a].y;
-        u += p;
-    }
-    F.v[LZB_V_U][vi] = u;
 }
 
-__global__ void __launch_bounds__(128) k3_uhat_st(Lv3 F, Lv3 C) {
+// u-hat = u - P u_c on the leaf level (compute_uhat, solver.cpp:120-143 in 3D)
+__global__ void __launch_bounds__(kStThreads) k3_uhat_st(Lv3 F, Lv3 C) {
     lzb_pdl_enter();
-    __shared__ double s_u[4][kStX];
-    __shared__ double s_w[28];
-    const int fx = blockIdx.x * blockDim.x + threadIdx.x, fy = blockIdx.y, fz = blockIdx.z + F.z0;
-    const RowStage R = row_stage(F, C, fy, fz);
-    if (threadIdx.x < 28) s_w[threadIdx.x] = g_w27[threadIdx.x];
-    for (int t = threadIdx.x; t < 4 * R.nx; t += blockDim.x) {
-        const int q = t / R.nx, j = t - q * R.nx, cx = min(R.px0 + j, C.N);
-        s_u[q][j] = C.v[LZB_V_U][vidx3(C.N, cx, R.py + (q & 1), R.pz + (q >> 1))];
+    __shared__ double s_u[kStCy][2][kStX];
+    __shared__ double s_g[kStY][kStX];
+    const int fx = blockIdx.x * blockDim.x + threadIdx.x;
+    const RowStage R = row_stage(F, C);
+    double u[kStY];  // the fine loads first (see k3_update_fine_st)
+    const int64_t vi0 = vidx3(F.N, min(fx, F.N), R.fy0, R.fz);
+#pragma unroll
+    for (int k = 0; k < kStY; ++k)
+        if (fx <= F.N && R.fy0 + k < R.fy1) u[k] = __ldcs(F.v[LZB_V_U] + vi0 + static_cast<int64_t>(k) * (F.N + 1));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    for (int q = warp; q < 2 * R.ny; q += nwarp) {  // a warp per staged coarse line
+        const int az = q & 1, iy = q >> 1;
+        const int64_t base = vidx3(C.N, 0, min(R.py0 + iy, C.N), R.pz + az);
+        for (int j = lane; j < R.nx; j += 32) s_u[iy][az][j] = C.v[LZB_V_U][base + min(R.px0 + j, C.N)];
     }
     __syncthreads();
+    const double wz0 = wax(R.lz, 0), wz1 = wax(R.lz, 1);
+    for (int k = warp; k < kStY; k += nwarp)  // a warp per fine row, lanes over the coarse x
+        for (int j = lane; j < R.nx; j += 32) {
+            const int fy = min(R.fy0 + k, F.N);
+            const int py = owner3(fy, C.N), ly = fy - 3 * py, jy = py - R.py0;
+            s_g[k][j] = wz0 * (wax(ly, 0) * s_u[jy][0][j] + wax(ly, 1) * s_u[jy + 1][0][j]) +
+                        wz1 * (wax(ly, 0) * s_u[jy][1][j] + wax(ly, 1) * s_u[jy + 1][1][j]);
+        }
+    __syncthreads();
     if (fx > F.N) return;
-    const int64_t vi = vidx3(F.N, fx, fy, fz);
     const int px = owner3(fx, C.N), lx = fx - 3 * px, jx = px - R.px0;
-    const int wx[2] = {3 - lx, lx}, wy[2] = {3 - R.ly, R.ly}, wz[2] = {3 - R.lz, R.lz};
-    const double u = F.v[LZB_V_U][vi];
-    double interp = 0.0;
+    const double wx0 = wax(lx, 0), wx1 = wax(lx, 1);
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
-        interp += s_w[wx[a & 1] * wy[(a >> 1) & 1] * wz[a >> 2]] * s_u[((a >> 1) & 1) | ((a >> 2) << 1)][jx + (a & 1)];
-    F.v[LZB_V_UHAT][vi] = u - interp;
+    for (int k = 0; k < kStY; ++k) {
+        if (R.fy0 + k >= R.fy1) continue;
+        __stcs(F.v[LZB_V_UHAT] + vi0 + static_cast<int64_t>(k) * (F.N + 1),
+               u[k] - (wx0 * s_g[k][jx] + wx1 * s_g[k][jx + 1]));
+    }
 }
 
 __global__ void k3_inject(Lv3 F, Lv3 C) {
@@ -1802,7 +1848,11 @@ private:
     // with a coarse level below) through the staged row kernel
     void uhat3(int l, int z0, int z1) {
         if (l == 0) LZB_LAUNCH(k3_uhat, vgz(0, z0, z1), 128, 0, s_, lvz(0, z0), lv(0), 0);
-        else LZB_LAUNCH(k3_uhat_st, vgz(l, z0, z1), 128, 0, s_, lvz(l, z0), lv(l - 1));
+        else LZB_LAUNCH(k3_uhat_st, vgst(l, z0, z1), kStThreads, 0, s_, lvz(l, z0), lv(l - 1));
+    }
+    // the staged row kernels: 128 x, kStY rows, one plane per block
+    dim3 vgst(int l, int z0, int z1) const {
+        return dim3(blocks_for(L3_[l].N + 1, kStThreads), (L3_[l].N + kStY) / kStY, z1 - z0);
     }
     // the leaf level's fused update on vertex planes [z0, z1): the coarse
     // factors (aux correction, prolongated correction) once per coarse vertex,
@@ -1810,7 +1860,7 @@ private:
     void update_fine3(int z0, int z1, bool pi, double damping) {
         if (pre3_.n < static_cast<size_t>(L3_[D_ - 1].nv)) pre3_.alloc(L3_[D_ - 1].nv);
         LZB_LAUNCH(k3_coarse_pre, vg(D_ - 1), 128, 0, s_, lv(D_ - 1), omega_, pi ? 1 : 0, pre3_.p);
-        LZB_LAUNCH(k3_update_fine_st, vgz(D_, z0, z1), 128, 0, s_, lvz(D_, z0), lv(D_ - 1), pre3_.p, pi ? 1 : 0,
+        LZB_LAUNCH(k3_update_fine_st, vgst(D_, z0, z1), kStThreads, 0, s_, lvz(D_, z0), lv(D_ - 1), pre3_.p, pi ? 1 : 0,
                    damping);
     }
     DevBuf<double2> pre3_;
