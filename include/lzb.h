@@ -195,6 +195,26 @@ int lzb_grid_plane_arrays(lzb_grid* g, void** planes, void** cp3, int* width);
 int lzb_grid_dist_phase(lzb_grid* g, int phase, int flags);
 int lzb_grid_dist_result(lzb_grid* g, double* norm2, uint64_t* slots20);
 int lzb_grid_dist_report(lzb_grid* g, double norm2, const uint64_t* slots20, lzb_cycle_report* rep);
+/* ---- the slab-distributed data plane in C++ (csrc/dist.cpp)
+ * The context owns an NCCL communicator (NCCL loaded at run time); one
+ * distributed cycle is the phases above with NCCL send/recv halos, in-place
+ * broadcasts of the replicated level D-1 rows and an on-device all-reduce of
+ * the norm and counters, all on the solve stream, one host read per cycle.
+ * The _loopback forms run the same plan over several slabs of one process
+ * (device copies instead of NCCL): the one-GPU check of the plan. */
+int lzb_nccl_unique_id(uint8_t* out128);
+int lzb_ctx_comm_init(lzb_ctx* ctx, const uint8_t* id128, int nranks, int rank);
+int lzb_ctx_comm_info(lzb_ctx* ctx, int* rank, int* nranks);
+int lzb_grid_dist_cycle(lzb_grid* g, lzb_cycle_report* out);
+int lzb_grid_dist_cycle_loopback(lzb_grid* const* slabs, int nslabs, lzb_cycle_report* out);
+/* slab assembly (each rank its leaf cell rows) + exchange of the leaf state */
+int lzb_grid_dist_assemble(lzb_grid* g, int n);
+int lzb_grid_dist_assemble_loopback(lzb_grid* const* slabs, int nslabs, int n);
+/* introspection for the data plane: context, depth, descriptor, the device
+ * address of the phase-2 result (double norm^2, then 20 u64 counter slots) */
+int lzb_grid_info(lzb_grid* g, lzb_ctx** ctx, int* depth);
+int lzb_grid_desc_of(lzb_grid* g, lzb_grid_desc* out);
+int lzb_grid_dist_result_dev(lzb_grid* g, void** result);
 /* Device time (CUDA events on the solve stream) of one hot kernel of the
  * leaf level, averaged over `reps` back-to-back launches: LZB_TK_* ids.
  * No reference counterpart: the measurement hook behind bench.py's roofline. */
@@ -251,6 +271,16 @@ int lzb_grid3_set_slab(lzb_grid3* g, int v0, int v1);
 int lzb_grid3_dist_phase(lzb_grid3* g, int phase);
 int lzb_grid3_dist_result(lzb_grid3* g, double* norm2);
 int lzb_grid3_dist_report(lzb_grid3* g, double norm2, lzb_cycle_report* out);
+/* the C++ data plane for the 3D grid (see lzb_grid_dist_cycle); assemble:
+ * the z-slab sharded assembly below with the level D-1 class planes exchanged */
+int lzb_grid3_dist_cycle(lzb_grid3* g, lzb_cycle_report* out);
+int lzb_grid3_dist_cycle_loopback(lzb_grid3* const* slabs, int nslabs, lzb_cycle_report* out);
+int lzb_grid3_dist_assemble(lzb_grid3* g, int n);
+int lzb_grid3_dist_assemble_loopback(lzb_grid3* const* slabs, int nslabs, int n);
+int lzb_grid3_dist_phase_flags(lzb_grid3* g, int phase, int flags);
+int lzb_grid3_dist_result_dev(lzb_grid3* g, void** norm2);
+int lzb_grid3_info(lzb_grid3* g, lzb_ctx** ctx, int* depth);
+int lzb_grid3_variant(lzb_grid3* g);
 /* z-slab sharded 3D assembly (parallel.distributed_assemble3): fixed-p
  * assembly of the leaf cells in z planes [cz0, cz1); the Galerkin coarse
  * operators of `level` for its coarse cells in z planes [pz0, pz1); every

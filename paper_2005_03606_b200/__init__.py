@@ -162,6 +162,17 @@ def lib():
         L.lzb_grid3_device_view.argtypes = [vp, C.c_int, C.c_int, C.POINTER(vp)]
         L.lzb_grid_plane_arrays.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(C.c_int)]
         L.lzb_grid_dist_phase.argtypes = [vp, C.c_int, C.c_int]
+        L.lzb_nccl_unique_id.argtypes = [vp]
+        L.lzb_ctx_comm_init.argtypes = [vp, vp, C.c_int, C.c_int]
+        L.lzb_ctx_comm_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.lzb_grid_dist_cycle.argtypes = [vp, C.POINTER(CycleReport)]
+        L.lzb_grid_dist_cycle_loopback.argtypes = [vp, C.c_int, C.POINTER(CycleReport)]
+        L.lzb_grid_dist_assemble.argtypes = [vp, C.c_int]
+        L.lzb_grid_dist_assemble_loopback.argtypes = [vp, C.c_int, C.c_int]
+        L.lzb_grid3_dist_cycle.argtypes = [vp, C.POINTER(CycleReport)]
+        L.lzb_grid3_dist_cycle_loopback.argtypes = [vp, C.c_int, C.POINTER(CycleReport)]
+        L.lzb_grid3_dist_assemble.argtypes = [vp, C.c_int]
+        L.lzb_grid3_dist_assemble_loopback.argtypes = [vp, C.c_int, C.c_int]
         L.lzb_grid_dist_result.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
         L.lzb_grid_dist_report.argtypes = [vp, C.c_double, C.POINTER(C.c_uint64), C.POINTER(CycleReport)]
         L.lzb_run_experiment_file.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
@@ -211,6 +222,43 @@ class Context:
     @property
     def solve_stream(self):
         return lib().lzb_ctx_solve_stream(self.h)
+
+    def comm_init(self, unique_id: bytes, nranks: int, rank: int):
+        """The context's NCCL communicator for the C++ slab data plane
+        (unique_id from nccl_unique_id() on rank 0, shared by the launcher)."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        _check(lib().lzb_ctx_comm_init(self.h, buf, nranks, rank))
+
+    def comm_info(self):
+        r, n = C.c_int(), C.c_int()
+        _check(lib().lzb_ctx_comm_info(self.h, C.byref(r), C.byref(n)))
+        return r.value, n.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().lzb_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def _handles(grids):
+    arr = (C.c_void_p * len(grids))(*[g.h.value if isinstance(g.h, C.c_void_p) else g.h for g in grids])
+    return arr
+
+
+def dist_cycle_loopback(grids) -> dict:
+    """One slab-distributed cycle of the C++ data plane over several slab grids
+    of this process (slab i of len(grids); device copies instead of NCCL)."""
+    r = CycleReport()
+    fn = lib().lzb_grid3_dist_cycle_loopback if isinstance(grids[0], Grid3) else lib().lzb_grid_dist_cycle_loopback
+    _check(fn(_handles(grids), len(grids), C.byref(r)))
+    return report_dict(r)
+
+
+def dist_assemble_loopback(grids, n):
+    fn = (lib().lzb_grid3_dist_assemble_loopback if isinstance(grids[0], Grid3)
+          else lib().lzb_grid_dist_assemble_loopback)
+    _check(fn(_handles(grids), len(grids), n))
 
 
 _default_ctx = None
@@ -464,6 +512,16 @@ class Grid:
         return [report_dict(arr[i]) for i in range(min(cap, n.value))]
 
     # slab-distributed cycle (parallel.py drives the phases and the exchanges)
+    def dist_cycle(self) -> dict:
+        """One slab-distributed cycle over the context's NCCL communicator
+        (this rank's slab; the C++ data plane, csrc/dist.cpp)."""
+        r = CycleReport()
+        _check(lib().lzb_grid_dist_cycle(self.h, C.byref(r)))
+        return report_dict(r)
+
+    def dist_assemble(self, n):
+        _check(lib().lzb_grid_dist_assemble(self.h, n))
+
     def set_slab(self, v0, v1):
         _check(lib().lzb_grid_set_slab(self.h, v0, v1))
 
@@ -791,6 +849,17 @@ class Grid3:
         return report_dict(r)
 
     # slab-distributed cycle (parallel.dist_cycle3)
+    def dist_cycle(self) -> dict:
+        """One z-slab-distributed cycle over the context's NCCL communicator
+        (the C++ data plane, csrc/dist.cpp; after init_cycle)."""
+        r = CycleReport()
+        _check(lib().lzb_grid3_dist_cycle(self.h, C.byref(r)))
+        return report_dict(r)
+
+    def dist_assemble(self, n):
+        """z-slab sharded assembly + the level-(D-1) class-plane exchange (NCCL)."""
+        _check(lib().lzb_grid3_dist_assemble(self.h, n))
+
     def set_slab(self, v0, v1):
         _check(lib().lzb_grid3_set_slab(self.h, v0, v1))
 

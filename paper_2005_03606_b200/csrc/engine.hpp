@@ -137,10 +137,14 @@ struct lzb_ctx {
     cudaStream_t solve = nullptr;
     cudaStream_t assembly = nullptr;
     lzb::DevBuf<int> err;  // device error flag (non-finite encode etc.)
+    // NCCL communicator of the slab-distributed data plane (dist.cpp; null: none)
+    void* comm = nullptr;
+    int comm_rank = 0, comm_size = 1;
 };
 
 namespace lzb {
 lzb_ctx* make_ctx(int device);
+void release_comm(lzb_ctx* c);  // dist.cpp
 void destroy_ctx(lzb_ctx* c);
 // Throws LZB_ERR_PROTOCOL if a device kernel raised the error flag since the last check.
 void check_device_flag(lzb_ctx* c, cudaStream_t s);

@@ -2566,6 +2566,7 @@ public:
     dim3 ugrid(int l) const { return dim3(blocks_for((L_[l].N + 1) / 2, kThreads), L_[l].N + 1); }
     dim3 ugrid_rows(int l, int r0, int r1) const { return dim3(blocks_for((L_[l].N + 1) / 2, kThreads), r1 - r0); }
     const lzb_grid_desc& desc() const { return d_; }
+    lzb_ctx* context() const { return ctx_; }
     int depth() const { return D_; }
     uint32_t cycle() const { return cycle_; }
 
@@ -3352,8 +3353,10 @@ public:
                     LZB_LAUNCH(k_residual, g, kThreads, 0, s_, V(l), d_.field);
                     if (l > 0) LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1), 0, 0.0);
                 }
-                LZB_CUDA(cudaMemcpyAsync(hres_, res_.p, sizeof(Result), cudaMemcpyDeviceToHost, s_));
-                sync_check();
+                if (!(flags & 2)) {  // flags bit 1: the C++ data plane reduces on the device (dist.cpp)
+                    LZB_CUDA(cudaMemcpyAsync(hres_, res_.p, sizeof(Result), cudaMemcpyDeviceToHost, s_));
+                    sync_check();
+                }
                 break;
             case 3:
                 for (int l = 0; l < D_; ++l)
@@ -3382,12 +3385,15 @@ public:
             case 5:
                 for (int l = D_ - 1; l >= 1; --l)
                     LZB_LAUNCH(k_inject, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1));
-                sync_check();
+                if (!(flags & 2)) sync_check();
                 break;
             default: throw Error(LZB_ERR_INVALID, "unknown phase");
         }
     }
 
+    // Device address of the phase-2 result (sum of r^2, then the 20 counter
+    // slots as u64) for an on-device reduction (dist.cpp)
+    void* dist_result_dev() const { return res_.p; }
     // Result of phase 2 for the host reduction: the slab's sum of r^2 and the
     // 20 counter slots.
     void dist_result(double* norm2, uint64_t* slots) const {
@@ -4073,11 +4079,23 @@ int lzb_grid_stream_image(lzb_grid* g, uint8_t* out, int64_t cap, int64_t* size)
 int lzb_grid_plane_arrays(lzb_grid* g, void** planes, void** cp3, int* width) {
     return guarded([&] { g->g->plane_arrays(planes, cp3, width); });
 }
+int lzb_grid_desc_of(lzb_grid* g, lzb_grid_desc* out) {
+    return guarded([&] { *out = g->g->desc(); });
+}
+int lzb_grid_info(lzb_grid* g, lzb_ctx** ctx, int* depth) {
+    return guarded([&] {
+        if (ctx) *ctx = g->g->context();
+        if (depth) *depth = g->g->depth();
+    });
+}
 int lzb_grid_set_slab(lzb_grid* g, int v0, int v1) {
     return guarded([&] { g->g->set_slab(v0, v1); });
 }
 int lzb_grid_dist_phase(lzb_grid* g, int phase, int flags) {
     return guarded([&] { g->g->dist_phase(phase, flags); });
+}
+int lzb_grid_dist_result_dev(lzb_grid* g, void** result) {
+    return guarded([&] { *result = g->g->dist_result_dev(); });
 }
 int lzb_grid_dist_result(lzb_grid* g, double* norm2, uint64_t* slots20) {
     return guarded([&] { g->g->dist_result(norm2, slots20); });

@@ -841,6 +841,15 @@ __global__ void k3_norm_partial(Lv3 F, double* partial, int zlo, int zhi) {
     if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
 }
 
+// the slab's sum of r^2 from the norm partials, the host loop's order (step())
+__global__ void k3_sum_partials(const double* partial, int n, double* out) {
+    lzb_pdl_enter();
+    if (threadIdx.x != 0) return;
+    double s2 = 0.0;
+    for (int i = 0; i < n; ++i) s2 += partial[i];
+    *out = s2;
+}
+
 __global__ void k3_snap(Lv3 L, int64_t nv) {
     lzb_pdl_enter();
     const int64_t i = gtid();
@@ -1601,7 +1610,11 @@ public:
     }
     dim3 vgz(int l, int z0, int z1) const { return dim3(blocks_for(L3_[l].N + 1, 128), L3_[l].N + 1, z1 - z0); }
 
-    void dist_phase(int phase) {
+    void* dist_result_dev() const { return res3_.p; }
+    lzb_ctx* context() const { return ctx_; }
+    int depth() const { return D_; }
+    int variant() const { return variant_; }
+    void dist_phase(int phase, int flags = 0) {
         if (L3_.empty()) throw Error(LZB_ERR_INVALID, "call init_cycle first");
         const int N = L3_[D_].N, v0 = sv0_, v1 = sv1_ < 0 ? N + 1 : sv1_;
         const int c0 = v0 / 3, c1 = (v1 + 2) / 3;
@@ -1627,6 +1640,10 @@ public:
                     uhat3(l, 0, L3_[l].N + 1);
                     residual3(l, 0, L3_[l].N + 1);
                     if (l > 0) LZB_LAUNCH(k3_restrict, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
+                }
+                if (flags & 2) {  // the C++ data plane: the slab's norm^2 stays on the device (dist.cpp)
+                    LZB_LAUNCH(k3_sum_partials, 1, 32, 0, s_, partial3_.p, kNormBlocks3, res3_.p);
+                    break;
                 }
                 std::vector<double> part(kNormBlocks3);
                 LZB_CUDA(cudaMemcpyAsync(part.data(), partial3_.p, kNormBlocks3 * sizeof(double),
@@ -1658,7 +1675,7 @@ public:
             }
             case 5:
                 for (int l = D_ - 1; l >= 1; --l) LZB_LAUNCH(k3_inject, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
-                sync();
+                if (!(flags & 2)) sync();
                 break;
             default: throw Error(LZB_ERR_INVALID, "unknown phase");
         }
@@ -1959,6 +1976,12 @@ int lzb_grid3_set_slab(lzb_grid3* g, int v0, int v1) {
 int lzb_grid3_dist_phase(lzb_grid3* g, int phase) {
     return lzb::guarded([&] { g->g->dist_phase(phase); });
 }
+int lzb_grid3_dist_phase_flags(lzb_grid3* g, int phase, int flags) {
+    return lzb::guarded([&] { g->g->dist_phase(phase, flags); });
+}
+int lzb_grid3_dist_result_dev(lzb_grid3* g, void** norm2) {
+    return lzb::guarded([&] { *norm2 = g->g->dist_result_dev(); });
+}
 int lzb_grid3_dist_result(lzb_grid3* g, double* norm2) {
     return lzb::guarded([&] { *norm2 = g->g->dist_norm2(); });
 }
@@ -1981,6 +2004,13 @@ int lzb_grid3_coarse_below(lzb_grid3* g, int level) {
     return lzb::guarded([&] {
         g->g->coarse_below(level);
         g->g->sync();
+    });
+}
+int lzb_grid3_variant(lzb_grid3* g) { return g->g->variant(); }
+int lzb_grid3_info(lzb_grid3* g, lzb_ctx** ctx, int* depth) {
+    return lzb::guarded([&] {
+        if (ctx) *ctx = g->g->context();
+        if (depth) *depth = g->g->depth();
     });
 }
 int lzb_grid3_level_ops(lzb_grid3* g, int level, void** ptr) {

@@ -68,6 +68,7 @@ lzb_ctx* make_ctx(int device) {
 void destroy_ctx(lzb_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    release_comm(c);
     if (c->solve) cudaStreamDestroy(c->solve);
     if (c->assembly) cudaStreamDestroy(c->assembly);
     delete c;
