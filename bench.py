@@ -293,6 +293,11 @@ def run_ours(args, world, rank, local):
     torch.cuda.set_device(local)
     ctx = lzb.Context(local)
     stream = torch.cuda.ExternalStream(ctx.solve_stream)
+    import torch.distributed as dist
+    if dist.is_initialized():  # the context's NCCL communicator for the C++ data plane (csrc/dist.cpp)
+        box = [lzb.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        ctx.comm_init(box[0], world, rank)
     f = lzb.field_sinusoid(0.9, 6.0)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")  # > 126 MB L2
 
@@ -559,15 +564,13 @@ def run_ours(args, world, rank, local):
     import torch.distributed as tdist5
     if tdist5.is_initialized():
         # z-slab sharded assembly (each rank its leaf planes + its level-5 Galerkin
-        # planes, one NCCL all-gather of those), then the slab-distributed cycle
-        from paper_2005_03606_b200 import parallel as par5
+        # planes, one NCCL exchange of those), then the slab-distributed cycle: the
+        # C++ data plane (csrc/dist.cpp) over the context's NCCL communicator
         g5.init_cycle(solver="adafac-pi", omega=0.6, max_cycles=10 ** 6)
-        slab5 = par5.Slab3(g5, rank, world)
-        comm5 = par5.TorchComm(stream=stream)
-        par5.distributed_assemble3([slab5], comm5, 2)
-        t5 = max_over_ranks(timed_steps(lambda: par5.distributed_assemble3([slab5], comm5, 2), 2) / 2, world)
+        g5.dist_assemble(2)
+        t5 = max_over_ranks(timed_steps(lambda: g5.dist_assemble(2), 2) / 2, world)
         c5["assembly"] = {"ms": 1e3 * t5, "sub_samples_per_s": 3 ** 18 * 8 / t5, "scaling": "strong",
-                          "mode": f"z-slabs over {world} ranks: slab assembly + level-5 Galerkin + all-gather"}
+                          "mode": f"z-slabs over {world} ranks: slab assembly + level-5 Galerkin + NCCL broadcasts"}
     else:
         g5.assemble_fixed(2)
         t5 = timed_steps(lambda: g5.assemble_fixed(2), 2) / 2
@@ -576,9 +579,10 @@ def run_ours(args, world, rank, local):
                           "lzmg_bytes_per_cell": st5.fine_stored_bytes / st5.fine_cells}
         g5.init_cycle(solver="adafac-pi", omega=0.6, max_cycles=10 ** 6)
     if tdist5.is_initialized():
-        par5.dist_cycle3([slab5], comm5, True)
-        t5c = timed_steps(lambda: par5.dist_cycle3([slab5], comm5, True), 3) / 3
-        c5["cycles"] = {"mode": f"z-slabs over {world} ranks, NCCL halos / all-gathers", "scaling": "strong"}
+        g5.dist_cycle()
+        t5c = timed_steps(lambda: g5.dist_cycle(), 3) / 3
+        c5["cycles"] = {"mode": f"z-slabs over {world} ranks, C++ data plane: NCCL halos / broadcasts / all-reduce",
+                        "scaling": "strong"}
     else:
         g5.step()  # builds the coarse operators
         t5c = timed_steps(lambda: g5.step(), 3) / 3
@@ -627,15 +631,14 @@ def run_ours(args, world, rank, local):
     strong = None
     import torch.distributed as tdist
     if tdist.is_initialized():
-        from paper_2005_03606_b200 import parallel
         gs = make(head)
-        parallel.distributed_assemble(gs, P)  # warm-up
-        ts = timed_steps(lambda: parallel.distributed_assemble(gs, P), args.steps)
+        gs.dist_assemble(P)  # warm-up
+        ts = timed_steps(lambda: gs.dist_assemble(P), args.steps)
         ts = max_over_ranks(ts, world)
         strong = {"value": SAMPLES_PER_STEP * args.steps / ts, "unit": "sub-samples/s",
                   "ms_per_step": 1e3 * ts / args.steps, "scaling": "strong", "ranks": world,
-                  "what": "slab assembly of one 729^2 p=32 pass split over the ranks + NCCL all-gather "
-                          "of the leaf operators/markers (replicated solve follows)"}
+                  "what": "slab assembly of one 729^2 p=32 pass split over the ranks + NCCL broadcasts "
+                          "of the leaf operators/markers (C++ data plane; replicated solve follows)"}
         gs.close()
         del gs
         # slab-distributed cycle (strong scaling on the 6561^2 grid): leaf rows split
@@ -643,18 +646,17 @@ def run_ours(args, world, rank, local):
         gd = lzb.Grid(lzb.make_desc(depth=HBM_LEVEL, field=f, delta_max=1e-8, solver="adafac-pi", omega=0.6,
                                     rhs_kind="sinprod", integration="fast", max_cycles=10 ** 6), 42, ctx)
         gd.assemble_fixed(4)
-        slab = parallel.Slab(gd, rank, world)
-        comm = parallel.TorchComm(stream=stream)
         for _ in range(2):
-            parallel.dist_cycle([slab], comm, True)
+            gd.dist_cycle()
         kd = max(3, args.steps)
-        td = timed_steps(lambda: parallel.dist_cycle([slab], comm, True), kd)
+        td = timed_steps(lambda: gd.dist_cycle(), kd)
         td = max_over_ranks(td, world)
         dofd = (3 ** HBM_LEVEL - 1) ** 2
         strong["smoother"] = {"value": dofd * kd / td, "unit": "DoF-updates/s", "ms_per_cycle": 1e3 * td / kd,
                               "scaling": "strong", "ranks": world,
                               "what": f"{3 ** HBM_LEVEL}^2 adaFAC-PI cycle, leaf rows in slabs, coarse levels "
-                                      "replicated, NCCL halo + all-gather exchanges (parallel.dist_cycle)"}
+                                      "replicated; C++ data plane (csrc/dist.cpp): NCCL send/recv halos, "
+                                      "broadcasts of level D-1, on-device all-reduce"}
         gd.close()
         del gd
 
