@@ -15,6 +15,9 @@
 // contributing cells in the reference's creation-rank order, so the solver
 // state is bit-identical to the reference (tests/test_gpu_parity.py).
 #include <algorithm>
+#include <array>
+#include <deque>
+#include <unordered_map>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -574,12 +577,19 @@ __global__ void __launch_bounds__(kIntThreads, 2) k_fixed_res(LevelView F, lzb_f
 // Each child entry feeds exactly one A entry, so the 144 child values are read
 // once each, straight from the (L1/L2-resident) fine operator array.
 constexpr int kCoarseThreads = 128;
+// only != null: the coarse_recompute tasks of a throttled ripple batch (cells
+// of this level, one launch per dependency generation), run unconditionally
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_geo(LevelView C, LevelView F, lzb_field f,
                                                                double delta_max, const uint32_t* cycle_ptr,
-                                                               unsigned long long* stats, int* err) {
+                                                               unsigned long long* stats, int* err,
+                                                               const int32_t* only, int nonly) {
     lzb_pdl_enter();
     const uint32_t cycle = *cycle_ptr;  // device-resident: the cycle is replayed as a CUDA graph
     int64_t c = gtid();
+    if (only) {
+        if (c >= nonly) return;
+        c = only[c];
+    }
     if (c >= static_cast<int64_t>(C.N) * C.N) return;
     const int cx = static_cast<int>(c % C.N), cy = static_cast<int>(c / C.N);
 
@@ -589,7 +599,8 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_geo(LevelView C, Leve
     // changed since the last attempt reproduces the stored result bit for bit
     // and publish_coarse would be a no-op (stream.cpp:153-158), so those
     // patches are skipped
-    if (C.pend) {
+    if (only) {
+    } else if (C.pend) {
         if (!C.pend[c]) return;
         C.pend[c] = 0;
     } else {
@@ -702,10 +713,15 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_geo(LevelView C, Leve
 // operator A for the operator-dependent prolongation, transfer.cpp:95-180).
 __global__ void __launch_bounds__(64) k_coarse(LevelView C, LevelView F, lzb_field f, int boxmg,
                                                double delta_max, const uint32_t* cycle_ptr,
-                                               unsigned long long* stats, int* err) {
+                                               unsigned long long* stats, int* err, const int32_t* only,
+                                               int nonly) {
     lzb_pdl_enter();
     const uint32_t cycle = *cycle_ptr;
     int64_t c = gtid();
+    if (only) {
+        if (c >= nonly) return;
+        c = only[c];
+    }
     if (c >= static_cast<int64_t>(C.N) * C.N) return;
     int cx = static_cast<int>(c % C.N), cy = static_cast<int>(c / C.N);
 
@@ -715,7 +731,8 @@ __global__ void __launch_bounds__(64) k_coarse(LevelView C, LevelView F, lzb_fie
     // changed since the last attempt reproduces the stored result bit for bit
     // and publish_coarse would be a no-op (stream.cpp:153-158), so those
     // patches are skipped
-    if (C.pend) {
+    if (only) {
+    } else if (C.pend) {
         if (!C.pend[c]) return;
         C.pend[c] = 0;
     } else {
@@ -2436,7 +2453,6 @@ public:
         partial_.alloc(kNormBlocks);
         if (d.variant == LZB_ADAFAC_PI && D_ >= 1) caux_.alloc(L_[D_ - 1].nv);
         if (d.policy == LZB_RIPPLE) {
-            if (d.throttle) throw Error(LZB_ERR_INVALID, "coarse-recompute = ripple runs every task (throttle = 0)");
             if (d.concurrent) throw Error(LZB_ERR_INVALID, "coarse-recompute = ripple needs the deterministic modes");
             for (int l = 0; l < D_; ++l) {
                 L_[l].dirty.alloc(L_[l].nc);
@@ -2672,7 +2688,8 @@ public:
     // TaskPool::drain_all (scheduler.cpp:125-141): finish every pending task.
     void drain() {
         if (d_.concurrent) try_commit(true);
-        if (ripple()) ripple_tasks();  // the high class first (scheduler.cpp:125-141)
+        if (ripple_fifo()) ripple_run_fifo(-1);  // the high class first (scheduler.cpp:125-141)
+        else if (ripple()) ripple_tasks();
         if (d_.mode == LZB_ANARCHIC || d_.forced_fraction > 0.0) {
             while (count_pending() > 0) round(1, true);
         }
@@ -2758,10 +2775,11 @@ public:
             const int l = post_order ? D_ - 1 - i : i;
             if (d_.transfer == LZB_BOXMG)
                 LZB_LAUNCH(k_coarse, blocks_for(L_[l].nc, 64), 64, 0, s_, V(l), V(l + 1), d_.field, 1,
-                           d_.delta_max, dcycle_.p, res_.p->s, ctx_->err.p);
+                           d_.delta_max, dcycle_.p, res_.p->s, ctx_->err.p, static_cast<const int32_t*>(nullptr), 0);
             else
                 LZB_LAUNCH(k_coarse_geo, blocks_for(L_[l].nc, kCoarseThreads), kCoarseThreads, 0, s_,
-                           V(l), V(l + 1), d_.field, d_.delta_max, dcycle_.p, res_.p->s, ctx_->err.p);
+                           V(l), V(l + 1), d_.field, d_.delta_max, dcycle_.p, res_.p->s, ctx_->err.p,
+                           static_cast<const int32_t*>(nullptr), 0);
         }
     }
     void coarse_pass() { coarse_pass_order(false); }
@@ -2822,12 +2840,16 @@ public:
         inject();
     }
 
-    void pool_begin_cycle() {  // TaskPool::begin_cycle, workers = 1 (scheduler.cpp:88-111)
+    // budget: the leaf tasks this begin_cycle may run (the cycle's throttle
+    // minus the high-class tasks already run; -1 = unlimited)
+    void pool_begin_cycle(int64_t budget = -2) {  // TaskPool::begin_cycle, workers = 1 (scheduler.cpp:88-111)
+        if (budget == -2) budget = d_.throttle ? static_cast<int64_t>(d_.throttle) : -1;
         // step tasks (anarchic) and forced tasks (any mode) are the leaf tasks
-        if (pending_ == 0 || (d_.mode != LZB_ANARCHIC && d_.forced_fraction <= 0.0)) return;
+        const int64_t leaf_pending = pending_ - static_cast<int64_t>(hq_pending_at_report_);
+        if (leaf_pending <= 0 || budget == 0 || (d_.mode != LZB_ANARCHIC && d_.forced_fraction <= 0.0)) return;
         long long limit = -1;
-        if (d_.throttle && static_cast<uint64_t>(pending_) > d_.throttle) {
-            // FIFO: only the `throttle` oldest spawns run this cycle
+        if (budget > 0 && leaf_pending > budget) {
+            // FIFO: only the `budget` oldest spawns run this cycle
             std::vector<long long> k(leaves_);
             std::vector<uint8_t> p2(leaves_);
             LZB_CUDA(cudaMemcpyAsync(k.data(), keys_.p, leaves_ * sizeof(long long), cudaMemcpyDeviceToHost, s_));
@@ -2836,11 +2858,103 @@ public:
             std::vector<long long> pend;
             for (int64_t c = 0; c < leaves_; ++c)
                 if (p2[c]) pend.push_back(k[c]);
-            std::nth_element(pend.begin(), pend.begin() + (d_.throttle - 1), pend.end());
-            limit = pend[d_.throttle - 1];
+            std::nth_element(pend.begin(), pend.begin() + (budget - 1), pend.end());
+            limit = pend[budget - 1];
         }
         round(1, true, limit);
     }
+
+    // ---- coarse-recompute = ripple with a throttle: the high class as a real
+    // FIFO (TaskPool high_, scheduler.cpp:95-111) on the host -- spawns in
+    // pre-order per walk, duplicates allowed, at most `throttle` tasks (high
+    // class first) per begin_cycle. A batch runs in dependency generations
+    // (a task waits for an earlier one on the same cell, its parent or a
+    // child: it reads the children's operators), one launch per generation
+    // and level over the listed cells.
+    static int32_t task_code(int l, int64_t c) { return static_cast<int32_t>((l << 27) | c); }
+    void build_preorder() {  // the walk order of the refined cells (solver.cpp:79-97, mesh.cpp:140-157)
+        preorder_.clear();
+        std::vector<std::array<int, 3>> st{{0, 0, 0}};
+        while (!st.empty()) {
+            auto [l, cx, cy] = st.back();
+            st.pop_back();
+            if (l >= D_) continue;
+            preorder_.push_back(task_code(l, static_cast<int64_t>(cy) * L_[l].N + cx));
+            for (int k = 8; k >= 0; --k)  // child lx * 3 + ly, pushed in reverse
+                st.push_back({l + 1, 3 * cx + k / 3, 3 * cy + k % 3});
+        }
+    }
+    // after the walk's take_dirty launches: the flagged cells, in pre-order, join the FIFO
+    void ripple_spawn_fifo() {
+        if (preorder_.empty()) build_preorder();
+        std::vector<std::vector<uint8_t>> fl(D_);
+        for (int l = 0; l < D_; ++l) {
+            fl[l].resize(L_[l].nc);
+            LZB_CUDA(cudaMemcpyAsync(fl[l].data(), L_[l].pend.p, L_[l].nc, cudaMemcpyDeviceToHost, s_));
+        }
+        sync_check();
+        for (int32_t code : preorder_) {
+            const int l = code >> 27;
+            if (fl[l][code & ((1 << 27) - 1)]) hq_.push_back(code);
+        }
+        for (int l = 0; l < D_; ++l) LZB_CUDA(cudaMemsetAsync(L_[l].pend.p, 0, L_[l].nc, s_));
+    }
+    // the first `budget` FIFO tasks (-1: all); returns how many ran
+    int64_t ripple_run_fifo(int64_t budget) {
+        const int64_t k = budget < 0 ? static_cast<int64_t>(hq_.size())
+                                     : std::min<int64_t>(budget, static_cast<int64_t>(hq_.size()));
+        if (k == 0) return 0;
+        std::vector<int32_t> batch(hq_.begin(), hq_.begin() + k);
+        hq_.erase(hq_.begin(), hq_.begin() + k);
+        std::unordered_map<int32_t, int> gen_of;
+        std::vector<int> gen(k);
+        int ngen = 0;
+        for (int64_t i = 0; i < k; ++i) {
+            const int l = batch[i] >> 27;
+            const int64_t c = batch[i] & ((1 << 27) - 1);
+            const int cx = static_cast<int>(c % L_[l].N), cy = static_cast<int>(c / L_[l].N);
+            int g = 0;
+            auto dep = [&](int32_t code) {
+                auto it = gen_of.find(code);
+                if (it != gen_of.end()) g = std::max(g, it->second + 1);
+            };
+            dep(batch[i]);
+            if (l > 0) dep(task_code(l - 1, static_cast<int64_t>(cy / 3) * L_[l - 1].N + cx / 3));
+            if (l + 1 < D_)
+                for (int k9 = 0; k9 < 9; ++k9)
+                    dep(task_code(l + 1, static_cast<int64_t>(3 * cy + k9 % 3) * L_[l + 1].N + 3 * cx + k9 / 3));
+            gen[i] = g;
+            gen_of[batch[i]] = g;
+            ngen = std::max(ngen, g + 1);
+        }
+        *hcycle_ = cycle_;
+        LZB_CUDA(cudaMemcpyAsync(dcycle_.p, hcycle_, sizeof(uint32_t), cudaMemcpyHostToDevice, s_));
+        std::vector<int32_t> cells;
+        DevBuf<int32_t> dcells(static_cast<size_t>(k));
+        for (int g = 0; g < ngen; ++g)
+            for (int l = 0; l < D_; ++l) {
+                cells.clear();
+                for (int64_t i = 0; i < k; ++i)
+                    if (gen[i] == g && (batch[i] >> 27) == l) cells.push_back(batch[i] & ((1 << 27) - 1));
+                if (cells.empty()) continue;
+                LZB_CUDA(cudaMemcpyAsync(dcells.p, cells.data(), cells.size() * sizeof(int32_t),
+                                         cudaMemcpyHostToDevice, s_));
+                const int n = static_cast<int>(cells.size());
+                if (d_.transfer == LZB_BOXMG)
+                    LZB_LAUNCH(k_coarse, blocks_for(n, 64), 64, 0, s_, V(l), V(l + 1), d_.field, 1, d_.delta_max,
+                               dcycle_.p, res_.p->s, ctx_->err.p, static_cast<const int32_t*>(dcells.p), n);
+                else
+                    LZB_LAUNCH(k_coarse_geo, blocks_for(n, kCoarseThreads), kCoarseThreads, 0, s_, V(l), V(l + 1),
+                               d_.field, d_.delta_max, dcycle_.p, res_.p->s, ctx_->err.p,
+                               static_cast<const int32_t*>(dcells.p), n);
+                LZB_CUDA(cudaStreamSynchronize(s_));  // dcells is reused by the next launch
+            }
+        return k;
+    }
+    bool ripple_fifo() const { return d_.policy == LZB_RIPPLE && d_.throttle > 0; }
+    std::deque<int32_t> hq_;        // pending coarse_recompute tasks (throttled ripple)
+    std::vector<int32_t> preorder_;  // refined cells in walk order
+    uint64_t hq_pending_at_report_ = 0;
 
     bool ripple() const { return d_.policy == LZB_RIPPLE; }
 
@@ -2854,10 +2968,11 @@ public:
         for (int l = 0; l < D_; ++l) {
             if (d_.transfer == LZB_BOXMG)
                 LZB_LAUNCH(k_coarse, blocks_for(L_[l].nc, 64), 64, 0, s_, V(l), V(l + 1), d_.field, 1, d_.delta_max,
-                           dcycle_.p, res_.p->s, ctx_->err.p);
+                           dcycle_.p, res_.p->s, ctx_->err.p, static_cast<const int32_t*>(nullptr), 0);
             else
                 LZB_LAUNCH(k_coarse_geo, blocks_for(L_[l].nc, kCoarseThreads), kCoarseThreads, 0, s_, V(l), V(l + 1),
-                           d_.field, d_.delta_max, dcycle_.p, res_.p->s, ctx_->err.p);
+                           d_.field, d_.delta_max, dcycle_.p, res_.p->s, ctx_->err.p,
+                           static_cast<const int32_t*>(nullptr), 0);
         }
     }
     // The walk's refined cells under ripple: take_dirty -> spawn (solver.cpp:86-90).
@@ -2866,14 +2981,23 @@ public:
             LZB_LAUNCH(k_take_dirty, blocks_for(L_[l].nc, kThreads), kThreads, 0, s_, V(l), cycle_);
     }
     void begin_cycle_tasks() {
+        if (ripple_fifo()) {
+            const int64_t ran = ripple_run_fifo(static_cast<int64_t>(d_.throttle));
+            pool_begin_cycle(static_cast<int64_t>(d_.throttle) - ran);
+            return;
+        }
         if (ripple()) ripple_tasks();
         pool_begin_cycle();
     }
 
     void assembly_pass() {  // solver.cpp:79-97
         *hcycle_ = cycle_;
-        if (ripple()) ripple_walk();
-        else coarse_pass();
+        if (ripple()) {
+            ripple_walk();
+            if (ripple_fifo()) ripple_spawn_fifo();
+        } else {
+            coarse_pass();
+        }
         leaves_pass();
     }
 
@@ -3114,8 +3238,12 @@ public:
             LZB_LAUNCH(k_spawn_forced, blocks_for(leaves_, kThreads), kThreads, 0, s_, V(D_), cycle_,
                        static_cast<long long>(leaves_), keys_.p, id0, d_.forced_fraction);
         }
-        if (ripple()) ripple_walk();
-        else run_graph(g_coarse_, &Grid::coarse_pass);
+        if (ripple()) {
+            ripple_walk();
+            if (ripple_fifo()) ripple_spawn_fifo();
+        } else {
+            run_graph(g_coarse_, &Grid::coarse_pass);
+        }
         leaves_pass();
         if (d_.concurrent && !batch_inflight_ && (cycle_ == 1 || pending_ > 0)) launch_batch();
         ensure_rhs();
@@ -3155,7 +3283,10 @@ public:
         ++cycle_;
         *hcycle_ = cycle_;
         rep.cycle = static_cast<int32_t>(cycle_);
-        if (ripple()) ripple_walk();
+        if (ripple()) {
+            ripple_walk();
+            if (ripple_fifo()) ripple_spawn_fifo();
+        }
         ensure_rhs();
         run_graph(g_vfront_, &Grid::vfront_body);  // (coarse pass) + leaf residual + norm -> host
         LZB_CUDA(cudaStreamSynchronize(s_));
@@ -3260,7 +3391,8 @@ public:
         dof_total_ += rep.dof_updates;
         rep.dof_updates_total = dof_total_;
         // leaf tasks (anarchic p2) + pending coarse_recompute tasks (ripple)
-        pending_ = static_cast<int64_t>(r.s[S_PENDING]);
+        pending_ = static_cast<int64_t>(r.s[S_PENDING]) + static_cast<int64_t>(hq_.size());
+        hq_pending_at_report_ = hq_.size();
         // anarchic: no task pending and nothing bottom means every leaf is top
         // (request_stencil spawns a task for every other leaf)
         if (d_.mode == LZB_ANARCHIC && pending_ == 0 && !batch_inflight_) all_top_ = true;

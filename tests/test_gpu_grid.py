@@ -96,6 +96,8 @@ def test_cycle_bit_identical_to_oracle(f, solver, asm):
 
 RIPPLE = [(f, s, a, t) for f in ["setup = quadrant\neps-low = 0.001", "setup = checkerboard\nfield-seed = 1"]
           for s in ["additive", "adafac-pi"] for a in ["eager", "adaptive", "anarchic"] for t in ["geometric", "boxmg"]]
+RIPPLE_THROTTLED = [(f, a, t, th) for f in ["setup = quadrant\neps-low = 0.001", "setup = theta\ntheta = 16"]
+                    for a in ["anarchic"] for t in ["geometric", "boxmg"] for th in [5, 20, 97]]
 
 
 @pytest.mark.parametrize("f,solver,asm,transfer", RIPPLE)
@@ -110,6 +112,24 @@ def test_ripple_bit_identical_to_oracle(f, solver, asm, transfer):
     assert_reports(g.run(), o.run())
     assert_state(g, o, d.depth)
     assert g.stream_image() == o.stream_image()
+
+
+@pytest.mark.parametrize("f,asm,transfer,throttle", RIPPLE_THROTTLED)
+def test_ripple_throttled_bit_identical_to_oracle(f, asm, transfer, throttle):
+    """coarse-recompute = ripple with a throttle (solver.cpp:86-90,
+    scheduler.cpp:88-111): the high-priority coarse_recompute tasks form a
+    FIFO with duplicates, at most `throttle` tasks per begin_cycle (coarse
+    first, the leaf tasks get the rest); device against the oracle, itself
+    pinned to the unmodified reference with throttle 20 (test_oracle_pin.py)."""
+    text = (f"{f}\ndepth = 3\nsolver = adafac-pi\nassembly = {asm}\nmax-cycles = 14\nomega = 0.6\nrhs = 1\n"
+            f"seed = 42\ncoarse-recompute = ripple\ntransfer = {transfer}\nthrottle = {throttle}\n")
+    g, o, d = grid_pair(text)
+    assert d.policy == lzb.T.RIPPLE and d.throttle == throttle
+    rg, ro = g.run(), o.run()
+    assert_reports(rg, ro)
+    assert_state(g, o, d.depth)
+    assert g.stream_image() == o.stream_image()
+    assert g.drain() == 0
 
 
 @pytest.mark.parametrize("setup", ["setup = theta\ntheta = 16", "setup = sinusoid"])
