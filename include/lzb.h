@@ -319,6 +319,15 @@ int lzb_tree3_cells(lzb_tree3* t, int64_t first, int64_t count, double* ops, int
 int lzb_tree3_init_cycle(lzb_tree3* t, int variant, double omega, double rhs_scale, uint64_t noise_seed,
                          int max_cycles, double target);
 int lzb_tree3_refresh_ops(lzb_tree3* t);
+/* Re-refinement (BASELINE configs[3]: topology change forcing re-assembly;
+ * the reference's apply_refinement_now + on_refinement, solver.cpp:402-418,
+ * mesh.cpp:236-312, stream.cpp:262-266, restated for the sphere tree): the
+ * refinement ball grows to `radius` (no coarsening, mesh.hpp:55), every leaf
+ * meeting it below lmax is refined; surviving leaves keep their operators,
+ * new leaves are assembled at n; during a cycle the new vertices start from
+ * the parent interpolant and the levels / loads / Galerkin operators are
+ * rebuilt. *new_leaves: the leaves created. */
+int lzb_tree3_refine(lzb_tree3* t, double radius, int n, int64_t* new_leaves);
 int lzb_tree3_step(lzb_tree3* t, lzb_cycle_report* out);
 int lzb_tree3_vertices(lzb_tree3* t, int level, int field, double* out);
 /* Average device ms of one leaf-level 3D cycle kernel (LZB_TK_UHAT .. LZB_TK_PROLONG). */

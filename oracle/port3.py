@@ -457,6 +457,7 @@ class Cycle3A:
     def __init__(self, leaves, leaf_ops, lmax, variant="adafac-pi", omega=0.6, rhs_scale=3 * math.pi ** 2, seed=42,
                  target=1e-10, max_cycles=100):
         self.D, self.omega, self.variant, self.target, self.max_cycles = lmax, omega, variant, target, max_cycles
+        self._rhs_scale = rhs_scale
         self.N = [3 ** l for l in range(lmax + 1)]
         leaves = np.asarray(leaves)
         leaf_ops = np.asarray(leaf_ops, dtype=np.float64).reshape(-1, 8, 8)
@@ -615,6 +616,50 @@ class Cycle3A:
                         continue
                     val += w * cu[hz + az, hy + ay, hx + ax]
                 u[iz, iy, ix] = val
+
+    def refine(self, leaves, leaf_ops):
+        """Re-refinement (the reference's apply_refinement_now, solver.cpp:402-418,
+        restated in 3D): the structure rebuilt from the new leaf set and
+        operators; u kept on the vertices that existed; a new vertex starts
+        from the parent level's interpolant at its first existing host cell
+        (coarse levels first, mesh.cpp:182-214), zero on the boundary; then
+        injection / hanging interpolation. History and cycle count carry on."""
+        old_u = [self.v[l]["u"] for l in range(self.D + 1)]
+        old_ve = self.vexist
+        hist, cyc, first = self.history, self.cycle, getattr(self, "first", None)
+        self.__init__(leaves, leaf_ops, self.D, self.variant, self.omega, self._rhs_scale, 0, self.target,
+                      self.max_cycles)
+        for l in range(self.D + 1):
+            u = np.where(old_ve[l], old_u[l], 0.0)
+            new = self.vexist[l] & ~old_ve[l]
+            if l > 0:
+                nc, cu = self.N[l - 1], self.v[l - 1]["u"]
+                for iz, iy, ix in zip(*np.nonzero(new & (self.kind[l] != 2))):
+                    cand = []
+                    for i in (ix, iy, iz):
+                        c1 = min(i // 3, nc - 1)
+                        cand.append((c1 - 1 if (i % 3 == 0 and c1 > 0) else c1, c1))
+                    host = None
+                    for hx in cand[0]:
+                        for hy in cand[1]:
+                            for hz in cand[2]:
+                                if host is None and self.exist[l - 1][hz, hy, hx]:
+                                    host = (hx, hy, hz)
+                    hx, hy, hz = host
+                    fx, fy, fz = (ix - 3.0 * hx) / 3.0, (iy - 3.0 * hy) / 3.0, (iz - 3.0 * hz) / 3.0
+                    val = 0.0
+                    for a in range(8):
+                        ax, ay, az = a & 1, (a >> 1) & 1, a >> 2
+                        w = (fx if ax else 1.0 - fx) * (fy if ay else 1.0 - fy) * (fz if az else 1.0 - fz)
+                        if w != 0.0:
+                            val += w * cu[hz + az, hy + ay, hx + ax]
+                    u[iz, iy, ix] = val
+            u = np.where(new & (self.kind[l] == 2), 0.0, u)
+            self.v[l]["u"] = u
+        self._finish()
+        self.history, self.cycle = hist, cyc
+        if first is not None:
+            self.first = first
 
     def step(self):
         self.cycle += 1

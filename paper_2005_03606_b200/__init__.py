@@ -156,6 +156,7 @@ def lib():
         L.lzb_tree3_cells.argtypes = [vp, i64, i64, vp, vp, vp, vp]
         L.lzb_tree3_init_cycle.argtypes = [vp, C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_int, C.c_double]
         L.lzb_tree3_refresh_ops.argtypes = [vp]
+        L.lzb_tree3_refine.argtypes = [vp, C.c_double, C.c_int, C.POINTER(C.c_int64)]
         L.lzb_tree3_step.argtypes = [vp, C.POINTER(CycleReport)]
         L.lzb_tree3_vertices.argtypes = [vp, C.c_int, C.c_int, vp]
         L.lzb_grid3_time_kernel.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_double)]
@@ -744,6 +745,17 @@ class Tree3:
 
     def refresh_ops(self):
         _check(lib().lzb_tree3_refresh_ops(self.h))
+
+    def refine(self, radius, n) -> int:
+        """Grow the refinement ball to `radius` (new leaves assembled at n, the
+        cycle state carried over); returns the number of new leaves."""
+        k = C.c_int64()
+        _check(lib().lzb_tree3_refine(self.h, radius, n, C.byref(k)))
+        per = np.zeros(8, np.int64)
+        tot = C.c_int64()
+        _check(lib().lzb_tree3_counts(self.h, _ptr(per), C.byref(tot)))
+        self.per_level, self.n_leaves = per, tot.value
+        return k.value
 
     def step(self) -> dict:
         r = CycleReport()

@@ -13,6 +13,7 @@
 // class planes over the leaf index (value q of leaf i at q * nleaves + i).
 #include <algorithm>
 #include <cmath>
+#include <unordered_map>
 #include <vector>
 
 namespace lzb {
@@ -170,6 +171,75 @@ __global__ void k4_copy_leaf_ops(const int4* __restrict__ leaves, int64_t n, int
 #pragma unroll
     for (int q = 0; q < 27; ++q) L.op[q * L.nop + j] = lop[q * nleaves + t];
 }
+// re-refinement: the class planes / widths / n of the surviving leaves moved
+// to their new leaf index (src = old index, -1 for a new leaf)
+__global__ void k4_gather_leaves(const int32_t* __restrict__ src, int64_t n_new, int64_t n_old,
+                                 const double* __restrict__ op_old, const int8_t* __restrict__ p3_old,
+                                 const int32_t* __restrict__ n_oldv, double* __restrict__ op_new,
+                                 int8_t* __restrict__ p3_new, int32_t* __restrict__ n_newv) {
+    lzb_pdl_enter();
+    const int64_t t = gtid();
+    if (t >= n_new) return;
+    const int32_t o = src[t];
+    if (o < 0) {
+        p3_new[t] = 0;
+        n_newv[t] = 0;
+        return;
+    }
+#pragma unroll
+    for (int q = 0; q < 27; ++q) op_new[q * n_new + t] = op_old[q * n_old + o];
+    p3_new[t] = p3_old[o];
+    n_newv[t] = n_oldv[o];
+}
+// re-refinement: a vertex that did not exist before starts from the d-linear
+// interpolant of the parent level (its first existing host cell), zero on the
+// Dirichlet boundary (solver.cpp:402-418 apply_refinement_now, mesh.cpp:182-214)
+__global__ void k4_new_vertices(LvA F, LvA C, const uint8_t* __restrict__ existed) {
+    lzb_pdl_enter();
+    int ix, iy, iz;
+    int64_t vi;
+    if (!vxyzA(F, ix, iy, iz, vi)) return;
+    const int k = F.vk[vi] & 3;
+    if (k == VK_OUT || existed[vi]) return;
+    if (k == VK_DIR) {
+        F.v[LZB_V_U][vi] = 0.0;
+        return;
+    }
+    const int nc = C.N;
+    int c1[3], c0[3];
+    const int f[3] = {ix, iy, iz};
+    for (int d = 0; d < 3; ++d) {
+        c1[d] = min(f[d] / 3, nc - 1);
+        c0[d] = (f[d] % 3 == 0 && c1[d] > 0) ? c1[d] - 1 : c1[d];
+    }
+    int hx = -1, hy = -1, hz = -1;
+    for (int a = 0; a < 2 && hx < 0; ++a)
+        for (int b = 0; b < 2 && hx < 0; ++b)
+            for (int c = 0; c < 2 && hx < 0; ++c) {
+                const int qx = a ? c1[0] : c0[0], qy = b ? c1[1] : c0[1], qz = c ? c1[2] : c0[2];
+                if (C.cf[cidx(nc, qx, qy, qz)]) {
+                    hx = qx;
+                    hy = qy;
+                    hz = qz;
+                }
+            }
+    if (hx < 0) return;
+    const double fx = (ix - 3.0 * hx) / 3.0, fy = (iy - 3.0 * hy) / 3.0, fz = (iz - 3.0 * hz) / 3.0;
+    double val = 0.0;
+    for (int a = 0; a < 8; ++a) {
+        const int ax = a & 1, ay = (a >> 1) & 1, az = a >> 2;
+        const double w = (ax ? fx : 1.0 - fx) * (ay ? fy : 1.0 - fy) * (az ? fz : 1.0 - fz);
+        if (w == 0.0) continue;
+        val += w * C.v[LZB_V_U][vidx3(nc, hx + ax, hy + ay, hz + az)];
+    }
+    F.v[LZB_V_U][vi] = val;
+}
+__global__ void k4_existed(LvA L, uint8_t* __restrict__ out) {
+    lzb_pdl_enter();
+    const int64_t t = gtid();
+    if (t < static_cast<int64_t>(L.N + 1) * (L.N + 1) * (L.N + 1)) out[t] = (L.vk[t] & 3) != VK_OUT;
+}
+
 // refined cells of C: Galerkin from the 27 children of F (k3_galerkin's class form)
 __global__ void __launch_bounds__(256) k4_galerkin(LvA C, LvA F) {
     lzb_pdl_enter();
@@ -591,6 +661,7 @@ public:
         max_cycles_ = max_cycles;
         target_ = target;
         const int D = lmax_;
+        rhs_scale_ = rhs_scale;
         A_.clear();
         A_.resize(D + 1);
         for (int l = 0; l <= D; ++l) {
@@ -604,6 +675,27 @@ public:
                 L.v[f].alloc(L.nv);
                 LZB_CUDA(cudaMemsetAsync(L.v[f].p, 0, L.v[f].bytes(), s_));
             }
+        }
+        setup_levels();
+        upload_galerkin_weights();
+        refresh_ops();
+        partialA_.alloc(kNormBlocksA);
+        for (int l = 0; l <= D; ++l) LZB_LAUNCH(k4_noise, vgA(l), 128, 0, s_, lv(l), l, seed);
+        finish_cycle();
+        for (int l = 0; l <= D; ++l)
+            LZB_LAUNCH(k4_load, vgA(l), 128, 0, s_, lv(l), rhs_scale, A_[l].h * A_[l].h * A_[l].h / 8.0);
+        cycle_ = 0;
+        history_.clear();
+        sync();
+    }
+
+    // the structure of every level from the current leaf list: vertex box,
+    // cell flags, operator index and slots, vertex kinds (the vertex fields
+    // are kept: init_cycle zeroes them, a re-refinement carries them over)
+    void setup_levels() {
+        const int D = lmax_;
+        for (int l = 0; l <= D; ++l) {
+            LevA& L = A_[l];
             // the vertex box of the level's existing cells: the leaves of level l
             // and the ancestors at level l of every deeper leaf
             int lo[3] = {L.N, L.N, L.N}, hi[3] = {-1, -1, -1};
@@ -655,16 +747,79 @@ public:
             L.op.alloc(static_cast<size_t>(std::max(cnt, 1)) * kCls3);
             LZB_LAUNCH(k4_classify, vgA(l), 128, 0, s_, lv(l));
         }
-        upload_galerkin_weights();
-        refresh_ops();
-        partialA_.alloc(kNormBlocksA);
-        for (int l = 0; l <= D; ++l) LZB_LAUNCH(k4_noise, vgA(l), 128, 0, s_, lv(l), l, seed);
-        finish_cycle();
-        for (int l = 0; l <= D; ++l)
-            LZB_LAUNCH(k4_load, vgA(l), 128, 0, s_, lv(l), rhs_scale, A_[l].h * A_[l].h * A_[l].h / 8.0);
-        cycle_ = 0;
-        history_.clear();
+    }
+
+    // Re-refinement (BASELINE configs[3]; the reference's apply_refinement_now,
+    // solver.cpp:402-418, mesh.cpp:236-312, restated for the sphere tree): the
+    // ball of refinement grows to `radius`, every leaf meeting it below lmax
+    // is refined (the topology changes: new leaves, vertices, hanging nodes);
+    // the surviving leaves keep their operators, the new ones are assembled at
+    // n (forced re-assembly, stream.cpp:262-266 on_refinement), new vertices
+    // start from the parent level's interpolant, the level structure, loads and
+    // Galerkin operators are rebuilt; the cycle continues (history kept).
+    // Returns the number of new leaves.
+    int64_t refine(double radius, int n) {
+        if (!(radius >= rad_)) throw Error(LZB_ERR_INVALID, "the refinement ball only grows (no coarsening, mesh.hpp:55)");
+        if (n < 1 || n > kMaxN3) throw Error(LZB_ERR_INVALID, "3D sub-samples per axis must be in 1..16");
+        const bool cyc = !A_.empty();
+        std::vector<DevBuf<uint8_t>> existed(cyc ? lmax_ + 1 : 0);
+        if (cyc)
+            for (int l = 0; l <= lmax_; ++l) {
+                existed[l].alloc(A_[l].nv);
+                LZB_LAUNCH(k4_existed, blocks_for(A_[l].nv, 256), 256, 0, s_, lv(l), existed[l].p);
+            }
+        // the new leaf set, the old leaves' slots
+        auto key = [](const int4& c) {
+            return (static_cast<uint64_t>(c.x) << 60) | (static_cast<uint64_t>(c.y) << 40) |
+                   (static_cast<uint64_t>(c.z) << 20) | static_cast<uint64_t>(c.w);
+        };
+        std::unordered_map<uint64_t, int32_t> old_idx;
+        old_idx.reserve(leaves_.size() * 2);
+        for (size_t i = 0; i < leaves_.size(); ++i) old_idx[key(leaves_[i])] = static_cast<int32_t>(i);
+        const int64_t n_old = n_leaves_;
+        rad_ = radius;
+        leaves_.clear();
+        for (int64_t& c : per_level_) c = 0;
+        build();
+        n_leaves_ = static_cast<int64_t>(leaves_.size());
+        std::vector<int32_t> src(n_leaves_), fresh;
+        for (int64_t i = 0; i < n_leaves_; ++i) {
+            auto it = old_idx.find(key(leaves_[i]));
+            src[i] = it == old_idx.end() ? -1 : it->second;
+            if (src[i] < 0) fresh.push_back(static_cast<int32_t>(i));
+        }
+        DevBuf<int32_t> dsrc(n_leaves_);
+        LZB_CUDA(cudaMemcpyAsync(dsrc.p, src.data(), src.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s_));
+        DevBuf<double> op2(static_cast<size_t>(n_leaves_) * kCls3);
+        DevBuf<int8_t> p32(n_leaves_);
+        DevBuf<int32_t> n2(n_leaves_);
+        LZB_LAUNCH(k4_gather_leaves, blocks_for(n_leaves_, 256), 256, 0, s_, dsrc.p, n_leaves_, n_old, op_.p, p3_.p,
+                   n_.p, op2.p, p32.p, n2.p);
+        LZB_CUDA(cudaStreamSynchronize(s_));
+        op_ = std::move(op2);
+        p3_ = std::move(p32);
+        n_ = std::move(n2);
+        dleaves_.alloc(n_leaves_);
+        LZB_CUDA(cudaMemcpy(dleaves_.p, leaves_.data(), n_leaves_ * sizeof(int4), cudaMemcpyHostToDevice));
+        n_shell_ = 0;  // the shell list indexed the old leaves
+        if (!fresh.empty()) {  // the new leaves: assembled now
+            shell_.alloc(fresh.size());
+            LZB_CUDA(cudaMemcpy(shell_.p, fresh.data(), fresh.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+            n_shell_ = static_cast<int64_t>(fresh.size());
+            assemble(n, true);
+            n_shell_ = 0;
+        }
+        if (cyc) {
+            setup_levels();
+            for (int l = 1; l <= lmax_; ++l)  // coarse levels first: interpolation chains through
+                LZB_LAUNCH(k4_new_vertices, vgA(l), 128, 0, s_, lv(l), lv(l - 1), existed[l].p);
+            refresh_ops();
+            finish_cycle();
+            for (int l = 0; l <= lmax_; ++l)
+                LZB_LAUNCH(k4_load, vgA(l), 128, 0, s_, lv(l), rhs_scale_, A_[l].h * A_[l].h * A_[l].h / 8.0);
+        }
         sync();
+        return static_cast<int64_t>(fresh.size());
     }
 
     // the leaves' current operators into the levels, then the Galerkin chain
@@ -755,7 +910,7 @@ private:
     std::vector<LevA> A_;
     DevBuf<double> partialA_;
     int variant_ = LZB_ADDITIVE, max_cycles_ = 100;
-    double omega_ = 0.6, target_ = 1e-10, first_ = 1.0;
+    double omega_ = 0.6, target_ = 1e-10, first_ = 1.0, rhs_scale_ = 0.0;
     uint32_t cycle_ = 0;
     std::vector<double> history_;
 
@@ -898,6 +1053,12 @@ int lzb_tree3_cells(lzb_tree3* t, int64_t first, int64_t count, double* ops, int
 int lzb_tree3_init_cycle(lzb_tree3* t, int variant, double omega, double rhs_scale, uint64_t noise_seed,
                          int max_cycles, double target) {
     return lzb::guarded([&] { t->t->init_cycle(variant, omega, rhs_scale, noise_seed, max_cycles, target); });
+}
+int lzb_tree3_refine(lzb_tree3* t, double radius, int n, int64_t* new_leaves) {
+    return lzb::guarded([&] {
+        const int64_t k = t->t->refine(radius, n);
+        if (new_leaves) *new_leaves = k;
+    });
 }
 int lzb_tree3_refresh_ops(lzb_tree3* t) {
     return lzb::guarded([&] {

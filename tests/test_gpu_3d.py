@@ -264,6 +264,53 @@ def test_tree3_cycle_matches_restatement(solver, lbase, lmax):
         assert np.abs(u - w).max() <= 1e-12 * max(np.abs(w).max(), 1.0), lvl
 
 
+@pytest.mark.parametrize("solver,lbase,lmax,radius", [("adafac-pi", 1, 3, 0.34), ("additive", 2, 3, 0.3)])
+def test_tree3_rerefinement_matches_restatement(solver, lbase, lmax, radius):
+    """Re-refinement during the solve (BASELINE configs[3]: the refined region
+    grows, topology changes, new leaves are assembled -- the reference's
+    apply_refinement_now, solver.cpp:402-418): surviving leaves keep their
+    operators bit for bit, the new ones are their fresh integration, the new
+    vertices start from the parent interpolant, and the cycle continues in
+    step with the restatement doing the same refinement."""
+    f = lzb.field3_sphere()
+    T3 = lzb.Tree3(lbase, lmax, f, delta_max=1e-8)
+    T3.assemble(2)
+    T3.init_cycle(solver=solver, omega=0.6, seed=11, max_cycles=100)
+    ops, _, _, lxyz = T3.cells(0, T3.n_leaves)
+    ref = o3.Cycle3A(lxyz, ops, lmax, variant=solver, omega=0.6, seed=11)
+    for _ in range(3):
+        a, b = T3.step(), ref.step()
+        assert a["residual"] == pytest.approx(b["residual"], rel=1e-10)
+    n0 = T3.n_leaves
+    k = T3.refine(radius, 2)
+    assert k > 0 and T3.n_leaves > n0
+    ops2, p32, n2, lxyz2 = T3.cells(0, T3.n_leaves)
+    old = {tuple(c): o for c, o in zip(lxyz.tolist(), ops)}
+    fresh = [i for i, c in enumerate(lxyz2.tolist()) if tuple(c) not in old]
+    assert len(fresh) == k
+    for i, c in enumerate(lxyz2.tolist()):
+        if tuple(c) in old:
+            assert np.array_equal(ops2[i], old[tuple(c)])
+    # the new leaves: their element matrices at n = 2 (codec-absorbed, delta 1e-8)
+    sel = fresh[:: max(1, len(fresh) // 16)]
+    h = np.array([(1.0 / 3) ** lxyz2[i][0] for i in sel])
+    want = lzb.integrate_elements3(f, lxyz2[sel, 1] * h, lxyz2[sel, 2] * h, lxyz2[sel, 3] * h, h, 2)
+    assert np.abs(ops2[sel] - want).max() <= 1e-7 and (n2[fresh] == 2).all()
+    ref.refine(lxyz2, ops2)
+    for lvl in range(lmax + 1):
+        u, w = T3.vertices(lvl, lzb.T.V_U), ref.v[lvl]["u"]
+        assert np.abs(u - w).max() <= 1e-12 * max(np.abs(w).max(), 1.0), lvl
+    for _ in range(4):
+        a, b = T3.step(), ref.step()
+        assert a["status"] == b["status"] and a["cycle"] == b["cycle"]
+        assert a["residual"] == pytest.approx(b["residual"], rel=1e-10)
+    for lvl in range(lmax + 1):
+        u, w = T3.vertices(lvl, lzb.T.V_U), ref.v[lvl]["u"]
+        assert np.abs(u - w).max() <= 1e-12 * max(np.abs(w).max(), 1.0), lvl
+    with pytest.raises(lzb.LzbError):
+        T3.refine(radius - 0.1, 2)  # no coarsening (mesh.hpp:55)
+
+
 @pytest.mark.parametrize("depth,nu", [(2, 1), (3, 2)])
 def test_vcycle3_matches_restatement(depth, nu):
     """V(nu, nu) cycles on the 3D hierarchy (the BASELINE configs' V(1,1) /
