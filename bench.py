@@ -530,24 +530,36 @@ def run_ours(args, world, rank, local):
         c4["p3_histogram"] = list(st4.p3_histogram)
         c4["record_factor"] = st4.fine_factor_totals
         # the delayed solve on the tree: p = 1 everywhere, adaFAC-PI cycles, and every 5
-        # cycles the interface shell re-assembled at the next p (2, 4, 8, 16) with the
-        # refined cells' Galerkin operators recomputed (forced re-assembly)
+        # cycles a re-refinement (the refined ball grows by the interface width: new
+        # leaves at level 6 assembled, new vertices interpolated, levels rebuilt --
+        # a topology change) and the interface shell re-assembled at the next p
+        # (2, 4, 8, 16) with the refined cells' Galerkin operators recomputed
+        t4.close()
+        t4 = lzb.Tree3(4, 6, lzb.field3_sphere(), delta_max=1e-8, ctx=ctx)
         t4.assemble(1)
         t4.init_cycle(solver="adafac-pi", omega=0.6, max_cycles=10 ** 6)
-        ladder, reps4 = [2, 4, 8, 16], []
+        ladder, reps4, events = [2, 4, 8, 16], [], []
 
         def c4_solve():
             for k in range(25):
                 if k % 5 == 0 and 0 < k // 5 <= len(ladder):
-                    t4.assemble_shell(ladder[k // 5 - 1])
+                    e = k // 5
+                    new = t4.refine(0.25 + 0.01 * e, ladder[e - 1])
+                    shell = t4.set_shell(0.01)
+                    t4.assemble_shell(ladder[e - 1])
                     t4.refresh_ops()
+                    events.append({"after_cycle": k, "radius": 0.25 + 0.01 * e, "new_leaves": new,
+                                   "leaves": t4.n_leaves, "shell_leaves": shell, "p": ladder[e - 1]})
                 reps4.append(t4.step())
 
         t_solve = timed_steps(c4_solve, 1)
         c4["cycles"] = {"cycles": len(reps4), "seconds": t_solve, "ms_per_cycle_incl_reassembly": 1e3 * t_solve / 25,
                         "normalized_after": reps4[-1]["normalized"], "variant": "adafac-pi, omega 0.6",
-                        "schedule": "p = 1, then the shell at p = 2, 4, 8, 16 after cycles 5, 10, 15, 20 (+ Galerkin "
-                                    "refresh of the refined cells)"}
+                        "refinements": events,
+                        "schedule": "p = 1, then after cycles 5, 10, 15, 20: re-refinement (refined ball radius "
+                                    "0.25 -> 0.26 .. 0.29, new level-6 leaves assembled, topology rebuilt) + the "
+                                    "interface shell re-assembled at p = 2, 4, 8, 16 + Galerkin refresh; wall time "
+                                    "includes the host-side tree rebuild"}
         t4.close()
         del t4
         torch.cuda.empty_cache()

@@ -768,26 +768,54 @@ public:
                 existed[l].alloc(A_[l].nv);
                 LZB_LAUNCH(k4_existed, blocks_for(A_[l].nv, 256), 256, 0, s_, lv(l), existed[l].p);
             }
-        // the new leaf set, the old leaves' slots
-        auto key = [](const int4& c) {
-            return (static_cast<uint64_t>(c.x) << 60) | (static_cast<uint64_t>(c.y) << 40) |
-                   (static_cast<uint64_t>(c.z) << 20) | static_cast<uint64_t>(c.w);
-        };
-        std::unordered_map<uint64_t, int32_t> old_idx;
-        old_idx.reserve(leaves_.size() * 2);
-        for (size_t i = 0; i < leaves_.size(); ++i) old_idx[key(leaves_[i])] = static_cast<int32_t>(i);
+        // the new leaf set, level-major, from the old one: a leaf that meets the
+        // grown ball below lmax is replaced by its refinement (build()'s rule with
+        // the new radius: the ball only grows, so every other leaf survives)
         const int64_t n_old = n_leaves_;
         rad_ = radius;
-        leaves_.clear();
-        for (int64_t& c : per_level_) c = 0;
-        build();
-        n_leaves_ = static_cast<int64_t>(leaves_.size());
-        std::vector<int32_t> src(n_leaves_), fresh;
-        for (int64_t i = 0; i < n_leaves_; ++i) {
-            auto it = old_idx.find(key(leaves_[i]));
-            src[i] = it == old_idx.end() ? -1 : it->second;
-            if (src[i] < 0) fresh.push_back(static_cast<int32_t>(i));
+        std::vector<std::vector<int4>> per(8);
+        std::vector<std::vector<int32_t>> per_src(8);
+        std::vector<int4> stack;
+        for (int64_t i = 0; i < n_old; ++i) {
+            const int4 c = leaves_[i];
+            double lo, hi;
+            box_range(c.y * HL_.h[c.x], c.z * HL_.h[c.x], c.w * HL_.h[c.x], HL_.h[c.x], lo, hi);
+            if (c.x >= lmax_ || lo > rad_) {
+                per[c.x].push_back(c);
+                per_src[c.x].push_back(static_cast<int32_t>(i));
+                continue;
+            }
+            stack.assign(1, c);
+            while (!stack.empty()) {
+                const int4 q = stack.back();
+                stack.pop_back();
+                bool refine = q.x < lmax_;
+                if (refine) {
+                    box_range(q.y * HL_.h[q.x], q.z * HL_.h[q.x], q.w * HL_.h[q.x], HL_.h[q.x], lo, hi);
+                    refine = lo <= rad_;
+                }
+                if (!refine) {
+                    per[q.x].push_back(q);
+                    per_src[q.x].push_back(-1);
+                    continue;
+                }
+                for (int dz = 2; dz >= 0; --dz)
+                    for (int dy = 2; dy >= 0; --dy)
+                        for (int dx = 2; dx >= 0; --dx)
+                            stack.push_back(make_int4(q.x + 1, 3 * q.y + dx, 3 * q.z + dy, 3 * q.w + dz));
+            }
         }
+        leaves_.clear();
+        std::vector<int32_t> src, fresh;
+        for (int l = 0; l < 8; ++l) {
+            per_level_[l] = static_cast<int64_t>(per[l].size());
+            leaves_.insert(leaves_.end(), per[l].begin(), per[l].end());
+            src.insert(src.end(), per_src[l].begin(), per_src[l].end());
+        }
+        n_leaves_ = static_cast<int64_t>(leaves_.size());
+        if (leaves_.size() > static_cast<size_t>(INT32_MAX)) throw Error(LZB_ERR_RESOURCE, "too many leaves");
+        for (int64_t i = 0; i < n_leaves_; ++i)
+            if (src[i] < 0) fresh.push_back(static_cast<int32_t>(i));
         DevBuf<int32_t> dsrc(n_leaves_);
         LZB_CUDA(cudaMemcpyAsync(dsrc.p, src.data(), src.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s_));
         DevBuf<double> op2(static_cast<size_t>(n_leaves_) * kCls3);
