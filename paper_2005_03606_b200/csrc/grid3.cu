@@ -19,6 +19,7 @@
 // the 8x8 matrix, padded to 28 doubles = 224 B per cell), index
 // (cz*N + cy)*N + cx; markers p3 (i8), n (i32).
 #include <complex>
+#include <type_traits>
 #include <memory>
 #include <vector>
 
@@ -385,18 +386,48 @@ __device__ __forceinline__ void plane_store3(const Planes3& P, int W, int64_t c,
 
 // Leaf class sources of the cycle kernels: FP64 planes, or compressed planes
 // at width W (27 values of one cell: load(c, out)).
+// fetch(c, raw) issues a cell's loads (no use: they stay in flight while the
+// caller computes), decode(raw, v) turns them into the 27 class values --
+// the z-marching residual prefetches the next cell layer with it.
 struct Src64 {
     const double* op;
     int64_t nc;
+    struct Raw {
+        double v[27];
+    };
     __device__ __forceinline__ double at(int64_t c, int q) const { return __ldg(op + q * nc + c); }
     __device__ __forceinline__ void load27(int64_t c, double* v) const {
 #pragma unroll
         for (int q = 0; q < 27; ++q) v[q] = at(c, q);
     }
+    __device__ __forceinline__ void fetch(int64_t c, Raw& r) const {
+#pragma unroll
+        for (int q = 0; q < 27; ++q) r.v[q] = at(c, q);
+    }
+    __device__ __forceinline__ void decode(const Raw& r, double* v) const {
+#pragma unroll
+        for (int q = 0; q < 27; ++q) v[q] = r.v[q];
+    }
 };
 template <int W>
 struct SrcComp {
     Planes3 P;
+    using Word = typename std::conditional<(W <= 4), uint32_t, unsigned long long>::type;
+    struct Raw {
+        Word w[27];
+        double e;
+    };
+    __device__ __forceinline__ void fetch(int64_t c, Raw& r) const {
+#pragma unroll
+        for (int q = 0; q < 27; ++q) r.w[q] = static_cast<Word>(plane_load3<W>(P, c, q));
+        r.e = __ldg(P.ec + c);
+    }
+    __device__ __forceinline__ void decode(const Raw& r, double* v) const {
+        const Base3 B(r.e, P.s1, P.h);
+        const PlaneDec dec(W);
+#pragma unroll
+        for (int q = 0; q < 27; ++q) v[q] = B(q / 9, (q / 3) % 3, q % 3) + dec(static_cast<unsigned long long>(r.w[q]));
+    }
     __device__ __forceinline__ void load27(int64_t c, double* v) const {
         unsigned long long w[27];
 #pragma unroll
@@ -678,7 +709,7 @@ __global__ void k3_uhat(Lv3 F, Lv3 C, int has_coarse) {
 // u / û corners of the layer below stay in registers.
 constexpr int kRzX = 32, kRzY = 8, kRzChunk = 32;  // chunk: vertex planes per block (at most)
 template <class Src>
-__global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_z(Lv3 F, Src S, int zbeg, int zend, int zc) {
+__global__ void __launch_bounds__(kRzX * kRzY, 1) k3_residual_z(Lv3 F, Src S, int zbeg, int zend, int zc) {
     lzb_pdl_enter();
     __shared__ double sy[3][8][kRzX * kRzY];  // [u, û, diag][corner][cell of the tile]
     const int tx = threadIdx.x % kRzX, ty = threadIdx.x / kRzX, t = threadIdx.x;
@@ -692,16 +723,26 @@ __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_z(Lv3 F, Src S, in
     const bool vthr = tx < kRzX - 1 && ty < kRzY - 1 && ix <= N && iy <= N;
     const double* __restrict__ U = F.v[LZB_V_U];
     const double* __restrict__ UH = F.v[LZB_V_UHAT];
+    const double* __restrict__ FL = F.v[LZB_V_FL];
     auto vid = [&](int x, int y, int z) {
         return (static_cast<int64_t>(min(max(z, 0), N)) * NV + min(max(y, 0), N)) * NV + min(max(x, 0), N);
     };
-    double ul[4], uhl[4];  // corners of the current layer's lower plane
+    auto cell = [&](int z) { return (static_cast<int64_t>(z) * N + cy) * N + cx; };
+    // software pipeline, one cell layer ahead: the next layer's class values
+    // and upper corners and the next vertex plane's load are in flight while
+    // the current layer computes (the kernel is latency-bound otherwise)
+    double ul[4], uhl[4], un[4], uhn[4];  // corners of the layer's lower / upper plane
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const int64_t v = vid(cx + (k & 1), cy + (k >> 1), zs - 1);
-        ul[k] = U[v];
-        uhl[k] = UH[v];
+        const int64_t v0 = vid(cx + (k & 1), cy + (k >> 1), zs - 1), v1 = vid(cx + (k & 1), cy + (k >> 1), zs);
+        ul[k] = U[v0];
+        uhl[k] = UH[v0];
+        un[k] = U[v1];
+        uhn[k] = UH[v1];
     }
+    typename Src::Raw nxt;
+    if (colok && zs - 1 >= 0) S.fetch(cell(zs - 1), nxt);
+    double fln = vthr ? FL[vid(ix, iy, zs)] : 0.0;  // plane zs: opened in the first iteration
     double rp = 0.0, rhp = 0.0, dgp = 0.0;  // partial sums of the vertex plane being completed
     for (int cz = zs - 1; cz < ze; ++cz) {
         // 1. this thread's cell of layer cz: row products into shared memory
@@ -710,16 +751,27 @@ __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_z(Lv3 F, Src S, in
         for (int k = 0; k < 4; ++k) {
             uu[k] = ul[k];
             uh[k] = uhl[k];
-            const int64_t v = vid(cx + (k & 1), cy + (k >> 1), cz + 1);
-            uu[4 + k] = U[v];
-            uh[4 + k] = UH[v];
-            ul[k] = uu[4 + k];
-            uhl[k] = uh[4 + k];
+            uu[4 + k] = un[k];
+            uh[4 + k] = uhn[k];
+            ul[k] = un[k];
+            uhl[k] = uhn[k];
         }
+        const typename Src::Raw cur = nxt;
         const bool ok = colok && cz >= 0 && cz < N;
+        const double flc = fln;
+        if (cz + 1 < ze) {  // the next layer's operands
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int64_t v = vid(cx + (k & 1), cy + (k >> 1), cz + 2);
+                un[k] = U[v];
+                uhn[k] = UH[v];
+            }
+            if (colok && cz + 1 < N) S.fetch(cell(cz + 1), nxt);
+            if (vthr) fln = FL[vid(ix, iy, cz + 2)];
+        }
         if (ok) {
             double K[27];
-            S.load27((static_cast<int64_t>(cz) * N + cy) * N + cx, K);
+            S.decode(cur, K);
 #pragma unroll
             for (int a = 0; a < 8; ++a) {
                 double au = 0.0, auh = 0.0;
@@ -758,12 +810,12 @@ __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_z(Lv3 F, Src S, in
                     rh = 0.0;
                 }
                 const int64_t vi = (static_cast<int64_t>(cz) * NV + iy) * NV + ix;
-                F.v[LZB_V_R][vi] = r;
-                F.v[LZB_V_RHAT][vi] = rh;
-                F.v[LZB_V_DIAG][vi] = dgp;
+                __stcs(F.v[LZB_V_R] + vi, r);
+                __stcs(F.v[LZB_V_RHAT] + vi, rh);
+                __stcs(F.v[LZB_V_DIAG] + vi, dgp);
             }
             if (cz + 1 < ze) {  // plane cz + 1: fl, then the cells of layer cz below it
-                rp = rhp = F.v[LZB_V_FL][(static_cast<int64_t>(cz + 1) * NV + iy) * NV + ix];
+                rp = rhp = flc;
                 dgp = 0.0;
                 if (cz >= 0) {
 #pragma unroll

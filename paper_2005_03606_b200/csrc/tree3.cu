@@ -12,6 +12,7 @@
 // levels are generated (parents in order, children z-major); operators are
 // class planes over the leaf index (value q of leaf i at q * nleaves + i).
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <unordered_map>
 #include <vector>
@@ -694,20 +695,32 @@ public:
     // are kept: init_cycle zeroes them, a re-refinement carries them over)
     void setup_levels() {
         const int D = lmax_;
+        // per level the bounding box of its existing cells: its leaves' box
+        // joined with the box of the parents of the level below (one pass
+        // over the leaves, then finest to coarsest)
+        std::vector<std::array<int, 6>> cb(D + 2, std::array<int, 6>{INT32_MAX, -1, INT32_MAX, -1, INT32_MAX, -1});
+        for (const int4& c : leaves_) {
+            auto& b = cb[c.x];
+            const int q[3] = {c.y, c.z, c.w};
+            for (int d = 0; d < 3; ++d) {
+                b[2 * d] = std::min(b[2 * d], q[d]);
+                b[2 * d + 1] = std::max(b[2 * d + 1], q[d]);
+            }
+        }
+        for (int l = D - 1; l >= 0; --l)
+            if (cb[l + 1][1] >= 0)
+                for (int d = 0; d < 3; ++d) {
+                    cb[l][2 * d] = std::min(cb[l][2 * d], cb[l + 1][2 * d] / 3);
+                    cb[l][2 * d + 1] = std::max(cb[l][2 * d + 1], cb[l + 1][2 * d + 1] / 3);
+                }
         for (int l = 0; l <= D; ++l) {
             LevA& L = A_[l];
             // the vertex box of the level's existing cells: the leaves of level l
             // and the ancestors at level l of every deeper leaf
-            int lo[3] = {L.N, L.N, L.N}, hi[3] = {-1, -1, -1};
-            for (const int4& c : leaves_) {
-                if (c.x < l) continue;
-                int sh = 1;
-                for (int k = l; k < c.x; ++k) sh *= 3;
-                const int q[3] = {c.y / sh, c.z / sh, c.w / sh};
-                for (int d = 0; d < 3; ++d) {
-                    lo[d] = std::min(lo[d], q[d]);
-                    hi[d] = std::max(hi[d], q[d]);
-                }
+            int lo[3], hi[3];
+            for (int d = 0; d < 3; ++d) {
+                lo[d] = cb[l][2 * d];
+                hi[d] = cb[l][2 * d + 1];
             }
             for (int d = 0; d < 3; ++d) {
                 L.box[2 * d] = hi[d] < 0 ? 0 : lo[d];
