@@ -18,6 +18,8 @@
 // Layout in HBM: cell operators as class records (the 27 distinct values of
 // the 8x8 matrix, padded to 28 doubles = 224 B per cell), index
 // (cz*N + cy)*N + cx; markers p3 (i8), n (i32).
+#include <cuda.h>
+
 #include <complex>
 #include <type_traits>
 #include <memory>
@@ -336,14 +338,28 @@ struct Base3 {
 // array of 27 planes of nc words, so a warp reads 2..8 consecutive bytes per
 // cell per piece. The stored operator is Base3(eps centre) + rt, bit for bit
 // the FP64 class value (k_assemble3 stores exactly that).
+// Storage of the leaf level's per-cell planes (class planes, plane-word
+// pieces, eps centre): a 3D array [z][y + 1][x + 1] with one leading pad row
+// and column (the TMA tiles of the residual start one cell before the block's
+// first vertex; tensor coordinates must not be negative) and the x extent
+// padded to xp (a multiple of 16: every row starts 16-byte aligned). nc is the
+// storage size of one plane (N (N + 1) xp); a cell's storage index is
+// plane_sidx of its linear index.
+__host__ __device__ __forceinline__ int64_t plane_sidx(int64_t c, int N, int xp) {
+    if (!xp) return c;
+    const int64_t t = c / N;
+    return ((t / N) * (N + 1) + t % N + 1) * xp + c % N + 1;
+}
 struct Planes3 {
     uint8_t* base;  // piece arrays back to back, largest piece first
     double* ec;     // eps at the cell centre
-    int64_t nc;
+    int64_t nc;     // storage elements per plane
     double h;
     double s1[3];  // seg_int classes of the n = 1 sub-interval
+    int N, xp;     // cells per axis, padded x extent (0: linear storage)
 };
 
+// c: the cell's storage index (plane_sidx)
 template <int W>
 __device__ __forceinline__ unsigned long long plane_load3(const Planes3& P, int64_t c, int q) {
     const int64_t i = q * P.nc + c;
@@ -391,23 +407,27 @@ __device__ __forceinline__ void plane_store3(const Planes3& P, int W, int64_t c,
 // the z-marching residual prefetches the next cell layer with it.
 struct Src64 {
     const double* op;
-    int64_t nc;
+    int64_t nc;      // storage elements per class plane
+    int N = 0, xp = 0;  // padded leaf storage (plane_sidx); 0: linear
     struct Raw {
         double v[27];
     };
-    __device__ __forceinline__ double at(int64_t c, int q) const { return __ldg(op + q * nc + c); }
+    __device__ __forceinline__ double at(int64_t c, int q) const { return __ldg(op + q * nc + plane_sidx(c, N, xp)); }
     __device__ __forceinline__ void load27(int64_t c, double* v) const {
+        const int64_t s = plane_sidx(c, N, xp);
 #pragma unroll
-        for (int q = 0; q < 27; ++q) v[q] = at(c, q);
+        for (int q = 0; q < 27; ++q) v[q] = __ldg(op + q * nc + s);
     }
     __device__ __forceinline__ void fetch(int64_t c, Raw& r) const {
+        const int64_t s = plane_sidx(c, N, xp);
 #pragma unroll
-        for (int q = 0; q < 27; ++q) r.v[q] = at(c, q);
+        for (int q = 0; q < 27; ++q) r.v[q] = __ldg(op + q * nc + s);
     }
     __device__ __forceinline__ void decode(const Raw& r, double* v) const {
 #pragma unroll
         for (int q = 0; q < 27; ++q) v[q] = r.v[q];
     }
+    static constexpr int kMinBlocks = 1;
 };
 template <int W>
 struct SrcComp {
@@ -418,21 +438,39 @@ struct SrcComp {
         double e;
     };
     __device__ __forceinline__ void fetch(int64_t c, Raw& r) const {
+        const int64_t sc = plane_sidx(c, P.N, P.xp);
 #pragma unroll
-        for (int q = 0; q < 27; ++q) r.w[q] = static_cast<Word>(plane_load3<W>(P, c, q));
-        r.e = __ldg(P.ec + c);
+        for (int q = 0; q < 27; ++q) r.w[q] = static_cast<Word>(plane_load3<W>(P, sc, q));
+        r.e = __ldg(P.ec + sc);
+    }
+    // the roundtrip value of a W-byte plane word (PlaneDec(W), with 32-bit
+    // integer work for the words of at most 4 bytes)
+    __device__ __forceinline__ static double dec(Word w) {
+        if constexpr (W == 8) {
+            return __longlong_as_double(static_cast<long long>(w));
+        } else if constexpr (W <= 4) {
+            if (w == 0) return 0.0;
+            constexpr int m = 8 * (W - 1) - 1;
+            const uint32_t sign = (w >> (8 * W - 1)) & 1u, e8 = (w >> m) & 0xffu, fr = w & ((1u << m) - 1u);
+            const uint32_t hi = (sign << 31) | ((e8 + 895u) << 20) | (m > 20 ? fr >> (m - 20) : fr << (20 - m));
+            const uint32_t lo = m > 20 ? fr << (52 - m) : 0u;
+            return __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
+        } else {
+            return PlaneDec(W)(static_cast<unsigned long long>(w));
+        }
     }
     __device__ __forceinline__ void decode(const Raw& r, double* v) const {
         const Base3 B(r.e, P.s1, P.h);
-        const PlaneDec dec(W);
 #pragma unroll
-        for (int q = 0; q < 27; ++q) v[q] = B(q / 9, (q / 3) % 3, q % 3) + dec(static_cast<unsigned long long>(r.w[q]));
+        for (int q = 0; q < 27; ++q) v[q] = B(q / 9, (q / 3) % 3, q % 3) + dec(r.w[q]);
     }
+    static constexpr int kMinBlocks = 1;
     __device__ __forceinline__ void load27(int64_t c, double* v) const {
         unsigned long long w[27];
+        const int64_t sc = plane_sidx(c, P.N, P.xp);
 #pragma unroll
-        for (int q = 0; q < 27; ++q) w[q] = plane_load3<W>(P, c, q);
-        const Base3 B(__ldg(P.ec + c), P.s1, P.h);
+        for (int q = 0; q < 27; ++q) w[q] = plane_load3<W>(P, sc, q);
+        const Base3 B(__ldg(P.ec + sc), P.s1, P.h);
         const PlaneDec dec(W);
 #pragma unroll
         for (int q = 0; q < 27; ++q) v[q] = B(q / 9, (q / 3) % 3, q % 3) + dec(w[q]);
@@ -516,9 +554,9 @@ __global__ void __launch_bounds__(128, 4) k_assemble3(Field3 F, int N, double h,
                                                       int64_t cbeg, int64_t cend) {
     lzb_pdl_enter();
     const int64_t c = cbeg + gtid();  // cells [cbeg, cend): whole z planes
-    const int64_t nc = static_cast<int64_t>(N) * N * N;
     if (c >= cend) return;
     const int cx = static_cast<int>(c % N), cy = static_cast<int>((c / N) % N), cz = static_cast<int>(c / N / N);
+    const int64_t nc = PL.nc, sc = plane_sidx(c, PL.N, PL.xp);  // storage of the planes
     const double x0 = cx * h, y0 = cy * h, z0 = cz * h;
     const double e = centre_eps3(F, x0, y0, z0, h);
     const Base3 B(e, PL.s1, h);  // A(n=1): eps(centre) * unit stiffness, recomputed per class (9 products)
@@ -541,7 +579,7 @@ __global__ void __launch_bounds__(128, 4) k_assemble3(Field3 F, int N, double h,
         atomicExch(wide, 1);  // record wider than the planes
         return;
     }
-    if (W != 0) PL.ec[c] = e;
+    if (W != 0) PL.ec[sc] = e;
     double delta = 0.0;
 #pragma unroll
     for (int q = 0; q < 27; ++q) {
@@ -552,8 +590,8 @@ __global__ void __launch_bounds__(128, 4) k_assemble3(Field3 F, int N, double h,
         }
         const double d = fabs(rt - sur[q]);
         delta = delta < d ? d : delta;
-        if (W == 0) op[q * nc + c] = B(q / 9, (q / 3) % 3, q % 3) + rt;
-        else plane_store3(PL, W, c, q, plane_word(rt, W));
+        if (W == 0) op[q * nc + sc] = B(q / 9, (q / 3) % 3, q % 3) + rt;
+        else plane_store3(PL, W, sc, q, plane_word(rt, W));
     }
     p3o[c] = static_cast<int8_t>(p3);
     no[c] = T.n;
@@ -709,7 +747,8 @@ __global__ void k3_uhat(Lv3 F, Lv3 C, int has_coarse) {
 // u / û corners of the layer below stay in registers.
 constexpr int kRzX = 32, kRzY = 8, kRzChunk = 32;  // chunk: vertex planes per block (at most)
 template <class Src>
-__global__ void __launch_bounds__(kRzX * kRzY, 1) k3_residual_z(Lv3 F, Src S, int zbeg, int zend, int zc) {
+__global__ void __launch_bounds__(kRzX * kRzY, Src::kMinBlocks) k3_residual_z(Lv3 F, Src S, int zbeg, int zend,
+                                                                              int zc) {
     lzb_pdl_enter();
     __shared__ double sy[3][8][kRzX * kRzY];  // [u, û, diag][corner][cell of the tile]
     const int tx = threadIdx.x % kRzX, ty = threadIdx.x / kRzX, t = threadIdx.x;
@@ -815,6 +854,221 @@ __global__ void __launch_bounds__(kRzX * kRzY, 1) k3_residual_z(Lv3 F, Src S, in
                 __stcs(F.v[LZB_V_DIAG] + vi, dgp);
             }
             if (cz + 1 < ze) {  // plane cz + 1: fl, then the cells of layer cz below it
+                rp = rhp = flc;
+                dgp = 0.0;
+                if (cz >= 0) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) sub(q, rp, rhp, dgp);
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---- the leaf residual with TMA tile staging (sm_100a: cp.async.bulk.tensor
+// + mbarrier). The leaf planes are 4D tensors [class q][z][y][x padded]; per
+// cell layer one elected thread issues one tensor copy per plane piece (the
+// block's 32 x 8 cells x 27 classes; out-of-range cells are zero-filled by
+// the TMA unit) plus, for compressed planes, one of eps(centre), into a
+// shared-memory stage armed on an mbarrier; the copy of layer cz + 1 runs
+// while the block's threads finish layer cz's vertex sums and open the next
+// layer. Each cell thread decodes its own 27 class values from the stage.
+// Same products, same sums, same order as k3_residual_z: identical results.
+struct TmaMaps {
+    CUtensorMap piece[3];  // plane pieces, largest first (FP64: piece 0 = the doubles)
+    CUtensorMap ec;        // eps(centre) (compressed planes)
+};
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+// piece sizes of a plane word of W bytes (W = 0: one piece of FP64 values)
+__host__ __device__ constexpr int tma_piece(int W, int k) {
+    return W == 0 ? (k == 0 ? 8 : 0)
+           : W == 8 ? (k == 0 ? 8 : 0)
+                    : (k == 0 ? ((W & 4) ? 4 : (W & 2) ? 2 : 1)
+                               : k == 1 ? ((W & 4) ? ((W & 2) ? 2 : (W & 1) ? 1 : 0) : (W & 2) ? ((W & 1) ? 1 : 0) : 0)
+                                        : ((W & 4) && (W & 2) && (W & 1)) ? 1 : 0);
+}
+constexpr int kTmaCells = kRzX * kRzY;  // cells of one layer of a block tile
+// A tensor copy's box must start 16-byte aligned in x: the box of a piece of
+// e-byte elements starts at the tile's first storage x rounded down to 16 / e
+// elements and is 32 + 16 / e elements wide (the tile sits at offset < 16 / e).
+__host__ __device__ constexpr int tma_width(int e) { return e ? kRzX + 16 / e : 0; }
+__host__ __device__ constexpr int tma_piece_bytes(int e) { return 27 * kRzY * tma_width(e) * e; }
+__host__ __device__ constexpr int tma_stage_bytes(int W) {
+    return tma_piece_bytes(tma_piece(W, 0)) + tma_piece_bytes(tma_piece(W, 1)) + tma_piece_bytes(tma_piece(W, 2)) +
+           (W ? kRzY * tma_width(8) * 8 : 0);
+}
+__host__ __device__ constexpr int tma_smem_bytes(int W) {
+    return 3 * 8 * kTmaCells * 8 + tma_stage_bytes(W) + 16;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_tma(Lv3 F, const __grid_constant__ TmaMaps M,
+                                                                 Planes3 P, int zbeg, int zend, int zc) {
+    lzb_pdl_enter();
+    extern __shared__ __align__(128) unsigned char smraw[];
+    double(*sy)[8][kTmaCells] = reinterpret_cast<double(*)[8][kTmaCells]>(smraw);  // [u, û, diag][corner][cell]
+    unsigned char* stage = smraw + 3 * 8 * kTmaCells * 8;
+    constexpr int e0 = tma_piece(W, 0), e1 = tma_piece(W, 1), e2 = tma_piece(W, 2);
+    constexpr int w0 = tma_width(e0), w1 = tma_width(e1), w2 = tma_width(e2), we = tma_width(8);
+    unsigned char* pc0 = stage;
+    unsigned char* pc1 = pc0 + tma_piece_bytes(e0);
+    unsigned char* pc2 = pc1 + tma_piece_bytes(e1);
+    double* sec = reinterpret_cast<double*>(pc2 + tma_piece_bytes(e2));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + tma_smem_bytes(W) - 16);
+    const int tx = threadIdx.x % kRzX, ty = threadIdx.x / kRzX, t = threadIdx.x;
+    const int N = F.N, NV = N + 1;
+    const int X0 = blockIdx.x * (kRzX - 1), Y0 = blockIdx.y * (kRzY - 1);
+    const int zs = zbeg + blockIdx.z * zc, ze = min(zs + zc, zend);
+    if (zs >= ze) return;
+    const int cx = X0 - 1 + tx, cy = Y0 - 1 + ty;  // this thread's cell column
+    const bool colok = cx >= 0 && cy >= 0 && cx < N && cy < N;
+    const int ix = X0 + tx, iy = Y0 + ty;  // this thread's vertex column (tx < 31, ty < 7)
+    const bool vthr = tx < kRzX - 1 && ty < kRzY - 1 && ix <= N && iy <= N;
+    const double* __restrict__ U = F.v[LZB_V_U];
+    const double* __restrict__ UH = F.v[LZB_V_UHAT];
+    const double* __restrict__ FL = F.v[LZB_V_FL];
+    auto vid = [&](int x, int y, int z) {
+        return (static_cast<int64_t>(min(max(z, 0), N)) * NV + min(max(y, 0), N)) * NV + min(max(x, 0), N);
+    };
+    auto issue = [&](int cz) {  // one elected thread: the layer's tiles into the stage
+        mbar_expect(bar, static_cast<uint32_t>(tma_stage_bytes(W)));
+        // storage x / y of cell (X0 - 1, Y0 - 1) are X0 / Y0 (the leading pad);
+        // each box starts at X0 rounded down to its 16-byte alignment
+        tma_load_4d(pc0, &M.piece[0], X0 & ~(16 / e0 - 1), Y0, cz, 0, bar);
+        if (e1) tma_load_4d(pc1, &M.piece[1], X0 & ~(16 / (e1 ? e1 : 1) - 1), Y0, cz, 0, bar);
+        if (e2) tma_load_4d(pc2, &M.piece[2], X0 & ~(16 / (e2 ? e2 : 1) - 1), Y0, cz, 0, bar);
+        if (W) tma_load_3d(sec, &M.ec, X0 & ~1, Y0, cz, bar);
+    };
+    auto layer_ok = [&](int cz) { return cz >= 0 && cz < N; };
+    if (t == 0) mbar_init(bar, 1);
+    __syncthreads();
+    uint32_t phase = 0;
+    if (t == 0 && layer_ok(zs - 1)) issue(zs - 1);
+    double ul[4], uhl[4];  // corners of the current layer's lower plane
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t v = vid(cx + (k & 1), cy + (k >> 1), zs - 1);
+        ul[k] = U[v];
+        uhl[k] = UH[v];
+    }
+    double rp = 0.0, rhp = 0.0, dgp = 0.0;  // partial sums of the vertex plane being completed
+    for (int cz = zs - 1; cz < ze; ++cz) {
+        double uu[8], uh[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            uu[k] = ul[k];
+            uh[k] = uhl[k];
+            const int64_t v = vid(cx + (k & 1), cy + (k >> 1), cz + 1);
+            uu[4 + k] = U[v];
+            uh[4 + k] = UH[v];
+            ul[k] = uu[4 + k];
+            uhl[k] = uh[4 + k];
+        }
+        const double flc = (vthr && cz + 1 < ze) ? FL[vid(ix, iy, cz + 1)] : 0.0;
+        if (layer_ok(cz)) {
+            mbar_wait(bar, phase);
+            phase ^= 1u;
+            if (colok) {
+                double K[27];
+                // the cell's slot in each box: row ty, column tx + the box's alignment offset
+                const int i0 = ty * w0 + tx + (X0 & (16 / e0 - 1));
+                if constexpr (W == 0) {
+#pragma unroll
+                    for (int q = 0; q < 27; ++q) K[q] = reinterpret_cast<const double*>(pc0)[q * kRzY * w0 + i0];
+                } else {
+                    const int i1 = ty * w1 + tx + (e1 ? (X0 & (16 / (e1 ? e1 : 1) - 1)) : 0);
+                    const int i2 = ty * w2 + tx + (e2 ? (X0 & (16 / (e2 ? e2 : 1) - 1)) : 0);
+                    const Base3 B(sec[ty * we + tx + (X0 & 1)], P.s1, P.h);
+#pragma unroll
+                    for (int q = 0; q < 27; ++q) {
+                        unsigned long long w;
+                        if constexpr (e0 == 8) w = reinterpret_cast<const unsigned long long*>(pc0)[q * kRzY * w0 + i0];
+                        else if constexpr (e0 == 4) w = reinterpret_cast<const uint32_t*>(pc0)[q * kRzY * w0 + i0];
+                        else if constexpr (e0 == 2) w = reinterpret_cast<const uint16_t*>(pc0)[q * kRzY * w0 + i0];
+                        else w = pc0[q * kRzY * w0 + i0];
+                        if constexpr (e1 == 2) w |= static_cast<unsigned long long>(reinterpret_cast<const uint16_t*>(pc1)[q * kRzY * w1 + i1]) << (8 * e0);
+                        else if constexpr (e1 == 1) w |= static_cast<unsigned long long>(pc1[q * kRzY * w1 + i1]) << (8 * e0);
+                        if constexpr (e2 == 1) w |= static_cast<unsigned long long>(pc2[q * kRzY * w2 + i2]) << (8 * (e0 + e1));
+                        K[q] = B(q / 9, (q / 3) % 3, q % 3) + SrcComp<W>::dec(static_cast<typename SrcComp<W>::Word>(w));
+                    }
+                }
+#pragma unroll
+                for (int a = 0; a < 8; ++a) {
+                    double au = 0.0, auh = 0.0;
+#pragma unroll
+                    for (int col = 0; col < 8; ++col) {  // explicit FMA (the 3D cycle is restated, not pinned bitwise)
+                        au = __fma_rn(K[cls3(a, col)], uu[col], au);
+                        auh = __fma_rn(K[cls3(a, col)], uh[col], auh);
+                    }
+                    sy[0][a][t] = au;
+                    sy[1][a][t] = auh;
+                    sy[2][a][t] = K[cls3(a, a)];
+                }
+            }
+        }
+        __syncthreads();  // the stage is consumed: the next layer's copy may land in it
+        if (t == 0 && cz + 1 < ze && layer_ok(cz + 1)) issue(cz + 1);
+        if (vthr) {
+            auto sub = [&](int q, double& r, double& rh, double& dg) {
+                const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;
+                const int row = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
+                const int ccx = ix - 1 + dx, ccy = iy - 1 + dy;
+                if (ccx < 0 || ccy < 0 || ccx >= N || ccy >= N) return;
+                const int c = (ty + dy) * kRzX + tx + dx;
+                r -= sy[0][row][c];
+                rh -= sy[1][row][c];
+                dg += sy[2][row][c];
+            };
+            if (cz >= zs && cz < N) {
+#pragma unroll
+                for (int q = 4; q < 8; ++q) sub(q, rp, rhp, dgp);
+            }
+            if (cz >= zs) {
+                double r = rp, rh = rhp;
+                if (bnd3(N, ix, iy, cz)) {
+                    r = 0.0;
+                    rh = 0.0;
+                }
+                const int64_t vi = (static_cast<int64_t>(cz) * NV + iy) * NV + ix;
+                __stcs(F.v[LZB_V_R] + vi, r);
+                __stcs(F.v[LZB_V_RHAT] + vi, rh);
+                __stcs(F.v[LZB_V_DIAG] + vi, dgp);
+            }
+            if (cz + 1 < ze) {
                 rp = rhp = flc;
                 dgp = 0.0;
                 if (cz >= 0) {
@@ -1345,13 +1599,15 @@ public:
         N_ = 1;
         for (int i = 0; i < depth; ++i) N_ *= 3;
         nc_ = static_cast<int64_t>(N_) * N_ * N_;
+        xp_ = (N_ + 1 + 15) / 16 * 16;
+        ncs_ = static_cast<int64_t>(N_) * (N_ + 1) * xp_;
         h_ = std::pow(1.0 / 3, depth);
         F_ = to_device(f, table_);
         if (W_ == 0) {
-            op_.alloc(static_cast<size_t>(nc_) * kCls3);
+            op_.alloc(static_cast<size_t>(ncs_) * kCls3);
         } else {  // compressed class planes + eps(centre); no FP64 leaf operators
-            planes_.alloc(static_cast<size_t>(nc_) * kCls3 * W_);
-            ec_.alloc(nc_);
+            planes_.alloc(static_cast<size_t>(ncs_) * kCls3 * W_);
+            ec_.alloc(ncs_);
         }
         wide_.alloc(1);
         LZB_CUDA(cudaMemsetAsync(wide_.p, 0, sizeof(int), s_));
@@ -1829,7 +2085,8 @@ private:
     lzb_ctx* ctx_;
     cudaStream_t s_ = nullptr;
     int D_, N_ = 1, n_last_ = 0, fixed_, W_ = 0;
-    int64_t nc_ = 1;
+    int64_t nc_ = 1, ncs_ = 1;  // leaf cells, storage elements of one leaf plane
+    int xp_ = 16;                // padded x extent of the leaf planes
     double h_ = 1.0, delta_;
     Field3 F_{};
     DevBuf<double> table_, op_, ec_;
@@ -1870,7 +2127,9 @@ private:
         Planes3 P{};
         P.base = planes_.p;
         P.ec = ec_.p;
-        P.nc = nc_;
+        P.nc = ncs_;
+        P.N = N_;
+        P.xp = xp_;
         P.h = h_;
         const AxisTab3 T1 = axis_tab3(1);
         for (int c = 0; c < 3; ++c) P.s1[c] = T1.s[0][c];
@@ -1880,7 +2139,7 @@ private:
     template <class Fn>
     void leaf_cls(Fn&& fn, int w = -1) const {
         switch (w < 0 ? W_ : w) {
-            case 0: fn(Src64{op_.p, nc_}); break;
+            case 0: fn(Src64{op_.p, ncs_, N_, xp_}); break;
             case 2: fn(SrcComp<2>{planes()}); break;
             case 3: fn(SrcComp<3>{planes()}); break;
             case 4: fn(SrcComp<4>{planes()}); break;
@@ -1903,12 +2162,92 @@ private:
             zc /= 2;
         const dim3 grid(bx, by, (z1 - z0 + zc - 1) / zc);
         const Lv3 v = lv(l);
+        if (l == D_ && use_tma_) {  // the leaves: TMA-staged tiles (k3_residual_tma)
+            const dim3 g2(bx, by, (z1 - z0 + zc2(bx, by, z0, z1) - 1) / zc2(bx, by, z0, z1));
+            const int zcl = zc2(bx, by, z0, z1);
+            switch (W_) {
+                case 0: launch_tma<0>(g2, v, z0, z1, zcl); break;
+                case 2: launch_tma<2>(g2, v, z0, z1, zcl); break;
+                case 3: launch_tma<3>(g2, v, z0, z1, zcl); break;
+                case 4: launch_tma<4>(g2, v, z0, z1, zcl); break;
+                case 5: launch_tma<5>(g2, v, z0, z1, zcl); break;
+                case 6: launch_tma<6>(g2, v, z0, z1, zcl); break;
+                case 7: launch_tma<7>(g2, v, z0, z1, zcl); break;
+                default: launch_tma<8>(g2, v, z0, z1, zcl); break;
+            }
+            return;
+        }
         if (l < D_ || W_ == 0) {
-            const Src64 S{l < D_ ? L3_[l].op.p : op_.p, static_cast<int64_t>(N) * N * N};
+            const Src64 S = l < D_ ? Src64{L3_[l].op.p, static_cast<int64_t>(N) * N * N}
+                                   : Src64{op_.p, ncs_, N_, xp_};
             LZB_LAUNCH(k3_residual_z<Src64>, grid, kRzX * kRzY, 0, s_, v, S, z0, z1, zc);
             return;
         }
         leaf_cls([&](auto S) { LZB_LAUNCH(k3_residual_z<decltype(S)>, grid, kRzX * kRzY, 0, s_, v, S, z0, z1, zc); });
+    }
+    // planes per block of the TMA residual: as residual3's rule with 2 blocks per SM
+    int zc2(int bx, int by, int z0, int z1) const {
+        int zc = kRzChunk;
+        while (zc > 2 && static_cast<int64_t>(bx) * by * ((z1 - z0 + zc - 1) / zc) < 4 * 2 * ctx_->sms) zc /= 2;
+        return zc;
+    }
+    // TMA tensor maps of the leaf planes (built once: the storage never moves)
+    bool use_tma_ = std::getenv("LZB_NO_TMA") == nullptr;
+    bool maps_ready_ = false;
+    TmaMaps maps_{};
+    void build_maps() {
+        if (maps_ready_) return;
+        using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+        static Encode encode = nullptr;
+        if (!encode) {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            LZB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+            if (!fn || q != cudaDriverEntryPointSuccess) throw Error(LZB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+            encode = reinterpret_cast<Encode>(fn);
+        }
+        auto dtype = [](int e) {
+            return e == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : e == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
+                   : e == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+        };
+        auto make = [&](CUtensorMap* m, void* base, int e, int rank) {
+            const cuuint64_t dims[4] = {static_cast<cuuint64_t>(xp_), static_cast<cuuint64_t>(N_ + 1),
+                                        static_cast<cuuint64_t>(N_), 27};
+            const cuuint64_t strides[3] = {static_cast<cuuint64_t>(xp_) * e,
+                                           static_cast<cuuint64_t>(xp_) * (N_ + 1) * e,
+                                           static_cast<cuuint64_t>(ncs_) * e};
+            const cuuint32_t box[4] = {static_cast<cuuint32_t>(tma_width(e)), kRzY, 1, 27}, es[4] = {1, 1, 1, 1};
+            const CUresult r = encode(m, dtype(e), rank, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) throw Error(LZB_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+        };
+        if (W_ == 0) {
+            make(&maps_.piece[0], op_.p, 8, 4);
+        } else {
+            size_t off = 0;
+            for (int k = 0; k < 3; ++k) {
+                const int e = tma_piece(W_, k);
+                if (!e) break;
+                make(&maps_.piece[k], planes_.p + off, e, 4);
+                off += static_cast<size_t>(e) * 27 * ncs_;
+            }
+            make(&maps_.ec, ec_.p, 8, 3);
+        }
+        maps_ready_ = true;
+    }
+    template <int W>
+    void launch_tma(dim3 g, const Lv3& v, int z0, int z1, int zc) {
+        build_maps();
+        static bool attr = false;
+        if (!attr) {
+            LZB_CUDA(cudaFuncSetAttribute(k3_residual_tma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          tma_smem_bytes(W)));
+            attr = true;
+        }
+        LZB_LAUNCH(k3_residual_tma<W>, g, kRzX * kRzY, tma_smem_bytes(W), s_, v, maps_, planes(), z0, z1, zc);
     }
     bool uhat_is_u_ = false;
     double damping3(int l) const { return variant_ == LZB_ADDITIVE ? std::pow(omega_, D_ - l + 1) : omega_; }
