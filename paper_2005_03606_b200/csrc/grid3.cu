@@ -464,6 +464,11 @@ struct SrcComp {
 #pragma unroll
         for (int q = 0; q < 27; ++q) v[q] = B(q / 9, (q / 3) % 3, q % 3) + dec(r.w[q]);
     }
+    __device__ __forceinline__ double at(int64_t c, int q) const {  // one class value
+        const int64_t sc = plane_sidx(c, P.N, P.xp);
+        const Base3 B(__ldg(P.ec + sc), P.s1, P.h);
+        return B(q / 9, (q / 3) % 3, q % 3) + dec(static_cast<Word>(plane_load3<W>(P, sc, q)));
+    }
     static constexpr int kMinBlocks = 1;
     __device__ __forceinline__ void load27(int64_t c, double* v) const {
         unsigned long long w[27];
@@ -935,20 +940,67 @@ __host__ __device__ constexpr int tma_smem_bytes(int W) {
     return 3 * 8 * kTmaCells * 8 + tma_stage_bytes(W) + 16;
 }
 
-template <int W>
+// The leaf level's Jacobi diagonal (the residual's dg: the 8 adjacent cells'
+// diagonal entries, in its order -- the 4 cells below the vertex plane, then
+// the 4 above), once per change of the leaf operators: the TMA residual does
+// not recompute / rewrite it every cycle.
+template <class Src>
+__global__ void k3_leaf_diag(Lv3 F, Src S) {
+    lzb_pdl_enter();
+    int ix, iy, iz;
+    int64_t vi;
+    if (!vxyz(F, ix, iy, iz, vi)) return;
+    const int N = F.N;
+    double dg = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;
+        const int row = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
+        const int cx = ix - 1 + dx, cy = iy - 1 + dy, cz = iz - 1 + dz;
+        if (cx < 0 || cy < 0 || cz < 0 || cx >= N || cy >= N || cz >= N) continue;
+        dg += S.at((static_cast<int64_t>(cz) * N + cy) * N + cx, cls3(row, row));
+    }
+    F.v[LZB_V_DIAG][vi] = dg;
+}
+
+// u / u-hat tiles of a vertex plane (corners of a block's 32 x 8 cells: x from
+// the cells' first column rounded down to even, 34 wide; y from the first
+// row, 9 rows) and the vertex plane's load tile (32 x 8)
+constexpr int kTmaUX = 34, kTmaUY = 9, kTmaFX = 32, kTmaFY = 8;
+// tensor-copy destinations start 128-byte aligned: each tile's slot rounded up
+constexpr int kTmaUSlot = (kTmaUX * kTmaUY * 8 + 127) / 128 * 128 / 8;  // doubles
+__host__ __device__ constexpr int tma_vbytes() { return (2 * kTmaUSlot + kTmaFX * kTmaFY) * 8; }
+
+struct TmaVMaps {
+    CUtensorMap u, uh, fl;
+};
+__host__ __device__ constexpr int tma_stage_total(int W) { return tma_stage_bytes(W) + tma_vbytes(); }
+__host__ __device__ constexpr int tma_smem_bytes2(int W, int S) {
+    return 2 * 8 * kTmaCells * 8 + S * tma_stage_total(W) + 16 * S;
+}
+
+// S stages: the tiles of iteration j land in stage j % S, issued S - 1
+// iterations ahead (S = 2 for the small compressed words, whose stages are
+// small; the FP64 planes' 66 KB stage leaves room for one per block)
+template <int W, int S>
 __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_tma(Lv3 F, const __grid_constant__ TmaMaps M,
-                                                                 Planes3 P, int zbeg, int zend, int zc) {
+                                                                 const __grid_constant__ TmaVMaps VM, Planes3 P,
+                                                                 int zbeg, int zend, int zc) {
     lzb_pdl_enter();
     extern __shared__ __align__(128) unsigned char smraw[];
-    double(*sy)[8][kTmaCells] = reinterpret_cast<double(*)[8][kTmaCells]>(smraw);  // [u, û, diag][corner][cell]
-    unsigned char* stage = smraw + 3 * 8 * kTmaCells * 8;
+    double(*sy)[8][kTmaCells] = reinterpret_cast<double(*)[8][kTmaCells]>(smraw);  // [u, û][corner][cell]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smraw + tma_smem_bytes2(W, S) - 16 * S);
+    unsigned char* stage = smraw + 2 * 8 * kTmaCells * 8;
     constexpr int e0 = tma_piece(W, 0), e1 = tma_piece(W, 1), e2 = tma_piece(W, 2);
     constexpr int w0 = tma_width(e0), w1 = tma_width(e1), w2 = tma_width(e2), we = tma_width(8);
-    unsigned char* pc0 = stage;
-    unsigned char* pc1 = pc0 + tma_piece_bytes(e0);
-    unsigned char* pc2 = pc1 + tma_piece_bytes(e1);
-    double* sec = reinterpret_cast<double*>(pc2 + tma_piece_bytes(e2));
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + tma_smem_bytes(W) - 16);
+    // the regions of stage st
+    auto pc0 = [&](int st) { return stage + st * tma_stage_total(W); };
+    auto pc1 = [&](int st) { return pc0(st) + tma_piece_bytes(e0); };
+    auto pc2 = [&](int st) { return pc1(st) + tma_piece_bytes(e1); };
+    auto sec = [&](int st) { return reinterpret_cast<double*>(pc2(st) + tma_piece_bytes(e2)); };
+    auto su = [&](int st) { return reinterpret_cast<double*>(pc0(st) + tma_stage_bytes(W)); };
+    auto suh = [&](int st) { return su(st) + kTmaUSlot; };
+    auto sfl = [&](int st) { return suh(st) + kTmaUSlot; };
     const int tx = threadIdx.x % kRzX, ty = threadIdx.x / kRzX, t = threadIdx.x;
     const int N = F.N, NV = N + 1;
     const int X0 = blockIdx.x * (kRzX - 1), Y0 = blockIdx.y * (kRzY - 1);
@@ -958,71 +1010,96 @@ __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_tma(Lv3 F, const _
     const bool colok = cx >= 0 && cy >= 0 && cx < N && cy < N;
     const int ix = X0 + tx, iy = Y0 + ty;  // this thread's vertex column (tx < 31, ty < 7)
     const bool vthr = tx < kRzX - 1 && ty < kRzY - 1 && ix <= N && iy <= N;
-    const double* __restrict__ U = F.v[LZB_V_U];
-    const double* __restrict__ UH = F.v[LZB_V_UHAT];
-    const double* __restrict__ FL = F.v[LZB_V_FL];
-    auto vid = [&](int x, int y, int z) {
-        return (static_cast<int64_t>(min(max(z, 0), N)) * NV + min(max(y, 0), N)) * NV + min(max(x, 0), N);
-    };
-    auto issue = [&](int cz) {  // one elected thread: the layer's tiles into the stage
-        mbar_expect(bar, static_cast<uint32_t>(tma_stage_bytes(W)));
-        // storage x / y of cell (X0 - 1, Y0 - 1) are X0 / Y0 (the leading pad);
-        // each box starts at X0 rounded down to its 16-byte alignment
-        tma_load_4d(pc0, &M.piece[0], X0 & ~(16 / e0 - 1), Y0, cz, 0, bar);
-        if (e1) tma_load_4d(pc1, &M.piece[1], X0 & ~(16 / (e1 ? e1 : 1) - 1), Y0, cz, 0, bar);
-        if (e2) tma_load_4d(pc2, &M.piece[2], X0 & ~(16 / (e2 ? e2 : 1) - 1), Y0, cz, 0, bar);
-        if (W) tma_load_3d(sec, &M.ec, X0 & ~1, Y0, cz, bar);
-    };
+    // tile origins (tensor coordinates are never negative; boxes start 16-byte aligned in x)
+    const int ux0 = max(X0 - 1, 0) & ~1, uy0 = max(Y0 - 1, 0), fx0 = X0 & ~1;
     auto layer_ok = [&](int cz) { return cz >= 0 && cz < N; };
-    if (t == 0) mbar_init(bar, 1);
+    auto issue = [&](int cz) {  // one elected thread: iteration cz's tiles into its stage
+        const bool cells = layer_ok(cz), load = cz + 1 < ze;
+        const int st = (cz - zs + 1) % S;
+        uint64_t* bar = bars + 2 * st;
+        uint32_t bytes = 0;
+        if (cells) bytes += tma_stage_bytes(W) + 2 * kTmaUX * kTmaUY * 8;
+        if (load) bytes += kTmaFX * kTmaFY * 8;
+        if (!bytes) return;
+        mbar_expect(bar, bytes);
+        if (cells) {
+            // storage x / y of cell (X0 - 1, Y0 - 1) are X0 / Y0 (the leading pad)
+            tma_load_4d(pc0(st), &M.piece[0], X0 & ~(16 / e0 - 1), Y0, cz, 0, bar);
+            if (e1) tma_load_4d(pc1(st), &M.piece[1], X0 & ~(16 / (e1 ? e1 : 1) - 1), Y0, cz, 0, bar);
+            if (e2) tma_load_4d(pc2(st), &M.piece[2], X0 & ~(16 / (e2 ? e2 : 1) - 1), Y0, cz, 0, bar);
+            if (W) tma_load_3d(sec(st), &M.ec, X0 & ~1, Y0, cz, bar);
+            tma_load_3d(su(st), &VM.u, ux0, uy0, cz + 1, bar);  // the layer's upper vertex plane
+            tma_load_3d(suh(st), &VM.uh, ux0, uy0, cz + 1, bar);
+        }
+        if (load) tma_load_3d(sfl(st), &VM.fl, fx0, Y0, cz + 1, bar);
+    };
+    auto needs = [&](int cz) { return layer_ok(cz) || cz + 1 < ze; };
+    if (t == 0)
+        for (int st = 0; st < S; ++st) mbar_init(bars + 2 * st, 1);
     __syncthreads();
-    uint32_t phase = 0;
-    if (t == 0 && layer_ok(zs - 1)) issue(zs - 1);
-    double ul[4], uhl[4];  // corners of the current layer's lower plane
+    uint32_t phases = 0;  // bit st: the parity stage st waits for next
+    if (t == 0)
+        for (int j = 0; j < S && zs - 1 + j < ze; ++j) issue(zs - 1 + j);
+    // this thread's corner slots in the u / u-hat tiles (clamped: a corner left
+    // of / below the tile only occurs for threads whose cell does not exist)
+    int us[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int64_t v = vid(cx + (k & 1), cy + (k >> 1), zs - 1);
-        ul[k] = U[v];
-        uhl[k] = UH[v];
-    }
-    double rp = 0.0, rhp = 0.0, dgp = 0.0;  // partial sums of the vertex plane being completed
-    for (int cz = zs - 1; cz < ze; ++cz) {
-        double uu[8], uh[8];
+    for (int k = 0; k < 4; ++k)
+        us[k] = max(cy + (k >> 1) - uy0, 0) * kTmaUX + max(cx + (k & 1) - ux0, 0);
+    const int fs = ty * kTmaFX + ix - fx0;
+    double ul[4], uhl[4];  // corners of the current layer's lower plane
+    {
+        auto vid = [&](int x, int y, int z) {
+            return (static_cast<int64_t>(min(max(z, 0), N)) * NV + min(max(y, 0), N)) * NV + min(max(x, 0), N);
+        };
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            uu[k] = ul[k];
-            uh[k] = uhl[k];
-            const int64_t v = vid(cx + (k & 1), cy + (k >> 1), cz + 1);
-            uu[4 + k] = U[v];
-            uh[4 + k] = UH[v];
-            ul[k] = uu[4 + k];
-            uhl[k] = uh[4 + k];
+            const int64_t v = vid(cx + (k & 1), cy + (k >> 1), zs - 1);
+            ul[k] = F.v[LZB_V_U][v];
+            uhl[k] = F.v[LZB_V_UHAT][v];
         }
-        const double flc = (vthr && cz + 1 < ze) ? FL[vid(ix, iy, cz + 1)] : 0.0;
+    }
+    double rp = 0.0, rhp = 0.0;  // partial sums of the vertex plane being completed
+    for (int cz = zs - 1; cz < ze; ++cz) {
+        const int st = (cz - zs + 1) % S;
+        double flc = 0.0;
+        if (needs(cz)) {
+            mbar_wait(bars + 2 * st, (phases >> st) & 1u);
+            phases ^= 1u << st;
+        }
+        if (vthr && cz + 1 < ze) flc = sfl(st)[fs];
         if (layer_ok(cz)) {
-            mbar_wait(bar, phase);
-            phase ^= 1u;
+            double uu[8], uh[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uu[k] = ul[k];
+                uh[k] = uhl[k];
+                uu[4 + k] = su(st)[us[k]];
+                uh[4 + k] = suh(st)[us[k]];
+                ul[k] = uu[4 + k];
+                uhl[k] = uh[4 + k];
+            }
             if (colok) {
                 double K[27];
                 // the cell's slot in each box: row ty, column tx + the box's alignment offset
                 const int i0 = ty * w0 + tx + (X0 & (16 / e0 - 1));
                 if constexpr (W == 0) {
 #pragma unroll
-                    for (int q = 0; q < 27; ++q) K[q] = reinterpret_cast<const double*>(pc0)[q * kRzY * w0 + i0];
+                    for (int q = 0; q < 27; ++q) K[q] = reinterpret_cast<const double*>(pc0(st))[q * kRzY * w0 + i0];
                 } else {
                     const int i1 = ty * w1 + tx + (e1 ? (X0 & (16 / (e1 ? e1 : 1) - 1)) : 0);
                     const int i2 = ty * w2 + tx + (e2 ? (X0 & (16 / (e2 ? e2 : 1) - 1)) : 0);
-                    const Base3 B(sec[ty * we + tx + (X0 & 1)], P.s1, P.h);
+                    const Base3 B(sec(st)[ty * we + tx + (X0 & 1)], P.s1, P.h);
 #pragma unroll
                     for (int q = 0; q < 27; ++q) {
                         unsigned long long w;
-                        if constexpr (e0 == 8) w = reinterpret_cast<const unsigned long long*>(pc0)[q * kRzY * w0 + i0];
-                        else if constexpr (e0 == 4) w = reinterpret_cast<const uint32_t*>(pc0)[q * kRzY * w0 + i0];
-                        else if constexpr (e0 == 2) w = reinterpret_cast<const uint16_t*>(pc0)[q * kRzY * w0 + i0];
-                        else w = pc0[q * kRzY * w0 + i0];
-                        if constexpr (e1 == 2) w |= static_cast<unsigned long long>(reinterpret_cast<const uint16_t*>(pc1)[q * kRzY * w1 + i1]) << (8 * e0);
-                        else if constexpr (e1 == 1) w |= static_cast<unsigned long long>(pc1[q * kRzY * w1 + i1]) << (8 * e0);
-                        if constexpr (e2 == 1) w |= static_cast<unsigned long long>(pc2[q * kRzY * w2 + i2]) << (8 * (e0 + e1));
+                        if constexpr (e0 == 8) w = reinterpret_cast<const unsigned long long*>(pc0(st))[q * kRzY * w0 + i0];
+                        else if constexpr (e0 == 4) w = reinterpret_cast<const uint32_t*>(pc0(st))[q * kRzY * w0 + i0];
+                        else if constexpr (e0 == 2) w = reinterpret_cast<const uint16_t*>(pc0(st))[q * kRzY * w0 + i0];
+                        else w = pc0(st)[q * kRzY * w0 + i0];
+                        if constexpr (e1 == 2) w |= static_cast<unsigned long long>(reinterpret_cast<const uint16_t*>(pc1(st))[q * kRzY * w1 + i1]) << (8 * e0);
+                        else if constexpr (e1 == 1) w |= static_cast<unsigned long long>(pc1(st)[q * kRzY * w1 + i1]) << (8 * e0);
+                        if constexpr (e2 == 1) w |= static_cast<unsigned long long>(pc2(st)[q * kRzY * w2 + i2]) << (8 * (e0 + e1));
                         K[q] = B(q / 9, (q / 3) % 3, q % 3) + SrcComp<W>::dec(static_cast<typename SrcComp<W>::Word>(w));
                     }
                 }
@@ -1036,14 +1113,13 @@ __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_tma(Lv3 F, const _
                     }
                     sy[0][a][t] = au;
                     sy[1][a][t] = auh;
-                    sy[2][a][t] = K[cls3(a, a)];
                 }
             }
         }
-        __syncthreads();  // the stage is consumed: the next layer's copy may land in it
-        if (t == 0 && cz + 1 < ze && layer_ok(cz + 1)) issue(cz + 1);
+        __syncthreads();  // the stage is consumed: iteration cz + S's tiles may land in it
+        if (t == 0 && cz + S < ze) issue(cz + S);
         if (vthr) {
-            auto sub = [&](int q, double& r, double& rh, double& dg) {
+            auto sub = [&](int q, double& r, double& rh) {
                 const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;
                 const int row = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
                 const int ccx = ix - 1 + dx, ccy = iy - 1 + dy;
@@ -1051,11 +1127,10 @@ __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_tma(Lv3 F, const _
                 const int c = (ty + dy) * kRzX + tx + dx;
                 r -= sy[0][row][c];
                 rh -= sy[1][row][c];
-                dg += sy[2][row][c];
             };
             if (cz >= zs && cz < N) {
 #pragma unroll
-                for (int q = 4; q < 8; ++q) sub(q, rp, rhp, dgp);
+                for (int q = 4; q < 8; ++q) sub(q, rp, rhp);
             }
             if (cz >= zs) {
                 double r = rp, rh = rhp;
@@ -1066,14 +1141,12 @@ __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_tma(Lv3 F, const _
                 const int64_t vi = (static_cast<int64_t>(cz) * NV + iy) * NV + ix;
                 __stcs(F.v[LZB_V_R] + vi, r);
                 __stcs(F.v[LZB_V_RHAT] + vi, rh);
-                __stcs(F.v[LZB_V_DIAG] + vi, dgp);
             }
             if (cz + 1 < ze) {
                 rp = rhp = flc;
-                dgp = 0.0;
                 if (cz >= 0) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) sub(q, rp, rhp, dgp);
+                    for (int q = 0; q < 4; ++q) sub(q, rp, rhp);
                 }
             }
         }
@@ -1628,6 +1701,7 @@ public:
         if (n < 1 || n > kMaxN3) throw Error(LZB_ERR_INVALID, "3D sub-samples per axis must be in 1..16");
         if (cz0 < 0 || cz1 > N_ || cz0 > cz1) throw Error(LZB_ERR_INVALID, "bad z plane range");
         ops_dirty_ = true;
+        leaf_diag_dirty_ = true;
         const AxisTab3 T = axis_tab3(n);
         const int64_t cb = static_cast<int64_t>(cz0) * N_ * N_, ce = static_cast<int64_t>(cz1) * N_ * N_;
         if (ce > cb)
@@ -1746,6 +1820,8 @@ public:
             if (l < D_) L.op.alloc(static_cast<size_t>(L.N) * L.N * L.N * kCls3);
         }
         partial3_.alloc(kNormBlocks3);
+        leaf_diag_dirty_ = true;  // fresh vertex arrays
+        vkey_[0] = vkey_[1] = vkey_[2] = nullptr;
         upload_galerkin_weights();
         res3_.alloc(1);
         for (int l = 0; l <= D_; ++l)
@@ -2163,6 +2239,11 @@ private:
         const dim3 grid(bx, by, (z1 - z0 + zc - 1) / zc);
         const Lv3 v = lv(l);
         if (l == D_ && use_tma_) {  // the leaves: TMA-staged tiles (k3_residual_tma)
+            if (leaf_diag_dirty_) {  // the Jacobi diagonal, once per change of the leaf operators
+                if (W_ == 0) LZB_LAUNCH(k3_leaf_diag<Src64>, vg(D_), 128, 0, s_, lv(D_), Src64{op_.p, ncs_, N_, xp_});
+                else leaf_cls([&](auto S) { LZB_LAUNCH(k3_leaf_diag<decltype(S)>, vg(D_), 128, 0, s_, lv(D_), S); });
+                leaf_diag_dirty_ = false;
+            }
             const dim3 g2(bx, by, (z1 - z0 + zc2(bx, by, z0, z1) - 1) / zc2(bx, by, z0, z1));
             const int zcl = zc2(bx, by, z0, z1);
             switch (W_) {
@@ -2194,12 +2275,10 @@ private:
     // TMA tensor maps of the leaf planes (built once: the storage never moves)
     bool use_tma_ = std::getenv("LZB_NO_TMA") == nullptr;
     bool maps_ready_ = false;
-    TmaMaps maps_{};
-    void build_maps() {
-        if (maps_ready_) return;
-        using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Encode encode_fn() {  // the driver's cuTensorMapEncodeTiled (no link-time libcuda dependency)
         static Encode encode = nullptr;
         if (!encode) {
             void* fn = nullptr;
@@ -2208,6 +2287,12 @@ private:
             if (!fn || q != cudaDriverEntryPointSuccess) throw Error(LZB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
             encode = reinterpret_cast<Encode>(fn);
         }
+        return encode;
+    }
+    TmaMaps maps_{};
+    void build_maps() {
+        if (maps_ready_) return;
+        auto encode = encode_fn();
         auto dtype = [](int e) {
             return e == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : e == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
                    : e == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
@@ -2240,14 +2325,39 @@ private:
     }
     template <int W>
     void launch_tma(dim3 g, const Lv3& v, int z0, int z1, int zc) {
+        constexpr int S = (W >= 2 && W <= 4) ? 2 : 1;  // stages (k3_residual_tma)
         build_maps();
         static bool attr = false;
         if (!attr) {
-            LZB_CUDA(cudaFuncSetAttribute(k3_residual_tma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          tma_smem_bytes(W)));
+            LZB_CUDA(cudaFuncSetAttribute(k3_residual_tma<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          tma_smem_bytes2(W, S)));
             attr = true;
         }
-        LZB_LAUNCH(k3_residual_tma<W>, g, kRzX * kRzY, tma_smem_bytes(W), s_, v, maps_, planes(), z0, z1, zc);
+        vmaps(v);
+        LZB_LAUNCH((k3_residual_tma<W, S>), g, kRzX * kRzY, tma_smem_bytes2(W, S), s_, v, maps_, vmaps_, planes(), z0,
+                   z1, zc);
+    }
+    bool leaf_diag_dirty_ = true;
+    // TMA maps of the leaf vertex fields the residual reads (u, u-hat -- u
+    // itself during V-cycles -- and the load), rebuilt when the pointers change
+    TmaVMaps vmaps_{};
+    const void* vkey_[3] = {nullptr, nullptr, nullptr};
+    void vmaps(const Lv3& v) {
+        const void* key[3] = {v.v[LZB_V_U], v.v[LZB_V_UHAT], v.v[LZB_V_FL]};
+        if (key[0] == vkey_[0] && key[1] == vkey_[1] && key[2] == vkey_[2]) return;
+        const cuuint64_t NV = static_cast<cuuint64_t>(N_) + 1;
+        const cuuint64_t dims[3] = {NV, NV, NV}, strides[2] = {NV * 8, NV * NV * 8};
+        auto make = [&](CUtensorMap* m, const void* base, cuuint32_t bx, cuuint32_t by) {
+            const cuuint32_t box[3] = {bx, by, 1}, es[3] = {1, 1, 1};
+            const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(base), dims, strides,
+                                           box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) throw Error(LZB_ERR_CUDA, "cuTensorMapEncodeTiled failed (vertex tiles)");
+        };
+        make(&vmaps_.u, key[0], kTmaUX, kTmaUY);
+        make(&vmaps_.uh, key[1], kTmaUX, kTmaUY);
+        make(&vmaps_.fl, key[2], kTmaFX, kTmaFY);
+        for (int i = 0; i < 3; ++i) vkey_[i] = key[i];
     }
     bool uhat_is_u_ = false;
     double damping3(int l) const { return variant_ == LZB_ADDITIVE ? std::pow(omega_, D_ - l + 1) : omega_; }
