@@ -15,7 +15,7 @@ for depth in [int(a) for a in (sys.argv[1:] or ["5", "6"])]:
     g.step()
     N = 3 ** depth
     nv, nc, nvc = (N + 1) ** 3, N ** 3, (N // 3 + 1) ** 3
-    rows = {"uhat": (lzb.TK_UHAT, 16 * nv), "residual": (lzb.TK_RESIDUAL, 48 * nv + 216 * nc),
+    rows = {"uhat": (lzb.TK_UHAT, 16 * nv), "residual": (lzb.TK_RESIDUAL, 40 * nv + 216 * nc),
             "restrict": (lzb.TK_RESTRICT, 8 * nv + 8 * nvc), "back(pre+update)": (lzb.TK_BACK, 32 * nv + 48 * nvc)}
     out = {}
     for name, (tk, b) in rows.items():
