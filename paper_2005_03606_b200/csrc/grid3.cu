@@ -505,14 +505,20 @@ __device__ __forceinline__ bool codec_plain(unsigned long long u) {
     const int E = static_cast<int>((u >> 52) & 0x7ff);
     return (u << 1) == 0 || (E >= 1023 - 127 && E <= 1023 + 127);
 }
-// the smallest width in [P, 7] a plain value passes, else 8
+// the smallest width in [P, 7] a plain value passes, else 8. Branch-free: the
+// dropped bits at widths 2..7 are nested masks of F (45, 37, .., 5 bits), so
+// the passing widths are upward closed and the smallest one is 2 + the number
+// of failing widths; F & mask <= T (real) iff F & mask <= floor(T) (integer,
+// the conversion saturates for a huge T)
 __device__ __forceinline__ int min_width_plain(unsigned long long u, double delta, int P) {
     if ((u << 1) == 0) return P;  // +-0: error 0 at every width
     const int E = static_cast<int>((u >> 52) & 0x7ff);
     const double T = delta * __longlong_as_double(static_cast<long long>(2098 - E) << 52);  // delta 2^(1075 - E)
-    const unsigned long long F = u & 0xFFFFFFFFFFFFFull;
-    while (P < 8 && static_cast<double>(F & ((1ull << (52 - mantissa_bits(P))) - 1)) > T) ++P;
-    return P;
+    const unsigned long long Ti = __double2ull_rz(T), F = u & 0xFFFFFFFFFFFFFull;
+    int w = 2;
+#pragma unroll
+    for (int q = 2; q <= 7; ++q) w += (F & ((1ull << (52 - mantissa_bits(q))) - 1)) > Ti ? 1 : 0;
+    return w > P ? w : P;
 }
 // roundtrip at width p3 in 2..7 of a plain value: the low fraction bits cleared
 __device__ __forceinline__ double rt_plain(unsigned long long u, int p3) {
@@ -552,12 +558,17 @@ __device__ __forceinline__ bool roundtrip_rec(double x, int p3, bool plain, doub
 // decoded operator (FP64 class planes, or eps(centre) + the compressed
 // planes of width W), width and n. One thread per cell; the record's 27
 // distinct surplus values are coded once (they stand for its 64 entries).
-__global__ void __launch_bounds__(128, 4) k_assemble3(Field3 F, int N, double h, AxisTab3 T, double delta_max,
+// KIND >= 0: the field kind fixed at compile time (the other kinds' sample
+// code is dropped: a smaller kernel, fewer instruction-cache misses)
+template <int KIND>
+__global__ void __launch_bounds__(128, 4) k_assemble3(Field3 Fin, int N, double h, AxisTab3 T, double delta_max,
                                                       int fixed_p3, double* __restrict__ op, Planes3 PL, int W,
                                                       int8_t* __restrict__ p3o, int32_t* __restrict__ no,
                                                       unsigned long long* stats, int* err, int* wide,
                                                       int64_t cbeg, int64_t cend) {
     lzb_pdl_enter();
+    Field3 F = Fin;
+    if (KIND >= 0) F.kind = KIND;
     const int64_t c = cbeg + gtid();  // cells [cbeg, cend): whole z planes
     if (c >= cend) return;
     const int cx = static_cast<int>(c % N), cy = static_cast<int>((c / N) % N), cz = static_cast<int>(c / N / N);
@@ -1705,8 +1716,14 @@ public:
         const AxisTab3 T = axis_tab3(n);
         const int64_t cb = static_cast<int64_t>(cz0) * N_ * N_, ce = static_cast<int64_t>(cz1) * N_ * N_;
         if (ce > cb)
-            LZB_LAUNCH(k_assemble3, blocks_for(ce - cb, 128), 128, 0, s_, F_, N_, h_, T, delta_, fixed_, op_.p,
-                       planes(), W_, p3_.p, n_.p, stats_.p, ctx_->err.p, wide_.p, cb, ce);
+        {
+            if (F_.kind == LZB_F3_GRF)
+                LZB_LAUNCH(k_assemble3<LZB_F3_GRF>, blocks_for(ce - cb, 128), 128, 0, s_, F_, N_, h_, T, delta_, fixed_,
+                           op_.p, planes(), W_, p3_.p, n_.p, stats_.p, ctx_->err.p, wide_.p, cb, ce);
+            else
+                LZB_LAUNCH(k_assemble3<-1>, blocks_for(ce - cb, 128), 128, 0, s_, F_, N_, h_, T, delta_, fixed_, op_.p,
+                           planes(), W_, p3_.p, n_.p, stats_.p, ctx_->err.p, wide_.p, cb, ce);
+        }
         n_last_ = n;
     }
 
