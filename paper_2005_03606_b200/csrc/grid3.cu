@@ -34,6 +34,12 @@ struct Field3 {
     int kind, n;
     double value;
     const double* grf;  // device, n^3
+    // the same table x-fastest and padded periodically to (n + 1)^3 (entry n =
+    // entry 0 per axis), after the n^3 table: value (i, j, k) at
+    // (k (n + 1) + j) (n + 1) + i. The 8 corners of a sample are then at fixed
+    // offsets from one base index (no wrap), and the cells of a warp (consecutive
+    // x) read neighbouring words.
+    const double* grf_t;
     lzb_field xy;
     double cx, cy, cz, radius, width, eps_in, eps_out;  // SPHERE
 };
@@ -112,7 +118,9 @@ struct GrfCell {
         bz = static_cast<int>(floor(z0 * n));
     }
     __device__ __forceinline__ int wrap(int i) const { return i >= n ? i - n : i; }
-    __device__ __forceinline__ static double lerp(double a, double b, double t) { return (1.0 - t) * a + t * b; }
+    // (1 - t) a + t b with the second product fused (the GRF paths are a
+    // restatement: one formula for every GRF sample, grf_sample below included)
+    __device__ __forceinline__ static double lerp(double a, double b, double t) { return fma(t, b, (1.0 - t) * a); }
     __device__ __forceinline__ void set_x(double x) {
         const double u = x * n, f = floor(u);
         const int o = static_cast<int>(f) - bx;  // 0 or 1
@@ -204,6 +212,96 @@ __device__ inline void accumulate3_grf(const Field3& F, double x0, double y0, do
     }
 }
 
+// ---- GRF samples of small cells, one sample at a time (h n_g < 1)
+// Per axis the sample's table interval o (0 .. n - 1) and parameter t.
+struct GAx {
+    double t;
+    int o;
+};
+template <bool WRAP>
+__device__ __forceinline__ GAx grf_axis(double x, int n) {
+    const double u = x * n, f = floor(u);
+    GAx a;
+    a.t = u - f;
+    a.o = static_cast<int>(f);
+    if (WRAP) {  // arbitrary boxes (lzb_integrate_elements3); grid cells lie in [0, 1)
+        a.o %= n;
+        a.o += a.o < 0 ? n : 0;
+    }
+    return a;
+}
+// exp of the trilinear interpolant at one sample: 8 loads at fixed offsets of
+// the padded x-fastest table, lerps in x, y, z order (GrfCell's order and
+// formula: the same bits).
+__device__ __forceinline__ double grf_sample(const double* __restrict__ Tp, int np, const GAx& ax, const GAx& ay,
+                                             const GAx& az) {
+    const double* p = Tp + (az.o * np + ay.o) * np + ax.o;
+    const int np2 = np * np;
+    const double a000 = __ldg(p), a100 = __ldg(p + 1), a010 = __ldg(p + np), a110 = __ldg(p + np + 1);
+    const double a001 = __ldg(p + np2), a101 = __ldg(p + np2 + 1), a011 = __ldg(p + np2 + np),
+                 a111 = __ldg(p + np2 + np + 1);
+    const double c00 = GrfCell::lerp(a000, a100, ax.t), c10 = GrfCell::lerp(a010, a110, ax.t);
+    const double c01 = GrfCell::lerp(a001, a101, ax.t), c11 = GrfCell::lerp(a011, a111, ax.t);
+    const double d0 = GrfCell::lerp(c00, c10, ay.t), d1 = GrfCell::lerp(c01, c11, ay.t);
+    return exp(GrfCell::lerp(d0, d1, az.t));
+}
+
+// The 27 class sums at a compile-time NS samples per axis (NS <= 2: at two
+// samples per row the geometric-sequence trick of accumulate3_grf saves no
+// exp), every loop unrolled, the sums in accumulate3's order with fused
+// multiply-adds. WRAP as grf_axis.
+template <int NS, bool WRAP>
+__device__ __forceinline__ void accumulate3_grf_direct(const Field3& F, double x0, double y0, double z0, double h,
+                                                       const AxisTab3& T, Acc3& A) {
+    const double inv = 1.0 / NS;
+    const int np = F.n + 1;
+    GAx ax[NS], ay[NS], az[NS];
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+        ax[i] = grf_axis<WRAP>(x0 + (i + 0.5) * inv * h, F.n);
+        ay[i] = grf_axis<WRAP>(y0 + (i + 0.5) * inv * h, F.n);
+        az[i] = grf_axis<WRAP>(z0 + (i + 0.5) * inv * h, F.n);
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) A.yz[q] = A.xz[q] = A.xy[q] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+        double B[3] = {0.0, 0.0, 0.0}, Cc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            double G = 0.0, Dz[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+            for (int k = 0; k < NS; ++k) {
+                const double e = grf_sample(F.grf_t, np, ax[i], ay[j], az[k]);
+                G += e;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) Dz[c] = fma(e, T.s[k][c], Dz[c]);
+            }
+#pragma unroll
+            for (int cy = 0; cy < 3; ++cy) {
+#pragma unroll
+                for (int cz = 0; cz < 3; ++cz) A.yz[cy * 3 + cz] = fma(T.s[j][cy], Dz[cz], A.yz[cy * 3 + cz]);
+                Cc[cy] = fma(T.s[j][cy], G, Cc[cy]);
+                B[cy] += Dz[cy];
+            }
+        }
+#pragma unroll
+        for (int cx = 0; cx < 3; ++cx)
+#pragma unroll
+            for (int c2 = 0; c2 < 3; ++c2) {
+                A.xz[cx * 3 + c2] = fma(T.s[i][cx], B[c2], A.xz[cx * 3 + c2]);
+                A.xy[cx * 3 + c2] = fma(T.s[i][cx], Cc[c2], A.xy[cx * 3 + c2]);
+            }
+    }
+}
+// eps at the centre of a small GRF cell (the n = 1 sample)
+template <bool WRAP>
+__device__ __forceinline__ double grf_centre(const Field3& F, double x0, double y0, double z0, double h) {
+    const double inv = 1.0 / 1;
+    return grf_sample(F.grf_t, F.n + 1, grf_axis<WRAP>(x0 + (0 + 0.5) * inv * h, F.n),
+                      grf_axis<WRAP>(y0 + (0 + 0.5) * inv * h, F.n), grf_axis<WRAP>(z0 + (0 + 0.5) * inv * h, F.n));
+}
+
 // The 27 class sums of one cell at n samples per axis.
 __device__ inline void accumulate3(const Field3& F, double x0, double y0, double z0, double h, const AxisTab3& T,
                                    Acc3& A) {
@@ -261,7 +359,11 @@ __global__ void k_elements3(Field3 F, int64_t count, const double* x0, const dou
     if (t >= count) return;
     if (nn[t] != T.n) return;  // batches are grouped by n on the host
     Acc3 A;
-    accumulate3(F, x0[t], y0[t], z0[t], h[t], T, A);
+    // the assembly kernels' path for each case (k_assemble3): the same bits
+    const bool small = F.kind == LZB_F3_GRF && h[t] * F.n < 1.0;
+    if (small && T.n == 1) accumulate3_grf_direct<1, true>(F, x0[t], y0[t], z0[t], h[t], T, A);
+    else if (small && T.n == 2) accumulate3_grf_direct<2, true>(F, x0[t], y0[t], z0[t], h[t], T, A);
+    else accumulate3(F, x0[t], y0[t], z0[t], h[t], T, A);
     const double hn = h[t] * (1.0 / T.n);
     for (int a = 0; a < 8; ++a)
         for (int b = 0; b < 8; ++b) out[64 * t + 8 * a + b] = entry3(A, hn, a, b);
@@ -553,15 +655,142 @@ __device__ __forceinline__ bool roundtrip_rec(double x, int p3, bool plain, doub
     return roundtrip_fast(x, p3, rt);
 }
 
+// ---- record coding of the 27 class surpluses, shared by the assembly kernels
+// Base3's values when the n = 1 seg_int classes are symmetric (s[0] == s[2]
+// bit for bit, which holds for the unit interval): class (cx, cy, cz) depends
+// on (cx == 1, cy == 1, cz == 1) only, 8 values instead of 27 evaluations.
+struct BaseVals {
+    double b[8];
+    bool sym;
+    __device__ __forceinline__ BaseVals(const Base3& B, const double* s) : sym(s[0] == s[2]) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) b[k] = B(k >> 2, (k >> 1) & 1, k & 1);
+    }
+    __device__ __forceinline__ double at(const Base3& B, int cx, int cy, int cz) const {
+        return sym ? b[(cx == 1) * 4 + (cy == 1) * 2 + (cz == 1)] : B(cx, cy, cz);
+    }
+};
+
+// choose_precision (codec.cpp:64-85 semantics) of a record whose values are
+// all plain, from the exponents first. A plain value v with biased exponent E
+// surely passes width q once the dropped bits are fewer than those of
+// T = delta 2^(1075 - E) (mask_q <= floor(T)), i.e. 61 - 8 q <= e_T with
+// e_T = E_delta - E + 52: q_sure(E) rises with E, so every value passes at
+// P = q_sure(E_max). From there the width walks down while every value still
+// passes the reference's own test |rt - v| <= delta at P - 1 (rt: the low
+// fraction bits cleared, the subtraction exact): the passing widths of each
+// value are upward closed, so the first width at which some
+// value fails is one below the answer. Typically one pass of 27 tests.
+// Records with a value that is not plain (zero, tiny, huge, non-finite) or a
+// non-normal delta take the general routine.
+template <int COUNT>
+__device__ __forceinline__ int choose_precision_exp(const double* v, double delta, bool& plain) {
+    unsigned hmax = 0, hmin = 0x7fffffffu;
+#pragma unroll
+    for (int i = 0; i < COUNT; ++i) {
+        const unsigned hi = static_cast<unsigned>(__double2hiint(v[i])) & 0x7fffffffu;
+        hmax = max(hmax, hi);
+        hmin = min(hmin, hi);
+    }
+    const int Emax = static_cast<int>(hmax >> 20), Emin = static_cast<int>(hmin >> 20);
+    const int Ed = (__double2hiint(delta) >> 20) & 0x7ff;
+    plain = Emin >= 1023 - 127 && Emax <= 1023 + 127;
+    if (Emax == 0x7ff || Ed == 0 || Ed == 0x7ff || __double2hiint(delta) < 0) {
+        plain = false;
+        return choose_precision_set<COUNT>(v, delta);
+    }
+    if (Emax < Ed) return 0;  // every |v| < 2^(E_delta - 1023) <= delta
+    if (Emax == Ed) {
+        bool all_small = true;
+#pragma unroll
+        for (int i = 0; i < COUNT; ++i) all_small = all_small && !(fabs(v[i]) > delta);
+        if (all_small) return 0;
+    }
+    if (!plain) return choose_precision_set<COUNT>(v, delta);
+    const int eT = Ed - Emax + 52;
+    int P = min(max((68 - eT) >> 3, 2), 8);
+    while (P > 2) {
+        const unsigned long long keep = ~((1ull << (69 - 8 * P)) - 1);  // width P - 1 drops 61 - 8 (P - 1) bits
+        bool fail = false;
+#pragma unroll
+        for (int i = 0; i < COUNT; ++i) {
+            const double rt = __longlong_as_double(__double_as_longlong(v[i]) & static_cast<long long>(keep));
+            fail = fail || fabs(v[i] - rt) > delta;
+        }
+        if (fail) break;
+        --P;
+    }
+    return P;
+}
+
+// codec::roundtrip of any value (the rare records with a value that is not plain)
+__device__ __noinline__ bool roundtrip_slow(double x, int p3, double& rt) { return roundtrip_fast(x, p3, rt); }
+
+// Codes one record and stores the decoded operator: p3 (chosen or forced),
+// per class the roundtrip value, the running delta, then FP64 planes
+// (W == 0: B + rt) or the W-byte plane words. Returns p3, or -1 on an error
+// (non-finite value: err set; record wider than the planes: wide set).
+template <class StoreOp>
+__device__ __forceinline__ int code_record27(const double* sur, const Base3& B, const BaseVals& BV, double delta_max,
+                                             int fixed_p3, int W, int* err, int* wide, double& delta,
+                                             StoreOp&& store) {
+    bool plain = false;
+    int p3 = choose_precision_exp<27>(sur, delta_max, plain);
+    if (fixed_p3) p3 = fixed_p3;
+    if (p3 < 0) {
+        atomicExch(err, 1);
+        return -1;
+    }
+    if (W != 0 && p3 > W) {
+        atomicExch(wide, 1);  // record wider than the planes
+        return -1;
+    }
+    delta = 0.0;
+    if (plain || p3 == 0 || p3 == 8) {
+        // plain values at widths 2..7: the low fraction bits cleared; 0: every rt is +0; 8: the value
+        const unsigned long long keep =
+            p3 == 0 ? 0ull : (p3 == 8 ? ~0ull : ~((1ull << (52 - mantissa_bits(p3))) - 1));
+        if (p3 == 8) {
+            bool finite = true;
+#pragma unroll
+            for (int q = 0; q < 27; ++q) finite = finite && dev_isfinite(sur[q]);
+            if (!finite) {
+                atomicExch(err, 1);
+                return -1;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 27; ++q) {
+            const double rt = __longlong_as_double(__double_as_longlong(sur[q]) & static_cast<long long>(keep));
+            delta = fmax(delta, fabs(rt - sur[q]));
+            store(q, BV.at(B, q / 9, (q / 3) % 3, q % 3), rt);
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 27; ++q) {
+            double rt;
+            if (!roundtrip_slow(sur[q], p3, rt)) {
+                atomicExch(err, 1);
+                return -1;
+            }
+            delta = fmax(delta, fabs(rt - sur[q]));
+            store(q, BV.at(B, q / 9, (q / 3) % 3, q % 3), rt);
+        }
+    }
+    return p3;
+}
+
 // Fixed-p assembly of every cell of a 3D level: integrate at n, code the
 // record against the n = 1 element (stream.cpp:82-111 in 3D), store the
 // decoded operator (FP64 class planes, or eps(centre) + the compressed
 // planes of width W), width and n. One thread per cell; the record's 27
 // distinct surplus values are coded once (they stand for its 64 entries).
 // KIND >= 0: the field kind fixed at compile time (the other kinds' sample
-// code is dropped: a smaller kernel, fewer instruction-cache misses)
-template <int KIND>
-__global__ void __launch_bounds__(128, 4) k_assemble3(Field3 Fin, int N, double h, AxisTab3 T, double delta_max,
+// code is dropped: a smaller kernel, fewer instruction-cache misses).
+// NS > 0 (GRF cells smaller than a table spacing): the samples per axis at
+// compile time, accumulate3_grf_direct; NS = 0: T.n samples, accumulate3.
+template <int KIND, int NS>
+__global__ void __launch_bounds__(128, 3) k_assemble3(Field3 Fin, int N, double h, AxisTab3 T, double delta_max,
                                                       int fixed_p3, double* __restrict__ op, Planes3 PL, int W,
                                                       int8_t* __restrict__ p3o, int32_t* __restrict__ no,
                                                       unsigned long long* stats, int* err, int* wide,
@@ -574,41 +803,26 @@ __global__ void __launch_bounds__(128, 4) k_assemble3(Field3 Fin, int N, double 
     const int cx = static_cast<int>(c % N), cy = static_cast<int>((c / N) % N), cz = static_cast<int>(c / N / N);
     const int64_t nc = PL.nc, sc = plane_sidx(c, PL.N, PL.xp);  // storage of the planes
     const double x0 = cx * h, y0 = cy * h, z0 = cz * h;
-    const double e = centre_eps3(F, x0, y0, z0, h);
-    const Base3 B(e, PL.s1, h);  // A(n=1): eps(centre) * unit stiffness, recomputed per class (9 products)
+    const double e = NS > 0 ? grf_centre<false>(F, x0, y0, z0, h) : centre_eps3(F, x0, y0, z0, h);
+    const Base3 B(e, PL.s1, h);  // A(n=1): eps(centre) * unit stiffness
+    const BaseVals BV(B, PL.s1);
     double sur[27];
     {
         Acc3 A;
-        accumulate3(F, x0, y0, z0, h, T, A);
+        if (NS > 0) accumulate3_grf_direct<(NS > 0 ? NS : 1), false>(F, x0, y0, z0, h, T, A);
+        else accumulate3(F, x0, y0, z0, h, T, A);
         const double hn = h * (1.0 / T.n);
 #pragma unroll
         for (int q = 0; q < 27; ++q)
-            sur[q] = class_value(A, hn, q / 9, (q / 3) % 3, q % 3) - B(q / 9, (q / 3) % 3, q % 3);
+            sur[q] = class_value(A, hn, q / 9, (q / 3) % 3, q % 3) - BV.at(B, q / 9, (q / 3) % 3, q % 3);
     }
-    bool plain = false;
-    const int p3 = fixed_p3 ? fixed_p3 : choose_precision_regular<27>(sur, delta_max, plain);
-    if (p3 < 0) {
-        atomicExch(err, 1);
-        return;
-    }
-    if (W != 0 && p3 > W) {
-        atomicExch(wide, 1);  // record wider than the planes
-        return;
-    }
-    if (W != 0) PL.ec[sc] = e;
-    double delta = 0.0;
-#pragma unroll
-    for (int q = 0; q < 27; ++q) {
-        double rt;
-        if (!roundtrip_rec(sur[q], p3, plain, rt)) {
-            atomicExch(err, 1);
-            return;
-        }
-        const double d = fabs(rt - sur[q]);
-        delta = delta < d ? d : delta;
-        if (W == 0) op[q * nc + sc] = B(q / 9, (q / 3) % 3, q % 3) + rt;
+    double delta;
+    const int p3 = code_record27(sur, B, BV, delta_max, fixed_p3, W, err, wide, delta, [&](int q, double b, double rt) {
+        if (W == 0) op[q * nc + sc] = b + rt;
         else plane_store3(PL, W, sc, q, plane_word(rt, W));
-    }
+    });
+    if (p3 < 0) return;
+    if (W != 0) PL.ec[sc] = e;
     p3o[c] = static_cast<int8_t>(p3);
     no[c] = T.n;
     atomic_max_double_bits(&stats[S_MAXDELTA], delta);
@@ -1656,10 +1870,17 @@ Field3 to_device(const lzb_field3& f, DevBuf<double>& table) {
     if (f.kind == LZB_F3_SPHERE && !(f.width > 0.0)) throw Error(LZB_ERR_INVALID, "sphere interface width must be > 0");
     if (f.kind == LZB_F3_GRF) {
         if (!f.grf || f.grf_n < 2) throw Error(LZB_ERR_INVALID, "GRF field needs a table");
-        const size_t n3 = static_cast<size_t>(f.grf_n) * f.grf_n * f.grf_n;
-        table.alloc(n3);
-        LZB_CUDA(cudaMemcpy(table.p, f.grf, n3 * sizeof(double), cudaMemcpyHostToDevice));
+        const size_t n = f.grf_n, n3 = n * n * n, np = n + 1, np3 = np * np * np;
+        std::vector<double> host(n3 + np3);
+        std::copy(f.grf, f.grf + n3, host.begin());
+        for (size_t k = 0; k < np; ++k)
+            for (size_t j = 0; j < np; ++j)
+                for (size_t i = 0; i < np; ++i)
+                    host[n3 + (k * np + j) * np + i] = f.grf[((i % n) * n + j % n) * n + k % n];
+        table.alloc(host.size());
+        LZB_CUDA(cudaMemcpy(table.p, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice));
         F.grf = table.p;
+        F.grf_t = table.p + n3;
     } else if (f.kind != LZB_F3_CONSTANT && f.kind != LZB_F3_EXTRUDED && f.kind != LZB_F3_SPHERE) {
         throw Error(LZB_ERR_INVALID, "unknown 3D field kind");
     }
@@ -1717,12 +1938,15 @@ public:
         const int64_t cb = static_cast<int64_t>(cz0) * N_ * N_, ce = static_cast<int64_t>(cz1) * N_ * N_;
         if (ce > cb)
         {
-            if (F_.kind == LZB_F3_GRF)
-                LZB_LAUNCH(k_assemble3<LZB_F3_GRF>, blocks_for(ce - cb, 128), 128, 0, s_, F_, N_, h_, T, delta_, fixed_,
-                           op_.p, planes(), W_, p3_.p, n_.p, stats_.p, ctx_->err.p, wide_.p, cb, ce);
-            else
-                LZB_LAUNCH(k_assemble3<-1>, blocks_for(ce - cb, 128), 128, 0, s_, F_, N_, h_, T, delta_, fixed_, op_.p,
-                           planes(), W_, p3_.p, n_.p, stats_.p, ctx_->err.p, wide_.p, cb, ce);
+            const bool small = F_.kind == LZB_F3_GRF && h_ * F_.n < 1.0;  // cells under one table spacing
+            auto go = [&](auto kern) {
+                LZB_LAUNCH(kern, blocks_for(ce - cb, 128), 128, 0, s_, F_, N_, h_, T, delta_, fixed_, op_.p, planes(),
+                           W_, p3_.p, n_.p, stats_.p, ctx_->err.p, wide_.p, cb, ce);
+            };
+            if (small && n == 1) go(k_assemble3<LZB_F3_GRF, 1>);
+            else if (small && n == 2) go(k_assemble3<LZB_F3_GRF, 2>);
+            else if (F_.kind == LZB_F3_GRF) go(k_assemble3<LZB_F3_GRF, 0>);
+            else go(k_assemble3<-1, 0>);
         }
         n_last_ = n;
     }
