@@ -2238,6 +2238,45 @@ __global__ void k_reset_stats(Result* r) {
     if (threadIdx.x < 13 || threadIdx.x == S_PENDING) r->s[threadIdx.x] = 0;
 }
 
+// ---- device-side cycle loop (Grid::run_device_loop): the termination test of
+// solver.cpp:8-16 on the device, steering a conditional WHILE graph node whose
+// body is one whole cycle, so a quiescent solve (no assembly work pending)
+// runs cycle after cycle without a host round trip per residual norm.
+struct LoopState {
+    double front;        // history.front(): the first residual of the solve
+    double target, divergence;
+    int32_t max_cycles;
+    uint32_t count, cap;  // cycles recorded by this launch / room in the history
+    int32_t status, err;
+};
+__global__ void k_loop_begin(uint32_t* cycle) {  // ++cycle (the epoch the coarse pass stamps)
+    lzb_pdl_enter();
+    if (threadIdx.x == 0) *cycle += 1;
+}
+// After a cycle's residual pass and stats: record the result, decide
+// (check_termination), and set the two conditions -- `update` (the IF node
+// around update + prolongation + injection: solver.cpp:359-370 runs them on
+// CONTINUE and on TIMEOUT) and `again` (the WHILE node).
+__global__ void k_loop_check(const Result* res, Result* hist, LoopState* st, const uint32_t* cycle, const int* err,
+                             cudaGraphConditionalHandle h_again, cudaGraphConditionalHandle h_update) {
+    lzb_pdl_enter();
+    if (threadIdx.x != 0) return;
+    const uint32_t i = st->count;
+    hist[i] = *res;
+    st->count = i + 1;
+    const double normalized = res->norm / st->front;
+    int status = LZB_CONTINUE;
+    if (normalized <= st->target) status = LZB_CONVERGED;
+    else if (normalized >= st->divergence) status = LZB_DIVERGED;
+    else if (static_cast<int>(*cycle) >= st->max_cycles) status = LZB_TIMEOUT;
+    const bool bad = *err != 0;  // a non-finite encode: the host throws, nothing more runs
+    st->status = status;
+    st->err = bad ? 1 : 0;
+    const bool update = !bad && (status == LZB_CONTINUE || status == LZB_TIMEOUT);
+    cudaGraphSetConditional(h_update, update ? 1u : 0u);
+    cudaGraphSetConditional(h_again, (!bad && status == LZB_CONTINUE && i + 1 < st->cap) ? 1u : 0u);
+}
+
 template <int KIND, bool FAST>
 void launch_step_k(cudaStream_t s, const LevelView& F, const LevelView& D, const lzb_field& f,
                    const int32_t* list, const int32_t* snap, const int* count_ptr, int64_t max_count,
@@ -2549,8 +2588,9 @@ public:
         if (hhist_) cudaFreeHost(hhist_);
         if (hcycle_) cudaFreeHost(hcycle_);
         if (herr_) cudaFreeHost(herr_);
-        for (cudaGraphExec_t* e : {&g_coarse_, &g_front_, &g_back_, &g_vfront_, &g_vback_})
+        for (cudaGraphExec_t* e : {&g_coarse_, &g_front_, &g_back_, &g_vfront_, &g_vback_, &g_loop_})
             if (*e) cudaGraphExecDestroy(*e);
+        if (hloop_) cudaFreeHost(hloop_);
         if (st_ready_) {
             cudaStreamSynchronize(cp_);
             cudaStreamDestroy(cp_);
@@ -2770,7 +2810,9 @@ public:
     // V-cycle's consistent Galerkin hierarchy)
     void coarse_pass_order(bool post_order) {
         // the epoch comes from pinned host memory at execution time (graph-replayable)
-        LZB_CUDA(cudaMemcpyAsync(dcycle_.p, hcycle_, sizeof(uint32_t), cudaMemcpyHostToDevice, s_));
+        // (the device loop's body counts the epoch on the device: k_loop_begin)
+        if (!loop_capture_)
+            LZB_CUDA(cudaMemcpyAsync(dcycle_.p, hcycle_, sizeof(uint32_t), cudaMemcpyHostToDevice, s_));
         for (int i = 0; i < D_; ++i) {
             const int l = post_order ? D_ - 1 - i : i;
             if (d_.transfer == LZB_BOXMG)
@@ -3552,10 +3594,154 @@ public:
         std::vector<lzb_cycle_report> out;
         if (d_.mode == LZB_EAGER) eager_setup();
         for (;;) {
-            out.push_back(step());
+            if (device_loop_ok()) run_device_loop(out);
+            else out.push_back(step());
             if (out.back().status != LZB_CONTINUE) break;
         }
         return out;
+    }
+
+    // ---- the quiescent cycles of run() as ONE graph launch (solver.cpp:421-444
+    // + 8-16 with the termination test on the device). Once no assembly work
+    // is left (every leaf top, no task pending or in flight) a cycle needs
+    // nothing from the host: coarse pass (change-gated, it still drains the
+    // one-level-per-cycle lag of the Galerkin hierarchy), residual pass, stats,
+    // termination, update. The graph is a conditional WHILE node; its body is
+    // that cycle, with the update passes inside a conditional IF node
+    // (k_loop_check sets both conditions). Each cycle's Result goes to a
+    // device history; the host reads it once after the loop and builds the
+    // same CycleReports step() would have. LZB_NO_DEVLOOP=1 keeps step().
+    static constexpr uint32_t kLoopCap = 4096;
+    bool device_loop_ok() const {
+        static const bool off = std::getenv("LZB_NO_DEVLOOP") != nullptr;
+        return !off && use_graphs_ && cycle_ >= 1 && !history_.empty() && all_top_ && pending_ == 0 &&
+               !batch_inflight_ && hq_.empty() && !ripple() && d_.forced_fraction <= 0.0 && slab_v1_ < 0 &&
+               static_cast<int>(cycle_) < d_.max_cycles;
+    }
+    void build_loop_graph() {
+        loop_hist_.alloc(kLoopCap);
+        loop_state_.alloc(1);
+        LZB_CUDA(cudaMallocHost(&hloop_, sizeof(LoopState) + kLoopCap * sizeof(Result)));
+        cudaGraph_t g = nullptr;
+        LZB_CUDA(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle h_again, h_update;
+        LZB_CUDA(cudaGraphConditionalHandleCreate(&h_again, g, 1, cudaGraphCondAssignDefault));
+        LZB_CUDA(cudaGraphConditionalHandleCreate(&h_update, g, 0, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams wp = {};
+        wp.type = cudaGraphNodeTypeConditional;
+        wp.conditional.handle = h_again;
+        wp.conditional.type = cudaGraphCondTypeWhile;
+        wp.conditional.size = 1;
+        cudaGraphNode_t wnode;
+        LZB_CUDA(cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
+        cudaGraph_t body = wp.conditional.phGraph_out[0], ifbody = nullptr, tmp = nullptr;
+        struct Flag {
+            bool& f;
+            explicit Flag(bool& x) : f(x) { f = true; }
+            ~Flag() { f = false; }
+        };
+        try {
+            const uint64_t l0 = g_launches.load();
+            LZB_CUDA(cudaStreamBeginCaptureToGraph(s_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+            try {
+                {
+                    PdlScope pdl;
+                    Flag in_loop(loop_capture_);
+                    LZB_LAUNCH(k_loop_begin, 1, 32, 0, s_, dcycle_.p);
+                    coarse_pass();
+                    residual_launches();
+                    stats_launches();
+                }
+                // plain launch and full edges around the decision kernel
+                LZB_LAUNCH(k_loop_check, 1, 32, 0, s_, static_cast<const Result*>(res_.p), loop_hist_.p, loop_state_.p,
+                           static_cast<const uint32_t*>(dcycle_.p), static_cast<const int*>(ctx_->err.p), h_again,
+                           h_update);
+                cudaStreamCaptureStatus cst;
+                const cudaGraphNode_t* deps = nullptr;
+                size_t ndeps = 0;
+                LZB_CUDA(cudaStreamGetCaptureInfo(s_, &cst, nullptr, nullptr, &deps, &ndeps));
+                cudaGraphNodeParams ip = {};
+                ip.type = cudaGraphNodeTypeConditional;
+                ip.conditional.handle = h_update;
+                ip.conditional.type = cudaGraphCondTypeIf;
+                ip.conditional.size = 1;
+                cudaGraphNode_t inode;
+                LZB_CUDA(cudaGraphAddNode(&inode, body, deps, ndeps, &ip));
+                LZB_CUDA(cudaStreamUpdateCaptureDependencies(s_, &inode, 1, cudaStreamSetCaptureDependencies));
+                ifbody = ip.conditional.phGraph_out[0];
+            } catch (...) {
+                cudaStreamEndCapture(s_, &tmp);
+                throw;
+            }
+            LZB_CUDA(cudaStreamEndCapture(s_, &tmp));
+            loop_kernels_[0] = g_launches.load() - l0;
+            LZB_CUDA(cudaStreamBeginCaptureToGraph(s_, ifbody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+            try {
+                PdlScope pdl;
+                back_body();
+            } catch (...) {
+                cudaStreamEndCapture(s_, &tmp);
+                throw;
+            }
+            LZB_CUDA(cudaStreamEndCapture(s_, &tmp));
+            loop_kernels_[1] = g_launches.load() - l0 - loop_kernels_[0];
+            g_launches.fetch_sub(loop_kernels_[0] + loop_kernels_[1]);  // counted when they run
+            LZB_CUDA(cudaGraphInstantiate(&g_loop_, g, 0));
+        } catch (...) {
+            cudaGraphDestroy(g);
+            throw;
+        }
+        LZB_CUDA(cudaGraphDestroy(g));
+    }
+    void run_device_loop(std::vector<lzb_cycle_report>& out) {
+        auto t0 = std::chrono::steady_clock::now();
+        ensure_rhs();
+        if (!g_loop_) build_loop_graph();
+        LoopState* hs = reinterpret_cast<LoopState*>(hloop_);
+        const Result* hh = reinterpret_cast<const Result*>(hloop_ + sizeof(LoopState));
+        std::memset(hs, 0, sizeof *hs);
+        hs->front = history_.front();
+        hs->target = d_.target;
+        hs->divergence = d_.divergence;
+        hs->max_cycles = d_.max_cycles;
+        hs->cap = kLoopCap;
+        *hcycle_ = cycle_;
+        LZB_CUDA(cudaMemcpyAsync(dcycle_.p, hcycle_, sizeof(uint32_t), cudaMemcpyHostToDevice, s_));
+        LZB_CUDA(cudaMemcpyAsync(loop_state_.p, hs, sizeof *hs, cudaMemcpyHostToDevice, s_));
+        LZB_CUDA(cudaGraphLaunch(g_loop_, s_));
+        LZB_CUDA(cudaMemcpyAsync(hs, loop_state_.p, sizeof *hs, cudaMemcpyDeviceToHost, s_));
+        LZB_CUDA(cudaStreamSynchronize(s_));
+        const uint32_t n = hs->count;
+        const int dev_status = hs->status;
+        const bool bad = hs->err != 0;
+        LZB_CUDA(cudaMemcpyAsync(hloop_ + sizeof(LoopState), loop_hist_.p, n * sizeof(Result), cudaMemcpyDeviceToHost,
+                                 s_));
+        LZB_CUDA(cudaStreamSynchronize(s_));
+        if (n == 0) throw Error(LZB_ERR_CUDA, "device cycle loop recorded no cycle");
+        const uint32_t good = bad ? n - 1 : n;  // the cycle that raised the flag is not reported (step() throws)
+        uint64_t updates = 0;
+        const size_t first = out.size();
+        for (uint32_t i = 0; i < good; ++i) {
+            lzb_cycle_report rep;
+            std::memset(&rep, 0, sizeof rep);
+            ++cycle_;
+            rep.cycle = static_cast<int32_t>(cycle_);
+            if (front_report(rep, hh[i])) ++updates;
+            finish_report(rep, hh[i]);
+            out.push_back(rep);
+        }
+        if (bad) ++cycle_;
+        *hcycle_ = cycle_;
+        g_launches.fetch_add(static_cast<uint64_t>(n) * loop_kernels_[0] + updates * loop_kernels_[1],
+                             std::memory_order_relaxed);
+        if (bad) {
+            LZB_CUDA(cudaMemset(ctx_->err.p, 0, sizeof(int)));
+            throw Error(LZB_ERR_PROTOCOL, "cannot encode non-finite operator entry");
+        }
+        if (out.back().status != dev_status)
+            throw Error(LZB_ERR_CUDA, "device cycle loop: host and device termination decisions differ");
+        const double w = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / good;
+        for (size_t i = first; i < out.size(); ++i) out[i].wall_seconds = w;
     }
 
     double pass(int which) {
@@ -4077,6 +4263,12 @@ private:
     bool all_top_ = false;        // every leaf converged (no request_stencil work left)
     cudaGraphExec_t g_coarse_ = nullptr, g_front_ = nullptr, g_back_ = nullptr;
     cudaGraphExec_t g_vfront_ = nullptr, g_vback_ = nullptr;  // V-cycle: front, sweeps (for vnu_)
+    cudaGraphExec_t g_loop_ = nullptr;  // the device-side cycle loop (run_device_loop)
+    bool loop_capture_ = false;         // capturing the loop body: the epoch is counted on the device
+    DevBuf<Result> loop_hist_;
+    DevBuf<LoopState> loop_state_;
+    unsigned char* hloop_ = nullptr;  // pinned: LoopState + the loop's Results
+    uint64_t loop_kernels_[2] = {0, 0};  // kernels per cycle: front part, update part
     int vnu_ = -1;
     bool uhat_is_u_ = false;
     uint64_t graph_kernels_[5] = {0, 0, 0, 0, 0};

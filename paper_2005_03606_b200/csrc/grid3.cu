@@ -551,12 +551,16 @@ struct SrcComp {
         if constexpr (W == 8) {
             return __longlong_as_double(static_cast<long long>(w));
         } else if constexpr (W <= 4) {
-            if (w == 0) return 0.0;
+            // e8 | fraction are contiguous in the word: one shift puts them at
+            // bit 20 of the high half, one add rebiases the exponent (no carry
+            // into the sign: e8 + 895 < 2048)
             constexpr int m = 8 * (W - 1) - 1;
-            const uint32_t sign = (w >> (8 * W - 1)) & 1u, e8 = (w >> m) & 0xffu, fr = w & ((1u << m) - 1u);
-            const uint32_t hi = (sign << 31) | ((e8 + 895u) << 20) | (m > 20 ? fr >> (m - 20) : fr << (20 - m));
-            const uint32_t lo = m > 20 ? fr << (52 - m) : 0u;
-            return __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
+            constexpr uint32_t body = (1u << (8 * W - 1)) - 1u;
+            const uint32_t mag = w & body;
+            const uint32_t hi = (m > 20 ? mag >> (m - 20) : mag << (20 - m)) + (895u << 20);
+            const uint32_t sg = (w >> (8 * W - 1)) << 31;
+            const uint32_t lo = m > 20 ? w << (52 - m) : 0u;
+            return w == 0 ? 0.0 : __hiloint2double(static_cast<int>(hi | sg), static_cast<int>(lo));
         } else {
             return PlaneDec(W)(static_cast<unsigned long long>(w));
         }
@@ -1207,7 +1211,7 @@ __host__ __device__ constexpr int tma_smem_bytes2(int W, int S) {
 // S stages: the tiles of iteration j land in stage j % S, issued S - 1
 // iterations ahead (S = 2 for the small compressed words, whose stages are
 // small; the FP64 planes' 66 KB stage leaves room for one per block)
-template <int W, int S>
+template <int W, int S, bool SYM>
 __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_tma(Lv3 F, const __grid_constant__ TmaMaps M,
                                                                  const __grid_constant__ TmaVMaps VM, Planes3 P,
                                                                  int zbeg, int zend, int zc) {
@@ -1314,7 +1318,14 @@ __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_tma(Lv3 F, const _
                 } else {
                     const int i1 = ty * w1 + tx + (e1 ? (X0 & (16 / (e1 ? e1 : 1) - 1)) : 0);
                     const int i2 = ty * w2 + tx + (e2 ? (X0 & (16 / (e2 ? e2 : 1) - 1)) : 0);
-                    const Base3 B(sec(st)[ty * we + tx + (X0 & 1)], P.s1, P.h);
+                    // SYM (the n = 1 classes symmetric, s1[0] == s1[2]: the unit interval): the
+                    // baseline takes 8 values, class (cx, cy, cz) -> (cx == 1, cy == 1, cz == 1)
+                    double b8[8];
+                    {
+                        const Base3 B(sec(st)[ty * we + tx + (X0 & 1)], P.s1, P.h);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) b8[k] = B(k >> 2, (k >> 1) & 1, k & 1);
+                    }
 #pragma unroll
                     for (int q = 0; q < 27; ++q) {
                         unsigned long long w;
@@ -1325,7 +1336,13 @@ __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_tma(Lv3 F, const _
                         if constexpr (e1 == 2) w |= static_cast<unsigned long long>(reinterpret_cast<const uint16_t*>(pc1(st))[q * kRzY * w1 + i1]) << (8 * e0);
                         else if constexpr (e1 == 1) w |= static_cast<unsigned long long>(pc1(st)[q * kRzY * w1 + i1]) << (8 * e0);
                         if constexpr (e2 == 1) w |= static_cast<unsigned long long>(pc2(st)[q * kRzY * w2 + i2]) << (8 * (e0 + e1));
-                        K[q] = B(q / 9, (q / 3) % 3, q % 3) + SrcComp<W>::dec(static_cast<typename SrcComp<W>::Word>(w));
+                        const double rt = SrcComp<W>::dec(static_cast<typename SrcComp<W>::Word>(w));
+                        if constexpr (SYM) {
+                            K[q] = b8[(q / 9 == 1) * 4 + ((q / 3) % 3 == 1) * 2 + (q % 3 == 1)] + rt;
+                        } else {
+                            const Base3 B(sec(st)[ty * we + tx + (X0 & 1)], P.s1, P.h);
+                            K[q] = B(q / 9, (q / 3) % 3, q % 3) + rt;
+                        }
                     }
                 }
 #pragma unroll
@@ -2570,13 +2587,20 @@ private:
         build_maps();
         static bool attr = false;
         if (!attr) {
-            LZB_CUDA(cudaFuncSetAttribute(k3_residual_tma<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            LZB_CUDA(cudaFuncSetAttribute(k3_residual_tma<W, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          tma_smem_bytes2(W, S)));
+            LZB_CUDA(cudaFuncSetAttribute(k3_residual_tma<W, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           tma_smem_bytes2(W, S)));
             attr = true;
         }
         vmaps(v);
-        LZB_LAUNCH((k3_residual_tma<W, S>), g, kRzX * kRzY, tma_smem_bytes2(W, S), s_, v, maps_, vmaps_, planes(), z0,
-                   z1, zc);
+        const Planes3 pl = planes();
+        if (pl.s1[0] == pl.s1[2])
+            LZB_LAUNCH((k3_residual_tma<W, S, true>), g, kRzX * kRzY, tma_smem_bytes2(W, S), s_, v, maps_, vmaps_, pl,
+                       z0, z1, zc);
+        else
+            LZB_LAUNCH((k3_residual_tma<W, S, false>), g, kRzX * kRzY, tma_smem_bytes2(W, S), s_, v, maps_, vmaps_, pl,
+                       z0, z1, zc);
     }
     bool leaf_diag_dirty_ = true;
     // TMA maps of the leaf vertex fields the residual reads (u, u-hat -- u

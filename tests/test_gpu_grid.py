@@ -550,3 +550,43 @@ def test_vertex_stencils_match_restatement():
         N = 3 ** lvl
         got = g.vertex_stencils(lvl)
         assert np.array_equal(got, _stencils_restated(g.cells(lvl)["ops"], N)), lvl
+
+
+DEVLOOP = [("setup = checkerboard\nfield-seed = 1", "adafac-pi", "eager", "geometric", 300, 1e-10),
+           ("setup = checkerboard\nfield-seed = 1", "additive", "anarchic", "boxmg", 25, 1e-10),   # timeout
+           ("setup = quadrant\neps-low = 0.001", "adafac-jac", "adaptive", "geometric", 400, 1e-9),
+           ("setup = sinusoid", "adafac-pi", "anarchic", "geometric", 200, 1e-10)]
+
+
+@pytest.mark.parametrize("f,solver,asm,transfer,cycles,target", DEVLOOP)
+def test_run_device_loop_matches_stepping(f, solver, asm, transfer, cycles, target):
+    """lzb_grid_run hands the quiescent cycles to the device-side loop (a
+    conditional WHILE graph, termination test on the device: solver.cpp:8-16,
+    421-444); stepping the same grid cycle by cycle from the host gives the
+    same reports (the same kernels, so the same bits) and the same state."""
+    text = (f"{f}\ndepth = 4\nsolver = {solver}\nassembly = {asm}\ntransfer = {transfer}\nmax-cycles = {cycles}\n"
+            f"omega = 0.6\nrhs = 1\nseed = 7\ntarget = {target}\n")
+    k = port.parse_keys(text)
+    d = port.desc_from_keys(k)
+    g, h = lzb.Grid(d, 7), lzb.Grid(d, 7)
+    rg = g.run()
+    if asm == "eager":
+        h.eager_setup()
+    rh = []
+    while not rh or rh[-1]["status"] == lzb.T.CONTINUE:
+        rh.append(h.step())
+    assert len(rg) > 8
+    assert_reports(rg, rh, rel=0.0)
+    for lvl in range(5):
+        for fld in (lzb.T.V_U, lzb.T.V_R, lzb.T.V_FL):
+            assert np.array_equal(g.vertices(lvl, fld), h.vertices(lvl, fld)), (lvl, fld)
+        assert np.array_equal(g.cells(lvl)["ops"], h.cells(lvl)["ops"])
+        assert np.array_equal(g.cells(lvl)["epoch"], h.cells(lvl)["epoch"])
+    # the loop's reports share one wall-clock share (its cycles ran in one graph launch)
+    if asm == "eager":  # quiescent from the second cycle on (anarchic runs may keep tasks pending to the end)
+        walls = [r["wall_seconds"] for r in rg[-4:]]
+        assert len(set(walls)) == 1
+    # and the grid carries on from the host afterwards
+    if rg[-1]["status"] == lzb.T.TIMEOUT:
+        a, b = g.step(), h.step()
+        assert a["residual"] == b["residual"] and a["cycle"] == b["cycle"]
