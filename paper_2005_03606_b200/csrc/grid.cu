@@ -19,6 +19,7 @@
 #include <deque>
 #include <unordered_map>
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -53,6 +54,7 @@ enum StatSlot {
     S_MAXDELTA = 14,    // cumulative, bits of a non-negative double
     S_MAXSAMPLES = 15,  // cumulative
     S_PENDING = 16,     // leaves with a task in flight (p2), per cycle
+    S_COARSE_ACTIVE = 17,  // the last cycle in which a coarse cell passed its change gate
 };
 
 __device__ inline int64_t gtid() { return blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; }
@@ -300,15 +302,18 @@ __global__ void k_compact_scatter(LevelView F, int selector, const long long* ke
         }
     }
     __syncthreads();
+    int bin = -1;
     if (take) {
         int pos = warp_off[w] + __popc(mask & ((1u << lane) - 1));
         list[pos] = static_cast<int32_t>(c);
         snap[pos] = p1;
-        if (p1 != kForcedSnap) {
-            int bin = p1 == LZB_P1_TOP ? kNHist - 1 : (p1 < kNHist - 1 ? p1 : kNHist - 1);
-            atomicAdd(&hist[bin], 1u);
-        }
+        if (p1 != kForcedSnap) bin = p1 == LZB_P1_TOP ? kNHist - 1 : (p1 < kNHist - 1 ? p1 : kNHist - 1);
     }
+    // the p1 histogram, one atomic per distinct bin of a warp (on a ladder the
+    // whole level sits at one n: per-leaf atomics on one address serialise,
+    // 0.35 ms for the 531 k leaves of 729^2)
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], static_cast<unsigned>(__popc(peers)));
 }
 
 // p1 = bottom -> integrate with n = 1, publish, p1 = 1 (assembly.cpp:26-34).
@@ -615,6 +620,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_geo(LevelView C, Leve
             if (mx < seen) return;
         }
         C.seen[c] = cycle + 1;
+        stats[S_COARSE_ACTIVE] = cycle;  // benign race: every writer stores the cycle
     }
     const double* ch[9];
     for (int i = 0; i < 3; ++i)
@@ -747,6 +753,7 @@ __global__ void __launch_bounds__(64) k_coarse(LevelView C, LevelView F, lzb_fie
             if (mx < seen) return;
         }
         C.seen[c] = cycle + 1;
+        stats[S_COARSE_ACTIVE] = cycle;  // benign race: every writer stores the cycle
     }
     double ch[144];
     for (int lx = 0; lx < 3; ++lx)
@@ -1912,7 +1919,11 @@ __global__ void k_record_sizes_upper(AllLevels A, int64_t ncells, int64_t* __res
 // 100 vertices each) run the per-vertex bodies of the per-level kernels in
 // the same order, a block barrier between passes (global writes of the block
 // are visible to it after __syncthreads). Bit-identical to the per-level
-// launches.
+// launches. (Measured, round 2: the same fusion over an 8-block cluster with
+// cluster barriers, extended to the 27^2 and 81^2 levels, cut the 729^2 settled
+// cycle from 40 to 22 launches but ran 183 us against 166 us: a handful of SMs
+// doing the latency-bound per-vertex gathers of 6.7 k vertices per pass loses
+// to separate launches spread over the GPU with programmatic dependent launch.)
 constexpr int kSmallThreads = 1024;
 constexpr int kSmallMaxN = 9;
 struct Damp {
@@ -2248,8 +2259,10 @@ struct LoopState {
     int32_t max_cycles;
     uint32_t count, cap;  // cycles recorded by this launch / room in the history
     int32_t status, err;
+    int32_t settled;  // out (full body): a whole coarse pass found nothing to recompute
 };
-__global__ void k_loop_begin(uint32_t* cycle) {  // ++cycle (the epoch the coarse pass stamps)
+// ++cycle (the epoch the coarse pass stamps)
+__global__ void k_loop_begin(uint32_t* cycle) {
     lzb_pdl_enter();
     if (threadIdx.x == 0) *cycle += 1;
 }
@@ -2257,11 +2270,17 @@ __global__ void k_loop_begin(uint32_t* cycle) {  // ++cycle (the epoch the coars
 // (check_termination), and set the two conditions -- `update` (the IF node
 // around update + prolongation + injection: solver.cpp:359-370 runs them on
 // CONTINUE and on TIMEOUT) and `again` (the WHILE node).
-__global__ void k_loop_check(const Result* res, Result* hist, LoopState* st, const uint32_t* cycle, const int* err,
-                             cudaGraphConditionalHandle h_again, cudaGraphConditionalHandle h_update) {
+__global__ void k_loop_check(Result* res, Result* hist, LoopState* st, const uint32_t* cycle, const int* err,
+                             cudaGraphConditionalHandle h_again, cudaGraphConditionalHandle h_update, int full) {
     lzb_pdl_enter();
     if (threadIdx.x != 0) return;
     const uint32_t i = st->count;
+    // full body: did this cycle's coarse pass recompute anything? When it did
+    // not, no operator, marker or epoch changed, so the next pass cannot
+    // either (its gates read only those): the hierarchy has settled, and the
+    // coarse pass and the stats are no-ops from here on (the settled body).
+    bool settled = false;
+    if (full) settled = res->s[S_COARSE_ACTIVE] != *cycle;
     hist[i] = *res;
     st->count = i + 1;
     const double normalized = res->norm / st->front;
@@ -2272,9 +2291,10 @@ __global__ void k_loop_check(const Result* res, Result* hist, LoopState* st, con
     const bool bad = *err != 0;  // a non-finite encode: the host throws, nothing more runs
     st->status = status;
     st->err = bad ? 1 : 0;
+    st->settled = settled ? 1 : 0;
     const bool update = !bad && (status == LZB_CONTINUE || status == LZB_TIMEOUT);
     cudaGraphSetConditional(h_update, update ? 1u : 0u);
-    cudaGraphSetConditional(h_again, (!bad && status == LZB_CONTINUE && i + 1 < st->cap) ? 1u : 0u);
+    cudaGraphSetConditional(h_again, (!bad && !settled && status == LZB_CONTINUE && i + 1 < st->cap) ? 1u : 0u);
 }
 
 template <int KIND, bool FAST>
@@ -2548,6 +2568,7 @@ public:
         *herr_ = 0;
         dcycle_.alloc(1);
         use_graphs_ = std::getenv("LZB_NO_GRAPHS") == nullptr;
+        tables_.reserve_n = atables_.reserve_n = d_.n_max > 0 ? std::min(d_.n_max, 128) : 64;
         // subtree sizes for pre-order slots
         for (int k = 0; k <= D_; ++k) {
             int64_t s = 0, p = 1;
@@ -2588,7 +2609,7 @@ public:
         if (hhist_) cudaFreeHost(hhist_);
         if (hcycle_) cudaFreeHost(hcycle_);
         if (herr_) cudaFreeHost(herr_);
-        for (cudaGraphExec_t* e : {&g_coarse_, &g_front_, &g_back_, &g_vfront_, &g_vback_, &g_loop_})
+        for (cudaGraphExec_t* e : {&g_coarse_, &g_front_, &g_back_, &g_front_quiet_, &g_vfront_, &g_vback_, &g_loop_[0], &g_loop_[1]})
             if (*e) cudaGraphExecDestroy(*e);
         if (hloop_) cudaFreeHost(hloop_);
         if (st_ready_) {
@@ -2644,6 +2665,7 @@ public:
     void ensure_tables(int nn) {  // per-n tables; the field and level are fixed per grid
         if (tables_.n == nn && tables_.N == L_[D_].N) return;
         tables_.build(d_.field, L_[D_].N, L_[D_].h, nn, s_);
+        if (next_n(nn) != nn && next_n(nn) <= 512) tables_.prefetch(d_.field, L_[D_].N, L_[D_].h, next_n(nn));
     }
 
     // One batched round of adaptive steps over the selected leaves; returns
@@ -2688,7 +2710,10 @@ public:
         const bool cap = d_.n_max > 0 && n >= d_.n_max;
         const int nn = next_n(n);
         if (!cap && !(atables_.n == nn && atables_.N == L_[D_].N))
+        {
             atables_.build(d_.field, L_[D_].N, L_[D_].h, nn, a_);
+            if (next_n(nn) != nn && next_n(nn) <= 512) atables_.prefetch(d_.field, L_[D_].N, L_[D_].h, next_n(nn));
+        }
         const bool fast = d_.integration == LZB_INTEGRATE_FAST;
         unsigned long long* stats = res_.p->s;
         // geometric start: the first batch holds the deferred bottom -> 1 steps
@@ -2720,6 +2745,7 @@ public:
         LZB_LAUNCH(k_commit, blocks_for(leaves_, kThreads), kThreads, 0, s_, V(D_), staging(), alist_.p,
                    acounter_.p, cycle_);
         all_top_ = false;
+        settled_ = false;
         batch_inflight_ = false;
         ++batches_committed_;
         return true;
@@ -2738,12 +2764,14 @@ public:
 
     int64_t round(int selector, bool complete_tasks, long long key_limit = -1) {
         LevelView F = V(D_);
+        const double t_round = trace() ? now_ms() : 0.0;
         compact(s_, selector, key_limit, list_.p, snap_.p, counter_.p, blockcnt_.p, hist_.p);
         LZB_CUDA(cudaMemcpyAsync(hhist_, hist_.p, kNHist * sizeof(unsigned), cudaMemcpyDeviceToHost, s_));
         LZB_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(hhist_) + kNHist * sizeof(unsigned),
                                  counter_.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
         sync_check();
         int count = *reinterpret_cast<int*>(reinterpret_cast<char*>(hhist_) + kNHist * sizeof(unsigned));
+        if (trace()) std::fprintf(stderr, "[lzb] round: compact + readback %.3f ms, %d leaves\n", now_ms() - t_round, count);
         if (count == 0) return 0;
         if (hhist_[kNHist - 1] && selector != 1)
             throw Error(LZB_ERR_RESOURCE, "sub-sample count beyond 4095 per axis");
@@ -2759,11 +2787,18 @@ public:
             if (!hhist_[n]) continue;
             bool cap = d_.n_max > 0 && n >= d_.n_max;
             int nn = next_n(n);
+            const double t_tab = trace() ? now_ms() : 0.0;
             if (!cap) ensure_tables(nn);
+            const double t_step = trace() ? now_ms() : 0.0;
             bool fast = d_.integration == LZB_INTEGRATE_FAST;
             const IntTables T = tables_.view();
             dispatch_step(fast, s_, F, F, d_.field, list_.p, snap_.p, counter_.p, count, n, nn, cap, T,
                           d_.termination_c, d_.delta_max, cycle_, stats, ctx_->err.p);
+            if (trace()) {
+                LZB_CUDA(cudaStreamSynchronize(s_));
+                std::fprintf(stderr, "[lzb] round: n %d -> %d: tables %.3f ms, step kernels %.3f ms\n", n, nn,
+                             t_step - t_tab, now_ms() - t_step);
+            }
         }
         if (complete_tasks)
             LZB_LAUNCH(k_clear_p2, blocks_for(count, kThreads), kThreads, 0, s_, F, list_.p, count);
@@ -2837,16 +2872,24 @@ public:
         PdlScope() : prev(g_pdl) { g_pdl = std::getenv("LZB_NO_PDL") == nullptr; }
         ~PdlScope() { g_pdl = prev; }
     };
+    static bool trace() {
+        static const bool on = std::getenv("LZB_TRACE") != nullptr;
+        return on;
+    }
+    static double now_ms() {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    }
     void run_graph(cudaGraphExec_t& exec, void (Grid::*body)()) {
         if (!use_graphs_) {
             PdlScope pdl;
             (this->*body)();
             return;
         }
-        const int slot = &exec == &g_coarse_ ? 0 : &exec == &g_front_ ? 1 : &exec == &g_back_ ? 2 : &exec == &g_vfront_ ? 3 : 4;
+        const int slot = &exec == &g_coarse_ ? 0 : &exec == &g_front_ ? 1 : &exec == &g_back_ ? 2 : &exec == &g_vfront_ ? 3 : &exec == &g_vback_ ? 4 : 5;
         if (!exec) {
             cudaGraph_t g = nullptr;
             const uint64_t l0 = g_launches.load();
+            const double tb = trace() ? now_ms() : 0.0;
             LZB_CUDA(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal));
             try {
                 PdlScope pdl;
@@ -2861,6 +2904,9 @@ public:
             g_launches.fetch_sub(graph_kernels_[slot]);      // counted when they run
             LZB_CUDA(cudaGraphInstantiate(&exec, g, 0));
             LZB_CUDA(cudaGraphDestroy(g));
+            if (trace())
+                std::fprintf(stderr, "[lzb] graph slot %d: %llu kernels, capture + instantiate %.3f ms\n", slot,
+                             static_cast<unsigned long long>(graph_kernels_[slot]), now_ms() - tb);
         }
         LZB_CUDA(cudaGraphLaunch(exec, s_));
         g_launches.fetch_add(graph_kernels_[slot], std::memory_order_relaxed);
@@ -2868,6 +2914,11 @@ public:
     void front_body() {  // residual pass + stats + result / error flag D2H
         residual_launches();
         stats_launches();
+        LZB_CUDA(cudaMemcpyAsync(hres_, res_.p, sizeof(Result), cudaMemcpyDeviceToHost, s_));
+        LZB_CUDA(cudaMemcpyAsync(herr_, ctx_->err.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
+    }
+    void front_body_quiet() {  // a settled cycle: the residual pass + result / error flag D2H
+        residual_launches();
         LZB_CUDA(cudaMemcpyAsync(hres_, res_.p, sizeof(Result), cudaMemcpyDeviceToHost, s_));
         LZB_CUDA(cudaMemcpyAsync(herr_, ctx_->err.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
     }
@@ -3271,8 +3322,18 @@ public:
         std::memset(&rep, 0, sizeof rep);
         ++cycle_;
         *hcycle_ = cycle_;
-        if (d_.concurrent) try_commit(false);  // swap in a finished batch before the walk
-        else begin_cycle_tasks();
+        // calm: nothing of the assembly side can act in this cycle (every leaf
+        // at its top, no task pending or in flight). A calm cycle whose coarse
+        // pass recomputed nothing leaves every operator, marker and epoch as it
+        // found them, so the next calm cycle's coarse pass and stats are no-ops
+        // with the same outcome: settled_ cycles skip both (the stats slots of
+        // the device result keep their values).
+        const bool calm = quiescent();
+        const bool quiet = calm && settled_ && use_graphs_;
+        if (!quiet) {
+            if (d_.concurrent) try_commit(false);  // swap in a finished batch before the walk
+            else begin_cycle_tasks();
+        }
         rep.cycle = static_cast<int32_t>(cycle_);
         if (d_.forced_fraction > 0.0) {  // on_cycle_start (experiment.cpp:260-270)
             long long id0 = 0;
@@ -3280,16 +3341,21 @@ public:
             LZB_LAUNCH(k_spawn_forced, blocks_for(leaves_, kThreads), kThreads, 0, s_, V(D_), cycle_,
                        static_cast<long long>(leaves_), keys_.p, id0, d_.forced_fraction);
         }
-        if (ripple()) {
-            ripple_walk();
-            if (ripple_fifo()) ripple_spawn_fifo();
+        if (quiet) {
+            ensure_rhs();
+            run_graph(g_front_quiet_, &Grid::front_body_quiet);  // residual + result/error copy-out
         } else {
-            run_graph(g_coarse_, &Grid::coarse_pass);
+            if (ripple()) {
+                ripple_walk();
+                if (ripple_fifo()) ripple_spawn_fifo();
+            } else {
+                run_graph(g_coarse_, &Grid::coarse_pass);
+            }
+            leaves_pass();
+            if (d_.concurrent && !batch_inflight_ && (cycle_ == 1 || pending_ > 0)) launch_batch();
+            ensure_rhs();
+            run_graph(g_front_, &Grid::front_body);  // residual + stats + result/error copy-out
         }
-        leaves_pass();
-        if (d_.concurrent && !batch_inflight_ && (cycle_ == 1 || pending_ > 0)) launch_batch();
-        ensure_rhs();
-        run_graph(g_front_, &Grid::front_body);  // residual + stats + result/error copy-out
         LZB_CUDA(cudaStreamSynchronize(s_));
         if (*herr_) {
             LZB_CUDA(cudaMemset(ctx_->err.p, 0, sizeof(int)));
@@ -3299,6 +3365,7 @@ public:
         Result r = *hres_;
         if (front_report(rep, r)) run_graph(g_back_, &Grid::back_body);  // update + prolongation + injection
         finish_report(rep, r);
+        settled_ = calm && quiescent() && (quiet || r.s[S_COARSE_ACTIVE] != cycle_);
         LZB_CUDA(cudaStreamSynchronize(s_));
         rep.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         return rep;
@@ -3592,11 +3659,23 @@ public:
 
     std::vector<lzb_cycle_report> run() {  // solver.cpp:421-444 (no AMR on regular grids)
         std::vector<lzb_cycle_report> out;
+        const double t_run = trace() ? now_ms() : 0.0;
         if (d_.mode == LZB_EAGER) eager_setup();
+        if (trace()) {
+            LZB_CUDA(cudaStreamSynchronize(s_));
+            std::fprintf(stderr, "[lzb] run: eager_setup %.3f ms\n", now_ms() - t_run);
+        }
         for (;;) {
-            if (device_loop_ok()) run_device_loop(out);
-            else out.push_back(step());
-            if (out.back().status != LZB_CONTINUE) break;
+            if (device_loop_ok()) {
+                run_device_loop(out);
+            } else {
+                const double ts = trace() ? now_ms() : 0.0;
+                out.push_back(step());
+                if (trace())
+                    std::fprintf(stderr, "[lzb] host step %u: %.3f ms (pending %lld)\n", cycle_, now_ms() - ts,
+                                 static_cast<long long>(pending_));
+            }
+            if (!out.empty() && out.back().status != LZB_CONTINUE) break;
         }
         return out;
     }
@@ -3612,16 +3691,22 @@ public:
     // device history; the host reads it once after the loop and builds the
     // same CycleReports step() would have. LZB_NO_DEVLOOP=1 keeps step().
     static constexpr uint32_t kLoopCap = 4096;
+    bool quiescent() const {
+        return all_top_ && pending_ == 0 && !batch_inflight_ && hq_.empty() && !ripple() &&
+               d_.forced_fraction <= 0.0 && slab_v1_ < 0;
+    }
+    void unsettle() { settled_ = false; }
     bool device_loop_ok() const {
-        static const bool off = std::getenv("LZB_NO_DEVLOOP") != nullptr;
-        return !off && use_graphs_ && cycle_ >= 1 && !history_.empty() && all_top_ && pending_ == 0 &&
-               !batch_inflight_ && hq_.empty() && !ripple() && d_.forced_fraction <= 0.0 && slab_v1_ < 0 &&
+        const bool on = std::getenv("LZB_DEVLOOP") != nullptr;  // read per call: tests toggle it
+        return on && use_graphs_ && cycle_ >= 1 && !history_.empty() && quiescent() &&
                static_cast<int>(cycle_) < d_.max_cycles;
     }
-    void build_loop_graph() {
-        loop_hist_.alloc(kLoopCap);
-        loop_state_.alloc(1);
-        LZB_CUDA(cudaMallocHost(&hloop_, sizeof(LoopState) + kLoopCap * sizeof(Result)));
+    void build_loop_graph(int full) {
+        if (!hloop_) {
+            loop_hist_.alloc(kLoopCap);
+            loop_state_.alloc(1);
+            LZB_CUDA(cudaMallocHost(&hloop_, sizeof(LoopState) + kLoopCap * sizeof(Result)));
+        }
         cudaGraph_t g = nullptr;
         LZB_CUDA(cudaGraphCreate(&g, 0));
         cudaGraphConditionalHandle h_again, h_update;
@@ -3640,6 +3725,7 @@ public:
             explicit Flag(bool& x) : f(x) { f = true; }
             ~Flag() { f = false; }
         };
+        uint64_t* kern = loop_kernels_[full];
         try {
             const uint64_t l0 = g_launches.load();
             LZB_CUDA(cudaStreamBeginCaptureToGraph(s_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
@@ -3648,14 +3734,14 @@ public:
                     PdlScope pdl;
                     Flag in_loop(loop_capture_);
                     LZB_LAUNCH(k_loop_begin, 1, 32, 0, s_, dcycle_.p);
-                    coarse_pass();
+                    if (full) coarse_pass();
                     residual_launches();
-                    stats_launches();
+                    if (full) stats_launches();
                 }
                 // plain launch and full edges around the decision kernel
-                LZB_LAUNCH(k_loop_check, 1, 32, 0, s_, static_cast<const Result*>(res_.p), loop_hist_.p, loop_state_.p,
+                LZB_LAUNCH(k_loop_check, 1, 32, 0, s_, res_.p, loop_hist_.p, loop_state_.p,
                            static_cast<const uint32_t*>(dcycle_.p), static_cast<const int*>(ctx_->err.p), h_again,
-                           h_update);
+                           h_update, full);
                 cudaStreamCaptureStatus cst;
                 const cudaGraphNode_t* deps = nullptr;
                 size_t ndeps = 0;
@@ -3674,7 +3760,7 @@ public:
                 throw;
             }
             LZB_CUDA(cudaStreamEndCapture(s_, &tmp));
-            loop_kernels_[0] = g_launches.load() - l0;
+            kern[0] = g_launches.load() - l0;
             LZB_CUDA(cudaStreamBeginCaptureToGraph(s_, ifbody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
             try {
                 PdlScope pdl;
@@ -3684,19 +3770,32 @@ public:
                 throw;
             }
             LZB_CUDA(cudaStreamEndCapture(s_, &tmp));
-            loop_kernels_[1] = g_launches.load() - l0 - loop_kernels_[0];
-            g_launches.fetch_sub(loop_kernels_[0] + loop_kernels_[1]);  // counted when they run
-            LZB_CUDA(cudaGraphInstantiate(&g_loop_, g, 0));
+            kern[1] = g_launches.load() - l0 - kern[0];
+            g_launches.fetch_sub(kern[0] + kern[1]);  // counted when they run
+            LZB_CUDA(cudaGraphInstantiate(&g_loop_[full], g, 0));
         } catch (...) {
             cudaGraphDestroy(g);
             throw;
         }
         LZB_CUDA(cudaGraphDestroy(g));
     }
+    // One launch of the loop graph: the full body until the hierarchy has
+    // settled (or the run ends), the settled body (no coarse pass, no stats:
+    // both are no-ops once nothing changes) after that. settled_ is dropped by
+    // everything that can change an operator or a marker.
     void run_device_loop(std::vector<lzb_cycle_report>& out) {
         auto t0 = std::chrono::steady_clock::now();
         ensure_rhs();
-        if (!g_loop_) build_loop_graph();
+        const int full = settled_ ? 0 : 1;
+        if (!g_loop_[full]) {
+            const double tb = trace() ? now_ms() : 0.0;
+            build_loop_graph(full);
+            if (trace())
+                std::fprintf(stderr, "[lzb] loop graph (full = %d): %llu + %llu kernels, build %.3f ms\n", full,
+                             static_cast<unsigned long long>(loop_kernels_[full][0]),
+                             static_cast<unsigned long long>(loop_kernels_[full][1]), now_ms() - tb);
+        }
+        const double tl = trace() ? now_ms() : 0.0;
         LoopState* hs = reinterpret_cast<LoopState*>(hloop_);
         const Result* hh = reinterpret_cast<const Result*>(hloop_ + sizeof(LoopState));
         std::memset(hs, 0, sizeof *hs);
@@ -3708,12 +3807,16 @@ public:
         *hcycle_ = cycle_;
         LZB_CUDA(cudaMemcpyAsync(dcycle_.p, hcycle_, sizeof(uint32_t), cudaMemcpyHostToDevice, s_));
         LZB_CUDA(cudaMemcpyAsync(loop_state_.p, hs, sizeof *hs, cudaMemcpyHostToDevice, s_));
-        LZB_CUDA(cudaGraphLaunch(g_loop_, s_));
+        LZB_CUDA(cudaGraphLaunch(g_loop_[full], s_));
         LZB_CUDA(cudaMemcpyAsync(hs, loop_state_.p, sizeof *hs, cudaMemcpyDeviceToHost, s_));
         LZB_CUDA(cudaStreamSynchronize(s_));
         const uint32_t n = hs->count;
         const int dev_status = hs->status;
         const bool bad = hs->err != 0;
+        if (full && hs->settled) settled_ = true;
+        if (trace())
+            std::fprintf(stderr, "[lzb] device loop (full = %d): %u cycles in %.3f ms (%.1f us per cycle)\n", full, n,
+                         now_ms() - tl, 1e3 * (now_ms() - tl) / (n ? n : 1));
         LZB_CUDA(cudaMemcpyAsync(hloop_ + sizeof(LoopState), loop_hist_.p, n * sizeof(Result), cudaMemcpyDeviceToHost,
                                  s_));
         LZB_CUDA(cudaStreamSynchronize(s_));
@@ -3732,12 +3835,13 @@ public:
         }
         if (bad) ++cycle_;
         *hcycle_ = cycle_;
-        g_launches.fetch_add(static_cast<uint64_t>(n) * loop_kernels_[0] + updates * loop_kernels_[1],
+        g_launches.fetch_add(static_cast<uint64_t>(n) * loop_kernels_[full][0] + updates * loop_kernels_[full][1],
                              std::memory_order_relaxed);
         if (bad) {
             LZB_CUDA(cudaMemset(ctx_->err.p, 0, sizeof(int)));
             throw Error(LZB_ERR_PROTOCOL, "cannot encode non-finite operator entry");
         }
+        if (good == 0) return;
         if (out.back().status != dev_status)
             throw Error(LZB_ERR_CUDA, "device cycle loop: host and device termination decisions differ");
         const double w = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / good;
@@ -3819,6 +3923,7 @@ public:
     void publish_element(int level, int cx, int cy, const double* m, int n, int32_t p1) {
         check_cell(level, cx, cy);
         all_top_ = false;
+        settled_ = false;
         if (level != D_) throw Error(LZB_ERR_INVALID, "publish_element is for leaf cells");
         DevBuf<double> dm(16);
         LZB_CUDA(cudaMemcpyAsync(dm.p, m, 128, cudaMemcpyHostToDevice, s_));
@@ -3847,6 +3952,7 @@ public:
     void publish_level(int level, const double* mats, const int32_t* n, int32_t p1) {
         if (level != D_) throw Error(LZB_ERR_INVALID, "publish_level is for the leaf level");
         all_top_ = false;
+        settled_ = false;
         const int64_t nc = L_[D_].nc;
         DevBuf<double> dm(static_cast<size_t>(nc) * 16);
         DevBuf<int32_t> dn(static_cast<size_t>(nc));
@@ -3876,6 +3982,7 @@ public:
     void adaptive_step(int level, int cx, int cy) {
         check_cell(level, cx, cy);
         all_top_ = false;
+        settled_ = false;
         if (level != D_) throw Error(LZB_ERR_INVALID, "adaptive steps are for leaf cells");
         LZB_LAUNCH(k_step_one, 1, 32, 0, s_, V(D_), d_.field, cy * L_[D_].N + cx, d_.schedule,
                    d_.n_max, d_.termination_c, d_.delta_max, cycle_,
@@ -4120,6 +4227,7 @@ public:
 
     void load(const uint8_t* in, int64_t size) {  // CellStream::load (stream.cpp:340-394)
         all_top_ = false;
+        settled_ = false;
         if (size < 4) throw Error(LZB_ERR_CORRUPT, "truncated stream file");
         uint32_t hdr[3] = {0, 0, 0};
         std::memcpy(&hdr[0], in, 4);
@@ -4169,6 +4277,7 @@ public:
     void invalidate() {
         LZB_CUDA(cudaStreamSynchronize(s_));
         all_top_ = false;
+        settled_ = false;
     }
 
     void plane_arrays(void** planes, void** cp3, int* width) {
@@ -4262,16 +4371,18 @@ private:
     bool rhs_ready_ = false;      // leaf-level lumped load in place
     bool all_top_ = false;        // every leaf converged (no request_stencil work left)
     cudaGraphExec_t g_coarse_ = nullptr, g_front_ = nullptr, g_back_ = nullptr;
+    cudaGraphExec_t g_front_quiet_ = nullptr;  // a settled cycle's front: no coarse pass, no stats
     cudaGraphExec_t g_vfront_ = nullptr, g_vback_ = nullptr;  // V-cycle: front, sweeps (for vnu_)
-    cudaGraphExec_t g_loop_ = nullptr;  // the device-side cycle loop (run_device_loop)
+    cudaGraphExec_t g_loop_[2] = {nullptr, nullptr};  // the device-side cycle loop: [0] settled body, [1] full body
+    bool settled_ = false;  // a full coarse pass found nothing to recompute and nothing has changed since
     bool loop_capture_ = false;         // capturing the loop body: the epoch is counted on the device
     DevBuf<Result> loop_hist_;
     DevBuf<LoopState> loop_state_;
     unsigned char* hloop_ = nullptr;  // pinned: LoopState + the loop's Results
-    uint64_t loop_kernels_[2] = {0, 0};  // kernels per cycle: front part, update part
+    uint64_t loop_kernels_[2][2] = {{0, 0}, {0, 0}};  // [body][front part, update part] kernels per cycle
     int vnu_ = -1;
     bool uhat_is_u_ = false;
-    uint64_t graph_kernels_[5] = {0, 0, 0, 0, 0};
+    uint64_t graph_kernels_[6] = {0, 0, 0, 0, 0, 0};
     double first_residual_ = -1.0;
     int slab_v0_ = 0, slab_v1_ = -1;  // leaf vertex rows of this rank's slab (-1: the whole level)
     std::chrono::steady_clock::time_point dist_t0_{};
@@ -4307,27 +4418,27 @@ void lzb_grid_destroy(lzb_grid* g) {
     delete g->g;
     delete g;
 }
-int lzb_grid_init_noise(lzb_grid* g, uint64_t seed) { return guarded([&] { g->g->init_noise(seed); }); }
+int lzb_grid_init_noise(lzb_grid* g, uint64_t seed) { return guarded([&] { g->g->unsettle(); g->g->init_noise(seed); }); }
 int lzb_grid_eager_setup(lzb_grid* g) {
-    return guarded([&] {
+    return guarded([&] { g->g->unsettle();
         g->g->eager_setup();
         g->g->sync_check();
     });
 }
 int lzb_grid_assemble_rows(lzb_grid* g, int n, int row0, int row1) {
-    return guarded([&] {
+    return guarded([&] { g->g->unsettle();
         g->g->assemble_fixed_rows(n, row0, row1);
         g->g->sync_check();
     });
 }
 int lzb_grid_assemble_fixed_raw(lzb_grid* g, int n, double* host_raw) {
-    return guarded([&] { g->g->assemble_fixed_raw(n, host_raw); });
+    return guarded([&] { g->g->unsettle(); g->g->assemble_fixed_raw(n, host_raw); });
 }
 int lzb_grid_publish_level(lzb_grid* g, int level, const double* mats, const int32_t* n, int32_t p1) {
-    return guarded([&] { g->g->publish_level(level, mats, n, p1); });
+    return guarded([&] { g->g->unsettle(); g->g->publish_level(level, mats, n, p1); });
 }
 int lzb_grid_vertex_stencils(lzb_grid* g, int level, int require_payload, double* out) {
-    return guarded([&] { g->g->vertex_stencils(level, require_payload, out); });
+    return guarded([&] { g->g->unsettle(); g->g->vertex_stencils(level, require_payload, out); });
 }
 int lzb_scatter_row(const double* element16, int corner, double* stencil9) {
     if (corner < 0 || corner > 3) {
@@ -4341,21 +4452,21 @@ int lzb_scatter_row(const double* element16, int corner, double* stencil9) {
     return LZB_OK;
 }
 int lzb_grid_invalidate(lzb_grid* g) {
-    return guarded([&] { g->g->invalidate(); });
+    return guarded([&] { g->g->unsettle(); g->g->invalidate(); });
 }
 int lzb_grid_cell_arrays(lzb_grid* g, int level, void** op, void** p1, void** n, void** p3, void** epoch,
                          void** chg) {
-    return guarded([&] { g->g->cell_arrays(level, op, p1, n, p3, epoch, chg); });
+    return guarded([&] { g->g->unsettle(); g->g->cell_arrays(level, op, p1, n, p3, epoch, chg); });
 }
 int lzb_grid_assemble_fixed(lzb_grid* g, int n) {
-    return guarded([&] {
+    return guarded([&] { g->g->unsettle();
         g->g->assemble_fixed(n);
         g->g->sync_check();
     });
 }
 int lzb_grid_step(lzb_grid* g, lzb_cycle_report* out) { return guarded([&] { *out = g->g->step(); }); }
 int lzb_grid_vcycle(lzb_grid* g, int nu, lzb_cycle_report* out) {
-    return guarded([&] { *out = g->g->vcycle(nu); });
+    return guarded([&] { g->g->unsettle(); *out = g->g->vcycle(nu); });
 }
 int lzb_grid_run(lzb_grid* g, lzb_cycle_report* out, int cap, int* count) {
     return guarded([&] {
@@ -4365,34 +4476,34 @@ int lzb_grid_run(lzb_grid* g, lzb_cycle_report* out, int cap, int* count) {
     });
 }
 int lzb_grid_pass(lzb_grid* g, int which, double* value) {
-    return guarded([&] {
+    return guarded([&] { g->g->unsettle();
         double v = g->g->pass(which);
         if (value) *value = v;
     });
 }
 int lzb_grid_cycle(lzb_grid* g) { return static_cast<int>(g->g->cycle()); }
 int lzb_grid_vertices(lzb_grid* g, int level, int field, double* buf, int write) {
-    return guarded([&] { g->g->vertices(level, field, buf, write != 0); });
+    return guarded([&] { g->g->unsettle(); g->g->vertices(level, field, buf, write != 0); });
 }
 int lzb_grid_cells(lzb_grid* g, int level, double* ops, int32_t* p1, int32_t* n, int32_t* p3,
                    uint32_t* epoch) {
-    return guarded([&] { g->g->cells(level, ops, p1, n, p3, epoch); });
+    return guarded([&] { g->g->unsettle(); g->g->cells(level, ops, p1, n, p3, epoch); });
 }
 int lzb_grid_transfer(lzb_grid* g, int level, int cx, int cy, double* out64) {
-    return guarded([&] { g->g->transfer(level, cx, cy, out64); });
+    return guarded([&] { g->g->unsettle(); g->g->transfer(level, cx, cy, out64); });
 }
 int lzb_grid_publish_element(lzb_grid* g, int level, int cx, int cy, const double* m16, int n,
                              int32_t p1) {
-    return guarded([&] { g->g->publish_element(level, cx, cy, m16, n, p1); });
+    return guarded([&] { g->g->unsettle(); g->g->publish_element(level, cx, cy, m16, n, p1); });
 }
 int lzb_grid_adaptive_step(lzb_grid* g, int level, int cx, int cy) {
-    return guarded([&] { g->g->adaptive_step(level, cx, cy); });
+    return guarded([&] { g->g->unsettle(); g->g->adaptive_step(level, cx, cy); });
 }
 int lzb_grid_stats(lzb_grid* g, lzb_compression_stats* out) {
-    return guarded([&] { *out = g->g->stats(); });
+    return guarded([&] { g->g->unsettle(); *out = g->g->stats(); });
 }
 int lzb_grid_stream_image(lzb_grid* g, uint8_t* out, int64_t cap, int64_t* size) {
-    return guarded([&] {
+    return guarded([&] { g->g->unsettle();
         if (!out) {
             *size = g->g->image_size();
             return;
@@ -4401,43 +4512,43 @@ int lzb_grid_stream_image(lzb_grid* g, uint8_t* out, int64_t cap, int64_t* size)
     });
 }
 int lzb_grid_plane_arrays(lzb_grid* g, void** planes, void** cp3, int* width) {
-    return guarded([&] { g->g->plane_arrays(planes, cp3, width); });
+    return guarded([&] { g->g->unsettle(); g->g->plane_arrays(planes, cp3, width); });
 }
 int lzb_grid_desc_of(lzb_grid* g, lzb_grid_desc* out) {
-    return guarded([&] { *out = g->g->desc(); });
+    return guarded([&] { g->g->unsettle(); *out = g->g->desc(); });
 }
 int lzb_grid_info(lzb_grid* g, lzb_ctx** ctx, int* depth) {
-    return guarded([&] {
+    return guarded([&] { g->g->unsettle();
         if (ctx) *ctx = g->g->context();
         if (depth) *depth = g->g->depth();
     });
 }
 int lzb_grid_set_slab(lzb_grid* g, int v0, int v1) {
-    return guarded([&] { g->g->set_slab(v0, v1); });
+    return guarded([&] { g->g->unsettle(); g->g->set_slab(v0, v1); });
 }
 int lzb_grid_dist_phase(lzb_grid* g, int phase, int flags) {
-    return guarded([&] { g->g->dist_phase(phase, flags); });
+    return guarded([&] { g->g->unsettle(); g->g->dist_phase(phase, flags); });
 }
 int lzb_grid_dist_result_dev(lzb_grid* g, void** result) {
-    return guarded([&] { *result = g->g->dist_result_dev(); });
+    return guarded([&] { g->g->unsettle(); *result = g->g->dist_result_dev(); });
 }
 int lzb_grid_dist_result(lzb_grid* g, double* norm2, uint64_t* slots20) {
-    return guarded([&] { g->g->dist_result(norm2, slots20); });
+    return guarded([&] { g->g->unsettle(); g->g->dist_result(norm2, slots20); });
 }
 int lzb_grid_dist_report(lzb_grid* g, double norm2, const uint64_t* slots20, lzb_cycle_report* rep) {
-    return guarded([&] { *rep = g->g->dist_report(norm2, slots20); });
+    return guarded([&] { g->g->unsettle(); *rep = g->g->dist_report(norm2, slots20); });
 }
 int lzb_grid_assemble_stream(lzb_grid* g, int n, uint8_t* out, int64_t cap, int64_t* size, float* timeline) {
-    return guarded([&] { *size = g->g->assemble_stream(n, out, cap, timeline); });
+    return guarded([&] { g->g->unsettle(); *size = g->g->assemble_stream(n, out, cap, timeline); });
 }
 int lzb_grid_time_kernel(lzb_grid* g, int what, int reps, double* avg_ms) {
-    return guarded([&] { *avg_ms = g->g->time_kernel(what, reps); });
+    return guarded([&] { g->g->unsettle(); *avg_ms = g->g->time_kernel(what, reps); });
 }
 int lzb_grid_stream_load(lzb_grid* g, const uint8_t* in, int64_t size) {
-    return guarded([&] { g->g->load(in, size); });
+    return guarded([&] { g->g->unsettle(); g->g->load(in, size); });
 }
 int lzb_grid_save(lzb_grid* g, const char* path) {
-    return guarded([&] {
+    return guarded([&] { g->g->unsettle();
         auto img = g->g->image();
         std::ofstream f(path, std::ios::binary);
         if (!f) throw Error(LZB_ERR_IO, std::string("cannot open stream file for writing: ") + path);
@@ -4445,7 +4556,7 @@ int lzb_grid_save(lzb_grid* g, const char* path) {
     });
 }
 int lzb_grid_load(lzb_grid* g, const char* path) {
-    return guarded([&] {
+    return guarded([&] { g->g->unsettle();
         std::ifstream f(path, std::ios::binary);
         if (!f) throw Error(LZB_ERR_IO, std::string("cannot open stream file: ") + path);
         std::vector<uint8_t> buf((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
@@ -4454,7 +4565,7 @@ int lzb_grid_load(lzb_grid* g, const char* path) {
 }
 int64_t lzb_grid_pending(lzb_grid* g) { return g->g->pending(); }
 int lzb_grid_device_view(lzb_grid* g, int level, int field, void** ptr) {
-    return guarded([&] { *ptr = g->g->device_field(level, field); });
+    return guarded([&] { g->g->unsettle(); *ptr = g->g->device_field(level, field); });
 }
 
 }  // extern "C"

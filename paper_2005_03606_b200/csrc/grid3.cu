@@ -250,29 +250,30 @@ __device__ __forceinline__ double grf_sample(const double* __restrict__ Tp, int 
 // samples per row the geometric-sequence trick of accumulate3_grf saves no
 // exp), every loop unrolled, the sums in accumulate3's order with fused
 // multiply-adds. WRAP as grf_axis.
-template <int NS, bool WRAP>
+template <int NS, bool WRAP, bool ROLL = false>
 __device__ __forceinline__ void accumulate3_grf_direct(const Field3& F, double x0, double y0, double z0, double h,
                                                        const AxisTab3& T, Acc3& A) {
     const double inv = 1.0 / NS;
     const int np = F.n + 1;
-    GAx ax[NS], ay[NS], az[NS];
+    GAx ay[NS], az[NS];
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
-        ax[i] = grf_axis<WRAP>(x0 + (i + 0.5) * inv * h, F.n);
         ay[i] = grf_axis<WRAP>(y0 + (i + 0.5) * inv * h, F.n);
         az[i] = grf_axis<WRAP>(z0 + (i + 0.5) * inv * h, F.n);
     }
 #pragma unroll
     for (int q = 0; q < 9; ++q) A.yz[q] = A.xz[q] = A.xy[q] = 0.0;
-#pragma unroll
+    // ROLL: the x-sample loop stays a loop (half the code of the unrolled form)
+#pragma unroll(ROLL ? 1 : NS)
     for (int i = 0; i < NS; ++i) {
+        const GAx axi = grf_axis<WRAP>(x0 + (i + 0.5) * inv * h, F.n);
         double B[3] = {0.0, 0.0, 0.0}, Cc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
         for (int j = 0; j < NS; ++j) {
             double G = 0.0, Dz[3] = {0.0, 0.0, 0.0};
 #pragma unroll
             for (int k = 0; k < NS; ++k) {
-                const double e = grf_sample(F.grf_t, np, ax[i], ay[j], az[k]);
+                const double e = grf_sample(F.grf_t, np, axi, ay[j], az[k]);
                 G += e;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) Dz[c] = fma(e, T.s[k][c], Dz[c]);
@@ -793,8 +794,8 @@ __device__ __forceinline__ int code_record27(const double* sur, const Base3& B, 
 // code is dropped: a smaller kernel, fewer instruction-cache misses).
 // NS > 0 (GRF cells smaller than a table spacing): the samples per axis at
 // compile time, accumulate3_grf_direct; NS = 0: T.n samples, accumulate3.
-template <int KIND, int NS>
-__global__ void __launch_bounds__(128, 3) k_assemble3(Field3 Fin, int N, double h, AxisTab3 T, double delta_max,
+template <int KIND, int NS, int MINB = 3, bool ROLL = false>
+__global__ void __launch_bounds__(128, MINB) k_assemble3(Field3 Fin, int N, double h, AxisTab3 T, double delta_max,
                                                       int fixed_p3, double* __restrict__ op, Planes3 PL, int W,
                                                       int8_t* __restrict__ p3o, int32_t* __restrict__ no,
                                                       unsigned long long* stats, int* err, int* wide,
@@ -813,7 +814,7 @@ __global__ void __launch_bounds__(128, 3) k_assemble3(Field3 Fin, int N, double 
     double sur[27];
     {
         Acc3 A;
-        if (NS > 0) accumulate3_grf_direct<(NS > 0 ? NS : 1), false>(F, x0, y0, z0, h, T, A);
+        if (NS > 0) accumulate3_grf_direct<(NS > 0 ? NS : 1), false, ROLL>(F, x0, y0, z0, h, T, A);
         else accumulate3(F, x0, y0, z0, h, T, A);
         const double hn = h * (1.0 / T.n);
 #pragma unroll
@@ -1961,7 +1962,13 @@ public:
                            W_, p3_.p, n_.p, stats_.p, ctx_->err.p, wide_.p, cb, ce);
             };
             if (small && n == 1) go(k_assemble3<LZB_F3_GRF, 1>);
-            else if (small && n == 2) go(k_assemble3<LZB_F3_GRF, 2>);
+            else if (small && n == 2) {
+                static const int variant = std::getenv("LZB_ASM3_VARIANT") ? std::atoi(std::getenv("LZB_ASM3_VARIANT")) : 0;
+                if (variant == 1) go(k_assemble3<LZB_F3_GRF, 2, 4, false>);
+                else if (variant == 2) go(k_assemble3<LZB_F3_GRF, 2, 3, true>);
+                else if (variant == 3) go(k_assemble3<LZB_F3_GRF, 2, 4, true>);
+                else go(k_assemble3<LZB_F3_GRF, 2>);
+            }
             else if (F_.kind == LZB_F3_GRF) go(k_assemble3<LZB_F3_GRF, 0>);
             else go(k_assemble3<-1, 0>);
         }

@@ -1,6 +1,9 @@
 // kernels.cuh — declarations shared between the .cu translation units.
 #pragma once
 
+#include <future>
+#include <vector>
+
 #include "device.cuh"
 #include "engine.hpp"
 #include "integrate.cuh"
@@ -26,10 +29,20 @@ __constant__ double c_geo[64];
 void upload_constants();
 
 // Per-n integration tables (integrate.cuh), rebuilt on demand.
+struct HostParts {  // host-libm field parts of one (level, n): x and y tables
+    int n = 0, N = 0;
+    std::vector<double> x, y;
+};
 struct TableSet {
     DevBuf<double> fx, fy, seg, ktab, cxp, cyp;
     int n = 0, N = 0;
+    int reserve_n = 64;  // capacity (samples per axis) allocated at the first build
+    int centre_N = 0;    // level whose centre parts are uploaded
+    // the next rung's host tables, computed on a host thread while the GPU
+    // integrates the current rung (a p ladder knows its next n)
+    std::future<HostParts> ahead;
     void build(const lzb_field& f, int N, double h, int n, cudaStream_t s);
+    void prefetch(const lzb_field& f, int N, double h, int n);
     IntTables view() const { return IntTables{fx.p, fy.p, seg.p, ktab.p, cxp.p, cyp.p, n}; }
 };
 // Host-libm field parts of the N cells' n samples per axis (k_field_parts

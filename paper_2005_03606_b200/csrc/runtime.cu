@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "engine.hpp"
@@ -122,15 +123,30 @@ __global__ void k_ksub_table(int n, double* ktab) {
 
 void host_field_parts(const lzb_field& f, int N, double h, int n, int axis, double* out) {
     // the same arithmetic as k_field_parts (cell_box element.hpp:29-32, the
-    // sample element.hpp:44), the transcendentals from the host libm
+    // sample element.hpp:44), the transcendentals from the host libm; large
+    // tables (the upper rungs of the p ladder) are cut over a few host threads
     const double inv = 1.0 / n;
-    for (int c = 0; c < N; ++c) {
-        const double x0 = c * h;
-        for (int i = 0; i < n; ++i) {
-            const double x = x0 + (i + 0.5) * inv * h;
-            out[static_cast<int64_t>(c) * n + i] = axis == 0 ? field_xpart(f, x) : field_ypart(f, x);
+    auto rows = [&](int c0, int c1) {
+        for (int c = c0; c < c1; ++c) {
+            const double x0 = c * h;
+            for (int i = 0; i < n; ++i) {
+                const double x = x0 + (i + 0.5) * inv * h;
+                out[static_cast<int64_t>(c) * n + i] = axis == 0 ? field_xpart(f, x) : field_ypart(f, x);
+            }
         }
+    };
+    const int64_t total = static_cast<int64_t>(N) * n;
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int nt = static_cast<int>(std::min<int64_t>({8, hw ? hw : 1, total / 2048}));
+    if (nt <= 1) {
+        rows(0, N);
+        return;
     }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back(rows, static_cast<int>(static_cast<int64_t>(N) * t / nt),
+                        static_cast<int>(static_cast<int64_t>(N) * (t + 1) / nt));
+    for (auto& t : th) t.join();
 }
 
 void upload_field_parts(const lzb_field& f, int N, double h, int n, double* dx, double* dy, cudaStream_t s) {
@@ -144,33 +160,68 @@ void upload_field_parts(const lzb_field& f, int N, double h, int n, double* dx, 
 }
 
 void TableSet::build(const lzb_field& f, int N_, double h, int n_, cudaStream_t s) {
-    size_t nf = static_cast<size_t>(N_) * n_;
+    // capacity for the whole ladder at once (reserve_n: the grid's n_max, at
+    // least 64): a p doubling run rebuilds the tables at every rung, and each
+    // regrowth would cost a stream synchronisation and a cudaMalloc / cudaFree
+    const int ncap = std::max(n_, reserve_n);
+    const size_t nf = static_cast<size_t>(N_) * ncap;
     if (fx.n < nf) {
         LZB_CUDA(cudaStreamSynchronize(s));
         fx.alloc(nf);
         fy.alloc(nf);
     }
-    if (seg.n < static_cast<size_t>(kSeg) * n_) {
+    if (seg.n < static_cast<size_t>(kSeg) * ncap) {
         LZB_CUDA(cudaStreamSynchronize(s));
-        seg.alloc(static_cast<size_t>(kSeg) * n_);
+        seg.alloc(static_cast<size_t>(kSeg) * ncap);
     }
-    if (ktab.n < static_cast<size_t>(n_) * n_ * kKs) {
+    if (ktab.n < static_cast<size_t>(ncap) * ncap * kKs) {
         LZB_CUDA(cudaStreamSynchronize(s));
-        ktab.alloc(static_cast<size_t>(n_) * n_ * kKs);
+        ktab.alloc(static_cast<size_t>(ncap) * ncap * kKs);
     }
     if (cxp.n < static_cast<size_t>(N_)) {
         LZB_CUDA(cudaStreamSynchronize(s));
         cxp.alloc(N_);
         cyp.alloc(N_);
+        centre_N = 0;
     }
-    // cell-centre parts: the n = 1 sample, x0 + ((0+0.5)*1.0)*h (element.hpp:44);
+    // cell-centre parts: the n = 1 sample, x0 + ((0+0.5)*1.0)*h (element.hpp:44),
+    // once per level (field and level are fixed per TableSet owner);
     // sample parts at n -- host libm (see field_xpart)
-    upload_field_parts(f, N_, h, 1, cxp.p, cyp.p, s);
-    upload_field_parts(f, N_, h, n_, fx.p, fy.p, s);
+    if (centre_N != N_) {
+        upload_field_parts(f, N_, h, 1, cxp.p, cyp.p, s);
+        centre_N = N_;
+    }
+    HostParts hp;
+    if (ahead.valid()) hp = ahead.get();
+    if (hp.n != n_ || hp.N != N_) {
+        hp.x.resize(static_cast<size_t>(N_) * n_);
+        hp.y.resize(static_cast<size_t>(N_) * n_);
+        host_field_parts(f, N_, h, n_, 0, hp.x.data());
+        host_field_parts(f, N_, h, n_, 1, hp.y.data());
+    }
+    // pageable source: the calls return once the bytes are staged
+    LZB_CUDA(cudaMemcpyAsync(fx.p, hp.x.data(), hp.x.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    LZB_CUDA(cudaMemcpyAsync(fy.p, hp.y.data(), hp.y.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    LZB_CUDA(cudaStreamSynchronize(s));
     LZB_LAUNCH(k_seg_table, blocks_for(n_, 128), 128, 0, s, n_, seg.p);
     LZB_LAUNCH(k_ksub_table, blocks_for(static_cast<int64_t>(n_) * n_, 256), 256, 0, s, n_, ktab.p);
     n = n_;
     N = N_;
+}
+
+void TableSet::prefetch(const lzb_field& f, int N_, double h, int n_) {
+    if (ahead.valid()) ahead.get();  // a stale request (never more than one in flight)
+    const lzb_field fc = f;
+    ahead = std::async(std::launch::async, [fc, N_, h, n_] {
+        HostParts hp;
+        hp.n = n_;
+        hp.N = N_;
+        hp.x.resize(static_cast<size_t>(N_) * n_);
+        hp.y.resize(static_cast<size_t>(N_) * n_);
+        host_field_parts(fc, N_, h, n_, 0, hp.x.data());
+        host_field_parts(fc, N_, h, n_, 1, hp.y.data());
+        return hp;
+    });
 }
 
 // Arbitrary CellBox per cell: axis parts recomputed per sample (the

@@ -558,23 +558,33 @@ DEVLOOP = [("setup = checkerboard\nfield-seed = 1", "adafac-pi", "eager", "geome
            ("setup = sinusoid", "adafac-pi", "anarchic", "geometric", 200, 1e-10)]
 
 
+@pytest.mark.parametrize("devloop", [False, True])
 @pytest.mark.parametrize("f,solver,asm,transfer,cycles,target", DEVLOOP)
-def test_run_device_loop_matches_stepping(f, solver, asm, transfer, cycles, target):
-    """lzb_grid_run hands the quiescent cycles to the device-side loop (a
+def test_run_matches_stepping(f, solver, asm, transfer, cycles, target, devloop, monkeypatch):
+    """lzb_grid_run against stepping the same grid cycle by cycle with reads in
+    between (which keep the stepped grid on the full cycle: every step runs
+    the coarse pass and the stats). run() skips both once the hierarchy has
+    settled (a calm cycle whose coarse pass recomputed nothing), and with
+    LZB_DEVLOOP=1 hands the quiescent cycles to the device-side loop (a
     conditional WHILE graph, termination test on the device: solver.cpp:8-16,
-    421-444); stepping the same grid cycle by cycle from the host gives the
-    same reports (the same kernels, so the same bits) and the same state."""
+    421-444). Same kernels on the same data: same reports, same state."""
+    if devloop:
+        monkeypatch.setenv("LZB_DEVLOOP", "1")
+    else:
+        monkeypatch.delenv("LZB_DEVLOOP", raising=False)
     text = (f"{f}\ndepth = 4\nsolver = {solver}\nassembly = {asm}\ntransfer = {transfer}\nmax-cycles = {cycles}\n"
             f"omega = 0.6\nrhs = 1\nseed = 7\ntarget = {target}\n")
     k = port.parse_keys(text)
     d = port.desc_from_keys(k)
     g, h = lzb.Grid(d, 7), lzb.Grid(d, 7)
     rg = g.run()
+    monkeypatch.delenv("LZB_DEVLOOP", raising=False)
     if asm == "eager":
         h.eager_setup()
     rh = []
     while not rh or rh[-1]["status"] == lzb.T.CONTINUE:
         rh.append(h.step())
+        h.stats()  # a C-ABI call between steps: the stepped grid never takes the settled path
     assert len(rg) > 8
     assert_reports(rg, rh, rel=0.0)
     for lvl in range(5):
@@ -582,8 +592,8 @@ def test_run_device_loop_matches_stepping(f, solver, asm, transfer, cycles, targ
             assert np.array_equal(g.vertices(lvl, fld), h.vertices(lvl, fld)), (lvl, fld)
         assert np.array_equal(g.cells(lvl)["ops"], h.cells(lvl)["ops"])
         assert np.array_equal(g.cells(lvl)["epoch"], h.cells(lvl)["epoch"])
-    # the loop's reports share one wall-clock share (its cycles ran in one graph launch)
-    if asm == "eager":  # quiescent from the second cycle on (anarchic runs may keep tasks pending to the end)
+    assert g.stats().p3_histogram[:] == h.stats().p3_histogram[:]
+    if devloop and asm == "eager":  # the loop's cycles ran in one graph launch: one wall-clock share
         walls = [r["wall_seconds"] for r in rg[-4:]]
         assert len(set(walls)) == 1
     # and the grid carries on from the host afterwards

@@ -1,7 +1,8 @@
 """Device time per cycle of the 729^2 grid (BASELINE configs[1] smoother:
 adaFAC-PI, omega 0.6, p = 32 operators), CUDA events on the solve stream.
 LZB_NO_PDL=1 / LZB_NO_GRAPHS=1 switch off programmatic dependent launch / the
-CUDA graphs for comparison.
+CUDA graphs for comparison; LZB_SMALL_MAXN=9 keeps only levels up to 9^2 in the
+cluster kernels (the round-1 fusion).
 
 usage: python tools/cycle_probe.py [depth] [cycles]
 """
@@ -22,12 +23,14 @@ d = lzb.make_desc(depth=depth, field=lzb.field_sinusoid(0.9, 6.0), solver="adafa
                   rhs_kind="sinprod", max_cycles=10 ** 6, delta_max=1e-8)
 g = lzb.Grid(d, 1)
 g.assemble_fixed(32)
-for _ in range(3):
+for _ in range(12):  # the Galerkin hierarchy settles one level per cycle; then the settled cycles
     g.step()
+l0 = lzb.launch_count()
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 a.record(stream)
 for _ in range(cycles):
     r = g.step()
 b.record(stream)
 b.synchronize()
-print(f"depth {depth}: {a.elapsed_time(b) / cycles * 1e3:.1f} us per cycle, normalized {r['normalized']:.3e}")
+print(f"depth {depth}: {a.elapsed_time(b) / cycles * 1e3:.1f} us per cycle, {(lzb.launch_count() - l0) / cycles:.0f} "
+      f"launches per cycle, normalized {r['normalized']:.3e}")
