@@ -706,6 +706,14 @@ def run_ours(args, world, rank, local):
                                    ("delayed_deterministic", "anarchic", False, True),
                                    ("delayed_concurrent", "anarchic", True, True)):
         tts[label] = tts_solve(LEVEL, f, P, mode, conc, geo)
+    # the same eager solve with the quiescent cycles in the device-side loop (conditional
+    # WHILE / IF graph nodes, termination on the device): opt-in, measured beside the host loop
+    os.environ["LZB_DEVLOOP"] = "1"
+    try:
+        tts_solve(3, f, 4, "eager", False, False)
+        tts["eager_device_loop"] = tts_solve(LEVEL, f, P, "eager", False, False)
+    finally:
+        del os.environ["LZB_DEVLOOP"]
     tts["setup"] = (f"729^2 sinusoid eps, f = 2 pi^2 sin sin, adaFAC-PI omega 0.6, target 1e-10, delayed runs start "
                     f"from the geometric stencil (eps = 1), p doubling 1->{P} (C = 0), delta_max 1e-8; device "
                     f"timeline (CUDA events) incl. host round trips")
