@@ -12,6 +12,11 @@
 // levels are generated (parents in order, children z-major); operators are
 // class planes over the leaf index (value q of leaf i at q * nleaves + i).
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 #include <array>
 #include <cmath>
 #include <unordered_map>
@@ -234,6 +239,67 @@ __global__ void k4_new_vertices(LvA F, LvA C, const uint8_t* __restrict__ existe
         val += w * C.v[LZB_V_U][vidx3(nc, hx + ax, hy + ay, hz + az)];
     }
     F.v[LZB_V_U][vi] = val;
+}
+// ---- the leaf list on the device (shell selection, level boxes, re-refinement)
+struct Ball3 {
+    double c[3];
+};
+// distance range [lo, hi] from the ball's centre to the points of a box: the
+// host box_range's arithmetic (Tree3::box_range), operation for operation
+__device__ __forceinline__ void box_range_dev(const Ball3& B, double x0, double y0, double z0, double h, double& lo,
+                                              double& hi) {
+    const double b[3][2] = {{x0, x0 + h}, {y0, y0 + h}, {z0, z0 + h}};
+    double near2 = 0.0, far2 = 0.0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const double c = B.c[d];
+        const double q = fmin(fmax(c, b[d][0]), b[d][1]);
+        near2 += (q - c) * (q - c);
+        const double f = fmax(fabs(b[d][0] - c), fabs(b[d][1] - c));
+        far2 += f * f;
+    }
+    lo = sqrt(near2);
+    hi = sqrt(far2);
+}
+// flag = the leaf's box meets the shell rlo <= |x - centre| <= rhi
+__global__ void k4_shell_flags(const int4* __restrict__ leaves, int64_t n, LeafLevels HL, Ball3 B, double rlo,
+                               double rhi, uint8_t* __restrict__ flag) {
+    lzb_pdl_enter();
+    const int64_t t = gtid();
+    if (t >= n) return;
+    const int4 c = leaves[t];
+    const double h = HL.h[c.x];
+    double lo, hi;
+    box_range_dev(B, c.y * h, c.z * h, c.w * h, h, lo, hi);
+    flag[t] = (hi >= rlo && lo <= rhi) ? 1 : 0;
+}
+// per level the bounding box of its leaves' cell coordinates: bb[l] =
+// {min x, max x, min y, max y, min z, max z} (initialised to {INT_MAX, -1, ..})
+__global__ void k4_leaf_bbox(const int4* __restrict__ leaves, int64_t n, int* __restrict__ bb) {
+    lzb_pdl_enter();
+    __shared__ int sb[8 * 6];
+    if (threadIdx.x < 48) sb[threadIdx.x] = (threadIdx.x & 1) ? -1 : INT32_MAX;
+    __syncthreads();
+    for (int64_t t = gtid(); t < n; t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int4 c = leaves[t];
+        const int q[3] = {c.y, c.z, c.w};
+        // leaves of a warp mostly share the level and lie close: the atomics hit shared memory
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            atomicMin(&sb[c.x * 6 + 2 * d], q[d]);
+            atomicMax(&sb[c.x * 6 + 2 * d + 1], q[d]);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 48) {
+        if (threadIdx.x & 1) atomicMax(&bb[threadIdx.x], sb[threadIdx.x]);
+        else atomicMin(&bb[threadIdx.x], sb[threadIdx.x]);
+    }
+}
+__global__ void k4_iota(int32_t* __restrict__ p, int64_t n, int32_t first) {
+    lzb_pdl_enter();
+    const int64_t t = gtid();
+    if (t < n) p[t] = first + static_cast<int32_t>(t);
 }
 __global__ void k4_existed(LvA L, uint8_t* __restrict__ out) {
     lzb_pdl_enter();
@@ -548,6 +614,10 @@ public:
         n_leaves_ = static_cast<int64_t>(leaves_.size());
         dleaves_.alloc(n_leaves_);
         LZB_CUDA(cudaMemcpy(dleaves_.p, leaves_.data(), n_leaves_ * sizeof(int4), cudaMemcpyHostToDevice));
+        // the list lives on the device from here on; the host keeps its level-major
+        // prefix of leaves below lmax (the only ones a re-refinement can replace)
+        leaves_.resize(static_cast<size_t>(n_leaves_ - per_level_[lmax_]));
+        leaves_.shrink_to_fit();
         op_.alloc(static_cast<size_t>(n_leaves_) * kCls3);
         p3_.alloc(n_leaves_);
         n_.alloc(n_leaves_);
@@ -574,20 +644,27 @@ public:
     }
 
     // The interface shell: leaves whose box meets {x : | |x - centre| - radius | <= band}.
+    // the leaves meeting the shell | r - radius | <= band, in leaf order: flags
+    // by a kernel (box_range's arithmetic), the index list by a device select
     int64_t set_shell(double band) {
         if (!(band >= 0.0)) throw Error(LZB_ERR_INVALID, "shell band must be >= 0");
-        std::vector<int32_t> list;
-        for (int64_t i = 0; i < n_leaves_; ++i) {
-            const int4& c = leaves_[i];
-            const double h = HL_.h[c.x];
-            double lo, hi;
-            box_range(c.y * h, c.z * h, c.w * h, h, lo, hi);
-            if (hi >= rad_ - band && lo <= rad_ + band) list.push_back(static_cast<int32_t>(i));
-        }
-        n_shell_ = static_cast<int64_t>(list.size());
-        shell_.alloc(std::max<int64_t>(n_shell_, 1));
+        DevBuf<uint8_t> flag(static_cast<size_t>(std::max<int64_t>(n_leaves_, 1)));
+        DevBuf<int32_t> list(static_cast<size_t>(std::max<int64_t>(n_leaves_, 1))), cnt(1);
+        LZB_LAUNCH(k4_shell_flags, blocks_for(n_leaves_, 256), 256, 0, s_, dleaves_.p, n_leaves_, HL_, ball(),
+                   rad_ - band, rad_ + band, flag.p);
+        cub::CountingInputIterator<int32_t> idx(0);
+        size_t tb = 0;
+        LZB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, idx, flag.p, list.p, cnt.p, static_cast<int>(n_leaves_), s_));
+        DevBuf<unsigned char> tmp(tb);
+        LZB_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, idx, flag.p, list.p, cnt.p, static_cast<int>(n_leaves_), s_));
+        int32_t k = 0;
+        LZB_CUDA(cudaMemcpyAsync(&k, cnt.p, sizeof k, cudaMemcpyDeviceToHost, s_));
+        LZB_CUDA(cudaStreamSynchronize(s_));
+        n_shell_ = k;
+        shell_.alloc(static_cast<size_t>(std::max<int64_t>(n_shell_, 1)));
         if (n_shell_)
-            LZB_CUDA(cudaMemcpy(shell_.p, list.data(), n_shell_ * sizeof(int32_t), cudaMemcpyHostToDevice));
+            LZB_CUDA(cudaMemcpyAsync(shell_.p, list.p, n_shell_ * sizeof(int32_t), cudaMemcpyDeviceToDevice, s_));
+        LZB_CUDA(cudaStreamSynchronize(s_));
         return n_shell_;
     }
 
@@ -648,7 +725,7 @@ public:
             for (int64_t i = 0; i < count; ++i) p3[i] = q[i];
         }
         if (n) LZB_CUDA(cudaMemcpy(n, n_.p + first, count * sizeof(int32_t), cudaMemcpyDeviceToHost));
-        if (lxyz) std::memcpy(lxyz, leaves_.data() + first, count * sizeof(int4));
+        if (lxyz) LZB_CUDA(cudaMemcpy(lxyz, dleaves_.p + first, count * sizeof(int4), cudaMemcpyDeviceToHost));
     }
 
     // ------------------------------------------------ the cycle on the tree
@@ -698,14 +775,13 @@ public:
         // per level the bounding box of its existing cells: its leaves' box
         // joined with the box of the parents of the level below (one pass
         // over the leaves, then finest to coarsest)
-        std::vector<std::array<int, 6>> cb(D + 2, std::array<int, 6>{INT32_MAX, -1, INT32_MAX, -1, INT32_MAX, -1});
-        for (const int4& c : leaves_) {
-            auto& b = cb[c.x];
-            const int q[3] = {c.y, c.z, c.w};
-            for (int d = 0; d < 3; ++d) {
-                b[2 * d] = std::min(b[2 * d], q[d]);
-                b[2 * d + 1] = std::max(b[2 * d + 1], q[d]);
-            }
+        std::vector<std::array<int, 6>> cb(std::max(D + 2, 8), std::array<int, 6>{INT32_MAX, -1, INT32_MAX, -1, INT32_MAX, -1});
+        {
+            DevBuf<int> bb(48);
+            LZB_CUDA(cudaMemcpyAsync(bb.p, cb.data(), 48 * sizeof(int), cudaMemcpyHostToDevice, s_));
+            LZB_LAUNCH(k4_leaf_bbox, 148 * 8, 256, 0, s_, dleaves_.p, n_leaves_, bb.p);
+            LZB_CUDA(cudaMemcpyAsync(cb.data(), bb.p, 48 * sizeof(int), cudaMemcpyDeviceToHost, s_));
+            LZB_CUDA(cudaStreamSynchronize(s_));
         }
         for (int l = D - 1; l >= 0; --l)
             if (cb[l + 1][1] >= 0)
@@ -775,6 +851,16 @@ public:
         if (!(radius >= rad_)) throw Error(LZB_ERR_INVALID, "the refinement ball only grows (no coarsening, mesh.hpp:55)");
         if (n < 1 || n > kMaxN3) throw Error(LZB_ERR_INVALID, "3D sub-samples per axis must be in 1..16");
         const bool cyc = !A_.empty();
+        static const bool tr = std::getenv("LZB_TRACE") != nullptr;
+        auto t_prev = std::chrono::steady_clock::now();
+        auto mark = [&](const char* what) {
+            if (!tr) return;
+            cudaStreamSynchronize(s_);
+            const auto t = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "[lzb] refine: %s %.1f ms\n", what,
+                         std::chrono::duration<double, std::milli>(t - t_prev).count());
+            t_prev = t;
+        };
         std::vector<DevBuf<uint8_t>> existed(cyc ? lmax_ + 1 : 0);
         if (cyc)
             for (int l = 0; l <= lmax_; ++l) {
@@ -784,12 +870,17 @@ public:
         // the new leaf set, level-major, from the old one: a leaf that meets the
         // grown ball below lmax is replaced by its refinement (build()'s rule with
         // the new radius: the ball only grows, so every other leaf survives)
-        const int64_t n_old = n_leaves_;
+        // Only leaves below lmax can be replaced, and they are the level-major
+        // prefix the host keeps (leaves_); the old level-lmax block (97 % of the
+        // leaves of the BASELINE tree) moves device to device, behind the new
+        // level-lmax leaves the replaced ones generate -- the order a walk over
+        // the whole old list would give.
+        const int64_t n_old = n_leaves_, n_lo_old = static_cast<int64_t>(leaves_.size()), n_top_old = n_old - n_lo_old;
         rad_ = radius;
         std::vector<std::vector<int4>> per(8);
         std::vector<std::vector<int32_t>> per_src(8);
         std::vector<int4> stack;
-        for (int64_t i = 0; i < n_old; ++i) {
+        for (int64_t i = 0; i < n_lo_old; ++i) {
             const int4 c = leaves_[i];
             double lo, hi;
             box_range(c.y * HL_.h[c.x], c.z * HL_.h[c.x], c.w * HL_.h[c.x], HL_.h[c.x], lo, hi);
@@ -818,19 +909,33 @@ public:
                             stack.push_back(make_int4(q.x + 1, 3 * q.y + dx, 3 * q.z + dy, 3 * q.w + dz));
             }
         }
-        leaves_.clear();
+        mark("existed flags + host walk of the leaves below lmax");
+        // head = the new leaves below lmax + the generated level-lmax leaves
+        std::vector<int4> head;
         std::vector<int32_t> src, fresh;
-        for (int l = 0; l < 8; ++l) {
-            per_level_[l] = static_cast<int64_t>(per[l].size());
-            leaves_.insert(leaves_.end(), per[l].begin(), per[l].end());
+        for (int l = 0; l <= lmax_; ++l) {
+            per_level_[l] = static_cast<int64_t>(per[l].size()) + (l == lmax_ ? n_top_old : 0);
+            head.insert(head.end(), per[l].begin(), per[l].end());
             src.insert(src.end(), per_src[l].begin(), per_src[l].end());
         }
-        n_leaves_ = static_cast<int64_t>(leaves_.size());
-        if (leaves_.size() > static_cast<size_t>(INT32_MAX)) throw Error(LZB_ERR_RESOURCE, "too many leaves");
-        for (int64_t i = 0; i < n_leaves_; ++i)
+        const int64_t n_head = static_cast<int64_t>(head.size());
+        leaves_.assign(head.begin(), head.end() - static_cast<int64_t>(per[lmax_].size()));
+        n_leaves_ = n_head + n_top_old;
+        if (n_leaves_ > static_cast<int64_t>(INT32_MAX)) throw Error(LZB_ERR_RESOURCE, "too many leaves");
+        for (int64_t i = 0; i < n_head; ++i)
             if (src[i] < 0) fresh.push_back(static_cast<int32_t>(i));
         DevBuf<int32_t> dsrc(n_leaves_);
-        LZB_CUDA(cudaMemcpyAsync(dsrc.p, src.data(), src.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s_));
+        DevBuf<int4> dl2(n_leaves_);
+        if (n_head) {
+            LZB_CUDA(cudaMemcpyAsync(dsrc.p, src.data(), n_head * sizeof(int32_t), cudaMemcpyHostToDevice, s_));
+            LZB_CUDA(cudaMemcpyAsync(dl2.p, head.data(), n_head * sizeof(int4), cudaMemcpyHostToDevice, s_));
+        }
+        if (n_top_old) {
+            LZB_LAUNCH(k4_iota, blocks_for(n_top_old, 256), 256, 0, s_, dsrc.p + n_head, n_top_old,
+                       static_cast<int32_t>(n_lo_old));
+            LZB_CUDA(cudaMemcpyAsync(dl2.p + n_head, dleaves_.p + n_lo_old, n_top_old * sizeof(int4),
+                                     cudaMemcpyDeviceToDevice, s_));
+        }
         DevBuf<double> op2(static_cast<size_t>(n_leaves_) * kCls3);
         DevBuf<int8_t> p32(n_leaves_);
         DevBuf<int32_t> n2(n_leaves_);
@@ -840,8 +945,8 @@ public:
         op_ = std::move(op2);
         p3_ = std::move(p32);
         n_ = std::move(n2);
-        dleaves_.alloc(n_leaves_);
-        LZB_CUDA(cudaMemcpy(dleaves_.p, leaves_.data(), n_leaves_ * sizeof(int4), cudaMemcpyHostToDevice));
+        dleaves_ = std::move(dl2);
+        mark("upload + gather of the leaf arrays");
         n_shell_ = 0;  // the shell list indexed the old leaves
         if (!fresh.empty()) {  // the new leaves: assembled now
             shell_.alloc(fresh.size());
@@ -850,11 +955,14 @@ public:
             assemble(n, true);
             n_shell_ = 0;
         }
+        mark("assembly of the new leaves");
         if (cyc) {
             setup_levels();
+            mark("setup_levels");
             for (int l = 1; l <= lmax_; ++l)  // coarse levels first: interpolation chains through
                 LZB_LAUNCH(k4_new_vertices, vgA(l), 128, 0, s_, lv(l), lv(l - 1), existed[l].p);
             refresh_ops();
+            mark("new vertices + refresh_ops");
             finish_cycle();
             for (int l = 0; l <= lmax_; ++l)
                 LZB_LAUNCH(k4_load, vgA(l), 128, 0, s_, lv(l), rhs_scale_, A_[l].h * A_[l].h * A_[l].h / 8.0);
@@ -986,6 +1094,7 @@ private:
         for (int l = 1; l <= lmax_; ++l) LZB_LAUNCH(k4_hanging, vgA(l), 128, 0, s_, lv(l), lv(l - 1));
     }
 
+    Ball3 ball() const { return Ball3{{cen_[0], cen_[1], cen_[2]}}; }
     // distance range [lo, hi] from the sphere centre to the points of a box
     void box_range(double x0, double y0, double z0, double h, double& lo, double& hi) const {
         const double b[3][2] = {{x0, x0 + h}, {y0, y0 + h}, {z0, z0 + h}};
@@ -1037,7 +1146,7 @@ private:
     double cen_[3] = {0.5, 0.5, 0.5}, rad_ = 0.0;
     Field3 F_{};
     LeafLevels HL_{};
-    std::vector<int4> leaves_;
+    std::vector<int4> leaves_;  // host copy of the level-major prefix: the leaves below lmax
     int64_t per_level_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int64_t n_leaves_ = 0, n_shell_ = 0;
     DevBuf<double> table_, op_;
