@@ -572,8 +572,11 @@ def run_ours(args, world, rank, local):
     # adaFAC-PI cycles; under torchrun the cycle runs z-slab distributed (NCCL)
     c5 = {"grid": "729^3 (depth 6), 387,420,489 cells", "eps": "exp(GRF), 64^3 periodic table, ell 0.05, sigma^2 1",
           "p": 2}
-    g5 = lzb.Grid3(6, lzb.field3_grf(lzb.grf_table(1, 64, 0.05, 1.0)), delta_max=1e-8, ctx=ctx)
     import torch.distributed as tdist5
+    # under torchrun each rank stores only its z-slab's leaf operators (+ one halo layer)
+    g5 = lzb.Grid3(6, lzb.field3_grf(lzb.grf_table(1, 64, 0.05, 1.0)), delta_max=1e-8, ctx=ctx,
+                   slab=(rank, world) if tdist5.is_initialized() else None)
+    c5["leaf_operator_bytes_per_rank"] = g5.leaf_storage()[0]
     if tdist5.is_initialized():
         # z-slab sharded assembly (each rank its leaf planes + its level-5 Galerkin
         # planes, one NCCL exchange of those), then the slab-distributed cycle: the

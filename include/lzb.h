@@ -246,6 +246,19 @@ int lzb_grid3_create(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_
  * LZB_ERR_RESOURCE. Restated 3D form of stream.cpp:82-111 + solver.cpp:145-175. */
 int lzb_grid3_create_planes(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3,
                             int plane_width, lzb_grid3** out);
+/* The same storing only the leaf operators of cell layers [cz0, cz1) (-1, -1:
+ * all): a z-slab window. Such a grid runs the plane-range assembly calls and
+ * the distributed cycle (lzb_grid3_dist_*); the one-GPU cycle, which reads
+ * every leaf, is rejected (LZB_ERR_INVALID). lzb_grid3_create_slab picks the
+ * window of slab `slab` of `nslabs` of the z-slab plan (csrc/dist.cpp): the
+ * leaf operators, 3/4 of a 729^3 grid's memory, then scale as 1/nslabs
+ * (the reference is shared-memory only). */
+int lzb_grid3_create_window(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3,
+                            int plane_width, int cz0, int cz1, lzb_grid3** out);
+int lzb_grid3_create_slab(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3,
+                          int plane_width, int nslabs, int slab, lzb_grid3** out);
+/* resident bytes of the leaf operator storage and the stored layer window */
+int lzb_grid3_leaf_storage(lzb_grid3* g, int64_t* bytes, int* cz0, int* cz1);
 int lzb_grid3_destroy(lzb_grid3* g);
 int lzb_grid3_assemble_fixed(lzb_grid3* g, int n);
 int lzb_grid3_stats(lzb_grid3* g, lzb_compression_stats* out);

@@ -128,6 +128,11 @@ def lib():
         L.lzb_integrate_elements3.argtypes = [vp, C.POINTER(T.Field3), i64, vp, vp, vp, vp, vp, vp]
         L.lzb_grid3_create.argtypes = [vp, C.c_int, C.POINTER(T.Field3), C.c_double, C.c_int, C.POINTER(vp)]
         L.lzb_grid_assemble_stream.argtypes = [vp, C.c_int, vp, i64, C.POINTER(i64), vp]
+        L.lzb_grid3_create_slab.argtypes = [vp, C.c_int, C.POINTER(T.Field3), C.c_double, C.c_int, C.c_int, C.c_int,
+                                            C.c_int, C.POINTER(vp)]
+        L.lzb_grid3_create_window.argtypes = [vp, C.c_int, C.POINTER(T.Field3), C.c_double, C.c_int, C.c_int,
+                                              C.c_int, C.c_int, C.POINTER(vp)]
+        L.lzb_grid3_leaf_storage.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.lzb_grid3_create_planes.argtypes = [vp, C.c_int, C.POINTER(T.Field3), C.c_double, C.c_int, C.c_int,
                                                C.POINTER(vp)]
         L.lzb_grid3_destroy.argtypes = [vp]
@@ -227,6 +232,7 @@ class Context:
     def comm_init(self, unique_id: bytes, nranks: int, rank: int):
         """The context's NCCL communicator for the C++ slab data plane
         (unique_id from nccl_unique_id() on rank 0, shared by the launcher)."""
+        _torch_nccl_first()
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         _check(lib().lzb_ctx_comm_init(self.h, buf, nranks, rank))
 
@@ -236,7 +242,19 @@ class Context:
         return r.value, n.value
 
 
+def _torch_nccl_first():
+    # liblzb.so loads NCCL at run time by soname (libnccl.so.2), preferring a copy the
+    # process already holds. When torch is installed its bundled NCCL must be that
+    # copy: loading the system library first would make a later `import torch`
+    # resolve libtorch_cuda.so against the wrong version.
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
 def nccl_unique_id() -> bytes:
+    _torch_nccl_first()
     buf = (C.c_uint8 * 128)()
     _check(lib().lzb_nccl_unique_id(buf))
     return bytes(buf)
@@ -793,15 +811,28 @@ class Grid3:
     """Leaves of a regular 3D grid (3^depth cells per axis): fixed-p assembly
     with the 64-entry record coding (lzb_grid3_*)."""
 
-    def __init__(self, depth, field, delta_max=1e-8, fixed_p3=0, plane_width=0, ctx: Context | None = None):
+    def __init__(self, depth, field, delta_max=1e-8, fixed_p3=0, plane_width=0, ctx: Context | None = None,
+                 slab: tuple[int, int] | None = None):
+        """slab = (rank, world): store only the leaf operators of that z-slab's
+        layers (lzb_grid3_create_slab); such a grid runs the distributed cycle."""
         self.ctx = ctx or default_context()
         self.depth, self.field = depth, field
         self.N = 3 ** depth
         self.plane_width = plane_width
         h = C.c_void_p()
-        _check(lib().lzb_grid3_create_planes(self.ctx.h, depth, C.byref(field), delta_max, fixed_p3, plane_width,
-                                             C.byref(h)))
+        if slab is None:
+            _check(lib().lzb_grid3_create_planes(self.ctx.h, depth, C.byref(field), delta_max, fixed_p3, plane_width,
+                                                 C.byref(h)))
+        else:
+            _check(lib().lzb_grid3_create_slab(self.ctx.h, depth, C.byref(field), delta_max, fixed_p3, plane_width,
+                                               slab[1], slab[0], C.byref(h)))
         self.h = h
+
+    def leaf_storage(self):
+        """(resident bytes of the leaf operators, first and end stored cell layer)"""
+        b, z0, z1 = C.c_int64(), C.c_int(), C.c_int()
+        _check(lib().lzb_grid3_leaf_storage(self.h, C.byref(b), C.byref(z0), C.byref(z1)))
+        return b.value, z0.value, z1.value
 
     def assemble_planes(self, n, cz0, cz1):
         _check(lib().lzb_grid3_assemble_planes(self.h, n, cz0, cz1))

@@ -558,6 +558,21 @@ int lzb_grid_dist_assemble_loopback(lzb_grid* const* slabs, int nslabs, int n) {
     });
 }
 
+int lzb_grid3_create_slab(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3,
+                          int plane_width, int nslabs, int slab, lzb_grid3** out) {
+    return guarded([&] {
+        if (depth < 1 || depth > 6) throw Error(LZB_ERR_INVALID, "slab grids need depth in 1..6");
+        if (nslabs < 1 || slab < 0 || slab >= nslabs) throw Error(LZB_ERR_INVALID, "bad slab / nslabs");
+        int N = 1;
+        for (int i = 0; i < depth; ++i) N *= 3;
+        const Slab s = slab_of(N, nslabs, slab);
+        // the leaf cell layers the slab's kernels read: its vertex planes' cells
+        // and one layer below (residual, Jacobi diagonal); its level-(D-1)
+        // Galerkin planes' children lie inside
+        check(lzb_grid3_create_window(ctx, depth, f, delta_max, fixed_p3, plane_width, std::max(s.v0 - 1, 0),
+                                      std::min(s.v1, N), out));
+    });
+}
 int lzb_grid3_dist_cycle(lzb_grid3* g, lzb_cycle_report* out) {
     return guarded([&] {
         std::vector<GridRef> s{GridRef::of(g)};

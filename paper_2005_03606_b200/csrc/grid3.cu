@@ -448,10 +448,13 @@ struct Base3 {
 // padded to xp (a multiple of 16: every row starts 16-byte aligned). nc is the
 // storage size of one plane (N (N + 1) xp); a cell's storage index is
 // plane_sidx of its linear index.
-__host__ __device__ __forceinline__ int64_t plane_sidx(int64_t c, int N, int xp) {
+// woff: the storage index of the first stored cell layer (a z-slab window of
+// the leaf level: a rank of the slab decomposition holds only the layers its
+// kernels read, Grid3's wz0_ .. wz1_)
+__host__ __device__ __forceinline__ int64_t plane_sidx(int64_t c, int N, int xp, int64_t woff = 0) {
     if (!xp) return c;
     const int64_t t = c / N;
-    return ((t / N) * (N + 1) + t % N + 1) * xp + c % N + 1;
+    return ((t / N) * (N + 1) + t % N + 1) * xp + c % N + 1 - woff;
 }
 struct Planes3 {
     uint8_t* base;  // piece arrays back to back, largest piece first
@@ -460,6 +463,7 @@ struct Planes3 {
     double h;
     double s1[3];  // seg_int classes of the n = 1 sub-interval
     int N, xp;     // cells per axis, padded x extent (0: linear storage)
+    int64_t woff;  // storage index of the window's first cell layer (plane_sidx)
 };
 
 // c: the cell's storage index (plane_sidx)
@@ -512,17 +516,18 @@ struct Src64 {
     const double* op;
     int64_t nc;      // storage elements per class plane
     int N = 0, xp = 0;  // padded leaf storage (plane_sidx); 0: linear
+    int64_t woff = 0;   // leaf window offset (plane_sidx)
     struct Raw {
         double v[27];
     };
-    __device__ __forceinline__ double at(int64_t c, int q) const { return __ldg(op + q * nc + plane_sidx(c, N, xp)); }
+    __device__ __forceinline__ double at(int64_t c, int q) const { return __ldg(op + q * nc + plane_sidx(c, N, xp, woff)); }
     __device__ __forceinline__ void load27(int64_t c, double* v) const {
-        const int64_t s = plane_sidx(c, N, xp);
+        const int64_t s = plane_sidx(c, N, xp, woff);
 #pragma unroll
         for (int q = 0; q < 27; ++q) v[q] = __ldg(op + q * nc + s);
     }
     __device__ __forceinline__ void fetch(int64_t c, Raw& r) const {
-        const int64_t s = plane_sidx(c, N, xp);
+        const int64_t s = plane_sidx(c, N, xp, woff);
 #pragma unroll
         for (int q = 0; q < 27; ++q) r.v[q] = __ldg(op + q * nc + s);
     }
@@ -541,7 +546,7 @@ struct SrcComp {
         double e;
     };
     __device__ __forceinline__ void fetch(int64_t c, Raw& r) const {
-        const int64_t sc = plane_sidx(c, P.N, P.xp);
+        const int64_t sc = plane_sidx(c, P.N, P.xp, P.woff);
 #pragma unroll
         for (int q = 0; q < 27; ++q) r.w[q] = static_cast<Word>(plane_load3<W>(P, sc, q));
         r.e = __ldg(P.ec + sc);
@@ -572,14 +577,14 @@ struct SrcComp {
         for (int q = 0; q < 27; ++q) v[q] = B(q / 9, (q / 3) % 3, q % 3) + dec(r.w[q]);
     }
     __device__ __forceinline__ double at(int64_t c, int q) const {  // one class value
-        const int64_t sc = plane_sidx(c, P.N, P.xp);
+        const int64_t sc = plane_sidx(c, P.N, P.xp, P.woff);
         const Base3 B(__ldg(P.ec + sc), P.s1, P.h);
         return B(q / 9, (q / 3) % 3, q % 3) + dec(static_cast<Word>(plane_load3<W>(P, sc, q)));
     }
     static constexpr int kMinBlocks = 1;
     __device__ __forceinline__ void load27(int64_t c, double* v) const {
         unsigned long long w[27];
-        const int64_t sc = plane_sidx(c, P.N, P.xp);
+        const int64_t sc = plane_sidx(c, P.N, P.xp, P.woff);
 #pragma unroll
         for (int q = 0; q < 27; ++q) w[q] = plane_load3<W>(P, sc, q);
         const Base3 B(__ldg(P.ec + sc), P.s1, P.h);
@@ -806,7 +811,7 @@ __global__ void __launch_bounds__(128, MINB) k_assemble3(Field3 Fin, int N, doub
     const int64_t c = cbeg + gtid();  // cells [cbeg, cend): whole z planes
     if (c >= cend) return;
     const int cx = static_cast<int>(c % N), cy = static_cast<int>((c / N) % N), cz = static_cast<int>(c / N / N);
-    const int64_t nc = PL.nc, sc = plane_sidx(c, PL.N, PL.xp);  // storage of the planes
+    const int64_t nc = PL.nc, sc = plane_sidx(c, PL.N, PL.xp, PL.woff);  // storage of the planes
     const double x0 = cx * h, y0 = cy * h, z0 = cz * h;
     const double e = NS > 0 ? grf_centre<false>(F, x0, y0, z0, h) : centre_eps3(F, x0, y0, z0, h);
     const Base3 B(e, PL.s1, h);  // A(n=1): eps(centre) * unit stiffness
@@ -1113,6 +1118,7 @@ __global__ void __launch_bounds__(kRzX * kRzY, Src::kMinBlocks) k3_residual_z(Lv
 struct TmaMaps {
     CUtensorMap piece[3];  // plane pieces, largest first (FP64: piece 0 = the doubles)
     CUtensorMap ec;        // eps(centre) (compressed planes)
+    int z0;                // first stored cell layer (tensor z = cell layer - z0)
 };
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -1254,10 +1260,11 @@ __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_tma(Lv3 F, const _
         mbar_expect(bar, bytes);
         if (cells) {
             // storage x / y of cell (X0 - 1, Y0 - 1) are X0 / Y0 (the leading pad)
-            tma_load_4d(pc0(st), &M.piece[0], X0 & ~(16 / e0 - 1), Y0, cz, 0, bar);
-            if (e1) tma_load_4d(pc1(st), &M.piece[1], X0 & ~(16 / (e1 ? e1 : 1) - 1), Y0, cz, 0, bar);
-            if (e2) tma_load_4d(pc2(st), &M.piece[2], X0 & ~(16 / (e2 ? e2 : 1) - 1), Y0, cz, 0, bar);
-            if (W) tma_load_3d(sec(st), &M.ec, X0 & ~1, Y0, cz, bar);
+            const int tz = cz - M.z0;  // the leaf planes' tensors start at the window's first layer
+            tma_load_4d(pc0(st), &M.piece[0], X0 & ~(16 / e0 - 1), Y0, tz, 0, bar);
+            if (e1) tma_load_4d(pc1(st), &M.piece[1], X0 & ~(16 / (e1 ? e1 : 1) - 1), Y0, tz, 0, bar);
+            if (e2) tma_load_4d(pc2(st), &M.piece[2], X0 & ~(16 / (e2 ? e2 : 1) - 1), Y0, tz, 0, bar);
+            if (W) tma_load_3d(sec(st), &M.ec, X0 & ~1, Y0, tz, bar);
             tma_load_3d(su(st), &VM.u, ux0, uy0, cz + 1, bar);  // the layer's upper vertex plane
             tma_load_3d(suh(st), &VM.uh, ux0, uy0, cz + 1, bar);
         }
@@ -1909,7 +1916,14 @@ Field3 to_device(const lzb_field3& f, DevBuf<double>& table) {
 
 class Grid3 {
 public:
-    Grid3(lzb_ctx* ctx, int depth, const lzb_field3& f, double delta_max, int fixed_p3, int plane_width = 0)
+    // [cz0, cz1): the leaf cell layers whose operators this grid stores (-1:
+    // all). A rank of the z-slab decomposition stores the layers its residual,
+    // diagonal and level-(D-1) Galerkin kernels read -- [max(v0 - 1, 0),
+    // min(v1, N)) for vertex planes [v0, v1) -- so the leaf operators, 3/4 of
+    // the memory of a 729^3 grid, scale as 1/ranks. Such a grid
+    // runs the distributed cycle and the plane-range assembly calls only.
+    Grid3(lzb_ctx* ctx, int depth, const lzb_field3& f, double delta_max, int fixed_p3, int plane_width = 0,
+          int cz0 = -1, int cz1 = -1)
         : ctx_(ctx), D_(depth), fixed_(fixed_p3), W_(plane_width), delta_(delta_max) {
         if (depth < 0 || depth > 6) throw Error(LZB_ERR_INVALID, "3D depth must be in 0..6");
         if (fixed_p3 != 0 && (fixed_p3 < 2 || fixed_p3 > 8)) throw Error(LZB_ERR_INVALID, "fixed_p3 must be 0 or 2..8");
@@ -1923,7 +1937,11 @@ public:
         for (int i = 0; i < depth; ++i) N_ *= 3;
         nc_ = static_cast<int64_t>(N_) * N_ * N_;
         xp_ = (N_ + 1 + 15) / 16 * 16;
-        ncs_ = static_cast<int64_t>(N_) * (N_ + 1) * xp_;
+        wz0_ = cz0 < 0 ? 0 : cz0;
+        wz1_ = cz1 < 0 ? N_ : cz1;
+        if (wz0_ < 0 || wz1_ > N_ || wz0_ >= wz1_) throw Error(LZB_ERR_INVALID, "bad leaf layer window");
+        ncs_ = static_cast<int64_t>(wz1_ - wz0_) * (N_ + 1) * xp_;
+        woff_ = static_cast<int64_t>(wz0_) * (N_ + 1) * xp_;
         h_ = std::pow(1.0 / 3, depth);
         F_ = to_device(f, table_);
         if (W_ == 0) {
@@ -1943,13 +1961,33 @@ public:
         LZB_CUDA(cudaStreamSynchronize(s_));
     }
 
-    void assemble_fixed(int n) { assemble_planes(n, 0, N_); }
+    bool windowed() const { return wz0_ != 0 || wz1_ != N_; }
+    void need_whole(const char* what) const {
+        if (windowed())
+            throw Error(LZB_ERR_INVALID, std::string(what) + ": this grid stores a z-slab window of the leaf operators; "
+                                                             "it runs the distributed cycle and plane-range calls");
+    }
+    void need_layers(int z0, int z1, const char* what) const {
+        if (z0 < wz0_ || z1 > wz1_)
+            throw Error(LZB_ERR_INVALID, std::string(what) + ": leaf cell layers outside the stored window");
+    }
+    // resident bytes of the leaf operator storage (the class planes or plane words + eps centre)
+    int64_t leaf_storage_bytes() const {
+        return W_ == 0 ? static_cast<int64_t>(op_.bytes()) : static_cast<int64_t>(planes_.bytes() + ec_.bytes());
+    }
+    void leaf_window(int* z0, int* z1) const {
+        *z0 = wz0_;
+        *z1 = wz1_;
+    }
+
+    void assemble_fixed(int n) { assemble_planes(n, wz0_, wz1_); }  // every stored layer
 
     // Fixed-p assembly of the leaf cells in z planes [cz0, cz1) (a z-slab of
     // the distributed assembly; cells are independent, no exchange).
     void assemble_planes(int n, int cz0, int cz1) {
         if (n < 1 || n > kMaxN3) throw Error(LZB_ERR_INVALID, "3D sub-samples per axis must be in 1..16");
         if (cz0 < 0 || cz1 > N_ || cz0 > cz1) throw Error(LZB_ERR_INVALID, "bad z plane range");
+        if (cz1 > cz0) need_layers(cz0, cz1, "assemble_planes");
         ops_dirty_ = true;
         leaf_diag_dirty_ = true;
         const AxisTab3 T = axis_tab3(n);
@@ -1985,6 +2023,7 @@ public:
         const int64_t cb = static_cast<int64_t>(pz0) * N * N, ce = static_cast<int64_t>(pz1) * N * N;
         if (ce <= cb) return;
         if (level + 1 == D_) {
+            need_layers(3 * pz0, 3 * pz1, "galerkin_planes");
             leaf_cls([&](auto S) {
                 LZB_LAUNCH(k3_galerkin<decltype(S)>, blocks_for(ce - cb, 256), 256, 0, s_, L3_[level].op.p, S, N,
                            cb, ce);
@@ -2042,6 +2081,8 @@ public:
 
     void cells(int64_t first, int64_t count, double* ops, int32_t* p3) {
         if (first < 0 || count < 0 || first + count > nc_) throw Error(LZB_ERR_INVALID, "bad cell range");
+        if (ops && count > 0)
+            need_layers(static_cast<int>(first / N_ / N_), static_cast<int>((first + count - 1) / N_ / N_) + 1, "cells");
         std::vector<double> cls(static_cast<size_t>(count) * kCls3);
         if (ops && count > 0) {
             DevBuf<double> tmp;
@@ -2100,6 +2141,7 @@ public:
 
     // Coarse operators from the leaves (after an assembly): Galerkin, finest first.
     void coarse_ops() {
+        need_whole("coarse operators from every leaf");
         for (int l = D_ - 1; l >= 0; --l) galerkin_planes(l, 0, L3_[l].N);
     }
 
@@ -2115,6 +2157,7 @@ public:
     lzb_cycle_report vcycle(int nu) {
         if (L3_.empty()) throw Error(LZB_ERR_INVALID, "call init_cycle first");
         if (nu < 0) throw Error(LZB_ERR_INVALID, "nu must be >= 0");
+        need_whole("vcycle");
         if (ops_dirty_) {
             coarse_ops();
             ops_dirty_ = false;
@@ -2178,6 +2221,7 @@ public:
 
     lzb_cycle_report step() {
         if (L3_.empty()) throw Error(LZB_ERR_INVALID, "call init_cycle first");
+        need_whole("step");
         if (ops_dirty_) {
             coarse_ops();
             ops_dirty_ = false;
@@ -2339,6 +2383,7 @@ public:
         if (L3_.empty()) throw Error(LZB_ERR_INVALID, "call init_cycle first");
         if (reps < 1) throw Error(LZB_ERR_INVALID, "reps must be >= 1");
         if (D_ < 1) throw Error(LZB_ERR_INVALID, "needs depth >= 1");
+        need_whole("time_kernel");
         if (ops_dirty_) {
             coarse_ops();
             ops_dirty_ = false;
@@ -2427,6 +2472,8 @@ private:
     cudaStream_t s_ = nullptr;
     int D_, N_ = 1, n_last_ = 0, fixed_, W_ = 0;
     int64_t nc_ = 1, ncs_ = 1;  // leaf cells, storage elements of one leaf plane
+    int wz0_ = 0, wz1_ = 1;     // the stored leaf cell layers (a z window; the whole level by default)
+    int64_t woff_ = 0;          // storage index of layer wz0_ (plane_sidx)
     int xp_ = 16;                // padded x extent of the leaf planes
     double h_ = 1.0, delta_;
     Field3 F_{};
@@ -2471,6 +2518,7 @@ private:
         P.nc = ncs_;
         P.N = N_;
         P.xp = xp_;
+        P.woff = woff_;
         P.h = h_;
         const AxisTab3 T1 = axis_tab3(1);
         for (int c = 0; c < 3; ++c) P.s1[c] = T1.s[0][c];
@@ -2480,7 +2528,7 @@ private:
     template <class Fn>
     void leaf_cls(Fn&& fn, int w = -1) const {
         switch (w < 0 ? W_ : w) {
-            case 0: fn(Src64{op_.p, ncs_, N_, xp_}); break;
+            case 0: fn(Src64{op_.p, ncs_, N_, xp_, woff_}); break;
             case 2: fn(SrcComp<2>{planes()}); break;
             case 3: fn(SrcComp<3>{planes()}); break;
             case 4: fn(SrcComp<4>{planes()}); break;
@@ -2505,8 +2553,11 @@ private:
         const Lv3 v = lv(l);
         if (l == D_ && use_tma_) {  // the leaves: TMA-staged tiles (k3_residual_tma)
             if (leaf_diag_dirty_) {  // the Jacobi diagonal, once per change of the leaf operators
-                if (W_ == 0) LZB_LAUNCH(k3_leaf_diag<Src64>, vg(D_), 128, 0, s_, lv(D_), Src64{op_.p, ncs_, N_, xp_});
-                else leaf_cls([&](auto S) { LZB_LAUNCH(k3_leaf_diag<decltype(S)>, vg(D_), 128, 0, s_, lv(D_), S); });
+                // (a windowed grid: of the vertex planes its residual covers, always its slab's)
+                const dim3 gd = windowed() ? vgz(D_, z0, z1) : vg(D_);
+                const Lv3 vd = windowed() ? lvz(D_, z0) : lv(D_);
+                if (W_ == 0) LZB_LAUNCH(k3_leaf_diag<Src64>, gd, 128, 0, s_, vd, Src64{op_.p, ncs_, N_, xp_, woff_});
+                else leaf_cls([&](auto S) { LZB_LAUNCH(k3_leaf_diag<decltype(S)>, gd, 128, 0, s_, vd, S); });
                 leaf_diag_dirty_ = false;
             }
             const dim3 g2(bx, by, (z1 - z0 + zc2(bx, by, z0, z1) - 1) / zc2(bx, by, z0, z1));
@@ -2525,7 +2576,7 @@ private:
         }
         if (l < D_ || W_ == 0) {
             const Src64 S = l < D_ ? Src64{L3_[l].op.p, static_cast<int64_t>(N) * N * N}
-                                   : Src64{op_.p, ncs_, N_, xp_};
+                                   : Src64{op_.p, ncs_, N_, xp_, woff_};
             LZB_LAUNCH(k3_residual_z<Src64>, grid, kRzX * kRzY, 0, s_, v, S, z0, z1, zc);
             return;
         }
@@ -2564,7 +2615,7 @@ private:
         };
         auto make = [&](CUtensorMap* m, void* base, int e, int rank) {
             const cuuint64_t dims[4] = {static_cast<cuuint64_t>(xp_), static_cast<cuuint64_t>(N_ + 1),
-                                        static_cast<cuuint64_t>(N_), 27};
+                                        static_cast<cuuint64_t>(wz1_ - wz0_), 27};
             const cuuint64_t strides[3] = {static_cast<cuuint64_t>(xp_) * e,
                                            static_cast<cuuint64_t>(xp_) * (N_ + 1) * e,
                                            static_cast<cuuint64_t>(ncs_) * e};
@@ -2586,6 +2637,7 @@ private:
             }
             make(&maps_.ec, ec_.p, 8, 3);
         }
+        maps_.z0 = wz0_;
         maps_ready_ = true;
     }
     template <int W>
@@ -2713,6 +2765,23 @@ int lzb_grid3_create_planes(lzb_ctx* ctx, int depth, const lzb_field3* f, double
         auto g = std::make_unique<lzb_grid3>();
         g->g = std::make_unique<lzb::Grid3>(ctx, depth, *f, delta_max, fixed_p3, plane_width);
         *out = g.release();
+    });
+}
+int lzb_grid3_create_window(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3,
+                            int plane_width, int cz0, int cz1, lzb_grid3** out) {
+    return lzb::guarded([&] {
+        auto g = std::make_unique<lzb_grid3>();
+        g->g = std::make_unique<lzb::Grid3>(ctx, depth, *f, delta_max, fixed_p3, plane_width, cz0, cz1);
+        *out = g.release();
+    });
+}
+int lzb_grid3_leaf_storage(lzb_grid3* g, int64_t* bytes, int* cz0, int* cz1) {
+    return lzb::guarded([&] {
+        if (bytes) *bytes = g->g->leaf_storage_bytes();
+        int a, b;
+        g->g->leaf_window(&a, &b);
+        if (cz0) *cz0 = a;
+        if (cz1) *cz1 = b;
     });
 }
 int lzb_grid3_destroy(lzb_grid3* g) {

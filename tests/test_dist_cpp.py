@@ -104,6 +104,55 @@ def test_cpp_dist_cycle3_loopback(world, solver):
         assert np.array_equal(a[v0:v1], b[v0:v1])
 
 
+@pytest.mark.parametrize("world,solver,width", [(2, "adafac-pi", 0), (3, "additive", 0), (3, "adafac-pi", 4)])
+def test_cpp_dist_cycle3_slab_local_storage(world, solver, width):
+    """Slab-local leaf operators (SURVEY §8e memory scaling): each slab grid
+    stores only the leaf cell layers its kernels read (its vertex planes' cells
+    and one layer below; lzb_grid3_create_slab), FP64 class planes or
+    compressed planes; the sharded assembly and the distributed cycle (TMA
+    tiles over the windowed tensors) give the undistributed grid's u bit for
+    bit, on about 1/world of the leaf operator memory each."""
+    depth = 3
+    N = 3 ** depth
+    f = lzb.field3_grf(lzb.grf_table(6, 16, 0.05, 1.0))
+    fixed = 4 if width else 0
+    ref = lzb.Grid3(depth, f, delta_max=1e-4, fixed_p3=fixed)
+    ref.assemble_fixed(2)
+    ref.init_cycle(solver=solver, omega=0.6, seed=9, max_cycles=100)
+    whole, _, _ = lzb.Grid3(depth, f, delta_max=1e-4, fixed_p3=fixed, plane_width=width).leaf_storage()
+    grids, total = [], 0
+    for r in range(world):
+        G = lzb.Grid3(depth, f, delta_max=1e-4, fixed_p3=fixed, plane_width=width, slab=(r, world))
+        v0, v1 = slab_vertex_rows(N, world, r)
+        b, z0, z1 = G.leaf_storage()
+        assert (z0, z1) == (max(v0 - 1, 0), min(v1, N))
+        assert b * N == whole * (z1 - z0)  # bytes proportional to the stored layers
+        total += b
+        G.init_cycle(solver=solver, omega=0.6, seed=9, max_cycles=100)
+        grids.append(G)
+    assert total <= whole * (N + world - 1) // N  # one halo layer per interior slab boundary
+    lzb.dist_assemble_loopback(grids, 2)
+    for _ in range(6):
+        w, g = ref.step(), lzb.dist_cycle_loopback(grids)
+        assert g["status"] == w["status"] and g["residual"] == pytest.approx(w["residual"], rel=1e-12)
+    for r, G in enumerate(grids):
+        v0, v1 = slab_vertex_rows(N, world, r)
+        for lvl in range(depth):
+            assert np.array_equal(G.vertices(lvl, lzb.T.V_U), ref.vertices(lvl, lzb.T.V_U)), lvl
+        a, b = G.vertices(depth, lzb.T.V_U), ref.vertices(depth, lzb.T.V_U)
+        assert np.array_equal(a[v0:v1], b[v0:v1])
+        # the stored operators are the undistributed grid's; layers outside the window are not held
+        _, z0, z1 = G.leaf_storage()
+        ops_g, _ = G.cells(z0 * N * N, (z1 - z0) * N * N)
+        ops_r, _ = ref.cells(z0 * N * N, (z1 - z0) * N * N)
+        assert np.array_equal(ops_g, ops_r)
+        if z0 > 0:
+            with pytest.raises(lzb.LzbError):
+                G.cells(0, N * N)
+        with pytest.raises(lzb.LzbError):
+            G.step()  # the one-GPU cycle reads every leaf
+
+
 def test_cpp_dist_nccl_single_rank():
     """The NCCL transport with a communicator of one rank (the context owns
     it): the 2D and 3D distributed cycles equal the undistributed ones."""
