@@ -710,22 +710,25 @@ __device__ __forceinline__ int choose_precision_exp(const double* v, double delt
         return choose_precision_set<COUNT>(v, delta);
     }
     if (Emax < Ed) return 0;  // every |v| < 2^(E_delta - 1023) <= delta
-    if (Emax == Ed) {
+    if (Emax == Ed) {  // rare: a rolled loop
         bool all_small = true;
-#pragma unroll
+#pragma unroll 1
         for (int i = 0; i < COUNT; ++i) all_small = all_small && !(fabs(v[i]) > delta);
         if (all_small) return 0;
     }
     if (!plain) return choose_precision_set<COUNT>(v, delta);
     const int eT = Ed - Emax + 52;
     int P = min(max((68 - eT) >> 3, 2), 8);
+    // (non-negative doubles order as their bit patterns: the comparisons with
+    // delta run on the integer pipe, the FP64 pipe keeps the subtractions)
+    const unsigned long long dbits = static_cast<unsigned long long>(__double_as_longlong(delta));
     while (P > 2) {
         const unsigned long long keep = ~((1ull << (69 - 8 * P)) - 1);  // width P - 1 drops 61 - 8 (P - 1) bits
         bool fail = false;
 #pragma unroll
         for (int i = 0; i < COUNT; ++i) {
             const double rt = __longlong_as_double(__double_as_longlong(v[i]) & static_cast<long long>(keep));
-            fail = fail || fabs(v[i] - rt) > delta;
+            fail = fail || (static_cast<unsigned long long>(__double_as_longlong(v[i] - rt)) & 0x7fffffffffffffffull) > dbits;
         }
         if (fail) break;
         --P;
@@ -760,23 +763,27 @@ __device__ __forceinline__ int code_record27(const double* sur, const Base3& B, 
         // plain values at widths 2..7: the low fraction bits cleared; 0: every rt is +0; 8: the value
         const unsigned long long keep =
             p3 == 0 ? 0ull : (p3 == 8 ? ~0ull : ~((1ull << (52 - mantissa_bits(p3))) - 1));
-        if (p3 == 8) {
+        if (p3 == 8) {  // rare: a rolled loop
             bool finite = true;
-#pragma unroll
+#pragma unroll 1
             for (int q = 0; q < 27; ++q) finite = finite && dev_isfinite(sur[q]);
             if (!finite) {
                 atomicExch(err, 1);
                 return -1;
             }
         }
+        unsigned long long dmax = 0;  // max |rt - sur| through the bit patterns (integer pipe)
 #pragma unroll
         for (int q = 0; q < 27; ++q) {
             const double rt = __longlong_as_double(__double_as_longlong(sur[q]) & static_cast<long long>(keep));
-            delta = fmax(delta, fabs(rt - sur[q]));
+            const unsigned long long d = static_cast<unsigned long long>(__double_as_longlong(rt - sur[q])) & 0x7fffffffffffffffull;
+            dmax = d > dmax ? d : dmax;
             store(q, BV.at(B, q / 9, (q / 3) % 3, q % 3), rt);
         }
+        delta = __longlong_as_double(static_cast<long long>(dmax));
     } else {
-#pragma unroll
+        // rare (a value that is not plain): a rolled loop, out of the hot path's code
+#pragma unroll 1
         for (int q = 0; q < 27; ++q) {
             double rt;
             if (!roundtrip_slow(sur[q], p3, rt)) {
@@ -784,7 +791,7 @@ __device__ __forceinline__ int code_record27(const double* sur, const Base3& B, 
                 return -1;
             }
             delta = fmax(delta, fabs(rt - sur[q]));
-            store(q, BV.at(B, q / 9, (q / 3) % 3, q % 3), rt);
+            store(q, B(q / 9, (q / 3) % 3, q % 3), rt);
         }
     }
     return p3;
@@ -799,7 +806,9 @@ __device__ __forceinline__ int code_record27(const double* sur, const Base3& B, 
 // code is dropped: a smaller kernel, fewer instruction-cache misses).
 // NS > 0 (GRF cells smaller than a table spacing): the samples per axis at
 // compile time, accumulate3_grf_direct; NS = 0: T.n samples, accumulate3.
-template <int KIND, int NS, int MINB = 3, bool ROLL = false>
+// COMP: the leaves are compressed planes (W > 0); false: FP64 class planes
+// (the plane-word store code is not instantiated: a third less code).
+template <int KIND, int NS, bool COMP, int MINB = 3, bool ROLL = false>
 __global__ void __launch_bounds__(128, MINB) k_assemble3(Field3 Fin, int N, double h, AxisTab3 T, double delta_max,
                                                       int fixed_p3, double* __restrict__ op, Planes3 PL, int W,
                                                       int8_t* __restrict__ p3o, int32_t* __restrict__ no,
@@ -828,11 +837,11 @@ __global__ void __launch_bounds__(128, MINB) k_assemble3(Field3 Fin, int N, doub
     }
     double delta;
     const int p3 = code_record27(sur, B, BV, delta_max, fixed_p3, W, err, wide, delta, [&](int q, double b, double rt) {
-        if (W == 0) op[q * nc + sc] = b + rt;
+        if constexpr (!COMP) op[q * nc + sc] = b + rt;
         else plane_store3(PL, W, sc, q, plane_word(rt, W));
     });
     if (p3 < 0) return;
-    if (W != 0) PL.ec[sc] = e;
+    if constexpr (COMP) PL.ec[sc] = e;
     p3o[c] = static_cast<int8_t>(p3);
     no[c] = T.n;
     atomic_max_double_bits(&stats[S_MAXDELTA], delta);
@@ -1999,16 +2008,15 @@ public:
                 LZB_LAUNCH(kern, blocks_for(ce - cb, 128), 128, 0, s_, F_, N_, h_, T, delta_, fixed_, op_.p, planes(),
                            W_, p3_.p, n_.p, stats_.p, ctx_->err.p, wide_.p, cb, ce);
             };
-            if (small && n == 1) go(k_assemble3<LZB_F3_GRF, 1>);
-            else if (small && n == 2) {
-                static const int variant = std::getenv("LZB_ASM3_VARIANT") ? std::atoi(std::getenv("LZB_ASM3_VARIANT")) : 0;
-                if (variant == 1) go(k_assemble3<LZB_F3_GRF, 2, 4, false>);
-                else if (variant == 2) go(k_assemble3<LZB_F3_GRF, 2, 3, true>);
-                else if (variant == 3) go(k_assemble3<LZB_F3_GRF, 2, 4, true>);
-                else go(k_assemble3<LZB_F3_GRF, 2>);
-            }
-            else if (F_.kind == LZB_F3_GRF) go(k_assemble3<LZB_F3_GRF, 0>);
-            else go(k_assemble3<-1, 0>);
+            auto pick = [&](auto comp) {
+                constexpr bool C = decltype(comp)::value;
+                if (small && n == 1) go(k_assemble3<LZB_F3_GRF, 1, C>);
+                else if (small && n == 2) go(k_assemble3<LZB_F3_GRF, 2, C>);
+                else if (F_.kind == LZB_F3_GRF) go(k_assemble3<LZB_F3_GRF, 0, C>);
+                else go(k_assemble3<-1, 0, C>);
+            };
+            if (W_ == 0) pick(std::false_type{});
+            else pick(std::true_type{});
         }
         n_last_ = n;
     }
