@@ -221,6 +221,46 @@ def cpu_baseline(seconds=10.0, threads=None):
             "sample": f"{k} level-6 cells at p={P}, oracle/lzb_oracle.c single thread, {dt:.1f} s"}
 
 
+def cpu_reference_extras():
+    """SURVEY §8d's other CPU timings, through the unmodified reference (oracle/_ref):
+    AdditiveSolver::step on the 729^2 grid (single-threaded by construction,
+    solver.cpp has no threads) and the codec loops on one core. Bounded: a few seconds."""
+    import numpy as np
+
+    from oracle import ref
+    if not ref.available():
+        return None
+    out = {}
+    cfg = ("setup = quadrant\neps-low = 0.001\ndepth = 6\nsolver = adafac-pi\nassembly = eager\nomega = 0.6\n"
+           "max-cycles = 100000\nrhs = 1\nseed = 42\n")
+    rig = ref.Rig(cfg)
+    rig.eager_setup()  # every leaf integrated to convergence first: the timed steps are pure cycles
+    rig.step()
+    k, t0 = 0, time.perf_counter()
+    while k < 3 or time.perf_counter() - t0 < 3.0:
+        rig.step()
+        k += 1
+    dt = (time.perf_counter() - t0) / k
+    rig.close()
+    out["step_729x729"] = {"ms_per_cycle": 1e3 * dt, "dof_updates_per_s": (N_AXIS - 1) ** 2 / dt, "cores": 1,
+                           "cycles": k, "what": "the unmodified reference's AdditiveSolver::step (adaFAC-PI, quadrant "
+                                                "eps, operators assembled beforehand), one thread"}
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(1 << 20) * 1e-3
+    t0 = time.perf_counter()
+    b = ref.encode_many(x, 4)
+    t1 = time.perf_counter()
+    ref.decode_many(b, 4)
+    t2 = time.perf_counter()
+    p3 = ref.choose_many(x, 16, 1e-8, 1)
+    t3 = time.perf_counter()
+    out["codec_1core"] = {"encode_values_per_s": x.size / (t1 - t0), "decode_values_per_s": x.size / (t2 - t1),
+                          "choose_precision_records_per_s": p3.size / (t3 - t2),
+                          "what": "codec::encode_value / decode_value at p3 = 4 and choose_precision over 16-entry "
+                                  "records (delta 1e-8), 2^20 values, one core"}
+    return out
+
+
 def cpu_delayed_solve(level, pmax):
     """The delayed solve of BASELINE configs[1] (geometric start, p doubling
     1 -> pmax, adaFAC-PI to 1e-10) on the host through the oracle restatement."""
@@ -803,6 +843,10 @@ def run_ours(args, world, rank, local):
         # task integrations on all host threads, the cycle itself single-threaded as
         # the reference's solver is)
         tts["cpu_measured"] = cpu_delayed_solve(LEVEL, P)
+        try:
+            base["extras"] = cpu_reference_extras()
+        except Exception as exc:  # noqa: BLE001
+            base["extras"] = {"error": repr(exc)}
     mp = peaks()
     line = {
         "metric": METRIC, "value": value, "unit": "sub-samples/s", "n_gpus": world, "steps": args.steps,
