@@ -1989,6 +1989,67 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_inject(AllLevels A, int
 }
 #undef LZB_FOR_VERTS
 
+// ---- the middle levels of the update pass in three launches. Between the
+// small levels (one block) and the leaf level (k_update_fine) the update pass
+// ran, per level, a snapshot, the adaFAC-PI injection, the aux correction and
+// the Jacobi step, and after the prolongation one injection per level: 16
+// launches of a few microseconds of work at 729^2, a third of the cycle's
+// latency. None of them depends on another level's result (the injections
+// read r, which the update pass never writes; the aux correction reads the
+// level below's aux and diagonal only; a level's injected u is the leaf
+// level's u at the same point), so each group runs as one launch over the
+// concatenated vertices of levels l0..l1, every vertex through the per-level
+// bodies in the per-level order: the same bits.
+struct MidRange {
+    int l0, l1;                 // levels l0..l1
+    int64_t start[kMaxLevels];  // first concatenated index of level l (start[l1 + 1] = total)
+};
+__device__ __forceinline__ bool mid_locate(const MidRange& R, int64_t t, int& l, int64_t& i) {
+    if (t >= R.start[R.l1 + 1]) return false;
+    l = R.l0;
+    while (l < R.l1 && t >= R.start[l + 1]) ++l;
+    i = t - R.start[l];
+    return true;
+}
+// usnap = u; aux = the injected residual of the level above (adaFAC-PI), else 0.
+// lc_aux >= 0: also the injection into level lc_aux (the top small level,
+// snapshot already taken by k_small_snap) -- its indices follow level l1's.
+__global__ void k_mid_snap(AllLevels A, MidRange R, int pi, int lc_aux, int64_t n_lc) {
+    lzb_pdl_enter();
+    const int64_t t = gtid();
+    int l;
+    int64_t i;
+    if (mid_locate(R, t, l, i)) {
+        k_snap_body<true>(i, A.L[l]);
+        if (pi) k_aux_inject_body<true>(i, A.L[l + 1], A.L[l]);
+        return;
+    }
+    const int64_t j = t - R.start[R.l1 + 1];
+    if (pi && lc_aux >= 0 && j < n_lc) k_aux_inject_body<true>(j, A.L[lc_aux + 1], A.L[lc_aux]);
+}
+// the aux correction (adaFAC-PI) and the Jacobi step of levels l0..l1
+__global__ void k_mid_update(AllLevels A, MidRange R, int pi, double omega, Damp dm) {
+    lzb_pdl_enter();
+    int l;
+    int64_t i;
+    if (!mid_locate(R, gtid(), l, i)) return;
+    if (pi && l > 0) k_aux_sub_body<true>(i, A.L[l], A.L[l - 1], omega);
+    k_jacobi_body<true>(i, A.L[l], dm.d[l]);
+}
+// inject_solution of levels l0..l1 from the leaf level (level l's vertex v is
+// leaf vertex 3^(D-l) v; the per-level chain copies the same value down)
+__global__ void k_mid_inject(AllLevels A, MidRange R) {
+    lzb_pdl_enter();
+    int l;
+    int64_t i;
+    if (!mid_locate(R, gtid(), l, i)) return;
+    const LevelView C = A.L[l], F = A.L[A.D];
+    const int NV = C.N + 1;
+    const int iy = static_cast<int>(i / NV), ix = static_cast<int>(i - static_cast<int64_t>(iy) * NV);
+    const int s3 = F.N / C.N;
+    C.v[LZB_V_U][i] = F.v[LZB_V_U][static_cast<int64_t>(s3 * iy) * (F.N + 1) + s3 * ix];
+}
+
 // Running image offset of the bands of level-1 subtrees (assemble_stream):
 // base[1] = base[0] + the band's bytes (its last local offset plus its last record).
 __global__ void k_chunk_base(const int64_t* __restrict__ sizes, const int64_t* __restrict__ offs, int64_t n,
@@ -2922,7 +2983,53 @@ public:
         LZB_CUDA(cudaMemcpyAsync(hres_, res_.p, sizeof(Result), cudaMemcpyDeviceToHost, s_));
         LZB_CUDA(cudaMemcpyAsync(herr_, ctx_->err.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
     }
+    MidRange mid_range(int l0, int l1) const {
+        MidRange R{};
+        R.l0 = l0;
+        R.l1 = l1;
+        int64_t at = 0;
+        for (int l = l0; l <= l1 + 1 && l < kMaxLevels; ++l) {
+            R.start[l] = at;
+            if (l <= l1) at += L_[l].nv;
+        }
+        return R;
+    }
+    // the fused middle levels (k_mid_*): additive and adaFAC-PI, at least one level
+    // between the small levels and the leaves; LZB_PLAIN_BACK=1 keeps the per-level launches
+    bool fused_back_ok() const {
+        static const bool plain = std::getenv("LZB_PLAIN_BACK") != nullptr;
+        return !plain && d_.variant != LZB_ADAFAC_JAC && small_lc() + 1 <= D_ - 1 && D_ + 1 < kMaxLevels;
+    }
+    void back_body_fused() {
+        const int lc = small_lc(), l0 = lc + 1, l1 = D_ - 1;
+        const bool pi = d_.variant == LZB_ADAFAC_PI;
+        const MidRange R = mid_range(l0, l1);
+        const int64_t nmid = R.start[l1 + 1], n_lc = lc >= 0 ? static_cast<int64_t>(L_[lc].nv) : 0;
+        Damp dm{};
+        for (int l = 0; l <= D_; ++l) dm.d[l] = damping(l);
+        if (lc >= 0) LZB_LAUNCH(k_small_snap, 1, kSmallThreads, 0, s_, all_levels(), lc);
+        LZB_LAUNCH(k_mid_snap, blocks_for(nmid + n_lc, kThreads), kThreads, 0, s_, all_levels(), R, pi ? 1 : 0, lc,
+                   n_lc);
+        LZB_LAUNCH(k_mid_update, blocks_for(nmid, kThreads), kThreads, 0, s_, all_levels(), R, pi ? 1 : 0, d_.omega,
+                   dm);
+        if (lc >= 0)
+            LZB_LAUNCH(k_small_back, 1, kSmallThreads, 0, s_, all_levels(), lc, static_cast<int>(d_.variant),
+                       d_.omega, dm, d_.field);
+        for (int l = std::max(lc, 0) + 1; l <= D_ - 1; ++l)
+            LZB_LAUNCH(k_prolong, ugrid(l), kThreads, 0, s_, V(l), V(l - 1));
+        if (pi) LZB_LAUNCH(k_scale_aux, vgrid(D_ - 1), kThreads, 0, s_, V(D_ - 1), d_.omega, caux_.p);
+        LZB_LAUNCH(k_update_fine, vgrid(D_), kThreads, 0, s_, V(D_), V(D_ - 1), pi ? caux_.p : nullptr,
+                   damping(D_));
+        // injection: levels D-1 .. max(lc, 0) straight from the leaves, then the small levels' chain
+        const MidRange Ri = mid_range(std::max(lc, 0), D_ - 1);
+        LZB_LAUNCH(k_mid_inject, blocks_for(Ri.start[D_], kThreads), kThreads, 0, s_, all_levels(), Ri);
+        if (lc >= 1) LZB_LAUNCH(k_small_inject, 1, kSmallThreads, 0, s_, all_levels(), lc);
+    }
     void back_body() {  // update + prolongation + injection
+        if (fused_back_ok()) {
+            back_body_fused();
+            return;
+        }
         update_launches(true, true);
         for (int l = std::max(small_lc(), 0) + 1; l <= D_ - 1; ++l)
             LZB_LAUNCH(k_prolong, ugrid(l), kThreads, 0, s_, V(l), V(l - 1));

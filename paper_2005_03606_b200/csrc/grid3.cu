@@ -1443,6 +1443,91 @@ __global__ void k3_restrict(Lv3 F, Lv3 C) {
     C.v[LZB_V_FL][vi] = acc;
 }
 
+// The same restriction as a staged z-march (the cycle's kernel; k3_restrict
+// above stays as the plain form, LZB_PLAIN_RESTRICT=1). Ownership and the
+// lattice weights are per-axis, so P^T is the tensor product of the 1D
+// restriction c[I] = (f[3I-2] + 2 f[3I-1] + 3 f[3I] + 2 f[3I+1] + f[3I+2]) / 3
+// (fine vertex 3I is owned by patch I - 1 at its lattice index 3, by patch 0
+// at index 0 when I = 0: weight 3 either way). A block owns 32 x 8 coarse
+// columns and a chunk of coarse planes; per fine plane it stages the 98 x 26
+// tile of r-hat with coalesced loads (each fine value is read once, not ~4.6
+// times through strided gathers), restricts in x, then y, in shared memory,
+// and every thread accumulates its column's value into the one or two coarse
+// planes the fine plane belongs to (ascending fine planes: the same order for
+// any chunking, so slab-range launches give the same bits). Integer weights,
+// one division by 27 per coarse vertex: the sums differ from k3_restrict's
+// (one rounded weight product per term) in the last bits only -- the 3D cycle
+// is a restatement with a 1e-10 parity bar.
+constexpr int kRsX = 32, kRsY = 8, kRsFX = 3 * kRsX + 2, kRsFY = 3 * kRsY + 2;
+__global__ void __launch_bounds__(kRsX * kRsY) k3_restrict_zm(Lv3 F, Lv3 C, int Z0, int Z1, int zc) {
+    lzb_pdl_enter();
+    __shared__ double tile[kRsFY][kRsFX];
+    __shared__ double s1[kRsFY][kRsX];
+    const int t = threadIdx.x, tx = t % kRsX, ty = t / kRsX;
+    const int IX0 = blockIdx.x * kRsX, IY0 = blockIdx.y * kRsY;
+    const int za = Z0 + blockIdx.z * zc, zb = min(za + zc, Z1);
+    if (za >= zb) return;
+    const int Nf = F.N, NVf = Nf + 1, Nc = C.N, NVc = Nc + 1;
+    const int IX = IX0 + tx, IY = IY0 + ty;
+    const bool own = IX < NVc && IY < NVc;
+    const int fx0 = 3 * IX0 - 2, fy0 = 3 * IY0 - 2;
+    const double* __restrict__ rh = F.v[LZB_V_RHAT];
+    double* __restrict__ out = C.v[LZB_V_FL];
+    double cur = 0.0, nxt = 0.0;  // coarse planes I and I + 1
+    int I = za;
+    const int fbeg = max(3 * za - 2, 0), fend = min(3 * (zb - 1) + 2, Nf);
+    // this thread's tile elements (the same for every fine plane): in-plane offset, or -1 outside the grid
+    constexpr int kPer = (kRsFY * kRsFX + kRsX * kRsY - 1) / (kRsX * kRsY);
+    int off[kPer];
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+        const int k = t + e * kRsX * kRsY;
+        const int r = k / kRsFX, c = k - r * kRsFX;
+        const int fy = fy0 + r, fx = fx0 + c;
+        off[e] = (k < kRsFY * kRsFX && fx >= 0 && fy >= 0 && fx <= Nf && fy <= Nf) ? fy * NVf + fx : -1;
+    }
+    double* const tflat = &tile[0][0];
+    double pre[kPer];  // the next fine plane's values, in flight while this one is restricted
+    auto fetch = [&](int fz) {
+        const double* pl = rh + static_cast<int64_t>(fz) * NVf * NVf;
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) pre[e] = off[e] >= 0 ? __ldg(pl + off[e]) : 0.0;
+    };
+    fetch(fbeg);
+    for (int fz = fbeg; fz <= fend; ++fz) {
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            const int k = t + e * kRsX * kRsY;
+            if (k < kRsFY * kRsFX) tflat[k] = pre[e];
+        }
+        __syncthreads();
+        if (fz < fend) fetch(fz + 1);
+        for (int r = ty; r < kRsFY; r += kRsY) {  // x: fine 3 IX + j sits in column 3 tx + j + 2
+            const double* p = &tile[r][3 * tx];
+            s1[r][tx] = ((p[0] + 2.0 * p[1]) + 3.0 * p[2]) + (2.0 * p[3] + p[4]);
+        }
+        __syncthreads();
+        const int r0 = 3 * ty;  // y: fine 3 IY + j sits in row 3 ty + j + 2
+        const double v = ((s1[r0][tx] + 2.0 * s1[r0 + 1][tx]) + 3.0 * s1[r0 + 2][tx]) +
+                         (2.0 * s1[r0 + 3][tx] + s1[r0 + 4][tx]);
+        // z: fine plane 3 q + m feeds coarse q (weights 3, 2, 1 for m = 0, 1, 2) and q + 1 (0, 1, 2)
+        const int q = fz / 3, m = fz - 3 * q;
+        const double wq = static_cast<double>(3 - m), wq1 = static_cast<double>(m);
+        if (q == I) cur += wq * v;
+        else if (q == I + 1) nxt += wq * v;
+        if (m != 0) {
+            if (q + 1 == I) cur += wq1 * v;
+            else if (q + 1 == I + 1) nxt += wq1 * v;
+        }
+        if (fz == 3 * I + 2 || fz == Nf) {  // coarse plane I is complete
+            if (own && I < zb) out[(static_cast<int64_t>(I) * NVc + IY) * NVc + IX] = cur / 27.0;
+            cur = nxt;
+            nxt = 0.0;
+            ++I;
+        }
+    }
+}
+
 // Per-block partial sums of r^2 over the interior vertices of planes
 // [max(zlo, 1), min(zhi, N)): block b takes rows b, b + G, ... four rows per
 // step (four independent loads in flight per thread), then a fixed-order tree.
@@ -2205,7 +2290,7 @@ public:
             for (int l = D_; l >= 1; --l) {
                 smooth(l, nu);
                 residual_plain(l);
-                LZB_LAUNCH(k3_restrict, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));  // fl_{l-1} = P^T r_l
+                restrict3(l, 0, L3_[l - 1].N + 1);  // fl_{l-1} = P^T r_l
                 LZB_CUDA(cudaMemsetAsync(L3_[l - 1].v[LZB_V_U].p, 0, L3_[l - 1].v[LZB_V_U].bytes(), s_));
             }
             for (int l = 1; l <= D_; ++l) {
@@ -2240,7 +2325,7 @@ public:
         for (int l = D_; l >= 0; --l) {
             uhat3(l, 0, L3_[l].N + 1);
             residual3(l, 0, L3_[l].N + 1);
-            if (l > 0) LZB_LAUNCH(k3_restrict, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
+            if (l > 0) restrict3(l, 0, L3_[l - 1].N + 1);
         }
         const int ng = L3_[D_].N > 1 ? kNormBlocks3 : 1;
         LZB_CUDA(cudaMemsetAsync(partial3_.p, 0, partial3_.bytes(), s_));
@@ -2334,13 +2419,13 @@ public:
                 break;
             }
             case 1:
-                LZB_LAUNCH(k3_restrict, vgz(D_ - 1, c0, c1), 128, 0, s_, lv(D_), lvz(D_ - 1, c0));
+                restrict3(D_, c0, c1);
                 break;
             case 2: {
                 for (int l = D_ - 1; l >= 0; --l) {
                     uhat3(l, 0, L3_[l].N + 1);
                     residual3(l, 0, L3_[l].N + 1);
-                    if (l > 0) LZB_LAUNCH(k3_restrict, vg(l - 1), 128, 0, s_, lv(l), lv(l - 1));
+                    if (l > 0) restrict3(l, 0, L3_[l - 1].N + 1);
                 }
                 if (flags & 2) {  // the C++ data plane: the slab's norm^2 stays on the device (dist.cpp)
                     LZB_LAUNCH(k3_sum_partials, 1, 32, 0, s_, partial3_.p, kNormBlocks3, res3_.p);
@@ -2400,7 +2485,7 @@ public:
             switch (what) {
                 case LZB_TK_UHAT: uhat3(D_, 0, L3_[D_].N + 1); break;
                 case LZB_TK_RESIDUAL: residual3(D_, 0, L3_[D_].N + 1); break;
-                case LZB_TK_RESTRICT: LZB_LAUNCH(k3_restrict, vg(D_ - 1), 128, 0, s_, lv(D_), lv(D_ - 1)); break;
+                case LZB_TK_RESTRICT: restrict3(D_, 0, L3_[D_ - 1].N + 1); break;
                 case LZB_TK_JACOBI: LZB_LAUNCH(k3_jacobi, vg(D_), 128, 0, s_, lv(D_), 0.0); break;
                 case LZB_TK_PROLONG: LZB_LAUNCH(k3_prolong, vg(D_), 128, 0, s_, lv(D_), lv(D_ - 1)); break;
                 case LZB_TK_BACK:  // the fused leaf update (u drifts by the prolongated correction)
@@ -2562,8 +2647,9 @@ private:
         if (l == D_ && use_tma_) {  // the leaves: TMA-staged tiles (k3_residual_tma)
             if (leaf_diag_dirty_) {  // the Jacobi diagonal, once per change of the leaf operators
                 // (a windowed grid: of the vertex planes its residual covers, always its slab's)
-                const dim3 gd = windowed() ? vgz(D_, z0, z1) : vg(D_);
-                const Lv3 vd = windowed() ? lvz(D_, z0) : lv(D_);
+                const int d0 = sv1_ < 0 ? z0 : sv0_, d1 = sv1_ < 0 ? z1 : sv1_;  // the slab's planes when set
+                const dim3 gd = windowed() ? vgz(D_, d0, d1) : vg(D_);
+                const Lv3 vd = windowed() ? lvz(D_, d0) : lv(D_);
                 if (W_ == 0) LZB_LAUNCH(k3_leaf_diag<Src64>, gd, 128, 0, s_, vd, Src64{op_.p, ncs_, N_, xp_, woff_});
                 else leaf_cls([&](auto S) { LZB_LAUNCH(k3_leaf_diag<decltype(S)>, gd, 128, 0, s_, vd, S); });
                 leaf_diag_dirty_ = false;
@@ -2668,6 +2754,23 @@ private:
         else
             LZB_LAUNCH((k3_residual_tma<W, S, false>), g, kRzX * kRzY, tma_smem_bytes2(W, S), s_, v, maps_, vmaps_, pl,
                        z0, z1, zc);
+    }
+    // fl_{l-1} = P^T r-hat_l on the coarse vertex planes [c0, c1) of level l - 1
+    void restrict3(int l, int c0, int c1) {
+        static const bool plain = std::getenv("LZB_PLAIN_RESTRICT") != nullptr;
+        if (plain) {
+            LZB_LAUNCH(k3_restrict, vgz(l - 1, c0, c1), 128, 0, s_, lv(l), lvz(l - 1, c0));
+            return;
+        }
+        const int NVc = L3_[l - 1].N + 1;
+        const int bx = (NVc + kRsX - 1) / kRsX, by = (NVc + kRsY - 1) / kRsY;
+        // chunks of coarse planes: one wave of resident blocks (8 per SM: 27 KB of shared
+        // memory, 62 registers), no partial second wave; each chunk re-reads 4 fine planes
+        int chunks = static_cast<int>(8LL * ctx_->sms / (static_cast<int64_t>(bx) * by));
+        chunks = std::max(1, std::min(chunks, (c1 - c0 + 3) / 4));
+        const int zc = (c1 - c0 + chunks - 1) / chunks;
+        LZB_LAUNCH(k3_restrict_zm, dim3(bx, by, (c1 - c0 + zc - 1) / zc), kRsX * kRsY, 0, s_, lv(l), lv(l - 1), c0,
+                   c1, zc);
     }
     bool leaf_diag_dirty_ = true;
     // TMA maps of the leaf vertex fields the residual reads (u, u-hat -- u
