@@ -1227,10 +1227,16 @@ __host__ __device__ constexpr int tma_smem_bytes2(int W, int S) {
 // S stages: the tiles of iteration j land in stage j % S, issued S - 1
 // iterations ahead (S = 2 for the small compressed words, whose stages are
 // small; the FP64 planes' 66 KB stage leaves room for one per block)
-template <int W, int S, bool SYM>
+// NORM: the block also sums r^2 of the vertices it writes (r is zero on the
+// boundary) into norm_part[block]: the residual norm of step() without the
+// 8 B per vertex re-read of k3_norm_partial (fixed order: per thread over its
+// planes, then a tree over the block; the blocks' partials are summed by
+// k3_sum_wide).
+template <int W, int S, bool SYM, bool NORM>
 __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_tma(Lv3 F, const __grid_constant__ TmaMaps M,
                                                                  const __grid_constant__ TmaVMaps VM, Planes3 P,
-                                                                 int zbeg, int zend, int zc) {
+                                                                 int zbeg, int zend, int zc,
+                                                                 double* __restrict__ norm_part) {
     lzb_pdl_enter();
     extern __shared__ __align__(128) unsigned char smraw[];
     double(*sy)[8][kTmaCells] = reinterpret_cast<double(*)[8][kTmaCells]>(smraw);  // [u, û][corner][cell]
@@ -1250,7 +1256,11 @@ __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_tma(Lv3 F, const _
     const int N = F.N, NV = N + 1;
     const int X0 = blockIdx.x * (kRzX - 1), Y0 = blockIdx.y * (kRzY - 1);
     const int zs = zbeg + blockIdx.z * zc, ze = min(zs + zc, zend);
-    if (zs >= ze) return;
+    if (zs >= ze) {
+        if (NORM && t == 0) norm_part[(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = 0.0;
+        return;
+    }
+    double nsum = 0.0;
     const int cx = X0 - 1 + tx, cy = Y0 - 1 + ty;  // this thread's cell column
     const bool colok = cx >= 0 && cy >= 0 && cx < N && cy < N;
     const int ix = X0 + tx, iy = Y0 + ty;  // this thread's vertex column (tx < 31, ty < 7)
@@ -1400,6 +1410,7 @@ __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_tma(Lv3 F, const _
                 const int64_t vi = (static_cast<int64_t>(cz) * NV + iy) * NV + ix;
                 __stcs(F.v[LZB_V_R] + vi, r);
                 __stcs(F.v[LZB_V_RHAT] + vi, rh);
+                if (NORM) nsum += r * r;
             }
             if (cz + 1 < ze) {
                 rp = rhp = flc;
@@ -1410,6 +1421,16 @@ __global__ void __launch_bounds__(kRzX * kRzY, 2) k3_residual_tma(Lv3 F, const _
             }
         }
         __syncthreads();
+    }
+    if (NORM) {  // the loop ended on a barrier: the row-product stage is free
+        double* red = &sy[0][0][0];
+        red[t] = nsum;
+        __syncthreads();
+        for (int w = (kRzX * kRzY) / 2; w > 0; w >>= 1) {
+            if (t < w) red[t] += red[t + w];
+            __syncthreads();
+        }
+        if (t == 0) norm_part[(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = red[0];
     }
 }
 
@@ -1571,6 +1592,21 @@ __global__ void k3_sum_partials(const double* partial, int n, double* out) {
     double s2 = 0.0;
     for (int i = 0; i < n; ++i) s2 += partial[i];
     *out = s2;
+}
+
+// sum of n partials in a fixed order: strided per thread, then a tree
+__global__ void __launch_bounds__(1024) k3_sum_wide(const double* __restrict__ partial, int n, double* out) {
+    lzb_pdl_enter();
+    __shared__ double sh[1024];
+    double a = 0.0;
+    for (int i = threadIdx.x; i < n; i += 1024) a += partial[i];
+    sh[threadIdx.x] = a;
+    __syncthreads();
+    for (int w = 512; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
 }
 
 __global__ void k3_snap(Lv3 L, int64_t nv) {
@@ -2216,7 +2252,13 @@ public:
                 L.v[f].alloc(L.nv);
                 LZB_CUDA(cudaMemsetAsync(L.v[f].p, 0, L.v[f].bytes(), s_));
             }
-            if (l < D_) L.op.alloc(static_cast<size_t>(L.N) * L.N * L.N * kCls3);
+            // the coarse operators survive a re-initialisation of the cycle (a fresh
+            // allocation holds nothing: they are then re-formed from the leaves)
+            const size_t nop = static_cast<size_t>(L.N) * L.N * L.N * kCls3;
+            if (l < D_ && L.op.n != nop) {
+                L.op.alloc(nop);
+                ops_dirty_ = true;
+            }
         }
         partial3_.alloc(kNormBlocks3);
         leaf_diag_dirty_ = true;  // fresh vertex arrays
@@ -2322,19 +2364,30 @@ public:
         lzb_cycle_report rep;
         std::memset(&rep, 0, sizeof rep);
         rep.cycle = static_cast<int32_t>(++cycle_);
+        // the leaf residual also sums r^2 (TMA kernel, NORM): no separate pass over r
+        const bool fused = use_tma_ && L3_[D_].N > 1 && std::getenv("LZB_PLAIN_NORM") == nullptr;
         for (int l = D_; l >= 0; --l) {
             uhat3(l, 0, L3_[l].N + 1);
+            fuse_norm_ = fused && l == D_;
             residual3(l, 0, L3_[l].N + 1);
+            fuse_norm_ = false;
             if (l > 0) restrict3(l, 0, L3_[l - 1].N + 1);
         }
-        const int ng = L3_[D_].N > 1 ? kNormBlocks3 : 1;
-        LZB_CUDA(cudaMemsetAsync(partial3_.p, 0, partial3_.bytes(), s_));
-        if (L3_[D_].N > 1) LZB_LAUNCH(k3_norm_partial, ng, 256, 0, s_, lv(D_), partial3_.p, 0, L3_[D_].N + 1);
-        std::vector<double> part(kNormBlocks3);
-        LZB_CUDA(cudaMemcpyAsync(part.data(), partial3_.p, kNormBlocks3 * sizeof(double), cudaMemcpyDeviceToHost, s_));
-        sync();
         double s2 = 0.0;
-        for (double x : part) s2 += x;
+        if (fused) {
+            LZB_LAUNCH(k3_sum_wide, 1, 1024, 0, s_, static_cast<const double*>(rpartial_.p), norm_blocks_, res3_.p);
+            LZB_CUDA(cudaMemcpyAsync(&s2, res3_.p, sizeof(double), cudaMemcpyDeviceToHost, s_));
+            sync();
+        } else {
+            const int ng = L3_[D_].N > 1 ? kNormBlocks3 : 1;
+            LZB_CUDA(cudaMemsetAsync(partial3_.p, 0, partial3_.bytes(), s_));
+            if (L3_[D_].N > 1) LZB_LAUNCH(k3_norm_partial, ng, 256, 0, s_, lv(D_), partial3_.p, 0, L3_[D_].N + 1);
+            std::vector<double> part(kNormBlocks3);
+            LZB_CUDA(cudaMemcpyAsync(part.data(), partial3_.p, kNormBlocks3 * sizeof(double), cudaMemcpyDeviceToHost,
+                                     s_));
+            sync();
+            for (double x : part) s2 += x;
+        }
         rep.residual = std::sqrt(s2);
         if (history_.empty()) first_ = rep.residual > 0.0 ? rep.residual : 1.0;
         history_.push_back(rep.residual);
@@ -2738,23 +2791,35 @@ private:
     void launch_tma(dim3 g, const Lv3& v, int z0, int z1, int zc) {
         constexpr int S = (W >= 2 && W <= 4) ? 2 : 1;  // stages (k3_residual_tma)
         build_maps();
-        static bool attr = false;
-        if (!attr) {
-            LZB_CUDA(cudaFuncSetAttribute(k3_residual_tma<W, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          tma_smem_bytes2(W, S)));
-            LZB_CUDA(cudaFuncSetAttribute(k3_residual_tma<W, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          tma_smem_bytes2(W, S)));
-            attr = true;
-        }
         vmaps(v);
         const Planes3 pl = planes();
-        if (pl.s1[0] == pl.s1[2])
-            LZB_LAUNCH((k3_residual_tma<W, S, true>), g, kRzX * kRzY, tma_smem_bytes2(W, S), s_, v, maps_, vmaps_, pl,
-                       z0, z1, zc);
-        else
-            LZB_LAUNCH((k3_residual_tma<W, S, false>), g, kRzX * kRzY, tma_smem_bytes2(W, S), s_, v, maps_, vmaps_, pl,
-                       z0, z1, zc);
+        const bool sym = pl.s1[0] == pl.s1[2];
+        double* np = nullptr;
+        if (fuse_norm_) {  // step(): the norm partials come from this launch
+            norm_blocks_ = static_cast<int>(g.x * g.y * g.z);
+            if (rpartial_.n < static_cast<size_t>(norm_blocks_)) rpartial_.alloc(norm_blocks_);
+            np = rpartial_.p;
+        }
+        static bool attr = false;  // per width: the four variants share the launch shape
+        if (!attr) {
+            const int bytes = tma_smem_bytes2(W, S);
+            LZB_CUDA(cudaFuncSetAttribute(k3_residual_tma<W, S, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+            LZB_CUDA(cudaFuncSetAttribute(k3_residual_tma<W, S, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+            LZB_CUDA(cudaFuncSetAttribute(k3_residual_tma<W, S, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+            LZB_CUDA(cudaFuncSetAttribute(k3_residual_tma<W, S, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+            attr = true;
+        }
+        auto go = [&](auto kern) {
+            LZB_LAUNCH(kern, g, kRzX * kRzY, tma_smem_bytes2(W, S), s_, v, maps_, vmaps_, pl, z0, z1, zc, np);
+        };
+        if (sym && np) go(k3_residual_tma<W, S, true, true>);
+        else if (sym) go(k3_residual_tma<W, S, true, false>);
+        else if (np) go(k3_residual_tma<W, S, false, true>);
+        else go(k3_residual_tma<W, S, false, false>);
     }
+    bool fuse_norm_ = false;  // set by step() around the leaf residual
+    int norm_blocks_ = 0;
+    DevBuf<double> rpartial_;
     // fl_{l-1} = P^T r-hat_l on the coarse vertex planes [c0, c1) of level l - 1
     void restrict3(int l, int c0, int c1) {
         static const bool plain = std::getenv("LZB_PLAIN_RESTRICT") != nullptr;

@@ -356,3 +356,31 @@ def test_vcycle3_then_step_matches_restatement():
     for lvl in range(depth + 1):
         u, w = G.vertices(lvl, lzb.T.V_U), ref.v[lvl]["u"]
         assert np.abs(u - w).max() <= 1e-12 * max(np.abs(w).max(), 1.0), lvl
+
+
+def test_reinit_cycle_keeps_coarse_operators():
+    """init_cycle after a solve (bench.py's C3 sequence: adaFAC-PI solve, then
+    V(2,2) cycles on the same operators) re-allocates the vertex arrays; the
+    coarse Galerkin operators must survive it (or be re-formed): the V-cycle
+    history equals a fresh grid's, bit for bit."""
+    f = lzb.field3_grf(lzb.grf_table(4, 16, 0.05, 1.0))
+
+    def vhist(pre):
+        g = lzb.Grid3(3, f, delta_max=1e-8)
+        g.assemble_fixed(3)
+        if pre:
+            g.init_cycle(solver="adafac-pi", omega=0.6, seed=11, max_cycles=100)
+            # other allocations come and go in between, as in a long-lived process
+            junk = [lzb.Grid3(2, f) for _ in range(3)]
+            for _ in range(6):
+                g.step()
+            for j in junk:
+                j.close()
+        g.init_cycle(solver="additive", omega=0.6, seed=5, max_cycles=100)
+        out = [g.vcycle(2)["residual"] for _ in range(4)]
+        g.close()
+        return out
+
+    a, b = vhist(False), vhist(True)
+    assert a == b
+    assert a[3] < 0.05 * a[0]  # the coarse correction works (smoothing alone gives ~0.5)
