@@ -1691,11 +1691,15 @@ __global__ void k3_prolong(Lv3 F, Lv3 C) {
 // changes the last bits only (tests: 1e-12 on u).
 constexpr int kStThreads = 256;  // fine x per block
 constexpr int kStX = 96;  // staged coarse x per line (256 / 3 + 3 rounded up)
-constexpr int kStY = 8;   // fine rows per block
+constexpr int kStY = 8;   // fine rows per block of the u-hat kernel
+constexpr int kStYu = 4;  // of the fused update (three arrays per row in registers: 64 registers, twice the
+                          // resident warps of the 8-row form; measured 5.2 -> 4.8 ms at 729^3, while the
+                          // u-hat kernel is faster with 8: 1.40 vs 1.83 ms)
 constexpr int kStCy = 5;  // coarse y lines the rows' owner patches span (<= kStY / 3 + 3)
 struct RowStage {
     int px0, nx, pz, lz, py0, ny, fy0, fy1, fz;
 };
+template <int ROWS>
 __device__ __forceinline__ RowStage row_stage(const Lv3& F, const Lv3& C) {
     RowStage r;
     const int fx0 = blockIdx.x * blockDim.x;
@@ -1705,8 +1709,8 @@ __device__ __forceinline__ RowStage row_stage(const Lv3& F, const Lv3& C) {
     r.fz = blockIdx.z + F.z0;
     r.pz = owner3(r.fz, C.N);
     r.lz = r.fz - 3 * r.pz;
-    r.fy0 = blockIdx.y * kStY;
-    r.fy1 = min(r.fy0 + kStY, F.N + 1);
+    r.fy0 = blockIdx.y * ROWS;
+    r.fy1 = min(r.fy0 + ROWS, F.N + 1);
     r.py0 = owner3(r.fy0, C.N);
     r.ny = owner3(r.fy1 - 1, C.N) + 2 - r.py0;
     return r;
@@ -1744,16 +1748,16 @@ __global__ void __launch_bounds__(kStThreads) k3_update_fine_st(Lv3 F, Lv3 C, co
                                                           double damping) {
     lzb_pdl_enter();
     __shared__ double2 s_pre[kStCy][2][kStX];
-    __shared__ double2 s_g[kStY][kStX];  // per row, per coarse x: (aux, correction) contracted over y, z
-    __shared__ unsigned char s_nz[kStY][kStX];
+    __shared__ double2 s_g[kStYu][kStX];  // per row, per coarse x: (aux, correction) contracted over y, z
+    __shared__ unsigned char s_nz[kStYu][kStX];
     const int fx = blockIdx.x * blockDim.x + threadIdx.x;
-    const RowStage R = row_stage(F, C);
+    const RowStage R = row_stage<kStYu>(F, C);
     const bool act = fx < F.N && fx > 0 && R.fz > 0 && R.fz < F.N;
     // the fine vertices' loads first: they stream from HBM while the block stages
-    double u[kStY], dg[kStY], r[kStY];
+    double u[kStYu], dg[kStYu], r[kStYu];
     const int64_t vi0 = vidx3(F.N, min(fx, F.N), R.fy0, R.fz);
 #pragma unroll
-    for (int k = 0; k < kStY; ++k) {
+    for (int k = 0; k < kStYu; ++k) {
         const int fy = R.fy0 + k;
         if (act && fy < R.fy1 && fy > 0 && fy < F.N) {
             const int64_t vi = vi0 + static_cast<int64_t>(k) * (F.N + 1);
@@ -1770,7 +1774,7 @@ __global__ void __launch_bounds__(kStThreads) k3_update_fine_st(Lv3 F, Lv3 C, co
     }
     __syncthreads();
     const double wz0 = wax(R.lz, 0), wz1 = wax(R.lz, 1);
-    for (int k = warp; k < kStY; k += nwarp)  // a warp per fine row, lanes over the coarse x
+    for (int k = warp; k < kStYu; k += nwarp)  // a warp per fine row, lanes over the coarse x
         for (int j = lane; j < R.nx; j += 32) {
             const int fy = min(R.fy0 + k, F.N);
             const int py = owner3(fy, C.N), ly = fy - 3 * py, jy = py - R.py0;
@@ -1786,7 +1790,7 @@ __global__ void __launch_bounds__(kStThreads) k3_update_fine_st(Lv3 F, Lv3 C, co
     const int px = owner3(fx, C.N), lx = fx - 3 * px, jx = px - R.px0;
     const double wx0 = wax(lx, 0), wx1 = wax(lx, 1);
 #pragma unroll
-    for (int k = 0; k < kStY; ++k) {
+    for (int k = 0; k < kStYu; ++k) {
         const int fy = R.fy0 + k;
         if (!(fy < R.fy1 && fy > 0 && fy < F.N)) continue;
         const double2 g0 = s_g[k][jx], g1 = s_g[k][jx + 1];
@@ -1804,7 +1808,7 @@ __global__ void __launch_bounds__(kStThreads) k3_uhat_st(Lv3 F, Lv3 C) {
     __shared__ double s_u[kStCy][2][kStX];
     __shared__ double s_g[kStY][kStX];
     const int fx = blockIdx.x * blockDim.x + threadIdx.x;
-    const RowStage R = row_stage(F, C);
+    const RowStage R = row_stage<kStY>(F, C);
     double u[kStY];  // the fine loads first (see k3_update_fine_st)
     const int64_t vi0 = vidx3(F.N, min(fx, F.N), R.fy0, R.fz);
 #pragma unroll
@@ -2875,8 +2879,8 @@ private:
         else LZB_LAUNCH(k3_uhat_st, vgst(l, z0, z1), kStThreads, 0, s_, lvz(l, z0), lv(l - 1));
     }
     // the staged row kernels: 128 x, kStY rows, one plane per block
-    dim3 vgst(int l, int z0, int z1) const {
-        return dim3(blocks_for(L3_[l].N + 1, kStThreads), (L3_[l].N + kStY) / kStY, z1 - z0);
+    dim3 vgst(int l, int z0, int z1, int rows = kStY) const {
+        return dim3(blocks_for(L3_[l].N + 1, kStThreads), (L3_[l].N + rows) / rows, z1 - z0);
     }
     // the leaf level's fused update on vertex planes [z0, z1): the coarse
     // factors (aux correction, prolongated correction) once per coarse vertex,
@@ -2884,7 +2888,7 @@ private:
     void update_fine3(int z0, int z1, bool pi, double damping) {
         if (pre3_.n < static_cast<size_t>(L3_[D_ - 1].nv)) pre3_.alloc(L3_[D_ - 1].nv);
         LZB_LAUNCH(k3_coarse_pre, vg(D_ - 1), 128, 0, s_, lv(D_ - 1), omega_, pi ? 1 : 0, pre3_.p);
-        LZB_LAUNCH(k3_update_fine_st, vgst(D_, z0, z1), kStThreads, 0, s_, lvz(D_, z0), lv(D_ - 1), pre3_.p, pi ? 1 : 0,
+        LZB_LAUNCH(k3_update_fine_st, vgst(D_, z0, z1, kStYu), kStThreads, 0, s_, lvz(D_, z0), lv(D_ - 1), pre3_.p, pi ? 1 : 0,
                    damping);
     }
     DevBuf<double2> pre3_;
