@@ -1987,6 +1987,42 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_inject(AllLevels A, int
         __syncthreads();
     }
 }
+// the bottom of a V(nu, nu) cycle (Grid::vback_body) on the small levels lc..0
+// in one block: down (nu sweeps, residual, restriction into a zero-start
+// coarse problem), then up (prolongation against a zero snapshot, nu sweeps)
+// -- the per-level launches' bodies in their order, a block barrier between
+// passes. Level 0 has no interior vertex: nothing is smoothed there.
+__global__ void __launch_bounds__(kSmallThreads) k_small_v(AllLevels A, int lc, int nu, double omega, lzb_field f) {
+    lzb_pdl_enter();
+    for (int l = lc; l >= 1; --l) {
+        const LevelView F = A.L[l], C = A.L[l - 1];
+        for (int k = 0; k <= nu; ++k) {  // nu sweeps, then the residual that is restricted
+            LZB_FOR_VERTS(F, i) k_residual_body<true>(i, F, f);
+            __syncthreads();
+            if (k == nu) break;
+            LZB_FOR_VERTS(F, i) k_jacobi_body<true>(i, F, omega);
+            __syncthreads();
+        }
+        LZB_FOR_VERTS(C, i) {
+            k_restrict_body<true>(i, F, C, 0, 0.0);
+            C.v[LZB_V_U][i] = 0.0;
+        }
+        __syncthreads();
+    }
+    for (int l = 1; l <= lc; ++l) {
+        const LevelView F = A.L[l], C = A.L[l - 1];
+        LZB_FOR_VERTS(C, i) C.v[LZB_V_USNAP][i] = 0.0;
+        __syncthreads();
+        LZB_FOR_VERTS(F, i) k_prolong_body<true>(i, F, C);
+        __syncthreads();
+        for (int k = 0; k < nu; ++k) {
+            LZB_FOR_VERTS(F, i) k_residual_body<true>(i, F, f);
+            __syncthreads();
+            LZB_FOR_VERTS(F, i) k_jacobi_body<true>(i, F, omega);
+            __syncthreads();
+        }
+    }
+}
 #undef LZB_FOR_VERTS
 
 // ---- the middle levels of the update pass in three launches. Between the
@@ -3565,13 +3601,17 @@ public:
     };
     void vback_body() {
         UhatAlias alias(uhat_is_u_);
-        for (int l = D_; l >= 1; --l) {
+        // levels lc..0 (at most 10^2 vertices each) run the bottom of the V in one block
+        static const bool plain = std::getenv("LZB_PLAIN_VSMALL") != nullptr;
+        const int lc = plain ? 0 : std::max(small_lc(), 0);
+        for (int l = D_; l > lc; --l) {
             vsmooth(l, vnu_);
             vresidual(l);
             LZB_LAUNCH(k_restrict, vgrid(l - 1), kThreads, 0, s_, V(l), V(l - 1), 0, 0.0);  // fl = P^T r
             LZB_CUDA(cudaMemsetAsync(L_[l - 1].v[LZB_V_U].p, 0, L_[l - 1].v[LZB_V_U].bytes(), s_));
         }
-        for (int l = 1; l <= D_; ++l) {
+        if (lc >= 1) LZB_LAUNCH(k_small_v, 1, kSmallThreads, 0, s_, all_levels(), lc, vnu_, d_.omega, d_.field);
+        for (int l = lc + 1; l <= D_; ++l) {
             LZB_CUDA(cudaMemsetAsync(L_[l - 1].v[LZB_V_USNAP].p, 0, L_[l - 1].v[LZB_V_USNAP].bytes(), s_));
             LZB_LAUNCH(k_prolong, ugrid(l), kThreads, 0, s_, V(l), V(l - 1));
             vsmooth(l, vnu_);
