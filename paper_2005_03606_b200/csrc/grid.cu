@@ -1141,6 +1141,148 @@ __global__ void __launch_bounds__(kThreads, 3) k_residual_comp(LevelView F, lzb_
     F.v[LZB_V_DIAG][vi] = dg;
 }
 
+// The same residual, cell-centric and staged (the leaf level's kernel; the
+// per-vertex gather above stays as LZB_PLAIN_COMP=1). The gather read each
+// cell's record four times, a slot row per adjacent vertex, with ~36 global
+// load instructions per vertex: it ran at 94 % of the L1 / LSU throughput and
+// no faster than the FP64 rows it replaces. Here a block owns a tile of
+// 32 x 8 cells (31 x 7 vertices, the 3D residual's tiling): each cell thread
+// reads its own record once (16 W contiguous bytes, coalesced across the
+// warp), rebuilds the 16 entries as baseline + roundtrip, forms its four row
+// products K_row . u and K_row . u-hat from the staged vertex tile -- the
+// per-vertex kernel's products, entry by entry in its order -- and stages them
+// with the diagonal entries; the vertex threads then subtract them in the
+// creation-rank order. Same bits (tests/test_gpu_grid.py
+// test_compressed_residual_bit_identical).
+// PlaneDec(W) with the width at compile time (a record coded at the planes'
+// own width, the common case: every record of a fixed-width sweep): for words
+// of at most 4 bytes the exponent | fraction bits are contiguous, one shift
+// puts them at bit 20 of the high half and one add rebiases the exponent
+// (grid3.cu's SrcComp<W>::dec).
+template <int W>
+__device__ __forceinline__ double plane_dec_fixed(unsigned long long w64) {
+    if constexpr (W == 8) {
+        return __longlong_as_double(static_cast<long long>(w64));
+    } else if constexpr (W <= 4) {
+        const uint32_t w = static_cast<uint32_t>(w64);
+        constexpr int m = 8 * (W - 1) - 1;
+        constexpr uint32_t body = (1u << (8 * W - 1)) - 1u;
+        const uint32_t mag = w & body;
+        const uint32_t hi = (m > 20 ? mag >> (m - 20) : mag << (20 - m)) + (895u << 20);
+        const uint32_t sg = (w >> (8 * W - 1)) << 31;
+        const uint32_t lo = m > 20 ? w << (52 - m) : 0u;
+        return w == 0 ? 0.0 : __hiloint2double(static_cast<int>(hi | sg), static_cast<int>(lo));
+    } else {
+        return PlaneDec(W)(w64);
+    }
+}
+constexpr int kCsX = 32, kCsY = 8;
+template <int W>
+__global__ void __launch_bounds__(kCsX * kCsY) k_residual_comp_st(LevelView F, lzb_field f,
+                                                                  const double* __restrict__ cxp,
+                                                                  const double* __restrict__ cyp, int r0, int r1) {
+    lzb_pdl_enter();
+    __shared__ double s_u[2][kCsY + 1][kCsX + 1];
+    __shared__ double s_a[3][4][kCsX * kCsY];  // K_row . u, K_row . u-hat, K[row][row] per cell
+    const int t = threadIdx.x, tx = t % kCsX, ty = t / kCsX;
+    const int N = F.N, NV = N + 1;
+    const int X0 = blockIdx.x * (kCsX - 1), Y0 = r0 + blockIdx.y * (kCsY - 1);  // the tile's first vertex
+    for (int k = t; k < (kCsY + 1) * (kCsX + 1); k += kCsX * kCsY) {
+        const int j = k / (kCsX + 1), i = k - j * (kCsX + 1);
+        const int x = min(max(X0 - 1 + i, 0), N), y = min(max(Y0 - 1 + j, 0), N);
+        const int64_t cv = static_cast<int64_t>(y) * NV + x;
+        s_u[0][j][i] = F.v[LZB_V_U][cv];
+        s_u[1][j][i] = F.v[LZB_V_UHAT][cv];
+    }
+    const int cx = X0 - 1 + tx, cy = Y0 - 1 + ty;
+    const bool cell = cx >= 0 && cy >= 0 && cx < N && cy < N;
+    uint32_t rw[4 * W];  // the record: 16 slots of W bytes
+    int cp = -1;
+    double e = 0.0;
+    if (cell) {
+        const int64_t c = static_cast<int64_t>(cy) * N + cx;
+        const uint4* src = reinterpret_cast<const uint4*>(F.cplanes + c * 16 * W);
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            const uint4 v = __ldcs(src + j);
+            rw[4 * j] = v.x;
+            rw[4 * j + 1] = v.y;
+            rw[4 * j + 2] = v.z;
+            rw[4 * j + 3] = v.w;
+        }
+        cp = F.cp3[c];  // -1: bottom (baseline), 0..W: slots, > W: FP64 row
+        e = field_combine(f, cxp[cx], cyp[cy]);  // eps(centre), the n = 1 sample
+    }
+    __syncthreads();
+    if (cell) {
+#pragma unroll
+        for (int row = 0; row < 4; ++row) {
+            double Kr[4];
+            if (cp < 0) {
+                for (int col = 0; col < 4; ++col) Kr[col] = baseline_entry(row * 4 + col, F.geo0 ? 1.0 : e);
+            } else if (cp == W) {  // coded at the planes' width: compile-time decode
+#pragma unroll
+                for (int col = 0; col < 4; ++col)
+                    Kr[col] = baseline_entry(row * 4 + col, e) + plane_dec_fixed<W>(slot_bytes<W>(rw + row * W, col));
+            } else if (cp <= W) {
+                const PlaneDec dec(cp);
+#pragma unroll
+                for (int col = 0; col < 4; ++col)
+                    Kr[col] = baseline_entry(row * 4 + col, e) + dec(slot_bytes<W>(rw + row * W, col));
+            } else {  // record wider than a slot: the FP64 row
+                const double* src = F.op + 16 * (static_cast<int64_t>(cy) * N + cx) + 4 * row;
+                for (int col = 0; col < 4; ++col) Kr[col] = src[col];
+            }
+            double su = 0.0, sh = 0.0;
+#pragma unroll
+            for (int col = 0; col < 4; ++col) {
+                su += Kr[col] * s_u[0][ty + cdy(col)][tx + cdx(col)];
+                sh += Kr[col] * s_u[1][ty + cdy(col)][tx + cdx(col)];
+            }
+            s_a[0][row][t] = su;
+            s_a[1][row][t] = sh;
+            s_a[2][row][t] = Kr[row];
+        }
+    }
+    __syncthreads();
+    const int ix = X0 + tx, iy = Y0 + ty;
+    if (tx >= kCsX - 1 || ty >= kCsY - 1 || ix > N || iy >= r1 || iy > N) return;
+    const int64_t vi = static_cast<int64_t>(iy) * NV + ix;
+    bool has[4];
+    has[0] = ix >= 1 && iy >= 1;
+    has[1] = ix < N && iy >= 1;
+    has[2] = ix >= 1 && iy < N;
+    has[3] = ix < N && iy < N;
+    double au[4], auh[4], kd[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int a = q & 1, b = q >> 1, row = (1 - a) + 2 * (1 - b);
+        const int ci = (ty + b) * kCsX + tx + a;  // the cell (ix - 1 + a, iy - 1 + b) in the tile
+        au[q] = s_a[0][row][ci];
+        auh[q] = s_a[1][row][ci];
+        kd[q] = s_a[2][row][ci];
+    }
+    const double fl = F.v[LZB_V_FL][vi];
+    const bool both = has[0] && has[3];
+    const bool swap12 = both && !(crank(F, ix, iy - 1) < crank(F, ix - 1, iy));
+    const double a1 = swap12 ? au[2] : au[1], a2 = swap12 ? au[1] : au[2];
+    const double h1 = swap12 ? auh[2] : auh[1], h2 = swap12 ? auh[1] : auh[2];
+    const double d1 = swap12 ? kd[2] : kd[1], d2 = swap12 ? kd[1] : kd[2];
+    const bool e1 = swap12 ? has[2] : has[1], e2 = swap12 ? has[1] : has[2];
+    double r = fl, rh = fl, dg = 0.0;
+    if (has[0]) { r -= au[0]; rh -= auh[0]; dg += kd[0]; }
+    if (e1) { r -= a1; rh -= h1; dg += d1; }
+    if (e2) { r -= a2; rh -= h2; dg += d2; }
+    if (has[3]) { r -= au[3]; rh -= auh[3]; dg += kd[3]; }
+    if (boundary(N, ix, iy)) {
+        r = 0.0;
+        rh = 0.0;
+    }
+    F.v[LZB_V_R][vi] = r;
+    F.v[LZB_V_RHAT][vi] = rh;
+    F.v[LZB_V_DIAG][vi] = dg;
+}
+
 // Restriction fl_{l-1} += P^T rhat_l over owned lattice vertices
 // (solver.cpp:177-200), gathered per coarse vertex in (cell rank, L) order.
 // mode 0: rhs restriction of rhat into fl; mode 1: adaFAC-Jac smoothed
@@ -3287,14 +3429,22 @@ public:
         const dim3 g = vgrid_rows(D_, r0, r1);
         const LevelView F = Vrow(D_, r0);
         const double *cx = centre_[1].x.p, *cy = centre_[1].y.p;
+        static const bool plain = std::getenv("LZB_PLAIN_COMP") != nullptr;
+        // staged cell-centric kernel: tiles of 31 x 7 vertices over rows [r0, r1)
+        const dim3 gs((L_[D_].N + 1 + kCsX - 2) / (kCsX - 1), (r1 - r0 + kCsY - 2) / (kCsY - 1));
+        const LevelView Fw = V(D_);
+        auto comp = [&](auto gather, auto staged) {
+            if (plain) LZB_LAUNCH(gather, g, kThreads, 0, s_, F, d_.field, cx, cy);
+            else LZB_LAUNCH(staged, gs, kCsX * kCsY, 0, s_, Fw, d_.field, cx, cy, r0, r1);
+        };
         switch (d_.plane_width) {
             case 0: LZB_LAUNCH(k_residual, g, kThreads, 0, s_, F, d_.field); break;
-            case 2: LZB_LAUNCH(k_residual_comp<2>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
-            case 3: LZB_LAUNCH(k_residual_comp<3>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
-            case 4: LZB_LAUNCH(k_residual_comp<4>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
-            case 5: LZB_LAUNCH(k_residual_comp<5>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
-            case 6: LZB_LAUNCH(k_residual_comp<6>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
-            case 7: LZB_LAUNCH(k_residual_comp<7>, g, kThreads, 0, s_, F, d_.field, cx, cy); break;
+            case 2: comp(k_residual_comp<2>, k_residual_comp_st<2>); break;
+            case 3: comp(k_residual_comp<3>, k_residual_comp_st<3>); break;
+            case 4: comp(k_residual_comp<4>, k_residual_comp_st<4>); break;
+            case 5: comp(k_residual_comp<5>, k_residual_comp_st<5>); break;
+            case 6: comp(k_residual_comp<6>, k_residual_comp_st<6>); break;
+            case 7: comp(k_residual_comp<7>, k_residual_comp_st<7>); break;
             case 8:
             // W = 8: a slot row is as wide as the FP64 row, which the residual reads
             default: LZB_LAUNCH(k_residual, g, kThreads, 0, s_, F, d_.field); break;
