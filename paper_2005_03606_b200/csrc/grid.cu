@@ -2192,27 +2192,44 @@ __device__ __forceinline__ bool mid_locate(const MidRange& R, int64_t t, int& l,
 // usnap = u; aux = the injected residual of the level above (adaFAC-PI), else 0.
 // lc_aux >= 0: also the injection into level lc_aux (the top small level,
 // snapshot already taken by k_small_snap) -- its indices follow level l1's.
-__global__ void k_mid_snap(AllLevels A, MidRange R, int pi, int lc_aux, int64_t n_lc) {
-    lzb_pdl_enter();
-    const int64_t t = gtid();
-    int l;
-    int64_t i;
-    if (mid_locate(R, t, l, i)) {
-        k_snap_body<true>(i, A.L[l]);
-        if (pi) k_aux_inject_body<true>(i, A.L[l + 1], A.L[l]);
-        return;
-    }
-    const int64_t j = t - R.start[R.l1 + 1];
-    if (pi && lc_aux >= 0 && j < n_lc) k_aux_inject_body<true>(j, A.L[lc_aux + 1], A.L[lc_aux]);
-}
-// the aux correction (adaFAC-PI) and the Jacobi step of levels l0..l1
-__global__ void k_mid_update(AllLevels A, MidRange R, int pi, double omega, Damp dm) {
+// R covers levels 0..l1 here: the small levels' snapshot (k_small_snap) rides
+// along; their injections (levels below lc_aux) stay in k_small_back, which
+// runs them in the per-level order after this kernel.
+__global__ void k_mid_snap(AllLevels A, MidRange R, int pi, int lc_aux) {
     lzb_pdl_enter();
     int l;
     int64_t i;
     if (!mid_locate(R, gtid(), l, i)) return;
+    k_snap_body<true>(i, A.L[l]);
+    if (pi && l >= lc_aux && l >= 0) k_aux_inject_body<true>(i, A.L[l + 1], A.L[l]);
+}
+// the aux correction (adaFAC-PI) and the Jacobi step of levels l0..l1
+// (and, adaFAC-PI, k_scale_aux of level l1 = D - 1 for the leaf update: it
+// reads that level's aux and diagonal, which nothing here writes)
+__global__ void k_mid_update(AllLevels A, MidRange R, int pi, double omega, Damp dm, double* __restrict__ caux) {
+    lzb_pdl_enter();
+    int l;
+    int64_t i;
+    if (!mid_locate(R, gtid(), l, i)) return;
+    if (pi && l == R.l1) {
+        const LevelView C = A.L[l];
+        const int NV = C.N + 1;
+        const int cy = static_cast<int>(i / NV), cx = static_cast<int>(i - static_cast<int64_t>(cy) * NV);
+        const double cdg = C.v[LZB_V_DIAG][i];
+        caux[i] = (!boundary(C.N, cx, cy) && cdg != 0.0) ? omega / cdg * C.v[LZB_V_AUX][i] : 0.0;
+    }
     if (pi && l > 0) k_aux_sub_body<true>(i, A.L[l], A.L[l - 1], omega);
     k_jacobi_body<true>(i, A.L[l], dm.d[l]);
+}
+// u-hat of levels l0..l1 (compute_uhat, solver.cpp:120-143): u of every level
+// is fixed during the residual pass, so the middle levels' u-hat do not wait
+// for the restriction chain
+__global__ void k_mid_uhat(AllLevels A, MidRange R) {
+    lzb_pdl_enter();
+    int l;
+    int64_t i;
+    if (!mid_locate(R, gtid(), l, i)) return;
+    k_uhat_body<true>(i, A.L[l], A.L[l > 0 ? l - 1 : 0], l > 0 ? 1 : 0);
 }
 // inject_solution of levels l0..l1 from the leaf level (level l's vertex v is
 // leaf vertex 3^(D-l) v; the per-level chain copies the same value down)
@@ -3182,20 +3199,20 @@ public:
         const int lc = small_lc(), l0 = lc + 1, l1 = D_ - 1;
         const bool pi = d_.variant == LZB_ADAFAC_PI;
         const MidRange R = mid_range(l0, l1);
-        const int64_t nmid = R.start[l1 + 1], n_lc = lc >= 0 ? static_cast<int64_t>(L_[lc].nv) : 0;
+        const int64_t nmid = R.start[l1 + 1];
         Damp dm{};
         for (int l = 0; l <= D_; ++l) dm.d[l] = damping(l);
-        if (lc >= 0) LZB_LAUNCH(k_small_snap, 1, kSmallThreads, 0, s_, all_levels(), lc);
-        LZB_LAUNCH(k_mid_snap, blocks_for(nmid + n_lc, kThreads), kThreads, 0, s_, all_levels(), R, pi ? 1 : 0, lc,
-                   n_lc);
+        // snapshots of every level below the leaves, the injected residuals of levels lc..D-1
+        const MidRange Rs = mid_range(0, l1);
+        LZB_LAUNCH(k_mid_snap, blocks_for(Rs.start[l1 + 1], kThreads), kThreads, 0, s_, all_levels(), Rs, pi ? 1 : 0,
+                   std::max(lc, 0));
         LZB_LAUNCH(k_mid_update, blocks_for(nmid, kThreads), kThreads, 0, s_, all_levels(), R, pi ? 1 : 0, d_.omega,
-                   dm);
+                   dm, caux_.p);
         if (lc >= 0)
             LZB_LAUNCH(k_small_back, 1, kSmallThreads, 0, s_, all_levels(), lc, static_cast<int>(d_.variant),
                        d_.omega, dm, d_.field);
         for (int l = std::max(lc, 0) + 1; l <= D_ - 1; ++l)
             LZB_LAUNCH(k_prolong, ugrid(l), kThreads, 0, s_, V(l), V(l - 1));
-        if (pi) LZB_LAUNCH(k_scale_aux, vgrid(D_ - 1), kThreads, 0, s_, V(D_ - 1), d_.omega, caux_.p);
         LZB_LAUNCH(k_update_fine, vgrid(D_), kThreads, 0, s_, V(D_), V(D_ - 1), pi ? caux_.p : nullptr,
                    damping(D_));
         // injection: levels D-1 .. max(lc, 0) straight from the leaves, then the small levels' chain
@@ -3461,9 +3478,16 @@ public:
 
     void residual_launches() {  // solver.cpp:145-210
         const int lc = small_lc();
+        static const bool plain = std::getenv("LZB_PLAIN_BACK") != nullptr;
+        const bool mid = !plain && lc + 1 <= D_ - 1 && D_ + 1 < kMaxLevels;  // one launch for the middle levels' u-hat
+        if (mid) {
+            const MidRange R = mid_range(lc + 1, D_ - 1);
+            LZB_LAUNCH(k_mid_uhat, blocks_for(R.start[D_], kThreads), kThreads, 0, s_, all_levels(), R);
+        }
         for (int l = D_; l > lc; --l) {
             const dim3 g = vgrid(l);
-            LZB_LAUNCH(k_uhat, ugrid(l), kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
+            if (!mid || l == D_)
+                LZB_LAUNCH(k_uhat, ugrid(l), kThreads, 0, s_, V(l), l > 0 ? V(l - 1) : V(l), l > 0 ? 1 : 0);
             if (l == D_) leaf_residual(0, L_[D_].N + 1);
             else LZB_LAUNCH(k_residual, g, kThreads, 0, s_, V(l), d_.field);
             if (l > 0)
