@@ -660,9 +660,11 @@ def run_ours(args, world, rank, local):
         c5["cycles"] = {"mode": f"z-slabs over {world} ranks, C++ data plane: NCCL halos / broadcasts / all-reduce",
                         "scaling": "strong"}
     else:
-        g5.step()  # builds the coarse operators
+        # the first cycle also forms the Galerkin coarse operators (the level-5 product
+        # reads all 84 GB of leaf planes) and the leaf Jacobi diagonal: the per-assembly set-up
+        t5first = timed_steps(lambda: g5.step(), 1)
         t5c = timed_steps(lambda: g5.step(), 3) / 3
-        c5["cycles"] = {"mode": "one GPU"}
+        c5["cycles"] = {"mode": "one GPU", "first_cycle_ms_incl_coarse_operators": 1e3 * t5first}
     t5c = max_over_ranks(t5c, world)
     c5["cycles"].update({"ms_per_cycle": 1e3 * t5c, "dof_updates_per_s": (3 ** 6 - 1) ** 3 / t5c})
     nv5, nc5 = (3 ** 6 + 1) ** 3, 3 ** 18
