@@ -521,6 +521,12 @@ struct Src64 {
         double v[27];
     };
     __device__ __forceinline__ double at(int64_t c, int q) const { return __ldg(op + q * nc + plane_sidx(c, N, xp, woff)); }
+    // the same from the cell's coordinates (Nl cells per axis): no 64-bit divisions
+    __device__ __forceinline__ double at_xyz(int cx, int cy, int cz, int Nl, int q) const {
+        const int64_t sc = xp ? (static_cast<int64_t>(cz) * (N + 1) + cy + 1) * xp + cx + 1 - woff
+                              : (static_cast<int64_t>(cz) * Nl + cy) * Nl + cx;
+        return __ldg(op + q * nc + sc);
+    }
     __device__ __forceinline__ void load27(int64_t c, double* v) const {
         const int64_t s = plane_sidx(c, N, xp, woff);
 #pragma unroll
@@ -575,6 +581,9 @@ struct SrcComp {
         const Base3 B(r.e, P.s1, P.h);
 #pragma unroll
         for (int q = 0; q < 27; ++q) v[q] = B(q / 9, (q / 3) % 3, q % 3) + dec(r.w[q]);
+    }
+    __device__ __forceinline__ double at_xyz(int cx, int cy, int cz, int Nl, int q) const {
+        return at((static_cast<int64_t>(cz) * Nl + cy) * Nl + cx, q);
     }
     __device__ __forceinline__ double at(int64_t c, int q) const {  // one class value
         const int64_t sc = plane_sidx(c, P.N, P.xp, P.woff);
@@ -1203,7 +1212,7 @@ __global__ void k3_leaf_diag(Lv3 F, Src S) {
         const int row = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
         const int cx = ix - 1 + dx, cy = iy - 1 + dy, cz = iz - 1 + dz;
         if (cx < 0 || cy < 0 || cz < 0 || cx >= N || cy >= N || cz >= N) continue;
-        dg += S.at((static_cast<int64_t>(cz) * N + cy) * N + cx, cls3(row, row));
+        dg += S.at_xyz(cx, cy, cz, N, cls3(row, row));
     }
     F.v[LZB_V_DIAG][vi] = dg;
 }
