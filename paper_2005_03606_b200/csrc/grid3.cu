@@ -828,8 +828,13 @@ __global__ void __launch_bounds__(128, MINB) k_assemble3(Field3 Fin, int N, doub
     if (KIND >= 0) F.kind = KIND;
     const int64_t c = cbeg + gtid();  // cells [cbeg, cend): whole z planes
     if (c >= cend) return;
-    const int cx = static_cast<int>(c % N), cy = static_cast<int>((c / N) % N), cz = static_cast<int>(c / N / N);
-    const int64_t nc = PL.nc, sc = plane_sidx(c, PL.N, PL.xp, PL.woff);  // storage of the planes
+    // (a level has at most 729^3 < 2^31 cells: 32-bit divisions; the storage index
+    // straight from the coordinates -- the 64-bit divisions were ~10 % of the p <= 2 kernel)
+    const uint32_t cu = static_cast<uint32_t>(c), tq = cu / static_cast<uint32_t>(N);
+    const int cx = static_cast<int>(cu - tq * N), cz = static_cast<int>(tq / static_cast<uint32_t>(N)),
+              cy = static_cast<int>(tq - static_cast<uint32_t>(cz) * N);
+    const int64_t nc = PL.nc;
+    const int64_t sc = PL.xp ? (static_cast<int64_t>(cz) * (PL.N + 1) + cy + 1) * PL.xp + cx + 1 - PL.woff : c;
     const double x0 = cx * h, y0 = cy * h, z0 = cz * h;
     const double e = NS > 0 ? grf_centre<false>(F, x0, y0, z0, h) : centre_eps3(F, x0, y0, z0, h);
     const Base3 B(e, PL.s1, h);  // A(n=1): eps(centre) * unit stiffness
