@@ -126,6 +126,11 @@ struct DevBuf {
         p = nullptr;
         n = 0;
     }
+    // alloc(count) unless the buffer already has exactly that size (contents kept then):
+    // a multi-GB cudaFree + cudaMalloc pair costs milliseconds
+    void ensure(size_t count) {
+        if (n != count || (count && !p)) alloc(count);
+    }
     size_t bytes() const { return n * sizeof(T); }
 };
 

@@ -802,13 +802,13 @@ public:
                 L.box[2 * d] = hi[d] < 0 ? 0 : lo[d];
                 L.box[2 * d + 1] = hi[d] < 0 ? 1 : hi[d] + 2;  // empty level: one (absent) vertex
             }
-            L.load.alloc(L.nv);
-            L.vk.alloc(L.nv);
+            L.load.ensure(L.nv);  // fixed sizes per level: allocated once, re-zeroed below
+            L.vk.ensure(L.nv);
             // kinds outside the launch box stay "outside" (read by injection across levels)
             LZB_CUDA(cudaMemsetAsync(L.vk.p, 0, L.vk.bytes(), s_));
             LZB_CUDA(cudaMemsetAsync(L.load.p, 0, L.load.bytes(), s_));
-            L.cf.alloc(L.nc);
-            L.oi.alloc(L.nc + 1);
+            L.cf.ensure(L.nc);
+            L.oi.ensure(L.nc + 1);
             LZB_CUDA(cudaMemsetAsync(L.cf.p, 0, L.cf.bytes(), s_));
         }
         // cell flags: leaves, then the refined parents level by level
@@ -819,14 +819,14 @@ public:
         // dense cell -> operator slot (exclusive scan of existence), slot counts
         for (int l = 0; l <= D; ++l) {
             LevA& L = A_[l];
-            DevBuf<int32_t> e01;
-            e01.alloc(L.nc + 1);
+            DevBuf<int32_t>& e01 = scan_in_;  // scratch of the finest level's size, kept across calls
+            if (e01.n < static_cast<size_t>(L.nc + 1)) e01.alloc(A_[D].nc + 1);
             LZB_CUDA(cudaMemsetAsync(e01.p + L.nc, 0, sizeof(int32_t), s_));
             LZB_LAUNCH(k4_exist01, blocks_for(L.nc, 256), 256, 0, s_, L.cf.p, L.nc, e01.p);
             size_t tb = 0;
             LZB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, e01.p, L.oi.p, static_cast<int>(L.nc + 1), s_));
-            DevBuf<unsigned char> tmp;
-            tmp.alloc(tb);
+            DevBuf<unsigned char>& tmp = scan_tmp_;
+            if (tmp.n < tb) tmp.alloc(tb);
             LZB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, e01.p, L.oi.p, static_cast<int>(L.nc + 1), s_));
             int32_t cnt = 0;
             LZB_CUDA(cudaMemcpyAsync(&cnt, L.oi.p + L.nc, sizeof(int32_t), cudaMemcpyDeviceToHost, s_));
@@ -861,10 +861,11 @@ public:
                          std::chrono::duration<double, std::milli>(t - t_prev).count());
             t_prev = t;
         };
-        std::vector<DevBuf<uint8_t>> existed(cyc ? lmax_ + 1 : 0);
+        std::vector<DevBuf<uint8_t>>& existed = existed_;  // kept across events (fixed sizes per level)
+        if (cyc && existed.size() != static_cast<size_t>(lmax_ + 1)) existed.resize(lmax_ + 1);
         if (cyc)
             for (int l = 0; l <= lmax_; ++l) {
-                existed[l].alloc(A_[l].nv);
+                existed[l].ensure(A_[l].nv);
                 LZB_LAUNCH(k4_existed, blocks_for(A_[l].nv, 256), 256, 0, s_, lv(l), existed[l].p);
             }
         // the new leaf set, level-major, from the old one: a leaf that meets the
@@ -1151,6 +1152,9 @@ private:
     int64_t n_leaves_ = 0, n_shell_ = 0;
     DevBuf<double> table_, op_;
     DevBuf<int4> dleaves_;
+    std::vector<DevBuf<uint8_t>> existed_;  // refine(): which vertices existed before the event
+    DevBuf<int32_t> scan_in_;          // setup_levels scratch (existence flags of a level's cells)
+    DevBuf<unsigned char> scan_tmp_;   // cub scan workspace
     DevBuf<int32_t> shell_, n_;
     DevBuf<int8_t> p3_;
     DevBuf<unsigned long long> stats_;
