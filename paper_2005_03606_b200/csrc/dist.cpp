@@ -493,7 +493,7 @@ using namespace lzb;
 
 extern "C" {
 
-int lzb_nccl_unique_id(uint8_t* out128) {
+int lzb_nccl_unique_id(uint8_t* out128) { LZB_RANGE("lzb_nccl_unique_id");
     return guarded([&] {
         ncclUniqueId id;
         nc(nccl().GetUniqueId(&id), "ncclGetUniqueId");
@@ -501,7 +501,7 @@ int lzb_nccl_unique_id(uint8_t* out128) {
     });
 }
 
-int lzb_ctx_comm_init(lzb_ctx* ctx, const uint8_t* id128, int nranks, int rank) {
+int lzb_ctx_comm_init(lzb_ctx* ctx, const uint8_t* id128, int nranks, int rank) { LZB_RANGE("lzb_ctx_comm_init");
     return guarded([&] {
         if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(LZB_ERR_INVALID, "bad rank / nranks");
         release_comm(ctx);
@@ -532,7 +532,7 @@ int lzb_grid_dist_cycle(lzb_grid* g, lzb_cycle_report* out) {
     });
 }
 
-int lzb_grid_dist_cycle_loopback(lzb_grid* const* slabs, int nslabs, lzb_cycle_report* out) {
+int lzb_grid_dist_cycle_loopback(lzb_grid* const* slabs, int nslabs, lzb_cycle_report* out) { LZB_RANGE("lzb_grid_dist_cycle_loopback");
     return guarded([&] {
         std::vector<GridRef> s;
         for (int i = 0; i < nslabs; ++i) s.push_back(GridRef::of(slabs[i]));
@@ -542,7 +542,7 @@ int lzb_grid_dist_cycle_loopback(lzb_grid* const* slabs, int nslabs, lzb_cycle_r
     });
 }
 
-int lzb_grid_dist_assemble(lzb_grid* g, int n) {
+int lzb_grid_dist_assemble(lzb_grid* g, int n) { LZB_RANGE("lzb_grid_dist_assemble");
     return guarded([&] {
         std::vector<GridRef> s{GridRef::of(g)};
         NcclTransport x(s[0].ctx);
@@ -550,7 +550,7 @@ int lzb_grid_dist_assemble(lzb_grid* g, int n) {
     });
 }
 
-int lzb_grid_dist_assemble_loopback(lzb_grid* const* slabs, int nslabs, int n) {
+int lzb_grid_dist_assemble_loopback(lzb_grid* const* slabs, int nslabs, int n) { LZB_RANGE("lzb_grid_dist_assemble_loopback");
     return guarded([&] {
         std::vector<GridRef> s;
         for (int i = 0; i < nslabs; ++i) s.push_back(GridRef::of(slabs[i]));
@@ -559,7 +559,7 @@ int lzb_grid_dist_assemble_loopback(lzb_grid* const* slabs, int nslabs, int n) {
 }
 
 int lzb_grid3_create_slab(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3,
-                          int plane_width, int nslabs, int slab, lzb_grid3** out) {
+                          int plane_width, int nslabs, int slab, lzb_grid3** out) { LZB_RANGE("lzb_grid3_create_slab");
     return guarded([&] {
         if (depth < 1 || depth > 6) throw Error(LZB_ERR_INVALID, "slab grids need depth in 1..6");
         if (nslabs < 1 || slab < 0 || slab >= nslabs) throw Error(LZB_ERR_INVALID, "bad slab / nslabs");
@@ -582,7 +582,7 @@ int lzb_grid3_dist_cycle(lzb_grid3* g, lzb_cycle_report* out) {
     });
 }
 
-int lzb_grid3_dist_cycle_loopback(lzb_grid3* const* slabs, int nslabs, lzb_cycle_report* out) {
+int lzb_grid3_dist_cycle_loopback(lzb_grid3* const* slabs, int nslabs, lzb_cycle_report* out) { LZB_RANGE("lzb_grid3_dist_cycle_loopback");
     return guarded([&] {
         std::vector<GridRef> s;
         for (int i = 0; i < nslabs; ++i) s.push_back(GridRef::of(slabs[i]));
@@ -592,7 +592,7 @@ int lzb_grid3_dist_cycle_loopback(lzb_grid3* const* slabs, int nslabs, lzb_cycle
     });
 }
 
-int lzb_grid3_dist_assemble(lzb_grid3* g, int n) {
+int lzb_grid3_dist_assemble(lzb_grid3* g, int n) { LZB_RANGE("lzb_grid3_dist_assemble");
     return guarded([&] {
         std::vector<GridRef> s{GridRef::of(g)};
         NcclTransport x(s[0].ctx);
@@ -601,7 +601,7 @@ int lzb_grid3_dist_assemble(lzb_grid3* g, int n) {
     });
 }
 
-int lzb_grid3_dist_assemble_loopback(lzb_grid3* const* slabs, int nslabs, int n) {
+int lzb_grid3_dist_assemble_loopback(lzb_grid3* const* slabs, int nslabs, int n) { LZB_RANGE("lzb_grid3_dist_assemble_loopback");
     return guarded([&] {
         std::vector<GridRef> s;
         for (int i = 0; i < nslabs; ++i) s.push_back(GridRef::of(slabs[i]));

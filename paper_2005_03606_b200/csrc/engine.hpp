@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstdint>
@@ -73,6 +74,17 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
         ::lzb::g_launches.fetch_add(1, std::memory_order_relaxed);                                  \
         ::lzb::cuda_check(cudaGetLastError(), #kernel);                                             \
     } while (0)
+
+// NVTX range per C-ABI phase call and per cycle graph (tracing).
+// nvtx3 is header-only; without a profiler attached a push/pop is one
+// indirect call through a null-initialised table.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define LZB_RANGE(name) ::lzb::NvtxRange lzb_nvtx_range_(name)
 
 template <typename F>
 int guarded(F&& f) {

@@ -3142,6 +3142,8 @@ public:
             return;
         }
         const int slot = &exec == &g_coarse_ ? 0 : &exec == &g_front_ ? 1 : &exec == &g_back_ ? 2 : &exec == &g_vfront_ ? 3 : &exec == &g_vback_ ? 4 : 5;
+        static const char* const kSlotName[6] = {"cycle:coarse", "cycle:front", "cycle:back", "vcycle:down", "vcycle:up", "cycle:graph"};
+        LZB_RANGE(kSlotName[slot]);
         if (!exec) {
             cudaGraph_t g = nullptr;
             const uint64_t l0 = g_launches.load();
@@ -4722,7 +4724,7 @@ using namespace lzb;
 
 extern "C" {
 
-int lzb_grid_create(lzb_ctx* ctx, const lzb_grid_desc* desc, lzb_grid** out) {
+int lzb_grid_create(lzb_ctx* ctx, const lzb_grid_desc* desc, lzb_grid** out) { LZB_RANGE("lzb_grid_create");
     return guarded([&] {
         auto* g = new lzb_grid{nullptr};
         try {
@@ -4739,26 +4741,26 @@ void lzb_grid_destroy(lzb_grid* g) {
     delete g->g;
     delete g;
 }
-int lzb_grid_init_noise(lzb_grid* g, uint64_t seed) { return guarded([&] { g->g->unsettle(); g->g->init_noise(seed); }); }
-int lzb_grid_eager_setup(lzb_grid* g) {
+int lzb_grid_init_noise(lzb_grid* g, uint64_t seed) { LZB_RANGE("lzb_grid_init_noise"); return guarded([&] { g->g->unsettle(); g->g->init_noise(seed); }); }
+int lzb_grid_eager_setup(lzb_grid* g) { LZB_RANGE("lzb_grid_eager_setup");
     return guarded([&] { g->g->unsettle();
         g->g->eager_setup();
         g->g->sync_check();
     });
 }
-int lzb_grid_assemble_rows(lzb_grid* g, int n, int row0, int row1) {
+int lzb_grid_assemble_rows(lzb_grid* g, int n, int row0, int row1) { LZB_RANGE("lzb_grid_assemble_rows");
     return guarded([&] { g->g->unsettle();
         g->g->assemble_fixed_rows(n, row0, row1);
         g->g->sync_check();
     });
 }
-int lzb_grid_assemble_fixed_raw(lzb_grid* g, int n, double* host_raw) {
+int lzb_grid_assemble_fixed_raw(lzb_grid* g, int n, double* host_raw) { LZB_RANGE("lzb_grid_assemble_fixed_raw");
     return guarded([&] { g->g->unsettle(); g->g->assemble_fixed_raw(n, host_raw); });
 }
-int lzb_grid_publish_level(lzb_grid* g, int level, const double* mats, const int32_t* n, int32_t p1) {
+int lzb_grid_publish_level(lzb_grid* g, int level, const double* mats, const int32_t* n, int32_t p1) { LZB_RANGE("lzb_grid_publish_level");
     return guarded([&] { g->g->unsettle(); g->g->publish_level(level, mats, n, p1); });
 }
-int lzb_grid_vertex_stencils(lzb_grid* g, int level, int require_payload, double* out) {
+int lzb_grid_vertex_stencils(lzb_grid* g, int level, int require_payload, double* out) { LZB_RANGE("lzb_grid_vertex_stencils");
     return guarded([&] { g->g->unsettle(); g->g->vertex_stencils(level, require_payload, out); });
 }
 int lzb_scatter_row(const double* element16, int corner, double* stencil9) {
@@ -4779,24 +4781,24 @@ int lzb_grid_cell_arrays(lzb_grid* g, int level, void** op, void** p1, void** n,
                          void** chg) {
     return guarded([&] { g->g->unsettle(); g->g->cell_arrays(level, op, p1, n, p3, epoch, chg); });
 }
-int lzb_grid_assemble_fixed(lzb_grid* g, int n) {
+int lzb_grid_assemble_fixed(lzb_grid* g, int n) { LZB_RANGE("lzb_grid_assemble_fixed");
     return guarded([&] { g->g->unsettle();
         g->g->assemble_fixed(n);
         g->g->sync_check();
     });
 }
-int lzb_grid_step(lzb_grid* g, lzb_cycle_report* out) { return guarded([&] { *out = g->g->step(); }); }
-int lzb_grid_vcycle(lzb_grid* g, int nu, lzb_cycle_report* out) {
+int lzb_grid_step(lzb_grid* g, lzb_cycle_report* out) { LZB_RANGE("lzb_grid_step"); return guarded([&] { *out = g->g->step(); }); }
+int lzb_grid_vcycle(lzb_grid* g, int nu, lzb_cycle_report* out) { LZB_RANGE("lzb_grid_vcycle");
     return guarded([&] { g->g->unsettle(); *out = g->g->vcycle(nu); });
 }
-int lzb_grid_run(lzb_grid* g, lzb_cycle_report* out, int cap, int* count) {
+int lzb_grid_run(lzb_grid* g, lzb_cycle_report* out, int cap, int* count) { LZB_RANGE("lzb_grid_run");
     return guarded([&] {
         auto reps = g->g->run();
         for (size_t i = 0; i < reps.size() && static_cast<int>(i) < cap; ++i) out[i] = reps[i];
         *count = static_cast<int>(reps.size());
     });
 }
-int lzb_grid_pass(lzb_grid* g, int which, double* value) {
+int lzb_grid_pass(lzb_grid* g, int which, double* value) { LZB_RANGE("lzb_grid_pass");
     return guarded([&] { g->g->unsettle();
         double v = g->g->pass(which);
         if (value) *value = v;
@@ -4817,13 +4819,13 @@ int lzb_grid_publish_element(lzb_grid* g, int level, int cx, int cy, const doubl
                              int32_t p1) {
     return guarded([&] { g->g->unsettle(); g->g->publish_element(level, cx, cy, m16, n, p1); });
 }
-int lzb_grid_adaptive_step(lzb_grid* g, int level, int cx, int cy) {
+int lzb_grid_adaptive_step(lzb_grid* g, int level, int cx, int cy) { LZB_RANGE("lzb_grid_adaptive_step");
     return guarded([&] { g->g->unsettle(); g->g->adaptive_step(level, cx, cy); });
 }
-int lzb_grid_stats(lzb_grid* g, lzb_compression_stats* out) {
+int lzb_grid_stats(lzb_grid* g, lzb_compression_stats* out) { LZB_RANGE("lzb_grid_stats");
     return guarded([&] { g->g->unsettle(); *out = g->g->stats(); });
 }
-int lzb_grid_stream_image(lzb_grid* g, uint8_t* out, int64_t cap, int64_t* size) {
+int lzb_grid_stream_image(lzb_grid* g, uint8_t* out, int64_t cap, int64_t* size) { LZB_RANGE("lzb_grid_stream_image");
     return guarded([&] { g->g->unsettle();
         if (!out) {
             *size = g->g->image_size();
@@ -4847,7 +4849,7 @@ int lzb_grid_info(lzb_grid* g, lzb_ctx** ctx, int* depth) {
 int lzb_grid_set_slab(lzb_grid* g, int v0, int v1) {
     return guarded([&] { g->g->unsettle(); g->g->set_slab(v0, v1); });
 }
-int lzb_grid_dist_phase(lzb_grid* g, int phase, int flags) {
+int lzb_grid_dist_phase(lzb_grid* g, int phase, int flags) { LZB_RANGE("lzb_grid_dist_phase");
     return guarded([&] { g->g->unsettle(); g->g->dist_phase(phase, flags); });
 }
 int lzb_grid_dist_result_dev(lzb_grid* g, void** result) {
@@ -4859,16 +4861,16 @@ int lzb_grid_dist_result(lzb_grid* g, double* norm2, uint64_t* slots20) {
 int lzb_grid_dist_report(lzb_grid* g, double norm2, const uint64_t* slots20, lzb_cycle_report* rep) {
     return guarded([&] { g->g->unsettle(); *rep = g->g->dist_report(norm2, slots20); });
 }
-int lzb_grid_assemble_stream(lzb_grid* g, int n, uint8_t* out, int64_t cap, int64_t* size, float* timeline) {
+int lzb_grid_assemble_stream(lzb_grid* g, int n, uint8_t* out, int64_t cap, int64_t* size, float* timeline) { LZB_RANGE("lzb_grid_assemble_stream");
     return guarded([&] { g->g->unsettle(); *size = g->g->assemble_stream(n, out, cap, timeline); });
 }
 int lzb_grid_time_kernel(lzb_grid* g, int what, int reps, double* avg_ms) {
     return guarded([&] { g->g->unsettle(); *avg_ms = g->g->time_kernel(what, reps); });
 }
-int lzb_grid_stream_load(lzb_grid* g, const uint8_t* in, int64_t size) {
+int lzb_grid_stream_load(lzb_grid* g, const uint8_t* in, int64_t size) { LZB_RANGE("lzb_grid_stream_load");
     return guarded([&] { g->g->unsettle(); g->g->load(in, size); });
 }
-int lzb_grid_save(lzb_grid* g, const char* path) {
+int lzb_grid_save(lzb_grid* g, const char* path) { LZB_RANGE("lzb_grid_save");
     return guarded([&] { g->g->unsettle();
         auto img = g->g->image();
         std::ofstream f(path, std::ios::binary);
@@ -4876,7 +4878,7 @@ int lzb_grid_save(lzb_grid* g, const char* path) {
         f.write(reinterpret_cast<const char*>(img.data()), static_cast<std::streamsize>(img.size()));
     });
 }
-int lzb_grid_load(lzb_grid* g, const char* path) {
+int lzb_grid_load(lzb_grid* g, const char* path) { LZB_RANGE("lzb_grid_load");
     return guarded([&] { g->g->unsettle();
         std::ifstream f(path, std::ios::binary);
         if (!f) throw Error(LZB_ERR_IO, std::string("cannot open stream file: ") + path);

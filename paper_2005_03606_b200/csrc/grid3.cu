@@ -1816,6 +1816,112 @@ __global__ void __launch_bounds__(kStThreads) k3_update_fine_st(Lv3 F, Lv3 C, co
     }
 }
 
+// The same update as a march along y: a block keeps its 256 fine x and walks
+// kMarchPatches owner-patch rows (3 fine rows each) of one vertex plane. The
+// coarse lines live in a ring of three slots (a patch row needs lines p and
+// p + 1; line p + 2 is fetched into a register during row p), the next patch
+// row's u / diag / r are loaded before the current one is computed, so the
+// loads of a block are in flight throughout instead of once per block, and
+// the staging is paid once per 81 rows instead of once per 4. Per vertex the
+// arithmetic is that of k3_update_fine_st, operation for operation (the two
+// kernels give identical bits; LZB_UPDATE3_ROWS=1 selects the row kernel).
+constexpr int kMarchPatches = 27;
+__global__ void __launch_bounds__(kStThreads, 3) k3_update_fine_march(Lv3 F, Lv3 C, const double2* __restrict__ pre,
+                                                                    int pi, double damping) {
+    lzb_pdl_enter();
+    __shared__ double2 s_ring[3][2][kStX];
+    __shared__ double2 s_g[3][kStX];
+    __shared__ unsigned char s_nz[3][kStX];
+    const int fz = blockIdx.z + F.z0;
+    if (fz <= 0 || fz >= F.N) return;  // boundary planes (uniform over the block)
+    const int tid = threadIdx.x;
+    const int fx0 = blockIdx.x * blockDim.x, fx = fx0 + tid;
+    const int fx1 = min(fx0 + static_cast<int>(blockDim.x) - 1, F.N);
+    const int px0 = owner3(fx0, C.N), nx = owner3(fx1, C.N) + 2 - px0;
+    const int pz = owner3(fz, C.N), lz = fz - 3 * pz;
+    const int p0 = blockIdx.y * kMarchPatches, p1 = min(p0 + kMarchPatches, C.N);
+    const bool act = fx < F.N && fx > 0;
+    const int NV = F.N + 1, NC1 = C.N + 1;
+    // staging role: thread (saz, sj) owns element sj of the coarse line at z plane pz + saz
+    const int saz = tid / kStX, sj = tid - saz * kStX;
+    const bool stg = saz < 2 && sj < nx;
+    const double2* cline = pre + vidx3(C.N, min(px0 + sj, C.N), 0, pz + (saz & 1));
+    int s0 = 0, s1 = 1, s2 = 2;  // ring slots of lines p, p + 1, p + 2
+    if (stg) {
+        s_ring[0][saz][sj] = cline[static_cast<int64_t>(p0) * NC1];
+        s_ring[1][saz][sj] = cline[static_cast<int64_t>(p0 + 1) * NC1];
+    }
+    double u[3], dg[3], r[3];
+    const double* __restrict__ gu = F.v[LZB_V_U] + vidx3(F.N, min(fx, F.N), 3 * p0 + 1, fz);
+    const double* __restrict__ gd = F.v[LZB_V_DIAG] + vidx3(F.N, min(fx, F.N), 3 * p0 + 1, fz);
+    const double* __restrict__ gr = F.v[LZB_V_R] + vidx3(F.N, min(fx, F.N), 3 * p0 + 1, fz);
+    double* __restrict__ gw = F.v[LZB_V_U] + vidx3(F.N, min(fx, F.N), 3 * p0 + 1, fz);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        if (act && 3 * p0 + 1 + k < F.N) {
+            u[k] = __ldcs(gu + k * NV);
+            dg[k] = __ldcs(gd + k * NV);
+            r[k] = __ldcs(gr + k * NV);
+        }
+    const int px = owner3(min(fx, F.N), C.N), lx = min(fx, F.N) - 3 * px, jx = px - px0;
+    const double wx0 = wax(lx, 0), wx1 = wax(lx, 1);
+    const double wz0 = wax(lz, 0), wz1 = wax(lz, 1);
+    __syncthreads();
+    for (int p = p0; p < p1; ++p) {
+        const bool more = p + 1 < p1;
+        double un[3], dgn[3], rn[3];
+        double2 ln = make_double2(0.0, 0.0);
+        if (more) {  // the next patch row's loads, in flight while this one is computed
+            gu += 3 * NV;
+            gd += 3 * NV;
+            gr += 3 * NV;
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                if (act && 3 * p + 4 + k < F.N) {
+                    un[k] = __ldcs(gu + k * NV);
+                    dgn[k] = __ldcs(gd + k * NV);
+                    rn[k] = __ldcs(gr + k * NV);
+                }
+            if (stg) ln = cline[static_cast<int64_t>(p + 2) * NC1];
+        }
+        for (int it = tid; it < 3 * kStX; it += kStThreads) {  // y, z contraction per fine row and coarse x
+            const int k = it / kStX, j = it - k * kStX;
+            if (j >= nx) continue;
+            const double wy0 = wax(k + 1, 0), wy1 = wax(k + 1, 1);
+            const double2 c00 = s_ring[s0][0][j], c10 = s_ring[s1][0][j], c01 = s_ring[s0][1][j], c11 = s_ring[s1][1][j];
+            s_g[k][j] = make_double2(wz0 * (wy0 * c00.x + wy1 * c10.x) + wz1 * (wy0 * c01.x + wy1 * c11.x),
+                                     wz0 * (wy0 * c00.y + wy1 * c10.y) + wz1 * (wy0 * c01.y + wy1 * c11.y));
+            s_nz[k][j] = (c00.y != 0.0) | (c10.y != 0.0) | (c01.y != 0.0) | (c11.y != 0.0);
+        }
+        __syncthreads();
+        if (act) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                if (!(3 * p + 1 + k < F.N)) continue;
+                const double2 g0 = s_g[k][jx], g1 = s_g[k][jx + 1];
+                double uu = u[k];
+                if (pi) uu -= wx0 * g0.x + wx1 * g1.x;
+                if (dg[k] != 0.0) uu += damping / dg[k] * r[k];
+                if (s_nz[k][jx] | s_nz[k][jx + 1]) uu += wx0 * g0.y + wx1 * g1.y;
+                __stcs(gw + k * NV, uu);
+            }
+        }
+        if (more && stg) s_ring[s2][saz][sj] = ln;
+        __syncthreads();
+        gw += 3 * NV;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            u[k] = un[k];
+            dg[k] = dgn[k];
+            r[k] = rn[k];
+        }
+        const int t = s0;
+        s0 = s1;
+        s1 = s2;
+        s2 = t;
+    }
+}
+
 // u-hat = u - P u_c on the leaf level (compute_uhat, solver.cpp:120-143 in 3D)
 __global__ void __launch_bounds__(kStThreads) k3_uhat_st(Lv3 F, Lv3 C) {
     lzb_pdl_enter();
@@ -2902,8 +3008,14 @@ private:
     void update_fine3(int z0, int z1, bool pi, double damping) {
         if (pre3_.n < static_cast<size_t>(L3_[D_ - 1].nv)) pre3_.alloc(L3_[D_ - 1].nv);
         LZB_LAUNCH(k3_coarse_pre, vg(D_ - 1), 128, 0, s_, lv(D_ - 1), omega_, pi ? 1 : 0, pre3_.p);
-        LZB_LAUNCH(k3_update_fine_st, vgst(D_, z0, z1, kStYu), kStThreads, 0, s_, lvz(D_, z0), lv(D_ - 1), pre3_.p, pi ? 1 : 0,
-                   damping);
+        static const bool rows = std::getenv("LZB_UPDATE3_ROWS") != nullptr;  // comparison switch (DESIGN 9b)
+        if (rows)
+            LZB_LAUNCH(k3_update_fine_st, vgst(D_, z0, z1, kStYu), kStThreads, 0, s_, lvz(D_, z0), lv(D_ - 1), pre3_.p,
+                       pi ? 1 : 0, damping);
+        else
+            LZB_LAUNCH(k3_update_fine_march,
+                       dim3(blocks_for(L3_[D_].N + 1, kStThreads), (L3_[D_ - 1].N + kMarchPatches - 1) / kMarchPatches, z1 - z0),
+                       kStThreads, 0, s_, lvz(D_, z0), lv(D_ - 1), pre3_.p, pi ? 1 : 0, damping);
     }
     DevBuf<double2> pre3_;
     void inject3() {
@@ -2919,12 +3031,12 @@ struct lzb_grid3 {
 
 extern "C" {
 
-int lzb_grf_table(uint64_t seed, int n, double ell, double sigma2, double* out) {
+int lzb_grf_table(uint64_t seed, int n, double ell, double sigma2, double* out) { LZB_RANGE("lzb_grf_table");
     return lzb::guarded([&] { lzb::grf_table(seed, n, ell, sigma2, out); });
 }
 
 int lzb_integrate_elements3(lzb_ctx* ctx, const lzb_field3* f, int64_t count, const double* x0, const double* y0,
-                            const double* z0, const double* h, const int32_t* n, double* out) {
+                            const double* z0, const double* h, const int32_t* n, double* out) { LZB_RANGE("lzb_integrate_elements3");
     return lzb::guarded([&] {
         using namespace lzb;
         if (count <= 0) return;
@@ -2956,11 +3068,11 @@ int lzb_integrate_elements3(lzb_ctx* ctx, const lzb_field3* f, int64_t count, co
     });
 }
 
-int lzb_grid3_create(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3, lzb_grid3** out) {
+int lzb_grid3_create(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3, lzb_grid3** out) { LZB_RANGE("lzb_grid3_create");
     return lzb_grid3_create_planes(ctx, depth, f, delta_max, fixed_p3, 0, out);
 }
 int lzb_grid3_create_planes(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3,
-                            int plane_width, lzb_grid3** out) {
+                            int plane_width, lzb_grid3** out) { LZB_RANGE("lzb_grid3_create_planes");
     return lzb::guarded([&] {
         auto g = std::make_unique<lzb_grid3>();
         g->g = std::make_unique<lzb::Grid3>(ctx, depth, *f, delta_max, fixed_p3, plane_width);
@@ -2968,14 +3080,14 @@ int lzb_grid3_create_planes(lzb_ctx* ctx, int depth, const lzb_field3* f, double
     });
 }
 int lzb_grid3_create_window(lzb_ctx* ctx, int depth, const lzb_field3* f, double delta_max, int fixed_p3,
-                            int plane_width, int cz0, int cz1, lzb_grid3** out) {
+                            int plane_width, int cz0, int cz1, lzb_grid3** out) { LZB_RANGE("lzb_grid3_create_window");
     return lzb::guarded([&] {
         auto g = std::make_unique<lzb_grid3>();
         g->g = std::make_unique<lzb::Grid3>(ctx, depth, *f, delta_max, fixed_p3, plane_width, cz0, cz1);
         *out = g.release();
     });
 }
-int lzb_grid3_leaf_storage(lzb_grid3* g, int64_t* bytes, int* cz0, int* cz1) {
+int lzb_grid3_leaf_storage(lzb_grid3* g, int64_t* bytes, int* cz0, int* cz1) { LZB_RANGE("lzb_grid3_leaf_storage");
     return lzb::guarded([&] {
         if (bytes) *bytes = g->g->leaf_storage_bytes();
         int a, b;
@@ -2987,38 +3099,38 @@ int lzb_grid3_leaf_storage(lzb_grid3* g, int64_t* bytes, int* cz0, int* cz1) {
 int lzb_grid3_destroy(lzb_grid3* g) {
     return lzb::guarded([&] { delete g; });
 }
-int lzb_grid3_assemble_fixed(lzb_grid3* g, int n) {
+int lzb_grid3_assemble_fixed(lzb_grid3* g, int n) { LZB_RANGE("lzb_grid3_assemble_fixed");
     return lzb::guarded([&] {
         g->g->assemble_fixed(n);
         g->g->sync();
     });
 }
-int lzb_grid3_stats(lzb_grid3* g, lzb_compression_stats* out) {
+int lzb_grid3_stats(lzb_grid3* g, lzb_compression_stats* out) { LZB_RANGE("lzb_grid3_stats");
     return lzb::guarded([&] { *out = g->g->stats(); });
 }
-int lzb_grid3_cells(lzb_grid3* g, int64_t first, int64_t count, double* ops, int32_t* p3) {
+int lzb_grid3_cells(lzb_grid3* g, int64_t first, int64_t count, double* ops, int32_t* p3) { LZB_RANGE("lzb_grid3_cells");
     return lzb::guarded([&] { g->g->cells(first, count, ops, p3); });
 }
 int lzb_grid3_init_cycle(lzb_grid3* g, int variant, double omega, double rhs_scale, uint64_t noise_seed,
                          int max_cycles, double target) {
     return lzb::guarded([&] { g->g->init_cycle(variant, omega, rhs_scale, noise_seed, max_cycles, target); });
 }
-int lzb_grid3_step(lzb_grid3* g, lzb_cycle_report* out) {
+int lzb_grid3_step(lzb_grid3* g, lzb_cycle_report* out) { LZB_RANGE("lzb_grid3_step");
     return lzb::guarded([&] { *out = g->g->step(); });
 }
-int lzb_grid3_vcycle(lzb_grid3* g, int nu, lzb_cycle_report* out) {
+int lzb_grid3_vcycle(lzb_grid3* g, int nu, lzb_cycle_report* out) { LZB_RANGE("lzb_grid3_vcycle");
     return lzb::guarded([&] { *out = g->g->vcycle(nu); });
 }
-int lzb_grid3_vertices(lzb_grid3* g, int level, int field, double* out) {
+int lzb_grid3_vertices(lzb_grid3* g, int level, int field, double* out) { LZB_RANGE("lzb_grid3_vertices");
     return lzb::guarded([&] { g->g->vertices(level, field, out); });
 }
-int lzb_grid3_set_slab(lzb_grid3* g, int v0, int v1) {
+int lzb_grid3_set_slab(lzb_grid3* g, int v0, int v1) { LZB_RANGE("lzb_grid3_set_slab");
     return lzb::guarded([&] { g->g->set_slab(v0, v1); });
 }
-int lzb_grid3_dist_phase(lzb_grid3* g, int phase) {
+int lzb_grid3_dist_phase(lzb_grid3* g, int phase) { LZB_RANGE("lzb_grid3_dist_phase");
     return lzb::guarded([&] { g->g->dist_phase(phase); });
 }
-int lzb_grid3_dist_phase_flags(lzb_grid3* g, int phase, int flags) {
+int lzb_grid3_dist_phase_flags(lzb_grid3* g, int phase, int flags) { LZB_RANGE("lzb_grid3_dist_phase_flags");
     return lzb::guarded([&] { g->g->dist_phase(phase, flags); });
 }
 int lzb_grid3_dist_result_dev(lzb_grid3* g, void** norm2) {
@@ -3027,38 +3139,38 @@ int lzb_grid3_dist_result_dev(lzb_grid3* g, void** norm2) {
 int lzb_grid3_dist_result(lzb_grid3* g, double* norm2) {
     return lzb::guarded([&] { *norm2 = g->g->dist_norm2(); });
 }
-int lzb_grid3_dist_report(lzb_grid3* g, double norm2, lzb_cycle_report* out) {
+int lzb_grid3_dist_report(lzb_grid3* g, double norm2, lzb_cycle_report* out) { LZB_RANGE("lzb_grid3_dist_report");
     return lzb::guarded([&] { *out = g->g->dist_report(norm2); });
 }
-int lzb_grid3_assemble_planes(lzb_grid3* g, int n, int cz0, int cz1) {
+int lzb_grid3_assemble_planes(lzb_grid3* g, int n, int cz0, int cz1) { LZB_RANGE("lzb_grid3_assemble_planes");
     return lzb::guarded([&] {
         g->g->assemble_planes(n, cz0, cz1);
         g->g->sync();
     });
 }
-int lzb_grid3_galerkin_planes(lzb_grid3* g, int level, int pz0, int pz1) {
+int lzb_grid3_galerkin_planes(lzb_grid3* g, int level, int pz0, int pz1) { LZB_RANGE("lzb_grid3_galerkin_planes");
     return lzb::guarded([&] {
         g->g->galerkin_planes(level, pz0, pz1);
         g->g->sync();
     });
 }
-int lzb_grid3_coarse_below(lzb_grid3* g, int level) {
+int lzb_grid3_coarse_below(lzb_grid3* g, int level) { LZB_RANGE("lzb_grid3_coarse_below");
     return lzb::guarded([&] {
         g->g->coarse_below(level);
         g->g->sync();
     });
 }
-int lzb_grid3_variant(lzb_grid3* g) { return g->g->variant(); }
+int lzb_grid3_variant(lzb_grid3* g) { LZB_RANGE("lzb_grid3_variant"); return g->g->variant(); }
 int lzb_grid3_info(lzb_grid3* g, lzb_ctx** ctx, int* depth) {
     return lzb::guarded([&] {
         if (ctx) *ctx = g->g->context();
         if (depth) *depth = g->g->depth();
     });
 }
-int lzb_grid3_level_ops(lzb_grid3* g, int level, void** ptr) {
+int lzb_grid3_level_ops(lzb_grid3* g, int level, void** ptr) { LZB_RANGE("lzb_grid3_level_ops");
     return lzb::guarded([&] { *ptr = g->g->level_ops(level); });
 }
-int lzb_grid3_time_kernel(lzb_grid3* g, int what, int reps, double* avg_ms) {
+int lzb_grid3_time_kernel(lzb_grid3* g, int what, int reps, double* avg_ms) { LZB_RANGE("lzb_grid3_time_kernel");
     return lzb::guarded([&] { *avg_ms = g->g->time_kernel(what, reps); });
 }
 int lzb_grid3_device_view(lzb_grid3* g, int level, int field, void** ptr) {

@@ -1169,7 +1169,7 @@ struct lzb_tree3 {
 extern "C" {
 
 int lzb_tree3_create(lzb_ctx* ctx, int lbase, int lmax, const lzb_field3* f, double delta_max, int fixed_p3,
-                     lzb_tree3** out) {
+                     lzb_tree3** out) { LZB_RANGE("lzb_tree3_create");
     return lzb::guarded([&] {
         auto t = std::make_unique<lzb_tree3>();
         t->t = std::make_unique<lzb::Tree3>(ctx, lbase, lmax, *f, delta_max, fixed_p3);
@@ -1179,51 +1179,51 @@ int lzb_tree3_create(lzb_ctx* ctx, int lbase, int lmax, const lzb_field3* f, dou
 int lzb_tree3_destroy(lzb_tree3* t) {
     return lzb::guarded([&] { delete t; });
 }
-int lzb_tree3_counts(lzb_tree3* t, int64_t* per_level, int64_t* total) {
+int lzb_tree3_counts(lzb_tree3* t, int64_t* per_level, int64_t* total) { LZB_RANGE("lzb_tree3_counts");
     return lzb::guarded([&] { t->t->counts(per_level, total); });
 }
-int lzb_tree3_assemble(lzb_tree3* t, int n) {
+int lzb_tree3_assemble(lzb_tree3* t, int n) { LZB_RANGE("lzb_tree3_assemble");
     return lzb::guarded([&] {
         t->t->assemble(n, false);
         t->t->sync();
     });
 }
-int lzb_tree3_set_shell(lzb_tree3* t, double band, int64_t* count) {
+int lzb_tree3_set_shell(lzb_tree3* t, double band, int64_t* count) { LZB_RANGE("lzb_tree3_set_shell");
     return lzb::guarded([&] { *count = t->t->set_shell(band); });
 }
-int lzb_tree3_assemble_shell(lzb_tree3* t, int n) {
+int lzb_tree3_assemble_shell(lzb_tree3* t, int n) { LZB_RANGE("lzb_tree3_assemble_shell");
     return lzb::guarded([&] {
         t->t->assemble(n, true);
         t->t->sync();
     });
 }
-int lzb_tree3_stats(lzb_tree3* t, lzb_compression_stats* out) {
+int lzb_tree3_stats(lzb_tree3* t, lzb_compression_stats* out) { LZB_RANGE("lzb_tree3_stats");
     return lzb::guarded([&] { *out = t->t->stats(); });
 }
 int lzb_tree3_cells(lzb_tree3* t, int64_t first, int64_t count, double* ops, int32_t* p3, int32_t* n,
-                    int32_t* lxyz) {
+                    int32_t* lxyz) { LZB_RANGE("lzb_tree3_cells");
     return lzb::guarded([&] { t->t->cells(first, count, ops, p3, n, lxyz); });
 }
 int lzb_tree3_init_cycle(lzb_tree3* t, int variant, double omega, double rhs_scale, uint64_t noise_seed,
                          int max_cycles, double target) {
     return lzb::guarded([&] { t->t->init_cycle(variant, omega, rhs_scale, noise_seed, max_cycles, target); });
 }
-int lzb_tree3_refine(lzb_tree3* t, double radius, int n, int64_t* new_leaves) {
+int lzb_tree3_refine(lzb_tree3* t, double radius, int n, int64_t* new_leaves) { LZB_RANGE("lzb_tree3_refine");
     return lzb::guarded([&] {
         const int64_t k = t->t->refine(radius, n);
         if (new_leaves) *new_leaves = k;
     });
 }
-int lzb_tree3_refresh_ops(lzb_tree3* t) {
+int lzb_tree3_refresh_ops(lzb_tree3* t) { LZB_RANGE("lzb_tree3_refresh_ops");
     return lzb::guarded([&] {
         t->t->refresh_ops();
         t->t->sync();
     });
 }
-int lzb_tree3_step(lzb_tree3* t, lzb_cycle_report* out) {
+int lzb_tree3_step(lzb_tree3* t, lzb_cycle_report* out) { LZB_RANGE("lzb_tree3_step");
     return lzb::guarded([&] { *out = t->t->step(); });
 }
-int lzb_tree3_vertices(lzb_tree3* t, int level, int field, double* out) {
+int lzb_tree3_vertices(lzb_tree3* t, int level, int field, double* out) { LZB_RANGE("lzb_tree3_vertices");
     return lzb::guarded([&] { t->t->vertices(level, field, out); });
 }
 

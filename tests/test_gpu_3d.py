@@ -384,3 +384,42 @@ def test_reinit_cycle_keeps_coarse_operators():
     a, b = vhist(False), vhist(True)
     assert a == b
     assert a[3] < 0.05 * a[0]  # the coarse correction works (smoothing alone gives ~0.5)
+
+
+_UPDATE3_SCRIPT = r"""
+import hashlib, sys
+sys.path.insert(0, ".")
+import numpy as np
+import paper_2005_03606_b200 as lzb
+depth, solver = int(sys.argv[1]), sys.argv[2]
+G = lzb.Grid3(depth, lzb.field3_grf(lzb.grf_table(5, 16, 0.05, 1.0)))
+G.assemble_fixed(1)
+G.init_cycle(solver=solver, omega=0.6, seed=42, max_cycles=100)
+res = [G.step()["residual"] for _ in range(3)]
+u = G.vertices(depth, lzb.T.V_U)
+print("HASH", hashlib.sha256(np.ascontiguousarray(u).tobytes()).hexdigest(), " ".join(repr(x) for x in res))
+"""
+
+
+@pytest.mark.parametrize("depth,solver", [(3, "adafac-pi"), (4, "additive"), (5, "adafac-pi")])
+def test_update3_march_bit_identical_to_row_kernel(depth, solver):
+    """The marching leaf update (k3_update_fine_march: 27 owner-patch rows per
+    block, ring of coarse lines, next rows prefetched) against the row-block
+    kernel it replaces (LZB_UPDATE3_ROWS=1): identical u bits and residuals
+    after three cycles; depth 5 has three march chunks per column, depth 3 a
+    short one (9 patches)."""
+    import os
+    import subprocess
+    import sys
+
+    outs = []
+    for rows in (False, True):
+        env = dict(os.environ)
+        env.pop("LZB_UPDATE3_ROWS", None)
+        if rows:
+            env["LZB_UPDATE3_ROWS"] = "1"
+        p = subprocess.run([sys.executable, "-c", _UPDATE3_SCRIPT, str(depth), solver], env=env, capture_output=True,
+                           text=True, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append([ln for ln in p.stdout.splitlines() if ln.startswith("HASH")][0])
+    assert outs[0] == outs[1]
