@@ -1825,9 +1825,9 @@ __global__ void __launch_bounds__(kStThreads) k3_update_fine_st(Lv3 F, Lv3 C, co
 // the staging is paid once per 81 rows instead of once per 4. Per vertex the
 // arithmetic is that of k3_update_fine_st, operation for operation (the two
 // kernels give identical bits; LZB_UPDATE3_ROWS=1 selects the row kernel).
-constexpr int kMarchPatches = 27;
+constexpr int kMarchPatches = 27;  // owner-patch rows per block (LZB_UPDATE3_PG overrides, for sweeps)
 __global__ void __launch_bounds__(kStThreads, 3) k3_update_fine_march(Lv3 F, Lv3 C, const double2* __restrict__ pre,
-                                                                    int pi, double damping) {
+                                                                    int pi, double damping, int pg) {
     lzb_pdl_enter();
     __shared__ double2 s_ring[3][2][kStX];
     __shared__ double2 s_g[3][kStX];
@@ -1839,7 +1839,7 @@ __global__ void __launch_bounds__(kStThreads, 3) k3_update_fine_march(Lv3 F, Lv3
     const int fx1 = min(fx0 + static_cast<int>(blockDim.x) - 1, F.N);
     const int px0 = owner3(fx0, C.N), nx = owner3(fx1, C.N) + 2 - px0;
     const int pz = owner3(fz, C.N), lz = fz - 3 * pz;
-    const int p0 = blockIdx.y * kMarchPatches, p1 = min(p0 + kMarchPatches, C.N);
+    const int p0 = blockIdx.y * pg, p1 = min(p0 + pg, C.N);
     const bool act = fx < F.N && fx > 0;
     const int NV = F.N + 1, NC1 = C.N + 1;
     // staging role: thread (saz, sj) owns element sj of the coarse line at z plane pz + saz
@@ -2671,8 +2671,10 @@ public:
                 case LZB_TK_RESTRICT: restrict3(D_, 0, L3_[D_ - 1].N + 1); break;
                 case LZB_TK_JACOBI: LZB_LAUNCH(k3_jacobi, vg(D_), 128, 0, s_, lv(D_), 0.0); break;
                 case LZB_TK_PROLONG: LZB_LAUNCH(k3_prolong, vg(D_), 128, 0, s_, lv(D_), lv(D_ - 1)); break;
-                case LZB_TK_BACK:  // the fused leaf update (u drifts by the prolongated correction)
-                    update_fine3(0, L3_[D_].N + 1, true, 0.0);
+                case LZB_TK_BACK:  // the fused leaf update with the cycle's own damping (u drifts by the Jacobi and
+                                   // prolongated corrections; a zero damping would send every damping / diag
+                                   // through the division's slow path, which no cycle does)
+                    update_fine3(0, L3_[D_].N + 1, true, damping3(D_));
                     break;
                 default: throw Error(LZB_ERR_INVALID, "unknown kernel id");
             }
@@ -3013,9 +3015,16 @@ private:
             LZB_LAUNCH(k3_update_fine_st, vgst(D_, z0, z1, kStYu), kStThreads, 0, s_, lvz(D_, z0), lv(D_ - 1), pre3_.p,
                        pi ? 1 : 0, damping);
         else
-            LZB_LAUNCH(k3_update_fine_march,
-                       dim3(blocks_for(L3_[D_].N + 1, kStThreads), (L3_[D_ - 1].N + kMarchPatches - 1) / kMarchPatches, z1 - z0),
-                       kStThreads, 0, s_, lvz(D_, z0), lv(D_ - 1), pre3_.p, pi ? 1 : 0, damping);
+        {
+            // 27 patch rows per block where that still fills the GPU several times over, else 9 (243^3: 726 blocks
+            // of 27 are 1.6 waves; measured 0.119 vs 0.109 ms)
+            static const int pg_env = std::getenv("LZB_UPDATE3_PG") ? std::max(1, std::atoi(std::getenv("LZB_UPDATE3_PG"))) : 0;
+            const int64_t blocks27 = static_cast<int64_t>(blocks_for(L3_[D_].N + 1, kStThreads)) *
+                                     ((L3_[D_ - 1].N + kMarchPatches - 1) / kMarchPatches) * (z1 - z0);
+            const int pg = pg_env ? pg_env : blocks27 >= 24LL * ctx_->sms ? kMarchPatches : kMarchPatches / 3;
+            LZB_LAUNCH(k3_update_fine_march, dim3(blocks_for(L3_[D_].N + 1, kStThreads), (L3_[D_ - 1].N + pg - 1) / pg, z1 - z0),
+                       kStThreads, 0, s_, lvz(D_, z0), lv(D_ - 1), pre3_.p, pi ? 1 : 0, damping, pg);
+        }
     }
     DevBuf<double2> pre3_;
     void inject3() {
