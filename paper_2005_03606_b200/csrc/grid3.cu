@@ -1966,6 +1966,88 @@ __global__ void __launch_bounds__(kStThreads) k3_uhat_st(Lv3 F, Lv3 C) {
     }
 }
 
+// u-hat as a march along y (the structure of k3_update_fine_march: ring of
+// coarse u lines, next patch row's u in flight while the current one is
+// contracted and stored). All vertices take part, boundary planes and rows
+// included; row 0 (lattice offset 0 of patch row 0) is the first chunk's
+// prologue. Same expression per vertex as k3_uhat_st, same bits.
+// Measured and NOT the default (LZB_UHAT3_MARCH=1 selects it): with one array
+// to read, three rows per step leave a thread 3 loads in flight against the
+// row kernel's 8 -- 729^3 1.67 ms against 1.34 ms, 243^3 0.066 against 0.052.
+__global__ void __launch_bounds__(kStThreads, 4) k3_uhat_march(Lv3 F, Lv3 C, int pg) {
+    lzb_pdl_enter();
+    __shared__ double s_ring[3][2][kStX];
+    __shared__ double s_g[3][kStX];
+    const int fz = blockIdx.z + F.z0;
+    const int tid = threadIdx.x;
+    const int fx0 = blockIdx.x * blockDim.x, fx = fx0 + tid;
+    const int fx1 = min(fx0 + static_cast<int>(blockDim.x) - 1, F.N);
+    const int px0 = owner3(fx0, C.N), nx = owner3(fx1, C.N) + 2 - px0;
+    const int pz = owner3(fz, C.N), lz = fz - 3 * pz;
+    const int p0 = blockIdx.y * pg, p1 = min(p0 + pg, C.N);
+    const bool act = fx <= F.N;
+    const int NV = F.N + 1, NC1 = C.N + 1;
+    const int saz = tid / kStX, sj = tid - saz * kStX;
+    const bool stg = saz < 2 && sj < nx;
+    const double* cline = C.v[LZB_V_U] + vidx3(C.N, min(px0 + sj, C.N), 0, pz + (saz & 1));
+    int s0 = 0, s1 = 1, s2 = 2;
+    if (stg) {
+        s_ring[0][saz][sj] = cline[static_cast<int64_t>(p0) * NC1];
+        s_ring[1][saz][sj] = cline[static_cast<int64_t>(p0 + 1) * NC1];
+    }
+    const int64_t v0 = vidx3(F.N, min(fx, F.N), 3 * p0 + 1, fz);
+    const double* __restrict__ gu = F.v[LZB_V_U] + v0;
+    double* __restrict__ gw = F.v[LZB_V_UHAT] + v0;
+    double u[3], u0 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        if (act) u[k] = __ldcs(gu + k * NV);
+    if (p0 == 0 && act) u0 = __ldcs(gu - NV);
+    const int px = owner3(min(fx, F.N), C.N), lx = min(fx, F.N) - 3 * px, jx = px - px0;
+    const double wx0 = wax(lx, 0), wx1 = wax(lx, 1);
+    const double wz0 = wax(lz, 0), wz1 = wax(lz, 1);
+    __syncthreads();
+    if (p0 == 0) {  // row 0
+        for (int j = tid; j < nx; j += kStThreads)
+            s_g[0][j] = wz0 * (wax(0, 0) * s_ring[0][0][j] + wax(0, 1) * s_ring[1][0][j]) +
+                        wz1 * (wax(0, 0) * s_ring[0][1][j] + wax(0, 1) * s_ring[1][1][j]);
+        __syncthreads();
+        if (act) __stcs(gw - NV, u0 - (wx0 * s_g[0][jx] + wx1 * s_g[0][jx + 1]));
+        __syncthreads();
+    }
+    for (int p = p0; p < p1; ++p) {
+        const bool more = p + 1 < p1;
+        double un[3], ln = 0.0;
+        if (more) {
+            gu += 3 * NV;
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                if (act) un[k] = __ldcs(gu + k * NV);
+            if (stg) ln = cline[static_cast<int64_t>(p + 2) * NC1];
+        }
+        for (int it = tid; it < 3 * kStX; it += kStThreads) {
+            const int k = it / kStX, j = it - k * kStX;
+            if (j >= nx) continue;
+            s_g[k][j] = wz0 * (wax(k + 1, 0) * s_ring[s0][0][j] + wax(k + 1, 1) * s_ring[s1][0][j]) +
+                        wz1 * (wax(k + 1, 0) * s_ring[s0][1][j] + wax(k + 1, 1) * s_ring[s1][1][j]);
+        }
+        __syncthreads();
+        if (act) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) __stcs(gw + k * NV, u[k] - (wx0 * s_g[k][jx] + wx1 * s_g[k][jx + 1]));
+        }
+        if (more && stg) s_ring[s2][saz][sj] = ln;
+        __syncthreads();
+        gw += 3 * NV;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) u[k] = un[k];
+        const int t = s0;
+        s0 = s1;
+        s1 = s2;
+        s2 = t;
+    }
+}
+
 __global__ void k3_inject(Lv3 F, Lv3 C) {
     lzb_pdl_enter();
     int ix, iy, iz;
@@ -3003,7 +3085,13 @@ private:
     // with a coarse level below) through the staged row kernel
     void uhat3(int l, int z0, int z1) {
         if (l == 0) LZB_LAUNCH(k3_uhat, vgz(0, z0, z1), 128, 0, s_, lvz(0, z0), lv(0), 0);
-        else LZB_LAUNCH(k3_uhat_st, vgst(l, z0, z1), kStThreads, 0, s_, lvz(l, z0), lv(l - 1));
+        else if (L3_[l].N >= 243 && std::getenv("LZB_UHAT3_MARCH") != nullptr) {  // opt-in: measured slower, see the kernel
+            const int64_t blocks27 = static_cast<int64_t>(blocks_for(L3_[l].N + 1, kStThreads)) *
+                                     ((L3_[l - 1].N + kMarchPatches - 1) / kMarchPatches) * (z1 - z0);
+            const int pg = blocks27 >= 24LL * ctx_->sms ? kMarchPatches : kMarchPatches / 3;
+            LZB_LAUNCH(k3_uhat_march, dim3(blocks_for(L3_[l].N + 1, kStThreads), (L3_[l - 1].N + pg - 1) / pg, z1 - z0),
+                       kStThreads, 0, s_, lvz(l, z0), lv(l - 1), pg);
+        } else LZB_LAUNCH(k3_uhat_st, vgst(l, z0, z1), kStThreads, 0, s_, lvz(l, z0), lv(l - 1));
     }
     // the staged row kernels: 128 x, kStY rows, one plane per block
     dim3 vgst(int l, int z0, int z1, int rows = kStY) const {

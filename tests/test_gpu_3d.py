@@ -416,8 +416,11 @@ def test_update3_march_bit_identical_to_row_kernel(depth, solver):
     for rows in (False, True):
         env = dict(os.environ)
         env.pop("LZB_UPDATE3_ROWS", None)
+        env.pop("LZB_UHAT3_MARCH", None)
         if rows:
             env["LZB_UPDATE3_ROWS"] = "1"
+        else:
+            env["LZB_UHAT3_MARCH"] = "1"  # the opt-in marching u-hat too (from 243^3 up)
         p = subprocess.run([sys.executable, "-c", _UPDATE3_SCRIPT, str(depth), solver], env=env, capture_output=True,
                            text=True, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
         assert p.returncode == 0, p.stderr[-2000:]
